@@ -1,0 +1,180 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the UNMODIFIED reference library, compiled
+// from /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libpagestream_ref.so.  Used to pin the oracle restatement
+// (golden vectors) and as the CPU baseline (bench.py --impl reference).
+// Nothing here is part of the product.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "pagestream/engine.hpp"
+#include "pagestream/graph.hpp"
+#include "pagestream/ingest.hpp"
+#include "pagestream/programs.hpp"
+#include "pagestream/reference.hpp"
+
+using namespace pagestream;
+
+namespace {
+thread_local std::string g_err;
+
+EdgeList make_edges(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                    const uint32_t* w) {
+  EdgeList el;
+  el.num_vertices = n;
+  el.edges.resize(m);
+  for (uint64_t i = 0; i < m; ++i) el.edges[i] = Edge{src[i], dst[i]};
+  if (w) el.weights.assign(w, w + m);
+  return el;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_error() { return g_err.c_str(); }
+
+// generate_rmat (ingest.cpp:112-141)
+int ref_generate_rmat(int scale, uint64_t ef, double a, double b, double c, double d,
+                      uint64_t seed, uint32_t* src, uint32_t* dst) {
+  return guard([&] {
+    RmatParams p;
+    p.scale = scale;
+    p.edge_factor = ef;
+    p.a = a;
+    p.b = b;
+    p.c = c;
+    p.d = d;
+    p.seed = seed;
+    EdgeList el = generate_rmat(p);
+    for (size_t i = 0; i < el.edges.size(); ++i) {
+      src[i] = el.edges[i].src;
+      dst[i] = el.edges[i].dst;
+    }
+  });
+}
+
+// assign_weights (ingest.cpp:143-152)
+int ref_assign_weights(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                       uint64_t seed, uint32_t lo, uint32_t hi, uint32_t* w) {
+  return guard([&] {
+    EdgeList el = assign_weights(make_edges(n, m, src, dst, nullptr), seed, lo, hi);
+    std::memcpy(w, el.weights.data(), m * 4);
+  });
+}
+
+// build_csr (graph.cpp:30-48)
+int ref_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                  const uint32_t* w, uint64_t* off, uint32_t* nbr, uint32_t* ow) {
+  return guard([&] {
+    CsrGraph g = build_csr(make_edges(n, m, src, dst, w));
+    std::memcpy(off, g.out_offsets.data(), (size_t(n) + 1) * 8);
+    if (m) std::memcpy(nbr, g.out_neighbors.data(), m * 4);
+    if (w && m) std::memcpy(ow, g.out_weights.data(), m * 4);
+  });
+}
+
+// build_csc_pages (graph.cpp:50-94), flattened: local offsets (|V| + P),
+// sources and weights concatenated in page order.
+int ref_build_csc_pages(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                        const uint32_t* w, uint32_t cap, uint32_t* local, uint32_t* in_src,
+                        uint32_t* in_w) {
+  return guard([&] {
+    PageSet ps = build_csc_pages(make_edges(n, m, src, dst, w), cap);
+    size_t lo = 0, eo = 0;
+    for (const CscPage& p : ps.pages) {
+      std::memcpy(local + lo, p.in_offsets.data(), p.in_offsets.size() * 4);
+      lo += p.in_offsets.size();
+      if (!p.in_sources.empty()) std::memcpy(in_src + eo, p.in_sources.data(), p.in_sources.size() * 4);
+      if (w && !p.in_weights.empty()) std::memcpy(in_w + eo, p.in_weights.data(), p.in_weights.size() * 4);
+      eo += p.in_sources.size();
+    }
+  });
+}
+
+// reference_solve (reference.cpp:77-90); algo 0 bfs, 1 cc, 2 sssp
+int ref_reference_solve(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                        const uint32_t* w, int algo, uint32_t source, uint32_t* out) {
+  return guard([&] {
+    CsrGraph g = build_csr(make_edges(n, m, src, dst, w));
+    std::vector<Value> v = reference_solve(g, AlgoKind(algo), source);
+    std::memcpy(out, v.data(), size_t(n) * 4);
+  });
+}
+
+// The reference engine run() on prebuilt structures (copied from flat
+// arrays with the reference layouts), returning values and metrics.
+// metrics_out[16]: passes, sparse, dense, recovery, pages_transferred,
+// bytes_transferred, attempts, valid, skipped, edges_read, virtual_makespan,
+// wall_seconds, has_accuracy, accuracy, 0, 0.
+int ref_run(uint32_t n, uint64_t m, const uint64_t* out_off, const uint32_t* out_nbr,
+            const uint32_t* out_w, const uint64_t* in_off, const uint32_t* in_src,
+            const uint32_t* in_w, uint32_t cap, int algo, uint32_t source, int predictor,
+            int schedule, int mrt, int reps, uint32_t window, int workers, int clock,
+            int execution, double density, uint32_t* values_out, double* metrics_out) {
+  return guard([&] {
+    CsrGraph g;
+    g.num_vertices = n;
+    g.out_offsets.assign(out_off, out_off + size_t(n) + 1);
+    g.out_neighbors.assign(out_nbr, out_nbr + m);
+    if (out_w) g.out_weights.assign(out_w, out_w + m);
+    PageSet ps;
+    ps.num_vertices = n;
+    ps.page_vertex_capacity = cap;
+    ps.weighted = in_w != nullptr;
+    const uint64_t np = (uint64_t(n) + cap - 1) / cap;
+    ps.pages.resize(np);
+    for (uint64_t p = 0; p < np; ++p) {
+      CscPage& pg = ps.pages[p];
+      pg.vertex_begin = uint32_t(p * cap);
+      pg.vertex_end = uint32_t(std::min<uint64_t>((p + 1) * cap, n));
+      const uint64_t lo = in_off[pg.vertex_begin], hi = in_off[pg.vertex_end];
+      pg.in_offsets.resize(size_t(pg.range()) + 1);
+      for (uint32_t v = 0; v <= pg.range(); ++v)
+        pg.in_offsets[v] = uint32_t(in_off[pg.vertex_begin + v] - lo);
+      pg.in_sources.assign(in_src + lo, in_src + hi);
+      if (in_w) pg.in_weights.assign(in_w + lo, in_w + hi);
+    }
+    VertexProgram prog;
+    prog.kind = AlgoKind(algo);
+    prog.source = source;
+    EngineConfig cfg;
+    cfg.page_vertex_capacity = cap;
+    cfg.density_threshold_fraction = density;
+    cfg.predictor = PredictorMode(predictor);
+    cfg.schedule.kind = ScheduleModeKind(schedule);
+    cfg.schedule.max_reentry_times = mrt;
+    cfg.schedule.buffer_repetitions = reps;
+    cfg.window_capacity = window;
+    cfg.transfer.worker_count = workers;
+    cfg.clock = ClockMode(clock);
+    cfg.execution = ExecutionPolicy(execution);
+    RunResult r = run(g, ps, prog, cfg);
+    if (values_out) std::memcpy(values_out, r.values.data(), size_t(n) * 4);
+    const MetricsReport& mm = r.metrics;
+    double out[16] = {double(mm.passes), double(mm.sparse_passes), double(mm.dense_passes),
+                      double(mm.recovery_passes), double(mm.pages_transferred),
+                      double(mm.bytes_transferred), double(mm.update_attempts),
+                      double(mm.valid_updates), double(mm.skipped_vertices),
+                      double(mm.edges_read), mm.virtual_makespan, mm.wall_seconds,
+                      mm.prediction_accuracy ? 1.0 : 0.0,
+                      mm.prediction_accuracy ? *mm.prediction_accuracy : 0.0, 0, 0};
+    std::memcpy(metrics_out, out, sizeof(out));
+  });
+}
+
+}  // extern "C"

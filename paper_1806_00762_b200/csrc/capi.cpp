@@ -1,0 +1,209 @@
+// extern "C" boundary of libseraph (include/seraph.h).  Every entry point
+// catches, records the message and returns the SR_E_* code that the C++
+// drop-in rethrows as the matching pagestream exception (errors.hpp:8-28).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "seraph.h"
+
+struct sr_ctx {
+  seraph::Engine* eng = nullptr;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(sr_ctx* ctx, F&& f) {
+  try {
+    f();
+    return SR_OK;
+  } catch (const seraph::EngineError& e) {
+    (ctx ? ctx->err : g_err) = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    (ctx ? ctx->err : g_err) = "host allocation failed";
+    return SR_E_OOM;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->err : g_err) = e.what();
+    return SR_E_INTERNAL;
+  }
+}
+
+void copy_passes(const std::vector<sr_pass_stats>& passes, sr_pass_stats* out, uint32_t cap,
+                 uint32_t* n_out) {
+  if (n_out) *n_out = uint32_t(passes.size());
+  if (out)
+    for (uint32_t i = 0; i < cap && i < passes.size(); ++i) out[i] = passes[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int sr_abi_version(void) { return SERAPH_ABI_VERSION; }
+
+const char* sr_global_error(void) { return g_err.c_str(); }
+
+void sr_default_config(sr_run_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->algo = SR_ALGO_BFS;
+  c->predictor = SR_PRED_OFF;
+  c->schedule = SR_SCHED_BASELINE;
+  c->max_reentry_times = 2;
+  c->buffer_repetitions = 3;
+  c->window_capacity = 8;
+  c->density_threshold_fraction = 0.05;
+  c->bytes_per_time_unit = 11.0;
+  c->edges_per_time_unit_per_worker = 1.75;
+  c->worker_count = 4;
+  c->clock = SR_CLOCK_VIRTUAL;
+  c->execution = SR_EXEC_DENSITY_SWITCHED;
+  c->pr_iterations = 20;
+  c->pr_damping = 0.85;
+}
+
+int sr_open(int device, uint64_t budget, sr_ctx** out) {
+  if (!out) return SR_E_CONFIG;
+  *out = nullptr;
+  sr_ctx* ctx = new (std::nothrow) sr_ctx();
+  if (!ctx) return SR_E_OOM;
+  const int rc = guard(nullptr, [&] { ctx->eng = new seraph::Engine(device, budget); });
+  if (rc != SR_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return SR_OK;
+}
+
+void sr_close(sr_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->eng;
+  delete ctx;
+}
+
+const char* sr_last_error(const sr_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int sr_device_query(int device, sr_device_info* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw seraph::EngineError(SR_E_CONFIG, "null output");
+    cudaDeviceProp prop{};
+    SR_CUDA(cudaGetDeviceProperties(&prop, device));
+    SR_CUDA(cudaSetDevice(device));
+    size_t fr = 0, tot = 0;
+    SR_CUDA(cudaMemGetInfo(&fr, &tot));
+    std::memset(out, 0, sizeof(*out));
+    out->device = device;
+    out->sm_count = prop.multiProcessorCount;
+    out->l2_bytes = prop.l2CacheSize;
+    out->cc_major = prop.major;
+    out->cc_minor = prop.minor;
+    out->total_mem = tot;
+    out->free_mem = fr;
+    std::strncpy(out->name, prop.name, sizeof(out->name) - 1);
+  });
+}
+
+int sr_load_csr(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                const uint32_t* w) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->load_csr(n, m, off, nbr, w); });
+}
+
+int sr_load_pages(sr_ctx* ctx, uint32_t n, uint32_t cap, int weighted, const sr_page_view* pages,
+                  uint32_t np) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->load_pages(n, cap, weighted != 0, pages, np); });
+}
+
+uint64_t sr_loaded_page_bytes(const sr_ctx* ctx) {
+  return ctx && ctx->eng ? ctx->eng->page_bytes_total() : 0;
+}
+
+int sr_run(sr_ctx* ctx, const sr_run_config* cfg, uint32_t* values_out, float* ranks_out,
+           sr_metrics* metrics_out, sr_pass_stats* per_pass, uint32_t cap, uint32_t* n_pass) {
+  if (!ctx || !cfg) return SR_E_CONFIG;
+  return guard(ctx, [&] {
+    sr_metrics m{};
+    std::vector<sr_pass_stats> passes;
+    ctx->eng->run(*cfg, values_out, ranks_out, m, passes);
+    if (metrics_out) *metrics_out = m;
+    copy_passes(passes, per_pass, cap, n_pass);
+  });
+}
+
+int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                 const uint32_t* w, uint32_t cap, int weighted_pages, const sr_page_view* pages,
+                 uint32_t np,
+                 const sr_run_config* cfg, uint32_t* values_out, float* ranks_out,
+                 sr_metrics* metrics_out, sr_pass_stats* per_pass, uint32_t pcap,
+                 uint32_t* n_pass) {
+  if (!ctx || !cfg) return SR_E_CONFIG;
+  return guard(ctx, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    ctx->eng->last_upload_seconds = 0;
+    ctx->eng->last_upload_bytes = 0;
+    const bool weighted = weighted_pages != 0;
+    ctx->eng->load_csr(n, m, off, nbr, w);
+    ctx->eng->load_pages(n, cap, weighted, pages, np);
+    const double up = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    sr_metrics mm{};
+    std::vector<sr_pass_stats> passes;
+    ctx->eng->run(*cfg, values_out, ranks_out, mm, passes);
+    mm.upload_seconds = up;
+    mm.h2d_bytes += ctx->eng->last_upload_bytes;
+    if (metrics_out) *metrics_out = mm;
+    copy_passes(passes, per_pass, pcap, n_pass);
+  });
+}
+
+int sr_get_trace(const sr_ctx* ctx, sr_trace_event* out, uint64_t cap, uint64_t* n_out) {
+  if (!ctx) return SR_E_CONFIG;
+  const auto& t = ctx->eng->trace;
+  if (n_out) *n_out = t.size();
+  if (out)
+    for (uint64_t i = 0; i < cap && i < t.size(); ++i) out[i] = t[i];
+  return SR_OK;
+}
+
+int sr_verify_fixpoint(sr_ctx* ctx, int algo, const uint32_t* values_host, uint64_t* viol) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] {
+    const uint64_t v = ctx->eng->verify_fixpoint(algo, values_host);
+    if (viol) *viol = v;
+  });
+}
+
+int sr_bench_pull_sweep(sr_ctx* ctx, int algo, uint32_t reps, double* ms, uint64_t* edges) {
+  if (!ctx || !ms || !edges) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->bench_pull_sweep(algo, reps, ms, edges); });
+}
+
+int sr_nccl_unique_id(uint8_t out[128]) {
+  return guard(nullptr, [&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess)
+      throw seraph::EngineError(SR_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "nccl unique id size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+int sr_attach_world(sr_ctx* ctx, int rank, int world, const uint8_t id[128]) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->attach_world(rank, world, id); });
+}
+
+}  // extern "C"

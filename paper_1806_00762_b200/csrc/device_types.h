@@ -1,0 +1,124 @@
+// Device-side data layout shared by the kernels (kernels.cu) and the host
+// engine (engine.cpp).  See DESIGN.md §3 "Data layout in HBM".
+#pragma once
+
+#include <cstdint>
+
+namespace seraph {
+
+constexpr uint32_t kUnreached = 0xffffffffu;  // reference types.hpp:14
+
+enum Algo : int { kBfs = 0, kCc = 1, kSssp = 2, kPageRank = 3 };
+enum GateKind : int { kGateOff = 0, kGateStrong = 1, kGateWeak = 2 };
+enum PassKindDev : int { kPassSparse = 0, kPassDense = 1, kPassRecovery = 2, kPassInit = 3 };
+
+// K1 work decomposition.  A page's destinations are cut at load time into
+// warp tiles: either a run of whole destinations (<= kTileMaxDests dests and
+// ~kTileEdgeBudget edges) or one chunk of a hub destination's in-edges.
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlockThreads = kWarpsPerBlock * 32;
+constexpr uint32_t kTileMaxDests = 256;
+constexpr uint32_t kTileEdgeBudget = 1024;
+constexpr uint32_t kHubChunk = 1024;      // edges per hub chunk tile
+constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id
+constexpr int kMaxSegments = 8;           // tile ranges per launch
+
+// Tile (uint4): x = edge_lo, y = edge_hi (page-local edge indices),
+// z = dest_lo (page-local), w = dest_hi (exclusive) or kHubFlag|hub_id.
+
+// One page as the kernels see it: page-local CSC arrays wherever the page
+// currently lives (resident arena or a streaming slot).
+struct PageDesc {
+  uint32_t vertex_begin;
+  uint32_t range;
+  uint64_t edge_count;
+  const uint32_t* offs;  // range+1 page-local offsets (graph.hpp:49)
+  const uint32_t* src;   // in_sources
+  const uint32_t* w;     // in_weights or nullptr
+};
+
+// Per page-run counters (KernelRunStats, scheduler.hpp:145-158).
+struct RunCtr {
+  unsigned long long attempts;
+  unsigned long long valid;
+  unsigned long long skipped;
+  unsigned long long edges;
+};
+
+// Scalars produced by the per-pass census (K4/K5), read back once per pass.
+struct Census {
+  // --- reset before every census ---
+  unsigned long long changed;      // changed vertices (next frontier size)
+  unsigned long long push_count;   // changed vertices with out-degree > 0
+  unsigned long long out_edges;    // sum of out-degree of changed vertices
+  unsigned long long status_hist[6];
+  unsigned long long valid;        // deterministic push: destinations improved
+  unsigned long long own_push;     // push-list entries owned by this rank
+  unsigned long long own_edges;    // their out-edge volume
+  // --- run-long accumulators ---
+  unsigned long long log_events;   // PredictionLog events (weak)
+  unsigned long long log_incorrect;
+  unsigned int min_changed;        // strong SSSP l accumulator (all kernels)
+  unsigned int cc_min_label;       // strong CC s result
+};
+constexpr unsigned kCensusResetBytes = 12 * sizeof(unsigned long long);
+
+struct Segments {
+  uint32_t n;
+  uint32_t tile_begin[kMaxSegments];
+  uint32_t task_prefix[kMaxSegments + 1];
+};
+
+struct PullArgs {
+  const uint4* tiles;
+  const uint32_t* tile_page;
+  const PageDesc* pages;
+  Segments seg;
+  uint32_t* values;        // async: read+write; det: read-only snapshot
+  uint32_t* next;          // det: write target (== values in async)
+  uint8_t* changed;        // changed-this-pass flags (engine.cpp:312-315)
+  const uint8_t* status;   // weak predictor DFA state (predictor.hpp:29)
+  uint32_t* hub_stamp;     // last run id that counted a hub's valid update
+  uint32_t run_id;
+  RunCtr* ctr;             // counters of this run: [page] or [0]
+  const RunCtr* prev_ctr;  // reentry: skip pages whose previous run was quiet
+  uint32_t ctr_per_page;   // 1: ctr/prev_ctr indexed by page, 0: all in ctr[0]
+  Census* census;          // min_changed accumulator
+  unsigned long long k_bfs;  // strong thresholds (predictor.hpp:47-52)
+  uint32_t s_cc;
+  uint32_t l_sssp;
+};
+
+struct PrArgs {
+  const uint4* tiles;
+  const uint32_t* tile_page;
+  const PageDesc* pages;
+  Segments seg;
+  const float* contrib_in;
+  float* rank_out;
+  float* contrib_out;
+  const float* inv_outdeg;
+  float* hub_sum;
+  RunCtr* ctr;
+  float base;   // (1-d)/N
+  float damp;   // d
+};
+
+struct PushArgs {
+  const uint32_t* list;              // frontier ids with out-degree > 0 (sorted)
+  const unsigned long long* pref;    // exclusive prefix of out-degree
+  const uint32_t* chunk_start;       // first list entry of every push chunk
+  uint32_t n_list;
+  unsigned long long total_edges;
+  const unsigned long long* out_offsets;
+  const uint32_t* out_neighbors;
+  const uint32_t* out_weights;
+  uint32_t* values;
+  uint32_t* next;  // det mode target
+  uint8_t* changed;
+  RunCtr* ctr;
+  Census* census;
+};
+constexpr uint32_t kPushChunk = 256;  // flattened edges per warp task
+
+}  // namespace seraph

@@ -1,0 +1,1302 @@
+// Host engine of libseraph: graph residency, the density-switched pass loop
+// and the transfer scheduler.  The loop follows the reference Runner
+// (proj/src/engine.cpp:225-416) decision for decision; all per-vertex work
+// runs in the sm_100a kernels of kernels.cu.
+#include "engine.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+
+#include "kernels.h"
+
+namespace seraph {
+
+namespace {
+
+int host_threads() {
+  unsigned h = std::thread::hardware_concurrency();
+  return h ? int(std::min(h, 64u)) : 8;
+}
+
+template <typename F>
+void parallel_for(size_t n, F&& f, int threads = 0) {
+  if (threads <= 0) threads = host_threads();
+  if (n == 0) return;
+  if (threads == 1 || n == 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::atomic<size_t> next{0};
+  const int t = int(std::min<size_t>(threads, n));
+  for (int k = 0; k < t; ++k)
+    pool.emplace_back([&] {
+      for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+uint64_t page_bytes_rule(uint32_t range, uint64_t edges, bool weighted) {
+  // graph.cpp:96-100: (offset entries + source entries [+ weight entries]) * 4
+  return (uint64_t(range) + 1 + edges * (weighted ? 2 : 1)) * 4ull;
+}
+
+struct TileJob {
+  uint32_t page, lo, hi;  // page-local destination range
+  std::vector<uint4> tiles;
+  std::vector<uint32_t> hubs;  // global vertex ids, local hub numbering
+};
+
+// Greedy cut of [lo, hi) into warp tiles (device_types.h).
+void cut_tiles(const uint32_t* offs, uint32_t vb, TileJob& job) {
+  uint32_t i = job.lo;
+  while (i < job.hi) {
+    const uint32_t deg = offs[i + 1] - offs[i];
+    if (deg > kHubChunk) {
+      const uint32_t hub = uint32_t(job.hubs.size());
+      job.hubs.push_back(vb + i);
+      for (uint32_t e = offs[i]; e < offs[i + 1]; e += kHubChunk)
+        job.tiles.push_back(make_uint4(e, std::min(e + kHubChunk, offs[i + 1]), i, kHubFlag | hub));
+      ++i;
+      continue;
+    }
+    uint32_t j = i;
+    uint32_t edges = 0;
+    while (j < job.hi && j - i < kTileMaxDests) {
+      const uint32_t d = offs[j + 1] - offs[j];
+      if (d > kHubChunk) break;
+      if (j > i && edges + d > kTileEdgeBudget) break;
+      edges += d;
+      ++j;
+    }
+    job.tiles.push_back(make_uint4(offs[i], offs[j], i, j));
+    i = j;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
+  SR_CUDA(cudaSetDevice(dev_));
+  SR_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev_));
+  SR_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  SR_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+  SR_CUDA(cudaEventCreate(&ev_start_));
+  SR_CUDA(cudaEventCreate(&ev_stop_));
+  SR_CUDA(cudaEventCreateWithFlags(&ev_step_, cudaEventDisableTiming));
+  blocks_per_sm_ = pull_blocks_per_sm(kSssp, kGateOff, false);
+  census_.reserve(1);
+  census_h_.reserve(1);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(dev_);
+  if (comm_) ncclCommDestroy(comm_);
+  for (auto& s : slots_) {
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.freed) cudaEventDestroy(s.freed);
+  }
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (xs_) cudaStreamSynchronize(xs_);
+  if (ev_start_) cudaEventDestroy(ev_start_);
+  if (ev_stop_) cudaEventDestroy(ev_stop_);
+  if (ev_step_) cudaEventDestroy(ev_step_);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (xs_) cudaStreamDestroy(xs_);
+}
+
+// ---------------------------------------------------------------------------
+// Graph upload
+// ---------------------------------------------------------------------------
+void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                      const uint32_t* w) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (!off) throw EngineError(SR_E_INPUT, "csr: out_offsets is null");
+  if (off[0] != 0 || off[n] != m)
+    throw EngineError(SR_E_INPUT, "csr: out_offsets must start at 0 and end at num_edges");
+  const auto t0 = std::chrono::steady_clock::now();
+  n_ = n;
+  m_ = m;
+  out_off_.reserve(size_t(n) + 1);
+  SR_CUDA(cudaMemcpyAsync(out_off_.p, off, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice, xs_));
+  uint64_t bytes = (uint64_t(n) + 1) * 8;
+  has_csr_edges_ = nbr != nullptr;
+  csr_weighted_ = false;
+  if (nbr && m) {
+    out_nbr_.reserve(m);
+    SR_CUDA(cudaMemcpyAsync(out_nbr_.p, nbr, m * 4, cudaMemcpyHostToDevice, xs_));
+    bytes += m * 4;
+    if (w) {
+      out_w_.reserve(m);
+      SR_CUDA(cudaMemcpyAsync(out_w_.p, w, m * 4, cudaMemcpyHostToDevice, xs_));
+      bytes += m * 4;
+      csr_weighted_ = true;
+    }
+  } else if (nbr && w) {
+    csr_weighted_ = true;  // weighted graph without edges
+  }
+  SR_CUDA(cudaStreamSynchronize(xs_));
+  has_csr_ = true;
+  last_upload_bytes += bytes;
+  last_upload_seconds +=
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Engine::build_tiles(uint32_t lo, uint32_t hi) {
+  // Jobs of at most 1M destinations so big pages cut in parallel.
+  std::vector<TileJob> jobs;
+  const uint32_t np = uint32_t(pages_.size());
+  for (uint32_t p = 0; p < np; ++p) {
+    const PageMeta& pm = pages_[p];
+    const uint32_t a = std::max(pm.vb, lo), b = std::min(pm.ve, hi);
+    if (a >= b) continue;
+    for (uint32_t x = a - pm.vb; x < b - pm.vb; x += (1u << 20))
+      jobs.push_back(TileJob{p, x, std::min(x + (1u << 20), b - pm.vb), {}, {}});
+  }
+  parallel_for(jobs.size(), [&](size_t j) {
+    const PageMeta& pm = pages_[jobs[j].page];
+    cut_tiles(pm.h_offs, pm.vb, jobs[j]);
+  });
+  std::vector<uint4> tiles;
+  std::vector<uint32_t> tile_page;
+  hub_vertex_h_.clear();
+  for (auto& pm : pages_) pm.tile_begin = pm.tile_end = 0;
+  size_t total = 0;
+  for (auto& j : jobs) total += j.tiles.size();
+  if (total >= (1ull << 32)) throw EngineError(SR_E_CONFIG, "graph too large: tile count");
+  tiles.reserve(total);
+  tile_page.reserve(total);
+  for (auto& j : jobs) {
+    PageMeta& pm = pages_[j.page];
+    if (pm.tile_end == 0 && pm.tile_begin == 0) pm.tile_begin = uint32_t(tiles.size());
+    const uint32_t hub_base = uint32_t(hub_vertex_h_.size());
+    for (uint4 t : j.tiles) {
+      if (t.w & kHubFlag) t.w = kHubFlag | ((t.w & ~kHubFlag) + hub_base);
+      tiles.push_back(t);
+      tile_page.push_back(j.page);
+    }
+    hub_vertex_h_.insert(hub_vertex_h_.end(), j.hubs.begin(), j.hubs.end());
+    pm.tile_end = uint32_t(tiles.size());
+  }
+  n_hubs_ = uint32_t(hub_vertex_h_.size());
+  tiles_.reserve(std::max<size_t>(tiles.size(), 1));
+  tile_page_.reserve(std::max<size_t>(tiles.size(), 1));
+  if (!tiles.empty()) {
+    SR_CUDA(cudaMemcpyAsync(tiles_.p, tiles.data(), tiles.size() * 16, cudaMemcpyHostToDevice, xs_));
+    SR_CUDA(cudaMemcpyAsync(tile_page_.p, tile_page.data(), tile_page.size() * 4,
+                            cudaMemcpyHostToDevice, xs_));
+  }
+  hub_vertex_.reserve(std::max<uint32_t>(n_hubs_, 1));
+  hub_stamp_.reserve(std::max<uint32_t>(n_hubs_, 1));
+  hub_sum_.reserve(std::max<uint32_t>(n_hubs_, 1));
+  if (n_hubs_) {
+    SR_CUDA(cudaMemcpyAsync(hub_vertex_.p, hub_vertex_h_.data(), n_hubs_ * 4,
+                            cudaMemcpyHostToDevice, xs_));
+    SR_CUDA(cudaMemsetAsync(hub_stamp_.p, 0, n_hubs_ * 4, xs_));
+    SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, xs_));
+  }
+  SR_CUDA(cudaStreamSynchronize(xs_));
+  run_id_ = 0;
+}
+
+void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* views,
+                        uint32_t np) {
+  SR_CUDA(cudaSetDevice(dev_));
+  const auto t0 = std::chrono::steady_clock::now();
+  if (np == 0 && n != 0) throw EngineError(SR_E_INPUT, "page set has no pages");
+  // ---- validate the CscPage contract (graph.hpp:46-65) ----
+  uint32_t expect = 0;
+  for (uint32_t p = 0; p < np; ++p) {
+    const sr_page_view& v = views[p];
+    if (v.vertex_begin != expect || v.vertex_end <= v.vertex_begin || v.vertex_end > n)
+      throw EngineError(SR_E_INPUT, "page " + std::to_string(p) +
+                                        ": destination ranges must tile [0, num_vertices)");
+    if (v.edge_count > 0xffffffffull)
+      throw EngineError(SR_E_CONFIG, "page " + std::to_string(p) +
+                                         " exceeds 2^32 edges (u32 local offsets, graph.hpp:49)");
+    const uint32_t range = v.vertex_end - v.vertex_begin;
+    if (!v.in_offsets || v.in_offsets[0] != 0 || v.in_offsets[range] != v.edge_count)
+      throw EngineError(SR_E_INPUT, "page " + std::to_string(p) + ": bad in_offsets");
+    if (v.edge_count && !v.in_sources)
+      throw EngineError(SR_E_INPUT, "page " + std::to_string(p) + ": null in_sources");
+    if (weighted && v.edge_count && !v.in_weights)
+      throw EngineError(SR_E_INPUT, "page " + std::to_string(p) + ": weighted page without weights");
+    expect = v.vertex_end;
+  }
+  if (expect != n) throw EngineError(SR_E_INPUT, "pages do not cover all vertices");
+
+  page_n_ = n;
+  cap_ = cap;
+  weighted_ = weighted;
+  pages_.assign(np, PageMeta{});
+  page_bytes_total_ = 0;
+  page_edges_total_ = 0;
+  for (uint32_t p = 0; p < np; ++p) {
+    PageMeta& pm = pages_[p];
+    pm.vb = views[p].vertex_begin;
+    pm.ve = views[p].vertex_end;
+    pm.edges = views[p].edge_count;
+    pm.bytes = page_bytes_rule(pm.ve - pm.vb, pm.edges, weighted);
+    pm.h_offs = views[p].in_offsets;
+    pm.h_src = views[p].in_sources;
+    pm.h_w = weighted ? views[p].in_weights : nullptr;
+    page_bytes_total_ += pm.bytes;
+    page_edges_total_ += pm.edges;
+  }
+  if (world_ <= 1) {
+    own_lo_ = 0;
+    own_hi_ = n;
+  } else {
+    // edge-balanced contiguous destination cut (sr_shard_plan)
+    std::vector<uint64_t> before(np + 1, 0);
+    for (uint32_t p = 0; p < np; ++p) before[p + 1] = before[p] + views[p].edge_count;
+    auto cut_at = [&](uint64_t target) -> uint32_t {
+      if (target == 0) return 0;
+      if (target >= before[np]) return n;
+      // smallest vertex whose global in-edge prefix reaches target
+      uint32_t p = uint32_t(std::lower_bound(before.begin() + 1, before.end(), target) -
+                            (before.begin() + 1));
+      const sr_page_view& v = views[p];
+      const uint32_t range = v.vertex_end - v.vertex_begin;
+      const uint64_t local = target - before[p];
+      const uint32_t* o = v.in_offsets;
+      const uint32_t k = uint32_t(std::lower_bound(o, o + range + 1, local) - o);
+      return v.vertex_begin + std::min(k, range);
+    };
+    own_lo_ = cut_at(before[np] * uint64_t(rank_) / uint64_t(world_));
+    own_hi_ = cut_at(before[np] * uint64_t(rank_ + 1) / uint64_t(world_));
+    if (rank_ == world_ - 1) own_hi_ = n;
+  }
+  build_tiles(own_lo_, own_hi_);
+
+  // ---- residency: the whole (owned) page set in HBM when it fits ----
+  uint64_t used_bytes = 0;
+  std::vector<char> used(np, 0);
+  for (uint32_t p = 0; p < np; ++p) {
+    used[p] = pages_[p].tile_end > pages_[p].tile_begin || (pages_[p].ve > pages_[p].vb &&
+                                                            pages_[p].vb < own_hi_ &&
+                                                            pages_[p].ve > own_lo_);
+    if (used[p]) used_bytes += pages_[p].bytes;
+  }
+  all_resident_ = budget_ == 0 || used_bytes <= budget_;
+  for (auto& s : slots_) {
+    s.page = -1;
+    s.last_use = -1;
+  }
+  plan_window_ = 0;
+  plan_cached_ = size_t(-1);
+  page_desc_h_.assign(np, PageDesc{});
+  uint64_t upload = 0;
+  if (all_resident_) {
+    uint64_t off_total = 0, edge_total = 0;
+    for (uint32_t p = 0; p < np; ++p) {
+      if (!used[p]) continue;
+      pages_[p].off_base = off_total;
+      pages_[p].edge_base = edge_total;
+      off_total += pages_[p].ve - pages_[p].vb + 1;
+      edge_total += pages_[p].edges;
+    }
+    arena_offs_.reserve(std::max<uint64_t>(off_total, 1));
+    arena_src_.reserve(std::max<uint64_t>(edge_total, 1));
+    if (weighted) arena_w_.reserve(std::max<uint64_t>(edge_total, 1));
+    for (uint32_t p = 0; p < np; ++p) {
+      PageMeta& pm = pages_[p];
+      PageDesc& d = page_desc_h_[p];
+      d.vertex_begin = pm.vb;
+      d.range = pm.ve - pm.vb;
+      d.edge_count = pm.edges;
+      if (!used[p]) continue;
+      d.offs = arena_offs_.p + pm.off_base;
+      d.src = arena_src_.p + pm.edge_base;
+      d.w = weighted ? arena_w_.p + pm.edge_base : nullptr;
+      SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.offs), pm.h_offs, (size_t(d.range) + 1) * 4,
+                              cudaMemcpyHostToDevice, xs_));
+      if (pm.edges) {
+        SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.src), pm.h_src, pm.edges * 4,
+                                cudaMemcpyHostToDevice, xs_));
+        if (weighted)
+          SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.w), pm.h_w, pm.edges * 4,
+                                  cudaMemcpyHostToDevice, xs_));
+      }
+      pm.on_device = true;
+      upload += pm.bytes;
+    }
+    SR_CUDA(cudaStreamSynchronize(xs_));
+    // host pointers are borrowed only for the call
+    for (auto& pm : pages_) pm.h_offs = pm.h_src = pm.h_w = nullptr;
+  } else {
+    // Out-of-core: keep a pinned host copy of every used page (the source
+    // of the copy-stream transfers); pages are admitted at run time.
+    uint64_t words = 0;
+    for (uint32_t p = 0; p < np; ++p)
+      if (used[p]) words += pages_[p].bytes / 4;
+    stage_.reserve(std::max<uint64_t>(words, 1));
+    uint64_t at = 0;
+    std::vector<std::pair<uint32_t, uint64_t>> place;
+    for (uint32_t p = 0; p < np; ++p) {
+      PageMeta& pm = pages_[p];
+      PageDesc& d = page_desc_h_[p];
+      d.vertex_begin = pm.vb;
+      d.range = pm.ve - pm.vb;
+      d.edge_count = pm.edges;
+      pm.on_device = false;
+      if (!used[p]) continue;
+      place.push_back({p, at});
+      at += pm.bytes / 4;
+    }
+    parallel_for(place.size(), [&](size_t k) {
+      PageMeta& pm = pages_[place[k].first];
+      uint32_t* base = stage_.p + place[k].second;
+      const size_t r1 = size_t(pm.ve - pm.vb) + 1;
+      std::memcpy(base, pm.h_offs, r1 * 4);
+      std::memcpy(base + r1, pm.h_src, pm.edges * 4);
+      if (weighted) std::memcpy(base + r1 + pm.edges, pm.h_w, pm.edges * 4);
+    });
+    for (auto& [p, off] : place) {
+      PageMeta& pm = pages_[p];
+      const size_t r1 = size_t(pm.ve - pm.vb) + 1;
+      pm.h_offs = stage_.p + off;
+      pm.h_src = stage_.p + off + r1;
+      pm.h_w = weighted ? stage_.p + off + r1 + pm.edges : nullptr;
+    }
+    for (auto& pm : pages_)
+      if (!pm.h_offs) pm.h_src = pm.h_w = nullptr;
+  }
+  page_desc_.reserve(std::max<uint32_t>(np, 1));
+  if (np)
+    SR_CUDA(cudaMemcpy(page_desc_.p, page_desc_h_.data(), np * sizeof(PageDesc),
+                       cudaMemcpyHostToDevice));
+  pages_loaded_ = true;
+  last_upload_bytes += upload;
+  last_upload_seconds +=
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// Run configuration
+// ---------------------------------------------------------------------------
+void Engine::validate(const sr_run_config& c) const {
+  // EngineConfig::validate (engine.cpp:43-49) + ScheduleMode::validate
+  // (scheduler.cpp:40-47) + run()'s structure checks (engine.cpp:421-431).
+  if (c.window_capacity < 2) throw EngineError(SR_E_CONFIG, "window capacity must be >= 2");
+  if (!(c.density_threshold_fraction > 0.0 && c.density_threshold_fraction <= 1.0))
+    throw EngineError(SR_E_CONFIG, "density threshold fraction must be in (0, 1]");
+  if (c.bytes_per_time_unit <= 0.0 || c.edges_per_time_unit_per_worker <= 0.0)
+    throw EngineError(SR_E_CONFIG, "transfer model rates must be positive");
+  if (c.worker_count < 1) throw EngineError(SR_E_CONFIG, "worker_count must be >= 1");
+  if (c.schedule < 0 || c.schedule > SR_SCHED_PIPELINED_FINE)
+    throw EngineError(SR_E_CONFIG, "unknown scheduler mode");
+  if (c.schedule == SR_SCHED_REENTRY && c.max_reentry_times < 1)
+    throw EngineError(SR_E_CONFIG, "max reentry times must be >= 1");
+  if (c.schedule == SR_SCHED_DOUBLE_BUFFER && c.buffer_repetitions < 1)
+    throw EngineError(SR_E_CONFIG, "double-buffer repetitions must be >= 1");
+  if (c.predictor < 0 || c.predictor > SR_PRED_WEAK)
+    throw EngineError(SR_E_CONFIG, "unknown predictor mode");
+  if (c.execution < 0 || c.execution > SR_EXEC_FORCE_DENSE)
+    throw EngineError(SR_E_CONFIG, "unknown execution policy");
+  if (c.algo < SR_ALGO_BFS || c.algo > SR_ALGO_PAGERANK)
+    throw EngineError(SR_E_CONFIG, "unknown algorithm");
+  if (!pages_loaded_) throw EngineError(SR_E_CONFIG, "no page set loaded");
+  if (!has_csr_) throw EngineError(SR_E_CONFIG, "no csr loaded");
+  if (n_ != page_n_) throw EngineError(SR_E_CONFIG, "csr and page set disagree on vertex count");
+  if (c.algo == SR_ALGO_SSSP && (!csr_weighted_ || !weighted_))
+    throw EngineError(SR_E_CONFIG, "sssp requires weighted graph structures");
+  if ((c.algo == SR_ALGO_BFS || c.algo == SR_ALGO_SSSP) && c.source >= n_)
+    throw EngineError(SR_E_CONFIG, "source vertex out of range");
+  if (c.algo != SR_ALGO_PAGERANK && !has_csr_edges_ && m_ > 0)
+    throw EngineError(SR_E_CONFIG, "traversal needs the csr adjacency (push stage)");
+  if (c.algo == SR_ALGO_PAGERANK) {
+    if (c.pr_iterations < 1) throw EngineError(SR_E_CONFIG, "pagerank iterations must be >= 1");
+    if (!(c.pr_damping >= 0.0 && c.pr_damping < 1.0))
+      throw EngineError(SR_E_CONFIG, "pagerank damping must be in [0, 1)");
+  }
+  if (c.clock == SR_CLOCK_VIRTUAL && c.algo != SR_ALGO_PAGERANK && world_ > 1)
+    throw EngineError(SR_E_CONFIG, "virtual clock runs on a single device");
+}
+
+void Engine::alloc_run_state(const sr_run_config& c) {
+  const size_t npad = (size_t(n_) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
+  const uint32_t nb = (n_ + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  if (c.algo == SR_ALGO_PAGERANK) {
+    rank_a_.reserve(npad);
+    rank_b_.reserve(npad);
+    contrib_a_.reserve(npad);
+    contrib_b_.reserve(npad);
+    inv_outdeg_.reserve(npad);
+  } else {
+    values_.reserve(npad);
+    changed_.reserve(npad);
+    if (det_) next_.reserve(npad);
+    if (c.predictor == SR_PRED_WEAK) {
+      status_.reserve(npad);
+      logstate_.reserve(npad);
+    }
+    if (c.predictor == SR_PRED_STRONG && c.algo == SR_ALGO_CC) {
+      snap_.reserve(npad);
+      delta_.reserve(npad);
+    }
+    list_.reserve(npad);
+    pref_.reserve(npad);
+    chunk_start_.reserve(m_ / kPushChunk + 2);
+    blk_cnt_.reserve(nb + 1);
+    blk_edges_.reserve(nb + 1);
+    if (world_ > 1) round_snap_.reserve(npad);
+  }
+  const size_t np = std::max<size_t>(pages_.size(), 1);
+  // counter entries per pass: gated (reentry) runs keep one entry per page
+  // and run; every other launch aggregates into a single entry.
+  size_t entries = size_t(std::max(1, c.max_reentry_times)) * np + np;
+  entries += (np + 1) * size_t(std::max(1, c.buffer_repetitions)) + 4096 + 64;
+  ctr_.reserve(entries);
+  ctr_h_.reserve(entries);
+}
+
+RunCtr* Engine::alloc_ctr(size_t entries) {
+  if (size_t(ctr_used_) + entries > ctr_.n)
+    throw EngineError(SR_E_INTERNAL, "counter arena exhausted");
+  RunCtr* r = ctr_.p + ctr_used_;
+  ctr_used_ += uint32_t(entries);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel launches over page sets
+// ---------------------------------------------------------------------------
+RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool det, RunCtr* ctr,
+                              const RunCtr* prev, bool per_page, bool pagerank) {
+  Segments seg{};
+  auto flush = [&]() {
+    if (seg.n == 0) return;
+    const uint32_t tasks = seg.task_prefix[seg.n];
+    int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                      (uint64_t(tasks) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    grid = std::max(grid, 1);
+    if (pagerank) {
+      PrArgs a{};
+      a.tiles = tiles_.p;
+      a.tile_page = tile_page_.p;
+      a.pages = page_desc_.p;
+      a.seg = seg;
+      a.contrib_in = contrib_a_.p;
+      a.rank_out = rank_b_.p;
+      a.contrib_out = contrib_b_.p;
+      a.inv_outdeg = inv_outdeg_.p;
+      a.hub_sum = hub_sum_.p;
+      a.ctr = ctr;
+      a.base = float((1.0 - pr_damp_) / double(n_));
+      a.damp = float(pr_damp_);
+      launch_pr_pull(a, grid, cs_);
+    } else {
+      PullArgs a{};
+      a.tiles = tiles_.p;
+      a.tile_page = tile_page_.p;
+      a.pages = page_desc_.p;
+      a.seg = seg;
+      a.values = values_.p;
+      a.next = det ? next_.p : values_.p;
+      a.changed = changed_.p;
+      a.status = status_.p;
+      a.hub_stamp = hub_stamp_.p;
+      a.run_id = ++run_id_;
+      a.ctr = ctr;
+      a.prev_ctr = prev;
+      a.ctr_per_page = per_page ? 1u : 0u;
+      a.census = census_.p;
+      a.k_bfs = k_bfs_;
+      a.s_cc = s_cc_;
+      a.l_sssp = l_sssp_;
+      launch_pull(algo_, gate, det, a, grid, cs_);
+    }
+    SR_CUDA(cudaGetLastError());
+    ++launches_;
+    seg = Segments{};
+  };
+  uint32_t last_end = 0xffffffffu;
+  for (uint32_t p : pages) {
+    const PageMeta& pm = pages_[p];
+    if (pm.tile_end <= pm.tile_begin) continue;
+    if (seg.n > 0 && pm.tile_begin == last_end) {
+      seg.task_prefix[seg.n] += pm.tile_end - pm.tile_begin;
+    } else {
+      if (seg.n == kMaxSegments) flush();
+      seg.tile_begin[seg.n] = pm.tile_begin;
+      seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (pm.tile_end - pm.tile_begin);
+      ++seg.n;
+    }
+    last_end = pm.tile_end;
+  }
+  flush();
+  return RunStats{};
+}
+
+// ---------------------------------------------------------------------------
+// Streaming window (out-of-core path)
+// ---------------------------------------------------------------------------
+void Engine::ensure_slots(uint32_t window, PassOut& po) {
+  // Budget plan for the out-of-core path: a ring of `window` slots sized for
+  // the largest streamed page, and the longest prefix of pages (id order,
+  // i.e. RMAT's heaviest pages first) that still fits cached permanently.
+  std::vector<uint32_t> used;
+  for (uint32_t p = 0; p < pages_.size(); ++p)
+    if (pages_[p].h_offs) used.push_back(p);
+  const uint32_t want = std::max<uint32_t>(window, 2);
+  const size_t U = used.size();
+  std::vector<uint64_t> suf_offs(U + 1, 0), suf_edges(U + 1, 0);
+  for (size_t k = U; k-- > 0;) {
+    const PageMeta& pm = pages_[used[k]];
+    suf_offs[k] = std::max<uint64_t>(suf_offs[k + 1], pm.ve - pm.vb + 1);
+    suf_edges[k] = std::max<uint64_t>(suf_edges[k + 1], pm.edges);
+  }
+  const uint64_t wmul = weighted_ ? 2 : 1;
+  size_t K = 0;
+  bool fits = false;
+  uint64_t prefix = 0;
+  for (size_t k = 0; k < U; ++k) {
+    const uint64_t slot_bytes = (suf_offs[k] + suf_edges[k] * wmul) * 4;
+    if (prefix + want * slot_bytes <= budget_) {
+      K = k;
+      fits = true;
+    }
+    prefix += pages_[used[k]].bytes;
+  }
+  if (!fits)
+    throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(budget_) +
+                                       " B cannot hold a window of " + std::to_string(want) +
+                                       " page slots of " +
+                                       std::to_string((suf_offs[0] + suf_edges[0] * wmul) * 4) + " B");
+  const uint64_t max_offs = suf_offs[K], max_edges = suf_edges[K];
+  const bool same_plan = plan_window_ == want && plan_cached_ == K && slots_.size() == want;
+  if (same_plan) return;
+  // (re)build the cache arena for pages used[0..K)
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  for (auto& pm : pages_) {
+    pm.on_device = false;
+    pm.slot = -1;
+  }
+  uint64_t off_total = 0, edge_total = 0;
+  for (size_t k = 0; k < K; ++k) {
+    PageMeta& pm = pages_[used[k]];
+    pm.off_base = off_total;
+    pm.edge_base = edge_total;
+    off_total += pm.ve - pm.vb + 1;
+    edge_total += pm.edges;
+  }
+  arena_offs_.release();
+  arena_src_.release();
+  arena_w_.release();
+  if (K) {
+    arena_offs_.reserve(off_total);
+    arena_src_.reserve(std::max<uint64_t>(edge_total, 1));
+    if (weighted_) arena_w_.reserve(std::max<uint64_t>(edge_total, 1));
+  }
+  for (size_t k = 0; k < K; ++k) {
+    const uint32_t p = used[k];
+    PageMeta& pm = pages_[p];
+    uint32_t* o = arena_offs_.p + pm.off_base;
+    uint32_t* sp = arena_src_.p + pm.edge_base;
+    uint32_t* wp = weighted_ ? arena_w_.p + pm.edge_base : nullptr;
+    SR_CUDA(cudaMemcpyAsync(o, pm.h_offs, (size_t(pm.ve - pm.vb) + 1) * 4, cudaMemcpyHostToDevice, xs_));
+    if (pm.edges) {
+      SR_CUDA(cudaMemcpyAsync(sp, pm.h_src, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
+      if (wp) SR_CUDA(cudaMemcpyAsync(wp, pm.h_w, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
+    }
+    launch_set_page_desc(page_desc_.p, p, o, sp, wp, xs_);
+    pm.on_device = true;
+    po.pages_transferred += 1;
+    po.bytes_transferred += pm.bytes;
+    h2d_bytes_ += pm.bytes;
+  }
+  for (auto& s : slots_) {
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.freed) cudaEventDestroy(s.freed);
+  }
+  slots_.clear();
+  slots_.resize(want);
+  for (auto& s : slots_) {
+    s.offs.reserve(std::max<uint64_t>(max_offs, 1));
+    s.src.reserve(std::max<uint64_t>(max_edges, 1));
+    if (weighted_) s.w.reserve(std::max<uint64_t>(max_edges, 1));
+    s.cap_offs = max_offs;
+    s.cap_edges = max_edges;
+    SR_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+    SR_CUDA(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
+    SR_CUDA(cudaEventRecord(s.freed, cs_));
+  }
+  SR_CUDA(cudaEventRecord(ev_step_, xs_));
+  SR_CUDA(cudaStreamWaitEvent(cs_, ev_step_, 0));
+  plan_window_ = want;
+  plan_cached_ = K;
+}
+
+void Engine::make_resident(uint32_t page, long long step, const std::vector<char>& protect,
+                           PassOut& po) {
+  PageMeta& pm = pages_[page];
+  if (pm.on_device || pm.slot >= 0) return;
+  int best = -1;
+  for (int s = 0; s < int(slots_.size()); ++s) {
+    const StreamSlot& sl = slots_[s];
+    if (sl.page < 0) {
+      best = s;
+      break;
+    }
+    if (protect[sl.page]) continue;
+    if (best < 0 || sl.last_use < slots_[best].last_use) best = s;
+  }
+  if (best < 0) throw EngineError(SR_E_CONTRACT, "transfer scheduled with no slot available");
+  StreamSlot& sl = slots_[best];
+  if (sl.page >= 0) pages_[sl.page].slot = -1;
+  // the copy may only overwrite the slot once its last reader finished
+  SR_CUDA(cudaStreamWaitEvent(xs_, sl.freed, 0));
+  const size_t r1 = size_t(pm.ve - pm.vb) + 1;
+  SR_CUDA(cudaMemcpyAsync(sl.offs.p, pm.h_offs, r1 * 4, cudaMemcpyHostToDevice, xs_));
+  if (pm.edges) {
+    SR_CUDA(cudaMemcpyAsync(sl.src.p, pm.h_src, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
+    if (weighted_)
+      SR_CUDA(cudaMemcpyAsync(sl.w.p, pm.h_w, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
+  }
+  launch_set_page_desc(page_desc_.p, page, sl.offs.p, sl.src.p, weighted_ ? sl.w.p : nullptr, xs_);
+  SR_CUDA(cudaEventRecord(sl.ready, xs_));
+  sl.page = int(page);
+  sl.last_use = step;
+  pm.slot = best;
+  po.pages_transferred += 1;
+  po.bytes_transferred += pm.bytes;
+  h2d_bytes_ += pm.bytes;
+}
+
+// ---------------------------------------------------------------------------
+// Dense pass, device-native schedule (ClockMode::Wall)
+// ---------------------------------------------------------------------------
+PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recovery,
+                                uint32_t pass_index, bool pagerank) {
+  (void)pass_index;
+  PassOut po;
+  const int mode = (recovery || pagerank) ? SR_SCHED_BASELINE : cfg.schedule;
+  const uint32_t B = cfg.window_capacity;
+  // admission order: pages already on the device first (reference
+  // scheduler.cpp:211-228), then the rest by id
+  std::vector<uint32_t> order;
+  std::vector<uint32_t> rest;
+  for (uint32_t p = 0; p < pages_.size(); ++p) {
+    if (pages_[p].tile_end <= pages_[p].tile_begin) continue;
+    if (pages_[p].on_device || pages_[p].slot >= 0) order.push_back(p);
+    else rest.push_back(p);
+  }
+  const size_t n_dev = order.size();
+  order.insert(order.end(), rest.begin(), rest.end());
+  const size_t n = order.size();
+
+  struct Step {
+    std::vector<uint32_t> pages;
+    int reps;
+    bool gated;
+  };
+  std::vector<Step> steps;
+  auto slice = [&](size_t lo, size_t hi) {
+    return std::vector<uint32_t>(order.begin() + lo, order.begin() + hi);
+  };
+  const bool stream = streaming();
+  switch (mode) {
+    case SR_SCHED_REENTRY:
+      if (!stream) {
+        steps.push_back({order, cfg.max_reentry_times, true});
+      } else {
+        if (n_dev) steps.push_back({slice(0, n_dev), cfg.max_reentry_times, true});
+        for (size_t i = n_dev; i < n; ++i) steps.push_back({slice(i, i + 1), cfg.max_reentry_times, true});
+      }
+      break;
+    case SR_SCHED_DOUBLE_BUFFER: {
+      const size_t half = std::max<size_t>(1, B / 2);
+      for (size_t lo = 0; lo < n; lo += half)
+        steps.push_back({slice(lo, std::min(lo + half, n)), cfg.buffer_repetitions, false});
+      break;
+    }
+    case SR_SCHED_PIPELINED:
+    case SR_SCHED_PIPELINED_FINE: {
+      const size_t cs = std::min<size_t>(B - 1, n);
+      for (size_t j = 0; cs && j + cs <= n; ++j) steps.push_back({slice(j, j + cs), 1, false});
+      break;
+    }
+    default:
+      if (!stream) {
+        steps.push_back({order, 1, false});
+      } else {
+        if (n_dev) steps.push_back({slice(0, n_dev), 1, false});
+        for (size_t i = n_dev; i < n; ++i) steps.push_back({slice(i, i + 1), 1, false});
+      }
+      break;
+  }
+
+  const uint32_t np = uint32_t(pages_.size());
+  std::vector<char> protect(np, 0);
+  auto set_protect = [&](size_t a, size_t b) {
+    std::fill(protect.begin(), protect.end(), 0);
+    for (size_t s = a; s < std::min(b, steps.size()); ++s)
+      for (uint32_t p : steps[s].pages) protect[p] = 1;
+  };
+  if (stream) ensure_slots(B, po);
+  if (!stream && !first_touch_done_) {
+    // resident window: every page admitted once per run (warm afterwards)
+    for (uint32_t p : order) {
+      po.pages_transferred += 1;
+      po.bytes_transferred += pages_[p].bytes;
+    }
+    first_touch_done_ = true;
+  }
+
+  for (size_t si = 0; si < steps.size(); ++si) {
+    const Step& st = steps[si];
+    const long long step_id = ++step_counter_;
+    if (stream) {
+      set_protect(si, si + 1);
+      for (uint32_t p : st.pages) make_resident(p, step_id, protect, po);
+      for (uint32_t p : st.pages)
+        if (pages_[p].slot >= 0) SR_CUDA(cudaStreamWaitEvent(cs_, slots_[pages_[p].slot].ready, 0));
+    }
+    const bool per_page = st.gated && st.pages.size() > 1;
+    RunCtr* prev = nullptr;
+    for (int r = 0; r < st.reps; ++r) {
+      RunCtr* slot = alloc_ctr(per_page ? std::max<size_t>(np, 1) : 1);
+      launch_pages(st.pages, gate, false, slot, (st.gated && r > 0) ? prev : nullptr, per_page,
+                   pagerank);
+      prev = slot;
+      po.kernel_runs += st.pages.size();
+    }
+    if (stream) {
+      for (uint32_t p : st.pages) {
+        const int s = pages_[p].slot;
+        if (s >= 0) {
+          SR_CUDA(cudaEventRecord(slots_[s].freed, cs_));
+          slots_[s].last_use = step_id;
+        }
+      }
+      // prefetch the next step's pages; LRU victims (pages of older steps
+      // first), never the next step's pages nor the idle-fill victim
+      if (si + 1 < steps.size()) {
+        set_protect(si + 1, si + 2);
+        if (mode == SR_SCHED_PIPELINED_FINE && !st.pages.empty())
+          protect[*std::min_element(st.pages.begin(), st.pages.end())] = 1;
+        bool pending = false;
+        cudaEvent_t last_ready = nullptr;
+        for (uint32_t p : steps[si + 1].pages) {
+          const bool was = pages_[p].on_device || pages_[p].slot >= 0;
+          make_resident(p, step_id, protect, po);
+          if (!was) {
+            pending = true;
+            last_ready = slots_[pages_[p].slot].ready;
+          }
+        }
+        if (mode == SR_SCHED_PIPELINED_FINE && pending && !st.pages.empty()) {
+          // fill_idle_slot (scheduler.cpp:153-158): while the stream is in
+          // flight and compute is idle, re-run the lowest-id page of the set
+          const uint32_t victim = *std::min_element(st.pages.begin(), st.pages.end());
+          SR_CUDA(cudaEventRecord(ev_step_, cs_));
+          int guard = 0;
+          while (cudaEventQuery(last_ready) == cudaErrorNotReady && guard < 4000) {
+            if (cudaEventQuery(ev_step_) == cudaSuccess) {
+              if (size_t(ctr_used_) + 1 > ctr_.n) break;
+              RunCtr* slot = alloc_ctr(1);
+              launch_pages({victim}, gate, false, slot, nullptr, false, pagerank);
+              po.kernel_runs += 1;
+              SR_CUDA(cudaEventRecord(ev_step_, cs_));
+              ++guard;
+            } else {
+              std::this_thread::yield();
+            }
+          }
+          const int s = pages_[victim].slot;
+          if (s >= 0) SR_CUDA(cudaEventRecord(slots_[s].freed, cs_));
+        }
+      }
+    }
+  }
+  return po;
+}
+
+// ---------------------------------------------------------------------------
+// Dense pass, deterministic virtual-clock schedule (ClockMode::Virtual)
+// ---------------------------------------------------------------------------
+PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool recovery,
+                                   uint32_t pass_index) {
+  if (streaming())
+    throw EngineError(SR_E_CONFIG,
+                      "virtual clock needs the page set resident (raise the hbm budget)");
+  std::vector<uint64_t> bytes(pages_.size());
+  for (size_t p = 0; p < pages_.size(); ++p) bytes[p] = pages_[p].bytes;
+  const uint32_t np = uint32_t(pages_.size());
+  VKernel kernel = [&](uint32_t page) -> RunStats {
+    RunCtr* slot = ctr_.p;  // slot 0, synchronous
+    SR_CUDA(cudaMemsetAsync(slot, 0, sizeof(RunCtr), cs_));
+    launch_pages({page}, gate, true, slot, nullptr, false, false);
+    launch_commit(values_.p, next_.p, pages_[page].vb, pages_[page].ve, cs_);
+    ++launches_;
+    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, slot, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    RunStats st;
+    st.attempts = ctr_h_.p[0].attempts;
+    st.valid = ctr_h_.p[0].valid;
+    st.skipped = ctr_h_.p[0].skipped;
+    st.edges = ctr_h_.p[0].edges;
+    return st;
+  };
+  (void)np;
+  const int mode = recovery ? SR_SCHED_BASELINE : cfg.schedule;
+  VPassResult r = vschedule_pass(bytes, mode, cfg.max_reentry_times, cfg.buffer_repetitions,
+                                 vwin_, vclock_, vmodel_, kernel, pass_index,
+                                 record_trace_ ? &trace : nullptr);
+  PassOut po;
+  po.totals = r.totals;
+  po.kernel_runs = r.kernel_runs;
+  po.pages_transferred = r.pages_transferred;
+  po.bytes_transferred = r.bytes_transferred;
+  return po;
+}
+
+// ---------------------------------------------------------------------------
+// Per-pass bookkeeping
+// ---------------------------------------------------------------------------
+void Engine::census(int pass_kind) {
+  SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
+  launch_census(n_, changed_.p, predictor_ == SR_PRED_WEAK ? status_.p : nullptr,
+                predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr,
+                has_csr_ ? out_off_.p : nullptr, pass_kind, own_lo_, own_hi_, blk_cnt_.p,
+                blk_edges_.p, census_.p, cs_);
+}
+
+void Engine::read_census() {
+  SR_CUDA(cudaMemcpyAsync(census_h_.p, census_.p, sizeof(Census), cudaMemcpyDeviceToHost, cs_));
+  if (ctr_used_)
+    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
+                            cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+}
+
+void Engine::build_push_list() {
+  const uint32_t nb = (n_ + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  launch_scan_blocks(nb, blk_cnt_.p, blk_edges_.p, cs_);
+  launch_compact(n_, own_lo_, own_hi_, changed_.p, out_off_.p, blk_cnt_.p, blk_edges_.p,
+                 list_.p, pref_.p, chunk_start_.p, cs_);
+}
+
+void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
+  (void)cfg;
+  const uint64_t n_list = census_h_.p->own_push;
+  const uint64_t total = census_h_.p->own_edges;
+  build_push_list();
+  RunCtr* slot = alloc_ctr(1);
+  if (total > 0) {
+    PushArgs a{};
+    a.list = list_.p;
+    a.pref = pref_.p;
+    a.chunk_start = chunk_start_.p;
+    a.n_list = uint32_t(n_list);
+    a.total_edges = total;
+    a.out_offsets = out_off_.p;
+    a.out_neighbors = out_nbr_.p;
+    a.out_weights = csr_weighted_ ? out_w_.p : nullptr;
+    a.values = values_.p;
+    a.next = det_ ? next_.p : values_.p;
+    a.changed = changed_.p;
+    a.ctr = slot;
+    a.census = census_.p;
+    const uint64_t chunks = (total + kPushChunk - 1) / kPushChunk;
+    const int grid = int(std::max<uint64_t>(
+        1, std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_, (chunks + kWarpsPerBlock - 1) / kWarpsPerBlock)));
+    launch_push(algo_, det_, a, grid, cs_);
+    SR_CUDA(cudaGetLastError());
+    ++launches_;
+    if (det_) launch_push_commit(values_.p, next_.p, changed_.p, n_, slot, census_.p, cs_);
+  }
+  (void)st;
+}
+
+void Engine::exchange_round(bool pagerank) {
+  if (world_ <= 1) return;
+  ncclResult_t r = ncclSuccess;
+  SR_CUDA(cudaSetDevice(dev_));
+  ncclGroupStart();
+  if (pagerank) {
+    r = ncclAllReduce(rank_b_.p, rank_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
+    if (r == ncclSuccess)
+      r = ncclAllReduce(contrib_b_.p, contrib_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
+  } else {
+    r = ncclAllReduce(values_.p, values_.p, n_, ncclUint32, ncclMin, comm_, cs_);
+    if (r == ncclSuccess)
+      r = ncclAllReduce(&census_.p->min_changed, &census_.p->min_changed, 1, ncclUint32, ncclMin,
+                        comm_, cs_);
+  }
+  if (r == ncclSuccess && ctr_used_)
+    r = ncclAllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * 4, ncclUint64, ncclSum, comm_, cs_);
+  ncclGroupEnd();
+  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + ncclGetErrorString(r));
+  if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
+}
+
+// ---------------------------------------------------------------------------
+// The pass loop (reference Runner::run, engine.cpp:371-416)
+// ---------------------------------------------------------------------------
+void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out,
+                 sr_metrics& m, std::vector<sr_pass_stats>& passes) {
+  SR_CUDA(cudaSetDevice(dev_));
+  validate(cfg);
+  algo_ = cfg.algo;
+  source_ = cfg.source;
+  predictor_ = cfg.algo == SR_ALGO_PAGERANK ? SR_PRED_OFF : cfg.predictor;
+  det_ = cfg.clock == SR_CLOCK_VIRTUAL && cfg.algo != SR_ALGO_PAGERANK;
+  record_trace_ = cfg.record_trace != 0;
+  pr_damp_ = cfg.pr_damping;
+  trace.clear();
+  std::memset(&m, 0, sizeof(m));
+  passes.clear();
+  launches_ = 0;
+  h2d_bytes_ = 0;
+  first_touch_done_ = false;
+  vwin_.reset(cfg.window_capacity);
+  vclock_ = VClock{};
+  vmodel_.bytes_per_unit = cfg.bytes_per_time_unit;
+  vmodel_.edges_per_unit_per_worker = cfg.edges_per_time_unit_per_worker;
+  vmodel_.workers = cfg.worker_count;
+  alloc_run_state(cfg);
+  if (cfg.algo == SR_ALGO_PAGERANK) run_pagerank(cfg, ranks_out, m, passes);
+  else run_traversal(cfg, values_out, m, passes);
+  m.kernel_launches = launches_;
+  m.h2d_bytes = h2d_bytes_;
+}
+
+void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_metrics& m,
+                           std::vector<sr_pass_stats>& passes) {
+  const bool weak = predictor_ == SR_PRED_WEAK;
+  const bool strong = predictor_ == SR_PRED_STRONG;
+  const size_t npad = values_.n;
+
+  const auto wall0 = std::chrono::steady_clock::now();
+  SR_CUDA(cudaEventRecord(ev_start_, cs_));
+  // ---- initial state (VertexValues ctor programs.hpp:61-64; Runner ctor
+  //      engine.cpp:225-245; initial_frontier engine.cpp:260-263) ----
+  launch_init_values(algo_, source_, n_, values_.p, cs_);
+  if (det_) SR_CUDA(cudaMemcpyAsync(next_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
+  SR_CUDA(cudaMemsetAsync(changed_.p, 0, npad, cs_));
+  if (weak) {
+    SR_CUDA(cudaMemsetAsync(status_.p, 0, npad, cs_));
+    SR_CUDA(cudaMemsetAsync(logstate_.p, 0, npad, cs_));
+  }
+  if (strong && algo_ == SR_ALGO_CC) {
+    SR_CUDA(cudaMemcpyAsync(snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
+    SR_CUDA(cudaMemsetAsync(delta_.p, 0, size_t(n_) * 4, cs_));
+  }
+  SR_CUDA(cudaMemsetAsync(census_.p, 0, sizeof(Census), cs_));
+  SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 8, cs_));  // min_changed, cc_min_label
+  k_bfs_ = 0;
+  s_cc_ = 0;
+  l_sssp_ = 0;
+  if (algo_ == SR_ALGO_CC) SR_CUDA(cudaMemsetAsync(changed_.p, 1, n_, cs_));
+  else SR_CUDA(cudaMemsetAsync(changed_.p + source_, 1, 1, cs_));
+  census(kPassInit);
+  ctr_used_ = 0;
+  read_census();
+
+  uint64_t f_count = census_h_.p->changed;
+  uint64_t f_out = census_h_.p->out_edges;
+  std::array<uint64_t, 6> hist{};
+  for (int s = 0; s < 6; ++s) hist[s] = census_h_.p->status_hist[s];
+  bool prev_dense = false;
+  uint32_t pass_index = 0;
+
+  auto account = [&](sr_pass_stats& st) {
+    m.passes += 1;
+    m.update_attempts += st.attempts;
+    m.valid_updates += st.valid_updates;
+    m.skipped_vertices += st.skipped;
+    m.edges_read += st.edges_read;
+    passes.push_back(st);
+  };
+  auto sum_ctr = [&](sr_pass_stats& st) {
+    for (size_t i = 0; i < size_t(ctr_used_); ++i) {
+      st.attempts += ctr_h_.p[i].attempts;
+      st.valid_updates += ctr_h_.p[i].valid;
+      st.skipped += ctr_h_.p[i].skipped;
+      st.edges_read += ctr_h_.p[i].edges;
+    }
+  };
+  auto begin_pass = [&]() {
+    ctr_used_ = 0;
+    SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
+    if (world_ > 1)
+      SR_CUDA(cudaMemcpyAsync(round_snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
+  };
+  auto after_census = [&]() {
+    f_count = census_h_.p->changed;
+    f_out = census_h_.p->out_edges;
+    for (int s = 0; s < 6; ++s) hist[s] = census_h_.p->status_hist[s];
+  };
+
+  auto do_recovery = [&]() {
+    // recovery_scan (engine.cpp:179-205): all-pull sweep, gate ignored,
+    // scheduled as a baseline pass; changed vertices reset to status 0.
+    begin_pass();
+    SR_CUDA(cudaMemsetAsync(changed_.p, 0, npad, cs_));
+    PassOut po = det_ ? dense_pass_virtual(cfg, kGateOff, true, pass_index)
+                      : dense_pass_wall(cfg, kGateOff, true, pass_index, false);
+    exchange_round(false);
+    census(kPassRecovery);
+    read_census();
+    after_census();
+    sr_pass_stats st{};
+    st.pass_index = pass_index;
+    st.kind = SR_PASS_RECOVERY;
+    if (det_) {
+      st.attempts = po.totals.attempts;
+      st.valid_updates = po.totals.valid;
+      st.skipped = po.totals.skipped;
+      st.edges_read = po.totals.edges;
+    } else {
+      sum_ctr(st);
+    }
+    st.changed_vertices = f_count;
+    m.pages_transferred += po.pages_transferred;
+    m.bytes_transferred += po.bytes_transferred;
+    m.kernel_runs += po.kernel_runs;
+    account(st);
+    m.recovery_passes += 1;
+    ++pass_index;
+  };
+
+  auto do_sparse = [&]() {
+    // sparse_push_pass (engine.cpp:63-93) on the device frontier
+    begin_pass();
+    RunStats dummy;
+    push_pass(cfg, dummy);
+    exchange_round(false);
+    census(kPassSparse);
+    read_census();
+    after_census();
+    sr_pass_stats st{};
+    st.pass_index = pass_index;
+    st.kind = SR_PASS_SPARSE_PUSH;
+    sum_ctr(st);
+    st.changed_vertices = f_count;
+    account(st);
+    m.sparse_passes += 1;
+    ++pass_index;
+  };
+
+  auto do_dense = [&]() {
+    // Runner::run_dense (engine.cpp:279-337)
+    begin_pass();
+    sr_pass_stats st{};
+    st.pass_index = pass_index;
+    st.kind = SR_PASS_DENSE_PULL;
+    if (weak) {
+      for (int s = 0; s < 6; ++s) st.status_counts[s] = hist[s];
+      st.has_status_counts = 1;
+    }
+    SR_CUDA(cudaMemsetAsync(changed_.p, 0, npad, cs_));
+    const int gate = predictor_ == SR_PRED_STRONG ? kGateStrong
+                     : predictor_ == SR_PRED_WEAK ? kGateWeak
+                                                   : kGateOff;
+    PassOut po = det_ ? dense_pass_virtual(cfg, gate, false, pass_index)
+                      : dense_pass_wall(cfg, gate, false, pass_index, false);
+    exchange_round(false);
+    census(kPassDense);
+    if (strong && algo_ == SR_ALGO_CC) launch_cc_refresh(n_, values_.p, snap_.p, delta_.p, census_.p, cs_);
+    read_census();
+    after_census();
+    if (det_) {
+      st.attempts = po.totals.attempts;
+      st.valid_updates = po.totals.valid;
+      st.skipped = po.totals.skipped;
+      st.edges_read = po.totals.edges;
+    } else {
+      sum_ctr(st);
+    }
+    st.changed_vertices = f_count;
+    if (strong) {
+      // refresh_thresholds (predictor.cpp:89-105)
+      k_bfs_ += 1;
+      if (algo_ == SR_ALGO_SSSP) {
+        l_sssp_ = census_h_.p->min_changed;
+        SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 4, cs_));
+      } else if (algo_ == SR_ALGO_CC) {
+        s_cc_ = census_h_.p->cc_min_label;
+        SR_CUDA(cudaMemsetAsync(&census_.p->cc_min_label, 0xff, 4, cs_));
+      }
+    }
+    m.pages_transferred += po.pages_transferred;
+    m.bytes_transferred += po.bytes_transferred;
+    m.kernel_runs += po.kernel_runs;
+    account(st);
+    m.dense_passes += 1;
+    ++pass_index;
+  };
+
+  for (;;) {
+    if (f_count == 0) {
+      if (weak && prev_dense) {
+        do_recovery();
+        prev_dense = false;
+        if (f_count == 0) break;
+        continue;
+      }
+      break;
+    }
+    bool sparse;
+    if (cfg.execution == SR_EXEC_FORCE_SPARSE) sparse = true;
+    else if (cfg.execution == SR_EXEC_FORCE_DENSE) sparse = false;
+    else  // density_switch (engine.cpp:56-61): dense iff out-edges > frac*|E|
+      sparse = !(double(f_out) > cfg.density_threshold_fraction * double(m_));
+    if (sparse && weak && prev_dense) {
+      do_recovery();  // dense-to-sparse switch retrieves dormant actives
+      prev_dense = false;
+      if (f_count == 0) break;
+      continue;
+    }
+    if (sparse) {
+      do_sparse();
+      prev_dense = false;
+    } else {
+      do_dense();
+      prev_dense = true;
+    }
+    if (pass_index > 100000) throw EngineError(SR_E_INTERNAL, "pass loop did not converge");
+  }
+
+  SR_CUDA(cudaEventRecord(ev_stop_, cs_));
+  if (values_out)
+    SR_CUDA(cudaMemcpyAsync(values_out, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  const auto wall1 = std::chrono::steady_clock::now();
+  float ms = 0;
+  SR_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_stop_));
+  m.device_seconds = ms * 1e-3;
+  if (values_out) m.d2h_bytes = uint64_t(n_) * 4;
+  m.virtual_makespan = vclock_.now;
+  if (cfg.clock == SR_CLOCK_WALL)
+    m.wall_seconds = std::chrono::duration<double>(wall1 - wall0).count();
+  if (weak && census_h_.p->log_events > 0) {
+    m.has_prediction_accuracy = 1;
+    m.prediction_accuracy =
+        double(census_h_.p->log_events - census_h_.p->log_incorrect) / double(census_h_.p->log_events);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PageRank (new algorithm; conventions pinned in DESIGN.md §2)
+// ---------------------------------------------------------------------------
+void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
+                          std::vector<sr_pass_stats>& passes) {
+  const auto wall0 = std::chrono::steady_clock::now();
+  SR_CUDA(cudaEventRecord(ev_start_, cs_));
+  launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
+  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
+  if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
+  for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
+    ctr_used_ = 0;
+    SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
+    if (world_ > 1) {
+      SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
+      SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
+    }
+    PassOut po = dense_pass_wall(cfg, kGateOff, false, it, true);
+    launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
+                           inv_outdeg_.p, float((1.0 - cfg.pr_damping) / double(n_)),
+                           float(cfg.pr_damping), cs_);
+    exchange_round(true);
+    if (ctr_used_)
+      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
+                              cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    sr_pass_stats st{};
+    st.pass_index = it;
+    st.kind = SR_PASS_DENSE_PULL;
+    for (size_t i = 0; i < size_t(ctr_used_); ++i) {
+      st.attempts += ctr_h_.p[i].attempts;
+      st.edges_read += ctr_h_.p[i].edges;
+    }
+    st.changed_vertices = n_;
+    m.pages_transferred += po.pages_transferred;
+    m.bytes_transferred += po.bytes_transferred;
+    m.kernel_runs += po.kernel_runs;
+    m.passes += 1;
+    m.dense_passes += 1;
+    m.update_attempts += st.attempts;
+    m.edges_read += st.edges_read;
+    passes.push_back(st);
+    std::swap(rank_a_.p, rank_b_.p);
+    std::swap(contrib_a_.p, contrib_b_.p);
+  }
+  SR_CUDA(cudaEventRecord(ev_stop_, cs_));
+  if (ranks_out)
+    SR_CUDA(cudaMemcpyAsync(ranks_out, rank_a_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  float ms = 0;
+  SR_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_stop_));
+  m.device_seconds = ms * 1e-3;
+  if (ranks_out) m.d2h_bytes = uint64_t(n_) * 4;
+  m.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+}
+
+// ---------------------------------------------------------------------------
+uint64_t Engine::verify_fixpoint(int algo, const uint32_t* values_host) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (!has_csr_edges_) throw EngineError(SR_E_CONFIG, "verify needs the csr adjacency");
+  if (algo == SR_ALGO_SSSP && !csr_weighted_) throw EngineError(SR_E_CONFIG, "sssp needs weights");
+  DBuf<unsigned long long> viol;
+  viol.reserve(1);
+  const size_t npad = size_t(n_) + 16;
+  if (values_host) {
+    values_.reserve(std::max(values_.n, npad));
+    SR_CUDA(cudaMemcpyAsync(values_.p, values_host, size_t(n_) * 4, cudaMemcpyHostToDevice, cs_));
+  } else if (!values_.p) {
+    throw EngineError(SR_E_DATA, "verify: no values from a previous run");
+  }
+  SR_CUDA(cudaMemsetAsync(viol.p, 0, 8, cs_));
+  launch_verify(algo, n_, out_off_.p, out_nbr_.p, csr_weighted_ ? out_w_.p : nullptr, values_.p,
+                viol.p, cs_);
+  unsigned long long h = 0;
+  SR_CUDA(cudaMemcpyAsync(&h, viol.p, 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  return h;
+}
+
+void Engine::bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (streaming()) throw EngineError(SR_E_CONFIG, "sweep bench needs a resident page set");
+  if (!values_.p) throw EngineError(SR_E_DATA, "sweep bench: run once first");
+  algo_ = algo;
+  const uint32_t np = uint32_t(pages_.size());
+  std::vector<uint32_t> all(np);
+  for (uint32_t p = 0; p < np; ++p) all[p] = p;
+  ctr_used_ = 0;
+  SR_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(RunCtr), cs_));
+  launch_pages(all, kGateOff, false, ctr_.p, nullptr, false, false);  // warm
+  SR_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(RunCtr), cs_));
+  SR_CUDA(cudaEventRecord(ev_start_, cs_));
+  for (uint32_t r = 0; r < reps; ++r) launch_pages(all, kGateOff, false, ctr_.p, nullptr, false, false);
+  SR_CUDA(cudaEventRecord(ev_stop_, cs_));
+  SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  float t = 0;
+  SR_CUDA(cudaEventElapsedTime(&t, ev_start_, ev_stop_));
+  *ms = reps ? t / reps : 0.0;
+  *edges = reps ? ctr_h_.p[0].edges / reps : 0;
+}
+
+void Engine::attach_world(int rank, int world, const uint8_t id[128]) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (world < 1 || rank < 0 || rank >= world) throw EngineError(SR_E_CONFIG, "bad rank/world");
+  if (pages_loaded_) throw EngineError(SR_E_CONFIG, "attach_world must precede load_pages");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  if (comm_) ncclCommDestroy(comm_);
+  comm_ = nullptr;
+  const ncclResult_t r = ncclCommInitRank(&comm_, world, uid, rank);
+  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl init: ") + ncclGetErrorString(r));
+  rank_ = rank;
+  world_ = world;
+}
+
+}  // namespace seraph

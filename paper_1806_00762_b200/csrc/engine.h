@@ -1,0 +1,238 @@
+// Host engine: owns the device state of one context and runs the
+// density-switched push/pull loop of the reference's Runner
+// (proj/src/engine.cpp:225-416) on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "device_types.h"
+#include "errors.h"
+#include "seraph.h"
+#include "vsched.h"
+
+namespace seraph {
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void reserve(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count) {
+      SR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      n = count;
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+struct PinBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  PinBuf() = default;
+  PinBuf(const PinBuf&) = delete;
+  PinBuf& operator=(const PinBuf&) = delete;
+  ~PinBuf() { release(); }
+  void reserve(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count) {
+      SR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(T), cudaHostAllocDefault));
+      n = count;
+    }
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct PageMeta {
+  uint32_t vb = 0, ve = 0;
+  uint64_t edges = 0;
+  uint64_t bytes = 0;        // page_bytes (graph.cpp:96-100)
+  uint32_t tile_begin = 0, tile_end = 0;
+  bool on_device = false;    // permanently resident (arena)
+  uint64_t off_base = 0, edge_base = 0;  // arena placement
+  // host copy used for streaming (pinned)
+  const uint32_t* h_offs = nullptr;
+  const uint32_t* h_src = nullptr;
+  const uint32_t* h_w = nullptr;
+  int slot = -1;             // streaming slot holding the page
+};
+
+struct StreamSlot {
+  DBuf<uint32_t> offs, src, w;
+  uint64_t cap_offs = 0, cap_edges = 0;
+  int page = -1;
+  long long last_use = -1;   // step index of the last launch that read it
+  cudaEvent_t ready = nullptr;  // copy finished (copy stream)
+  cudaEvent_t freed = nullptr;  // last reader finished (compute stream)
+};
+
+struct PassOut {
+  RunStats totals;
+  uint64_t kernel_runs = 0;
+  uint64_t pages_transferred = 0;
+  uint64_t bytes_transferred = 0;
+};
+
+class Engine {
+ public:
+  Engine(int device, uint64_t budget);
+  ~Engine();
+
+  void load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                const uint32_t* w);
+  void load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* pages,
+                  uint32_t np);
+  uint64_t page_bytes_total() const { return page_bytes_total_; }
+  void run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out, sr_metrics& m,
+           std::vector<sr_pass_stats>& passes);
+  uint64_t verify_fixpoint(int algo, const uint32_t* values_host);
+  void bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges);
+  void attach_world(int rank, int world, const uint8_t id[128]);
+
+  std::string err;
+  std::vector<sr_trace_event> trace;
+  double last_upload_seconds = 0;
+  uint64_t last_upload_bytes = 0;
+
+ private:
+  // ---- configuration of the current run ----
+  struct RunState;
+  void validate(const sr_run_config& cfg) const;
+  void alloc_run_state(const sr_run_config& cfg);
+  void run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_metrics& m,
+                     std::vector<sr_pass_stats>& passes);
+  void run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
+                    std::vector<sr_pass_stats>& passes);
+
+  // dense-pass drivers
+  PassOut dense_pass_wall(const sr_run_config& cfg, int gate, bool recovery, uint32_t pass_index,
+                          bool pagerank);
+  PassOut dense_pass_virtual(const sr_run_config& cfg, int gate, bool recovery,
+                             uint32_t pass_index);
+  RunStats launch_pages(const std::vector<uint32_t>& pages, int gate, bool det, RunCtr* ctr,
+                        const RunCtr* prev, bool per_page, bool pagerank);
+  void push_pass(const sr_run_config& cfg, RunStats& st);
+  void census(int pass_kind);
+  void build_push_list();
+  void read_census();
+  void exchange_round(bool pagerank);
+
+  // streaming
+  bool streaming() const { return !all_resident_; }
+  void ensure_slots(uint32_t window, PassOut& po);
+  uint32_t plan_window_ = 0;
+  size_t plan_cached_ = size_t(-1);
+  void make_resident(uint32_t page, long long step, const std::vector<char>& protect,
+                     PassOut& po);
+  void build_tiles(uint32_t lo, uint32_t hi);
+
+  int dev_ = 0;
+  uint64_t budget_ = 0;
+  int sm_count_ = 148;
+  cudaStream_t cs_ = nullptr;  // compute stream
+  cudaStream_t xs_ = nullptr;  // copy stream
+  cudaEvent_t ev_start_ = nullptr, ev_stop_ = nullptr, ev_step_ = nullptr;
+
+  // CSR (push stage, out-degrees)
+  uint32_t n_ = 0;
+  uint64_t m_ = 0;
+  bool has_csr_ = false, has_csr_edges_ = false, csr_weighted_ = false;
+  DBuf<unsigned long long> out_off_;
+  DBuf<uint32_t> out_nbr_, out_w_;
+
+  // pages
+  bool pages_loaded_ = false;
+  uint32_t page_n_ = 0, cap_ = 0;
+  bool weighted_ = false;
+  std::vector<PageMeta> pages_;
+  std::vector<uint32_t> hub_vertex_h_;
+  uint64_t page_bytes_total_ = 0;
+  uint64_t page_edges_total_ = 0;
+  bool all_resident_ = true;
+  DBuf<uint32_t> arena_offs_, arena_src_, arena_w_;
+  PinBuf<uint32_t> stage_;  // pinned host copy of streamed pages
+  DBuf<uint4> tiles_;
+  DBuf<uint32_t> tile_page_;
+  DBuf<PageDesc> page_desc_;
+  std::vector<PageDesc> page_desc_h_;
+  DBuf<uint32_t> hub_vertex_, hub_stamp_;
+  DBuf<float> hub_sum_;
+  uint32_t n_hubs_ = 0;
+  std::vector<StreamSlot> slots_;
+  long long step_counter_ = 0;
+  bool first_touch_done_ = false;  // resident path: admission counted once per run
+
+  // run state
+  DBuf<uint32_t> values_, next_, snap_, round_snap_;
+  DBuf<int> delta_;
+  DBuf<uint8_t> changed_, status_, logstate_;
+  DBuf<uint32_t> list_, chunk_start_, blk_cnt_;
+  DBuf<unsigned long long> pref_, blk_edges_;
+  DBuf<Census> census_;
+  PinBuf<Census> census_h_;
+  DBuf<RunCtr> ctr_;
+  PinBuf<RunCtr> ctr_h_;
+  uint32_t ctr_used_ = 0;  // entries of ctr_ handed out in the current pass
+  RunCtr* alloc_ctr(size_t entries);
+  DBuf<float> rank_a_, rank_b_, contrib_a_, contrib_b_, inv_outdeg_;
+  uint32_t run_id_ = 0;
+  uint64_t launches_ = 0;
+  uint64_t h2d_bytes_ = 0;
+  int blocks_per_sm_ = 4;
+
+  // algorithm state of the current run
+  int algo_ = 0;
+  uint32_t source_ = 0;
+  int predictor_ = 0;
+  bool det_ = false;
+  unsigned long long k_bfs_ = 0;
+  uint32_t s_cc_ = 0, l_sssp_ = 0;
+  VWindow vwin_;
+  VClock vclock_;
+  VModel vmodel_;
+  bool record_trace_ = false;
+  double pr_damp_ = 0.85;
+
+  // multi-GPU
+  int rank_ = 0, world_ = 1;
+  ncclComm_t comm_ = nullptr;
+  uint32_t own_lo_ = 0, own_hi_ = 0;  // owned destination range
+};
+
+}  // namespace seraph

@@ -1,0 +1,1077 @@
+// sm_100a kernels of the subgraph-iteration engine.
+//
+//   K1  pull_relax      dense pull over CSC pages   (ref engine.cpp:103-177)
+//   K3  push_relax      sparse push over frontier   (ref engine.cpp:63-93)
+//   K4  census/compact  changed flags -> frontier   (ref engine.cpp:312-315, :12-19)
+//   K5  weak DFA step   in the census               (ref engine.cpp:317-328, predictor.cpp:18-41)
+//   K6  cc_refresh      strong CC threshold         (ref predictor.cpp:55-105)
+//   K7  recovery sweep  = K1 with the gate off      (ref engine.cpp:179-205)
+//   K8  pr_pull         PageRank pull-sum           (new; no reference counterpart)
+//
+// The path is sparse and irregular: no tensor cores.  Everything is sized
+// for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
+// based segmented reductions, ballot/prefix-sum compaction, persistent grids.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_types.h"
+#include "kernels.h"
+
+namespace seraph {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T x, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    T y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+  return x;
+}
+
+__device__ __forceinline__ uint32_t warp_min(uint32_t x) { return __reduce_min_sync(kFull, x); }
+
+// VertexProgram::combine (programs.hpp:31-45): saturating at kUnreached.
+template <int A>
+__device__ __forceinline__ uint32_t combine(uint32_t a, uint32_t w) {
+  if (A == kCc) return a;
+  if (a == kUnreached) return kUnreached;
+  if (A == kBfs) return a + 1u;
+  const uint32_t s = a + w;
+  return s < a ? kUnreached : s;
+}
+
+// PredictorGate::should_attempt (engine.hpp:86-98) with strong_converged
+// (predictor.cpp:43-53) and weak_should_attempt (predictor.hpp:32-34).
+template <int A, int G>
+__device__ __forceinline__ bool gate_attempt(uint32_t v, uint32_t cur, const PullArgs& a) {
+  if (G == kGateOff) return true;
+  if (G == kGateWeak) {
+    const uint8_t s = a.status[v];
+    return s == 0 || s == 1 || s == 5;
+  }
+  if (A == kBfs) return !(cur != kUnreached && (unsigned long long)cur <= a.k_bfs);
+  if (A == kCc) return !(cur < a.s_cc);
+  return !(cur < a.l_sssp);
+}
+
+// Map a flat task index of this launch onto a tile index.
+__device__ __forceinline__ uint32_t task_to_tile(const Segments& seg, uint32_t t) {
+  uint32_t s = 0;
+#pragma unroll 1
+  while (s + 1 < seg.n && t >= seg.task_prefix[s + 1]) ++s;
+  return seg.tile_begin[s] + (t - seg.task_prefix[s]);
+}
+
+struct ActEntry {
+  uint32_t local;   // page-local destination
+  uint32_t estart;  // page-local first in-edge
+  uint32_t pref;    // exclusive prefix of active edges inside the tile
+  uint32_t cur;     // destination value when the tile was gated
+};
+
+struct LaneCtr {
+  unsigned long long attempts, valid, skipped, edges;
+  __device__ void clear() { attempts = valid = skipped = edges = 0; }
+};
+
+__device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
+  unsigned long long at = warp_sum(c.attempts), va = warp_sum(c.valid),
+                     sk = warp_sum(c.skipped), ed = warp_sum(c.edges);
+  if (lane == 0 && dst) {
+    if (at) atomicAdd(&dst->attempts, at);
+    if (va) atomicAdd(&dst->valid, va);
+    if (sk) atomicAdd(&dst->skipped, sk);
+    if (ed) atomicAdd(&dst->edges, ed);
+  }
+  c.clear();
+}
+
+// ---------------------------------------------------------------------------
+// K1: dense pull relaxation.  One warp per tile, persistent grid, each warp
+// owns a contiguous slice of the launch's tasks (page changes are rare, so
+// the per-page counters are flushed a handful of times per warp).
+//
+// Range tile, phase A: lanes walk 32 destinations at a time, load the value
+// and offsets, apply the predictor gate and compact the attempted
+// destinations with in-edges into a shared-memory list (ballot + scan).
+// Phase B: the attempted destinations' in-edges are consumed 32 at a time as
+// one virtual, gap-free edge stream; a 5-step shuffle search maps each lane
+// to its destination, the gather values[src] is combined, and a shuffle
+// segmented min-scan reduces per destination.  The destination's last lane
+// stores the result (single writer: plain store, no atomic).
+// Hub tile: one chunk of a high in-degree destination; warp min-reduce and
+// atomicMin, with the run-id stamp counting the update once per run.
+// ---------------------------------------------------------------------------
+template <int A, int G, bool DET>
+__global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
+  __shared__ ActEntry s_act[kWarpsPerBlock][kTileMaxDests];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  ActEntry* act = s_act[warp];
+
+  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
+  const uint32_t nw = gridDim.x * kWarpsPerBlock;
+  const uint32_t total = a.seg.task_prefix[a.seg.n];
+  const uint32_t t_begin = (uint32_t)(((unsigned long long)total * gw) / nw);
+  const uint32_t t_end = (uint32_t)(((unsigned long long)total * (gw + 1)) / nw);
+
+  LaneCtr c;
+  c.clear();
+  uint32_t lane_min = kUnreached;
+  uint32_t cur_page = 0xffffffffu;
+  PageDesc pd{};
+  const uint32_t* __restrict__ values_ro = a.values;
+
+  for (uint32_t t = t_begin; t < t_end; ++t) {
+    const uint32_t ti = task_to_tile(a.seg, t);
+    const uint32_t p = a.tile_page[ti];
+    if (p != cur_page) {
+      if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
+      cur_page = p;
+      pd = a.pages[p];
+    }
+    if (a.prev_ctr && a.prev_ctr[a.ctr_per_page ? p : 0].valid == 0) continue;  // reentry: quiet
+    const uint4 tile = a.tiles[ti];
+    const uint32_t vb = pd.vertex_begin;
+    const uint32_t* __restrict__ offs = pd.offs;
+    const uint32_t* __restrict__ src = pd.src;
+    const uint32_t* __restrict__ wts = pd.w;
+
+    if (tile.w & kHubFlag) {
+      // ---- hub chunk -------------------------------------------------------
+      const uint32_t d = tile.z;
+      const uint32_t v = vb + d;
+      const uint32_t cur = DET ? __ldg(values_ro + v) : *(volatile uint32_t*)(a.values + v);
+      const bool att = gate_attempt<A, G>(v, cur, a);
+      const uint32_t lo_d = offs[d];
+      if (lane == 0 && tile.x == lo_d) {  // owner chunk counts the visit once
+        c.attempts += att;
+        c.skipped += !att;
+        c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
+      }
+      if (!att) continue;
+      uint32_t best = kUnreached;
+      uint32_t e = tile.x + lane;
+#pragma unroll 4
+      for (; e < tile.y; e += 32) {
+        const uint32_t s = src[e];
+        const uint32_t w = (A == kSssp) ? wts[e] : 0u;
+        const uint32_t sv = DET ? __ldg(values_ro + s) : a.values[s];
+        best = min(best, combine<A>(sv, w));
+      }
+      best = warp_min(best);
+      if (lane == 0 && best < cur) {
+        bool improved;
+        if (DET) {
+          atomicMin(a.next + v, best);
+          improved = true;
+        } else {
+          const uint32_t old = atomicMin(a.values + v, best);
+          improved = best < old;
+        }
+        if (improved) {
+          a.changed[v] = 1;
+          lane_min = min(lane_min, best);
+          const uint32_t hub = tile.w & ~kHubFlag;
+          if (atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
+        }
+      }
+      continue;
+    }
+
+    // ---- range tile: phase A (gate + compaction) ----------------------------
+    const uint32_t dl = tile.z, dh = tile.w;
+    uint32_t n_act = 0, tot = 0;
+    for (uint32_t base = dl; base < dh; base += 32) {
+      const uint32_t i = base + lane;
+      const bool in = i < dh;
+      uint32_t cur = 0, lo = 0, deg = 0;
+      bool att = false;
+      if (in) {
+        const uint32_t v = vb + i;
+        cur = DET ? __ldg(values_ro + v) : a.values[v];
+        lo = offs[i];
+        deg = offs[i + 1] - lo;
+        att = gate_attempt<A, G>(v, cur, a);
+      }
+      c.attempts += att;
+      c.skipped += (in && !att);
+      c.edges += att ? deg : 0u;
+      const bool live = att && deg > 0;
+      const uint32_t dd = live ? deg : 0u;
+      const uint32_t incl = warp_incl_scan(dd, lane);
+      const unsigned m = __ballot_sync(kFull, live);
+      if (live) {
+        const uint32_t pos = n_act + __popc(m & lanemask_lt());
+        act[pos] = ActEntry{i, lo, tot + incl - dd, cur};
+      }
+      n_act += __popc(m);
+      tot += __shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    if (n_act == 0) {
+      __syncwarp();
+      continue;
+    }
+
+    // ---- phase B: gap-free edge stream of the attempted destinations --------
+    uint32_t ad = 0;
+    uint32_t carry = kUnreached;
+    for (uint32_t q0 = 0; q0 < tot; q0 += 32) {
+      const uint32_t wi = ad + lane;
+      ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
+      const uint32_t q = q0 + lane;
+      const bool qv = q < tot;
+      uint32_t k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
+        if (b <= q) k += step;
+      }
+      const uint32_t my_local = __shfl_sync(kFull, e.local, k);
+      const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
+      const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
+      const uint32_t my_cur = __shfl_sync(kFull, e.cur, k);
+      const uint32_t nxt_pref = __shfl_sync(kFull, e.pref, (k + 1) & 31);
+      uint32_t cand = kUnreached;
+      if (qv) {
+        const uint32_t eidx = my_estart + (q - my_pref);
+        const uint32_t s = src[eidx];
+        const uint32_t w = (A == kSssp) ? wts[eidx] : 0u;
+        const uint32_t sv = DET ? __ldg(values_ro + s) : a.values[s];
+        cand = combine<A>(sv, w);
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t oc = __shfl_up_sync(kFull, cand, off);
+        const uint32_t ok = __shfl_up_sync(kFull, k, off);
+        if (lane >= off && ok == k) cand = min(cand, oc);
+      }
+      if (k == 0) cand = min(cand, carry);
+      uint32_t end = nxt_pref;
+      if (k == 31) end = (ad + 32 < n_act) ? act[ad + 32].pref : tot;
+      const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
+      const bool tail = qv && (lane == 31 || q + 1 >= tot || k_down != k);
+      const bool complete = end <= q0 + 32;
+      if (tail && complete && cand < my_cur) {
+        const uint32_t v = vb + my_local;
+        if (DET) a.next[v] = cand;
+        else a.values[v] = cand;
+        a.changed[v] = 1;
+        c.valid += 1;
+        lane_min = min(lane_min, cand);
+      }
+      const uint32_t k31 = __shfl_sync(kFull, k, 31);
+      const uint32_t c31 = __shfl_sync(kFull, cand, 31);
+      const uint32_t e31 = __shfl_sync(kFull, end, 31);
+      if (e31 > q0 + 32) {
+        ad += k31;
+        carry = c31;
+      } else {
+        ad += k31 + 1;
+        carry = kUnreached;
+      }
+    }
+    __syncwarp();
+  }
+  if (cur_page != 0xffffffffu) flush_ctr(c, a.ctr + (a.ctr_per_page ? cur_page : 0), lane);
+  lane_min = warp_min(lane_min);
+  if (lane == 0 && lane_min != kUnreached) atomicMin(&a.census->min_changed, lane_min);
+}
+
+__global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __restrict__ next,
+                              uint32_t lo, uint32_t hi) {
+  for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi;
+       v += gridDim.x * blockDim.x)
+    values[v] = next[v];
+}
+
+// ---------------------------------------------------------------------------
+// K8: PageRank pull-sum (Jacobi; contrib_in is read-only in the launch).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
+  __shared__ ActEntry s_act[kWarpsPerBlock][kTileMaxDests];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  ActEntry* act = s_act[warp];
+  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
+  const uint32_t nw = gridDim.x * kWarpsPerBlock;
+  const uint32_t total = a.seg.task_prefix[a.seg.n];
+  const uint32_t t_begin = (uint32_t)(((unsigned long long)total * gw) / nw);
+  const uint32_t t_end = (uint32_t)(((unsigned long long)total * (gw + 1)) / nw);
+  LaneCtr c;
+  c.clear();
+  uint32_t cur_page = 0xffffffffu;
+  PageDesc pd{};
+  const float* __restrict__ contrib = a.contrib_in;
+
+  for (uint32_t t = t_begin; t < t_end; ++t) {
+    const uint32_t ti = task_to_tile(a.seg, t);
+    const uint32_t p = a.tile_page[ti];
+    if (p != cur_page) {
+      cur_page = p;
+      pd = a.pages[p];
+    }
+    const uint4 tile = a.tiles[ti];
+    const uint32_t vb = pd.vertex_begin;
+    const uint32_t* __restrict__ offs = pd.offs;
+    const uint32_t* __restrict__ src = pd.src;
+    if (tile.w & kHubFlag) {
+      const uint32_t d = tile.z;
+      const uint32_t lo_d = offs[d];
+      if (lane == 0 && tile.x == lo_d) {
+        c.attempts += 1;
+        c.edges += offs[d + 1] - lo_d;
+      }
+      float sum = 0.f;
+      uint32_t e = tile.x + lane;
+#pragma unroll 4
+      for (; e < tile.y; e += 32) sum += __ldg(contrib + src[e]);
+      sum = warp_sum(sum);
+      if (lane == 0) atomicAdd(a.hub_sum + (tile.w & ~kHubFlag), sum);
+      continue;
+    }
+    const uint32_t dl = tile.z, dh = tile.w;
+    uint32_t n_act = 0, tot = 0;
+    for (uint32_t base = dl; base < dh; base += 32) {
+      const uint32_t i = base + lane;
+      const bool in = i < dh;
+      uint32_t lo = 0, deg = 0;
+      if (in) {
+        lo = offs[i];
+        deg = offs[i + 1] - lo;
+        if (deg == 0) {  // no in-edges: teleport share only
+          const uint32_t v = vb + i;
+          a.rank_out[v] = a.base;
+          a.contrib_out[v] = a.base * a.inv_outdeg[v];
+        }
+      }
+      c.attempts += in;
+      c.edges += deg;
+      const bool live = deg > 0;
+      const uint32_t incl = warp_incl_scan(deg, lane);
+      const unsigned m = __ballot_sync(kFull, live);
+      if (live) {
+        const uint32_t pos = n_act + __popc(m & lanemask_lt());
+        act[pos] = ActEntry{i, lo, tot + incl - deg, 0u};
+      }
+      n_act += __popc(m);
+      tot += __shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    if (n_act == 0) {
+      __syncwarp();
+      continue;
+    }
+    uint32_t ad = 0;
+    float carry = 0.f;
+    for (uint32_t q0 = 0; q0 < tot; q0 += 32) {
+      const uint32_t wi = ad + lane;
+      ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
+      const uint32_t q = q0 + lane;
+      const bool qv = q < tot;
+      uint32_t k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
+        if (b <= q) k += step;
+      }
+      const uint32_t my_local = __shfl_sync(kFull, e.local, k);
+      const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
+      const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
+      const uint32_t nxt_pref = __shfl_sync(kFull, e.pref, (k + 1) & 31);
+      float x = 0.f;
+      if (qv) x = __ldg(contrib + src[my_estart + (q - my_pref)]);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float ox = __shfl_up_sync(kFull, x, off);
+        const uint32_t ok = __shfl_up_sync(kFull, k, off);
+        if (lane >= off && ok == k) x += ox;
+      }
+      if (k == 0) x += carry;
+      uint32_t end = nxt_pref;
+      if (k == 31) end = (ad + 32 < n_act) ? act[ad + 32].pref : tot;
+      const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
+      const bool tail = qv && (lane == 31 || q + 1 >= tot || k_down != k);
+      const bool complete = end <= q0 + 32;
+      if (tail && complete) {
+        const uint32_t v = vb + my_local;
+        const float r = a.base + a.damp * x;
+        a.rank_out[v] = r;
+        a.contrib_out[v] = r * a.inv_outdeg[v];
+      }
+      const uint32_t k31 = __shfl_sync(kFull, k, 31);
+      const float x31 = __shfl_sync(kFull, x, 31);
+      const uint32_t e31 = __shfl_sync(kFull, end, 31);
+      if (e31 > q0 + 32) {
+        ad += k31;
+        carry = x31;
+      } else {
+        ad += k31 + 1;
+        carry = 0.f;
+      }
+    }
+    __syncwarp();
+  }
+  flush_ctr(c, a.ctr, lane);
+}
+
+__global__ void pr_hub_finalize_kernel(const uint32_t* hub_vertex, uint32_t n_hubs,
+                                       float* hub_sum, float* rank_out, float* contrib_out,
+                                       const float* inv_outdeg, float base, float damp) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n_hubs) return;
+  const uint32_t v = hub_vertex[h];
+  const float r = base + damp * hub_sum[h];
+  rank_out[v] = r;
+  contrib_out[v] = r * inv_outdeg[v];
+  hub_sum[h] = 0.f;
+}
+
+__global__ void pr_init_kernel(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
+                               float init) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    rank[v] = init;
+    contrib[v] = init * inv_outdeg[v];
+  }
+}
+
+__global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, float* inv) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const unsigned long long d = off[v + 1] - off[v];
+    inv[v] = d ? 1.0f / (float)d : 0.0f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: sparse push.  The frontier list (ids with out-degree > 0, ascending)
+// and its exclusive out-degree prefix form one flat edge space; each warp
+// task is kPushChunk consecutive edges whose first list entry was recorded
+// by the compaction (chunk_start), so no search over the prefix is needed.
+// ---------------------------------------------------------------------------
+template <int A, bool DET>
+__global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const uint32_t nw = gridDim.x * kWarpsPerBlock;
+  const unsigned long long nchunks = (a.total_edges + kPushChunk - 1) / kPushChunk;
+  LaneCtr c;
+  c.clear();
+  uint32_t lane_min = kUnreached;
+  for (unsigned long long ch = gw; ch < nchunks; ch += nw) {
+    const unsigned long long q_lo = ch * kPushChunk;
+    const unsigned long long q_hi = min(q_lo + kPushChunk, a.total_edges);
+    uint32_t ad = a.chunk_start[ch];
+    for (unsigned long long q0 = q_lo; q0 < q_hi; q0 += 32) {
+      // window of up to 32 consecutive frontier entries starting at ad
+      const uint32_t wi = ad + lane;
+      long long rel = 1ll << 40;  // entry start relative to q0
+      uint32_t u = 0, uval = kUnreached;
+      unsigned long long ebase = 0;
+      if (wi < a.n_list) {
+        rel = (long long)(a.pref[wi]) - (long long)q0;
+        u = a.list[wi];
+        ebase = a.out_offsets[u];
+        uval = DET ? __ldg(a.values + u) : a.values[u];
+      }
+      const int relc = rel > 64 ? 64 : (int)rel;  // entries before q0 are negative
+      const unsigned long long q = q0 + lane;
+      const bool qv = q < q_hi;
+      uint32_t k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int b = __shfl_sync(kFull, relc, k + step);
+        if (b <= lane) k += step;
+      }
+      const int my_rel = __shfl_sync(kFull, relc, k);
+      const unsigned long long my_base_lo = __shfl_sync(kFull, (unsigned)ebase, k);
+      const unsigned long long my_base_hi = __shfl_sync(kFull, (unsigned)(ebase >> 32), k);
+      const uint32_t my_val = __shfl_sync(kFull, uval, k);
+      if (qv) {
+        const unsigned long long eidx =
+            ((my_base_hi << 32) | my_base_lo) + (unsigned long long)((long long)lane - my_rel);
+        const uint32_t v = a.out_neighbors[eidx];
+        const uint32_t w = (A == kSssp) ? a.out_weights[eidx] : 0u;
+        const uint32_t cand = combine<A>(my_val, w);
+        c.attempts += 1;
+        c.edges += 1;
+        if (DET) {
+          if (cand < __ldg(a.values + v)) {
+            atomicMin(a.next + v, cand);
+            a.changed[v] = 1;
+          }
+        } else if (cand < *(volatile uint32_t*)(a.values + v)) {
+          const uint32_t old = atomicMin(a.values + v, cand);
+          if (cand < old) {
+            c.valid += 1;
+            a.changed[v] = 1;
+            lane_min = min(lane_min, cand);
+          }
+        }
+      }
+      // advance the window start to the entry that contains q0 + 32
+      int end_rel = __shfl_sync(kFull, relc, (k + 1) & 31);
+      if (k == 31) {
+        end_rel = 64;
+        if (ad + 32 < a.n_list) {
+          const long long r = (long long)a.pref[ad + 32] - (long long)q0;
+          end_rel = r > 64 ? 64 : (int)r;
+        }
+      }
+      const uint32_t k_last = __shfl_sync(kFull, k, 31);
+      const int e_last = __shfl_sync(kFull, end_rel, 31);
+      ad += k_last + (e_last <= 32 ? 1u : 0u);
+    }
+  }
+  flush_ctr(c, a.ctr, lane);
+  lane_min = warp_min(lane_min);
+  if (lane == 0 && lane_min != kUnreached) atomicMin(&a.census->min_changed, lane_min);
+}
+
+__global__ void push_commit_kernel(uint32_t* __restrict__ values, const uint32_t* __restrict__ next,
+                                   const uint8_t* __restrict__ changed, uint32_t n, RunCtr* ctr,
+                                   Census* c) {
+  unsigned long long cnt = 0;
+  uint32_t mn = kUnreached;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (changed[v]) {
+      const uint32_t nv = next[v];
+      if (nv < values[v]) {
+        values[v] = nv;
+        ++cnt;
+        mn = min(mn, nv);
+      }
+    }
+  }
+  cnt = warp_sum(cnt);
+  mn = warp_min(mn);
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt) atomicAdd(&ctr->valid, cnt);
+    if (mn != kUnreached) atomicMin(&c->min_changed, mn);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5 census: one pass over the per-vertex byte arrays.  Weak DFA step
+// (predictor.cpp:18-41) for dense passes, status reset for recovery
+// (engine.cpp:197-202), PredictionLog bookkeeping (predictor.cpp:107-138)
+// folded into one byte per vertex, status histogram of the NEXT pass,
+// frontier size and out-edge volume (density_switch input, engine.cpp:56-61).
+// logstate byte: bits0-1 consecutive fails (saturated at 3), bit2 armed,
+// bit3 one pending (not yet falsified) converged-prediction event.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint8_t log_change(uint8_t ls, unsigned long long& incorrect) {
+  if (ls & 8) ++incorrect;
+  return 4;  // fails=0, armed, no pending
+}
+__device__ __forceinline__ uint8_t log_attempt(uint8_t ls, bool changed,
+                                               unsigned long long& events,
+                                               unsigned long long& incorrect) {
+  if (changed) return log_change(ls, incorrect);
+  uint8_t fails = ls & 3;
+  if (fails < 3) ++fails;
+  uint8_t out = (ls & ~3) | fails;
+  if ((ls & 4) && fails == 2) {
+    ++events;
+    out = (out & ~4) | 8;
+  }
+  return out;
+}
+
+__global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
+                                                     uint8_t* status, uint8_t* logstate,
+                                                     const unsigned long long* __restrict__ out_off,
+                                                     int pass_kind, uint32_t own_lo, uint32_t own_hi,
+                                                     uint32_t* blk_cnt,
+                                                     unsigned long long* blk_edges, Census* cz) {
+  __shared__ unsigned long long s_hist[6];
+  __shared__ unsigned long long s_red[3][8];
+  if (threadIdx.x < 6) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t v0 = blockIdx.x * kCensusBlockVerts + threadIdx.x * 16;
+  unsigned long long n_changed = 0, n_push = 0, edges = 0, events = 0, incorrect = 0;
+  unsigned long long own_push = 0, own_edges = 0;
+  unsigned hist[6] = {0, 0, 0, 0, 0, 0};
+  if (v0 < n) {
+    uint4 cw = *reinterpret_cast<const uint4*>(changed + v0);
+    const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
+    uint4 sw{}, lw{};
+    if (status) sw = *reinterpret_cast<const uint4*>(status + v0);
+    if (logstate) lw = *reinterpret_cast<const uint4*>(logstate + v0);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(&sw);
+    uint8_t* lb = reinterpret_cast<uint8_t*>(&lw);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t v = v0 + j;
+      if (v >= n) break;
+      const bool ch = cb[j] != 0;
+      if (ch) {
+        ++n_changed;
+        const unsigned long long d = out_off ? out_off[v + 1] - out_off[v] : 0ull;
+        edges += d;
+        n_push += d > 0;
+        if (v >= own_lo && v < own_hi) {
+          own_edges += d;
+          own_push += d > 0;
+        }
+      }
+      if (status) {
+        uint8_t s = sb[j];
+        if (pass_kind == kPassDense) {
+          const bool attempt_state = (s == 0 || s == 1 || s == 5);
+          if (attempt_state) {
+            if (logstate) lb[j] = log_attempt(lb[j], ch, events, incorrect);
+            s = ch ? 0 : (s == 0 ? 5 : (s == 5 ? 3 : 4));
+          } else {
+            s = (s == 3) ? 2 : (s == 2 ? 1 : 3);
+          }
+        } else if (ch && pass_kind != kPassInit) {
+          if (pass_kind == kPassRecovery) s = 0;
+          if (logstate) lb[j] = log_change(lb[j], incorrect);
+        }
+        sb[j] = s;
+        hist[s < 6 ? s : 0]++;
+      }
+    }
+    if (status) *reinterpret_cast<uint4*>(status + v0) = sw;
+    if (logstate) *reinterpret_cast<uint4*>(logstate + v0) = lw;
+  }
+  if (status) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      unsigned x = warp_sum(hist[s]);
+      if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_hist[s], (unsigned long long)x);
+    }
+  }
+  n_changed = warp_sum(n_changed);
+  n_push = warp_sum(n_push);
+  edges = warp_sum(edges);
+  events = warp_sum(events);
+  incorrect = warp_sum(incorrect);
+  own_push = warp_sum(own_push);
+  own_edges = warp_sum(own_edges);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][w] = n_changed;
+    s_red[1][w] = own_push;
+    s_red[2][w] = own_edges;
+    if (n_push) atomicAdd(&cz->push_count, n_push);
+    if (edges) atomicAdd(&cz->out_edges, edges);
+    if (events) atomicAdd(&cz->log_events, events);
+    if (incorrect) atomicAdd(&cz->log_incorrect, incorrect);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a0 = 0, a1 = 0, a2 = 0;
+    for (int i = 0; i < 8; ++i) {
+      a0 += s_red[0][i];
+      a1 += s_red[1][i];
+      a2 += s_red[2][i];
+    }
+    blk_cnt[blockIdx.x] = (uint32_t)a1;
+    blk_edges[blockIdx.x] = a2;
+    if (a0) atomicAdd(&cz->changed, a0);
+    if (a1) atomicAdd(&cz->own_push, a1);
+    if (a2) atomicAdd(&cz->own_edges, a2);
+  }
+  if (status && threadIdx.x < 6 && s_hist[threadIdx.x])
+    atomicAdd(&cz->status_hist[threadIdx.x], s_hist[threadIdx.x]);
+}
+
+// Exclusive scan of the per-block (count, edges) pairs; one block.
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t* cnt,
+                                                           unsigned long long* edges) {
+  __shared__ uint32_t s_c[32];
+  __shared__ unsigned long long s_e[32];
+  __shared__ uint32_t carry_c;
+  __shared__ unsigned long long carry_e;
+  if (threadIdx.x == 0) {
+    carry_c = 0;
+    carry_e = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < nb; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t xc = i < nb ? cnt[i] : 0u;
+    const unsigned long long xe = i < nb ? edges[i] : 0ull;
+    uint32_t ic = warp_incl_scan(xc, lane);
+    unsigned long long ie = warp_incl_scan(xe, lane);
+    if (lane == 31) {
+      s_c[w] = ic;
+      s_e[w] = ie;
+    }
+    __syncthreads();
+    if (w == 0) {
+      uint32_t tc = s_c[lane];
+      unsigned long long te = s_e[lane];
+      uint32_t sc = warp_incl_scan(tc, lane);
+      unsigned long long se = warp_incl_scan(te, lane);
+      s_c[lane] = sc - tc;
+      s_e[lane] = se - te;
+    }
+    __syncthreads();
+    const uint32_t oc = carry_c + s_c[w] + ic - xc;
+    const unsigned long long oe = carry_e + s_e[w] + ie - xe;
+    __syncthreads();
+    if (i < nb) {
+      cnt[i] = oc;
+      edges[i] = oe;
+    }
+    if (threadIdx.x == 1023) {
+      carry_c = oc + xc;
+      carry_e = oe + xe;
+    }
+    __syncthreads();
+  }
+}
+
+// Ordered compaction of changed vertices with out-degree > 0 into the push
+// list, with their exclusive out-degree prefix and push-chunk starts; clears
+// the changed flags for the next pass.
+__global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_lo, uint32_t own_hi,
+                                                      uint8_t* changed,
+                                                      const unsigned long long* __restrict__ out_off,
+                                                      const uint32_t* __restrict__ blk_off,
+                                                      const unsigned long long* __restrict__ blk_eoff,
+                                                      uint32_t* list, unsigned long long* pref,
+                                                      uint32_t* chunk_start) {
+  __shared__ uint32_t s_c[8];
+  __shared__ unsigned long long s_e[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t v0 = blockIdx.x * kCensusBlockVerts + threadIdx.x * 16;
+  uint4 cw = make_uint4(0, 0, 0, 0);
+  if (v0 < n) cw = *reinterpret_cast<const uint4*>(changed + v0);
+  const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
+  uint32_t cnt = 0;
+  unsigned long long edges = 0;
+  unsigned long long deg[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    deg[j] = 0;
+    const uint32_t v = v0 + j;
+    if (v < n && cb[j] && v >= own_lo && v < own_hi) {
+      deg[j] = out_off[v + 1] - out_off[v];
+      cnt += deg[j] > 0;
+      edges += deg[j];
+    }
+  }
+  const uint32_t ic = warp_incl_scan(cnt, lane);
+  const unsigned long long ie = warp_incl_scan(edges, lane);
+  if (lane == 31) {
+    s_c[w] = ic;
+    s_e[w] = ie;
+  }
+  __syncthreads();
+  uint32_t wc = 0;
+  unsigned long long we = 0;
+  for (int i = 0; i < w; ++i) {
+    wc += s_c[i];
+    we += s_e[i];
+  }
+  uint32_t pos = blk_off[blockIdx.x] + wc + ic - cnt;
+  unsigned long long ep = blk_eoff[blockIdx.x] + we + ie - edges;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (deg[j] > 0) {
+      list[pos] = v0 + j;
+      pref[pos] = ep;
+      const unsigned long long c_lo = (ep + kPushChunk - 1) / kPushChunk;
+      const unsigned long long c_hi = (ep + deg[j] + kPushChunk - 1) / kPushChunk;
+      for (unsigned long long ch = c_lo; ch < c_hi; ++ch) chunk_start[ch] = pos;
+      ++pos;
+      ep += deg[j];
+    }
+  }
+  if (v0 < n) *reinterpret_cast<uint4*>(changed + v0) = make_uint4(0, 0, 0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// K6: strong CC threshold.  The reference keeps exact per-label counts and
+// diffs them against the previous refresh (predictor.cpp:55-87).  The net
+// change of label L since the refresh is  #{v: cur_v = L} - #{v: snap_v = L},
+// so it is computed from (snapshot, current) pairs of moved vertices, with
+// match_any aggregation of the hot label, and the minimum label with a
+// nonzero net change is s.
+// ---------------------------------------------------------------------------
+__global__ void cc_delta_kernel(uint32_t n, const uint32_t* __restrict__ values,
+                                const uint32_t* __restrict__ snap, int* delta) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t v = base + threadIdx.x;
+    uint32_t cur = 0, old = 0;
+    bool moved = false;
+    if (v < n) {
+      cur = values[v];
+      old = snap[v];
+      moved = cur != old;
+    }
+    const unsigned am = __ballot_sync(kFull, moved);
+    if (moved) {
+      const unsigned m_in = __match_any_sync(am, cur);
+      if (lane == __ffs(m_in) - 1) atomicAdd(delta + cur, __popc(m_in));
+      const unsigned m_out = __match_any_sync(am, old);
+      if (lane == __ffs(m_out) - 1) atomicSub(delta + old, __popc(m_out));
+    }
+  }
+}
+
+__global__ void cc_min_kernel(uint32_t n, const uint32_t* __restrict__ values,
+                              const uint32_t* __restrict__ snap, const int* __restrict__ delta,
+                              Census* cz) {
+  uint32_t best = kUnreached;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t cur = values[v], old = snap[v];
+    if (cur != old) {
+      if (delta[cur] != 0) best = min(best, cur);
+      if (delta[old] != 0) best = min(best, old);
+    }
+  }
+  best = warp_min(best);
+  if ((threadIdx.x & 31) == 0 && best != kUnreached) atomicMin(&cz->cc_min_label, best);
+}
+
+__global__ void cc_reset_kernel(uint32_t n, const uint32_t* __restrict__ values, uint32_t* snap,
+                                int* delta) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t cur = values[v], old = snap[v];
+    if (cur != old) {
+      delta[cur] = 0;
+      delta[old] = 0;
+      snap[v] = cur;
+    }
+  }
+}
+
+__global__ void init_values_kernel(int algo, uint32_t source, uint32_t n, uint32_t* values) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    values[v] = (algo == kCc) ? v : (v == source ? 0u : kUnreached);
+}
+
+__global__ void fill_u32_kernel(uint32_t* p, uint32_t n, uint32_t x) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = x;
+}
+
+template <int A>
+__global__ void verify_kernel(uint32_t n, const unsigned long long* __restrict__ off,
+                              const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ w,
+                              const uint32_t* __restrict__ values, unsigned long long* viol) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long bad = 0;
+  for (uint32_t u = gw; u < n; u += nw) {
+    const uint32_t vu = values[u];
+    for (unsigned long long e = off[u] + lane; e < off[u + 1]; e += 32) {
+      const uint32_t cand = combine<A>(vu, A == kSssp ? w[e] : 0u);
+      if (cand < values[nbr[e]]) ++bad;
+    }
+  }
+  bad = warp_sum(bad);
+  if (lane == 0 && bad) atomicAdd(viol, bad);
+}
+
+inline int grid_for(unsigned long long work, int block, int cap = 148 * 16) {
+  unsigned long long g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (unsigned long long)cap) g = cap;
+  return (int)g;
+}
+
+__global__ void mark_changed_kernel(uint32_t n, const uint32_t* __restrict__ values,
+                                    const uint32_t* __restrict__ snap, uint8_t* changed) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (values[v] < snap[v]) changed[v] = 1;
+}
+
+__global__ void set_page_desc_kernel(PageDesc* d, uint32_t page, const uint32_t* offs,
+                                     const uint32_t* src, const uint32_t* w) {
+  d[page].offs = offs;
+  d[page].src = src;
+  d[page].w = w;
+}
+
+}  // namespace
+
+void launch_mark_changed(uint32_t n, const uint32_t* values, const uint32_t* snap,
+                         uint8_t* changed, cudaStream_t s) {
+  if (!n) return;
+  mark_changed_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, values, snap, changed);
+}
+
+void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, const uint32_t* src,
+                          const uint32_t* w, cudaStream_t s) {
+  set_page_desc_kernel<<<1, 1, 0, s>>>(d, page, offs, src, w);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int A, int G, bool D>
+static void pull_dispatch3(const PullArgs& a, int grid, cudaStream_t s) {
+  pull_relax_kernel<A, G, D><<<grid, kBlockThreads, 0, s>>>(a);
+}
+template <int A, int G>
+static void pull_dispatch2(bool det, const PullArgs& a, int grid, cudaStream_t s) {
+  if (det) pull_dispatch3<A, G, true>(a, grid, s);
+  else pull_dispatch3<A, G, false>(a, grid, s);
+}
+template <int A>
+static void pull_dispatch1(int gate, bool det, const PullArgs& a, int grid, cudaStream_t s) {
+  switch (gate) {
+    case kGateStrong: pull_dispatch2<A, kGateStrong>(det, a, grid, s); break;
+    case kGateWeak: pull_dispatch2<A, kGateWeak>(det, a, grid, s); break;
+    default: pull_dispatch2<A, kGateOff>(det, a, grid, s); break;
+  }
+}
+
+void launch_pull(int algo, int gate, bool det, const PullArgs& a, int grid, cudaStream_t s) {
+  switch (algo) {
+    case kBfs: pull_dispatch1<kBfs>(gate, det, a, grid, s); break;
+    case kCc: pull_dispatch1<kCc>(gate, det, a, grid, s); break;
+    default: pull_dispatch1<kSssp>(gate, det, a, grid, s); break;
+  }
+}
+
+int pull_blocks_per_sm(int algo, int gate, bool det) {
+  int nb = 0;
+  (void)gate;
+  (void)det;
+  if (algo == kSssp)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kSssp, kGateOff, false>,
+                                                  kBlockThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kBfs, kGateOff, false>,
+                                                  kBlockThreads, 0);
+  return nb > 0 ? nb : 1;
+}
+
+void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t hi,
+                   cudaStream_t s) {
+  if (hi <= lo) return;
+  commit_kernel<<<grid_for(hi - lo, 256), 256, 0, s>>>(values, next, lo, hi);
+}
+
+void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s) {
+  pr_pull_kernel<<<grid, kBlockThreads, 0, s>>>(a);
+}
+
+void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
+                            float* rank_out, float* contrib_out, const float* inv_outdeg,
+                            float base, float damp, cudaStream_t s) {
+  if (!n_hubs) return;
+  pr_hub_finalize_kernel<<<(n_hubs + 255) / 256, 256, 0, s>>>(hub_vertex, n_hubs, hub_sum,
+                                                              rank_out, contrib_out, inv_outdeg,
+                                                              base, damp);
+}
+
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n, float init,
+                    cudaStream_t s) {
+  pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, n, init);
+}
+
+void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
+                       cudaStream_t s) {
+  inv_outdeg_kernel<<<grid_for(n, 256), 256, 0, s>>>(out_offsets, n, inv);
+}
+
+void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s) {
+  switch (algo) {
+    case kBfs:
+      if (det) push_relax_kernel<kBfs, true><<<grid, kBlockThreads, 0, s>>>(a);
+      else push_relax_kernel<kBfs, false><<<grid, kBlockThreads, 0, s>>>(a);
+      break;
+    case kCc:
+      if (det) push_relax_kernel<kCc, true><<<grid, kBlockThreads, 0, s>>>(a);
+      else push_relax_kernel<kCc, false><<<grid, kBlockThreads, 0, s>>>(a);
+      break;
+    default:
+      if (det) push_relax_kernel<kSssp, true><<<grid, kBlockThreads, 0, s>>>(a);
+      else push_relax_kernel<kSssp, false><<<grid, kBlockThreads, 0, s>>>(a);
+      break;
+  }
+}
+
+void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
+                        uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s) {
+  push_commit_kernel<<<grid_for(n, 256), 256, 0, s>>>(values, next, changed, n, ctr, c);
+}
+
+void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
+                   const unsigned long long* out_offsets, int pass_kind, uint32_t own_lo,
+                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
+                   cudaStream_t s) {
+  const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  if (!nb) return;
+  census_kernel<<<nb, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind, own_lo,
+                                   own_hi, blk_cnt, blk_edges, c);
+}
+
+void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
+                        cudaStream_t s) {
+  if (!nblocks) return;
+  scan_blocks_kernel<<<1, 1024, 0, s>>>(nblocks, blk_cnt, blk_edges);
+}
+
+void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
+                    const unsigned long long* out_offsets, const uint32_t* blk_off,
+                    const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
+                    uint32_t* chunk_start, cudaStream_t s) {
+  const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  if (!nb) return;
+  compact_kernel<<<nb, 256, 0, s>>>(n, own_lo, own_hi, changed, out_offsets, blk_off, blk_eoff,
+                                    list, pref, chunk_start);
+}
+
+void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* delta, Census* c,
+                       cudaStream_t s) {
+  if (!n) return;
+  const int g = grid_for(n, 256);
+  cc_delta_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
+  cc_min_kernel<<<g, 256, 0, s>>>(n, values, snap, delta, c);
+  cc_reset_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
+}
+
+void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values, cudaStream_t s) {
+  if (!n) return;
+  init_values_kernel<<<grid_for(n, 256), 256, 0, s>>>(algo, source, n, values);
+}
+
+void launch_init_hub_stamp(uint32_t* stamp, uint32_t n, cudaStream_t s) {
+  if (!n) return;
+  fill_u32_kernel<<<grid_for(n, 256), 256, 0, s>>>(stamp, n, 0u);
+}
+
+void launch_verify(int algo, uint32_t n, const unsigned long long* out_offsets,
+                   const uint32_t* nbr, const uint32_t* w, const uint32_t* values,
+                   unsigned long long* violations, cudaStream_t s) {
+  if (!n) return;
+  const int g = grid_for((unsigned long long)n * 32, 256);
+  switch (algo) {
+    case kBfs: verify_kernel<kBfs><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
+    case kCc: verify_kernel<kCc><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
+    default: verify_kernel<kSssp><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
+  }
+}
+
+}  // namespace seraph

@@ -1,0 +1,63 @@
+// Host-callable launchers for the sm_100a kernels in kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_types.h"
+
+namespace seraph {
+
+// K1 / K7: dense pull relaxation over a set of tile segments.
+void launch_pull(int algo, int gate, bool det, const PullArgs& a, int grid, cudaStream_t s);
+// Deterministic mode commit: values[v] = next[v] for v in [lo, hi).
+void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t hi,
+                   cudaStream_t s);
+// K8: PageRank pull-sum + hub finalize.
+void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
+void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
+                            float* rank_out, float* contrib_out, const float* inv_outdeg,
+                            float base, float damp, cudaStream_t s);
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
+                    float init, cudaStream_t s);
+void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
+                       cudaStream_t s);
+// K3: sparse push over the compacted frontier.
+void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s);
+// Deterministic push commit: for changed v with next[v] < values[v].
+void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
+                        uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s);
+// K4/K5: per-pass census (+ weak DFA step, prediction log, status histogram).
+constexpr uint32_t kCensusBlockVerts = 4096;
+void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
+                   const unsigned long long* out_offsets, int pass_kind, uint32_t own_lo,
+                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
+                   cudaStream_t s);
+void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
+                        cudaStream_t s);
+void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
+                    const unsigned long long* out_offsets, const uint32_t* blk_off,
+                    const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
+                    uint32_t* chunk_start, cudaStream_t s);
+// Multi-GPU: flag vertices improved by any rank during the round.
+void launch_mark_changed(uint32_t n, const uint32_t* values, const uint32_t* snap,
+                         uint8_t* changed, cudaStream_t s);
+// Streaming: point a page descriptor at the slot now holding the page.
+void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, const uint32_t* src,
+                          const uint32_t* w, cudaStream_t s);
+// K6: strong CC threshold (net label-population change since the last refresh).
+void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* delta,
+                       Census* c, cudaStream_t s);
+// Values initialisation (VertexProgram::init, programs.hpp:20-28).
+void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
+                        cudaStream_t s);
+void launch_init_hub_stamp(uint32_t* stamp, uint32_t n, cudaStream_t s);
+// Fixpoint-law verifier.
+void launch_verify(int algo, uint32_t n, const unsigned long long* out_offsets,
+                   const uint32_t* nbr, const uint32_t* w, const uint32_t* values,
+                   unsigned long long* violations, cudaStream_t s);
+
+int pull_blocks_per_sm(int algo, int gate, bool det);
+
+}  // namespace seraph

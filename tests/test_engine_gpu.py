@@ -1,0 +1,352 @@
+"""GPU parity tests of the hot path, through the C-ABI (libseraph.so).
+
+Mirrors the reference's engine tests (proj/tests/test_engine.cpp,
+test_bench.cpp) and the reconstructed oracle-equivalence matrix (SURVEY §4,
+SPEC acceptance criterion 1).  The oracle is oracle/liboracle.so, itself pinned
+to the reference (tests/test_oracle.py).  Bar: bit-exact u32 values for
+BFS/CC/SSSP; PageRank within 1e-6 absolute per vertex (north_star).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1806_00762_b200 import pagestream as ps
+
+pytestmark = pytest.mark.gpu
+
+MODES = list(ps.ScheduleModeKind)
+PREDS = list(ps.PredictorMode)
+PR_TOL = 1e-6
+
+
+def graph(n, edges, weights=None):
+    return ps.EdgeList.from_pairs(n, edges, weights)
+
+
+def built(el, cap):
+    return ps.build_csr(el), ps.build_csc_pages(el, cap)
+
+
+def program_for(kind, source, el):
+    if kind == ps.AlgoKind.BFS:
+        return ps.make_bfs(source, el.num_vertices)
+    if kind == ps.AlgoKind.CC:
+        return ps.make_cc()
+    return ps.make_sssp(source, el.num_vertices, el.weighted())
+
+
+def oracle_values(el, kind, source):
+    return O.solve(el.num_vertices, el.src, el.dst, el.weights if el.weighted() else None,
+                   int(kind), source)
+
+
+def random_edge_list(rng, max_v, max_e, weighted=True):
+    # tests/support.hpp:121-132 (numpy stream, same shape of inputs)
+    n = int(rng.integers(1, max_v + 1))
+    m = int(rng.integers(0, max_e + 1))
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    w = rng.integers(1, 17, m).astype(np.uint32) if weighted else np.zeros(0, np.uint32)
+    return ps.EdgeList(n, src, dst, w)
+
+
+def cfg_of(mode=ps.ScheduleModeKind.BASELINE, pred=ps.PredictorMode.OFF,
+           clock=ps.ClockMode.VIRTUAL, window=8, execution=ps.ExecutionPolicy.DENSITY_SWITCHED,
+           **kw):
+    c = ps.EngineConfig(predictor=pred, window_capacity=window, clock=clock, execution=execution,
+                        **kw)
+    c.schedule.kind = mode
+    return c
+
+
+# --------------------------------------------------------------------------
+# reference unit goldens (test_engine.cpp)
+# --------------------------------------------------------------------------
+def test_run_bfs_two_vertex(engine):  # test_engine.cpp:135-141
+    el = graph(2, [(0, 1)])
+    csr, pages = built(el, 1)
+    r = engine.run_graph(csr, pages, ps.make_bfs(0, 2), ps.EngineConfig())
+    assert r.values.tolist() == [0, 1]
+    assert r.metrics.passes <= 2
+
+
+def test_run_cc_edgeless_one_quiet_pass(engine):  # test_engine.cpp:143-150
+    el = graph(3, [])
+    csr, pages = built(el, 2)
+    r = engine.run_graph(csr, pages, ps.make_cc(), ps.EngineConfig())
+    assert r.values.tolist() == [0, 1, 2]
+    assert r.metrics.passes == 1
+    assert r.metrics.valid_updates == 0
+
+
+def test_dense_pull_counts_on_path(engine):  # test_engine.cpp:107-118 (Jacobi run: 1 update)
+    el = graph(3, [(0, 1), (1, 2)])
+    csr, pages = built(el, 4)
+    c = cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE)
+    r = engine.run_graph(csr, pages, ps.make_bfs(0, 3), c)
+    p0 = r.metrics.per_pass[0]
+    assert p0.kind == ps.PassKind.DENSE_PULL
+    assert (p0.attempts, p0.skipped, p0.edges_read, p0.valid_updates) == (3, 0, 2, 1)
+    assert r.values.tolist() == [0, 1, 2]
+
+
+def test_weak_dormancy_corrected_by_recovery(engine):  # test_engine.cpp:232-254
+    el = graph(4, [(0, 3), (3, 2), (2, 1)])
+    csr, pages = built(el, 1)
+    for clock in ps.ClockMode:
+        c = cfg_of(pred=ps.PredictorMode.WEAK, execution=ps.ExecutionPolicy.FORCE_DENSE,
+                   window=4, clock=clock)
+        r = engine.run_graph(csr, pages, ps.make_bfs(0, 4), c)
+        assert r.values.tolist() == [0, 3, 2, 1]
+        assert r.metrics.recovery_passes >= 1
+        if clock == ps.ClockMode.VIRTUAL:
+            assert any(p.kind == ps.PassKind.RECOVERY and p.changed_vertices > 0
+                       for p in r.metrics.per_pass)
+
+
+def test_metrics_partition_attempts_and_skips(engine):  # test_engine.cpp:281-293
+    el = graph(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5)])
+    csr, pages = built(el, 2)
+    c = cfg_of(pred=ps.PredictorMode.WEAK, execution=ps.ExecutionPolicy.FORCE_DENSE)
+    r = engine.run_graph(csr, pages, ps.make_bfs(0, 6), c)
+    for st in r.metrics.per_pass:
+        if st.kind != ps.PassKind.DENSE_PULL:
+            continue
+        assert st.attempts + st.skipped >= 6
+        assert st.valid_updates <= st.attempts
+
+
+def test_last_pass_quiet(engine):  # test_engine.cpp:222-230
+    rng = np.random.default_rng(61)
+    el = random_edge_list(rng, 30, 80, False)
+    csr, pages = built(el, 4)
+    for clock in ps.ClockMode:
+        r = engine.run_graph(csr, pages, ps.make_cc(), cfg_of(clock=clock))
+        assert r.metrics.per_pass[-1].valid_updates == 0
+
+
+def test_status_histogram_invariants(engine):  # test_bench.cpp:159-192
+    rng = np.random.default_rng(23)
+    el = random_edge_list(rng, 40, 160, True)
+    csr, pages = built(el, 8)
+    c = cfg_of(pred=ps.PredictorMode.WEAK, execution=ps.ExecutionPolicy.FORCE_DENSE)
+    r = engine.run_graph(csr, pages, ps.make_sssp(0, el.num_vertices, True), c)
+    first = True
+    for st in r.metrics.per_pass:
+        if not st.has_status_counts:
+            continue
+        s = st.status_counts
+        attempted, skipped = s[0] + s[1] + s[5], s[2] + s[3] + s[4]
+        assert attempted + skipped == el.num_vertices
+        assert st.changed_vertices <= attempted
+        if first:
+            assert s[0] == el.num_vertices
+            first = False
+    assert ps.write_status_histogram_csv(r.metrics).startswith(
+        "pass,s0,s1,s2,s3,s4,s5,attempted,skipped,real")
+    r2 = engine.run_graph(csr, pages, ps.make_cc(), ps.EngineConfig())
+    with pytest.raises(ps.DataError):
+        ps.write_status_histogram_csv(r2.metrics)
+
+
+def test_config_validation_errors(engine):  # test_engine.cpp:295-305, :307-315
+    el = graph(3, [(0, 1)], [5])
+    csr, pages = built(el, 2)
+    bad = ps.EngineConfig(window_capacity=1)
+    with pytest.raises(ps.ConfigError):
+        engine.run_graph(csr, pages, ps.make_bfs(0, 3), bad)
+    unweighted = graph(3, [(0, 1)])
+    csr_u, pages_u = built(unweighted, 2)
+    with pytest.raises(ps.ConfigError):
+        engine.run_graph(csr_u, pages_u, ps.VertexProgram(ps.AlgoKind.SSSP, 0),
+                         ps.EngineConfig())
+
+
+# --------------------------------------------------------------------------
+# property tests (test_engine.cpp:152-220)
+# --------------------------------------------------------------------------
+def test_fixpoint_law_random(engine):
+    rng = np.random.default_rng(31)
+    for _ in range(20):
+        el = random_edge_list(rng, 30, 90, True)
+        csr, pages = built(el, 5)
+        for clock in ps.ClockMode:
+            r = engine.run_graph(csr, pages, ps.make_sssp(0, el.num_vertices, True),
+                                 cfg_of(window=3, clock=clock))
+            assert engine.verify_fixpoint(ps.AlgoKind.SSSP) == 0
+            assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.SSSP, 0))
+
+
+def test_mode_independence_execution_policies(engine):
+    rng = np.random.default_rng(47)
+    for _ in range(15):
+        el = random_edge_list(rng, 24, 70, True)
+        source = int(rng.integers(0, el.num_vertices))
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.CC, ps.AlgoKind.SSSP):
+            g = ps.symmetrize(el) if kind == ps.AlgoKind.CC else el
+            csr, pages = built(g, 4)
+            want = oracle_values(g, kind, source)
+            for pol in ps.ExecutionPolicy:
+                for clock in ps.ClockMode:
+                    r = engine.run_graph(csr, pages, program_for(kind, source, g),
+                                         cfg_of(window=3, execution=pol, clock=clock))
+                    assert np.array_equal(r.values, want), (kind, pol, clock)
+
+
+def test_predictors_preserve_values_strong_never_adds_attempts(engine):
+    rng = np.random.default_rng(53)
+    for _ in range(12):
+        el = random_edge_list(rng, 40, 150, True)
+        source = int(rng.integers(0, el.num_vertices))
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.CC, ps.AlgoKind.SSSP):
+            if kind == ps.AlgoKind.SSSP and not el.weighted():
+                continue  # edgeless draw: no weights, make_sssp would reject it
+            g = ps.symmetrize(el) if kind == ps.AlgoKind.CC else el
+            csr, pages = built(g, 6)
+            prog = program_for(kind, source, g)
+            base = engine.run_graph(csr, pages, prog, cfg_of(window=4))
+            strong = engine.run_graph(csr, pages, prog, cfg_of(window=4, pred=ps.PredictorMode.STRONG))
+            weak = engine.run_graph(csr, pages, prog, cfg_of(window=4, pred=ps.PredictorMode.WEAK))
+            assert np.array_equal(strong.values, base.values)
+            assert strong.metrics.update_attempts <= base.metrics.update_attempts
+            assert np.array_equal(weak.values, base.values)
+            assert np.array_equal(base.values, oracle_values(g, kind, source))
+
+
+# --------------------------------------------------------------------------
+# oracle-equivalence matrix (SPEC acceptance criterion 1)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_rmat_matrix_all_modes(engine, seed):
+    scale = 9
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 8, seed=seed)
+    w = O.assign_weights(src.size, O.mix64(seed ^ 0x77), 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    for kind, g in ((ps.AlgoKind.BFS, el), (ps.AlgoKind.SSSP, el), (ps.AlgoKind.CC, sym)):
+        csr, pages = built(g, ps.resolve_page_capacity(0, n))
+        want = oracle_values(g, kind, 0)
+        for mode in MODES:
+            for pred in PREDS:
+                for window in (2, 4, 8):
+                    for clock in ps.ClockMode:
+                        c = cfg_of(mode=mode, pred=pred, window=window, clock=clock)
+                        r = engine.run_graph(csr, pages, program_for(kind, 0, g), c)
+                        assert np.array_equal(r.values, want), (kind, mode, pred, window, clock)
+
+
+def test_virtual_clock_is_deterministic(engine):
+    src, dst = O.generate_rmat(8, 8, seed=11)
+    n = 256
+    el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
+    csr, pages = built(el, ps.resolve_page_capacity(0, n))
+    for mode in MODES:
+        for pred in PREDS:
+            c = cfg_of(mode=mode, pred=pred, window=4, record_trace=True)
+            a = engine.run_graph(csr, pages, ps.make_bfs(0, n), c)
+            b = engine.run_graph(csr, pages, ps.make_bfs(0, n), c)
+            fa = (a.metrics.passes, a.metrics.update_attempts, a.metrics.valid_updates,
+                  a.metrics.edges_read, a.metrics.bytes_transferred, a.metrics.virtual_makespan)
+            fb = (b.metrics.passes, b.metrics.update_attempts, b.metrics.valid_updates,
+                  b.metrics.edges_read, b.metrics.bytes_transferred, b.metrics.virtual_makespan)
+            assert fa == fb, (mode, pred)
+            assert [(e.time, e.kind, e.page_id) for e in a.trace] == \
+                   [(e.time, e.kind, e.page_id) for e in b.trace]
+
+
+# --------------------------------------------------------------------------
+# out-of-core path (forced HBM budget)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", MODES)
+def test_streaming_matches_resident(mode):
+    scale = 12
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=5)
+    w = O.assign_weights(src.size, 3, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 64)
+    sizes = [ps.page_bytes(p, True) for p in pages.pages]
+    total = sum(sizes)
+    budget = 4 * max(sizes) + total // 8  # window of 4 slots + a small cache
+    assert budget < total
+    want = oracle_values(el, ps.AlgoKind.SSSP, 0)
+    with ps.Engine(0, budget) as eng:
+        c = cfg_of(mode=mode, clock=ps.ClockMode.WALL, window=4,
+                   execution=ps.ExecutionPolicy.FORCE_DENSE)
+        r = eng.run_graph(csr, pages, ps.make_sssp(0, n, True), c)
+        assert np.array_equal(r.values, want)
+        assert r.metrics.bytes_transferred >= total  # every page admitted at least once
+        pr = eng.run_graph(csr, pages, ps.make_pagerank(), c)
+    ref = O.pagerank(n, src, dst, 20, 0.85)
+    assert np.abs(pr.ranks.astype(np.float64) - ref).max() < PR_TOL
+
+
+# --------------------------------------------------------------------------
+# PageRank (new; conventions DESIGN.md §2)
+# --------------------------------------------------------------------------
+def test_pagerank_known_answers(engine):
+    # directed 3-cycle: uniform 1/3 is the fixed point
+    el = graph(3, [(0, 1), (1, 2), (2, 0)])
+    csr, pages = built(el, 2)
+    r = engine.run_graph(csr, pages, ps.make_pagerank(), ps.EngineConfig())
+    assert np.allclose(r.ranks, 1 / 3, atol=1e-7)
+    # 2-vertex 0->1, dangling mass dropped: r0 = (1-d)/2, r1 = (1-d)/2 + d*r0(prev)
+    el = graph(2, [(0, 1)])
+    csr, pages = built(el, 1)
+    d = 0.85
+    r = engine.run_graph(csr, pages, ps.make_pagerank(), ps.EngineConfig())
+    assert abs(r.ranks[0] - (1 - d) / 2) < 1e-7
+    assert abs(r.ranks[1] - ((1 - d) / 2 + d * (1 - d) / 2)) < 1e-7
+
+
+@pytest.mark.parametrize("scale", [10, 14])
+def test_pagerank_rmat_vs_oracle(engine, scale):
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=2)
+    el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
+    csr, pages = built(el, n // 16)
+    r = engine.run_graph(csr, pages, ps.make_pagerank(), ps.EngineConfig())
+    ref = O.pagerank(n, src, dst, 20, 0.85)
+    assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
+    assert r.metrics.passes == 20
+
+
+# --------------------------------------------------------------------------
+# bigger graphs: hub chunks, many tiles, sparse/dense switching
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("scale", [14, 16])
+def test_rmat_large_parity(engine, scale):
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=0)
+    w = O.assign_weights(src.size, 1, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, (n + 15) // 16)
+    for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+        want = oracle_values(el, kind, 0)
+        for mode in (ps.ScheduleModeKind.BASELINE, ps.ScheduleModeKind.REENTRY,
+                     ps.ScheduleModeKind.PIPELINED_FINE):
+            for pred in PREDS:
+                c = cfg_of(mode=mode, pred=pred, clock=ps.ClockMode.WALL)
+                r = engine.run_graph(csr, pages, program_for(kind, 0, el), c)
+                assert np.array_equal(r.values, want), (kind, mode, pred)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    csr, pages = built(sym, (n + 15) // 16)
+    want = oracle_values(sym, ps.AlgoKind.CC, 0)
+    for pred in PREDS:
+        r = engine.run_graph(csr, pages, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+        assert np.array_equal(r.values, want), pred
+
+
+def test_fixpoint_verifier_detects_violations(engine):
+    n = 1 << 10
+    src, dst = O.generate_rmat(10, 16, seed=4)
+    w = O.assign_weights(src.size, 9, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, 64)
+    r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True), cfg_of(clock=ps.ClockMode.WALL))
+    assert engine.verify_fixpoint(ps.AlgoKind.SSSP) == 0
+    bad = r.values.copy()
+    reached = np.nonzero(bad != ps.kUnreached)[0]
+    bad[reached[1:50]] += 1000
+    assert engine.verify_fixpoint(ps.AlgoKind.SSSP, bad) > 0
