@@ -12,10 +12,10 @@ LIB := $(PKG)/libseraph.so
 
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(SRC)
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I$(CUDA_HOME)/include
-LDFLAGS := -shared -L$(CUDA_HOME)/lib64 -lcudart -lnccl -lpthread -Wl,-rpath,$(CUDA_HOME)/lib64
+LDFLAGS := -shared -L$(CUDA_HOME)/lib64 -lcudart -ldl -lpthread -Wl,-rpath,$(CUDA_HOME)/lib64
 
 HDRS := include/seraph.h $(wildcard $(SRC)/*.h)
-OBJS := $(BUILD)/kernels.o $(BUILD)/engine.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/engine.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o $(BUILD)/nccl_dyn.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle

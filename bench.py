@@ -1,0 +1,444 @@
+#!/usr/bin/env python3
+"""Benchmark of the subgraph-iteration hot path (BASELINE.json metric).
+
+Default workload (N=1): configs[1] of BASELINE.json -- SSSP on RMAT scale-24
+(edge factor 16, uint32 weights in [1,64]), multi-pass subgraph iteration,
+16 CSC pages, one B200.  A "step" is one pagestream::run() to convergence.
+
+  value  = |E| / time-to-converge (graph GTEPS) with the graph resident in HBM,
+           timed with CUDA events on the engine's stream, max over ranks;
+  e2e    = the same metric through the public C-ABI call sr_run_graph with the
+           graph in pinned host memory (H2D upload + D2H of the values inside
+           the timed region);
+  roofline = the dominant kernel (K1 dense pull sweep) against measured HBM BW;
+  cpu_baseline = the reference's own run() (oracle/_ref, compiled from the
+           reference sources) on the box's host cores, same graph and config.
+
+`--impl reference` times the reference run() alone (rank 0 only under torchrun).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS and time-to-converge (BFS/SSSP/PR/CC, RMAT) at 1/2/4/8 B200 vs CPU ref"
+ALGOS = {"bfs": 0, "cc": 1, "sssp": 2, "pagerank": 3}
+MODES = {"baseline": 0, "reentry": 1, "double-buffer": 2, "pipelined": 3, "pipelined-fine": 4}
+PREDS = {"off": 0, "strong": 1, "weak": 2}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--algo", default="sssp", choices=list(ALGOS))
+    p.add_argument("--scale", type=int, default=24)
+    p.add_argument("--edge-factor", type=int, default=16)
+    p.add_argument("--uniform", action="store_true", help="a=b=c=d=0.25 (uniform random)")
+    p.add_argument("--pages", type=int, default=16)
+    p.add_argument("--mode", default="reentry", choices=list(MODES))
+    p.add_argument("--predictor", default="strong", choices=list(PREDS))
+    p.add_argument("--window", type=int, default=8)
+    p.add_argument("--mrt", type=int, default=2)
+    p.add_argument("--budget-gb", type=float, default=0.0, help="forced HBM budget for pages")
+    p.add_argument("--pr-iters", type=int, default=20)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def workload(args):
+    """Synthetic RMAT graph of the named scale (library host generator), CSR +
+    16 CSC pages, all arrays in pinned host memory (e2e inputs)."""
+    from paper_1806_00762_b200 import _native as N
+    from paper_1806_00762_b200 import pagestream as ps
+
+    t0 = time.time()
+    quad = (0.25, 0.25, 0.25, 0.25) if args.uniform else (0.57, 0.19, 0.19, 0.05)
+    el = ps.generate_rmat_fast(args.scale, args.edge_factor, *quad, seed=args.seed)
+    weighted = args.algo == "sssp"
+    if weighted:
+        el = ps.assign_weights_fast(el, args.seed + 1, 1, 64)
+    if args.algo == "cc":
+        el = ps.symmetrize(el)
+    n, m = el.num_vertices, el.num_edges()
+    cap = (n + args.pages - 1) // args.pages
+
+    arena = N.PinnedArena()
+    pin = [True]
+
+    def pinned(count, dtype):
+        if pin[0]:
+            try:
+                return arena.array(count, dtype)
+            except N.Error:
+                pin[0] = False  # no device (CPU-only reference arm): pageable memory
+        return np.empty(count, dtype)
+
+    out_off = pinned(n + 1, np.uint64)
+    out_nbr = pinned(m, np.uint32)
+    out_w = pinned(m if weighted else 0, np.uint32)
+    in_off = np.zeros(n + 1, np.uint64)
+    in_src = pinned(m, np.uint32)
+    in_w = pinned(m if weighted else 0, np.uint32)
+    N.check(N.lib.sr_build_csr(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
+                               N.ptr(out_off), N.ptr(out_nbr), N.ptr(out_w), 0))
+    N.check(N.lib.sr_build_csc(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
+                               N.ptr(in_off), N.ptr(in_src), N.ptr(in_w), 0))
+    npg = (n + cap - 1) // cap
+    local = pinned(n + npg, np.uint32)
+    N.check(N.lib.sr_page_offsets(n, cap, N.ptr(in_off), N.ptr(local)))
+    csr = ps.CsrGraph(n, out_off, out_nbr, out_w)
+    pages = ps.pages_from_csc(n, cap, in_off, in_src, in_w, local)
+    del el
+    return dict(csr=csr, pages=pages, n=n, m=m, cap=cap, in_off=in_off, in_src=in_src,
+                in_w=in_w if weighted else None, weighted=weighted, build_s=time.time() - t0,
+                arena=arena, pinned=pin[0])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i - 5] for r in rows for i in range(5, 9) if r[i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as fh:
+                d = json.load(fh)
+            return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic(workload_key):
+    """dram bytes per launch of K1 from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        d = json.load(fh)
+    e = d.get(workload_key)
+    return e.get("dram_bytes_per_launch") if e else None
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    from paper_1806_00762_b200 import _native as N
+    from paper_1806_00762_b200 import pagestream as ps
+
+    W = workload(args)
+    csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
+    algo = ALGOS[args.algo]
+    prog = ps.VertexProgram(ps.AlgoKind(algo), 0)
+    cfg = ps.EngineConfig(predictor=ps.PredictorMode(PREDS[args.predictor]),
+                          window_capacity=args.window, clock=ps.ClockMode.WALL,
+                          pr_iterations=args.pr_iters)
+    cfg.schedule.kind = ps.ScheduleModeKind(MODES[args.mode])
+    cfg.schedule.max_reentry_times = args.mrt
+    budget = int(args.budget_gb * 2**30)
+
+    def sync():
+        N.check(N.lib.sr_device_sync(local_rank))
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+    eng = ps.Engine(local_rank, budget)
+    if world > 1:
+        uid = [None]
+        if rank == 0:
+            buf = (N.C.c_uint8 * 128)()
+            N.check(N.lib.sr_nccl_unique_id(N.C.byref(buf)))
+            uid[0] = bytes(buf)
+        dist.broadcast_object_list(uid, src=0)
+        eng.attach_world(rank, world, uid[0])
+    eng.load(csr, pages)
+
+    def one():
+        r = eng.run(prog, cfg, want_values=False)
+        return r
+
+    for _ in range(max(args.warmup, 0)):
+        one()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    sync()
+    dev_s, runs = [], []
+    t0 = time.time()
+    for _ in range(args.steps):
+        r = one()
+        dev_s.append(r.metrics.device_seconds)
+        runs.append(r)
+    sync()
+    wall = time.time() - t0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_s = sum(dev_s) / len(dev_s)
+    if world > 1:
+        t = torch.tensor([step_s], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s = float(t.item())
+    last = runs[-1].metrics
+    iters = args.pr_iters if algo == 3 else 1
+    value = m * iters / step_s / 1e9
+    gteps_read = last.edges_read / (dev_s[-1]) / 1e9
+    launches = sum(r.metrics.kernel_launches for r in runs)
+
+    # parity at full size: device fixpoint law + source value
+    parity = {}
+    if algo in (0, 2):
+        res = eng.run(prog, cfg)
+        viol = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
+        parity = {"fixpoint_violations": viol, "source_value": int(res.values[0]),
+                  "reached": int((res.values != ps.kUnreached).sum())}
+    elif algo == 1:
+        res = eng.run(prog, cfg)
+        parity = {"fixpoint_violations": eng.verify_fixpoint(ps.AlgoKind.CC, res.values)}
+
+    # roofline: the dominant kernel = K1 dense pull sweep over all pages
+    roof = None
+    if not args.budget_gb and algo != 3:
+        ms, edges = eng.bench_pull_sweep(ps.AlgoKind(algo), 20)
+        per_edge = 12 if algo == 2 else 8
+        alg_bytes = per_edge * edges + 8 * n
+        peak, src_ = measured_peaks()
+        achieved = alg_bytes / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "pull_relax_kernel (K1 sweep)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": src_,
+                "traffic": profile_traffic(f"{args.algo}-s{args.scale}"),
+                "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": round(ms, 4),
+                "per_unit": f"{per_edge} B/edge + 8 B/destination"}
+    elif algo == 3:
+        peak, src_ = measured_peaks()
+        roof = {"bound": "hbm" if not args.budget_gb else "host-link", "peak": peak,
+                "unit": "GB/s", "peak_source": src_, "traffic": None}
+
+    # e2e: the public C-ABI one-shot call with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e_eng = ps.Engine(local_rank, budget)
+        if world > 1:
+            e2e = None
+        else:
+            vals = np.empty(n, np.uint32) if algo != 3 else None
+            e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
+            sync()
+            t1 = time.time()
+            reps = max(1, min(args.steps, 5))
+            for _ in range(reps):
+                rr = e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)
+            sync()
+            e2e_s = (time.time() - t1) / reps
+            csr_bytes = csr.out_offsets.nbytes + csr.out_neighbors.nbytes + csr.out_weights.nbytes
+            page_bytes = sum(p.in_offsets.nbytes + p.in_sources.nbytes + p.in_weights.nbytes
+                             for p in pages.pages)
+            e2e = {"value": round(m * iters / e2e_s / 1e9, 4), "unit": "GTEPS",
+                   "seconds_per_step": round(e2e_s, 5),
+                   "h2d_bytes_per_step": int(csr_bytes + page_bytes),
+                   "d2h_bytes_per_step": int(n * 4),
+                   "upload_seconds": round(rr.metrics.upload_seconds, 5),
+                   "call": "sr_run_graph (pagestream::run drop-in), pinned host inputs"}
+        e2e_eng.close()
+
+    # CPU baseline: the reference's run() on the same graph, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, W, sample_runs=1)
+
+    ms_per_step = step_s * 1e3
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "u32" if algo != 3 else "f32", "data": "synthetic",
+        "config": {"workload": f"C2: {args.algo.upper()} RMAT-{args.scale} ef{args.edge_factor}"
+                               f"{' w[1,64]' if W['weighted'] else ''}, {len(pages.pages)} pages,"
+                               f" {args.mode}/{args.predictor}, window {args.window}",
+                   "algo": args.algo, "scale": args.scale, "vertices": n, "edges": m,
+                   "pages": len(pages.pages), "schedule": args.mode,
+                   "predictor": args.predictor, "window": args.window, "source": 0,
+                   "hbm_budget_gb": args.budget_gb or None,
+                   "l2": "inputs larger than L2 (CSC %.2f GB vs 126 MB L2)" % (
+                       sum(ps.page_bytes(p, W["weighted"]) for p in pages.pages) / 1e9),
+                   "graph_build_s": round(W["build_s"], 2),
+                   "parallelism": f"dp{world}" if world > 1 else "single"},
+        "time_to_converge_ms": round(ms_per_step, 4),
+        "gteps_read": round(gteps_read, 4),
+        "passes": {"total": last.passes, "dense": last.dense_passes, "sparse": last.sparse_passes,
+                   "recovery": last.recovery_passes, "edges_read": last.edges_read},
+        "wall_ms_per_step": round(wall / args.steps * 1e3, 4),
+        "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
+        "clocks": clocks, "parity": parity,
+    }
+    eng.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(args, W, sample_runs=1):
+    """The reference run() (oracle/_ref) on this box's host cores, same graph and config.
+    Falls back to the oracle port (Dijkstra/BFS/CC restatement) if _ref was not built."""
+    from oracle import oracle as O
+    cores = args.cpu_threads or os.cpu_count() or 1
+    csr, pages = W["csr"], W["pages"]
+    algo = ALGOS[args.algo]
+    ref = O.load_reference()
+    if ref is not None and algo != 3:
+        g = O.RefGraph(ref, W["n"], csr.out_offsets, csr.out_neighbors,
+                       csr.out_weights if W["weighted"] else None, W["in_off"], W["in_src"],
+                       W["in_w"], W["cap"])
+        secs, mets = [], None
+        for _ in range(sample_runs):
+            _, mets = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
+                            args.window, cores, 1, 0, 0.05)
+            secs.append(mets["wall_seconds"])
+        g.close()
+        t = min(secs)
+        return {"value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
+                "kind": "reference", "seconds": round(t, 3),
+                "sample": f"{sample_runs} full reference run() of the same workload "
+                          f"(ClockMode::Wall, {cores} OpenMP workers)",
+                "edges_read": mets["edges_read"], "passes": mets["passes"]}
+    # port: the oracle's sequential solver on the same CSR
+    t0 = time.time()
+    if algo == 3:
+        return None
+    O.solve_csr(algo, W["n"], csr.out_offsets, csr.out_neighbors,
+                csr.out_weights if W["weighted"] else None, 0)
+    t = time.time() - t0
+    return {"value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "port",
+            "seconds": round(t, 3), "sample": "oracle sequential solver, full graph"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    W = workload(args)
+    from oracle import oracle as O
+    ref = O.load_reference()
+    algo = ALGOS[args.algo]
+    cores = args.cpu_threads or os.cpu_count() or 1
+    if ref is None or algo == 3:
+        why = "oracle/_ref not built" if ref is None else "reference has no PageRank"
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return
+    csr, pages = W["csr"], W["pages"]
+    g = O.RefGraph(ref, W["n"], csr.out_offsets, csr.out_neighbors,
+                   csr.out_weights if W["weighted"] else None, W["in_off"], W["in_src"],
+                   W["in_w"], W["cap"])
+
+    def one():
+        _, met = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
+                       args.window, cores, 1, 0, 0.05)
+        return met
+
+    for _ in range(max(args.warmup, 0)):
+        one()
+    secs, met = [], None
+    for _ in range(args.steps):
+        met = one()
+        secs.append(met["wall_seconds"])
+    g.close()
+    t = sum(secs) / len(secs)
+    value = W["m"] / t / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "GTEPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"C2: {args.algo.upper()} RMAT-{args.scale}, {len(pages.pages)} pages,"
+                               f" {args.mode}/{args.predictor}, window {args.window}",
+                   "algo": args.algo, "scale": args.scale, "edges": W["m"]},
+        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores,
+                         "kind": "reference",
+                         "sample": "full reference run() per step (ClockMode::Wall)"},
+        "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "passes": met["passes"], "edges_read": met["edges_read"],
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

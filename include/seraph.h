@@ -225,6 +225,14 @@ int sr_verify_fixpoint(sr_ctx* ctx, int algo, const uint32_t* values_host,
 int sr_bench_pull_sweep(sr_ctx* ctx, int algo, uint32_t reps, double* ms_per_sweep,
                         uint64_t* edges_per_sweep);
 
+/* ---- host plumbing ------------------------------------------------------ */
+/* Page-locked host buffers (cudaHostAlloc): inputs in pinned memory upload at
+ * full link speed and are what the out-of-core path streams from. */
+int sr_host_alloc(uint64_t bytes, void** out);
+void sr_host_free(void* p);
+/* cudaDeviceSynchronize on `device` (bench bracketing without torch). */
+int sr_device_sync(int device);
+
 /* ---- multi-GPU (one process per GPU) ----------------------------------- */
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the host. */
 int sr_nccl_unique_id(uint8_t out[128]);

@@ -48,6 +48,7 @@ def _load_oracle():
         "oracle_sssp": (None, [_U32, _VP, _VP, _VP, _U32, _VP]),
         "oracle_brute_fixpoint": (None, [_U32, _U64, _VP, _VP, _VP, C.c_int, _U32, _VP]),
         "oracle_pagerank": (None, [_U32, _VP, _VP, _VP, _U32, _D, _VP]),
+        "oracle_mt64_nth": (_U64, [_U64, _U64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -72,6 +73,10 @@ def assign_weights(m, seed, lo=1, hi=64):
     w = np.empty(m, np.uint32)
     assert lib.oracle_assign_weights(m, seed, lo, hi, _p(w)) == 0
     return w
+
+
+def mt64_nth(seed: int, nth: int) -> int:
+    return int(lib.oracle_mt64_nth(seed, nth))
 
 
 def mix64(x: int) -> int:
@@ -168,6 +173,10 @@ def load_reference():
         "ref_build_csr": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
         "ref_build_csc_pages": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _U32, _VP, _VP, _VP]),
         "ref_reference_solve": (C.c_int, [_U32, _U64, _VP, _VP, _VP, C.c_int, _U32, _VP]),
+        "ref_prepare": (_VP, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, _U32]),
+        "ref_release": (None, [_VP]),
+        "ref_run_prepared": (C.c_int, [_VP, C.c_int, _U32, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       _U32, C.c_int, C.c_int, C.c_int, _D, _VP, _VP]),
         "ref_run": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, _U32, C.c_int, _U32,
                               C.c_int, C.c_int, C.c_int, C.c_int, _U32, C.c_int, C.c_int,
                               C.c_int, _D, _VP, _VP]),
@@ -193,3 +202,36 @@ def ref_run(ref, n, out_off, out_nbr, out_w, in_off, in_src, in_w, cap, algo, so
             "bytes_transferred", "update_attempts", "valid_updates", "skipped_vertices",
             "edges_read", "virtual_makespan", "wall_seconds", "has_accuracy", "accuracy"]
     return vals, dict(zip(keys, met[:14].tolist()))
+
+
+_REF_KEYS = ["passes", "sparse_passes", "dense_passes", "recovery_passes", "pages_transferred",
+             "bytes_transferred", "update_attempts", "valid_updates", "skipped_vertices",
+             "edges_read", "virtual_makespan", "wall_seconds", "has_accuracy", "accuracy"]
+
+
+class RefGraph:
+    """The reference's CsrGraph + PageSet built once from flat arrays (same layouts)."""
+
+    def __init__(self, ref, n, out_off, out_nbr, out_w, in_off, in_src, in_w, cap):
+        self.ref = ref
+        self.n = n
+        self.h = ref.ref_prepare(n, out_nbr.size, _p(out_off), _p(out_nbr), _p(out_w),
+                                 _p(in_off), _p(in_src), _p(in_w), cap)
+        if not self.h:
+            raise RuntimeError(ref.ref_error().decode())
+
+    def run(self, algo, source=0, predictor=0, schedule=0, mrt=2, reps=3, window=8, workers=4,
+            clock=1, execution=0, density=0.05, want_values=False):
+        vals = np.empty(self.n, np.uint32) if want_values else None
+        met = np.zeros(16, np.float64)
+        rc = self.ref.ref_run_prepared(self.h, algo, source, predictor, schedule, mrt, reps,
+                                       window, workers, clock, execution, density, _p(vals),
+                                       _p(met))
+        if rc != 0:
+            raise RuntimeError(self.ref.ref_error().decode())
+        return vals, dict(zip(_REF_KEYS, met[:14].tolist()))
+
+    def close(self):
+        if self.h:
+            self.ref.ref_release(self.h)
+            self.h = None

@@ -116,6 +116,88 @@ int ref_reference_solve(uint32_t n, uint64_t m, const uint32_t* src, const uint3
   });
 }
 
+// Prebuilt reference structures, so repeated timed runs only execute run().
+struct RefGraph {
+  CsrGraph csr;
+  PageSet pages;
+};
+
+static RefGraph* make_ref_graph(uint32_t n, uint64_t m, const uint64_t* out_off,
+                                const uint32_t* out_nbr, const uint32_t* out_w,
+                                const uint64_t* in_off, const uint32_t* in_src,
+                                const uint32_t* in_w, uint32_t cap) {
+  auto* g = new RefGraph();
+  g->csr.num_vertices = n;
+  g->csr.out_offsets.assign(out_off, out_off + size_t(n) + 1);
+  g->csr.out_neighbors.assign(out_nbr, out_nbr + m);
+  if (out_w) g->csr.out_weights.assign(out_w, out_w + m);
+  PageSet& ps = g->pages;
+  ps.num_vertices = n;
+  ps.page_vertex_capacity = cap;
+  ps.weighted = in_w != nullptr;
+  const uint64_t np = (uint64_t(n) + cap - 1) / cap;
+  ps.pages.resize(np);
+  for (uint64_t p = 0; p < np; ++p) {
+    CscPage& pg = ps.pages[p];
+    pg.vertex_begin = uint32_t(p * cap);
+    pg.vertex_end = uint32_t(std::min<uint64_t>((p + 1) * cap, n));
+    const uint64_t lo = in_off[pg.vertex_begin], hi = in_off[pg.vertex_end];
+    pg.in_offsets.resize(size_t(pg.range()) + 1);
+    for (uint32_t v = 0; v <= pg.range(); ++v)
+      pg.in_offsets[v] = uint32_t(in_off[pg.vertex_begin + v] - lo);
+    pg.in_sources.assign(in_src + lo, in_src + hi);
+    if (in_w) pg.in_weights.assign(in_w + lo, in_w + hi);
+  }
+  return g;
+}
+
+void* ref_prepare(uint32_t n, uint64_t m, const uint64_t* out_off, const uint32_t* out_nbr,
+                  const uint32_t* out_w, const uint64_t* in_off, const uint32_t* in_src,
+                  const uint32_t* in_w, uint32_t cap) {
+  RefGraph* g = nullptr;
+  guard([&] { g = make_ref_graph(n, m, out_off, out_nbr, out_w, in_off, in_src, in_w, cap); });
+  return g;
+}
+
+void ref_release(void* h) { delete static_cast<RefGraph*>(h); }
+
+static void fill_metrics(const MetricsReport& mm, double* metrics_out) {
+  double out[16] = {double(mm.passes), double(mm.sparse_passes), double(mm.dense_passes),
+                    double(mm.recovery_passes), double(mm.pages_transferred),
+                    double(mm.bytes_transferred), double(mm.update_attempts),
+                    double(mm.valid_updates), double(mm.skipped_vertices),
+                    double(mm.edges_read), mm.virtual_makespan, mm.wall_seconds,
+                    mm.prediction_accuracy ? 1.0 : 0.0,
+                    mm.prediction_accuracy ? *mm.prediction_accuracy : 0.0, 0, 0};
+  std::memcpy(metrics_out, out, sizeof(out));
+}
+
+// pagestream::run (engine.hpp:125) on a prepared graph.
+int ref_run_prepared(void* h, int algo, uint32_t source, int predictor, int schedule, int mrt,
+                     int reps, uint32_t window, int workers, int clock, int execution,
+                     double density, uint32_t* values_out, double* metrics_out) {
+  return guard([&] {
+    RefGraph* g = static_cast<RefGraph*>(h);
+    VertexProgram prog;
+    prog.kind = AlgoKind(algo);
+    prog.source = source;
+    EngineConfig cfg;
+    cfg.page_vertex_capacity = g->pages.page_vertex_capacity;
+    cfg.density_threshold_fraction = density;
+    cfg.predictor = PredictorMode(predictor);
+    cfg.schedule.kind = ScheduleModeKind(schedule);
+    cfg.schedule.max_reentry_times = mrt;
+    cfg.schedule.buffer_repetitions = reps;
+    cfg.window_capacity = window;
+    cfg.transfer.worker_count = workers;
+    cfg.clock = ClockMode(clock);
+    cfg.execution = ExecutionPolicy(execution);
+    RunResult r = run(g->csr, g->pages, prog, cfg);
+    if (values_out) std::memcpy(values_out, r.values.data(), r.values.size() * 4);
+    fill_metrics(r.metrics, metrics_out);
+  });
+}
+
 // The reference engine run() on prebuilt structures (copied from flat
 // arrays with the reference layouts), returning values and metrics.
 // metrics_out[16]: passes, sparse, dense, recovery, pages_transferred,

@@ -308,3 +308,15 @@ void oracle_pagerank(uint32_t n, const uint64_t* in_off, const uint32_t* in_src,
   }
   free(contrib);
 }
+
+/* n-th output (1-based) of std::mt19937_64 seeded with `seed`; the C++
+ * standard pins the 10000th output of the default seed 5489 at
+ * 9981545732273789042 ([rand.predef]). */
+uint64_t oracle_mt64_nth(uint64_t seed, uint64_t nth) {
+  mt64* g = (mt64*)malloc(sizeof(mt64));
+  mt64_seed(g, seed);
+  uint64_t x = 0;
+  for (uint64_t i = 0; i < nth; ++i) x = mt64_next(g);
+  free(g);
+  return x;
+}

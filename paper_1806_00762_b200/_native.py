@@ -189,6 +189,9 @@ SIGNATURES = {
     "sr_verify_fixpoint": (C.c_int, [_VP, C.c_int, _VP, C.POINTER(_U64)]),
     "sr_bench_pull_sweep": (C.c_int, [_VP, C.c_int, _U32, C.POINTER(_D), C.POINTER(_U64)]),
     "sr_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8 * 128)]),
+    "sr_host_alloc": (C.c_int, [_U64, C.POINTER(_VP)]),
+    "sr_host_free": (None, [_VP]),
+    "sr_device_sync": (C.c_int, [C.c_int]),
     "sr_attach_world": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(C.c_uint8 * 128)]),
     "sr_shard_plan": (C.c_int, [_U32, _VP, _U32, _VP]),
     "sr_rmat_generate": (C.c_int, [C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP, C.c_int]),
@@ -235,3 +238,25 @@ def ptr(a) -> int | None:
         return None
     assert a.flags["C_CONTIGUOUS"], "arrays passed to libseraph must be contiguous"
     return a.ctypes.data
+
+
+class PinnedArena:
+    """Page-locked host arrays from sr_host_alloc (freed with the arena)."""
+
+    def __init__(self):
+        self._bufs = []
+
+    def array(self, n: int, dtype) -> "np.ndarray":
+        import numpy as np
+        dt = np.dtype(dtype)
+        nbytes = max(int(n) * dt.itemsize, 1)
+        p = C.c_void_p()
+        check(lib.sr_host_alloc(nbytes, C.byref(p)))
+        self._bufs.append(p.value)
+        buf = (C.c_uint8 * nbytes).from_address(p.value)
+        return np.frombuffer(buf, dtype=dt, count=int(n))
+
+    def close(self):
+        for p in self._bufs:
+            lib.sr_host_free(p)
+        self._bufs = []

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "nccl_dyn.h"
 #include "seraph.h"
 
 struct sr_ctx {
@@ -192,12 +193,32 @@ int sr_bench_pull_sweep(sr_ctx* ctx, int algo, uint32_t reps, double* ms, uint64
 
 int sr_nccl_unique_id(uint8_t out[128]) {
   return guard(nullptr, [&] {
+    const seraph::NcclApi& nc = seraph::nccl();
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
+    const ncclResult_t r = nc.GetUniqueId(&id);
     if (r != ncclSuccess)
-      throw seraph::EngineError(SR_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+      throw seraph::EngineError(SR_E_NCCL, std::string("ncclGetUniqueId: ") + nc.GetErrorString(r));
     static_assert(sizeof(id) == 128, "nccl unique id size");
     std::memcpy(out, &id, 128);
+  });
+}
+
+int sr_host_alloc(uint64_t bytes, void** out) {
+  return guard(nullptr, [&] {
+    if (!out) throw seraph::EngineError(SR_E_CONFIG, "null output");
+    *out = nullptr;
+    if (bytes) SR_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+  });
+}
+
+void sr_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sr_device_sync(int device) {
+  return guard(nullptr, [&] {
+    SR_CUDA(cudaSetDevice(device));
+    SR_CUDA(cudaDeviceSynchronize());
   });
 }
 

@@ -10,6 +10,7 @@
 #include <thread>
 
 #include "kernels.h"
+#include "nccl_dyn.h"
 
 namespace seraph {
 
@@ -94,7 +95,7 @@ Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  if (comm_) ncclCommDestroy(comm_);
+  if (comm_) nccl().CommDestroy(comm_);
   for (auto& s : slots_) {
     if (s.ready) cudaEventDestroy(s.ready);
     if (s.freed) cudaEventDestroy(s.freed);
@@ -917,21 +918,22 @@ void Engine::exchange_round(bool pagerank) {
   if (world_ <= 1) return;
   ncclResult_t r = ncclSuccess;
   SR_CUDA(cudaSetDevice(dev_));
-  ncclGroupStart();
+  const NcclApi& nc = nccl();
+  nc.GroupStart();
   if (pagerank) {
-    r = ncclAllReduce(rank_b_.p, rank_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
+    r = nc.AllReduce(rank_b_.p, rank_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
     if (r == ncclSuccess)
-      r = ncclAllReduce(contrib_b_.p, contrib_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
+      r = nc.AllReduce(contrib_b_.p, contrib_b_.p, n_, ncclFloat, ncclSum, comm_, cs_);
   } else {
-    r = ncclAllReduce(values_.p, values_.p, n_, ncclUint32, ncclMin, comm_, cs_);
+    r = nc.AllReduce(values_.p, values_.p, n_, ncclUint32, ncclMin, comm_, cs_);
     if (r == ncclSuccess)
-      r = ncclAllReduce(&census_.p->min_changed, &census_.p->min_changed, 1, ncclUint32, ncclMin,
-                        comm_, cs_);
+      r = nc.AllReduce(&census_.p->min_changed, &census_.p->min_changed, 1, ncclUint32, ncclMin,
+                       comm_, cs_);
   }
   if (r == ncclSuccess && ctr_used_)
-    r = ncclAllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * 4, ncclUint64, ncclSum, comm_, cs_);
-  ncclGroupEnd();
-  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + ncclGetErrorString(r));
+    r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * 4, ncclUint64, ncclSum, comm_, cs_);
+  nc.GroupEnd();
+  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
   if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
 }
 
@@ -1291,10 +1293,11 @@ void Engine::attach_world(int rank, int world, const uint8_t id[128]) {
   if (pages_loaded_) throw EngineError(SR_E_CONFIG, "attach_world must precede load_pages");
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
-  if (comm_) ncclCommDestroy(comm_);
+  const NcclApi& nc = nccl();
+  if (comm_) nc.CommDestroy(comm_);
   comm_ = nullptr;
-  const ncclResult_t r = ncclCommInitRank(&comm_, world, uid, rank);
-  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl init: ") + ncclGetErrorString(r));
+  const ncclResult_t r = nc.CommInitRank(&comm_, world, uid, rank);
+  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl init: ") + nc.GetErrorString(r));
   rank_ = rank;
   world_ = world;
 }

@@ -23,6 +23,7 @@ namespace seraph {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kUnroll = 4;  // 32-edge sub-chunks in flight per warp (K1)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -234,62 +235,87 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
     }
 
     // ---- phase B: gap-free edge stream of the attempted destinations --------
+    // kUnroll sub-chunks of 32 edges per step: destinations of all sub-chunks
+    // are resolved first (shared memory + shuffles only), then every source,
+    // weight and gather load is issued back to back, then reduced in order.
     uint32_t ad = 0;
     uint32_t carry = kUnreached;
-    for (uint32_t q0 = 0; q0 < tot; q0 += 32) {
-      const uint32_t wi = ad + lane;
-      ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
-      const uint32_t q = q0 + lane;
-      const bool qv = q < tot;
-      uint32_t k = 0;
+    for (uint32_t q0 = 0; q0 < tot; q0 += 32 * kUnroll) {
+      uint32_t eidx[kUnroll], loc[kUnroll], curv[kUnroll], endv[kUnroll], kk[kUnroll];
+      uint32_t adj = ad;
 #pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
-        if (b <= q) k += step;
+      for (int j = 0; j < kUnroll; ++j) {
+        const uint32_t qj = q0 + 32u * j;
+        kk[j] = 0;
+        eidx[j] = 0xffffffffu;
+        loc[j] = curv[j] = 0;
+        endv[j] = 0;
+        if (qj >= tot) continue;  // warp-uniform
+        const uint32_t wi = adj + lane;
+        ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
+        const uint32_t q = qj + lane;
+        uint32_t k = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
+          if (b <= q) k += step;
+        }
+        const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
+        const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
+        loc[j] = __shfl_sync(kFull, e.local, k);
+        curv[j] = __shfl_sync(kFull, e.cur, k);
+        uint32_t end = __shfl_sync(kFull, e.pref, (k + 1) & 31);
+        if (k == 31) end = (adj + 32 < n_act) ? act[adj + 32].pref : tot;
+        endv[j] = end;
+        kk[j] = k;
+        if (q < tot) eidx[j] = my_estart + (q - my_pref);
+        const uint32_t k31 = __shfl_sync(kFull, k, 31);
+        const uint32_t e31 = __shfl_sync(kFull, end, 31);
+        adj += (e31 > qj + 32) ? k31 : k31 + 1;
       }
-      const uint32_t my_local = __shfl_sync(kFull, e.local, k);
-      const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
-      const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
-      const uint32_t my_cur = __shfl_sync(kFull, e.cur, k);
-      const uint32_t nxt_pref = __shfl_sync(kFull, e.pref, (k + 1) & 31);
-      uint32_t cand = kUnreached;
-      if (qv) {
-        const uint32_t eidx = my_estart + (q - my_pref);
-        const uint32_t s = src[eidx];
-        const uint32_t w = (A == kSssp) ? wts[eidx] : 0u;
-        const uint32_t sv = DET ? __ldg(values_ro + s) : a.values[s];
-        cand = combine<A>(sv, w);
+      uint32_t sv[kUnroll], wv[kUnroll];
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        sv[j] = 0;
+        wv[j] = 0;
+        if (eidx[j] != 0xffffffffu) {
+          sv[j] = __ldcs(src + eidx[j]);
+          if (A == kSssp) wv[j] = __ldcs(wts + eidx[j]);
+        }
       }
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t oc = __shfl_up_sync(kFull, cand, off);
-        const uint32_t ok = __shfl_up_sync(kFull, k, off);
-        if (lane >= off && ok == k) cand = min(cand, oc);
+      for (int j = 0; j < kUnroll; ++j)
+        if (eidx[j] != 0xffffffffu) sv[j] = DET ? __ldg(values_ro + sv[j]) : a.values[sv[j]];
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        const uint32_t qj = q0 + 32u * j;
+        if (qj >= tot) break;  // warp-uniform
+        const uint32_t k = kk[j];
+        const uint32_t q = qj + lane;
+        uint32_t cand = (eidx[j] != 0xffffffffu) ? combine<A>(sv[j], wv[j]) : kUnreached;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t oc = __shfl_up_sync(kFull, cand, off);
+          const uint32_t ok = __shfl_up_sync(kFull, k, off);
+          if (lane >= off && ok == k) cand = min(cand, oc);
+        }
+        if (k == 0) cand = min(cand, carry);
+        const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
+        const bool tail = q < tot && (lane == 31 || q + 1 >= tot || k_down != k);
+        const bool complete = endv[j] <= qj + 32;
+        if (tail && complete && cand < curv[j]) {
+          const uint32_t v = vb + loc[j];
+          if (DET) a.next[v] = cand;
+          else a.values[v] = cand;
+          a.changed[v] = 1;
+          c.valid += 1;
+          lane_min = min(lane_min, cand);
+        }
+        const uint32_t c31 = __shfl_sync(kFull, cand, 31);
+        const uint32_t e31 = __shfl_sync(kFull, endv[j], 31);
+        carry = (e31 > qj + 32) ? c31 : kUnreached;
       }
-      if (k == 0) cand = min(cand, carry);
-      uint32_t end = nxt_pref;
-      if (k == 31) end = (ad + 32 < n_act) ? act[ad + 32].pref : tot;
-      const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
-      const bool tail = qv && (lane == 31 || q + 1 >= tot || k_down != k);
-      const bool complete = end <= q0 + 32;
-      if (tail && complete && cand < my_cur) {
-        const uint32_t v = vb + my_local;
-        if (DET) a.next[v] = cand;
-        else a.values[v] = cand;
-        a.changed[v] = 1;
-        c.valid += 1;
-        lane_min = min(lane_min, cand);
-      }
-      const uint32_t k31 = __shfl_sync(kFull, k, 31);
-      const uint32_t c31 = __shfl_sync(kFull, cand, 31);
-      const uint32_t e31 = __shfl_sync(kFull, end, 31);
-      if (e31 > q0 + 32) {
-        ad += k31;
-        carry = c31;
-      } else {
-        ad += k31 + 1;
-        carry = kUnreached;
-      }
+      ad = adj;
     }
     __syncwarp();
   }
