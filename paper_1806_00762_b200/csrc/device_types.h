@@ -70,6 +70,7 @@ struct Segments {
 };
 
 struct PullArgs {
+  unsigned* work;          // per-launch tile counter (dynamic scheduling)
   const uint4* tiles;
   const uint32_t* tile_page;
   const PageDesc* pages;

@@ -298,11 +298,12 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       pages_[p].off_base = off_total;
       pages_[p].edge_base = edge_total;
       off_total += pages_[p].ve - pages_[p].vb + 1;
-      edge_total += pages_[p].edges;
+      edge_total += (pages_[p].edges + 7) & ~7ull;  // K1 reads 32 B-aligned runs
     }
+    edge_total += 8;  // slack past the last page
     arena_offs_.reserve(std::max<uint64_t>(off_total, 1));
-    arena_src_.reserve(std::max<uint64_t>(edge_total, 1));
-    if (weighted) arena_w_.reserve(std::max<uint64_t>(edge_total, 1));
+    arena_src_.reserve(edge_total);
+    if (weighted) arena_w_.reserve(edge_total);
     for (uint32_t p = 0; p < np; ++p) {
       PageMeta& pm = pages_[p];
       PageDesc& d = page_desc_h_[p];
@@ -455,6 +456,19 @@ void Engine::alloc_run_state(const sr_run_config& c) {
   ctr_h_.reserve(entries);
 }
 
+unsigned* Engine::next_work_counter() {
+  if (!work_.p) {
+    work_.reserve(1 << 16);
+    SR_CUDA(cudaMemsetAsync(work_.p, 0, work_.n * sizeof(unsigned), cs_));
+    work_used_ = 0;
+  }
+  if (work_used_ == work_.n) {
+    SR_CUDA(cudaMemsetAsync(work_.p, 0, work_.n * sizeof(unsigned), cs_));
+    work_used_ = 0;
+  }
+  return work_.p + work_used_++;
+}
+
 RunCtr* Engine::alloc_ctr(size_t entries) {
   if (size_t(ctr_used_) + entries > ctr_.n)
     throw EngineError(SR_E_INTERNAL, "counter arena exhausted");
@@ -492,6 +506,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       launch_pr_pull(a, grid, cs_);
     } else {
       PullArgs a{};
+      a.work = next_work_counter();
       a.tiles = tiles_.p;
       a.tile_page = tile_page_.p;
       a.pages = page_desc_.p;
@@ -583,8 +598,9 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
     pm.off_base = off_total;
     pm.edge_base = edge_total;
     off_total += pm.ve - pm.vb + 1;
-    edge_total += pm.edges;
+    edge_total += (pm.edges + 7) & ~7ull;
   }
+  edge_total += 8;
   arena_offs_.release();
   arena_src_.release();
   arena_w_.release();
@@ -618,8 +634,8 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
   slots_.resize(want);
   for (auto& s : slots_) {
     s.offs.reserve(std::max<uint64_t>(max_offs, 1));
-    s.src.reserve(std::max<uint64_t>(max_edges, 1));
-    if (weighted_) s.w.reserve(std::max<uint64_t>(max_edges, 1));
+    s.src.reserve(max_edges + 8);
+    if (weighted_) s.w.reserve(max_edges + 8);
     s.cap_offs = max_offs;
     s.cap_edges = max_edges;
     SR_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));

@@ -210,6 +210,9 @@ class Engine {
   PinBuf<RunCtr> ctr_h_;
   uint32_t ctr_used_ = 0;  // entries of ctr_ handed out in the current pass
   RunCtr* alloc_ctr(size_t entries);
+  DBuf<unsigned> work_;     // K1 per-launch tile counters (ring, zeroed on wrap)
+  size_t work_used_ = 0;
+  unsigned* next_work_counter();
   DBuf<float> rank_a_, rank_b_, contrib_a_, contrib_b_, inv_outdeg_;
   uint32_t run_id_ = 0;
   uint64_t launches_ = 0;

@@ -23,7 +23,8 @@ namespace seraph {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kUnroll = 4;  // 32-edge sub-chunks in flight per warp (K1)
+constexpr int kLaneEdges = 8;  // consecutive edges per lane per K1 phase-B round
+constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -107,33 +108,35 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: dense pull relaxation.  One warp per tile, persistent grid, each warp
-// owns a contiguous slice of the launch's tasks (page changes are rare, so
-// the per-page counters are flushed a handful of times per warp).
+// K1: dense pull relaxation.  One warp per tile; persistent grid; warps grab
+// kGrab consecutive tiles at a time from a per-launch work counter, so a
+// warp stuck on dense tiles does not leave the others idle at the tail.
 //
-// Range tile, phase A: lanes walk 32 destinations at a time, load the value
-// and offsets, apply the predictor gate and compact the attempted
-// destinations with in-edges into a shared-memory list (ballot + scan).
-// Phase B: the attempted destinations' in-edges are consumed 32 at a time as
-// one virtual, gap-free edge stream; a 5-step shuffle search maps each lane
-// to its destination, the gather values[src] is combined, and a shuffle
-// segmented min-scan reduces per destination.  The destination's last lane
-// stores the result (single writer: plain store, no atomic).
-// Hub tile: one chunk of a high in-degree destination; warp min-reduce and
-// atomicMin, with the run-id stamp counting the update once per run.
+// Range tile, phase A: lanes walk 32 destinations at a time, load value and
+// offsets, apply the predictor gate and compact the attempted destinations
+// with in-edges into a shared-memory list (ballot + scan), so the edges of
+// skipped destinations are never read.  Phase B: the attempted destinations'
+// in-edges form one gap-free stream; each lane takes kLaneEdges CONSECUTIVE
+// positions (one shared-memory binary search per run), issues all source,
+// weight and gather loads back to back (memory-level parallelism), folds the
+// run per destination in registers and merges partial minima across lanes
+// with a shared-memory atomicMin.  Phase C: one lane per destination
+// compares the minimum with the gated value and stores it (the page owns its
+// destinations: plain store, no global atomic).
+// Hub tile: one kHubChunk slice of a high in-degree destination; warp
+// min-reduce, global atomicMin, and a run-id stamp that counts the
+// destination's valid update once per run.
 // ---------------------------------------------------------------------------
 template <int A, int G, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
-  __shared__ ActEntry s_act[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_cur[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_best[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  ActEntry* act = s_act[warp];
-
-  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
-  const uint32_t nw = gridDim.x * kWarpsPerBlock;
+  uint32_t* best_of = s_best[warp];
   const uint32_t total = a.seg.task_prefix[a.seg.n];
-  const uint32_t t_begin = (uint32_t)(((unsigned long long)total * gw) / nw);
-  const uint32_t t_end = (uint32_t)(((unsigned long long)total * (gw + 1)) / nw);
 
   LaneCtr c;
   c.clear();
@@ -142,182 +145,187 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
   PageDesc pd{};
   const uint32_t* __restrict__ values_ro = a.values;
 
-  for (uint32_t t = t_begin; t < t_end; ++t) {
-    const uint32_t ti = task_to_tile(a.seg, t);
-    const uint32_t p = a.tile_page[ti];
-    if (p != cur_page) {
-      if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
-      cur_page = p;
-      pd = a.pages[p];
-    }
-    if (a.prev_ctr && a.prev_ctr[a.ctr_per_page ? p : 0].valid == 0) continue;  // reentry: quiet
-    const uint4 tile = a.tiles[ti];
-    const uint32_t vb = pd.vertex_begin;
-    const uint32_t* __restrict__ offs = pd.offs;
-    const uint32_t* __restrict__ src = pd.src;
-    const uint32_t* __restrict__ wts = pd.w;
+  for (;;) {
+    uint32_t t0 = 0;
+    if (lane == 0) t0 = atomicAdd(a.work, kGrab);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= total) break;
+    const uint32_t t1 = min(t0 + kGrab, total);
+    for (uint32_t t = t0; t < t1; ++t) {
+      const uint32_t ti = task_to_tile(a.seg, t);
+      const uint32_t p = a.tile_page[ti];
+      if (p != cur_page) {
+        if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
+        cur_page = p;
+        pd = a.pages[p];
+      }
+      if (a.prev_ctr && a.prev_ctr[a.ctr_per_page ? p : 0].valid == 0) continue;  // quiet page
+      const uint4 tile = a.tiles[ti];
+      const uint32_t vb = pd.vertex_begin;
+      const uint32_t* __restrict__ offs = pd.offs;
+      const uint32_t* __restrict__ src = pd.src;
+      const uint32_t* __restrict__ wts = pd.w;
 
-    if (tile.w & kHubFlag) {
-      // ---- hub chunk -------------------------------------------------------
-      const uint32_t d = tile.z;
-      const uint32_t v = vb + d;
-      const uint32_t cur = DET ? __ldg(values_ro + v) : *(volatile uint32_t*)(a.values + v);
-      const bool att = gate_attempt<A, G>(v, cur, a);
-      const uint32_t lo_d = offs[d];
-      if (lane == 0 && tile.x == lo_d) {  // owner chunk counts the visit once
+      if (tile.w & kHubFlag) {
+        // ---- hub chunk -----------------------------------------------------
+        const uint32_t d = tile.z;
+        const uint32_t v = vb + d;
+        const uint32_t cur = DET ? __ldg(values_ro + v) : *(volatile uint32_t*)(a.values + v);
+        const bool att = gate_attempt<A, G>(v, cur, a);
+        const uint32_t lo_d = offs[d];
+        if (lane == 0 && tile.x == lo_d) {  // owner chunk counts the visit once
+          c.attempts += att;
+          c.skipped += !att;
+          c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
+        }
+        if (!att) continue;
+        uint32_t best = kUnreached;
+        uint32_t e = tile.x + lane;
+#pragma unroll 8
+        for (; e < tile.y; e += 32) {
+          const uint32_t sidx = __ldcs(src + e);
+          const uint32_t w = (A == kSssp) ? __ldcs(wts + e) : 0u;
+          const uint32_t sv = DET ? __ldg(values_ro + sidx) : a.values[sidx];
+          best = min(best, combine<A>(sv, w));
+        }
+        best = warp_min(best);
+        if (lane == 0 && best < cur) {
+          bool improved;
+          if (DET) {
+            atomicMin(a.next + v, best);
+            improved = true;
+          } else {
+            const uint32_t old = atomicMin(a.values + v, best);
+            improved = best < old;
+          }
+          if (improved) {
+            a.changed[v] = 1;
+            lane_min = min(lane_min, best);
+            const uint32_t hub = tile.w & ~kHubFlag;
+            if (atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
+          }
+        }
+        continue;
+      }
+
+      // ---- range tile: phase A (gate + entry list) ---------------------------
+      // Entries = destinations with in-edges, in edge order; bit 31 of
+      // s_loc marks the attempted ones.  pref = first edge relative to ebase.
+      const uint32_t dl = tile.z, dh = tile.w;
+      const uint32_t ebase = tile.x & ~7u;  // 32-byte aligned run grid
+      uint32_t n_ent = 0;
+      unsigned any_att = 0;
+      for (uint32_t base = dl; base < dh; base += 32) {
+        const uint32_t i = base + lane;
+        const bool in = i < dh;
+        uint32_t cur = 0, lo = 0, deg = 0;
+        bool att = false;
+        if (in) {
+          const uint32_t v = vb + i;
+          cur = DET ? __ldg(values_ro + v) : a.values[v];
+          lo = __ldcs(offs + i);
+          deg = __ldcs(offs + i + 1) - lo;
+          att = gate_attempt<A, G>(v, cur, a);
+        }
         c.attempts += att;
-        c.skipped += !att;
-        c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
-      }
-      if (!att) continue;
-      uint32_t best = kUnreached;
-      uint32_t e = tile.x + lane;
-#pragma unroll 4
-      for (; e < tile.y; e += 32) {
-        const uint32_t s = src[e];
-        const uint32_t w = (A == kSssp) ? wts[e] : 0u;
-        const uint32_t sv = DET ? __ldg(values_ro + s) : a.values[s];
-        best = min(best, combine<A>(sv, w));
-      }
-      best = warp_min(best);
-      if (lane == 0 && best < cur) {
-        bool improved;
-        if (DET) {
-          atomicMin(a.next + v, best);
-          improved = true;
-        } else {
-          const uint32_t old = atomicMin(a.values + v, best);
-          improved = best < old;
+        c.skipped += (in && !att);
+        c.edges += att ? deg : 0u;
+        const bool has = in && deg > 0;
+        const unsigned m = __ballot_sync(kFull, has);
+        any_att |= __ballot_sync(kFull, has && att);
+        if (has) {
+          const uint32_t pos = n_ent + __popc(m & lanemask_lt());
+          s_pref[warp][pos] = lo - ebase;
+          s_loc[warp][pos] = i | (att ? 0x80000000u : 0u);
+          s_cur[warp][pos] = cur;
+          best_of[pos] = kUnreached;
         }
-        if (improved) {
-          a.changed[v] = 1;
-          lane_min = min(lane_min, best);
-          const uint32_t hub = tile.w & ~kHubFlag;
-          if (atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
-        }
+        n_ent += __popc(m);
       }
-      continue;
-    }
-
-    // ---- range tile: phase A (gate + compaction) ----------------------------
-    const uint32_t dl = tile.z, dh = tile.w;
-    uint32_t n_act = 0, tot = 0;
-    for (uint32_t base = dl; base < dh; base += 32) {
-      const uint32_t i = base + lane;
-      const bool in = i < dh;
-      uint32_t cur = 0, lo = 0, deg = 0;
-      bool att = false;
-      if (in) {
-        const uint32_t v = vb + i;
-        cur = DET ? __ldg(values_ro + v) : a.values[v];
-        lo = offs[i];
-        deg = offs[i + 1] - lo;
-        att = gate_attempt<A, G>(v, cur, a);
-      }
-      c.attempts += att;
-      c.skipped += (in && !att);
-      c.edges += att ? deg : 0u;
-      const bool live = att && deg > 0;
-      const uint32_t dd = live ? deg : 0u;
-      const uint32_t incl = warp_incl_scan(dd, lane);
-      const unsigned m = __ballot_sync(kFull, live);
-      if (live) {
-        const uint32_t pos = n_act + __popc(m & lanemask_lt());
-        act[pos] = ActEntry{i, lo, tot + incl - dd, cur};
-      }
-      n_act += __popc(m);
-      tot += __shfl_sync(kFull, incl, 31);
-    }
-    __syncwarp();
-    if (n_act == 0) {
       __syncwarp();
-      continue;
-    }
+      if (!any_att) {
+        __syncwarp();
+        continue;
+      }
+      const uint32_t* pref_of = s_pref[warp];
+      const uint32_t* loc_of = s_loc[warp];
+      const uint32_t lo_pos = tile.x - ebase;   // first valid position
+      const uint32_t span = tile.y - ebase;     // one past the last position
 
-    // ---- phase B: gap-free edge stream of the attempted destinations --------
-    // kUnroll sub-chunks of 32 edges per step: destinations of all sub-chunks
-    // are resolved first (shared memory + shuffles only), then every source,
-    // weight and gather load is issued back to back, then reduced in order.
-    uint32_t ad = 0;
-    uint32_t carry = kUnreached;
-    for (uint32_t q0 = 0; q0 < tot; q0 += 32 * kUnroll) {
-      uint32_t eidx[kUnroll], loc[kUnroll], curv[kUnroll], endv[kUnroll], kk[kUnroll];
-      uint32_t adj = ad;
+      // ---- phase B: aligned 8-edge runs, vector loads, masked gathers --------
+      for (uint32_t r0 = 0; r0 < span; r0 += 32 * kLaneEdges) {
+        const uint32_t pos0 = r0 + lane * kLaneEdges;
+        if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
+          const uint32_t q = max(pos0, lo_pos);
+          uint32_t lo = 0, hi = n_ent - 1;  // last entry with pref <= q
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (pref_of[mid] <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          uint32_t ent = lo;
+          uint32_t nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
+          bool att_e = (loc_of[ent] >> 31) != 0;
+          uint32_t eid[kLaneEdges];
+          unsigned live = 0;
 #pragma unroll
-      for (int j = 0; j < kUnroll; ++j) {
-        const uint32_t qj = q0 + 32u * j;
-        kk[j] = 0;
-        eidx[j] = 0xffffffffu;
-        loc[j] = curv[j] = 0;
-        endv[j] = 0;
-        if (qj >= tot) continue;  // warp-uniform
-        const uint32_t wi = adj + lane;
-        ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
-        const uint32_t q = qj + lane;
-        uint32_t k = 0;
+          for (int t = 0; t < kLaneEdges; ++t) {
+            const uint32_t pp = pos0 + t;
+            if (pp >= nxt && pp < span) {  // entries hold >= 1 edge: one step
+              ++ent;
+              nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
+              att_e = (loc_of[ent] >> 31) != 0;
+            }
+            eid[t] = ent;
+            if (pp >= lo_pos && pp < span && att_e) live |= 1u << t;
+          }
+          if (live) {
+            const uint4* sp = reinterpret_cast<const uint4*>(src + ebase + pos0);
+            const uint4 s0 = __ldcs(sp), s1 = __ldcs(sp + 1);
+            uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+            if (A == kSssp) {
+              const uint4* wp = reinterpret_cast<const uint4*>(wts + ebase + pos0);
+              w0 = __ldcs(wp);
+              w1 = __ldcs(wp + 1);
+            }
+            const uint32_t sv_idx[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const uint32_t wv[kLaneEdges] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t sv[kLaneEdges];
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
-          if (b <= q) k += step;
+            for (int t = 0; t < kLaneEdges; ++t)
+              sv[t] = (live >> t & 1u) ? (DET ? __ldg(values_ro + sv_idx[t]) : a.values[sv_idx[t]])
+                                       : kUnreached;
+            uint32_t run_ent = 0xffffffffu, run_best = kUnreached;
+#pragma unroll
+            for (int t = 0; t < kLaneEdges; ++t) {
+              if (!(live >> t & 1u)) continue;
+              if (eid[t] != run_ent) {
+                if (run_ent != 0xffffffffu) atomicMin(best_of + run_ent, run_best);
+                run_ent = eid[t];
+                run_best = kUnreached;
+              }
+              run_best = min(run_best, combine<A>(sv[t], wv[t]));
+            }
+            atomicMin(best_of + run_ent, run_best);
+          }
         }
-        const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
-        const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
-        loc[j] = __shfl_sync(kFull, e.local, k);
-        curv[j] = __shfl_sync(kFull, e.cur, k);
-        uint32_t end = __shfl_sync(kFull, e.pref, (k + 1) & 31);
-        if (k == 31) end = (adj + 32 < n_act) ? act[adj + 32].pref : tot;
-        endv[j] = end;
-        kk[j] = k;
-        if (q < tot) eidx[j] = my_estart + (q - my_pref);
-        const uint32_t k31 = __shfl_sync(kFull, k, 31);
-        const uint32_t e31 = __shfl_sync(kFull, end, 31);
-        adj += (e31 > qj + 32) ? k31 : k31 + 1;
       }
-      uint32_t sv[kUnroll], wv[kUnroll];
-#pragma unroll
-      for (int j = 0; j < kUnroll; ++j) {
-        sv[j] = 0;
-        wv[j] = 0;
-        if (eidx[j] != 0xffffffffu) {
-          sv[j] = __ldcs(src + eidx[j]);
-          if (A == kSssp) wv[j] = __ldcs(wts + eidx[j]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kUnroll; ++j)
-        if (eidx[j] != 0xffffffffu) sv[j] = DET ? __ldg(values_ro + sv[j]) : a.values[sv[j]];
-#pragma unroll
-      for (int j = 0; j < kUnroll; ++j) {
-        const uint32_t qj = q0 + 32u * j;
-        if (qj >= tot) break;  // warp-uniform
-        const uint32_t k = kk[j];
-        const uint32_t q = qj + lane;
-        uint32_t cand = (eidx[j] != 0xffffffffu) ? combine<A>(sv[j], wv[j]) : kUnreached;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t oc = __shfl_up_sync(kFull, cand, off);
-          const uint32_t ok = __shfl_up_sync(kFull, k, off);
-          if (lane >= off && ok == k) cand = min(cand, oc);
-        }
-        if (k == 0) cand = min(cand, carry);
-        const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
-        const bool tail = q < tot && (lane == 31 || q + 1 >= tot || k_down != k);
-        const bool complete = endv[j] <= qj + 32;
-        if (tail && complete && cand < curv[j]) {
-          const uint32_t v = vb + loc[j];
-          if (DET) a.next[v] = cand;
-          else a.values[v] = cand;
+      __syncwarp();
+      // ---- phase C: one lane per attempted destination stores its minimum ---
+      for (uint32_t i = lane; i < n_ent; i += 32) {
+        const uint32_t l = loc_of[i];
+        const uint32_t b = best_of[i];
+        if ((l >> 31) && b < s_cur[warp][i]) {
+          const uint32_t v = vb + (l & 0x7fffffffu);
+          if (DET) a.next[v] = b;
+          else a.values[v] = b;
           a.changed[v] = 1;
           c.valid += 1;
-          lane_min = min(lane_min, cand);
+          lane_min = min(lane_min, b);
         }
-        const uint32_t c31 = __shfl_sync(kFull, cand, 31);
-        const uint32_t e31 = __shfl_sync(kFull, endv[j], 31);
-        carry = (e31 > qj + 32) ? c31 : kUnreached;
       }
-      ad = adj;
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (cur_page != 0xffffffffu) flush_ctr(c, a.ctr + (a.ctr_per_page ? cur_page : 0), lane);
   lane_min = warp_min(lane_min);
