@@ -350,3 +350,38 @@ def test_fixpoint_verifier_detects_violations(engine):
     reached = np.nonzero(bad != ps.kUnreached)[0]
     bad[reached[1:50]] += 1000
     assert engine.verify_fixpoint(ps.AlgoKind.SSSP, bad) > 0
+
+
+# --------------------------------------------------------------------------
+# golden fixtures produced by the reference itself (tests/golden/make_golden.py):
+# the engine consumes the reference-built CSR/CSC page arrays directly
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["rmat_s8_ef16_seed3", "rmat_s10_ef16_seed0",
+                                  "rmat_s12_ef8_seed1"])
+def test_reference_golden_fixtures(engine, name):
+    import os
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz")))
+    n, cap = int(g["n"][0]), int(g["cap"][0])
+    csr = ps.CsrGraph(n, g["csr_off"], g["csr_nbr"], g["csr_w"])
+    local = g["page_local"]
+    npg = (n + cap - 1) // cap
+    in_off = np.zeros(n + 1, np.uint64)
+    base = 0
+    for p in range(npg):
+        vb, ve = p * cap, min((p + 1) * cap, n)
+        loc = local[vb + p: ve + p + 1].astype(np.uint64)
+        in_off[vb:ve + 1] = base + loc
+        base += int(loc[-1])
+    pages = ps.pages_from_csc(n, cap, in_off, g["page_src"], g["page_w"], local)
+    for mode in MODES:
+        for pred in PREDS:
+            for clock in ps.ClockMode:
+                c = cfg_of(mode=mode, pred=pred, clock=clock)
+                r = engine.run_graph(csr, pages, ps.make_bfs(0, n), c)
+                assert np.array_equal(r.values, g["bfs"]), (mode, pred, clock)
+                r = engine.run(ps.make_sssp(0, n, True), c)
+                assert np.array_equal(r.values, g["sssp"]), (mode, pred, clock)
+    sym = ps.EdgeList(n, *O.symmetrize(g["src"], g["dst"], g["w"]))
+    csr2, pages2 = built(sym, cap)
+    r = engine.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=ps.PredictorMode.STRONG))
+    assert np.array_equal(r.values, g["cc"])
