@@ -1,0 +1,154 @@
+// pagestream_seraph.hpp -- C++ drop-in for the reference's hot path.
+//
+// Header-only bridge from the reference's own types
+// (proj/include/pagestream/{graph,programs,engine,metrics}.hpp) to the C-ABI
+// of libseraph.so (include/seraph.h).  A reference build replaces the body of
+// pagestream::run (proj/src/engine.cpp:421-433) with
+//     return pagestream::seraph::run(csr, pages, program, config);
+// and links libseraph.so.  Errors come back as the
+// reference's exception classes (proj/include/pagestream/errors.hpp:8-28).
+#pragma once
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pagestream/engine.hpp"
+#include "pagestream/errors.hpp"
+#include "seraph.h"
+
+namespace pagestream::seraph {
+
+// Map an SR_E_* code onto the reference's exception taxonomy.
+[[noreturn]] inline void rethrow(int rc, const char* msg) {
+  const std::string m = msg ? msg : "libseraph error";
+  switch (rc) {
+    case SR_E_CONFIG: throw ConfigError(m);
+    case SR_E_INPUT: throw InputError(m);
+    case SR_E_CONTRACT: throw ContractError(m);
+    case SR_E_DATA: throw DataError(m);
+    case SR_E_FORMAT: throw FormatError(m);
+    case SR_E_PARSE: throw ParseError(m);
+    default: throw Error(m);
+  }
+}
+
+// One context per device, reused across calls; run() is serialised per
+// device (the reference allows concurrent run() calls, bench.cpp:254-259).
+struct DeviceContext {
+  sr_ctx* ctx = nullptr;
+  std::mutex mu;
+  ~DeviceContext() {
+    if (ctx) sr_close(ctx);
+  }
+};
+
+inline DeviceContext& device_context(int device = 0) {
+  static DeviceContext dc[16];
+  DeviceContext& d = dc[device & 15];
+  std::lock_guard<std::mutex> lk(d.mu);
+  if (!d.ctx) {
+    const int rc = sr_open(device, 0, &d.ctx);
+    if (rc != SR_OK) rethrow(rc, sr_global_error());
+  }
+  return d;
+}
+
+inline sr_run_config to_c(const VertexProgram& program, const EngineConfig& config) {
+  sr_run_config c;
+  sr_default_config(&c);
+  c.algo = int32_t(program.kind);  // AlgoKind: Bfs=0, Cc=1, Sssp=2 (types.hpp:20)
+  c.source = program.source;
+  c.predictor = int32_t(config.predictor);
+  c.schedule = int32_t(config.schedule.kind);
+  c.max_reentry_times = config.schedule.max_reentry_times;
+  c.buffer_repetitions = config.schedule.buffer_repetitions;
+  c.window_capacity = config.window_capacity;
+  c.density_threshold_fraction = config.density_threshold_fraction;
+  c.bytes_per_time_unit = config.transfer.bytes_per_time_unit;
+  c.edges_per_time_unit_per_worker = config.transfer.edges_per_time_unit_per_worker;
+  c.worker_count = config.transfer.worker_count;
+  c.clock = config.clock == ClockMode::Wall ? SR_CLOCK_WALL : SR_CLOCK_VIRTUAL;
+  c.execution = int32_t(config.execution);
+  c.record_trace = config.record_trace ? 1 : 0;
+  c.seed = config.seed;
+  return c;
+}
+
+// pagestream::run (engine.hpp:125-126) executed by libseraph on `device`.
+inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProgram& program,
+                     const EngineConfig& config, int device = 0) {
+  config.validate();  // engine.cpp:422 (ConfigError on the host, as before)
+  if (csr.num_vertices != pages.num_vertices)
+    throw ConfigError("csr and page set disagree on vertex count");
+  if (program.uses_weights() && (!csr.weighted() || !pages.weighted))
+    throw ConfigError("sssp requires weighted graph structures");
+  if (program.kind != AlgoKind::Cc && program.source >= csr.num_vertices)
+    throw ConfigError("source vertex out of range");
+
+  std::vector<sr_page_view> views(pages.pages.size());
+  for (size_t i = 0; i < views.size(); ++i) {
+    const CscPage& p = pages.pages[i];
+    views[i] = sr_page_view{p.vertex_begin, p.vertex_end, p.in_offsets.data(),
+                            p.in_sources.data(),
+                            pages.weighted ? p.in_weights.data() : nullptr, p.edge_count()};
+  }
+  const sr_run_config c = to_c(program, config);
+  RunResult r;
+  r.values.resize(csr.num_vertices);
+  sr_metrics m{};
+  std::vector<sr_pass_stats> passes(256);
+  uint32_t npass = 0;
+  DeviceContext& dc = device_context(device);
+  std::lock_guard<std::mutex> lk(dc.mu);
+  for (;;) {
+    const int rc = sr_run_graph(dc.ctx, csr.num_vertices, csr.num_edges(), csr.out_offsets.data(),
+                                csr.out_neighbors.data(),
+                                csr.weighted() ? csr.out_weights.data() : nullptr,
+                                pages.page_vertex_capacity, pages.weighted ? 1 : 0, views.data(),
+                                uint32_t(views.size()), &c, r.values.data(), nullptr, &m,
+                                passes.data(), uint32_t(passes.size()), &npass);
+    if (rc != SR_OK) rethrow(rc, sr_last_error(dc.ctx));
+    if (npass <= passes.size()) break;
+    passes.resize(npass);  // rerun with room for every pass record
+  }
+  MetricsReport& mr = r.metrics;
+  mr.passes = m.passes;
+  mr.sparse_passes = m.sparse_passes;
+  mr.dense_passes = m.dense_passes;
+  mr.recovery_passes = m.recovery_passes;
+  mr.pages_transferred = m.pages_transferred;
+  mr.bytes_transferred = m.bytes_transferred;
+  mr.update_attempts = m.update_attempts;
+  mr.valid_updates = m.valid_updates;
+  mr.skipped_vertices = m.skipped_vertices;
+  mr.edges_read = m.edges_read;
+  mr.virtual_makespan = m.virtual_makespan;
+  mr.wall_seconds = m.wall_seconds;
+  if (m.has_prediction_accuracy) mr.prediction_accuracy = m.prediction_accuracy;
+  for (uint32_t i = 0; i < npass; ++i) {
+    const sr_pass_stats& s = passes[i];
+    PassStats ps;
+    ps.pass_index = s.pass_index;
+    ps.kind = PassKind(s.kind);
+    ps.attempts = s.attempts;
+    ps.valid_updates = s.valid_updates;
+    ps.skipped = s.skipped;
+    ps.edges_read = s.edges_read;
+    ps.changed_vertices = s.changed_vertices;
+    for (int k = 0; k < 6; ++k) ps.status_counts[k] = s.status_counts[k];
+    ps.has_status_counts = s.has_status_counts != 0;
+    mr.per_pass.push_back(ps);
+  }
+  if (config.record_trace) {
+    uint64_t n = 0;
+    sr_get_trace(dc.ctx, nullptr, 0, &n);
+    std::vector<sr_trace_event> ev(n);
+    sr_get_trace(dc.ctx, ev.data(), n, &n);
+    for (const auto& e : ev)
+      r.trace.push_back(TraceEvent{e.time, TraceEventKind(e.kind), e.page_id, e.pass_index});
+  }
+  return r;
+}
+
+}  // namespace pagestream::seraph

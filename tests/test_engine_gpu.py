@@ -385,3 +385,17 @@ def test_reference_golden_fixtures(engine, name):
     csr2, pages2 = built(sym, cap)
     r = engine.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=ps.PredictorMode.STRONG))
     assert np.array_equal(r.values, g["cc"])
+
+
+def test_cpp_dropin_bridge_against_reference_run():
+    """oracle/_ref/bridge_check: the reference's own run() vs the C++ drop-in
+    pagestream::seraph::run on identical reference-built objects."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref",
+                       "bridge_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/bridge_check not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "0 failures" in out.stdout
