@@ -232,6 +232,9 @@ int sr_host_alloc(uint64_t bytes, void** out);
 void sr_host_free(void* p);
 /* cudaDeviceSynchronize on `device` (bench bracketing without torch). */
 int sr_device_sync(int device);
+/* Host-link roofline denominator: pinned host -> device cudaMemcpyAsync of
+ * `bytes`, best of `reps`, timed with CUDA events (GB/s = 1e9 B/s). */
+int sr_bench_h2d(int device, uint64_t bytes, uint32_t reps, double* gbps);
 
 /* ---- multi-GPU (one process per GPU) ----------------------------------- */
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the host. */

@@ -156,7 +156,14 @@ int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const
     ctx->eng->last_upload_seconds = 0;
     ctx->eng->last_upload_bytes = 0;
     const bool weighted = weighted_pages != 0;
-    ctx->eng->load_csr(n, m, off, nbr, w);
+    // Resident page set on one device: upload only the CSR offsets and derive
+    // the push adjacency on the device (half the bytes over the host link).
+    uint64_t page_bytes = 0;
+    for (uint32_t i = 0; i < np; ++i)
+      page_bytes += (uint64_t(pages[i].vertex_end - pages[i].vertex_begin) + 1 +
+                     pages[i].edge_count * (weighted ? 2 : 1)) * 4;
+    const bool derive = ctx->eng->world() == 1 && ctx->eng->fits_budget(page_bytes);
+    ctx->eng->load_csr(n, m, off, derive ? nullptr : nbr, derive ? nullptr : w);
     ctx->eng->load_pages(n, cap, weighted, pages, np);
     const double up = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     sr_metrics mm{};
@@ -219,6 +226,37 @@ int sr_device_sync(int device) {
   return guard(nullptr, [&] {
     SR_CUDA(cudaSetDevice(device));
     SR_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+int sr_bench_h2d(int device, uint64_t bytes, uint32_t reps, double* gbps) {
+  return guard(nullptr, [&] {
+    if (!gbps || !bytes) throw seraph::EngineError(SR_E_CONFIG, "bad arguments");
+    SR_CUDA(cudaSetDevice(device));
+    seraph::PinBuf<uint8_t> h;
+    seraph::DBuf<uint8_t> d;
+    h.reserve(bytes);
+    d.reserve(bytes);
+    std::memset(h.p, 1, bytes);
+    cudaStream_t st;
+    cudaEvent_t a, b;
+    SR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SR_CUDA(cudaEventCreate(&a));
+    SR_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (uint32_t r = 0; r < reps + 1; ++r) {
+      SR_CUDA(cudaEventRecord(a, st));
+      SR_CUDA(cudaMemcpyAsync(d.p, h.p, bytes, cudaMemcpyHostToDevice, st));
+      SR_CUDA(cudaEventRecord(b, st));
+      SR_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      SR_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (r > 0 && ms < best) best = ms;  // first copy warms the path
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    *gbps = double(bytes) / (double(best) * 1e-3) / 1e9;
   });
 }
 

@@ -91,6 +91,7 @@ struct PullArgs {
 };
 
 struct PrArgs {
+  unsigned* work;  // per-launch tile counter
   const uint4* tiles;
   const uint32_t* tile_page;
   const PageDesc* pages;

@@ -139,11 +139,42 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   } else if (nbr && w) {
     csr_weighted_ = true;  // weighted graph without edges
   }
+  const size_t npad = (size_t(n) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
+  outdeg_.reserve(npad);
+  SR_CUDA(cudaMemsetAsync(outdeg_.p, 0, npad * 4, xs_));
+  launch_outdeg(out_off_.p, n, outdeg_.p, xs_);
   SR_CUDA(cudaStreamSynchronize(xs_));
   has_csr_ = true;
+  csr_derived_ = false;
   last_upload_bytes += bytes;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Engine::maybe_derive_csr() {
+  // sr_load_csr without out_neighbors + a resident page set: build the push
+  // adjacency on the device instead of shipping it over the host link.
+  if (!has_csr_ || has_csr_edges_ || !pages_loaded_ || !all_resident_ || world_ > 1) return;
+  if (n_ != page_n_ || m_ != page_edges_total_) return;
+  if (m_ == 0) {
+    has_csr_edges_ = true;
+    csr_weighted_ = weighted_;
+    csr_derived_ = true;
+    return;
+  }
+  out_nbr_.reserve(m_);
+  if (weighted_) out_w_.reserve(m_);
+  DBuf<uint32_t> cursor;
+  cursor.reserve(n_);
+  SR_CUDA(cudaMemsetAsync(cursor.p, 0, size_t(n_) * 4, xs_));
+  const uint32_t n_tiles = uint32_t(tiles_.n ? pages_.back().tile_end : 0);
+  launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, n_tiles, out_off_.p, cursor.p,
+                        out_nbr_.p, weighted_ ? out_w_.p : nullptr, sm_count_ * 8, xs_);
+  SR_CUDA(cudaGetLastError());
+  SR_CUDA(cudaStreamSynchronize(xs_));
+  has_csr_edges_ = true;
+  csr_weighted_ = weighted_;
+  csr_derived_ = true;
 }
 
 void Engine::build_tiles(uint32_t lo, uint32_t hi) {
@@ -372,6 +403,10 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     SR_CUDA(cudaMemcpy(page_desc_.p, page_desc_h_.data(), np * sizeof(PageDesc),
                        cudaMemcpyHostToDevice));
   pages_loaded_ = true;
+  if (csr_derived_) {  // the derived adjacency belonged to the previous page set
+    has_csr_edges_ = false;
+    csr_derived_ = false;
+  }
   last_upload_bytes += upload;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -491,6 +526,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
     grid = std::max(grid, 1);
     if (pagerank) {
       PrArgs a{};
+      a.work = next_work_counter();
       a.tiles = tiles_.p;
       a.tile_page = tile_page_.p;
       a.pages = page_desc_.p;
@@ -879,7 +915,7 @@ void Engine::census(int pass_kind) {
   SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
   launch_census(n_, changed_.p, predictor_ == SR_PRED_WEAK ? status_.p : nullptr,
                 predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr,
-                has_csr_ ? out_off_.p : nullptr, pass_kind, own_lo_, own_hi_, blk_cnt_.p,
+                has_csr_ ? outdeg_.p : nullptr, pass_kind, own_lo_, own_hi_, blk_cnt_.p,
                 blk_edges_.p, census_.p, cs_);
 }
 
@@ -894,7 +930,7 @@ void Engine::read_census() {
 void Engine::build_push_list() {
   const uint32_t nb = (n_ + kCensusBlockVerts - 1) / kCensusBlockVerts;
   launch_scan_blocks(nb, blk_cnt_.p, blk_edges_.p, cs_);
-  launch_compact(n_, own_lo_, own_hi_, changed_.p, out_off_.p, blk_cnt_.p, blk_edges_.p,
+  launch_compact(n_, own_lo_, own_hi_, changed_.p, outdeg_.p, blk_cnt_.p, blk_edges_.p,
                  list_.p, pref_.p, chunk_start_.p, cs_);
 }
 
@@ -959,6 +995,7 @@ void Engine::exchange_round(bool pagerank) {
 void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out,
                  sr_metrics& m, std::vector<sr_pass_stats>& passes) {
   SR_CUDA(cudaSetDevice(dev_));
+  maybe_derive_csr();
   validate(cfg);
   algo_ = cfg.algo;
   source_ = cfg.source;

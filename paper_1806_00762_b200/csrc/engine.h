@@ -119,6 +119,9 @@ class Engine {
   void load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* pages,
                   uint32_t np);
   uint64_t page_bytes_total() const { return page_bytes_total_; }
+  // True when a page set of `bytes` would be held resident (no streaming).
+  bool fits_budget(uint64_t bytes) const { return budget_ == 0 || bytes <= budget_; }
+  int world() const { return world_; }
   void run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out, sr_metrics& m,
            std::vector<sr_pass_stats>& passes);
   uint64_t verify_fixpoint(int algo, const uint32_t* values_host);
@@ -175,6 +178,9 @@ class Engine {
   bool has_csr_ = false, has_csr_edges_ = false, csr_weighted_ = false;
   DBuf<unsigned long long> out_off_;
   DBuf<uint32_t> out_nbr_, out_w_;
+  DBuf<uint32_t> outdeg_;  // u32 out-degrees (census/compaction vector loads)
+  void maybe_derive_csr();  // push adjacency = transpose of resident pages
+  bool csr_derived_ = false;
 
   // pages
   bool pages_loaded_ = false;

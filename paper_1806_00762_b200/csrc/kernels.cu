@@ -332,6 +332,97 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
   if (lane == 0 && lane_min != kUnreached) atomicMin(&a.census->min_changed, lane_min);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side CSR adjacency from the resident CSC pages (§8(f) row 1): every
+// in-edge (src -> v, w) of every page is scattered to out_off[src] + a
+// per-source cursor.  Same tile walk as K1 (aligned 8-edge runs per lane).
+// Order inside an adjacency list is arbitrary; the push kernel and the
+// fixpoint are order-independent (SURVEY §7 "Asynchronous semantics").
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlockThreads)
+csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
+                      const PageDesc* __restrict__ pages, uint32_t n_tiles,
+                      const unsigned long long* __restrict__ out_off, uint32_t* cursor,
+                      uint32_t* out_nbr, uint32_t* out_w) {
+  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t ti = blockIdx.x * kWarpsPerBlock + warp; ti < n_tiles;
+       ti += gridDim.x * kWarpsPerBlock) {
+    const PageDesc pd = pages[tile_page[ti]];
+    const uint4 tile = tiles[ti];
+    const uint32_t* __restrict__ src = pd.src;
+    const uint32_t* __restrict__ wts = pd.w;
+    if (tile.w & kHubFlag) {
+      const uint32_t v = pd.vertex_begin + tile.z;
+      for (uint32_t e = tile.x + lane; e < tile.y; e += 32) {
+        const uint32_t s = src[e];
+        const unsigned long long pos = out_off[s] + atomicAdd(cursor + s, 1u);
+        out_nbr[pos] = v;
+        if (out_w) out_w[pos] = wts[e];
+      }
+      continue;
+    }
+    const uint32_t dl = tile.z, dh = tile.w;
+    const uint32_t ebase = tile.x & ~7u;
+    uint32_t n_ent = 0;
+    for (uint32_t base = dl; base < dh; base += 32) {
+      const uint32_t i = base + lane;
+      uint32_t lo = 0, deg = 0;
+      if (i < dh) {
+        lo = pd.offs[i];
+        deg = pd.offs[i + 1] - lo;
+      }
+      const unsigned m = __ballot_sync(kFull, deg > 0);
+      if (deg > 0) {
+        const uint32_t pos = n_ent + __popc(m & lanemask_lt());
+        s_pref[warp][pos] = lo - ebase;
+        s_loc[warp][pos] = i;
+      }
+      n_ent += __popc(m);
+    }
+    __syncwarp();
+    const uint32_t lo_pos = tile.x - ebase, span = tile.y - ebase;
+    for (uint32_t r0 = 0; n_ent && r0 < span; r0 += 32 * kLaneEdges) {
+      const uint32_t pos0 = r0 + lane * kLaneEdges;
+      if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
+        const uint32_t q = max(pos0, lo_pos);
+        uint32_t lo = 0, hi = n_ent - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_pref[warp][mid] <= q) lo = mid;
+          else hi = mid - 1;
+        }
+        uint32_t ent = lo;
+        uint32_t nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+#pragma unroll
+        for (int t = 0; t < kLaneEdges; ++t) {
+          const uint32_t pp = pos0 + t;
+          if (pp >= span) break;
+          if (pp >= nxt) {
+            ++ent;
+            nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+          }
+          if (pp < lo_pos) continue;
+          const uint32_t e = ebase + pp;
+          const uint32_t s = src[e];
+          const unsigned long long pos = out_off[s] + atomicAdd(cursor + s, 1u);
+          out_nbr[pos] = pd.vertex_begin + s_loc[warp][ent];
+          if (out_w) out_w[pos] = wts[e];
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void outdeg_kernel(const unsigned long long* __restrict__ off, uint32_t n,
+                              uint32_t* deg) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    deg[v] = (uint32_t)(off[v + 1] - off[v]);
+}
+
 __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __restrict__ next,
                               uint32_t lo, uint32_t hi) {
   for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi;
@@ -340,131 +431,145 @@ __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __r
 }
 
 // ---------------------------------------------------------------------------
-// K8: PageRank pull-sum (Jacobi; contrib_in is read-only in the launch).
+// K8: PageRank pull-sum (Jacobi: contrib_in is read-only in the launch).
+// Same tile walk as K1: entries per destination, aligned 8-edge lane runs
+// with uint4 source loads, gathers of contrib[src], per-lane fold and a
+// shared-memory float atomicAdd merge; hub chunks go through hub_sum.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
-  __shared__ ActEntry s_act[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
+  __shared__ float s_sum[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  ActEntry* act = s_act[warp];
-  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
-  const uint32_t nw = gridDim.x * kWarpsPerBlock;
+  float* sum_of = s_sum[warp];
   const uint32_t total = a.seg.task_prefix[a.seg.n];
-  const uint32_t t_begin = (uint32_t)(((unsigned long long)total * gw) / nw);
-  const uint32_t t_end = (uint32_t)(((unsigned long long)total * (gw + 1)) / nw);
   LaneCtr c;
   c.clear();
   uint32_t cur_page = 0xffffffffu;
   PageDesc pd{};
   const float* __restrict__ contrib = a.contrib_in;
 
-  for (uint32_t t = t_begin; t < t_end; ++t) {
-    const uint32_t ti = task_to_tile(a.seg, t);
-    const uint32_t p = a.tile_page[ti];
-    if (p != cur_page) {
-      cur_page = p;
-      pd = a.pages[p];
-    }
-    const uint4 tile = a.tiles[ti];
-    const uint32_t vb = pd.vertex_begin;
-    const uint32_t* __restrict__ offs = pd.offs;
-    const uint32_t* __restrict__ src = pd.src;
-    if (tile.w & kHubFlag) {
-      const uint32_t d = tile.z;
-      const uint32_t lo_d = offs[d];
-      if (lane == 0 && tile.x == lo_d) {
-        c.attempts += 1;
-        c.edges += offs[d + 1] - lo_d;
+  for (;;) {
+    uint32_t t0 = 0;
+    if (lane == 0) t0 = atomicAdd(a.work, kGrab);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= total) break;
+    const uint32_t t1 = min(t0 + kGrab, total);
+    for (uint32_t t = t0; t < t1; ++t) {
+      const uint32_t ti = task_to_tile(a.seg, t);
+      const uint32_t p = a.tile_page[ti];
+      if (p != cur_page) {
+        cur_page = p;
+        pd = a.pages[p];
       }
-      float sum = 0.f;
-      uint32_t e = tile.x + lane;
-#pragma unroll 4
-      for (; e < tile.y; e += 32) sum += __ldg(contrib + src[e]);
-      sum = warp_sum(sum);
-      if (lane == 0) atomicAdd(a.hub_sum + (tile.w & ~kHubFlag), sum);
-      continue;
-    }
-    const uint32_t dl = tile.z, dh = tile.w;
-    uint32_t n_act = 0, tot = 0;
-    for (uint32_t base = dl; base < dh; base += 32) {
-      const uint32_t i = base + lane;
-      const bool in = i < dh;
-      uint32_t lo = 0, deg = 0;
-      if (in) {
-        lo = offs[i];
-        deg = offs[i + 1] - lo;
-        if (deg == 0) {  // no in-edges: teleport share only
-          const uint32_t v = vb + i;
-          a.rank_out[v] = a.base;
-          a.contrib_out[v] = a.base * a.inv_outdeg[v];
+      const uint4 tile = a.tiles[ti];
+      const uint32_t vb = pd.vertex_begin;
+      const uint32_t* __restrict__ offs = pd.offs;
+      const uint32_t* __restrict__ src = pd.src;
+      if (tile.w & kHubFlag) {
+        const uint32_t d = tile.z;
+        const uint32_t lo_d = offs[d];
+        if (lane == 0 && tile.x == lo_d) {
+          c.attempts += 1;
+          c.edges += offs[d + 1] - lo_d;
+        }
+        float sum = 0.f;
+        uint32_t e = tile.x + lane;
+#pragma unroll 8
+        for (; e < tile.y; e += 32) sum += __ldg(contrib + __ldcs(src + e));
+        sum = warp_sum(sum);
+        if (lane == 0) atomicAdd(a.hub_sum + (tile.w & ~kHubFlag), sum);
+        continue;
+      }
+      const uint32_t dl = tile.z, dh = tile.w;
+      const uint32_t ebase = tile.x & ~7u;
+      uint32_t n_ent = 0;
+      for (uint32_t base = dl; base < dh; base += 32) {
+        const uint32_t i = base + lane;
+        const bool in = i < dh;
+        uint32_t lo = 0, deg = 0;
+        if (in) {
+          lo = __ldcs(offs + i);
+          deg = __ldcs(offs + i + 1) - lo;
+          if (deg == 0) {  // no in-edges: teleport share only
+            const uint32_t v = vb + i;
+            a.rank_out[v] = a.base;
+            a.contrib_out[v] = a.base * a.inv_outdeg[v];
+          }
+        }
+        c.attempts += in;
+        c.edges += deg;
+        const unsigned m = __ballot_sync(kFull, deg > 0);
+        if (deg > 0) {
+          const uint32_t pos = n_ent + __popc(m & lanemask_lt());
+          s_pref[warp][pos] = lo - ebase;
+          s_loc[warp][pos] = i;
+          sum_of[pos] = 0.f;
+        }
+        n_ent += __popc(m);
+      }
+      __syncwarp();
+      if (n_ent == 0) {
+        __syncwarp();
+        continue;
+      }
+      const uint32_t lo_pos = tile.x - ebase, span = tile.y - ebase;
+      for (uint32_t r0 = 0; r0 < span; r0 += 32 * kLaneEdges) {
+        const uint32_t pos0 = r0 + lane * kLaneEdges;
+        if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
+          const uint32_t q = max(pos0, lo_pos);
+          uint32_t lo = 0, hi = n_ent - 1;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (s_pref[warp][mid] <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          uint32_t ent = lo;
+          uint32_t nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+          uint32_t eid[kLaneEdges];
+          unsigned live = 0;
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t) {
+            const uint32_t pp = pos0 + t;
+            if (pp >= nxt && pp < span) {
+              ++ent;
+              nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+            }
+            eid[t] = ent;
+            if (pp >= lo_pos && pp < span) live |= 1u << t;
+          }
+          const uint4* sp = reinterpret_cast<const uint4*>(src + ebase + pos0);
+          const uint4 s0 = __ldcs(sp), s1 = __ldcs(sp + 1);
+          const uint32_t sidx[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          float x[kLaneEdges];
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t)
+            x[t] = (live >> t & 1u) ? __ldg(contrib + sidx[t]) : 0.f;
+          uint32_t run_ent = 0xffffffffu;
+          float run = 0.f;
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t) {
+            if (!(live >> t & 1u)) continue;
+            if (eid[t] != run_ent) {
+              if (run_ent != 0xffffffffu) atomicAdd(sum_of + run_ent, run);
+              run_ent = eid[t];
+              run = 0.f;
+            }
+            run += x[t];
+          }
+          if (run_ent != 0xffffffffu) atomicAdd(sum_of + run_ent, run);
         }
       }
-      c.attempts += in;
-      c.edges += deg;
-      const bool live = deg > 0;
-      const uint32_t incl = warp_incl_scan(deg, lane);
-      const unsigned m = __ballot_sync(kFull, live);
-      if (live) {
-        const uint32_t pos = n_act + __popc(m & lanemask_lt());
-        act[pos] = ActEntry{i, lo, tot + incl - deg, 0u};
-      }
-      n_act += __popc(m);
-      tot += __shfl_sync(kFull, incl, 31);
-    }
-    __syncwarp();
-    if (n_act == 0) {
       __syncwarp();
-      continue;
-    }
-    uint32_t ad = 0;
-    float carry = 0.f;
-    for (uint32_t q0 = 0; q0 < tot; q0 += 32) {
-      const uint32_t wi = ad + lane;
-      ActEntry e = (wi < n_act) ? act[wi] : ActEntry{0u, 0u, tot, 0u};
-      const uint32_t q = q0 + lane;
-      const bool qv = q < tot;
-      uint32_t k = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t b = __shfl_sync(kFull, e.pref, k + step);
-        if (b <= q) k += step;
-      }
-      const uint32_t my_local = __shfl_sync(kFull, e.local, k);
-      const uint32_t my_estart = __shfl_sync(kFull, e.estart, k);
-      const uint32_t my_pref = __shfl_sync(kFull, e.pref, k);
-      const uint32_t nxt_pref = __shfl_sync(kFull, e.pref, (k + 1) & 31);
-      float x = 0.f;
-      if (qv) x = __ldg(contrib + src[my_estart + (q - my_pref)]);
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float ox = __shfl_up_sync(kFull, x, off);
-        const uint32_t ok = __shfl_up_sync(kFull, k, off);
-        if (lane >= off && ok == k) x += ox;
-      }
-      if (k == 0) x += carry;
-      uint32_t end = nxt_pref;
-      if (k == 31) end = (ad + 32 < n_act) ? act[ad + 32].pref : tot;
-      const uint32_t k_down = __shfl_down_sync(kFull, k, 1);
-      const bool tail = qv && (lane == 31 || q + 1 >= tot || k_down != k);
-      const bool complete = end <= q0 + 32;
-      if (tail && complete) {
-        const uint32_t v = vb + my_local;
-        const float r = a.base + a.damp * x;
+      for (uint32_t i = lane; i < n_ent; i += 32) {
+        const uint32_t v = vb + s_loc[warp][i];
+        const float r = a.base + a.damp * sum_of[i];
         a.rank_out[v] = r;
         a.contrib_out[v] = r * a.inv_outdeg[v];
       }
-      const uint32_t k31 = __shfl_sync(kFull, k, 31);
-      const float x31 = __shfl_sync(kFull, x, 31);
-      const uint32_t e31 = __shfl_sync(kFull, end, 31);
-      if (e31 > q0 + 32) {
-        ad += k31;
-        carry = x31;
-      } else {
-        ad += k31 + 1;
-        carry = 0.f;
-      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   flush_ctr(c, a.ctr, lane);
 }
@@ -633,7 +738,7 @@ __device__ __forceinline__ uint8_t log_attempt(uint8_t ls, bool changed,
 
 __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
                                                      uint8_t* status, uint8_t* logstate,
-                                                     const unsigned long long* __restrict__ out_off,
+                                                     const uint32_t* __restrict__ outdeg,
                                                      int pass_kind, uint32_t own_lo, uint32_t own_hi,
                                                      uint32_t* blk_cnt,
                                                      unsigned long long* blk_edges, Census* cz) {
@@ -648,6 +753,21 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
   if (v0 < n) {
     uint4 cw = *reinterpret_cast<const uint4*>(changed + v0);
     const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
+    uint32_t dg[16];
+    if (outdeg && (cw.x | cw.y | cw.z | cw.w)) {
+      const uint4* dp = reinterpret_cast<const uint4*>(outdeg + v0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 d4 = dp[k];
+        dg[4 * k] = d4.x;
+        dg[4 * k + 1] = d4.y;
+        dg[4 * k + 2] = d4.z;
+        dg[4 * k + 3] = d4.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) dg[k] = 0;
+    }
     uint4 sw{}, lw{};
     if (status) sw = *reinterpret_cast<const uint4*>(status + v0);
     if (logstate) lw = *reinterpret_cast<const uint4*>(logstate + v0);
@@ -660,7 +780,7 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
       const bool ch = cb[j] != 0;
       if (ch) {
         ++n_changed;
-        const unsigned long long d = out_off ? out_off[v + 1] - out_off[v] : 0ull;
+        const unsigned long long d = dg[j];
         edges += d;
         n_push += d > 0;
         if (v >= own_lo && v < own_hi) {
@@ -784,7 +904,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t
 // the changed flags for the next pass.
 __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_lo, uint32_t own_hi,
                                                       uint8_t* changed,
-                                                      const unsigned long long* __restrict__ out_off,
+                                                      const uint32_t* __restrict__ outdeg,
                                                       const uint32_t* __restrict__ blk_off,
                                                       const unsigned long long* __restrict__ blk_eoff,
                                                       uint32_t* list, unsigned long long* pref,
@@ -804,7 +924,7 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_l
     deg[j] = 0;
     const uint32_t v = v0 + j;
     if (v < n && cb[j] && v >= own_lo && v < own_hi) {
-      deg[j] = out_off[v + 1] - out_off[v];
+      deg[j] = outdeg[v];
       cnt += deg[j] > 0;
       edges += deg[j];
     }
@@ -1052,7 +1172,7 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
 }
 
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
-                   const unsigned long long* out_offsets, int pass_kind, uint32_t own_lo,
+                   const uint32_t* out_offsets, int pass_kind, uint32_t own_lo,
                    uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
                    cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
@@ -1068,7 +1188,7 @@ void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long*
 }
 
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
-                    const unsigned long long* out_offsets, const uint32_t* blk_off,
+                    const uint32_t* out_offsets, const uint32_t* blk_off,
                     const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
                     uint32_t* chunk_start, cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
@@ -1084,6 +1204,19 @@ void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* 
   cc_delta_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
   cc_min_kernel<<<g, 256, 0, s>>>(n, values, snap, delta, c);
   cc_reset_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
+}
+
+void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
+                           uint32_t n_tiles, const unsigned long long* out_off, uint32_t* cursor,
+                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s) {
+  if (!n_tiles) return;
+  csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, n_tiles, out_off,
+                                                       cursor, out_nbr, out_w);
+}
+
+void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s) {
+  if (!n) return;
+  outdeg_kernel<<<grid_for(n, 256), 256, 0, s>>>(off, n, deg);
 }
 
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values, cudaStream_t s) {

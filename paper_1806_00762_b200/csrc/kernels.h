@@ -31,13 +31,13 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
 // K4/K5: per-pass census (+ weak DFA step, prediction log, status histogram).
 constexpr uint32_t kCensusBlockVerts = 4096;
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
-                   const unsigned long long* out_offsets, int pass_kind, uint32_t own_lo,
+                   const uint32_t* outdeg, int pass_kind, uint32_t own_lo,
                    uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
                    cudaStream_t s);
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
                         cudaStream_t s);
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
-                    const unsigned long long* out_offsets, const uint32_t* blk_off,
+                    const uint32_t* outdeg, const uint32_t* blk_off,
                     const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
                     uint32_t* chunk_start, cudaStream_t s);
 // Multi-GPU: flag vertices improved by any rank during the round.
@@ -49,6 +49,11 @@ void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, cons
 // K6: strong CC threshold (net label-population change since the last refresh).
 void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* delta,
                        Census* c, cudaStream_t s);
+// Device-side CSR adjacency from resident CSC pages; out-degrees (u32).
+void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
+                           uint32_t n_tiles, const unsigned long long* out_off, uint32_t* cursor,
+                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s);
+void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s);
 // Values initialisation (VertexProgram::init, programs.hpp:20-28).
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
                         cudaStream_t s);

@@ -399,3 +399,21 @@ def test_cpp_dropin_bridge_against_reference_run():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "0 failures" in out.stdout
+
+
+def test_csr_offsets_only_derives_push_adjacency():
+    """sr_load_csr without out_neighbors: the push adjacency is built on the device
+    from the resident pages (device-side graph build)."""
+    n = 1 << 12
+    src, dst = O.generate_rmat(12, 16, seed=8)
+    w = O.assign_weights(src.size, 2, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 16)
+    with ps.Engine(0) as eng:
+        eng.load_pages(pages)
+        eng.load_csr(csr, with_edges=False)
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+            for ex in ps.ExecutionPolicy:
+                r = eng.run(program_for(kind, 0, el), cfg_of(clock=ps.ClockMode.WALL, execution=ex))
+                assert np.array_equal(r.values, oracle_values(el, kind, 0)), (kind, ex)
+        assert eng.verify_fixpoint(ps.AlgoKind.SSSP, oracle_values(el, ps.AlgoKind.SSSP, 0)) == 0
