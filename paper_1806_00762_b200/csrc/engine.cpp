@@ -88,6 +88,7 @@ Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
   SR_CUDA(cudaEventCreate(&ev_start_));
   SR_CUDA(cudaEventCreate(&ev_stop_));
   SR_CUDA(cudaEventCreateWithFlags(&ev_step_, cudaEventDisableTiming));
+  SR_CUDA(cudaEventCreateWithFlags(&ev_tiles_, cudaEventDisableTiming));
   blocks_per_sm_ = pull_blocks_per_sm(kSssp, kGateOff, false);
   census_.reserve(1);
   census_h_.reserve(1);
@@ -96,6 +97,7 @@ Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
 Engine::~Engine() {
   cudaSetDevice(dev_);
   if (comm_) nccl().CommDestroy(comm_);
+  for (cudaEvent_t e : page_events_) cudaEventDestroy(e);
   for (auto& s : slots_) {
     if (s.ready) cudaEventDestroy(s.ready);
     if (s.freed) cudaEventDestroy(s.freed);
@@ -105,6 +107,7 @@ Engine::~Engine() {
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (ev_stop_) cudaEventDestroy(ev_stop_);
   if (ev_step_) cudaEventDestroy(ev_step_);
+  if (ev_tiles_) cudaEventDestroy(ev_tiles_);
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
 }
@@ -164,20 +167,19 @@ void Engine::maybe_derive_csr() {
   }
   out_nbr_.reserve(m_);
   if (weighted_) out_w_.reserve(m_);
-  DBuf<uint32_t> cursor;
-  cursor.reserve(n_);
-  SR_CUDA(cudaMemsetAsync(cursor.p, 0, size_t(n_) * 4, xs_));
-  const uint32_t n_tiles = uint32_t(tiles_.n ? pages_.back().tile_end : 0);
-  launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, n_tiles, out_off_.p, cursor.p,
-                        out_nbr_.p, weighted_ ? out_w_.p : nullptr, sm_count_ * 8, xs_);
+  csr_cursor_.reserve(n_);
+  SR_CUDA(cudaMemsetAsync(csr_cursor_.p, 0, size_t(n_) * 4, cs_));
+  for (const PageMeta& pm : pages_)
+    launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, pm.tile_begin, pm.tile_end,
+                          out_off_.p, csr_cursor_.p, out_nbr_.p, weighted_ ? out_w_.p : nullptr,
+                          sm_count_ * 8, cs_);
   SR_CUDA(cudaGetLastError());
-  SR_CUDA(cudaStreamSynchronize(xs_));
   has_csr_edges_ = true;
   csr_weighted_ = weighted_;
   csr_derived_ = true;
 }
 
-void Engine::build_tiles(uint32_t lo, uint32_t hi) {
+void Engine::build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st) {
   // Jobs of at most 1M destinations so big pages cut in parallel.
   std::vector<TileJob> jobs;
   const uint32_t np = uint32_t(pages_.size());
@@ -192,45 +194,45 @@ void Engine::build_tiles(uint32_t lo, uint32_t hi) {
     const PageMeta& pm = pages_[jobs[j].page];
     cut_tiles(pm.h_offs, pm.vb, jobs[j]);
   });
-  std::vector<uint4> tiles;
-  std::vector<uint32_t> tile_page;
   hub_vertex_h_.clear();
   for (auto& pm : pages_) pm.tile_begin = pm.tile_end = 0;
   size_t total = 0;
   for (auto& j : jobs) total += j.tiles.size();
   if (total >= (1ull << 32)) throw EngineError(SR_E_CONFIG, "graph too large: tile count");
-  tiles.reserve(total);
-  tile_page.reserve(total);
+  tile_stage_.reserve(std::max<size_t>(total, 1));
+  tile_page_stage_.reserve(std::max<size_t>(total, 1));
+  size_t at = 0;
   for (auto& j : jobs) {
     PageMeta& pm = pages_[j.page];
-    if (pm.tile_end == 0 && pm.tile_begin == 0) pm.tile_begin = uint32_t(tiles.size());
+    if (pm.tile_end == 0 && pm.tile_begin == 0) pm.tile_begin = uint32_t(at);
     const uint32_t hub_base = uint32_t(hub_vertex_h_.size());
     for (uint4 t : j.tiles) {
       if (t.w & kHubFlag) t.w = kHubFlag | ((t.w & ~kHubFlag) + hub_base);
-      tiles.push_back(t);
-      tile_page.push_back(j.page);
+      tile_stage_.p[at] = t;
+      tile_page_stage_.p[at] = j.page;
+      ++at;
     }
     hub_vertex_h_.insert(hub_vertex_h_.end(), j.hubs.begin(), j.hubs.end());
-    pm.tile_end = uint32_t(tiles.size());
+    pm.tile_end = uint32_t(at);
   }
   n_hubs_ = uint32_t(hub_vertex_h_.size());
-  tiles_.reserve(std::max<size_t>(tiles.size(), 1));
-  tile_page_.reserve(std::max<size_t>(tiles.size(), 1));
-  if (!tiles.empty()) {
-    SR_CUDA(cudaMemcpyAsync(tiles_.p, tiles.data(), tiles.size() * 16, cudaMemcpyHostToDevice, xs_));
-    SR_CUDA(cudaMemcpyAsync(tile_page_.p, tile_page.data(), tile_page.size() * 4,
-                            cudaMemcpyHostToDevice, xs_));
+  tiles_.reserve(std::max<size_t>(total, 1));
+  tile_page_.reserve(std::max<size_t>(total, 1));
+  if (total) {
+    SR_CUDA(cudaMemcpyAsync(tiles_.p, tile_stage_.p, total * 16, cudaMemcpyHostToDevice, st));
+    SR_CUDA(cudaMemcpyAsync(tile_page_.p, tile_page_stage_.p, total * 4, cudaMemcpyHostToDevice,
+                            st));
   }
   hub_vertex_.reserve(std::max<uint32_t>(n_hubs_, 1));
   hub_stamp_.reserve(std::max<uint32_t>(n_hubs_, 1));
   hub_sum_.reserve(std::max<uint32_t>(n_hubs_, 1));
   if (n_hubs_) {
-    SR_CUDA(cudaMemcpyAsync(hub_vertex_.p, hub_vertex_h_.data(), n_hubs_ * 4,
-                            cudaMemcpyHostToDevice, xs_));
-    SR_CUDA(cudaMemsetAsync(hub_stamp_.p, 0, n_hubs_ * 4, xs_));
-    SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, xs_));
+    hub_stage_.reserve(n_hubs_);
+    std::memcpy(hub_stage_.p, hub_vertex_h_.data(), n_hubs_ * 4);
+    SR_CUDA(cudaMemcpyAsync(hub_vertex_.p, hub_stage_.p, n_hubs_ * 4, cudaMemcpyHostToDevice, st));
+    SR_CUDA(cudaMemsetAsync(hub_stamp_.p, 0, n_hubs_ * 4, st));
+    SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, st));
   }
-  SR_CUDA(cudaStreamSynchronize(xs_));
   run_id_ = 0;
 }
 
@@ -302,15 +304,11 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     own_hi_ = cut_at(before[np] * uint64_t(rank_ + 1) / uint64_t(world_));
     if (rank_ == world_ - 1) own_hi_ = n;
   }
-  build_tiles(own_lo_, own_hi_);
-
   // ---- residency: the whole (owned) page set in HBM when it fits ----
   uint64_t used_bytes = 0;
   std::vector<char> used(np, 0);
   for (uint32_t p = 0; p < np; ++p) {
-    used[p] = pages_[p].tile_end > pages_[p].tile_begin || (pages_[p].ve > pages_[p].vb &&
-                                                            pages_[p].vb < own_hi_ &&
-                                                            pages_[p].ve > own_lo_);
+    used[p] = pages_[p].vb < own_hi_ && pages_[p].ve > own_lo_;
     if (used[p]) used_bytes += pages_[p].bytes;
   }
   all_resident_ = budget_ == 0 || used_bytes <= budget_;
@@ -321,6 +319,11 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
   page_desc_h_.assign(np, PageDesc{});
+  for (uint32_t p = 0; p < np; ++p) {
+    page_desc_h_[p].vertex_begin = pages_[p].vb;
+    page_desc_h_[p].range = pages_[p].ve - pages_[p].vb;
+    page_desc_h_[p].edge_count = pages_[p].edges;
+  }
   uint64_t upload = 0;
   if (all_resident_) {
     uint64_t off_total = 0, edge_total = 0;
@@ -335,16 +338,24 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     arena_offs_.reserve(std::max<uint64_t>(off_total, 1));
     arena_src_.reserve(edge_total);
     if (weighted) arena_w_.reserve(edge_total);
+    // 1) page copies on the copy stream, one event per page; the largest
+    //    page (RMAT page 0) goes first so tile cutting hides under its DMA
+    while (page_events_.size() < np) {
+      cudaEvent_t e;
+      SR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      page_events_.push_back(e);
+    }
     for (uint32_t p = 0; p < np; ++p) {
       PageMeta& pm = pages_[p];
       PageDesc& d = page_desc_h_[p];
-      d.vertex_begin = pm.vb;
-      d.range = pm.ve - pm.vb;
-      d.edge_count = pm.edges;
       if (!used[p]) continue;
       d.offs = arena_offs_.p + pm.off_base;
       d.src = arena_src_.p + pm.edge_base;
       d.w = weighted ? arena_w_.p + pm.edge_base : nullptr;
+    }
+    auto copy_page = [&](uint32_t p) {
+      PageMeta& pm = pages_[p];
+      const PageDesc& d = page_desc_h_[p];
       SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.offs), pm.h_offs, (size_t(d.range) + 1) * 4,
                               cudaMemcpyHostToDevice, xs_));
       if (pm.edges) {
@@ -354,15 +365,61 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
           SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.w), pm.h_w, pm.edges * 4,
                                   cudaMemcpyHostToDevice, xs_));
       }
+      SR_CUDA(cudaEventRecord(page_events_[p], xs_));
       pm.on_device = true;
       upload += pm.bytes;
+    };
+    uint32_t first = np;
+    for (uint32_t p = 0; p < np && first == np; ++p)
+      if (used[p]) first = p;
+    if (first < np) copy_page(first);
+    // 2) cut tiles on the host while that DMA runs, then the small uploads
+    build_tiles(own_lo_, own_hi_, xs_);
+    page_desc_.reserve(std::max<uint32_t>(np, 1));
+    desc_stage_.reserve(std::max<uint32_t>(np, 1));
+    std::memcpy(desc_stage_.p, page_desc_h_.data(), np * sizeof(PageDesc));
+    SR_CUDA(cudaMemcpyAsync(page_desc_.p, desc_stage_.p, np * sizeof(PageDesc),
+                            cudaMemcpyHostToDevice, xs_));
+    SR_CUDA(cudaEventRecord(ev_tiles_, xs_));
+    for (uint32_t p = first + 1; p < np; ++p)
+      if (used[p]) copy_page(p);
+    // 3) device-side push adjacency, page by page as each copy lands
+    if (csr_derived_) {
+      has_csr_edges_ = false;
+      csr_derived_ = false;
     }
-    SR_CUDA(cudaStreamSynchronize(xs_));
-    // host pointers are borrowed only for the call
+    const bool derive = has_csr_ && !has_csr_edges_ && world_ == 1 && n_ == n &&
+                        m_ == page_edges_total_;
+    SR_CUDA(cudaStreamWaitEvent(cs_, ev_tiles_, 0));
+    if (derive && m_) {
+      out_nbr_.reserve(m_);
+      if (weighted) out_w_.reserve(m_);
+      csr_cursor_.reserve(n_);
+      SR_CUDA(cudaMemsetAsync(csr_cursor_.p, 0, size_t(n_) * 4, cs_));
+      for (uint32_t p = 0; p < np; ++p) {
+        if (!used[p]) continue;
+        SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
+        launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, pages_[p].tile_begin,
+                              pages_[p].tile_end, out_off_.p, csr_cursor_.p, out_nbr_.p,
+                              weighted ? out_w_.p : nullptr, sm_count_ * 8, cs_);
+      }
+      SR_CUDA(cudaGetLastError());
+    }
+    if (derive) {
+      has_csr_edges_ = true;
+      csr_weighted_ = weighted;
+      csr_derived_ = true;
+    }
+    // compute work on the pages is ordered after every copy
+    for (uint32_t p = 0; p < np; ++p)
+      if (used[p]) SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
+    SR_CUDA(cudaStreamSynchronize(xs_));  // host buffers are borrowed only for the call
     for (auto& pm : pages_) pm.h_offs = pm.h_src = pm.h_w = nullptr;
   } else {
     // Out-of-core: keep a pinned host copy of every used page (the source
     // of the copy-stream transfers); pages are admitted at run time.
+    build_tiles(own_lo_, own_hi_, cs_);
+    SR_CUDA(cudaStreamSynchronize(cs_));
     uint64_t words = 0;
     for (uint32_t p = 0; p < np; ++p)
       if (used[p]) words += pages_[p].bytes / 4;
@@ -398,15 +455,18 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     for (auto& pm : pages_)
       if (!pm.h_offs) pm.h_src = pm.h_w = nullptr;
   }
-  page_desc_.reserve(std::max<uint32_t>(np, 1));
-  if (np)
-    SR_CUDA(cudaMemcpy(page_desc_.p, page_desc_h_.data(), np * sizeof(PageDesc),
-                       cudaMemcpyHostToDevice));
-  pages_loaded_ = true;
-  if (csr_derived_) {  // the derived adjacency belonged to the previous page set
-    has_csr_edges_ = false;
-    csr_derived_ = false;
+  if (!all_resident_) {
+    page_desc_.reserve(std::max<uint32_t>(np, 1));
+    if (np)
+      SR_CUDA(cudaMemcpyAsync(page_desc_.p, page_desc_h_.data(), np * sizeof(PageDesc),
+                              cudaMemcpyHostToDevice, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    if (csr_derived_) {  // the derived adjacency belonged to the previous page set
+      has_csr_edges_ = false;
+      csr_derived_ = false;
+    }
   }
+  pages_loaded_ = true;
   last_upload_bytes += upload;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

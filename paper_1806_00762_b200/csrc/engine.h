@@ -163,7 +163,13 @@ class Engine {
   size_t plan_cached_ = size_t(-1);
   void make_resident(uint32_t page, long long step, const std::vector<char>& protect,
                      PassOut& po);
-  void build_tiles(uint32_t lo, uint32_t hi);
+  void build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st);
+  std::vector<cudaEvent_t> page_events_;  // resident upload: copy done per page
+  cudaEvent_t ev_tiles_ = nullptr;
+  PinBuf<uint4> tile_stage_;
+  PinBuf<uint32_t> tile_page_stage_, hub_stage_;
+  PinBuf<PageDesc> desc_stage_;
+  DBuf<uint32_t> csr_cursor_;
 
   int dev_ = 0;
   uint64_t budget_ = 0;

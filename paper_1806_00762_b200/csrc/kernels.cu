@@ -341,14 +341,14 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlockThreads)
 csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
-                      const PageDesc* __restrict__ pages, uint32_t n_tiles,
+                      const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
                       const unsigned long long* __restrict__ out_off, uint32_t* cursor,
                       uint32_t* out_nbr, uint32_t* out_w) {
   __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  for (uint32_t ti = blockIdx.x * kWarpsPerBlock + warp; ti < n_tiles;
+  for (uint32_t ti = tile_lo + blockIdx.x * kWarpsPerBlock + warp; ti < tile_hi;
        ti += gridDim.x * kWarpsPerBlock) {
     const PageDesc pd = pages[tile_page[ti]];
     const uint4 tile = tiles[ti];
@@ -1207,11 +1207,14 @@ void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* 
 }
 
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
-                           uint32_t n_tiles, const unsigned long long* out_off, uint32_t* cursor,
-                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s) {
-  if (!n_tiles) return;
-  csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, n_tiles, out_off,
-                                                       cursor, out_nbr, out_w);
+                           uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
+                           uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
+                           cudaStream_t s) {
+  if (tile_hi <= tile_lo) return;
+  const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (uint32_t(grid) > need) grid = int(need);
+  csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, tile_lo, tile_hi,
+                                                       out_off, cursor, out_nbr, out_w);
 }
 
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s) {

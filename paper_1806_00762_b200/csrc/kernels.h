@@ -51,8 +51,9 @@ void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* 
                        Census* c, cudaStream_t s);
 // Device-side CSR adjacency from resident CSC pages; out-degrees (u32).
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
-                           uint32_t n_tiles, const unsigned long long* out_off, uint32_t* cursor,
-                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s);
+                           uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
+                           uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
+                           cudaStream_t s);
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s);
 // Values initialisation (VertexProgram::init, programs.hpp:20-28).
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
