@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libseraph.so")
+LIB_PATH = os.environ.get("SERAPH_LIB") or os.path.join(_HERE, "libseraph.so")
 
 
 class Error(RuntimeError):

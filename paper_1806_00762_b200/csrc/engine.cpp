@@ -540,6 +540,7 @@ void Engine::alloc_run_state(const sr_run_config& c) {
     chunk_start_.reserve(m_ / kPushChunk + 2);
     blk_cnt_.reserve(nb + 1);
     blk_edges_.reserve(nb + 1);
+    census_part_.reserve(size_t(nb + 1) * 13);
     if (world_ > 1) round_snap_.reserve(npad);
   }
   const size_t np = std::max<size_t>(pages_.size(), 1);
@@ -976,7 +977,7 @@ void Engine::census(int pass_kind) {
   launch_census(n_, changed_.p, predictor_ == SR_PRED_WEAK ? status_.p : nullptr,
                 predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr,
                 has_csr_ ? outdeg_.p : nullptr, pass_kind, own_lo_, own_hi_, blk_cnt_.p,
-                blk_edges_.p, census_.p, cs_);
+                blk_edges_.p, census_part_.p, census_.p, cs_);
 }
 
 void Engine::read_census() {

@@ -215,7 +215,7 @@ class Engine {
   DBuf<int> delta_;
   DBuf<uint8_t> changed_, status_, logstate_;
   DBuf<uint32_t> list_, chunk_start_, blk_cnt_;
-  DBuf<unsigned long long> pref_, blk_edges_;
+  DBuf<unsigned long long> pref_, blk_edges_, census_part_;
   DBuf<Census> census_;
   PinBuf<Census> census_h_;
   DBuf<RunCtr> ctr_;

@@ -23,6 +23,7 @@ namespace seraph {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCensusParts = 13;  // per-block census partials
 constexpr int kLaneEdges = 8;  // consecutive edges per lane per K1 phase-B round
 constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
 
@@ -107,6 +108,40 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
   c.clear();
 }
 
+// End-of-kernel flush: warp sums -> shared memory -> one atomic per counter
+// per block (thousands of same-address atomics per launch would serialise).
+// `scratch` reuses the caller's tile shared memory (>= 40 words): extra
+// static shared memory would push 4 blocks/SM past a carveout step and
+// shrink the L1 that serves the gathers.
+__device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t lane_min,
+                                            Census* census, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
+  uint32_t* mins = scratch + 2 * 4 * kWarpsPerBlock;
+  const unsigned long long at = warp_sum(c.attempts), va = warp_sum(c.valid),
+                           sk = warp_sum(c.skipped), ed = warp_sum(c.edges);
+  lane_min = warp_min(lane_min);
+  __syncthreads();  // every warp is done with its tile scratch
+  if (lane == 0) {
+    red[0 * kWarpsPerBlock + warp] = at;
+    red[1 * kWarpsPerBlock + warp] = va;
+    red[2 * kWarpsPerBlock + warp] = sk;
+    red[3 * kWarpsPerBlock + warp] = ed;
+    mins[warp] = lane_min;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long x = red[lane];  // lane = counter * 8 + warp
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) x += __shfl_down_sync(kFull, x, off, 8);
+    uint32_t m = lane < kWarpsPerBlock ? mins[lane] : kUnreached;
+    m = warp_min(m);
+    if (dst && (lane & 7) == 0 && x) atomicAdd(&dst->attempts + (lane >> 3), x);
+    if (lane == 0 && census && m != kUnreached) atomicMin(&census->min_changed, m);
+  }
+  c.clear();
+}
+
 // ---------------------------------------------------------------------------
 // K1: dense pull relaxation.  One warp per tile; persistent grid; warps grab
 // kGrab consecutive tiles at a time from a per-launch work counter, so a
@@ -129,7 +164,7 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
 // ---------------------------------------------------------------------------
 template <int A, int G, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
-  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_cur[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_best[kWarpsPerBlock][kTileMaxDests];
@@ -327,9 +362,12 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
       __syncwarp();
     }
   }
-  if (cur_page != 0xffffffffu) flush_ctr(c, a.ctr + (a.ctr_per_page ? cur_page : 0), lane);
-  lane_min = warp_min(lane_min);
-  if (lane == 0 && lane_min != kUnreached) atomicMin(&a.census->min_changed, lane_min);
+  if (a.ctr_per_page) {
+    if (cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
+    block_flush(c, nullptr, lane_min, a.census, &s_pref[0][0]);
+  } else {
+    block_flush(c, a.ctr, lane_min, a.census, &s_pref[0][0]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -344,7 +382,7 @@ csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restric
                       const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
                       const unsigned long long* __restrict__ out_off, uint32_t* cursor,
                       uint32_t* out_nbr, uint32_t* out_w) {
-  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -437,7 +475,7 @@ __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __r
 // shared-memory float atomicAdd merge; hub chunks go through hub_sum.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
-  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   __shared__ float s_sum[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
@@ -571,7 +609,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
       __syncwarp();
     }
   }
-  flush_ctr(c, a.ctr, lane);
+  block_flush(c, a.ctr, kUnreached, nullptr, &s_pref[0][0]);
 }
 
 __global__ void pr_hub_finalize_kernel(const uint32_t* hub_vertex, uint32_t n_hubs,
@@ -609,6 +647,7 @@ __global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, flo
 // ---------------------------------------------------------------------------
 template <int A, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
+  __shared__ __align__(16) uint32_t s_scratch[2 * 4 * kWarpsPerBlock + kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kWarpsPerBlock;
@@ -681,9 +720,7 @@ __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
       ad += k_last + (e_last <= 32 ? 1u : 0u);
     }
   }
-  flush_ctr(c, a.ctr, lane);
-  lane_min = warp_min(lane_min);
-  if (lane == 0 && lane_min != kUnreached) atomicMin(&a.census->min_changed, lane_min);
+  block_flush(c, a.ctr, lane_min, a.census, s_scratch);
 }
 
 __global__ void push_commit_kernel(uint32_t* __restrict__ values, const uint32_t* __restrict__ next,
@@ -742,113 +779,128 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
                                                      int pass_kind, uint32_t own_lo, uint32_t own_hi,
                                                      uint32_t* blk_cnt,
                                                      unsigned long long* blk_edges, Census* cz) {
-  __shared__ unsigned long long s_hist[6];
-  __shared__ unsigned long long s_red[3][8];
-  if (threadIdx.x < 6) s_hist[threadIdx.x] = 0;
-  __syncthreads();
-  const uint32_t v0 = blockIdx.x * kCensusBlockVerts + threadIdx.x * 16;
-  unsigned long long n_changed = 0, n_push = 0, edges = 0, events = 0, incorrect = 0;
-  unsigned long long own_push = 0, own_edges = 0;
-  unsigned hist[6] = {0, 0, 0, 0, 0, 0};
-  if (v0 < n) {
-    uint4 cw = *reinterpret_cast<const uint4*>(changed + v0);
-    const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
-    uint32_t dg[16];
-    if (outdeg && (cw.x | cw.y | cw.z | cw.w)) {
-      const uint4* dp = reinterpret_cast<const uint4*>(outdeg + v0);
+  // grid-stride over 4096-vertex chunks; per-chunk (count, edges) for the
+  // compaction scan, run totals reduced once per block (few global atomics)
+  __shared__ unsigned long long s_chunk[2][8];
+  __shared__ unsigned long long s_tot[kCensusParts][8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t nchunks = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  unsigned long long tot[kCensusParts];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint4 d4 = dp[k];
-        dg[4 * k] = d4.x;
-        dg[4 * k + 1] = d4.y;
-        dg[4 * k + 2] = d4.z;
-        dg[4 * k + 3] = d4.w;
-      }
-    } else {
+  for (int k = 0; k < kCensusParts; ++k) tot[k] = 0;
+  for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const uint32_t v0 = ch * kCensusBlockVerts + threadIdx.x * 16;
+    unsigned long long own_push = 0, own_edges = 0;
+    if (v0 < n) {
+      const uint4 cw = *reinterpret_cast<const uint4*>(changed + v0);
+      const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
+      uint32_t dg[16];
+      if (outdeg && (cw.x | cw.y | cw.z | cw.w)) {
+        const uint4* dp = reinterpret_cast<const uint4*>(outdeg + v0);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) dg[k] = 0;
-    }
-    uint4 sw{}, lw{};
-    if (status) sw = *reinterpret_cast<const uint4*>(status + v0);
-    if (logstate) lw = *reinterpret_cast<const uint4*>(logstate + v0);
-    uint8_t* sb = reinterpret_cast<uint8_t*>(&sw);
-    uint8_t* lb = reinterpret_cast<uint8_t*>(&lw);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t v = v0 + j;
-      if (v >= n) break;
-      const bool ch = cb[j] != 0;
-      if (ch) {
-        ++n_changed;
-        const unsigned long long d = dg[j];
-        edges += d;
-        n_push += d > 0;
-        if (v >= own_lo && v < own_hi) {
-          own_edges += d;
-          own_push += d > 0;
+        for (int k = 0; k < 4; ++k) {
+          const uint4 d4 = dp[k];
+          dg[4 * k] = d4.x;
+          dg[4 * k + 1] = d4.y;
+          dg[4 * k + 2] = d4.z;
+          dg[4 * k + 3] = d4.w;
         }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) dg[k] = 0;
       }
-      if (status) {
-        uint8_t s = sb[j];
-        if (pass_kind == kPassDense) {
-          const bool attempt_state = (s == 0 || s == 1 || s == 5);
-          if (attempt_state) {
-            if (logstate) lb[j] = log_attempt(lb[j], ch, events, incorrect);
-            s = ch ? 0 : (s == 0 ? 5 : (s == 5 ? 3 : 4));
-          } else {
-            s = (s == 3) ? 2 : (s == 2 ? 1 : 3);
+      uint4 sw{}, lw{};
+      if (status) sw = *reinterpret_cast<const uint4*>(status + v0);
+      if (logstate) lw = *reinterpret_cast<const uint4*>(logstate + v0);
+      uint8_t* sb = reinterpret_cast<uint8_t*>(&sw);
+      uint8_t* lb = reinterpret_cast<uint8_t*>(&lw);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t v = v0 + j;
+        if (v >= n) break;
+        const bool ch_ = cb[j] != 0;
+        if (ch_) {
+          const unsigned long long d = dg[j];
+          tot[0] += 1;
+          tot[1] += d > 0;
+          tot[2] += d;
+          if (v >= own_lo && v < own_hi) {
+            own_edges += d;
+            own_push += d > 0;
           }
-        } else if (ch && pass_kind != kPassInit) {
-          if (pass_kind == kPassRecovery) s = 0;
-          if (logstate) lb[j] = log_change(lb[j], incorrect);
         }
-        sb[j] = s;
-        hist[s < 6 ? s : 0]++;
+        if (status) {
+          uint8_t st = sb[j];
+          if (pass_kind == kPassDense) {
+            const bool attempt_state = (st == 0 || st == 1 || st == 5);
+            if (attempt_state) {
+              if (logstate) lb[j] = log_attempt(lb[j], ch_, tot[5], tot[6]);
+              st = ch_ ? 0 : (st == 0 ? 5 : (st == 5 ? 3 : 4));
+            } else {
+              st = (st == 3) ? 2 : (st == 2 ? 1 : 3);
+            }
+          } else if (ch_ && pass_kind != kPassInit) {
+            if (pass_kind == kPassRecovery) st = 0;
+            if (logstate) lb[j] = log_change(lb[j], tot[6]);
+          }
+          sb[j] = st;
+          switch (st) {
+            case 0: tot[7]++; break;
+            case 1: tot[8]++; break;
+            case 2: tot[9]++; break;
+            case 3: tot[10]++; break;
+            case 4: tot[11]++; break;
+            default: tot[12]++; break;
+          }
+        }
       }
+      if (status) *reinterpret_cast<uint4*>(status + v0) = sw;
+      if (logstate) *reinterpret_cast<uint4*>(logstate + v0) = lw;
     }
-    if (status) *reinterpret_cast<uint4*>(status + v0) = sw;
-    if (logstate) *reinterpret_cast<uint4*>(logstate + v0) = lw;
+    tot[3] += own_push;
+    tot[4] += own_edges;
+    own_push = warp_sum(own_push);
+    own_edges = warp_sum(own_edges);
+    if (lane == 0) {
+      s_chunk[0][w] = own_push;
+      s_chunk[1][w] = own_edges;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long a = 0, b = 0;
+      for (int i = 0; i < 8; ++i) {
+        a += s_chunk[0][i];
+        b += s_chunk[1][i];
+      }
+      blk_cnt[ch] = (uint32_t)a;
+      blk_edges[ch] = b;
+    }
+    __syncthreads();
   }
-  if (status) {
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      unsigned x = warp_sum(hist[s]);
-      if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_hist[s], (unsigned long long)x);
-    }
-  }
-  n_changed = warp_sum(n_changed);
-  n_push = warp_sum(n_push);
-  edges = warp_sum(edges);
-  events = warp_sum(events);
-  incorrect = warp_sum(incorrect);
-  own_push = warp_sum(own_push);
-  own_edges = warp_sum(own_edges);
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    s_red[0][w] = n_changed;
-    s_red[1][w] = own_push;
-    s_red[2][w] = own_edges;
-    if (n_push) atomicAdd(&cz->push_count, n_push);
-    if (edges) atomicAdd(&cz->out_edges, edges);
-    if (events) atomicAdd(&cz->log_events, events);
-    if (incorrect) atomicAdd(&cz->log_incorrect, incorrect);
+  for (int k = 0; k < kCensusParts; ++k) {
+    const unsigned long long x = warp_sum(tot[k]);
+    if (lane == 0) s_tot[k][w] = x;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long a0 = 0, a1 = 0, a2 = 0;
-    for (int i = 0; i < 8; ++i) {
-      a0 += s_red[0][i];
-      a1 += s_red[1][i];
-      a2 += s_red[2][i];
+  if (threadIdx.x < kCensusParts) {
+    unsigned long long a = 0;
+    for (int i = 0; i < 8; ++i) a += s_tot[threadIdx.x][i];
+    if (a) {
+      unsigned long long* dst;
+      switch (threadIdx.x) {
+        case 0: dst = &cz->changed; break;
+        case 1: dst = &cz->push_count; break;
+        case 2: dst = &cz->out_edges; break;
+        case 3: dst = &cz->own_push; break;
+        case 4: dst = &cz->own_edges; break;
+        case 5: dst = &cz->log_events; break;
+        case 6: dst = &cz->log_incorrect; break;
+        default: dst = &cz->status_hist[threadIdx.x - 7]; break;
+      }
+      atomicAdd(dst, a);
     }
-    blk_cnt[blockIdx.x] = (uint32_t)a1;
-    blk_edges[blockIdx.x] = a2;
-    if (a0) atomicAdd(&cz->changed, a0);
-    if (a1) atomicAdd(&cz->own_push, a1);
-    if (a2) atomicAdd(&cz->own_edges, a2);
   }
-  if (status && threadIdx.x < 6 && s_hist[threadIdx.x])
-    atomicAdd(&cz->status_hist[threadIdx.x], s_hist[threadIdx.x]);
 }
 
 // Exclusive scan of the per-block (count, edges) pairs; one block.
@@ -1173,12 +1225,14 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
 
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
                    const uint32_t* out_offsets, int pass_kind, uint32_t own_lo,
-                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
-                   cudaStream_t s) {
+                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges,
+                   unsigned long long* part, Census* c, cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
   if (!nb) return;
-  census_kernel<<<nb, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind, own_lo,
-                                   own_hi, blk_cnt, blk_edges, c);
+  (void)part;
+  const int grid = int(nb < 148u * 4u ? nb : 148u * 4u);
+  census_kernel<<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind, own_lo,
+                                     own_hi, blk_cnt, blk_edges, c);
 }
 
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,

@@ -32,8 +32,8 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
 constexpr uint32_t kCensusBlockVerts = 4096;
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
                    const uint32_t* outdeg, int pass_kind, uint32_t own_lo,
-                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges, Census* c,
-                   cudaStream_t s);
+                   uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges,
+                   unsigned long long* part, Census* c, cudaStream_t s);
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
                         cudaStream_t s);
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
