@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--edge-factor", type=int, default=16)
     p.add_argument("--uniform", action="store_true", help="a=b=c=d=0.25 (uniform random)")
     p.add_argument("--pages", type=int, default=16)
-    p.add_argument("--mode", default="reentry", choices=list(MODES))
+    p.add_argument("--mode", default="baseline", choices=list(MODES))
     p.add_argument("--predictor", default="strong", choices=list(PREDS))
     p.add_argument("--window", type=int, default=8)
     p.add_argument("--mrt", type=int, default=2)
@@ -189,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
     prog = ps.VertexProgram(ps.AlgoKind(algo), 0)
     cfg = ps.EngineConfig(predictor=ps.PredictorMode(PREDS[args.predictor]),
                           window_capacity=args.window, clock=ps.ClockMode.WALL,
-                          pr_iterations=args.pr_iters)
+                          pr_iterations=args.pr_iters, profile_kernels=True)
     cfg.schedule.kind = ps.ScheduleModeKind(MODES[args.mode])
     cfg.schedule.max_reentry_times = args.mrt
     budget = int(args.budget_gb * 2**30)
@@ -258,20 +258,34 @@ def run_ours(args, rank, world, local_rank):
         res = eng.run(prog, cfg)
         parity = {"fixpoint_violations": eng.verify_fixpoint(ps.AlgoKind.CC, res.values)}
 
-    # roofline: the dominant kernel = K1 dense pull sweep over all pages
+    # roofline: the dominant kernel (K1 dense pull) timed launch by launch with
+    # CUDA events on the engine stream inside the timed runs; algorithmic bytes
+    # per SURVEY §8(d): per edge read (src 4 + gathered value 4 [+ weight 4])
+    # + 8 B per attempted destination, over the dense/recovery passes.
     roof = None
     if not args.budget_gb and algo != 3:
-        ms, edges = eng.bench_pull_sweep(ps.AlgoKind(algo), 20)
         per_edge = 12 if algo == 2 else 8
-        alg_bytes = per_edge * edges + 8 * n
+        k1_bytes = k1_s = 0.0
+        k1_launches = 0
+        for r in runs:
+            for st in r.metrics.per_pass:
+                if st.kind != ps.PassKind.SPARSE_PUSH:
+                    k1_bytes += per_edge * st.edges_read + 8 * st.attempts
+            k1_s += r.metrics.relax_seconds
+            k1_launches += r.metrics.relax_launches
         peak, src_ = measured_peaks()
-        achieved = alg_bytes / (ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "pull_relax_kernel (K1 sweep)",
+        achieved = k1_bytes / k1_s / 1e9
+        ms, edges = eng.bench_pull_sweep(ps.AlgoKind(algo), 20)
+        roof = {"bound": "hbm", "kernel": "pull_relax_kernel (K1), launches inside the timed runs",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": src_,
                 "traffic": profile_traffic(f"{args.algo}-s{args.scale}"),
-                "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": round(ms, 4),
-                "per_unit": f"{per_edge} B/edge + 8 B/destination"}
+                "algorithmic_bytes_per_launch": int(k1_bytes / max(k1_launches, 1)),
+                "launch_ms": round(k1_s / max(k1_launches, 1) * 1e3, 4),
+                "launches": k1_launches, "share_of_step": round(k1_s / sum(dev_s), 3),
+                "per_unit": f"{per_edge} B/edge read + 8 B/attempted destination",
+                "isolated_sweep": {"ms": round(ms, 4), "edges": edges,
+                                   "note": "gate-off sweep over the converged values"}}
     elif algo == 3:
         iters = args.pr_iters
         if args.budget_gb:
@@ -296,6 +310,17 @@ def run_ours(args, rank, world, local_rank):
                     "traffic": profile_traffic(f"pagerank-s{args.scale}"),
                     "algorithmic_bytes_per_launch": 8 * m + 16 * n,
                     "per_unit": "8 B/edge + 16 B/destination per iteration"}
+
+    # the multi-pass subgraph-iteration schedules on the same resident graph
+    schedules = {}
+    if algo != 3 and world == 1:
+        for mode in ("reentry", "pipelined"):
+            c2 = ps.EngineConfig(predictor=cfg.predictor, window_capacity=args.window,
+                                 clock=ps.ClockMode.WALL)
+            c2.schedule.kind = ps.ScheduleModeKind(MODES[mode])
+            eng.run(prog, c2, want_values=False)
+            t = min(eng.run(prog, c2, want_values=False).metrics.device_seconds for _ in range(3))
+            schedules[mode] = {"ms": round(t * 1e3, 3), "gteps": round(m / t / 1e9, 2)}
 
     # e2e: the public C-ABI one-shot call with pinned host buffers
     e2e = None
@@ -355,7 +380,7 @@ def run_ours(args, rank, world, local_rank):
                    "recovery": last.recovery_passes, "edges_read": last.edges_read},
         "wall_ms_per_step": round(wall / args.steps * 1e3, 4),
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
-        "clocks": clocks, "parity": parity,
+        "clocks": clocks, "parity": parity, "schedules": schedules,
     }
     eng.close()
     if rank == 0:

@@ -101,6 +101,10 @@ typedef struct {
   /* PageRank (new algorithm, no reference counterpart) */
   uint32_t pr_iterations; /* default 20 */
   double pr_damping;      /* default 0.85 */
+  /* Time every relax-kernel launch (K1 pull / K8 PageRank) with CUDA events
+   * on the compute stream; totals land in sr_metrics.relax_seconds. */
+  int32_t profile_kernels;
+  int32_t pad_;
 } sr_run_config;
 
 /* PassStats (metrics.hpp:17-29). */
@@ -141,6 +145,8 @@ typedef struct {
   uint64_t h2d_bytes;      /* bytes actually moved host->device during the run */
   uint64_t d2h_bytes;
   uint64_t kernel_runs;    /* page-runs (DensePassOutcome::kernel_runs) */
+  double relax_seconds;    /* sum of timed K1/K8 launch durations (profile_kernels) */
+  uint64_t relax_launches;
 } sr_metrics;
 
 typedef struct {

@@ -99,6 +99,8 @@ class RunConfig(C.Structure):
         ("seed", C.c_uint64),
         ("pr_iterations", C.c_uint32),
         ("pr_damping", C.c_double),
+        ("profile_kernels", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -140,6 +142,8 @@ class MetricsC(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("kernel_runs", C.c_uint64),
+        ("relax_seconds", C.c_double),
+        ("relax_launches", C.c_uint64),
     ]
 
 

@@ -108,6 +108,10 @@ Engine::~Engine() {
   if (ev_stop_) cudaEventDestroy(ev_stop_);
   if (ev_step_) cudaEventDestroy(ev_step_);
   if (ev_tiles_) cudaEventDestroy(ev_tiles_);
+  for (auto& e : relax_ev_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
 }
@@ -585,6 +589,17 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
     int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
                                       (uint64_t(tasks) + kWarpsPerBlock - 1) / kWarpsPerBlock));
     grid = std::max(grid, 1);
+    std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
+    if (profile_kernels_) {
+      if (relax_ev_used_ == relax_ev_.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        SR_CUDA(cudaEventCreate(&e.first));
+        SR_CUDA(cudaEventCreate(&e.second));
+        relax_ev_.push_back(e);
+      }
+      evp = &relax_ev_[relax_ev_used_++];
+      SR_CUDA(cudaEventRecord(evp->first, cs_));
+    }
     if (pagerank) {
       PrArgs a{};
       a.work = next_work_counter();
@@ -624,6 +639,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
     ++launches_;
     seg = Segments{};
   };
@@ -1064,6 +1080,8 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   det_ = cfg.clock == SR_CLOCK_VIRTUAL && cfg.algo != SR_ALGO_PAGERANK;
   record_trace_ = cfg.record_trace != 0;
   pr_damp_ = cfg.pr_damping;
+  profile_kernels_ = cfg.profile_kernels != 0;
+  relax_ev_used_ = 0;
   trace.clear();
   std::memset(&m, 0, sizeof(m));
   passes.clear();
@@ -1080,6 +1098,10 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   else run_traversal(cfg, values_out, m, passes);
   m.kernel_launches = launches_;
   m.h2d_bytes = h2d_bytes_;
+  if (profile_kernels_) {
+    m.relax_seconds = collect_relax_seconds();
+    m.relax_launches = relax_ev_used_;
+  }
 }
 
 void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_metrics& m,
@@ -1399,6 +1421,16 @@ void Engine::bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edg
   SR_CUDA(cudaEventElapsedTime(&t, ev_start_, ev_stop_));
   *ms = reps ? t / reps : 0.0;
   *edges = reps ? ctr_h_.p[0].edges / reps : 0;
+}
+
+double Engine::collect_relax_seconds() {
+  double total = 0;
+  for (size_t i = 0; i < relax_ev_used_; ++i) {
+    float ms = 0;
+    SR_CUDA(cudaEventElapsedTime(&ms, relax_ev_[i].first, relax_ev_[i].second));
+    total += ms * 1e-3;
+  }
+  return total;
 }
 
 void Engine::attach_world(int rank, int world, const uint8_t id[128]) {

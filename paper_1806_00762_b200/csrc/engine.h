@@ -243,6 +243,10 @@ class Engine {
   VModel vmodel_;
   bool record_trace_ = false;
   double pr_damp_ = 0.85;
+  bool profile_kernels_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> relax_ev_;  // pool
+  size_t relax_ev_used_ = 0;
+  double collect_relax_seconds();
 
   // multi-GPU
   int rank_ = 0, world_ = 1;

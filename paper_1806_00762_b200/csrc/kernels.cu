@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
         for (; e < tile.y; e += 32) {
           const uint32_t sidx = __ldcs(src + e);
           const uint32_t w = (A == kSssp) ? __ldcs(wts + e) : 0u;
+          if (A == kSssp && w >= cur) continue;  // cannot improve: skip the gather
           const uint32_t sv = DET ? __ldg(values_ro + sidx) : a.values[sidx];
           best = min(best, combine<A>(sv, w));
         }
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
           uint32_t ent = lo;
           uint32_t nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
           bool att_e = (loc_of[ent] >> 31) != 0;
-          uint32_t eid[kLaneEdges];
+          uint32_t cur_e = (A == kSssp) ? s_cur[warp][ent] : 0u;
+          uint32_t eid[kLaneEdges], ecur[kLaneEdges];
           unsigned live = 0;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t) {
@@ -310,8 +312,10 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
               ++ent;
               nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
               att_e = (loc_of[ent] >> 31) != 0;
+              if (A == kSssp) cur_e = s_cur[warp][ent];
             }
             eid[t] = ent;
+            ecur[t] = cur_e;
             if (pp >= lo_pos && pp < span && att_e) live |= 1u << t;
           }
           if (live) {
@@ -325,6 +329,13 @@ __global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
             }
             const uint32_t sv_idx[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
             const uint32_t wv[kLaneEdges] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            if (A == kSssp) {
+              // values are >= 0, so an edge with w >= the destination's value
+              // cannot improve it: no gather (the wavefront-bound part of K1)
+#pragma unroll
+              for (int t = 0; t < kLaneEdges; ++t)
+                if (wv[t] >= ecur[t]) live &= ~(1u << t);
+            }
             uint32_t sv[kLaneEdges];
 #pragma unroll
             for (int t = 0; t < kLaneEdges; ++t)

@@ -365,6 +365,7 @@ class EngineConfig:
     # PageRank (new)
     pr_iterations: int = 20
     pr_damping: float = 0.85
+    profile_kernels: bool = False  # time K1/K8 launches (MetricsReport.relax_seconds)
 
     def validate(self) -> None:  # engine.cpp:43-49
         if self.window_capacity < 2:
@@ -399,6 +400,7 @@ class EngineConfig:
         c.seed = int(self.seed)
         c.pr_iterations = int(self.pr_iterations)
         c.pr_damping = float(self.pr_damping)
+        c.profile_kernels = 1 if self.profile_kernels else 0
         return c
 
 
@@ -441,6 +443,8 @@ class MetricsReport:
     kernel_runs: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    relax_seconds: float = 0.0
+    relax_launches: int = 0
 
     def throughput(self) -> float:  # metrics.hpp:51-56
         t = self.wall_seconds if self.wall_seconds > 0 else self.virtual_makespan
@@ -480,7 +484,8 @@ def _metrics_from_c(m: N.MetricsC, passes) -> MetricsReport:
     for f in ("passes", "sparse_passes", "dense_passes", "recovery_passes", "pages_transferred",
               "bytes_transferred", "update_attempts", "valid_updates", "skipped_vertices",
               "edges_read", "virtual_makespan", "wall_seconds", "device_seconds",
-              "upload_seconds", "kernel_launches", "kernel_runs", "h2d_bytes", "d2h_bytes"):
+              "upload_seconds", "kernel_launches", "kernel_runs", "h2d_bytes", "d2h_bytes",
+              "relax_seconds", "relax_launches"):
         setattr(r, f, getattr(m, f))
     if m.has_prediction_accuracy:
         r.prediction_accuracy = m.prediction_accuracy

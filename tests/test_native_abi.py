@@ -135,3 +135,18 @@ def test_shard_plan_edge_balanced():
         assert cuts[0] == 0 and cuts[-1] == 4096 and (np.diff(cuts.astype(int)) >= 0).all()
         loads = np.diff(in_off[cuts.astype(np.int64)].astype(np.int64))
         assert loads.max() <= src.size / parts + int(np.diff(in_off.astype(np.int64)).max())
+
+
+def test_struct_sizes_match_compiled_header(tmp_path):
+    """ctypes mirrors of the C-ABI structs have the compiler's sizes."""
+    import subprocess
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "seraph.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(sr_page_view),sizeof(sr_run_config),sizeof(sr_pass_stats),'
+                   'sizeof(sr_metrics),sizeof(sr_trace_event),sizeof(sr_device_info));}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = [C.sizeof(t) for t in (N.PageView, N.RunConfig, N.PassStatsC, N.MetricsC,
+                                  N.TraceEventC, N.DeviceInfo)]
+    assert got == want
