@@ -28,7 +28,8 @@ def report(path, key, tag):
     rd = to_bytes(*d["dram__bytes_read.sum"])
     wr = to_bytes(*d["dram__bytes_write.sum"])
     out = {"source": os.path.basename(path), "kernel": d["kernel"],
-           "duration_ms": float(d["gpu__time_duration.sum"][0]),
+           "duration_ms": float(d["gpu__time_duration.sum"][0]) *
+                          {"ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(d["gpu__time_duration.sum"][1], 1.0),
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
            "metrics": {k: v for k, v in d.items() if k not in ("kernel",)}}
     os.makedirs(PROF, exist_ok=True)
