@@ -17,7 +17,7 @@ enum PassKindDev : int { kPassSparse = 0, kPassDense = 1, kPassRecovery = 2, kPa
 // ~kTileEdgeBudget edges) or one chunk of a hub destination's in-edges.
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlockThreads = kWarpsPerBlock * 32;
-constexpr uint32_t kTileMaxDests = 256;
+constexpr uint32_t kTileMaxDests = 128;  // 16 KB smem per block: 6 blocks/SM + L1 room
 constexpr uint32_t kTileEdgeBudget = 1024;
 constexpr uint32_t kHubChunk = 1024;      // edges per hub chunk tile
 constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id

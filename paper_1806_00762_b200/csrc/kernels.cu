@@ -163,7 +163,7 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
 // destination's valid update once per run.
 // ---------------------------------------------------------------------------
 template <int A, int G, bool DET>
-__global__ void __launch_bounds__(kBlockThreads) pull_relax_kernel(PullArgs a) {
+__global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_cur[kWarpsPerBlock][kTileMaxDests];
