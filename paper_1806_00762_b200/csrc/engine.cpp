@@ -112,6 +112,7 @@ Engine::~Engine() {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  for (cudaEvent_t e : wtrace_pool_) cudaEventDestroy(e);
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
 }
@@ -583,12 +584,21 @@ RunCtr* Engine::alloc_ctr(size_t entries) {
 RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool det, RunCtr* ctr,
                               const RunCtr* prev, bool per_page, bool pagerank) {
   Segments seg{};
+  std::vector<uint32_t> seg_pages;
   auto flush = [&]() {
     if (seg.n == 0) return;
     const uint32_t tasks = seg.task_prefix[seg.n];
     int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
                                       (uint64_t(tasks) + kWarpsPerBlock - 1) / kWarpsPerBlock));
     grid = std::max(grid, 1);
+    WallTraceRec* tr = nullptr;
+    if (record_trace_ && !det) {
+      wtrace_.push_back(WallTraceRec{trace_event(), trace_event(), seg_pages,
+                                     trace_reentry_ ? SR_TRACE_REENTRY : SR_TRACE_KERNEL_START,
+                                     cur_pass_});
+      tr = &wtrace_.back();
+      SR_CUDA(cudaEventRecord(tr->a, cs_));
+    }
     std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
     if (profile_kernels_) {
       if (relax_ev_used_ == relax_ev_.size()) {
@@ -640,17 +650,20 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
     }
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    if (tr) SR_CUDA(cudaEventRecord(tr->b, cs_));
     ++launches_;
     seg = Segments{};
+    seg_pages.clear();
   };
   uint32_t last_end = 0xffffffffu;
   for (uint32_t p : pages) {
     const PageMeta& pm = pages_[p];
     if (pm.tile_end <= pm.tile_begin) continue;
+    if (seg.n == kMaxSegments && !(pm.tile_begin == last_end)) flush();
+    seg_pages.push_back(p);
     if (seg.n > 0 && pm.tile_begin == last_end) {
       seg.task_prefix[seg.n] += pm.tile_end - pm.tile_begin;
     } else {
-      if (seg.n == kMaxSegments) flush();
       seg.tile_begin[seg.n] = pm.tile_begin;
       seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (pm.tile_end - pm.tile_begin);
       ++seg.n;
@@ -780,6 +793,13 @@ void Engine::make_resident(uint32_t page, long long step, const std::vector<char
   if (sl.page >= 0) pages_[sl.page].slot = -1;
   // the copy may only overwrite the slot once its last reader finished
   SR_CUDA(cudaStreamWaitEvent(xs_, sl.freed, 0));
+  WallTraceRec* tr = nullptr;
+  if (record_trace_) {
+    wtrace_.push_back(WallTraceRec{trace_event(), trace_event(), {page}, SR_TRACE_XFER_START,
+                                   cur_pass_});
+    tr = &wtrace_.back();
+    SR_CUDA(cudaEventRecord(tr->a, xs_));
+  }
   const size_t r1 = size_t(pm.ve - pm.vb) + 1;
   SR_CUDA(cudaMemcpyAsync(sl.offs.p, pm.h_offs, r1 * 4, cudaMemcpyHostToDevice, xs_));
   if (pm.edges) {
@@ -788,6 +808,7 @@ void Engine::make_resident(uint32_t page, long long step, const std::vector<char
       SR_CUDA(cudaMemcpyAsync(sl.w.p, pm.h_w, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
   }
   launch_set_page_desc(page_desc_.p, page, sl.offs.p, sl.src.p, weighted_ ? sl.w.p : nullptr, xs_);
+  if (tr) SR_CUDA(cudaEventRecord(tr->b, xs_));
   SR_CUDA(cudaEventRecord(sl.ready, xs_));
   sl.page = int(page);
   sl.last_use = step;
@@ -802,7 +823,7 @@ void Engine::make_resident(uint32_t page, long long step, const std::vector<char
 // ---------------------------------------------------------------------------
 PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recovery,
                                 uint32_t pass_index, bool pagerank) {
-  (void)pass_index;
+  cur_pass_ = pass_index;
   PassOut po;
   const int mode = (recovery || pagerank) ? SR_SCHED_BASELINE : cfg.schedule;
   const uint32_t B = cfg.window_capacity;
@@ -890,8 +911,10 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
     RunCtr* prev = nullptr;
     for (int r = 0; r < st.reps; ++r) {
       RunCtr* slot = alloc_ctr(per_page ? std::max<size_t>(np, 1) : 1);
+      trace_reentry_ = r > 0;
       launch_pages(st.pages, gate, false, slot, (st.gated && r > 0) ? prev : nullptr, per_page,
                    pagerank);
+      trace_reentry_ = false;
       prev = slot;
       po.kernel_runs += st.pages.size();
     }
@@ -929,7 +952,9 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
             if (cudaEventQuery(ev_step_) == cudaSuccess) {
               if (size_t(ctr_used_) + 1 > ctr_.n) break;
               RunCtr* slot = alloc_ctr(1);
+              trace_reentry_ = true;
               launch_pages({victim}, gate, false, slot, nullptr, false, pagerank);
+              trace_reentry_ = false;
               po.kernel_runs += 1;
               SR_CUDA(cudaEventRecord(ev_step_, cs_));
               ++guard;
@@ -1082,6 +1107,8 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   pr_damp_ = cfg.pr_damping;
   profile_kernels_ = cfg.profile_kernels != 0;
   relax_ev_used_ = 0;
+  wtrace_.clear();
+  wtrace_pool_used_ = 0;
   trace.clear();
   std::memset(&m, 0, sizeof(m));
   passes.clear();
@@ -1098,6 +1125,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   else run_traversal(cfg, values_out, m, passes);
   m.kernel_launches = launches_;
   m.h2d_bytes = h2d_bytes_;
+  finish_wall_trace();
   if (profile_kernels_) {
     m.relax_seconds = collect_relax_seconds();
     m.relax_launches = relax_ev_used_;
@@ -1421,6 +1449,40 @@ void Engine::bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edg
   SR_CUDA(cudaEventElapsedTime(&t, ev_start_, ev_stop_));
   *ms = reps ? t / reps : 0.0;
   *edges = reps ? ctr_h_.p[0].edges / reps : 0;
+}
+
+cudaEvent_t Engine::trace_event() {
+  if (wtrace_pool_used_ == wtrace_pool_.size()) {
+    cudaEvent_t e;
+    SR_CUDA(cudaEventCreate(&e));
+    wtrace_pool_.push_back(e);
+  }
+  return wtrace_pool_[wtrace_pool_used_++];
+}
+
+// Convert the recorded events to TraceEvents (milliseconds since the run's
+// start event), sorted like VirtualClock::drain (scheduler.cpp:79-88).
+void Engine::finish_wall_trace() {
+  if (!record_trace_ || det_) return;
+  std::vector<sr_trace_event> out;
+  for (const WallTraceRec& r : wtrace_) {
+    float ta = 0, tb = 0;
+    SR_CUDA(cudaEventElapsedTime(&ta, ev_start_, r.a));
+    SR_CUDA(cudaEventElapsedTime(&tb, ev_start_, r.b));
+    const int end_kind = r.start_kind == SR_TRACE_XFER_START ? SR_TRACE_XFER_END : SR_TRACE_KERNEL_END;
+    for (uint32_t p : r.pages) {
+      out.push_back(sr_trace_event{double(ta), r.start_kind, p, r.pass, 0});
+      out.push_back(sr_trace_event{double(tb), end_kind, p, r.pass, 0});
+    }
+  }
+  std::stable_sort(out.begin(), out.end(), [](const sr_trace_event& a, const sr_trace_event& b) {
+    if (a.time != b.time) return a.time < b.time;
+    if (a.page_id != b.page_id) return a.page_id < b.page_id;
+    return a.kind < b.kind;
+  });
+  trace.insert(trace.end(), out.begin(), out.end());
+  wtrace_.clear();
+  wtrace_pool_used_ = 0;
 }
 
 double Engine::collect_relax_seconds() {

@@ -242,6 +242,21 @@ class Engine {
   VClock vclock_;
   VModel vmodel_;
   bool record_trace_ = false;
+  // Wall-clock trace (record_trace in ClockMode::Wall): CUDA events around
+  // every launch (compute stream) and page transfer (copy stream).
+  struct WallTraceRec {
+    cudaEvent_t a, b;
+    std::vector<uint32_t> pages;
+    int start_kind;  // SR_TRACE_KERNEL_START / SR_TRACE_REENTRY / SR_TRACE_XFER_START
+    uint32_t pass;
+  };
+  std::vector<WallTraceRec> wtrace_;
+  std::vector<cudaEvent_t> wtrace_pool_;
+  size_t wtrace_pool_used_ = 0;
+  cudaEvent_t trace_event();
+  bool trace_reentry_ = false;
+  uint32_t cur_pass_ = 0;
+  void finish_wall_trace();
   double pr_damp_ = 0.85;
   bool profile_kernels_ = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> relax_ev_;  // pool

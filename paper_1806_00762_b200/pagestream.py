@@ -467,6 +467,26 @@ class RunResult:
     ranks: Optional[np.ndarray] = None  # f32 per vertex (PageRank)
 
 
+_TRACE_NAMES = {TraceEventKind.XFER_START: "xfer_start", TraceEventKind.XFER_END: "xfer_end",
+                TraceEventKind.KERNEL_START: "kernel_start", TraceEventKind.KERNEL_END: "kernel_end",
+                TraceEventKind.REENTRY: "reentry"}
+
+
+def write_trace_csv(trace) -> str:  # scheduler.cpp:60-67
+    """Virtual clock: model time units; Wall clock: milliseconds of CUDA events."""
+    out = ["event_time,event_kind,page_id,pass_index"]
+    for e in trace:
+        out.append(f"{e.time:.6f},{_TRACE_NAMES[TraceEventKind(e.kind)]},{e.page_id},{e.pass_index}")
+    return "\n".join(out) + "\n"
+
+
+def simulate_pass_makespan(pass_trace) -> float:  # scheduler.cpp:69-77
+    if not pass_trace:
+        return 0.0
+    ts = [e.time for e in pass_trace]
+    return max(ts) - min(ts)
+
+
 def write_status_histogram_csv(report: MetricsReport) -> str:  # metrics.cpp:9-27
     rows = [p for p in report.per_pass if p.has_status_counts]
     if not rows:

@@ -417,3 +417,38 @@ def test_csr_offsets_only_derives_push_adjacency():
                 r = eng.run(program_for(kind, 0, el), cfg_of(clock=ps.ClockMode.WALL, execution=ex))
                 assert np.array_equal(r.values, oracle_values(el, kind, 0)), (kind, ex)
         assert eng.verify_fixpoint(ps.AlgoKind.SSSP, oracle_values(el, ps.AlgoKind.SSSP, 0)) == 0
+
+
+@pytest.mark.parametrize("mode", [ps.ScheduleModeKind.BASELINE, ps.ScheduleModeKind.PIPELINED,
+                                  ps.ScheduleModeKind.PIPELINED_FINE])
+def test_wall_trace_from_cuda_events(mode):
+    """ClockMode::Wall traces are CUDA-event timestamps on the copy and compute
+    streams; streamed pages never run before their transfer ends
+    (test_scheduler.cpp:309-331) and every page runs every pass (:281-307)."""
+    n = 1 << 12
+    src, dst = O.generate_rmat(12, 16, seed=5)
+    el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
+    csr, pages = built(el, n // 16)
+    sizes = [ps.page_bytes(p, False) for p in pages.pages]
+    budget = 4 * max(sizes) + sum(sizes) // 10
+    with ps.Engine(0, budget) as eng:
+        c = cfg_of(mode=mode, clock=ps.ClockMode.WALL, window=4, record_trace=True,
+                   execution=ps.ExecutionPolicy.FORCE_DENSE)
+        r = eng.run_graph(csr, pages, ps.make_bfs(0, n), c)
+    assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.BFS, 0))
+    kinds = {e.kind for e in r.trace}
+    assert ps.TraceEventKind.XFER_START in kinds and ps.TraceEventKind.KERNEL_END in kinds
+    times = [e.time for e in r.trace]
+    assert times == sorted(times)
+    arrived = {}
+    for e in r.trace:
+        key = (e.pass_index, e.page_id)
+        if e.kind == ps.TraceEventKind.XFER_END:
+            arrived[key] = e.time
+        if e.kind in (ps.TraceEventKind.KERNEL_START, ps.TraceEventKind.REENTRY) and key in arrived:
+            assert e.time >= arrived[key] - 1e-3
+    for p in range(r.metrics.dense_passes):
+        seen = {e.page_id for e in r.trace if e.pass_index == p and
+                e.kind in (ps.TraceEventKind.KERNEL_START, ps.TraceEventKind.REENTRY)}
+        assert seen == set(range(len(pages.pages)))
+    assert ps.write_trace_csv(r.trace).startswith("event_time,event_kind,page_id,pass_index\n")
