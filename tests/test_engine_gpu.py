@@ -428,9 +428,10 @@ def test_wall_trace_from_cuda_events(mode):
     n = 1 << 12
     src, dst = O.generate_rmat(12, 16, seed=5)
     el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
-    csr, pages = built(el, n // 16)
+    csr, pages = built(el, n // 64)
     sizes = [ps.page_bytes(p, False) for p in pages.pages]
     budget = 4 * max(sizes) + sum(sizes) // 10
+    assert budget < sum(sizes)  # out-of-core
     with ps.Engine(0, budget) as eng:
         c = cfg_of(mode=mode, clock=ps.ClockMode.WALL, window=4, record_trace=True,
                    execution=ps.ExecutionPolicy.FORCE_DENSE)
