@@ -515,7 +515,7 @@ void Engine::validate(const sr_run_config& c) const {
     if (!(c.pr_damping >= 0.0 && c.pr_damping < 1.0))
       throw EngineError(SR_E_CONFIG, "pagerank damping must be in [0, 1)");
   }
-  if (c.clock == SR_CLOCK_VIRTUAL && c.algo != SR_ALGO_PAGERANK && world_ > 1)
+  if (c.clock == SR_CLOCK_VIRTUAL && c.algo != SR_ALGO_PAGERANK && comm_)
     throw EngineError(SR_E_CONFIG, "virtual clock runs on a single device");
 }
 
@@ -546,7 +546,7 @@ void Engine::alloc_run_state(const sr_run_config& c) {
     blk_cnt_.reserve(nb + 1);
     blk_edges_.reserve(nb + 1);
     census_part_.reserve(size_t(nb + 1) * 13);
-    if (world_ > 1) round_snap_.reserve(npad);
+    if (comm_) round_snap_.reserve(npad);
   }
   const size_t np = std::max<size_t>(pages_.size(), 1);
   // counter entries per pass: gated (reentry) runs keep one entry per page
@@ -1069,7 +1069,7 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
 }
 
 void Engine::exchange_round(bool pagerank) {
-  if (world_ <= 1) return;
+  if (!comm_) return;  // attached to a world (any size, incl. 1): merge every round
   ncclResult_t r = ncclSuccess;
   SR_CUDA(cudaSetDevice(dev_));
   const NcclApi& nc = nccl();
@@ -1190,7 +1190,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   auto begin_pass = [&]() {
     ctr_used_ = 0;
     SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
-    if (world_ > 1)
+    if (comm_)
       SR_CUDA(cudaMemcpyAsync(round_snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
   };
   auto after_census = [&]() {
@@ -1361,7 +1361,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
     ctr_used_ = 0;
     SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
-    if (world_ > 1) {
+    if (comm_) {
       SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
       SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
     }

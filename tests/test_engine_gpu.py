@@ -453,3 +453,28 @@ def test_wall_trace_from_cuda_events(mode):
                 e.kind in (ps.TraceEventKind.KERNEL_START, ps.TraceEventKind.REENTRY)}
         assert seen == set(range(len(pages.pages)))
     assert ps.write_trace_csv(r.trace).startswith("event_time,event_kind,page_id,pass_index\n")
+
+
+def test_nccl_exchange_path_single_rank():
+    """The multi-GPU round protocol on real NCCL with a 1-rank communicator:
+    every pass runs the values MIN all-reduce, counter SUM all-reduce and the
+    frontier re-derivation from (merged < snapshot); results stay bit-exact."""
+    import ctypes as C
+    from paper_1806_00762_b200 import _native as N
+    buf = (C.c_uint8 * 128)()
+    N.check(N.lib.sr_nccl_unique_id(C.byref(buf)))
+    n = 1 << 12
+    src, dst = O.generate_rmat(12, 16, seed=6)
+    w = O.assign_weights(src.size, 4, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 16)
+    with ps.Engine(0) as eng:
+        eng.attach_world(0, 1, bytes(buf))
+        eng.load(csr, pages)
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+            for pred in PREDS:
+                r = eng.run(program_for(kind, 0, el), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, oracle_values(el, kind, 0)), (kind, pred)
+        pr = eng.run(ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL))
+    ref = O.pagerank(n, src, dst, 20, 0.85)
+    assert np.abs(pr.ranks.astype(np.float64) - ref).max() < PR_TOL
