@@ -59,7 +59,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
-    return p.parse_args()
+    a = p.parse_args()
+    # lean host graph (no host CSR adjacency) when nothing on this run needs it
+    a.lean = a.impl == "ours" and a.no_cpu_baseline and not a.budget_gb and a.gpus == 1
+    return a
 
 
 # ---------------------------------------------------------------------------
@@ -91,14 +94,22 @@ def workload(args):
                 pin[0] = False  # no device (CPU-only reference arm): pageable memory
         return np.empty(count, dtype)
 
+    # The host CSR adjacency is only needed by the reference (cpu_baseline,
+    # --impl reference) and by the out-of-core path; otherwise the engine
+    # derives it on the device from the resident pages and only the
+    # out-degree prefix is built here.
+    lean = getattr(args, "lean", False)
     out_off = pinned(n + 1, np.uint64)
-    out_nbr = pinned(m, np.uint32)
-    out_w = pinned(m if weighted else 0, np.uint32)
+    out_nbr = pinned(0 if lean else m, np.uint32)
+    out_w = pinned(m if (weighted and not lean) else 0, np.uint32)
     in_off = np.zeros(n + 1, np.uint64)
     in_src = pinned(m, np.uint32)
     in_w = pinned(m if weighted else 0, np.uint32)
-    N.check(N.lib.sr_build_csr(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
-                               N.ptr(out_off), N.ptr(out_nbr), N.ptr(out_w), 0))
+    if lean:
+        N.check(N.lib.sr_out_offsets(n, m, N.ptr(el.src), N.ptr(out_off), 0))
+    else:
+        N.check(N.lib.sr_build_csr(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
+                                   N.ptr(out_off), N.ptr(out_nbr), N.ptr(out_w), 0))
     N.check(N.lib.sr_build_csc(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
                                N.ptr(in_off), N.ptr(in_src), N.ptr(in_w), 0))
     npg = (n + cap - 1) // cap
@@ -109,7 +120,7 @@ def workload(args):
     del el
     return dict(csr=csr, pages=pages, n=n, m=m, cap=cap, in_off=in_off, in_src=in_src,
                 in_w=in_w if weighted else None, weighted=weighted, build_s=time.time() - t0,
-                arena=arena, pinned=pin[0])
+                arena=arena, pinned=pin[0], lean=lean)
 
 
 class ClockSampler:
@@ -211,7 +222,8 @@ def run_ours(args, rank, world, local_rank):
             uid[0] = bytes(buf)
         dist.broadcast_object_list(uid, src=0)
         eng.attach_world(rank, world, uid[0])
-    eng.load(csr, pages)
+    eng.load_csr(csr, with_edges=not W.get("lean"))
+    eng.load_pages(pages)
 
     def one():
         r = eng.run(prog, cfg, want_values=False)

@@ -278,6 +278,14 @@ int sr_build_csc(uint32_t num_vertices, uint64_t num_edges, const uint32_t* src,
                  uint32_t* in_sources, uint32_t* in_weights, int threads);
 int sr_page_offsets(uint32_t num_vertices, uint32_t page_vertex_capacity,
                     const uint64_t* in_offsets_global, uint32_t* local_offsets);
+/* Out-degree prefix (CSR out_offsets) without the adjacency: enough for
+ * sr_load_csr(..., NULL, NULL) when the pages are resident. */
+int sr_out_offsets(uint32_t num_vertices, uint64_t num_edges, const uint32_t* src,
+                   uint64_t* out_offsets, int threads);
+/* symmetrize (graph.cpp:102-118), parallel: 2*num_edges outputs. */
+int sr_symmetrize(uint64_t num_edges, const uint32_t* src, const uint32_t* dst,
+                  const uint32_t* w, uint32_t* out_src, uint32_t* out_dst, uint32_t* out_w,
+                  int threads);
 
 #ifdef __cplusplus
 }

@@ -204,6 +204,8 @@ SIGNATURES = {
     "sr_build_csr": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
     "sr_build_csc": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
     "sr_page_offsets": (C.c_int, [_U32, _U32, _VP, _VP]),
+    "sr_out_offsets": (C.c_int, [_U32, _U64, _VP, _VP, C.c_int]),
+    "sr_symmetrize": (C.c_int, [_U64, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
 }
 
 

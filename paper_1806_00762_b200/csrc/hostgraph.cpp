@@ -165,6 +165,46 @@ int sr_build_csc(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* ds
   return SR_OK;
 }
 
+int sr_out_offsets(uint32_t n, uint64_t m, const uint32_t* src, uint64_t* out_offsets,
+                   int threads) {
+  // out-degree prefix only (the push adjacency can be derived on the device)
+  const int T = clamp_threads(threads);
+  std::vector<std::atomic<uint64_t>> deg(size_t(n) + 1);
+  for (auto& d : deg) d.store(0, std::memory_order_relaxed);
+  std::atomic<bool> bad{false};
+  run_threads(T, [&](int t) {
+    const uint64_t lo = m * t / T, hi = m * (t + 1) / T;
+    for (uint64_t e = lo; e < hi; ++e) {
+      if (src[e] >= n) {
+        bad = true;
+        return;
+      }
+      deg[size_t(src[e]) + 1].fetch_add(1, std::memory_order_relaxed);
+    }
+  });
+  if (bad) return SR_E_INPUT;
+  out_offsets[0] = 0;
+  for (size_t v = 1; v <= n; ++v) out_offsets[v] = out_offsets[v - 1] + deg[v].load();
+  return SR_OK;
+}
+
+int sr_symmetrize(uint64_t m, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                  uint32_t* osrc, uint32_t* odst, uint32_t* ow, int threads) {
+  // symmetrize (graph.cpp:102-118): edge i then its reverse, weights copied
+  const int T = clamp_threads(threads);
+  run_threads(T, [&](int t) {
+    const uint64_t lo = m * t / T, hi = m * (t + 1) / T;
+    for (uint64_t i = lo; i < hi; ++i) {
+      osrc[2 * i] = src[i];
+      odst[2 * i] = dst[i];
+      osrc[2 * i + 1] = dst[i];
+      odst[2 * i + 1] = src[i];
+      if (w) ow[2 * i] = ow[2 * i + 1] = w[i];
+    }
+  });
+  return SR_OK;
+}
+
 int sr_page_offsets(uint32_t n, uint32_t cap, const uint64_t* in_off, uint32_t* local) {
   if (cap < 1) return SR_E_CONFIG;
   const uint64_t np = (uint64_t(n) + cap - 1) / cap;

@@ -248,15 +248,16 @@ def page_bytes(page: CscPage, weighted: bool, entry_bytes: int = kEntryBytes) ->
     return int(entries) * entry_bytes
 
 
-def symmetrize(el: EdgeList) -> EdgeList:
+def symmetrize(el: EdgeList, threads: int = 0) -> EdgeList:
     """Append the reverse of every edge, interleaved as in graph.cpp:102-118."""
     el.validate()
     m = el.num_edges()
     src = np.empty(2 * m, np.uint32)
     dst = np.empty(2 * m, np.uint32)
-    src[0::2], src[1::2] = el.src, el.dst
-    dst[0::2], dst[1::2] = el.dst, el.src
-    w = np.repeat(el.weights, 2) if el.weighted() else np.zeros(0, np.uint32)
+    w = np.empty(2 * m if el.weighted() else 0, np.uint32)
+    if m:
+        N.check(N.lib.sr_symmetrize(m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
+                                    N.ptr(src), N.ptr(dst), N.ptr(w), threads))
     return EdgeList(el.num_vertices, src, dst, w)
 
 
