@@ -241,6 +241,9 @@ int sr_device_sync(int device);
 /* Host-link roofline denominator: pinned host -> device cudaMemcpyAsync of
  * `bytes`, best of `reps`, timed with CUDA events (GB/s = 1e9 B/s). */
 int sr_bench_h2d(int device, uint64_t bytes, uint32_t reps, double* gbps);
+/* Evict the L2 between timed steps: write a device buffer of `bytes`
+ * (> L2 size) on the context's compute stream. */
+int sr_flush_l2(sr_ctx* ctx, uint64_t bytes);
 
 /* ---- multi-GPU (one process per GPU) ----------------------------------- */
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the host. */

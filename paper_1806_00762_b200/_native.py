@@ -197,6 +197,7 @@ SIGNATURES = {
     "sr_host_free": (None, [_VP]),
     "sr_device_sync": (C.c_int, [C.c_int]),
     "sr_bench_h2d": (C.c_int, [C.c_int, _U64, _U32, C.POINTER(_D)]),
+    "sr_flush_l2": (C.c_int, [_VP, _U64]),
     "sr_attach_world": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(C.c_uint8 * 128)]),
     "sr_shard_plan": (C.c_int, [_U32, _VP, _U32, _VP]),
     "sr_rmat_generate": (C.c_int, [C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP, C.c_int]),

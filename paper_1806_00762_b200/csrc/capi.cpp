@@ -260,6 +260,11 @@ int sr_bench_h2d(int device, uint64_t bytes, uint32_t reps, double* gbps) {
   });
 }
 
+int sr_flush_l2(sr_ctx* ctx, uint64_t bytes) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->flush_l2(bytes); });
+}
+
 int sr_attach_world(sr_ctx* ctx, int rank, int world, const uint8_t id[128]) {
   if (!ctx) return SR_E_CONFIG;
   return guard(ctx, [&] { ctx->eng->attach_world(rank, world, id); });

@@ -1495,6 +1495,13 @@ double Engine::collect_relax_seconds() {
   return total;
 }
 
+void Engine::flush_l2(uint64_t bytes) {
+  SR_CUDA(cudaSetDevice(dev_));
+  l2_flush_.reserve(bytes);
+  SR_CUDA(cudaMemsetAsync(l2_flush_.p, int(++flush_gen_ & 0xff), bytes, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+}
+
 void Engine::attach_world(int rank, int world, const uint8_t id[128]) {
   SR_CUDA(cudaSetDevice(dev_));
   if (world < 1 || rank < 0 || rank >= world) throw EngineError(SR_E_CONFIG, "bad rank/world");

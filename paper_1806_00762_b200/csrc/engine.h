@@ -127,6 +127,9 @@ class Engine {
   uint64_t verify_fixpoint(int algo, const uint32_t* values_host);
   void bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges);
   void attach_world(int rank, int world, const uint8_t id[128]);
+  void flush_l2(uint64_t bytes);
+  DBuf<uint8_t> l2_flush_;
+  unsigned flush_gen_ = 0;
 
   std::string err;
   std::vector<sr_trace_event> trace;

@@ -567,7 +567,11 @@ class Engine:
         self.load_pages(pages)
 
     def load_csr(self, csr: CsrGraph, with_edges: bool = True) -> None:
-        N.check(N.lib.sr_load_csr(self._h, csr.num_vertices, csr.num_edges(),
+        # |E| from the offsets: a lean CsrGraph (offsets only) has no adjacency
+        m = int(csr.out_offsets[-1]) if csr.out_offsets.size else 0
+        if with_edges and csr.out_neighbors.size != m:
+            raise InputError("csr: out_neighbors length does not match out_offsets[-1]")
+        N.check(N.lib.sr_load_csr(self._h, csr.num_vertices, m,
                                   N.ptr(csr.out_offsets),
                                   N.ptr(csr.out_neighbors) if with_edges else None,
                                   N.ptr(csr.out_weights) if with_edges else None), self._h)
@@ -636,6 +640,9 @@ class Engine:
         if config.record_trace:
             res.trace = self.trace()
         return res
+
+    def flush_l2(self, nbytes: int = 512 << 20) -> None:
+        N.check(N.lib.sr_flush_l2(self._h, int(nbytes)), self._h)
 
     def trace(self) -> List[TraceEvent]:
         n = C.c_uint64()
