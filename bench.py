@@ -277,18 +277,23 @@ def run_ours(args, rank, world, local_rank):
         parity = {"fixpoint_violations": eng.verify_fixpoint(ps.AlgoKind.CC, res.values)}
 
     # roofline: the dominant kernel (K1 dense pull) timed launch by launch with
-    # CUDA events on the engine stream inside the timed runs; algorithmic bytes
-    # per SURVEY §8(d): per edge read (src 4 + gathered value 4 [+ weight 4])
-    # + 8 B per attempted destination, over the dense/recovery passes.
+    # CUDA events on the engine stream inside the timed runs.  Algorithmic
+    # bytes per SURVEY §8(d) -- per edge read: in_sources 4 [+ weight 4];
+    # per gathered source value: 4 (destinations/edges that provably cannot
+    # improve are not gathered and not charged); per attempted destination 8 --
+    # over the dense/recovery passes.
     roof = None
     if not args.budget_gb and algo != 3:
-        per_edge = 12 if algo == 2 else 8
+        per_edge = 8 if algo == 2 else 4
         k1_bytes = k1_s = 0.0
-        k1_launches = 0
+        k1_launches = k1_gathers = k1_edges = 0
         for r in runs:
             for st in r.metrics.per_pass:
                 if st.kind != ps.PassKind.SPARSE_PUSH:
                     k1_bytes += per_edge * st.edges_read + 8 * st.attempts
+                    k1_edges += st.edges_read
+            k1_bytes += 4 * r.metrics.gathers
+            k1_gathers += r.metrics.gathers
             k1_s += r.metrics.relax_seconds
             k1_launches += r.metrics.relax_launches
         peak, src_ = measured_peaks()
@@ -301,7 +306,8 @@ def run_ours(args, rank, world, local_rank):
                 "algorithmic_bytes_per_launch": int(k1_bytes / max(k1_launches, 1)),
                 "launch_ms": round(k1_s / max(k1_launches, 1) * 1e3, 4),
                 "launches": k1_launches, "share_of_step": round(k1_s / sum(dev_s), 3),
-                "per_unit": f"{per_edge} B/edge read + 8 B/attempted destination",
+                "per_unit": f"{per_edge} B/edge read + 4 B/gathered source + 8 B/attempted destination",
+                "gathered_fraction": round(k1_gathers / max(k1_edges, 1), 4),
                 "isolated_sweep": {"ms": round(ms, 4), "edges": edges,
                                    "note": "gate-off sweep over the converged values"}}
     elif algo == 3:

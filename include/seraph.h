@@ -147,6 +147,7 @@ typedef struct {
   uint64_t kernel_runs;    /* page-runs (DensePassOutcome::kernel_runs) */
   double relax_seconds;    /* sum of timed K1/K8 launch durations (profile_kernels) */
   uint64_t relax_launches;
+  uint64_t gathers;        /* source values K1/K8 actually loaded (skips excluded) */
 } sr_metrics;
 
 typedef struct {

@@ -144,6 +144,7 @@ class MetricsC(C.Structure):
         ("kernel_runs", C.c_uint64),
         ("relax_seconds", C.c_double),
         ("relax_launches", C.c_uint64),
+        ("gathers", C.c_uint64),
     ]
 
 

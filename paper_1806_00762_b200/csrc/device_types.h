@@ -43,6 +43,7 @@ struct RunCtr {
   unsigned long long valid;
   unsigned long long skipped;
   unsigned long long edges;
+  unsigned long long gathers;  // source values actually loaded (roofline bytes)
 };
 
 // Scalars produced by the per-pass census (K4/K5), read back once per pass.

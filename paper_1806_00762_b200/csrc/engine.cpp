@@ -995,6 +995,7 @@ PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool reco
     st.valid = ctr_h_.p[0].valid;
     st.skipped = ctr_h_.p[0].skipped;
     st.edges = ctr_h_.p[0].edges;
+    gathers_total_ += ctr_h_.p[0].gathers;
     return st;
   };
   (void)np;
@@ -1085,7 +1086,8 @@ void Engine::exchange_round(bool pagerank) {
                        comm_, cs_);
   }
   if (r == ncclSuccess && ctr_used_)
-    r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * 4, ncclUint64, ncclSum, comm_, cs_);
+    r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), ncclUint64,
+                     ncclSum, comm_, cs_);
   nc.GroupEnd();
   if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
   if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
@@ -1107,6 +1109,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   pr_damp_ = cfg.pr_damping;
   profile_kernels_ = cfg.profile_kernels != 0;
   relax_ev_used_ = 0;
+  gathers_total_ = 0;
   wtrace_.clear();
   wtrace_pool_used_ = 0;
   trace.clear();
@@ -1125,6 +1128,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   else run_traversal(cfg, values_out, m, passes);
   m.kernel_launches = launches_;
   m.h2d_bytes = h2d_bytes_;
+  m.gathers = gathers_total_;
   finish_wall_trace();
   if (profile_kernels_) {
     m.relax_seconds = collect_relax_seconds();
@@ -1181,6 +1185,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   };
   auto sum_ctr = [&](sr_pass_stats& st) {
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
+      gathers_total_ += ctr_h_.p[i].gathers;
       st.attempts += ctr_h_.p[i].attempts;
       st.valid_updates += ctr_h_.p[i].valid;
       st.skipped += ctr_h_.p[i].skipped;
@@ -1378,6 +1383,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     st.pass_index = it;
     st.kind = SR_PASS_DENSE_PULL;
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
+      gathers_total_ += ctr_h_.p[i].gathers;
       st.attempts += ctr_h_.p[i].attempts;
       st.edges_read += ctr_h_.p[i].edges;
     }

@@ -92,20 +92,32 @@ struct ActEntry {
 };
 
 struct LaneCtr {
-  unsigned long long attempts, valid, skipped, edges;
-  __device__ void clear() { attempts = valid = skipped = edges = 0; }
+  unsigned long long attempts, valid, skipped, edges, gathers;
+  __device__ void clear() { attempts = valid = skipped = edges = gathers = 0; }
 };
 
 __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
   unsigned long long at = warp_sum(c.attempts), va = warp_sum(c.valid),
-                     sk = warp_sum(c.skipped), ed = warp_sum(c.edges);
+                     sk = warp_sum(c.skipped), ed = warp_sum(c.edges),
+                     ga = warp_sum(c.gathers);
   if (lane == 0 && dst) {
     if (at) atomicAdd(&dst->attempts, at);
     if (va) atomicAdd(&dst->valid, va);
     if (sk) atomicAdd(&dst->skipped, sk);
     if (ed) atomicAdd(&dst->edges, ed);
+    if (ga) atomicAdd(&dst->gathers, ga);
   }
   c.clear();
+}
+
+// Smallest candidate any in-edge can produce (values are >= 0):
+// combine(0, w) = 1 for BFS, 0 for CC; SSSP bounds per edge by its weight.
+// A destination whose value is <= this bound cannot improve: its sources
+// are not gathered (it still counts as attempted with all its edges read,
+// the reference's accounting, engine.cpp:103-128).
+template <int A>
+__device__ __forceinline__ uint32_t candidate_floor() {
+  return A == kBfs ? 1u : 0u;
 }
 
 // End-of-kernel flush: warp sums -> shared memory -> one atomic per counter
@@ -115,28 +127,30 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
 // shrink the L1 that serves the gathers.
 __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t lane_min,
                                             Census* census, uint32_t* scratch) {
+  constexpr int kCtr = 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
-  uint32_t* mins = scratch + 2 * 4 * kWarpsPerBlock;
-  const unsigned long long at = warp_sum(c.attempts), va = warp_sum(c.valid),
-                           sk = warp_sum(c.skipped), ed = warp_sum(c.edges);
+  uint32_t* mins = scratch + 2 * kCtr * kWarpsPerBlock;
+  const unsigned long long v[kCtr] = {warp_sum(c.attempts), warp_sum(c.valid),
+                                      warp_sum(c.skipped), warp_sum(c.edges),
+                                      warp_sum(c.gathers)};
   lane_min = warp_min(lane_min);
   __syncthreads();  // every warp is done with its tile scratch
   if (lane == 0) {
-    red[0 * kWarpsPerBlock + warp] = at;
-    red[1 * kWarpsPerBlock + warp] = va;
-    red[2 * kWarpsPerBlock + warp] = sk;
-    red[3 * kWarpsPerBlock + warp] = ed;
+#pragma unroll
+    for (int k = 0; k < kCtr; ++k) red[k * kWarpsPerBlock + warp] = v[k];
     mins[warp] = lane_min;
   }
   __syncthreads();
   if (warp == 0) {
-    unsigned long long x = red[lane];  // lane = counter * 8 + warp
-#pragma unroll
-    for (int off = 4; off > 0; off >>= 1) x += __shfl_down_sync(kFull, x, off, 8);
     uint32_t m = lane < kWarpsPerBlock ? mins[lane] : kUnreached;
     m = warp_min(m);
-    if (dst && (lane & 7) == 0 && x) atomicAdd(&dst->attempts + (lane >> 3), x);
+    if (lane < kCtr && dst) {
+      unsigned long long x = 0;
+#pragma unroll
+      for (int w = 0; w < kWarpsPerBlock; ++w) x += red[lane * kWarpsPerBlock + w];
+      if (x) atomicAdd(&dst->attempts + lane, x);
+    }
     if (lane == 0 && census && m != kUnreached) atomicMin(&census->min_changed, m);
   }
   c.clear();
@@ -213,7 +227,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           c.skipped += !att;
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
-        if (!att) continue;
+        if (!att || cur <= candidate_floor<A>()) continue;
         uint32_t best = kUnreached;
         uint32_t e = tile.x + lane;
 #pragma unroll 8
@@ -222,6 +236,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           const uint32_t w = (A == kSssp) ? __ldcs(wts + e) : 0u;
           if (A == kSssp && w >= cur) continue;  // cannot improve: skip the gather
           const uint32_t sv = DET ? __ldg(values_ro + sidx) : a.values[sidx];
+          c.gathers += 1;
           best = min(best, combine<A>(sv, w));
         }
         best = warp_min(best);
@@ -266,13 +281,14 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         c.attempts += att;
         c.skipped += (in && !att);
         c.edges += att ? deg : 0u;
+        const bool need = att && cur > candidate_floor<A>();  // can it still improve?
         const bool has = in && deg > 0;
         const unsigned m = __ballot_sync(kFull, has);
-        any_att |= __ballot_sync(kFull, has && att);
+        any_att |= __ballot_sync(kFull, has && need);
         if (has) {
           const uint32_t pos = n_ent + __popc(m & lanemask_lt());
           s_pref[warp][pos] = lo - ebase;
-          s_loc[warp][pos] = i | (att ? 0x80000000u : 0u);
+          s_loc[warp][pos] = i | (need ? 0x80000000u : 0u);
           s_cur[warp][pos] = cur;
           best_of[pos] = kUnreached;
         }
@@ -341,6 +357,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             for (int t = 0; t < kLaneEdges; ++t)
               sv[t] = (live >> t & 1u) ? (DET ? __ldg(values_ro + sv_idx[t]) : a.values[sv_idx[t]])
                                        : kUnreached;
+            c.gathers += __popc(live);
             uint32_t run_ent = 0xffffffffu, run_best = kUnreached;
 #pragma unroll
             for (int t = 0; t < kLaneEdges; ++t) {
@@ -525,6 +542,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
         }
         float sum = 0.f;
         uint32_t e = tile.x + lane;
+        if (e < tile.y) c.gathers += (tile.y - e + 31) / 32;
 #pragma unroll 8
         for (; e < tile.y; e += 32) sum += __ldg(contrib + __ldcs(src + e));
         sum = warp_sum(sum);
@@ -595,6 +613,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t)
             x[t] = (live >> t & 1u) ? __ldg(contrib + sidx[t]) : 0.f;
+          c.gathers += __popc(live);
           uint32_t run_ent = 0xffffffffu;
           float run = 0.f;
 #pragma unroll
@@ -658,7 +677,7 @@ __global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, flo
 // ---------------------------------------------------------------------------
 template <int A, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
-  __shared__ __align__(16) uint32_t s_scratch[2 * 4 * kWarpsPerBlock + kWarpsPerBlock];
+  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kWarpsPerBlock;
