@@ -102,6 +102,7 @@ struct PrArgs {
   float* contrib_out;
   const float* inv_outdeg;
   float* hub_sum;
+  float* acc;   // source-blocked mode: partial sums accumulate here (else null)
   RunCtr* ctr;
   float base;   // (1-d)/N
   float damp;   // d

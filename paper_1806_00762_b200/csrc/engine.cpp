@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cstdlib>
 #include <thread>
 
 #include "kernels.h"
@@ -323,6 +324,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
   }
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
+  sb_.built = false;
   page_desc_h_.assign(np, PageDesc{});
   for (uint32_t p = 0; p < np; ++p) {
     page_desc_h_[p].vertex_begin = pages_[p].vb;
@@ -1354,10 +1356,153 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 }
 
 // ---------------------------------------------------------------------------
+// Source-blocked sub-pages for PageRank: when the contrib array outgrows the
+// L2, every iteration sweeps the sub-pages block by block so the gathers of
+// one sweep stay inside a blk_verts slice (SERAPH_PR_BLOCK_VERTS, default
+// 16 Mi vertices = 64 MB of f32; 0 disables).
+// ---------------------------------------------------------------------------
+bool Engine::build_src_blocks() {
+  if (sb_.built) return true;
+  if (!all_resident_ || world_ > 1 || comm_) return false;
+  uint64_t blk = 16ull << 20;
+  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) blk = std::strtoull(e, nullptr, 10);
+  if (blk == 0 || n_ <= blk) return false;
+  const uint32_t np = uint32_t(pages_.size());
+  for (uint32_t p = 0; p < np; ++p)
+    if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
+  const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
+  const uint32_t n_tiles = pages_.back().tile_end;
+  // 1) counts per (block, destination)
+  DBuf<uint32_t> cnt;
+  cnt.reserve(size_t(nb) * n_);
+  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
+  launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
+                   cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
+  // 2) page-local offsets per sub-page, sub-page sizes
+  DBuf<unsigned long long> goff, bp_edges, bp_base;
+  goff.reserve(size_t(nb) * n_);
+  bp_edges.reserve(size_t(nb) * np);
+  bp_base.reserve(size_t(nb) * np);
+  launch_src_block_scan(cnt.p, goff.p, page_desc_.p, np, nb, n_, bp_edges.p, cs_);
+  std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
+  SR_CUDA(cudaMemcpyAsync(edges_h.data(), bp_edges.p, edges_h.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  unsigned long long at = 0;
+  for (size_t k = 0; k < edges_h.size(); ++k) {  // block-major, 32 B aligned sub-pages
+    base_h[k] = at;
+    at += (edges_h[k] + 7) & ~7ull;
+    if (edges_h[k] > 0xffffffffull) return false;
+  }
+  sb_.src.reserve(at + 8);
+  SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
+  // 3) scatter the sources (cnt reused as cursors)
+  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
+  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
+                   cnt.p, goff.p, sb_.src.p, bp_base.p, sm_count_ * 8, cs_);
+  // 4) u32 local offsets, copied back to cut tiles on the host
+  const size_t per_block = size_t(n_) + np;
+  sb_.offs.reserve(size_t(nb) * per_block);
+  launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
+  std::vector<uint32_t> offs_h(size_t(nb) * per_block);
+  SR_CUDA(cudaMemcpyAsync(offs_h.data(), sb_.offs.p, offs_h.size() * 4, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaGetLastError());
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  std::vector<TileJob> jobs;
+  for (uint32_t b = 0; b < nb; ++b)
+    for (uint32_t p = 0; p < np; ++p) {
+      const uint32_t range = pages_[p].ve - pages_[p].vb;
+      for (uint32_t x = 0; x < range; x += (1u << 20))
+        jobs.push_back(TileJob{b * np + p, x, std::min(x + (1u << 20), range), {}, {}});
+    }
+  parallel_for(jobs.size(), [&](size_t j) {
+    const uint32_t k = jobs[j].page, b = k / np, p = k % np;
+    cut_tiles(offs_h.data() + size_t(b) * per_block + size_t(p) * cap_ + p, pages_[p].vb, jobs[j]);
+  });
+  std::vector<uint4> tiles;
+  std::vector<uint32_t> tpage;
+  sb_.block_tile_begin.assign(nb + 1, 0);
+  for (auto& j : jobs) {
+    if (j.page % np == 0 && j.lo == 0) sb_.block_tile_begin[j.page / np] = uint32_t(tiles.size());
+    for (const uint4& t : j.tiles) {
+      tiles.push_back(t);
+      tpage.push_back(j.page);
+    }
+  }
+  sb_.block_tile_begin[nb] = uint32_t(tiles.size());
+  std::vector<PageDesc> desc(size_t(nb) * np);
+  for (uint32_t b = 0; b < nb; ++b)
+    for (uint32_t p = 0; p < np; ++p) {
+      PageDesc& d = desc[size_t(b) * np + p];
+      d.vertex_begin = pages_[p].vb;
+      d.range = pages_[p].ve - pages_[p].vb;
+      d.edge_count = edges_h[size_t(b) * np + p];
+      d.offs = sb_.offs.p + size_t(b) * per_block + size_t(p) * cap_ + p;
+      d.src = sb_.src.p + base_h[size_t(b) * np + p];
+      d.w = nullptr;
+    }
+  sb_.tiles.reserve(std::max<size_t>(tiles.size(), 1));
+  sb_.tile_page.reserve(std::max<size_t>(tiles.size(), 1));
+  sb_.desc.reserve(desc.size());
+  SR_CUDA(cudaMemcpy(sb_.tiles.p, tiles.data(), tiles.size() * 16, cudaMemcpyHostToDevice));
+  SR_CUDA(cudaMemcpy(sb_.tile_page.p, tpage.data(), tpage.size() * 4, cudaMemcpyHostToDevice));
+  SR_CUDA(cudaMemcpy(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc), cudaMemcpyHostToDevice));
+  sb_.acc.reserve(n_);
+  SR_CUDA(cudaMemset(sb_.acc.p, 0, size_t(n_) * 4));
+  sb_.blk_verts = uint32_t(blk);
+  sb_.n_blocks = nb;
+  sb_.built = true;
+  return true;
+}
+
+void Engine::pr_blocked_pass(float base, float damp) {
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
+    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
+    if (t1 <= t0) continue;
+    PrArgs a{};
+    a.work = next_work_counter();
+    a.tiles = sb_.tiles.p;
+    a.tile_page = sb_.tile_page.p;
+    a.pages = sb_.desc.p;
+    a.seg.n = 1;
+    a.seg.tile_begin[0] = t0;
+    a.seg.task_prefix[0] = 0;
+    a.seg.task_prefix[1] = t1 - t0;
+    a.contrib_in = contrib_a_.p;
+    a.rank_out = rank_b_.p;
+    a.contrib_out = contrib_b_.p;
+    a.inv_outdeg = inv_outdeg_.p;
+    a.hub_sum = hub_sum_.p;
+    a.acc = sb_.acc.p;
+    a.ctr = nullptr;
+    a.base = base;
+    a.damp = damp;
+    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
+    if (profile_kernels_) {
+      if (relax_ev_used_ == relax_ev_.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        SR_CUDA(cudaEventCreate(&e.first));
+        SR_CUDA(cudaEventCreate(&e.second));
+        relax_ev_.push_back(e);
+      }
+      evp = &relax_ev_[relax_ev_used_++];
+      SR_CUDA(cudaEventRecord(evp->first, cs_));
+    }
+    launch_pr_pull(a, std::max(grid, 1), cs_);
+    SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    ++launches_;
+  }
+  launch_pr_block_finalize(n_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p, base, damp, cs_);
+}
+
+// ---------------------------------------------------------------------------
 // PageRank (new algorithm; conventions pinned in DESIGN.md §2)
 // ---------------------------------------------------------------------------
 void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
                           std::vector<sr_pass_stats>& passes) {
+  const bool blocked = build_src_blocks();
   const auto wall0 = std::chrono::steady_clock::now();
   SR_CUDA(cudaEventRecord(ev_start_, cs_));
   launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
@@ -1370,10 +1515,23 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
       SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
       SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
     }
-    PassOut po = dense_pass_wall(cfg, kGateOff, false, it, true);
-    launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
-                           inv_outdeg_.p, float((1.0 - cfg.pr_damping) / double(n_)),
-                           float(cfg.pr_damping), cs_);
+    PassOut po;
+    const float base = float((1.0 - cfg.pr_damping) / double(n_));
+    if (blocked) {
+      pr_blocked_pass(base, float(cfg.pr_damping));
+      po.kernel_runs = sb_.n_blocks * pages_.size();
+      if (!first_touch_done_) {
+        for (const auto& pm : pages_) {
+          po.pages_transferred += 1;
+          po.bytes_transferred += pm.bytes;
+        }
+        first_touch_done_ = true;
+      }
+    } else {
+      po = dense_pass_wall(cfg, kGateOff, false, it, true);
+      launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
+                             inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
+    }
     exchange_round(true);
     if (ctr_used_)
       SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
@@ -1386,6 +1544,11 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
       gathers_total_ += ctr_h_.p[i].gathers;
       st.attempts += ctr_h_.p[i].attempts;
       st.edges_read += ctr_h_.p[i].edges;
+    }
+    if (blocked) {  // every destination and edge once per iteration
+      st.attempts = n_;
+      st.edges_read = page_edges_total_;
+      gathers_total_ += page_edges_total_;
     }
     st.changed_vertices = n_;
     m.pages_transferred += po.pages_transferred;

@@ -267,6 +267,21 @@ class Engine {
   size_t relax_ev_used_ = 0;
   double collect_relax_seconds();
 
+  // Source-blocked copy of the resident pages for PageRank (K8 locality):
+  // sub-page (p, b) holds page p's in-edges whose source lies in block b.
+  struct SrcBlocks {
+    bool built = false;
+    uint32_t blk_verts = 0, n_blocks = 0;
+    DBuf<uint32_t> offs, src;
+    DBuf<uint4> tiles;
+    DBuf<uint32_t> tile_page;
+    DBuf<PageDesc> desc;
+    DBuf<float> acc;
+    std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
+  } sb_;
+  bool build_src_blocks();
+  void pr_blocked_pass(float base, float damp);
+
   // multi-GPU
   int rank_ = 0, world_ = 1;
   ncclComm_t comm_ = nullptr;

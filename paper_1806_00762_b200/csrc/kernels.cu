@@ -483,6 +483,142 @@ csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Source-blocked page split (K8 locality): every in-edge
+// (s -> v) of a resident page goes to sub-page (page, s / blk_verts), so one
+// sweep over the sub-pages of a block gathers only a blk_verts-wide slice of
+// the vertex array (L2-resident).  mode 0 counts per (block, destination),
+// mode 1 scatters the sources using goff (exclusive scan of the counts) and
+// cur (zeroed counts) as cursors.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlockThreads)
+src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
+                 const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
+                 uint32_t n, uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
+                 const unsigned long long* __restrict__ goff, uint32_t* out_src,
+                 const unsigned long long* __restrict__ bp_base) {
+  __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
+  __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  auto emit = [&](uint32_t p, uint32_t v, uint32_t s) {
+    const uint32_t b = s / blk_verts;
+    const size_t k = size_t(b) * n + v;
+    if (mode == 0) {
+      atomicAdd(cnt + k, 1u);
+    } else {
+      const uint32_t at = atomicAdd(cnt + k, 1u);
+      out_src[bp_base[size_t(b) * n_pages + p] + goff[k] + at] = s;
+    }
+  };
+  for (uint32_t ti = tile_lo + blockIdx.x * kWarpsPerBlock + warp; ti < tile_hi;
+       ti += gridDim.x * kWarpsPerBlock) {
+    const uint32_t pg = tile_page[ti];
+    const PageDesc pd = pages[pg];
+    const uint4 tile = tiles[ti];
+    const uint32_t* __restrict__ src = pd.src;
+    if (tile.w & kHubFlag) {
+      const uint32_t v = pd.vertex_begin + tile.z;
+      for (uint32_t e = tile.x + lane; e < tile.y; e += 32) emit(pg, v, src[e]);
+      continue;
+    }
+    const uint32_t dl = tile.z, dh = tile.w;
+    const uint32_t ebase = tile.x & ~7u;
+    uint32_t n_ent = 0;
+    for (uint32_t base = dl; base < dh; base += 32) {
+      const uint32_t i = base + lane;
+      uint32_t lo = 0, deg = 0;
+      if (i < dh) {
+        lo = pd.offs[i];
+        deg = pd.offs[i + 1] - lo;
+      }
+      const unsigned m = __ballot_sync(kFull, deg > 0);
+      if (deg > 0) {
+        const uint32_t pos = n_ent + __popc(m & lanemask_lt());
+        s_pref[warp][pos] = lo - ebase;
+        s_loc[warp][pos] = i;
+      }
+      n_ent += __popc(m);
+    }
+    __syncwarp();
+    const uint32_t lo_pos = tile.x - ebase, span = tile.y - ebase;
+    for (uint32_t r0 = 0; n_ent && r0 < span; r0 += 32 * kLaneEdges) {
+      const uint32_t pos0 = r0 + lane * kLaneEdges;
+      if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
+        const uint32_t q = max(pos0, lo_pos);
+        uint32_t lo = 0, hi = n_ent - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_pref[warp][mid] <= q) lo = mid;
+          else hi = mid - 1;
+        }
+        uint32_t ent = lo;
+        uint32_t nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+        for (int t = 0; t < kLaneEdges; ++t) {
+          const uint32_t pp = pos0 + t;
+          if (pp >= span) break;
+          if (pp >= nxt) {
+            ++ent;
+            nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
+          }
+          if (pp < lo_pos) continue;
+          emit(pg, pd.vertex_begin + s_loc[warp][ent], src[ebase + pp]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Per-block exclusive scan helper: goff[b*n + v] = sum_{u < v, u in the same
+// page} cnt[b*n + u] (page-local offsets, u64), one thread block per
+// (page, block) pair, sequential chunks of 1024 with warp scans.
+__global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __restrict__ cnt,
+                                                              unsigned long long* goff,
+                                                              const PageDesc* __restrict__ pages,
+                                                              uint32_t n_pages, uint32_t n,
+                                                              unsigned long long* bp_edges) {
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const uint32_t pb = blockIdx.x;  // = b * n_pages + p
+  const uint32_t p = pb % n_pages, b = pb / n_pages;
+  const PageDesc pd = pages[p];
+  const size_t base = size_t(b) * n + pd.vertex_begin;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < pd.range; c0 += 1024) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned long long x = i < pd.range ? cnt[base + i] : 0ull;
+    const unsigned long long incl = warp_incl_scan(x, lane);
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned long long t = s_w[lane];
+      const unsigned long long si = warp_incl_scan(t, lane);
+      s_w[lane] = si - t;
+    }
+    __syncthreads();
+    const unsigned long long ex = s_carry + s_w[w] + incl - x;
+    if (i < pd.range) goff[base + i] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = ex + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bp_edges[pb] = s_carry;
+}
+
+__global__ void pr_block_finalize_kernel(uint32_t n, float* acc, float* rank_out, float* contrib_out,
+                                         const float* __restrict__ inv_outdeg, float base,
+                                         float damp) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const float r = base + damp * acc[v];
+    rank_out[v] = r;
+    contrib_out[v] = r * inv_outdeg[v];
+    acc[v] = 0.f;
+  }
+}
+
 __global__ void outdeg_kernel(const unsigned long long* __restrict__ off, uint32_t n,
                               uint32_t* deg) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
@@ -546,7 +682,10 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
 #pragma unroll 8
         for (; e < tile.y; e += 32) sum += __ldg(contrib + __ldcs(src + e));
         sum = warp_sum(sum);
-        if (lane == 0) atomicAdd(a.hub_sum + (tile.w & ~kHubFlag), sum);
+        if (lane == 0) {
+          if (a.acc) atomicAdd(a.acc + vb + d, sum);  // source-blocked partial
+          else atomicAdd(a.hub_sum + (tile.w & ~kHubFlag), sum);
+        }
         continue;
       }
       const uint32_t dl = tile.z, dh = tile.w;
@@ -559,7 +698,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
         if (in) {
           lo = __ldcs(offs + i);
           deg = __ldcs(offs + i + 1) - lo;
-          if (deg == 0) {  // no in-edges: teleport share only
+          if (deg == 0 && !a.acc) {  // no in-edges: teleport share only
             const uint32_t v = vb + i;
             a.rank_out[v] = a.base;
             a.contrib_out[v] = a.base * a.inv_outdeg[v];
@@ -632,6 +771,10 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
       __syncwarp();
       for (uint32_t i = lane; i < n_ent; i += 32) {
         const uint32_t v = vb + s_loc[warp][i];
+        if (a.acc) {  // source-blocked: this block's partial sum
+          atomicAdd(a.acc + v, sum_of[i]);
+          continue;
+        }
         const float r = a.base + a.damp * sum_of[i];
         a.rank_out[v] = r;
         a.contrib_out[v] = r * a.inv_outdeg[v];
@@ -1299,6 +1442,58 @@ void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const 
   if (uint32_t(grid) > need) grid = int(need);
   csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, tile_lo, tile_hi,
                                                        out_off, cursor, out_nbr, out_w);
+}
+
+void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
+                      const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
+                      uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
+                      const unsigned long long* goff, uint32_t* out_src,
+                      const unsigned long long* bp_base, int grid, cudaStream_t s) {
+  if (tile_hi <= tile_lo) return;
+  const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (uint32_t(grid) > need) grid = int(need);
+  src_block_kernel<<<grid, kBlockThreads, 0, s>>>(mode, tiles, tile_page, pages, tile_lo, tile_hi,
+                                                  n, blk_verts, n_pages, cnt, goff, out_src,
+                                                  bp_base);
+}
+
+__global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                                      const unsigned long long* __restrict__ goff,
+                                      const unsigned long long* __restrict__ bp_edges,
+                                      uint32_t* offs) {
+  // sub-page (p, b) local offsets live at b*(n + n_pages) + p*cap + p
+  const size_t total = size_t(n_blocks) * (size_t(n) + n_pages);
+  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
+       k += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(k / (size_t(n) + n_pages));
+    const uint32_t r = uint32_t(k % (size_t(n) + n_pages));  // = p*cap + p + i
+    const uint32_t p = r / (cap + 1) < n_pages ? r / (cap + 1) : n_pages - 1;
+    const uint32_t i = r - p * (cap + 1);
+    const uint32_t vb = p * cap;
+    const uint32_t range = min(cap, n - vb);
+    if (i < range) offs[k] = uint32_t(goff[size_t(b) * n + vb + i]);
+    else if (i == range) offs[k] = uint32_t(bp_edges[size_t(b) * n_pages + p]);
+  }
+}
+
+void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                           const unsigned long long* goff, const unsigned long long* bp_edges,
+                           uint32_t* offs, cudaStream_t s) {
+  src_block_offs_kernel<<<148 * 8, 256, 0, s>>>(n, cap, n_pages, n_blocks, goff, bp_edges, offs);
+}
+
+void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
+                           uint32_t n_pages, uint32_t n_blocks, uint32_t n,
+                           unsigned long long* bp_edges, cudaStream_t s) {
+  if (!n_pages || !n_blocks) return;
+  src_block_scan_kernel<<<n_pages * n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges);
+}
+
+void launch_pr_block_finalize(uint32_t n, float* acc, float* rank_out, float* contrib_out,
+                              const float* inv_outdeg, float base, float damp, cudaStream_t s) {
+  if (!n) return;
+  pr_block_finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, acc, rank_out, contrib_out,
+                                                            inv_outdeg, base, damp);
 }
 
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s) {

@@ -55,6 +55,21 @@ void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const 
                            uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
                            cudaStream_t s);
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s);
+// Source-blocked page split for PageRank locality (count / scan / scatter)
+// and the per-iteration finalize of the accumulated partial sums.
+void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
+                      const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
+                      uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
+                      const unsigned long long* goff, uint32_t* out_src,
+                      const unsigned long long* bp_base, int grid, cudaStream_t s);
+void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                           const unsigned long long* goff, const unsigned long long* bp_edges,
+                           uint32_t* offs, cudaStream_t s);
+void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
+                           uint32_t n_pages, uint32_t n_blocks, uint32_t n,
+                           unsigned long long* bp_edges, cudaStream_t s);
+void launch_pr_block_finalize(uint32_t n, float* acc, float* rank_out, float* contrib_out,
+                              const float* inv_outdeg, float base, float damp, cudaStream_t s);
 // Values initialisation (VertexProgram::init, programs.hpp:20-28).
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
                         cudaStream_t s);
