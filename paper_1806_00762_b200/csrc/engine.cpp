@@ -1364,7 +1364,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 bool Engine::build_src_blocks() {
   if (sb_.built) return true;
   if (!all_resident_ || world_ > 1 || comm_) return false;
-  uint64_t blk = 16ull << 20;
+  uint64_t blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
   if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) blk = std::strtoull(e, nullptr, 10);
   if (blk == 0 || n_ <= blk) return false;
   const uint32_t np = uint32_t(pages_.size());
