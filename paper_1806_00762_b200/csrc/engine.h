@@ -280,6 +280,14 @@ class Engine {
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
   } sb_;
   bool build_src_blocks();
+  // persistent sparse stage buffers
+  DBuf<Census> loop_cz_;
+  DBuf<RunCtr> loop_ctr_;
+  DBuf<unsigned> loop_res_;
+  PinBuf<Census> loop_cz_h_;
+  PinBuf<RunCtr> loop_ctr_h_;
+  PinBuf<unsigned> loop_res_h_;
+  int coop_ok_ = -1;
   void pr_blocked_pass(float base, float damp);
 
   // multi-GPU

@@ -11,6 +11,7 @@
 // The path is sparse and irregular: no tensor cores.  Everything is sized
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -818,20 +819,18 @@ __global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, flo
 // task is kPushChunk consecutive edges whose first list entry was recorded
 // by the compaction (chunk_start), so no search over the prefix is needed.
 // ---------------------------------------------------------------------------
+// Body shared by the standalone push launch and the persistent sparse loop:
+// frontier list / prefix / chunk starts are read through L2 (__ldcg) because
+// the persistent loop rewrites them every pass from other SMs.
 template <int A, bool DET>
-__global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
-  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
+__device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32_t nw, LaneCtr& c,
+                                          uint32_t& lane_min) {
   const int lane = threadIdx.x & 31;
-  const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const uint32_t nw = gridDim.x * kWarpsPerBlock;
   const unsigned long long nchunks = (a.total_edges + kPushChunk - 1) / kPushChunk;
-  LaneCtr c;
-  c.clear();
-  uint32_t lane_min = kUnreached;
   for (unsigned long long ch = gw; ch < nchunks; ch += nw) {
     const unsigned long long q_lo = ch * kPushChunk;
     const unsigned long long q_hi = min(q_lo + kPushChunk, a.total_edges);
-    uint32_t ad = a.chunk_start[ch];
+    uint32_t ad = __ldcg(a.chunk_start + ch);
     for (unsigned long long q0 = q_lo; q0 < q_hi; q0 += 32) {
       // window of up to 32 consecutive frontier entries starting at ad
       const uint32_t wi = ad + lane;
@@ -839,10 +838,10 @@ __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
       uint32_t u = 0, uval = kUnreached;
       unsigned long long ebase = 0;
       if (wi < a.n_list) {
-        rel = (long long)(a.pref[wi]) - (long long)q0;
-        u = a.list[wi];
+        rel = (long long)__ldcg(a.pref + wi) - (long long)q0;
+        u = __ldcg(a.list + wi);
         ebase = a.out_offsets[u];
-        uval = DET ? __ldg(a.values + u) : a.values[u];
+        uval = DET ? __ldg(a.values + u) : __ldcg(a.values + u);
       }
       const int relc = rel > 64 ? 64 : (int)rel;  // entries before q0 are negative
       const unsigned long long q = q0 + lane;
@@ -884,7 +883,7 @@ __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
       if (k == 31) {
         end_rel = 64;
         if (ad + 32 < a.n_list) {
-          const long long r = (long long)a.pref[ad + 32] - (long long)q0;
+          const long long r = (long long)__ldcg(a.pref + ad + 32) - (long long)q0;
           end_rel = r > 64 ? 64 : (int)r;
         }
       }
@@ -893,6 +892,16 @@ __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
       ad += k_last + (e_last <= 32 ? 1u : 0u);
     }
   }
+}
+
+template <int A, bool DET>
+__global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
+  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
+  LaneCtr c;
+  c.clear();
+  uint32_t lane_min = kUnreached;
+  push_body<A, DET>(a, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
+                    gridDim.x * kWarpsPerBlock, c, lane_min);
   block_flush(c, a.ctr, lane_min, a.census, s_scratch);
 }
 
@@ -946,12 +955,14 @@ __device__ __forceinline__ uint8_t log_attempt(uint8_t ls, bool changed,
   return out;
 }
 
-__global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
-                                                     uint8_t* status, uint8_t* logstate,
-                                                     const uint32_t* __restrict__ outdeg,
-                                                     int pass_kind, uint32_t own_lo, uint32_t own_hi,
-                                                     uint32_t* blk_cnt,
-                                                     unsigned long long* blk_edges, Census* cz) {
+// Census body (grid-stride over 4096-vertex chunks, 256 threads); per-pass
+// totals go to cz_pass, run-long accumulators (prediction log) to cz_run.
+__device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, uint8_t* status,
+                                            uint8_t* logstate, const uint32_t* __restrict__ outdeg,
+                                            int pass_kind, uint32_t own_lo, uint32_t own_hi,
+                                            uint32_t* blk_cnt, unsigned long long* blk_edges,
+                                            Census* cz_pass, Census* cz_run, uint32_t bid,
+                                            uint32_t nblk) {
   // grid-stride over 4096-vertex chunks; per-chunk (count, edges) for the
   // compaction scan, run totals reduced once per block (few global atomics)
   __shared__ unsigned long long s_chunk[2][8];
@@ -961,11 +972,11 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
   unsigned long long tot[kCensusParts];
 #pragma unroll
   for (int k = 0; k < kCensusParts; ++k) tot[k] = 0;
-  for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  for (uint32_t ch = bid; ch < nchunks; ch += nblk) {
     const uint32_t v0 = ch * kCensusBlockVerts + threadIdx.x * 16;
     unsigned long long own_push = 0, own_edges = 0;
     if (v0 < n) {
-      const uint4 cw = *reinterpret_cast<const uint4*>(changed + v0);
+      const uint4 cw = __ldcg(reinterpret_cast<const uint4*>(changed + v0));
       const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
       uint32_t dg[16];
       if (outdeg && (cw.x | cw.y | cw.z | cw.w)) {
@@ -983,8 +994,8 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
         for (int k = 0; k < 16; ++k) dg[k] = 0;
       }
       uint4 sw{}, lw{};
-      if (status) sw = *reinterpret_cast<const uint4*>(status + v0);
-      if (logstate) lw = *reinterpret_cast<const uint4*>(logstate + v0);
+      if (status) sw = __ldcg(reinterpret_cast<const uint4*>(status + v0));
+      if (logstate) lw = __ldcg(reinterpret_cast<const uint4*>(logstate + v0));
       uint8_t* sb = reinterpret_cast<uint8_t*>(&sw);
       uint8_t* lb = reinterpret_cast<uint8_t*>(&lw);
 #pragma unroll
@@ -1062,23 +1073,34 @@ __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* 
     if (a) {
       unsigned long long* dst;
       switch (threadIdx.x) {
-        case 0: dst = &cz->changed; break;
-        case 1: dst = &cz->push_count; break;
-        case 2: dst = &cz->out_edges; break;
-        case 3: dst = &cz->own_push; break;
-        case 4: dst = &cz->own_edges; break;
-        case 5: dst = &cz->log_events; break;
-        case 6: dst = &cz->log_incorrect; break;
-        default: dst = &cz->status_hist[threadIdx.x - 7]; break;
+        case 0: dst = &cz_pass->changed; break;
+        case 1: dst = &cz_pass->push_count; break;
+        case 2: dst = &cz_pass->out_edges; break;
+        case 3: dst = &cz_pass->own_push; break;
+        case 4: dst = &cz_pass->own_edges; break;
+        case 5: dst = &cz_run->log_events; break;
+        case 6: dst = &cz_run->log_incorrect; break;
+        default: dst = &cz_pass->status_hist[threadIdx.x - 7]; break;
       }
       atomicAdd(dst, a);
     }
   }
+  __syncthreads();  // s_tot is reused by the next call in a persistent loop
 }
 
-// Exclusive scan of the per-block (count, edges) pairs; one block.
-__global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t* cnt,
-                                                           unsigned long long* edges) {
+__global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
+                                                     uint8_t* status, uint8_t* logstate,
+                                                     const uint32_t* __restrict__ outdeg,
+                                                     int pass_kind, uint32_t own_lo, uint32_t own_hi,
+                                                     uint32_t* blk_cnt,
+                                                     unsigned long long* blk_edges, Census* cz) {
+  census_body(n, changed, status, logstate, outdeg, pass_kind, own_lo, own_hi, blk_cnt, blk_edges,
+              cz, cz, blockIdx.x, gridDim.x);
+}
+
+// Exclusive scan of the per-chunk (count, edges) pairs by ONE block (any
+// blockDim that is a multiple of 32).
+__device__ __forceinline__ void scan_body(uint32_t nb, uint32_t* cnt, unsigned long long* edges) {
   __shared__ uint32_t s_c[32];
   __shared__ unsigned long long s_e[32];
   __shared__ uint32_t carry_c;
@@ -1089,10 +1111,11 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (uint32_t base = 0; base < nb; base += 1024) {
+  const int nwarps = blockDim.x >> 5;
+  for (uint32_t base = 0; base < nb; base += blockDim.x) {
     const uint32_t i = base + threadIdx.x;
-    const uint32_t xc = i < nb ? cnt[i] : 0u;
-    const unsigned long long xe = i < nb ? edges[i] : 0ull;
+    const uint32_t xc = i < nb ? __ldcg(cnt + i) : 0u;
+    const unsigned long long xe = i < nb ? __ldcg(edges + i) : 0ull;
     uint32_t ic = warp_incl_scan(xc, lane);
     unsigned long long ie = warp_incl_scan(xe, lane);
     if (lane == 31) {
@@ -1101,8 +1124,8 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t
     }
     __syncthreads();
     if (w == 0) {
-      uint32_t tc = s_c[lane];
-      unsigned long long te = s_e[lane];
+      uint32_t tc = lane < nwarps ? s_c[lane] : 0u;
+      unsigned long long te = lane < nwarps ? s_e[lane] : 0ull;
       uint32_t sc = warp_incl_scan(tc, lane);
       unsigned long long se = warp_incl_scan(te, lane);
       s_c[lane] = sc - tc;
@@ -1116,7 +1139,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t
       cnt[i] = oc;
       edges[i] = oe;
     }
-    if (threadIdx.x == 1023) {
+    if (threadIdx.x == blockDim.x - 1) {
       carry_c = oc + xc;
       carry_e = oe + xe;
     }
@@ -1124,22 +1147,26 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t
   }
 }
 
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t nb, uint32_t* cnt,
+                                                           unsigned long long* edges) {
+  scan_body(nb, cnt, edges);
+}
+
 // Ordered compaction of changed vertices with out-degree > 0 into the push
 // list, with their exclusive out-degree prefix and push-chunk starts; clears
 // the changed flags for the next pass.
-__global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_lo, uint32_t own_hi,
-                                                      uint8_t* changed,
-                                                      const uint32_t* __restrict__ outdeg,
-                                                      const uint32_t* __restrict__ blk_off,
-                                                      const unsigned long long* __restrict__ blk_eoff,
-                                                      uint32_t* list, unsigned long long* pref,
-                                                      uint32_t* chunk_start) {
+__device__ __forceinline__ void compact_chunk(uint32_t chunk, uint32_t n, uint32_t own_lo,
+                                              uint32_t own_hi, uint8_t* changed,
+                                              const uint32_t* __restrict__ outdeg,
+                                              const uint32_t* blk_off,
+                                              const unsigned long long* blk_eoff, uint32_t* list,
+                                              unsigned long long* pref, uint32_t* chunk_start) {
   __shared__ uint32_t s_c[8];
   __shared__ unsigned long long s_e[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t v0 = blockIdx.x * kCensusBlockVerts + threadIdx.x * 16;
+  const uint32_t v0 = chunk * kCensusBlockVerts + threadIdx.x * 16;
   uint4 cw = make_uint4(0, 0, 0, 0);
-  if (v0 < n) cw = *reinterpret_cast<const uint4*>(changed + v0);
+  if (v0 < n) cw = __ldcg(reinterpret_cast<const uint4*>(changed + v0));
   const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
   uint32_t cnt = 0;
   unsigned long long edges = 0;
@@ -1167,8 +1194,8 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_l
     wc += s_c[i];
     we += s_e[i];
   }
-  uint32_t pos = blk_off[blockIdx.x] + wc + ic - cnt;
-  unsigned long long ep = blk_eoff[blockIdx.x] + we + ie - edges;
+  uint32_t pos = __ldcg(blk_off + chunk) + wc + ic - cnt;
+  unsigned long long ep = __ldcg(blk_eoff + chunk) + we + ie - edges;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (deg[j] > 0) {
@@ -1182,6 +1209,79 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_l
     }
   }
   if (v0 < n) *reinterpret_cast<uint4*>(changed + v0) = make_uint4(0, 0, 0, 0);
+  __syncthreads();  // s_c/s_e reused by the next chunk
+}
+
+__global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_lo, uint32_t own_hi,
+                                                      uint8_t* changed,
+                                                      const uint32_t* __restrict__ outdeg,
+                                                      const uint32_t* __restrict__ blk_off,
+                                                      const unsigned long long* __restrict__ blk_eoff,
+                                                      uint32_t* list, unsigned long long* pref,
+                                                      uint32_t* chunk_start) {
+  compact_chunk(blockIdx.x, n, own_lo, own_hi, changed, outdeg, blk_off, blk_eoff, list, pref,
+                chunk_start);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent sparse stage: scan -> compaction -> push -> census -> density
+// decision, repeated on the device with grid-wide barriers (cooperative
+// launch), so consecutive sparse passes (engine.cpp:265-277 loop) cost no
+// host round trip.  Cross-block data is read through L2 (__ldcg): L1 is not
+// coherent across SMs inside one persistent launch.
+// ---------------------------------------------------------------------------
+template <int A>
+__global__ void __launch_bounds__(kBlockThreads) sparse_loop_kernel(SparseLoopArgs L) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
+  const uint32_t nchunks = (L.n + kCensusBlockVerts - 1) / kCensusBlockVerts;
+  uint32_t done = 0, reason = 2;
+  for (uint32_t it = 0; it < L.max_passes; ++it) {
+    const Census* prev = it == 0 ? L.cz_run : L.cz_pass + (it - 1);
+    // (1) exclusive scan of the chunk counts left by the previous census
+    if (blockIdx.x == 0) scan_body(nchunks, L.blk_cnt, L.blk_edges);
+    grid.sync();
+    // (2) ordered compaction into the push list (clears the changed flags)
+    for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x)
+      compact_chunk(ch, L.n, L.own_lo, L.own_hi, L.push.changed, L.outdeg, L.blk_cnt,
+                    L.blk_edges, const_cast<uint32_t*>(L.push.list),
+                    const_cast<unsigned long long*>(L.push.pref),
+                    const_cast<uint32_t*>(L.push.chunk_start));
+    grid.sync();
+    // (3) push
+    PushArgs pa = L.push;
+    pa.n_list = uint32_t(__ldcg(&prev->own_push));
+    pa.total_edges = __ldcg(&prev->own_edges);
+    LaneCtr c;
+    c.clear();
+    uint32_t lane_min = kUnreached;
+    push_body<A, false>(pa, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
+                        gridDim.x * kWarpsPerBlock, c, lane_min);
+    block_flush(c, L.pass_ctr + it, lane_min, L.cz_run, s_scratch);
+    grid.sync();
+    // (4) census of the new frontier
+    census_body(L.n, L.push.changed, L.status, L.logstate, L.outdeg, kPassSparse, L.own_lo,
+                L.own_hi, L.blk_cnt, L.blk_edges, L.cz_pass + it, L.cz_run, blockIdx.x,
+                gridDim.x);
+    grid.sync();
+    // (5) density_switch (engine.cpp:56-61), identical in every thread
+    done = it + 1;
+    const unsigned long long changed = __ldcg(&L.cz_pass[it].changed);
+    const unsigned long long out_edges = __ldcg(&L.cz_pass[it].out_edges);
+    if (changed == 0) {
+      reason = 0;
+      break;
+    }
+    if (!L.force_sparse && double(out_edges) > L.dense_threshold) {
+      reason = 1;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    L.result[0] = done;
+    L.result[1] = reason;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1389,6 +1489,25 @@ void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s
       else push_relax_kernel<kSssp, false><<<grid, kBlockThreads, 0, s>>>(a);
       break;
   }
+}
+
+int sparse_loop_blocks(int algo) {
+  int nb = 0;
+  if (algo == kSssp)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kSssp>, kBlockThreads, 0);
+  else if (algo == kCc)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kCc>, kBlockThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kBfs>, kBlockThreads, 0);
+  return nb;
+}
+
+cudaError_t launch_sparse_loop(int algo, const SparseLoopArgs& a, int grid, cudaStream_t s) {
+  void* args[] = {const_cast<SparseLoopArgs*>(&a)};
+  const void* fn = algo == kSssp ? (const void*)sparse_loop_kernel<kSssp>
+                   : algo == kCc ? (const void*)sparse_loop_kernel<kCc>
+                                 : (const void*)sparse_loop_kernel<kBfs>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, 0, s);
 }
 
 void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
