@@ -1264,8 +1264,10 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     if (coop_ok_ < 0) {
       int v = 0;
       cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev_);
-      coop_ok_ = v && sparse_loop_blocks(algo_) > 0;
-      if (const char* e = std::getenv("SERAPH_SPARSE_LOOP")) coop_ok_ = coop_ok_ && std::atoi(e) != 0;
+      // measured neutral on C1/C2 (the per-pass cost is the O(|V|) census and
+      // compaction work, not the host round trip): opt-in via SERAPH_SPARSE_LOOP=1
+      const char* e = std::getenv("SERAPH_SPARSE_LOOP");
+      coop_ok_ = v && sparse_loop_blocks(algo_) > 0 && e && std::atoi(e) != 0;
     }
     if (!coop_ok_) return false;
     constexpr uint32_t kMaxLoop = 256;

@@ -496,3 +496,28 @@ def test_pagerank_source_blocked(blk, monkeypatch):
     assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
     assert np.abs(r2.ranks.astype(np.float64) - ref).max() < PR_TOL
     assert r.metrics.edges_read == 20 * src.size
+
+
+def test_persistent_sparse_loop(monkeypatch):
+    """SERAPH_SPARSE_LOOP=1: consecutive sparse passes run inside one cooperative
+    launch (grid-wide barriers); values stay bit-exact, pass records complete."""
+    monkeypatch.setenv("SERAPH_SPARSE_LOOP", "1")
+    n = 1 << 14
+    src, dst = O.generate_rmat(14, 16, seed=13)
+    w = O.assign_weights(src.size, 6, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 16)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    csr2, pages2 = built(sym, n // 16)
+    with ps.Engine(0) as eng:
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+            for pred in PREDS:
+                for ex in (ps.ExecutionPolicy.DENSITY_SWITCHED, ps.ExecutionPolicy.FORCE_SPARSE):
+                    r = eng.run_graph(csr, pages, program_for(kind, 0, el),
+                                      cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex))
+                    assert np.array_equal(r.values, oracle_values(el, kind, 0)), (kind, pred, ex)
+                    assert len(r.metrics.per_pass) == r.metrics.passes
+                    assert r.metrics.per_pass[-1].valid_updates == 0
+        r = eng.run_graph(csr2, pages2, ps.make_cc(),
+                          cfg_of(clock=ps.ClockMode.WALL, execution=ps.ExecutionPolicy.FORCE_SPARSE))
+        assert np.array_equal(r.values, oracle_values(sym, ps.AlgoKind.CC, 0))
