@@ -59,8 +59,7 @@ struct Census {
   // --- run-long accumulators ---
   unsigned long long log_events;   // PredictionLog events (weak)
   unsigned long long log_incorrect;
-  unsigned int min_changed;        // strong SSSP l accumulator (all kernels)
-  unsigned int cc_min_label;       // strong CC s result
+  unsigned int min_changed;        // strong SSSP l / CC s accumulator (all kernels)
 };
 constexpr unsigned kCensusResetBytes = 12 * sizeof(unsigned long long);
 
@@ -86,6 +85,8 @@ struct PullArgs {
   const RunCtr* prev_ctr;  // reentry: skip pages whose previous run was quiet
   uint32_t ctr_per_page;   // 1: ctr/prev_ctr indexed by page, 0: all in ctr[0]
   Census* census;          // min_changed accumulator
+  uint32_t count_dest;     // 1: count attempts/skipped (0 on source blocks > 0)
+  uint32_t count_valid;    // 1: count valid updates (0 in source-blocked passes)
   unsigned long long k_bfs;  // strong thresholds (predictor.hpp:47-52)
   uint32_t s_cc;
   uint32_t l_sssp;
@@ -103,6 +104,7 @@ struct PrArgs {
   const float* inv_outdeg;
   float* hub_sum;
   float* acc;   // source-blocked mode: partial sums accumulate here (else null)
+  const uint32_t* pi;  // hot-source relabel: contrib index of vertex v (else null)
   RunCtr* ctr;
   float base;   // (1-d)/N
   float damp;   // d

@@ -84,6 +84,7 @@ void cut_tiles(const uint32_t* offs, uint32_t vb, TileJob& job) {
 Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
   SR_CUDA(cudaSetDevice(dev_));
   SR_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev_));
+  SR_CUDA(cudaDeviceGetAttribute(&l2_bytes_, cudaDevAttrL2CacheSize, dev_));
   SR_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   SR_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
   SR_CUDA(cudaEventCreate(&ev_start_));
@@ -155,6 +156,7 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   SR_CUDA(cudaStreamSynchronize(xs_));
   has_csr_ = true;
   csr_derived_ = false;
+  prl_.built = false;  // the relabel follows the out-degrees
   last_upload_bytes += bytes;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -325,6 +327,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
   sb_.built = false;
+  prl_.built = false;
   page_desc_h_.assign(np, PageDesc{});
   for (uint32_t p = 0; p < np; ++p) {
     page_desc_h_[p].vertex_begin = pages_[p].vb;
@@ -538,10 +541,6 @@ void Engine::alloc_run_state(const sr_run_config& c) {
       status_.reserve(npad);
       logstate_.reserve(npad);
     }
-    if (c.predictor == SR_PRED_STRONG && c.algo == SR_ALGO_CC) {
-      snap_.reserve(npad);
-      delta_.reserve(npad);
-    }
     list_.reserve(npad);
     pref_.reserve(npad);
     chunk_start_.reserve(m_ / kPushChunk + 2);
@@ -624,6 +623,10 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.contrib_out = contrib_b_.p;
       a.inv_outdeg = inv_outdeg_.p;
       a.hub_sum = hub_sum_.p;
+      if (prl_.built) {
+        a.pages = prl_.desc.p;
+        a.pi = prl_.pi.p;
+      }
       a.ctr = ctr;
       a.base = float((1.0 - pr_damp_) / double(n_));
       a.damp = float(pr_damp_);
@@ -645,6 +648,8 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.prev_ctr = prev;
       a.ctr_per_page = per_page ? 1u : 0u;
       a.census = census_.p;
+      a.count_dest = 1;
+      a.count_valid = 1;
       a.k_bfs = k_bfs_;
       a.s_cc = s_cc_;
       a.l_sssp = l_sssp_;
@@ -898,6 +903,16 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
       po.bytes_transferred += pages_[p].bytes;
     }
     first_touch_done_ = true;
+  }
+
+  last_pass_blocked_ = false;
+  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && world_ == 1 && !comm_ &&
+      pull_block_verts()) {
+    if (pull_blocked_pass(gate, alloc_ctr(1))) {
+      last_pass_blocked_ = true;
+      po.kernel_runs += order.size();
+      return po;
+    }
   }
 
   for (size_t si = 0; si < steps.size(); ++si) {
@@ -1155,12 +1170,8 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     SR_CUDA(cudaMemsetAsync(status_.p, 0, npad, cs_));
     SR_CUDA(cudaMemsetAsync(logstate_.p, 0, npad, cs_));
   }
-  if (strong && algo_ == SR_ALGO_CC) {
-    SR_CUDA(cudaMemcpyAsync(snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
-    SR_CUDA(cudaMemsetAsync(delta_.p, 0, size_t(n_) * 4, cs_));
-  }
   SR_CUDA(cudaMemsetAsync(census_.p, 0, sizeof(Census), cs_));
-  SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 8, cs_));  // min_changed, cc_min_label
+  SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 4, cs_));
   k_bfs_ = 0;
   s_cc_ = 0;
   l_sssp_ = 0;
@@ -1227,6 +1238,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
       st.edges_read = po.totals.edges;
     } else {
       sum_ctr(st);
+      if (last_pass_blocked_) st.valid_updates = f_count;  // destinations changed
     }
     st.changed_vertices = f_count;
     m.pages_transferred += po.pages_transferred;
@@ -1359,7 +1371,6 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
                       : dense_pass_wall(cfg, gate, false, pass_index, false);
     exchange_round(false);
     census(kPassDense);
-    if (strong && algo_ == SR_ALGO_CC) launch_cc_refresh(n_, values_.p, snap_.p, delta_.p, census_.p, cs_);
     read_census();
     after_census();
     if (det_) {
@@ -1369,17 +1380,22 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
       st.edges_read = po.totals.edges;
     } else {
       sum_ctr(st);
+      if (last_pass_blocked_) st.valid_updates = f_count;  // destinations changed
     }
     st.changed_vertices = f_count;
     if (strong) {
-      // refresh_thresholds (predictor.cpp:89-105)
+      // refresh_thresholds (predictor.cpp:89-105).  SSSP l = min value
+      // written since the last refresh.  CC s (LabelHistogram::refresh,
+      // predictor.cpp:66-79: the smallest label whose population changed)
+      // is the same quantity: labels only decrease, so the smallest label
+      // written since the refresh gained a vertex and lost none (a vertex
+      // leaving it would have written a smaller label), and every label
+      // that changed population was either written (>= that minimum) or
+      // left for a smaller written label.  No per-label histogram needed.
       k_bfs_ += 1;
-      if (algo_ == SR_ALGO_SSSP) {
-        l_sssp_ = census_h_.p->min_changed;
+      if (algo_ == SR_ALGO_SSSP || algo_ == SR_ALGO_CC) {
+        (algo_ == SR_ALGO_SSSP ? l_sssp_ : s_cc_) = census_h_.p->min_changed;
         SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 4, cs_));
-      } else if (algo_ == SR_ALGO_CC) {
-        s_cc_ = census_h_.p->cc_min_label;
-        SR_CUDA(cudaMemsetAsync(&census_.p->cc_min_label, 0xff, 4, cs_));
       }
     }
     m.pages_transferred += po.pages_transferred;
@@ -1448,12 +1464,11 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 // one sweep stay inside a blk_verts slice (SERAPH_PR_BLOCK_VERTS, default
 // 16 Mi vertices = 64 MB of f32; 0 disables).
 // ---------------------------------------------------------------------------
-bool Engine::build_src_blocks() {
-  if (sb_.built) return true;
+bool Engine::build_src_blocks(uint64_t blk) {
+  if (sb_.built && sb_.blk_verts == blk) return true;
   if (!all_resident_ || world_ > 1 || comm_) return false;
-  uint64_t blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
-  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) blk = std::strtoull(e, nullptr, 10);
   if (blk == 0 || n_ <= blk) return false;
+  sb_.built = false;
   const uint32_t np = uint32_t(pages_.size());
   for (uint32_t p = 0; p < np; ++p)
     if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
@@ -1464,7 +1479,7 @@ bool Engine::build_src_blocks() {
   cnt.reserve(size_t(nb) * n_);
   SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
   launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
+                   cnt.p, nullptr, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
   // 2) page-local offsets per sub-page, sub-page sizes
   DBuf<unsigned long long> goff, bp_edges, bp_base;
   goff.reserve(size_t(nb) * n_);
@@ -1481,11 +1496,14 @@ bool Engine::build_src_blocks() {
     if (edges_h[k] > 0xffffffffull) return false;
   }
   sb_.src.reserve(at + 8);
+  if (weighted_) sb_.w.reserve(at + 8);
+  else sb_.w.release();
   SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
   // 3) scatter the sources (cnt reused as cursors)
   SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
   launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, goff.p, sb_.src.p, bp_base.p, sm_count_ * 8, cs_);
+                   cnt.p, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, bp_base.p,
+                   sm_count_ * 8, cs_);
   // 4) u32 local offsets, copied back to cut tiles on the host
   const size_t per_block = size_t(n_) + np;
   sb_.offs.reserve(size_t(nb) * per_block);
@@ -1525,7 +1543,7 @@ bool Engine::build_src_blocks() {
       d.edge_count = edges_h[size_t(b) * np + p];
       d.offs = sb_.offs.p + size_t(b) * per_block + size_t(p) * cap_ + p;
       d.src = sb_.src.p + base_h[size_t(b) * np + p];
-      d.w = nullptr;
+      d.w = weighted_ ? sb_.w.p + base_h[size_t(b) * np + p] : nullptr;
     }
   sb_.tiles.reserve(std::max<size_t>(tiles.size(), 1));
   sb_.tile_page.reserve(std::max<size_t>(tiles.size(), 1));
@@ -1539,6 +1557,104 @@ bool Engine::build_src_blocks() {
   sb_.n_blocks = nb;
   sb_.built = true;
   return true;
+}
+
+// Hot-source relabel (SERAPH_PR_RELABEL: unset = when the contribution array
+// outgrows half the L2, 0 = never, 1 = always).  Built once per resident
+// page set, on the device: radix sort of the out-degrees, inverse
+// permutation, relabelled source arena.  Values are unchanged: every
+// destination sums the same contributions in the same edge order.
+bool Engine::build_pr_relabel() {
+  if (prl_.built) return true;
+  int mode = -1;
+  if (const char* e = std::getenv("SERAPH_PR_RELABEL")) mode = std::atoi(e);
+  if (mode == 0 || !all_resident_ || world_ > 1 || comm_ || n_ == 0 || !has_csr_) return false;
+  if (mode < 0 && uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return false;
+  const uint32_t np = uint32_t(pages_.size());
+  prl_.pi.reserve(n_);
+  prl_.gsrc.reserve(std::max<size_t>(arena_src_.n, 4));
+  launch_pr_relabel(outdeg_.p, n_, prl_.pi.p, arena_src_.p, arena_src_.n & ~size_t(3),
+                    prl_.gsrc.p, cs_);
+  std::vector<PageDesc> desc(page_desc_h_);
+  for (uint32_t p = 0; p < np; ++p)
+    if (desc[p].src) desc[p].src = prl_.gsrc.p + (desc[p].src - arena_src_.p);
+  prl_.desc.reserve(std::max<uint32_t>(np, 1));
+  SR_CUDA(cudaMemcpyAsync(prl_.desc.p, desc.data(), np * sizeof(PageDesc), cudaMemcpyHostToDevice,
+                          cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));  // desc is a stack vector
+  prl_.built = true;
+  return true;
+}
+
+// Source-blocked dense pull (K1): when the vertex array outgrows the L2,
+// a baseline-schedule dense pass sweeps the source-blocked sub-pages block by
+// block, so every launch gathers from one blk-vertex slice that stays in
+// L2 instead of 32-byte DRAM sectors spread over the whole array.
+// SERAPH_PULL_BLOCK_VERTS: block size (0 = off; default 16 Mi vertices =
+// 64 MB of values, used when the array exceeds half the L2).  Values are
+// unchanged (min-combine is order independent; every destination sees
+// every in-edge once per pass).  Attempts/skips are counted on block 0,
+// edges on every block, valid updates = destinations changed in the pass.
+uint64_t Engine::pull_block_verts() const {
+  uint64_t blk = 16ull << 20;
+  if (const char* e = std::getenv("SERAPH_PULL_BLOCK_VERTS")) blk = std::strtoull(e, nullptr, 10);
+  if (blk == 0 || n_ <= blk) return 0;
+  if (!std::getenv("SERAPH_PULL_BLOCK_VERTS") && uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2)
+    return 0;
+  return blk;
+}
+
+bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
+  const uint64_t blk = pull_block_verts();
+  if (!blk || !build_src_blocks(blk)) return false;
+  const uint32_t run_id = ++run_id_;
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
+    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
+    if (t1 <= t0) continue;
+    PullArgs a{};
+    a.work = next_work_counter();
+    a.tiles = sb_.tiles.p;
+    a.tile_page = sb_.tile_page.p;
+    a.pages = sb_.desc.p;
+    a.seg.n = 1;
+    a.seg.tile_begin[0] = t0;
+    a.seg.task_prefix[0] = 0;
+    a.seg.task_prefix[1] = t1 - t0;
+    a.values = values_.p;
+    a.next = values_.p;
+    a.changed = changed_.p;
+    a.status = status_.p;
+    a.hub_stamp = hub_stamp_.p;
+    a.run_id = run_id;
+    a.ctr = ctr;
+    a.census = census_.p;
+    a.count_dest = b == 0 ? 1u : 0u;
+    a.count_valid = 0;
+    a.k_bfs = k_bfs_;
+    a.s_cc = s_cc_;
+    a.l_sssp = l_sssp_;
+    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    auto* evp = relax_begin();
+    launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
+    SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    ++launches_;
+  }
+  return true;
+}
+
+std::pair<cudaEvent_t, cudaEvent_t>* Engine::relax_begin() {
+  if (!profile_kernels_) return nullptr;
+  if (relax_ev_used_ == relax_ev_.size()) {
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    SR_CUDA(cudaEventCreate(&e.first));
+    SR_CUDA(cudaEventCreate(&e.second));
+    relax_ev_.push_back(e);
+  }
+  auto* evp = &relax_ev_[relax_ev_used_++];
+  SR_CUDA(cudaEventRecord(evp->first, cs_));
+  return evp;
 }
 
 void Engine::pr_blocked_pass(float base, float damp) {
@@ -1589,11 +1705,20 @@ void Engine::pr_blocked_pass(float base, float damp) {
 // ---------------------------------------------------------------------------
 void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
                           std::vector<sr_pass_stats>& passes) {
-  const bool blocked = build_src_blocks();
+  const bool relabel = build_pr_relabel();
+  uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
+  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
+  const bool blocked = !relabel && build_src_blocks(pr_blk);
+  const uint32_t* pi = relabel ? prl_.pi.p : nullptr;
   const auto wall0 = std::chrono::steady_clock::now();
   SR_CUDA(cudaEventRecord(ev_start_, cs_));
   launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
-  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
+  if (relabel) {  // positions of vertices without out-edges are read as 0, never written
+    SR_CUDA(cudaMemsetAsync(contrib_a_.p, 0, size_t(n_) * 4, cs_));
+    SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
+  }
+  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, pi, n_,
+                 n_ ? float(1.0 / double(n_)) : 0.f, cs_);
   if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
     ctr_used_ = 0;
@@ -1617,7 +1742,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     } else {
       po = dense_pass_wall(cfg, kGateOff, false, it, true);
       launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
-                             inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
+                             inv_outdeg_.p, pi, base, float(cfg.pr_damping), cs_);
     }
     exchange_round(true);
     if (ctr_used_)

@@ -214,8 +214,7 @@ class Engine {
   bool first_touch_done_ = false;  // resident path: admission counted once per run
 
   // run state
-  DBuf<uint32_t> values_, next_, snap_, round_snap_;
-  DBuf<int> delta_;
+  DBuf<uint32_t> values_, next_, round_snap_;
   DBuf<uint8_t> changed_, status_, logstate_;
   DBuf<uint32_t> list_, chunk_start_, blk_cnt_;
   DBuf<unsigned long long> pref_, blk_edges_, census_part_;
@@ -272,14 +271,28 @@ class Engine {
   struct SrcBlocks {
     bool built = false;
     uint32_t blk_verts = 0, n_blocks = 0;
-    DBuf<uint32_t> offs, src;
+    DBuf<uint32_t> offs, src, w;
     DBuf<uint4> tiles;
     DBuf<uint32_t> tile_page;
     DBuf<PageDesc> desc;
     DBuf<float> acc;
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
   } sb_;
-  bool build_src_blocks();
+  bool build_src_blocks(uint64_t blk_verts);
+  uint64_t pull_block_verts() const;
+  bool pull_blocked_pass(int gate, RunCtr* ctr);
+  bool last_pass_blocked_ = false;
+  std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
+  int l2_bytes_ = 0;
+  // Hot-source relabel of the resident pages for PageRank (K8 locality):
+  // pi (vertex -> position by descending out-degree) and a relabelled copy
+  // of the source arena; contributions are stored in pi order.
+  struct PrRelabel {
+    bool built = false;
+    DBuf<uint32_t> pi, gsrc;
+    DBuf<PageDesc> desc;
+  } prl_;
+  bool build_pr_relabel();
   // persistent sparse stage buffers
   DBuf<Census> loop_cz_;
   DBuf<RunCtr> loop_ctr_;

@@ -12,11 +12,14 @@
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device_types.h"
+#include "errors.h"
 #include "kernels.h"
 
 namespace seraph {
@@ -224,8 +227,8 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         const bool att = gate_attempt<A, G>(v, cur, a);
         const uint32_t lo_d = offs[d];
         if (lane == 0 && tile.x == lo_d) {  // owner chunk counts the visit once
-          c.attempts += att;
-          c.skipped += !att;
+          c.attempts += att & a.count_dest;
+          c.skipped += !att & a.count_dest;
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
         if (!att || cur <= candidate_floor<A>()) continue;
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             a.changed[v] = 1;
             lane_min = min(lane_min, best);
             const uint32_t hub = tile.w & ~kHubFlag;
-            if (atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
+            if (a.count_valid && atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
           }
         }
         continue;
@@ -279,8 +282,8 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           deg = __ldcs(offs + i + 1) - lo;
           att = gate_attempt<A, G>(v, cur, a);
         }
-        c.attempts += att;
-        c.skipped += (in && !att);
+        c.attempts += att & a.count_dest;
+        c.skipped += (in && !att) & a.count_dest;
         c.edges += att ? deg : 0u;
         const bool need = att && cur > candidate_floor<A>();  // can it still improve?
         const bool has = in && deg > 0;
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           if (DET) a.next[v] = b;
           else a.values[v] = b;
           a.changed[v] = 1;
-          c.valid += 1;
+          c.valid += a.count_valid;
           lane_min = min(lane_min, b);
         }
       }
@@ -496,20 +499,22 @@ __global__ void __launch_bounds__(kBlockThreads)
 src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
                  const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
                  uint32_t n, uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                 const unsigned long long* __restrict__ goff, uint32_t* out_src,
+                 const unsigned long long* __restrict__ goff, uint32_t* out_src, uint32_t* out_w,
                  const unsigned long long* __restrict__ bp_base) {
   __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  auto emit = [&](uint32_t p, uint32_t v, uint32_t s) {
+  auto emit = [&](uint32_t p, uint32_t v, uint32_t s, const uint32_t* wp) {
     const uint32_t b = s / blk_verts;
     const size_t k = size_t(b) * n + v;
     if (mode == 0) {
       atomicAdd(cnt + k, 1u);
     } else {
       const uint32_t at = atomicAdd(cnt + k, 1u);
-      out_src[bp_base[size_t(b) * n_pages + p] + goff[k] + at] = s;
+      const unsigned long long o = bp_base[size_t(b) * n_pages + p] + goff[k] + at;
+      out_src[o] = s;
+      if (out_w) out_w[o] = *wp;
     }
   };
   for (uint32_t ti = tile_lo + blockIdx.x * kWarpsPerBlock + warp; ti < tile_hi;
@@ -520,7 +525,7 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
     const uint32_t* __restrict__ src = pd.src;
     if (tile.w & kHubFlag) {
       const uint32_t v = pd.vertex_begin + tile.z;
-      for (uint32_t e = tile.x + lane; e < tile.y; e += 32) emit(pg, v, src[e]);
+      for (uint32_t e = tile.x + lane; e < tile.y; e += 32) emit(pg, v, src[e], pd.w + e);
       continue;
     }
     const uint32_t dl = tile.z, dh = tile.w;
@@ -563,7 +568,7 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
             nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
           }
           if (pp < lo_pos) continue;
-          emit(pg, pd.vertex_begin + s_loc[warp][ent], src[ebase + pp]);
+          emit(pg, pd.vertex_begin + s_loc[warp][ent], src[ebase + pp], pd.w + ebase + pp);
         }
       }
     }
@@ -639,6 +644,19 @@ __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __r
 // with uint4 source loads, gathers of contrib[src], per-lane fold and a
 // shared-memory float atomicAdd merge; hub chunks go through hub_sum.
 // ---------------------------------------------------------------------------
+// Contributions live in gather order: identity, or the hot-source relabel
+// pi (sources by descending out-degree) so the gathers of K8 concentrate on
+// an L2-resident prefix.  A vertex without out-edges is never gathered:
+// under the relabel its (zero) contribution is not written.
+__device__ __forceinline__ void pr_store_contrib(float* contrib, const uint32_t* pi, uint32_t v,
+                                                 float x) {
+  if (!pi) {
+    contrib[v] = x;
+  } else if (x != 0.f) {
+    contrib[__ldg(pi + v)] = x;
+  }
+}
+
 __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
@@ -702,7 +720,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           if (deg == 0 && !a.acc) {  // no in-edges: teleport share only
             const uint32_t v = vb + i;
             a.rank_out[v] = a.base;
-            a.contrib_out[v] = a.base * a.inv_outdeg[v];
+            pr_store_contrib(a.contrib_out, a.pi, v, a.base * a.inv_outdeg[v]);
           }
         }
         c.attempts += in;
@@ -778,7 +796,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
         }
         const float r = a.base + a.damp * sum_of[i];
         a.rank_out[v] = r;
-        a.contrib_out[v] = r * a.inv_outdeg[v];
+        pr_store_contrib(a.contrib_out, a.pi, v, r * a.inv_outdeg[v]);
       }
       __syncwarp();
     }
@@ -788,21 +806,56 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
 
 __global__ void pr_hub_finalize_kernel(const uint32_t* hub_vertex, uint32_t n_hubs,
                                        float* hub_sum, float* rank_out, float* contrib_out,
-                                       const float* inv_outdeg, float base, float damp) {
+                                       const float* inv_outdeg, const uint32_t* pi, float base,
+                                       float damp) {
   const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= n_hubs) return;
   const uint32_t v = hub_vertex[h];
   const float r = base + damp * hub_sum[h];
   rank_out[v] = r;
-  contrib_out[v] = r * inv_outdeg[v];
+  pr_store_contrib(contrib_out, pi, v, r * inv_outdeg[v]);
   hub_sum[h] = 0.f;
 }
 
-__global__ void pr_init_kernel(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
-                               float init) {
+__global__ void pr_init_kernel(float* rank, float* contrib, const float* inv_outdeg,
+                               const uint32_t* pi, uint32_t n, float init) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     rank[v] = init;
-    contrib[v] = init * inv_outdeg[v];
+    pr_store_contrib(contrib, pi, v, init * inv_outdeg[v]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Hot-source relabel for K8 (built once per resident page set): pi = rank of
+// every vertex in descending out-degree order (stable, so ties keep id
+// order), then a relabelled copy of every page's in_sources.  On RMAT-26 the
+// ~11 M highest-degree sources (44 MB of contributions) carry ~97 % of the
+// in-edges, so the gathers hit a prefix that stays in the 126 MB L2 instead
+// of 32-byte DRAM sectors spread over the whole 256 MB array.
+// ---------------------------------------------------------------------------
+__global__ void iota_kernel(uint32_t* p, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = i;
+}
+
+__global__ void perm_invert_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* pi) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    pi[perm[i]] = i;
+}
+
+// out[i] = pi[src[i]] over a whole source arena (uint4 vectors; the arena is
+// 32 B aligned and padded).  Slack words (ids >= n) map to 0.
+__global__ void relabel_src_kernel(const uint4* __restrict__ src, size_t n4,
+                                   const uint32_t* __restrict__ pi, uint32_t n, uint4* out) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const uint4 s = __ldcs(src + i);
+    uint4 r;
+    r.x = s.x < n ? __ldg(pi + s.x) : 0u;
+    r.y = s.y < n ? __ldg(pi + s.y) : 0u;
+    r.z = s.z < n ? __ldg(pi + s.z) : 0u;
+    r.w = s.w < n ? __ldg(pi + s.w) : 0u;
+    __stcs(out + i, r);
   }
 }
 
@@ -1292,55 +1345,6 @@ __global__ void __launch_bounds__(kBlockThreads) sparse_loop_kernel(SparseLoopAr
 // match_any aggregation of the hot label, and the minimum label with a
 // nonzero net change is s.
 // ---------------------------------------------------------------------------
-__global__ void cc_delta_kernel(uint32_t n, const uint32_t* __restrict__ values,
-                                const uint32_t* __restrict__ snap, int* delta) {
-  const int lane = threadIdx.x & 31;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const uint32_t v = base + threadIdx.x;
-    uint32_t cur = 0, old = 0;
-    bool moved = false;
-    if (v < n) {
-      cur = values[v];
-      old = snap[v];
-      moved = cur != old;
-    }
-    const unsigned am = __ballot_sync(kFull, moved);
-    if (moved) {
-      const unsigned m_in = __match_any_sync(am, cur);
-      if (lane == __ffs(m_in) - 1) atomicAdd(delta + cur, __popc(m_in));
-      const unsigned m_out = __match_any_sync(am, old);
-      if (lane == __ffs(m_out) - 1) atomicSub(delta + old, __popc(m_out));
-    }
-  }
-}
-
-__global__ void cc_min_kernel(uint32_t n, const uint32_t* __restrict__ values,
-                              const uint32_t* __restrict__ snap, const int* __restrict__ delta,
-                              Census* cz) {
-  uint32_t best = kUnreached;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t cur = values[v], old = snap[v];
-    if (cur != old) {
-      if (delta[cur] != 0) best = min(best, cur);
-      if (delta[old] != 0) best = min(best, old);
-    }
-  }
-  best = warp_min(best);
-  if ((threadIdx.x & 31) == 0 && best != kUnreached) atomicMin(&cz->cc_min_label, best);
-}
-
-__global__ void cc_reset_kernel(uint32_t n, const uint32_t* __restrict__ values, uint32_t* snap,
-                                int* delta) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t cur = values[v], old = snap[v];
-    if (cur != old) {
-      delta[cur] = 0;
-      delta[old] = 0;
-      snap[v] = cur;
-    }
-  }
-}
-
 __global__ void init_values_kernel(int algo, uint32_t source, uint32_t n, uint32_t* values) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     values[v] = (algo == kCc) ? v : (v == source ? 0u : kUnreached);
@@ -1457,16 +1461,42 @@ void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s) {
 
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
-                            float base, float damp, cudaStream_t s) {
+                            const uint32_t* pi, float base, float damp, cudaStream_t s) {
   if (!n_hubs) return;
   pr_hub_finalize_kernel<<<(n_hubs + 255) / 256, 256, 0, s>>>(hub_vertex, n_hubs, hub_sum,
                                                               rank_out, contrib_out, inv_outdeg,
-                                                              base, damp);
+                                                              pi, base, damp);
 }
 
-void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n, float init,
-                    cudaStream_t s) {
-  pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, n, init);
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, const uint32_t* pi,
+                    uint32_t n, float init, cudaStream_t s) {
+  pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, pi, n, init);
+}
+
+void launch_pr_relabel(const uint32_t* outdeg, uint32_t n, uint32_t* pi, const uint32_t* src,
+                       size_t src_words, uint32_t* gsrc, cudaStream_t s) {
+  if (!n) return;
+  uint32_t *keys = nullptr, *ids = nullptr, *perm = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  SR_CUDA(cudaMallocAsync(&keys, size_t(n) * 4, s));
+  SR_CUDA(cudaMallocAsync(&ids, size_t(n) * 4, s));
+  SR_CUDA(cudaMallocAsync(&perm, size_t(n) * 4, s));
+  iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n);
+  SR_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, outdeg, keys, ids, perm,
+                                                    int(n), 0, 32, s));
+  SR_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+  SR_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, outdeg, keys, ids, perm,
+                                                    int(n), 0, 32, s));
+  perm_invert_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, n, pi);
+  const size_t n4 = src_words / 4;
+  if (n4)
+    relabel_src_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
+        reinterpret_cast<const uint4*>(src), n4, pi, n, reinterpret_cast<uint4*>(gsrc));
+  SR_CUDA(cudaFreeAsync(tmp, s));
+  SR_CUDA(cudaFreeAsync(keys, s));
+  SR_CUDA(cudaFreeAsync(ids, s));
+  SR_CUDA(cudaFreeAsync(perm, s));
 }
 
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
@@ -1543,15 +1573,6 @@ void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* chang
                                     list, pref, chunk_start);
 }
 
-void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* delta, Census* c,
-                       cudaStream_t s) {
-  if (!n) return;
-  const int g = grid_for(n, 256);
-  cc_delta_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
-  cc_min_kernel<<<g, 256, 0, s>>>(n, values, snap, delta, c);
-  cc_reset_kernel<<<g, 256, 0, s>>>(n, values, snap, delta);
-}
-
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
                            uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
                            uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
@@ -1566,13 +1587,13 @@ void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const 
 void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                      const unsigned long long* goff, uint32_t* out_src,
+                      const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
                       const unsigned long long* bp_base, int grid, cudaStream_t s) {
   if (tile_hi <= tile_lo) return;
   const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (uint32_t(grid) > need) grid = int(need);
   src_block_kernel<<<grid, kBlockThreads, 0, s>>>(mode, tiles, tile_page, pages, tile_lo, tile_hi,
-                                                  n, blk_verts, n_pages, cnt, goff, out_src,
+                                                  n, blk_verts, n_pages, cnt, goff, out_src, out_w,
                                                   bp_base);
 }
 

@@ -18,9 +18,13 @@ void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
-                            float base, float damp, cudaStream_t s);
-void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
-                    float init, cudaStream_t s);
+                            const uint32_t* pi, float base, float damp, cudaStream_t s);
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, const uint32_t* pi,
+                    uint32_t n, float init, cudaStream_t s);
+// Hot-source relabel: pi = descending-out-degree rank of every vertex;
+// gsrc[i] = pi[src[i]] over a source arena of src_words (multiple of 4).
+void launch_pr_relabel(const uint32_t* outdeg, uint32_t n, uint32_t* pi, const uint32_t* src,
+                       size_t src_words, uint32_t* gsrc, cudaStream_t s);
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
                        cudaStream_t s);
 // K3: sparse push over the compacted frontier.
@@ -50,8 +54,6 @@ void launch_mark_changed(uint32_t n, const uint32_t* values, const uint32_t* sna
 void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, const uint32_t* src,
                           const uint32_t* w, cudaStream_t s);
 // K6: strong CC threshold (net label-population change since the last refresh).
-void launch_cc_refresh(uint32_t n, const uint32_t* values, uint32_t* snap, int* delta,
-                       Census* c, cudaStream_t s);
 // Device-side CSR adjacency from resident CSC pages; out-degrees (u32).
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
                            uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
@@ -63,7 +65,7 @@ void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cud
 void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                      const unsigned long long* goff, uint32_t* out_src,
+                      const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
                       const unsigned long long* bp_base, int grid, cudaStream_t s);
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,

@@ -485,6 +485,7 @@ def test_pagerank_source_blocked(blk, monkeypatch):
     """Source-blocked K8 sweeps (the path large graphs take when the contrib
     array outgrows L2), forced on a small graph: same ranks within 1e-6."""
     monkeypatch.setenv("SERAPH_PR_BLOCK_VERTS", blk)
+    monkeypatch.setenv("SERAPH_PR_RELABEL", "0")
     n = 1 << 14
     src, dst = O.generate_rmat(14, 16, seed=12)
     el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
@@ -521,3 +522,56 @@ def test_persistent_sparse_loop(monkeypatch):
         r = eng.run_graph(csr2, pages2, ps.make_cc(),
                           cfg_of(clock=ps.ClockMode.WALL, execution=ps.ExecutionPolicy.FORCE_SPARSE))
         assert np.array_equal(r.values, oracle_values(sym, ps.AlgoKind.CC, 0))
+
+
+@pytest.mark.parametrize("scale", [12, 15])
+def test_pagerank_hot_source_relabel(scale, monkeypatch):
+    """Hot-source relabel (contributions stored by descending out-degree, the
+    path RMAT-26 takes), forced on small graphs with dangling vertices and
+    hubs: ranks within 1e-6 of the fp64 oracle, identical counters."""
+    monkeypatch.setenv("SERAPH_PR_RELABEL", "1")
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=21)
+    el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
+    csr, pages = built(el, n // 16)
+    ref = O.pagerank(n, src, dst, 20, 0.85)
+    with ps.Engine(0) as eng:
+        r = eng.run_graph(csr, pages, ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL))
+        r2 = eng.run(ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL, pr_iterations=7))
+    assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
+    assert r.metrics.edges_read == 20 * src.size
+    assert np.abs(r2.ranks.astype(np.float64) - O.pagerank(n, src, dst, 7, 0.85)).max() < PR_TOL
+
+
+@pytest.mark.parametrize("blk", ["700", "5000"])
+def test_pull_source_blocked(blk, monkeypatch):
+    """Source-blocked dense pulls (K1 over per-source-block sub-pages, the path
+    graphs take when the vertex array outgrows L2), forced on RMAT-14:
+    bit-exact BFS/SSSP/CC for every predictor, reference-shaped counters."""
+    monkeypatch.setenv("SERAPH_PULL_BLOCK_VERTS", blk)
+    n = 1 << 14
+    src, dst = O.generate_rmat(14, 16, seed=22)
+    w = O.assign_weights(src.size, 9, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 16)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    csr2, pages2 = built(sym, n // 16)
+    with ps.Engine(0) as eng:
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+            want = oracle_values(el, kind, 0)
+            for pred in PREDS:
+                for ex in (ps.ExecutionPolicy.DENSITY_SWITCHED, ps.ExecutionPolicy.FORCE_DENSE):
+                    r = eng.run_graph(csr, pages, program_for(kind, 0, el),
+                                      cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex))
+                    assert np.array_equal(r.values, want), (kind, pred, ex)
+                    for st in r.metrics.per_pass:
+                        assert st.valid_updates <= st.attempts
+                        if st.kind != ps.PassKind.SPARSE_PUSH and pred == ps.PredictorMode.OFF:
+                            assert st.attempts == n
+                            assert st.edges_read == src.size
+                    assert r.metrics.per_pass[-1].valid_updates == 0
+        want = oracle_values(sym, ps.AlgoKind.CC, 0)
+        for pred in PREDS:
+            r = eng.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+            assert np.array_equal(r.values, want), pred
+            assert eng.verify_fixpoint(ps.AlgoKind.CC, r.values) == 0

@@ -1,0 +1,50 @@
+"""Dev tool: per-launch table from an ncu --csv launch list (gpu__time_duration, dram bytes)."""
+import csv
+import sys
+from collections import OrderedDict
+
+
+def rows(path):
+    with open(path) as fh:
+        lines = [ln for ln in fh if ln.startswith('"')]
+    return list(csv.DictReader(lines))
+
+
+def main(path, full=False):
+    per = OrderedDict()
+    order = []
+    for r in rows(path):
+        key = (r["ID"], r["Kernel Name"])
+        if key not in per:
+            per[key] = {}
+            order.append(key)
+        v = r["Metric Value"].replace(",", "")
+        try:
+            per[key][r["Metric Name"]] = (float(v), r["Metric Unit"])
+        except ValueError:
+            pass
+    tot = 0.0
+    agg = OrderedDict()
+    for key in order:
+        m = per[key]
+        t, u = m.get("gpu__time_duration.sum", (0.0, "ns"))
+        t_us = t / 1000.0 if u == "ns" else (t * 1000.0 if u == "ms" else t)
+        rd = m.get("dram__bytes_read.sum", (0.0, "byte"))
+        wr = m.get("dram__bytes_write.sum", (0.0, "byte"))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = rd[0] * scale.get(rd[1], 1) + wr[0] * scale.get(wr[1], 1)
+        tot += t_us
+        name = key[1].split("(")[0]
+        a = agg.setdefault(name, [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += t_us
+        a[2] += b
+        if full:
+            print(f"{key[0]:>5} {t_us:10.1f} us {b / 1e9:8.3f} GB {b / max(t_us, 1e-9) / 1e3:8.1f} GB/s  {name}")
+    print(f"total {tot:.1f} us")
+    for name, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{n:5d} {t:12.1f} us {t / tot * 100:5.1f}% {b / 1e9:9.3f} GB {b / max(t, 1e-9) / 1e3:8.1f} GB/s  {name}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], "--full" in sys.argv)

@@ -1,0 +1,86 @@
+"""Dev tool: per-pass breakdown of one converge run (stats + per-kernel device time).
+
+    python tools/pass_probe.py --algo sssp --scale 24
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --csv \
+        python tools/pass_probe.py ...   # only the probed run is captured
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_1806_00762_b200 import pagestream as ps  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--algo", default="sssp")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--pages", type=int, default=16)
+    ap.add_argument("--uniform", action="store_true")
+    ap.add_argument("--mode", default="baseline")
+    ap.add_argument("--predictor", default="strong")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--sweep", default="", help="VAR=v1,v2,...: time one run per setting")
+    ap.add_argument("--verify", action="store_true")
+    a = ap.parse_args()
+    ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform,
+                            pages=a.pages, seed=0, lean=True)
+    W = bench.workload(ns)
+    print(f"# build {W['build_s']:.1f}s n={W['n']} m={W['m']}", flush=True)
+    eng = ps.Engine(0)
+    eng.load_csr(W["csr"], with_edges=False)
+    eng.load_pages(W["pages"])
+    kind = ps.AlgoKind(bench.ALGOS[a.algo])
+    prog = ps.VertexProgram(kind, 0)
+    cfg = ps.EngineConfig(predictor=ps.PredictorMode(bench.PREDS[a.predictor]),
+                          clock=ps.ClockMode.WALL, profile_kernels=True)
+    cfg.schedule.kind = ps.ScheduleModeKind(bench.MODES[a.mode])
+    if a.sweep:
+        var, vals = a.sweep.split("=", 1)
+        base = None
+        for v in vals.split(","):
+            os.environ[var] = v
+            r = eng.run(prog, cfg, want_values=a.verify)  # builds per-setting structures
+            extra = {}
+            if a.verify and kind != ps.AlgoKind.PAGERANK:
+                extra["violations"] = eng.verify_fixpoint(kind, r.values)
+            if a.verify:
+                got = r.ranks if kind == ps.AlgoKind.PAGERANK else r.values
+                if base is None:
+                    base = got.copy()
+                elif kind == ps.AlgoKind.PAGERANK:
+                    extra["max_diff_vs_first"] = float(abs(got.astype("f8") - base).max())
+                else:
+                    extra["equal_to_first"] = bool((got == base).all())
+            ts = []
+            for _ in range(a.reps):
+                ts.append(eng.run(prog, cfg, want_values=False).metrics.device_seconds * 1e3)
+            print(json.dumps({var: v, "ms": [round(t, 3) for t in ts], "first_ms":
+                              round(r.metrics.device_seconds * 1e3, 3), **extra}), flush=True)
+        return
+    for _ in range(a.reps):
+        r = eng.run(prog, cfg, want_values=False)
+    cudart = ctypes.CDLL("libcudart.so")
+    cudart.cudaProfilerStart()
+    r = eng.run(prog, cfg, want_values=False)
+    cudart.cudaDeviceSynchronize()
+    cudart.cudaProfilerStop()
+    m = r.metrics
+    print(json.dumps({"ms": round(m.device_seconds * 1e3, 4),
+                      "relax_ms": round(m.relax_seconds * 1e3, 4),
+                      "relax_launches": m.relax_launches, "launches": m.kernel_launches,
+                      "gathers": m.gathers, "edges_read": m.edges_read}))
+    for st in m.per_pass:
+        print(json.dumps({"pass": st.pass_index, "kind": int(st.kind), "attempts": st.attempts,
+                          "valid": st.valid_updates, "skipped": st.skipped,
+                          "edges": st.edges_read, "changed": st.changed_vertices}))
+
+
+if __name__ == "__main__":
+    main()
