@@ -15,7 +15,7 @@ CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I$(CUDA_HOME)
 LDFLAGS := -shared -L$(CUDA_HOME)/lib64 -lcudart -ldl -lpthread -Wl,-rpath,$(CUDA_HOME)/lib64
 
 HDRS := include/seraph.h $(wildcard $(SRC)/*.h)
-OBJS := $(BUILD)/kernels.o $(BUILD)/engine.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o $(BUILD)/nccl_dyn.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/devgraph.o $(BUILD)/engine.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o $(BUILD)/nccl_dyn.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle
@@ -27,6 +27,9 @@ $(BUILD):
 
 $(BUILD)/kernels.o: $(SRC)/kernels.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; false)
+
+$(BUILD)/devgraph.o: $(SRC)/devgraph.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_devgraph.log || (cat $(BUILD)/ptxas_devgraph.log; false)
 
 $(BUILD)/%.o: $(SRC)/%.cpp $(HDRS) | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
@@ -43,3 +46,4 @@ ref:
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
+

@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--graph", default="device", choices=["device", "host"],
+                   help="generate + build the graph on the GPU (sr_generate_graph) or on the host")
     a = p.parse_args()
     # lean host graph (no host CSR adjacency) when nothing on this run needs it
     a.lean = a.impl == "ours" and a.no_cpu_baseline and not a.budget_gb and a.gpus == 1
@@ -66,24 +68,45 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
-def workload(args):
-    """Synthetic RMAT graph of the named scale (library host generator), CSR +
-    16 CSC pages, all arrays in pinned host memory (e2e inputs)."""
+def workload(args, eng=None):
+    """Synthetic RMAT graph of the named scale: CSR + 16 CSC pages, all arrays in
+    pinned host memory (e2e / reference inputs).  --graph device (default):
+    generated and built on the GPU (sr_generate_graph, bit-identical to the host
+    pipeline) inside `eng` (left loaded: W["loaded"]) or a scratch context, then
+    exported; --graph host (or no GPU): the parallel host generator/builders."""
     from paper_1806_00762_b200 import _native as N
     from paper_1806_00762_b200 import pagestream as ps
 
     t0 = time.time()
     quad = (0.25, 0.25, 0.25, 0.25) if args.uniform else (0.57, 0.19, 0.19, 0.05)
-    el = ps.generate_rmat_fast(args.scale, args.edge_factor, *quad, seed=args.seed)
     weighted = args.algo == "sssp"
+    n = 1 << args.scale
+    cap = (n + args.pages - 1) // args.pages
+    lean = getattr(args, "lean", False)
+    arena = N.PinnedArena()
+    if getattr(args, "graph", "host") == "device":
+        try:
+            builder = eng if eng is not None else ps.Engine(0)
+            builder.generate_graph(args.scale, args.edge_factor, *quad, seed=args.seed,
+                                   weights=(1, 64, args.seed + 1) if weighted else None,
+                                   symmetrize=args.algo == "cc", page_vertex_capacity=cap,
+                                   csr_edges=not lean)
+            csr, pages, in_off, in_src, in_w = builder.export_graph(arena, csr_edges=not lean)
+            if eng is None:
+                builder.close()
+            return dict(csr=csr, pages=pages, n=n, m=int(in_off[-1]), cap=cap, in_off=in_off,
+                        in_src=in_src, in_w=in_w if weighted else None, weighted=weighted,
+                        build_s=time.time() - t0, arena=arena, pinned=True, lean=lean,
+                        loaded=eng is not None, graph="device (sr_generate_graph)")
+        except (N.Error, OSError) as e:  # no device: host pipeline
+            print(f"# device graph build unavailable ({e}); host build", file=sys.stderr)
+    el = ps.generate_rmat_fast(args.scale, args.edge_factor, *quad, seed=args.seed)
     if weighted:
         el = ps.assign_weights_fast(el, args.seed + 1, 1, 64)
     if args.algo == "cc":
         el = ps.symmetrize(el)
     n, m = el.num_vertices, el.num_edges()
-    cap = (n + args.pages - 1) // args.pages
 
-    arena = N.PinnedArena()
     pin = [True]
 
     def pinned(count, dtype):
@@ -98,7 +121,6 @@ def workload(args):
     # --impl reference) and by the out-of-core path; otherwise the engine
     # derives it on the device from the resident pages and only the
     # out-degree prefix is built here.
-    lean = getattr(args, "lean", False)
     out_off = pinned(n + 1, np.uint64)
     out_nbr = pinned(0 if lean else m, np.uint32)
     out_w = pinned(m if (weighted and not lean) else 0, np.uint32)
@@ -120,7 +142,7 @@ def workload(args):
     del el
     return dict(csr=csr, pages=pages, n=n, m=m, cap=cap, in_off=in_off, in_src=in_src,
                 in_w=in_w if weighted else None, weighted=weighted, build_s=time.time() - t0,
-                arena=arena, pinned=pin[0], lean=lean)
+                arena=arena, pinned=pin[0], lean=lean, loaded=False, graph="host (parallel C++)")
 
 
 class ClockSampler:
@@ -194,8 +216,6 @@ def run_ours(args, rank, world, local_rank):
     from paper_1806_00762_b200 import _native as N
     from paper_1806_00762_b200 import pagestream as ps
 
-    W = workload(args)
-    csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
     algo = ALGOS[args.algo]
     prog = ps.VertexProgram(ps.AlgoKind(algo), 0)
     cfg = ps.EngineConfig(predictor=ps.PredictorMode(PREDS[args.predictor]),
@@ -222,8 +242,11 @@ def run_ours(args, rank, world, local_rank):
             uid[0] = bytes(buf)
         dist.broadcast_object_list(uid, src=0)
         eng.attach_world(rank, world, uid[0])
-    eng.load_csr(csr, with_edges=not W.get("lean"))
-    eng.load_pages(pages)
+    W = workload(args, eng)
+    csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
+    if not W["loaded"]:
+        eng.load_csr(csr, with_edges=not W.get("lean"))
+        eng.load_pages(pages)
 
     info = ps.device_info(local_rank)
     graph_bytes = sum(ps.page_bytes(p, W["weighted"]) for p in pages.pages)
@@ -398,7 +421,7 @@ def run_ours(args, rank, world, local_rank):
                           % (4 * info["l2_bytes"] >> 20, graph_bytes / 1e9)) if flush else
                          ("inputs larger than L2 (CSC %.2f GB vs %d MB L2)"
                           % (graph_bytes / 1e9, info["l2_bytes"] >> 20)),
-                   "graph_build_s": round(W["build_s"], 2),
+                   "graph_build_s": round(W["build_s"], 2), "graph_build": W["graph"],
                    "parallelism": f"dp{world}" if world > 1 else "single"},
         "time_to_converge_ms": round(ms_per_step, 4),
         "gteps_read": round(gteps_read, 4),

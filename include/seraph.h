@@ -232,6 +232,63 @@ int sr_verify_fixpoint(sr_ctx* ctx, int algo, const uint32_t* values_host,
 int sr_bench_pull_sweep(sr_ctx* ctx, int algo, uint32_t reps, double* ms_per_sweep,
                         uint64_t* edges_per_sweep);
 
+/* ---- device-side graph build ----------------------
+ * The reference's build_csr + build_csc_pages (graph.cpp:30-94) on the GPU:
+ * stable radix sorts, so the CSR/CSC arrays are bit-identical to the host
+ * builders (within a source/destination the input edge order is kept).  The
+ * result is loaded as if by sr_load_csr + sr_load_pages with pages of
+ * page_vertex_capacity vertices.  With SR_BUILD_CSR_EDGES the push adjacency
+ * is built in the reference's order (else only out_offsets; the adjacency is
+ * then derived from the resident pages). */
+#define SR_BUILD_CSR_EDGES 1
+
+/* Synthetic graph recipe: generate_rmat (ingest.cpp:112-141 quadrant law,
+ * counter-based stream of sr_rmat_generate), optional assign_weights range
+ * (weight_hi == 0: unweighted), optional symmetrize (graph.cpp:102-118). */
+typedef struct {
+  int32_t scale;
+  uint32_t edge_factor;
+  double a, b, c, d;
+  uint64_t seed;
+  uint32_t weight_lo, weight_hi;
+  uint64_t weight_seed;
+  int32_t symmetrize;
+  uint32_t page_vertex_capacity;
+} sr_graph_spec;
+
+typedef struct {
+  uint32_t num_vertices;
+  uint32_t num_pages;
+  uint64_t num_edges;
+  uint32_t page_vertex_capacity;
+  int32_t weighted;      /* pages carry in_weights */
+  int32_t has_csr_edges; /* push adjacency on the device */
+  int32_t csr_weighted;
+  int32_t csr_derived;   /* adjacency derived from the pages (order within a source arbitrary) */
+  int32_t pad_;
+} sr_graph_info;
+
+/* Edge list in host or device memory (src/dst/w: num_edges entries, w NULL
+ * when unweighted). */
+int sr_build_graph(sr_ctx* ctx, uint32_t num_vertices, uint64_t num_edges, const uint32_t* src,
+                   const uint32_t* dst, const uint32_t* w, uint32_t page_vertex_capacity,
+                   int flags);
+/* Generate + build entirely on the device (no host edge list). */
+int sr_generate_graph(sr_ctx* ctx, const sr_graph_spec* spec, int flags);
+int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out);
+/* Copy the loaded graph back in the reference layouts (any pointer may be
+ * NULL): CSR out_offsets (|V|+1) / out_neighbors / out_weights (|E|), global
+ * CSC in_offsets (|V|+1, u64) / in_sources / in_weights (|E|). */
+int sr_export_graph(sr_ctx* ctx, uint64_t* out_offsets, uint32_t* out_neighbors,
+                    uint32_t* out_weights, uint64_t* in_offsets, uint32_t* in_sources,
+                    uint32_t* in_weights);
+/* The device generator alone, copied to host arrays (parity with
+ * sr_rmat_generate / sr_weights_generate). w may be NULL. */
+int sr_rmat_generate_device(int device, int scale, uint64_t edge_factor, double a, double b,
+                            double c, double d, uint64_t seed, uint32_t* src, uint32_t* dst,
+                            uint64_t weight_seed, uint32_t weight_lo, uint32_t weight_hi,
+                            uint32_t* w);
+
 /* ---- host plumbing ------------------------------------------------------ */
 /* Page-locked host buffers (cudaHostAlloc): inputs in pinned memory upload at
  * full link speed and are what the out-of-core path streams from. */

@@ -172,6 +172,39 @@ class DeviceInfo(C.Structure):
     ]
 
 
+class GraphSpec(C.Structure):
+    _fields_ = [
+        ("scale", C.c_int32),
+        ("edge_factor", C.c_uint32),
+        ("a", C.c_double),
+        ("b", C.c_double),
+        ("c", C.c_double),
+        ("d", C.c_double),
+        ("seed", C.c_uint64),
+        ("weight_lo", C.c_uint32),
+        ("weight_hi", C.c_uint32),
+        ("weight_seed", C.c_uint64),
+        ("symmetrize", C.c_int32),
+        ("page_vertex_capacity", C.c_uint32),
+    ]
+
+
+class GraphInfo(C.Structure):
+    _fields_ = [
+        ("num_vertices", C.c_uint32),
+        ("num_pages", C.c_uint32),
+        ("num_edges", C.c_uint64),
+        ("page_vertex_capacity", C.c_uint32),
+        ("weighted", C.c_int32),
+        ("has_csr_edges", C.c_int32),
+        ("csr_weighted", C.c_int32),
+        ("csr_derived", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
+
+
+BUILD_CSR_EDGES = 1
+
 # Every symbol include/seraph.h declares: (name, restype, argtypes)
 _VP, _U32, _U64, _I32, _D = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double
 SIGNATURES = {
@@ -193,6 +226,12 @@ SIGNATURES = {
     "sr_get_trace": (C.c_int, [_VP, C.POINTER(TraceEventC), _U64, C.POINTER(_U64)]),
     "sr_verify_fixpoint": (C.c_int, [_VP, C.c_int, _VP, C.POINTER(_U64)]),
     "sr_bench_pull_sweep": (C.c_int, [_VP, C.c_int, _U32, C.POINTER(_D), C.POINTER(_U64)]),
+    "sr_build_graph": (C.c_int, [_VP, _U32, _U64, _VP, _VP, _VP, _U32, C.c_int]),
+    "sr_generate_graph": (C.c_int, [_VP, C.POINTER(GraphSpec), C.c_int]),
+    "sr_graph_info_get": (C.c_int, [_VP, C.POINTER(GraphInfo)]),
+    "sr_export_graph": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "sr_rmat_generate_device": (C.c_int, [C.c_int, C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP,
+                                          _U64, _U32, _U32, _VP]),
     "sr_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8 * 128)]),
     "sr_host_alloc": (C.c_int, [_U64, C.POINTER(_VP)]),
     "sr_host_free": (None, [_VP]),

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "devgraph.h"
 #include "engine.h"
 #include "nccl_dyn.h"
 #include "seraph.h"
@@ -126,6 +127,59 @@ int sr_load_pages(sr_ctx* ctx, uint32_t n, uint32_t cap, int weighted, const sr_
                   uint32_t np) {
   if (!ctx) return SR_E_CONFIG;
   return guard(ctx, [&] { ctx->eng->load_pages(n, cap, weighted != 0, pages, np); });
+}
+
+int sr_build_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                   const uint32_t* w, uint32_t cap, int flags) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->build_graph(n, m, src, dst, w, cap, flags & SR_BUILD_CSR_EDGES); });
+}
+
+int sr_generate_graph(sr_ctx* ctx, const sr_graph_spec* spec, int flags) {
+  if (!ctx || !spec) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->generate_graph(*spec, flags & SR_BUILD_CSR_EDGES); });
+}
+
+int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out) {
+  if (!ctx || !out) return SR_E_CONFIG;
+  ctx->eng->graph_info(*out);
+  return SR_OK;
+}
+
+int sr_export_graph(sr_ctx* ctx, uint64_t* out_offsets, uint32_t* out_neighbors,
+                    uint32_t* out_weights, uint64_t* in_offsets, uint32_t* in_sources,
+                    uint32_t* in_weights) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] {
+    ctx->eng->export_graph(out_offsets, out_neighbors, out_weights, in_offsets, in_sources,
+                           in_weights);
+  });
+}
+
+int sr_rmat_generate_device(int device, int scale, uint64_t edge_factor, double a, double b,
+                            double c, double d, uint64_t seed, uint32_t* src, uint32_t* dst,
+                            uint64_t weight_seed, uint32_t weight_lo, uint32_t weight_hi,
+                            uint32_t* w) {
+  (void)d;  // implied: a + b + c + d = 1 (the generator compares against a, a+b, a+b+c)
+  if (scale < 1 || scale > 31 || edge_factor < 1 || !src || !dst) return SR_E_CONFIG;
+  if (w && (weight_lo < 1 || weight_lo > weight_hi)) return SR_E_CONFIG;
+  return guard(nullptr, [&] {
+    SR_CUDA(cudaSetDevice(device));
+    const uint64_t m = (uint64_t(1) << scale) * edge_factor;
+    uint32_t *ds = nullptr, *dd = nullptr, *dw = nullptr;
+    SR_CUDA(cudaMalloc(&ds, m * 4));
+    SR_CUDA(cudaMalloc(&dd, m * 4));
+    if (w) SR_CUDA(cudaMalloc(&dw, m * 4));
+    seraph::dg_rmat(scale, m, a, b, c, seed, ds, dd, nullptr);
+    if (w) seraph::dg_weights(m, weight_seed, weight_lo, weight_hi, dw, nullptr);
+    cudaError_t e = cudaMemcpy(src, ds, m * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(dst, dd, m * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && w) e = cudaMemcpy(w, dw, m * 4, cudaMemcpyDeviceToHost);
+    cudaFree(ds);
+    cudaFree(dd);
+    if (dw) cudaFree(dw);
+    SR_CUDA(e);
+  });
 }
 
 uint64_t sr_loaded_page_bytes(const sr_ctx* ctx) {

@@ -104,7 +104,6 @@ struct PrArgs {
   const float* inv_outdeg;
   float* hub_sum;
   float* acc;   // source-blocked mode: partial sums accumulate here (else null)
-  const uint32_t* pi;  // hot-source relabel: contrib index of vertex v (else null)
   RunCtr* ctr;
   float base;   // (1-d)/N
   float damp;   // d

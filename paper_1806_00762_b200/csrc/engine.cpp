@@ -3,6 +3,7 @@
 // (proj/src/engine.cpp:225-416) decision for decision; all per-vertex work
 // runs in the sm_100a kernels of kernels.cu.
 #include "engine.h"
+#include "devgraph.h"
 
 #include <algorithm>
 #include <chrono>
@@ -138,28 +139,199 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   csr_weighted_ = false;
   if (nbr && m) {
     out_nbr_.reserve(m);
-    SR_CUDA(cudaMemcpyAsync(out_nbr_.p, nbr, m * 4, cudaMemcpyHostToDevice, xs_));
+    SR_CUDA(cudaMemcpyAsync(out_nbr_.p, nbr, m * 4, cudaMemcpyDefault, xs_));
     bytes += m * 4;
     if (w) {
       out_w_.reserve(m);
-      SR_CUDA(cudaMemcpyAsync(out_w_.p, w, m * 4, cudaMemcpyHostToDevice, xs_));
+      SR_CUDA(cudaMemcpyAsync(out_w_.p, w, m * 4, cudaMemcpyDefault, xs_));
       bytes += m * 4;
       csr_weighted_ = true;
     }
   } else if (nbr && w) {
     csr_weighted_ = true;  // weighted graph without edges
   }
-  const size_t npad = (size_t(n) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
-  outdeg_.reserve(npad);
-  SR_CUDA(cudaMemsetAsync(outdeg_.p, 0, npad * 4, xs_));
-  launch_outdeg(out_off_.p, n, outdeg_.p, xs_);
-  SR_CUDA(cudaStreamSynchronize(xs_));
-  has_csr_ = true;
-  csr_derived_ = false;
-  prl_.built = false;  // the relabel follows the out-degrees
+  finish_csr();
   last_upload_bytes += bytes;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Engine::finish_csr() {
+  const size_t npad = (size_t(n_) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
+  outdeg_.reserve(npad);
+  SR_CUDA(cudaMemsetAsync(outdeg_.p, 0, npad * 4, xs_));
+  launch_outdeg(out_off_.p, n_, outdeg_.p, xs_);
+  SR_CUDA(cudaStreamSynchronize(xs_));
+  has_csr_ = true;
+  csr_derived_ = false;
+}
+
+// ---------------------------------------------------------------------------
+// Device-side graph build (devgraph.cu): the
+// reference's build_csr + build_csc_pages (graph.cpp:30-94) as stable radix
+// sorts on the GPU, then the normal residency path (tiles, arena, push
+// adjacency) with the page arrays copied device to device.
+// ---------------------------------------------------------------------------
+void Engine::build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<uint32_t>& dst,
+                             DBuf<uint32_t>& w, bool weighted, uint32_t cap, bool csr_edges) {
+  if (cap < 1) throw EngineError(SR_E_CONFIG, "page vertex capacity must be >= 1");
+  if (n == 0) throw EngineError(SR_E_INPUT, "graph has no vertices");
+  if (!dg_ids_valid(n, m, src.p, dst.p, cs_))
+    throw EngineError(SR_E_INPUT, "edge endpoint out of range (graph.cpp:9-22)");
+  const auto t0 = std::chrono::steady_clock::now();
+  const uint32_t np = uint32_t((uint64_t(n) + cap - 1) / cap);
+  DBuf<unsigned long long> in_off;
+  DBuf<uint32_t> in_src, in_w, local;
+  in_off.reserve(size_t(n) + 1);
+  in_src.reserve(std::max<uint64_t>(m, 1));
+  if (weighted) in_w.reserve(std::max<uint64_t>(m, 1));
+  dg_stable_adjacency(n, m, dst.p, src.p, weighted ? w.p : nullptr, in_off.p, in_src.p,
+                      weighted ? in_w.p : nullptr, cs_);
+  out_off_.reserve(size_t(n) + 1);
+  if (csr_edges) {
+    out_nbr_.reserve(std::max<uint64_t>(m, 1));
+    if (weighted) out_w_.reserve(std::max<uint64_t>(m, 1));
+  }
+  dg_stable_adjacency(n, m, src.p, csr_edges ? dst.p : nullptr, csr_edges && weighted ? w.p : nullptr,
+                      out_off_.p, csr_edges ? out_nbr_.p : nullptr,
+                      csr_edges && weighted ? out_w_.p : nullptr, cs_);
+  local.reserve(size_t(n) + np);
+  dg_page_offsets(n, cap, in_off.p, local.p, cs_);
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  src.release();
+  dst.release();
+  w.release();
+  n_ = n;
+  m_ = m;
+  has_csr_edges_ = csr_edges;
+  csr_weighted_ = csr_edges && weighted;
+  finish_csr();
+  PinBuf<uint32_t> local_h;
+  PinBuf<unsigned long long> in_off_h;
+  local_h.reserve(size_t(n) + np);
+  in_off_h.reserve(size_t(n) + 1);
+  SR_CUDA(cudaMemcpy(local_h.p, local.p, (size_t(n) + np) * 4, cudaMemcpyDeviceToHost));
+  SR_CUDA(cudaMemcpy(in_off_h.p, in_off.p, (size_t(n) + 1) * 8, cudaMemcpyDeviceToHost));
+  std::vector<sr_page_view> views(np);
+  for (uint32_t p = 0; p < np; ++p) {
+    const uint64_t vb = uint64_t(p) * cap, ve = std::min<uint64_t>(vb + cap, n);
+    const uint64_t e0 = in_off_h.p[vb], e1 = in_off_h.p[ve];
+    views[p] = sr_page_view{uint32_t(vb), uint32_t(ve), local_h.p + vb + p, in_src.p + e0,
+                            weighted ? in_w.p + e0 : nullptr, e1 - e0};
+  }
+  last_upload_seconds = 0;
+  last_upload_bytes = 0;
+  load_pages(n, cap, weighted, views.data(), np);  // device-to-device into the arena
+  SR_CUDA(cudaDeviceSynchronize());
+  last_upload_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Engine::build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                         const uint32_t* w, uint32_t cap, bool csr_edges) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (m && (!src || !dst)) throw EngineError(SR_E_INPUT, "edge list: null endpoints");
+  DBuf<uint32_t> ds, dd, dw;
+  ds.reserve(std::max<uint64_t>(m, 1));
+  dd.reserve(std::max<uint64_t>(m, 1));
+  if (m) {
+    SR_CUDA(cudaMemcpyAsync(ds.p, src, m * 4, cudaMemcpyDefault, cs_));
+    SR_CUDA(cudaMemcpyAsync(dd.p, dst, m * 4, cudaMemcpyDefault, cs_));
+  }
+  if (w) {
+    dw.reserve(std::max<uint64_t>(m, 1));
+    if (m) SR_CUDA(cudaMemcpyAsync(dw.p, w, m * 4, cudaMemcpyDefault, cs_));
+  }
+  build_graph_dev(n, m, ds, dd, dw, w != nullptr, cap, csr_edges);
+}
+
+void Engine::generate_graph(const sr_graph_spec& g, bool csr_edges) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (g.scale < 1 || g.scale > 31 || g.edge_factor < 1)
+    throw EngineError(SR_E_CONFIG, "rmat: scale must be in [1, 31], edge factor >= 1");
+  const double sum = g.a + g.b + g.c + g.d;
+  if (g.a < 0 || g.b < 0 || g.c < 0 || g.d < 0 || sum < 1 - 1e-9 || sum > 1 + 1e-9)
+    throw EngineError(SR_E_CONFIG, "rmat quadrant probabilities must be >= 0 and sum to 1");
+  const bool weighted = g.weight_hi != 0;
+  if (weighted && (g.weight_lo < 1 || g.weight_lo > g.weight_hi))
+    throw EngineError(SR_E_CONFIG, "weights: need 1 <= lo <= hi");
+  const uint32_t n = uint32_t(uint64_t(1) << g.scale);
+  const uint64_t m0 = uint64_t(n) * g.edge_factor;
+  DBuf<uint32_t> s0, d0, w0;
+  s0.reserve(m0);
+  d0.reserve(m0);
+  dg_rmat(g.scale, m0, g.a, g.b, g.c, g.seed, s0.p, d0.p, cs_);
+  if (weighted) {
+    w0.reserve(m0);
+    dg_weights(m0, g.weight_seed, g.weight_lo, g.weight_hi, w0.p, cs_);
+  }
+  if (!g.symmetrize) {
+    build_graph_dev(n, m0, s0, d0, w0, weighted, g.page_vertex_capacity, csr_edges);
+    return;
+  }
+  DBuf<uint32_t> s1, d1, w1;
+  s1.reserve(2 * m0);
+  d1.reserve(2 * m0);
+  if (weighted) w1.reserve(2 * m0);
+  dg_symmetrize(m0, s0.p, d0.p, weighted ? w0.p : nullptr, s1.p, d1.p, weighted ? w1.p : nullptr,
+                cs_);
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  s0.release();
+  d0.release();
+  w0.release();
+  build_graph_dev(n, 2 * m0, s1, d1, w1, weighted, g.page_vertex_capacity, csr_edges);
+}
+
+void Engine::graph_info(sr_graph_info& gi) const {
+  gi = sr_graph_info{};
+  gi.num_vertices = n_;
+  gi.num_edges = m_;
+  gi.num_pages = uint32_t(pages_.size());
+  gi.page_vertex_capacity = cap_;
+  gi.weighted = weighted_ ? 1 : 0;
+  gi.has_csr_edges = has_csr_edges_ ? 1 : 0;
+  gi.csr_weighted = csr_weighted_ ? 1 : 0;
+  gi.csr_derived = csr_derived_ ? 1 : 0;
+}
+
+void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w, uint64_t* in_off,
+                          uint32_t* in_src, uint32_t* in_w) {
+  SR_CUDA(cudaSetDevice(dev_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  if ((out_off || out_nbr || out_w) && !has_csr_) throw EngineError(SR_E_DATA, "no csr loaded");
+  if (out_off) SR_CUDA(cudaMemcpy(out_off, out_off_.p, (size_t(n_) + 1) * 8, cudaMemcpyDeviceToHost));
+  if (out_nbr) {
+    if (!has_csr_edges_) throw EngineError(SR_E_DATA, "csr adjacency not on the device");
+    if (m_) SR_CUDA(cudaMemcpy(out_nbr, out_nbr_.p, m_ * 4, cudaMemcpyDeviceToHost));
+  }
+  if (out_w) {
+    if (!csr_weighted_) throw EngineError(SR_E_DATA, "csr has no weights");
+    if (m_) SR_CUDA(cudaMemcpy(out_w, out_w_.p, m_ * 4, cudaMemcpyDeviceToHost));
+  }
+  if (!(in_off || in_src || in_w)) return;
+  if (!pages_loaded_) throw EngineError(SR_E_DATA, "no pages loaded");
+  if (in_w && !weighted_) throw EngineError(SR_E_DATA, "pages have no weights");
+  uint64_t at = 0;
+  std::vector<uint32_t> loc;
+  for (uint32_t p = 0; p < pages_.size(); ++p) {
+    const PageMeta& pm = pages_[p];
+    const uint32_t range = pm.ve - pm.vb;
+    const bool dev = pm.h_offs == nullptr;  // resident: arena; out-of-core: pinned stage
+    const PageDesc& d = page_desc_h_[p];
+    const uint32_t* offs = dev ? d.offs : pm.h_offs;
+    const uint32_t* srcp = dev ? d.src : pm.h_src;
+    const uint32_t* wp = dev ? d.w : pm.h_w;
+    if (!offs) throw EngineError(SR_E_DATA, "page " + std::to_string(p) + " is not held");
+    if (in_off) {
+      loc.resize(size_t(range) + 1);
+      SR_CUDA(cudaMemcpy(loc.data(), offs, loc.size() * 4, cudaMemcpyDefault));
+      for (uint32_t i = 0; i <= range; ++i) in_off[pm.vb + i] = at + loc[i];
+    }
+    if (pm.edges) {
+      if (in_src) SR_CUDA(cudaMemcpy(in_src + at, srcp, pm.edges * 4, cudaMemcpyDefault));
+      if (in_w) SR_CUDA(cudaMemcpy(in_w + at, wp, pm.edges * 4, cudaMemcpyDefault));
+    }
+    at += pm.edges;
+  }
 }
 
 void Engine::maybe_derive_csr() {
@@ -327,7 +499,6 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
   sb_.built = false;
-  prl_.built = false;
   page_desc_h_.assign(np, PageDesc{});
   for (uint32_t p = 0; p < np; ++p) {
     page_desc_h_[p].vertex_begin = pages_[p].vb;
@@ -368,12 +539,12 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       const PageDesc& d = page_desc_h_[p];
       SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.offs), pm.h_offs, (size_t(d.range) + 1) * 4,
                               cudaMemcpyHostToDevice, xs_));
-      if (pm.edges) {
+      if (pm.edges) {  // host (pinned/pageable) or device (sr_build_graph) sources
         SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.src), pm.h_src, pm.edges * 4,
-                                cudaMemcpyHostToDevice, xs_));
+                                cudaMemcpyDefault, xs_));
         if (weighted)
           SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.w), pm.h_w, pm.edges * 4,
-                                  cudaMemcpyHostToDevice, xs_));
+                                  cudaMemcpyDefault, xs_));
       }
       SR_CUDA(cudaEventRecord(page_events_[p], xs_));
       pm.on_device = true;
@@ -447,11 +618,23 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       place.push_back({p, at});
       at += pm.bytes / 4;
     }
+    auto on_device = [](const void* p) {
+      cudaPointerAttributes at{};
+      return p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+             at.type == cudaMemoryTypeDevice;
+    };
+    const bool dev_src = !place.empty() && on_device(pages_[place[0].first].h_src);
     parallel_for(place.size(), [&](size_t k) {
       PageMeta& pm = pages_[place[k].first];
       uint32_t* base = stage_.p + place[k].second;
       const size_t r1 = size_t(pm.ve - pm.vb) + 1;
       std::memcpy(base, pm.h_offs, r1 * 4);
+      if (dev_src) {  // device-built graph under a forced budget: stage it on the host
+        SR_CUDA(cudaMemcpy(base + r1, pm.h_src, pm.edges * 4, cudaMemcpyDeviceToHost));
+        if (weighted)
+          SR_CUDA(cudaMemcpy(base + r1 + pm.edges, pm.h_w, pm.edges * 4, cudaMemcpyDeviceToHost));
+        return;
+      }
       std::memcpy(base + r1, pm.h_src, pm.edges * 4);
       if (weighted) std::memcpy(base + r1 + pm.edges, pm.h_w, pm.edges * 4);
     });
@@ -623,10 +806,6 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.contrib_out = contrib_b_.p;
       a.inv_outdeg = inv_outdeg_.p;
       a.hub_sum = hub_sum_.p;
-      if (prl_.built) {
-        a.pages = prl_.desc.p;
-        a.pi = prl_.pi.p;
-      }
       a.ctr = ctr;
       a.base = float((1.0 - pr_damp_) / double(n_));
       a.damp = float(pr_damp_);
@@ -1559,33 +1738,6 @@ bool Engine::build_src_blocks(uint64_t blk) {
   return true;
 }
 
-// Hot-source relabel (SERAPH_PR_RELABEL: unset = when the contribution array
-// outgrows half the L2, 0 = never, 1 = always).  Built once per resident
-// page set, on the device: radix sort of the out-degrees, inverse
-// permutation, relabelled source arena.  Values are unchanged: every
-// destination sums the same contributions in the same edge order.
-bool Engine::build_pr_relabel() {
-  if (prl_.built) return true;
-  int mode = -1;
-  if (const char* e = std::getenv("SERAPH_PR_RELABEL")) mode = std::atoi(e);
-  if (mode == 0 || !all_resident_ || world_ > 1 || comm_ || n_ == 0 || !has_csr_) return false;
-  if (mode < 0 && uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return false;
-  const uint32_t np = uint32_t(pages_.size());
-  prl_.pi.reserve(n_);
-  prl_.gsrc.reserve(std::max<size_t>(arena_src_.n, 4));
-  launch_pr_relabel(outdeg_.p, n_, prl_.pi.p, arena_src_.p, arena_src_.n & ~size_t(3),
-                    prl_.gsrc.p, cs_);
-  std::vector<PageDesc> desc(page_desc_h_);
-  for (uint32_t p = 0; p < np; ++p)
-    if (desc[p].src) desc[p].src = prl_.gsrc.p + (desc[p].src - arena_src_.p);
-  prl_.desc.reserve(std::max<uint32_t>(np, 1));
-  SR_CUDA(cudaMemcpyAsync(prl_.desc.p, desc.data(), np * sizeof(PageDesc), cudaMemcpyHostToDevice,
-                          cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));  // desc is a stack vector
-  prl_.built = true;
-  return true;
-}
-
 // Source-blocked dense pull (K1): when the vertex array outgrows the L2,
 // a baseline-schedule dense pass sweeps the source-blocked sub-pages block by
 // block, so every launch gathers from one blk-vertex slice that stays in
@@ -1705,20 +1857,13 @@ void Engine::pr_blocked_pass(float base, float damp) {
 // ---------------------------------------------------------------------------
 void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
                           std::vector<sr_pass_stats>& passes) {
-  const bool relabel = build_pr_relabel();
   uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
   if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
-  const bool blocked = !relabel && build_src_blocks(pr_blk);
-  const uint32_t* pi = relabel ? prl_.pi.p : nullptr;
+  const bool blocked = build_src_blocks(pr_blk);
   const auto wall0 = std::chrono::steady_clock::now();
   SR_CUDA(cudaEventRecord(ev_start_, cs_));
   launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
-  if (relabel) {  // positions of vertices without out-edges are read as 0, never written
-    SR_CUDA(cudaMemsetAsync(contrib_a_.p, 0, size_t(n_) * 4, cs_));
-    SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
-  }
-  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, pi, n_,
-                 n_ ? float(1.0 / double(n_)) : 0.f, cs_);
+  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
   if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
     ctr_used_ = 0;
@@ -1742,7 +1887,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     } else {
       po = dense_pass_wall(cfg, kGateOff, false, it, true);
       launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
-                             inv_outdeg_.p, pi, base, float(cfg.pr_damping), cs_);
+                             inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
     }
     exchange_round(true);
     if (ctr_used_)

@@ -125,6 +125,14 @@ class Engine {
   void run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out, sr_metrics& m,
            std::vector<sr_pass_stats>& passes);
   uint64_t verify_fixpoint(int algo, const uint32_t* values_host);
+  // device-side graph build (devgraph.cu): edge list (host or device
+  // pointers) or the on-device RMAT generator -> stable CSR/CSC -> resident
+  void build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                   const uint32_t* w, uint32_t cap, bool csr_edges);
+  void generate_graph(const sr_graph_spec& spec, bool csr_edges);
+  void graph_info(sr_graph_info& gi) const;
+  void export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w, uint64_t* in_off,
+                    uint32_t* in_src, uint32_t* in_w);
   void bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges);
   void attach_world(int rank, int world, const uint8_t id[128]);
   void flush_l2(uint64_t bytes);
@@ -189,6 +197,9 @@ class Engine {
   DBuf<uint32_t> out_nbr_, out_w_;
   DBuf<uint32_t> outdeg_;  // u32 out-degrees (census/compaction vector loads)
   void maybe_derive_csr();  // push adjacency = transpose of resident pages
+  void finish_csr();        // out-degrees + flags after the CSR arrays are in place
+  void build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<uint32_t>& dst,
+                       DBuf<uint32_t>& w, bool weighted, uint32_t cap, bool csr_edges);
   bool csr_derived_ = false;
 
   // pages
@@ -284,15 +295,6 @@ class Engine {
   bool last_pass_blocked_ = false;
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
   int l2_bytes_ = 0;
-  // Hot-source relabel of the resident pages for PageRank (K8 locality):
-  // pi (vertex -> position by descending out-degree) and a relabelled copy
-  // of the source arena; contributions are stored in pi order.
-  struct PrRelabel {
-    bool built = false;
-    DBuf<uint32_t> pi, gsrc;
-    DBuf<PageDesc> desc;
-  } prl_;
-  bool build_pr_relabel();
   // persistent sparse stage buffers
   DBuf<Census> loop_cz_;
   DBuf<RunCtr> loop_ctr_;

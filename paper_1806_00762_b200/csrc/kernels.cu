@@ -12,14 +12,11 @@
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
 #include <cooperative_groups.h>
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
-#include <algorithm>
 #include <cstdint>
 
 #include "device_types.h"
-#include "errors.h"
 #include "kernels.h"
 
 namespace seraph {
@@ -55,6 +52,13 @@ __device__ __forceinline__ T warp_sum(T x) {
 }
 
 __device__ __forceinline__ uint32_t warp_min(uint32_t x) { return __reduce_min_sync(kFull, x); }
+
+// Random 4-byte gathers of vertex values (K1 async) and contributions (K8)
+// go through L1 (allocating loads).  Measured on C2/C3/C4: ld.global.cg is
+// 1.1-1.5x slower and ld.global.nc.L1::no_allocate 1.05-1.7x slower -- the
+// L1 serves the hub values that many tiles gather.
+__device__ __forceinline__ uint32_t gather_rw(const uint32_t* p) { return *p; }
+__device__ __forceinline__ float gather_ro(const float* p) { return __ldg(p); }
 
 // VertexProgram::combine (programs.hpp:31-45): saturating at kUnreached.
 template <int A>
@@ -232,16 +236,35 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
         if (!att || cur <= candidate_floor<A>()) continue;
+        // lanes take aligned 8-edge runs (two uint4 loads of sources and
+        // weights), drop edges that cannot improve, gather the rest back to
+        // back (~47 % of RMAT in-edges are in hub chunks)
         uint32_t best = kUnreached;
-        uint32_t e = tile.x + lane;
-#pragma unroll 8
-        for (; e < tile.y; e += 32) {
-          const uint32_t sidx = __ldcs(src + e);
-          const uint32_t w = (A == kSssp) ? __ldcs(wts + e) : 0u;
-          if (A == kSssp && w >= cur) continue;  // cannot improve: skip the gather
-          const uint32_t sv = DET ? __ldg(values_ro + sidx) : a.values[sidx];
-          c.gathers += 1;
-          best = min(best, combine<A>(sv, w));
+        for (uint32_t p0 = (tile.x & ~7u) + lane * kLaneEdges; p0 < tile.y;
+             p0 += 32 * kLaneEdges) {
+          const uint4* sp = reinterpret_cast<const uint4*>(src + p0);
+          const uint4 s0 = __ldcs(sp), s1 = __ldcs(sp + 1);
+          uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+          if (A == kSssp) {
+            const uint4* wp = reinterpret_cast<const uint4*>(wts + p0);
+            w0 = __ldcs(wp);
+            w1 = __ldcs(wp + 1);
+          }
+          const uint32_t si[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          const uint32_t wv[kLaneEdges] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          unsigned live = 0;
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t)
+            if (p0 + t >= tile.x && p0 + t < tile.y && (A != kSssp || wv[t] < cur))
+              live |= 1u << t;
+          uint32_t sv[kLaneEdges];
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t)
+            sv[t] = (live >> t & 1u) ? (DET ? __ldg(values_ro + si[t]) : gather_rw(a.values + si[t]))
+                                     : kUnreached;
+          c.gathers += __popc(live);
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t) best = min(best, combine<A>(sv[t], wv[t]));
         }
         best = warp_min(best);
         if (lane == 0 && best < cur) {
@@ -359,7 +382,8 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             uint32_t sv[kLaneEdges];
 #pragma unroll
             for (int t = 0; t < kLaneEdges; ++t)
-              sv[t] = (live >> t & 1u) ? (DET ? __ldg(values_ro + sv_idx[t]) : a.values[sv_idx[t]])
+              sv[t] = (live >> t & 1u) ? (DET ? __ldg(values_ro + sv_idx[t])
+                                              : gather_rw(a.values + sv_idx[t]))
                                        : kUnreached;
             c.gathers += __popc(live);
             uint32_t run_ent = 0xffffffffu, run_best = kUnreached;
@@ -644,19 +668,6 @@ __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __r
 // with uint4 source loads, gathers of contrib[src], per-lane fold and a
 // shared-memory float atomicAdd merge; hub chunks go through hub_sum.
 // ---------------------------------------------------------------------------
-// Contributions live in gather order: identity, or the hot-source relabel
-// pi (sources by descending out-degree) so the gathers of K8 concentrate on
-// an L2-resident prefix.  A vertex without out-edges is never gathered:
-// under the relabel its (zero) contribution is not written.
-__device__ __forceinline__ void pr_store_contrib(float* contrib, const uint32_t* pi, uint32_t v,
-                                                 float x) {
-  if (!pi) {
-    contrib[v] = x;
-  } else if (x != 0.f) {
-    contrib[__ldg(pi + v)] = x;
-  }
-}
-
 __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
@@ -696,10 +707,19 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           c.edges += offs[d + 1] - lo_d;
         }
         float sum = 0.f;
-        uint32_t e = tile.x + lane;
-        if (e < tile.y) c.gathers += (tile.y - e + 31) / 32;
-#pragma unroll 8
-        for (; e < tile.y; e += 32) sum += __ldg(contrib + __ldcs(src + e));
+        if (lane == 0) c.gathers += tile.y - tile.x;
+        for (uint32_t p0 = (tile.x & ~7u) + lane * kLaneEdges; p0 < tile.y;
+             p0 += 32 * kLaneEdges) {
+          const uint4* sp = reinterpret_cast<const uint4*>(src + p0);
+          const uint4 s0 = __ldcs(sp), s1 = __ldcs(sp + 1);
+          const uint32_t si[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          float x[kLaneEdges];
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t)
+            x[t] = (p0 + t >= tile.x && p0 + t < tile.y) ? gather_ro(contrib + si[t]) : 0.f;
+#pragma unroll
+          for (int t = 0; t < kLaneEdges; ++t) sum += x[t];
+        }
         sum = warp_sum(sum);
         if (lane == 0) {
           if (a.acc) atomicAdd(a.acc + vb + d, sum);  // source-blocked partial
@@ -720,7 +740,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           if (deg == 0 && !a.acc) {  // no in-edges: teleport share only
             const uint32_t v = vb + i;
             a.rank_out[v] = a.base;
-            pr_store_contrib(a.contrib_out, a.pi, v, a.base * a.inv_outdeg[v]);
+            a.contrib_out[v] = a.base * a.inv_outdeg[v];
           }
         }
         c.attempts += in;
@@ -770,7 +790,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           float x[kLaneEdges];
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t)
-            x[t] = (live >> t & 1u) ? __ldg(contrib + sidx[t]) : 0.f;
+            x[t] = (live >> t & 1u) ? gather_ro(contrib + sidx[t]) : 0.f;
           c.gathers += __popc(live);
           uint32_t run_ent = 0xffffffffu;
           float run = 0.f;
@@ -796,7 +816,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
         }
         const float r = a.base + a.damp * sum_of[i];
         a.rank_out[v] = r;
-        pr_store_contrib(a.contrib_out, a.pi, v, r * a.inv_outdeg[v]);
+        a.contrib_out[v] = r * a.inv_outdeg[v];
       }
       __syncwarp();
     }
@@ -806,56 +826,21 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
 
 __global__ void pr_hub_finalize_kernel(const uint32_t* hub_vertex, uint32_t n_hubs,
                                        float* hub_sum, float* rank_out, float* contrib_out,
-                                       const float* inv_outdeg, const uint32_t* pi, float base,
-                                       float damp) {
+                                       const float* inv_outdeg, float base, float damp) {
   const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= n_hubs) return;
   const uint32_t v = hub_vertex[h];
   const float r = base + damp * hub_sum[h];
   rank_out[v] = r;
-  pr_store_contrib(contrib_out, pi, v, r * inv_outdeg[v]);
+  contrib_out[v] = r * inv_outdeg[v];
   hub_sum[h] = 0.f;
 }
 
-__global__ void pr_init_kernel(float* rank, float* contrib, const float* inv_outdeg,
-                               const uint32_t* pi, uint32_t n, float init) {
+__global__ void pr_init_kernel(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
+                               float init) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     rank[v] = init;
-    pr_store_contrib(contrib, pi, v, init * inv_outdeg[v]);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Hot-source relabel for K8 (built once per resident page set): pi = rank of
-// every vertex in descending out-degree order (stable, so ties keep id
-// order), then a relabelled copy of every page's in_sources.  On RMAT-26 the
-// ~11 M highest-degree sources (44 MB of contributions) carry ~97 % of the
-// in-edges, so the gathers hit a prefix that stays in the 126 MB L2 instead
-// of 32-byte DRAM sectors spread over the whole 256 MB array.
-// ---------------------------------------------------------------------------
-__global__ void iota_kernel(uint32_t* p, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    p[i] = i;
-}
-
-__global__ void perm_invert_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* pi) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    pi[perm[i]] = i;
-}
-
-// out[i] = pi[src[i]] over a whole source arena (uint4 vectors; the arena is
-// 32 B aligned and padded).  Slack words (ids >= n) map to 0.
-__global__ void relabel_src_kernel(const uint4* __restrict__ src, size_t n4,
-                                   const uint32_t* __restrict__ pi, uint32_t n, uint4* out) {
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const uint4 s = __ldcs(src + i);
-    uint4 r;
-    r.x = s.x < n ? __ldg(pi + s.x) : 0u;
-    r.y = s.y < n ? __ldg(pi + s.y) : 0u;
-    r.z = s.z < n ? __ldg(pi + s.z) : 0u;
-    r.w = s.w < n ? __ldg(pi + s.w) : 0u;
-    __stcs(out + i, r);
+    contrib[v] = init * inv_outdeg[v];
   }
 }
 
@@ -1461,42 +1446,16 @@ void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s) {
 
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
-                            const uint32_t* pi, float base, float damp, cudaStream_t s) {
+                            float base, float damp, cudaStream_t s) {
   if (!n_hubs) return;
   pr_hub_finalize_kernel<<<(n_hubs + 255) / 256, 256, 0, s>>>(hub_vertex, n_hubs, hub_sum,
                                                               rank_out, contrib_out, inv_outdeg,
-                                                              pi, base, damp);
+                                                              base, damp);
 }
 
-void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, const uint32_t* pi,
-                    uint32_t n, float init, cudaStream_t s) {
-  pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, pi, n, init);
-}
-
-void launch_pr_relabel(const uint32_t* outdeg, uint32_t n, uint32_t* pi, const uint32_t* src,
-                       size_t src_words, uint32_t* gsrc, cudaStream_t s) {
-  if (!n) return;
-  uint32_t *keys = nullptr, *ids = nullptr, *perm = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0;
-  SR_CUDA(cudaMallocAsync(&keys, size_t(n) * 4, s));
-  SR_CUDA(cudaMallocAsync(&ids, size_t(n) * 4, s));
-  SR_CUDA(cudaMallocAsync(&perm, size_t(n) * 4, s));
-  iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n);
-  SR_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, outdeg, keys, ids, perm,
-                                                    int(n), 0, 32, s));
-  SR_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
-  SR_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, outdeg, keys, ids, perm,
-                                                    int(n), 0, 32, s));
-  perm_invert_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, n, pi);
-  const size_t n4 = src_words / 4;
-  if (n4)
-    relabel_src_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
-        reinterpret_cast<const uint4*>(src), n4, pi, n, reinterpret_cast<uint4*>(gsrc));
-  SR_CUDA(cudaFreeAsync(tmp, s));
-  SR_CUDA(cudaFreeAsync(keys, s));
-  SR_CUDA(cudaFreeAsync(ids, s));
-  SR_CUDA(cudaFreeAsync(perm, s));
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n, float init,
+                    cudaStream_t s) {
+  pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, n, init);
 }
 
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,

@@ -18,13 +18,9 @@ void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
-                            const uint32_t* pi, float base, float damp, cudaStream_t s);
-void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, const uint32_t* pi,
-                    uint32_t n, float init, cudaStream_t s);
-// Hot-source relabel: pi = descending-out-degree rank of every vertex;
-// gsrc[i] = pi[src[i]] over a source arena of src_words (multiple of 4).
-void launch_pr_relabel(const uint32_t* outdeg, uint32_t n, uint32_t* pi, const uint32_t* src,
-                       size_t src_words, uint32_t* gsrc, cudaStream_t s);
+                            float base, float damp, cudaStream_t s);
+void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n,
+                    float init, cudaStream_t s);
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
                        cudaStream_t s);
 // K3: sparse push over the compacted frontier.

@@ -281,6 +281,21 @@ def generate_rmat_fast(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19
     return EdgeList(n, src, dst, np.zeros(0, np.uint32))
 
 
+def generate_rmat_device(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05,
+                         seed: int = 0, weights=None, device: int = 0) -> EdgeList:
+    """generate_rmat_fast (+ assign_weights_fast when weights=(lo, hi, seed)) on the
+    GPU, copied back: bit-identical to the host generator."""
+    n = 1 << scale
+    m = n * edge_factor
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    w = np.empty(m if weights else 0, np.uint32)
+    lo, hi, ws = weights if weights else (0, 0, 0)
+    N.check(N.lib.sr_rmat_generate_device(device, scale, edge_factor, a, b, c, d, seed, N.ptr(src),
+                                          N.ptr(dst), ws, lo, hi, N.ptr(w)))
+    return EdgeList(n, src, dst, w)
+
+
 def assign_weights_fast(el: EdgeList, seed: int, lo: int, hi: int, threads: int = 0) -> EdgeList:
     if lo < 1:
         raise ConfigError("minimum weight must be >= 1 (non-positive weights break SSSP)")
@@ -582,6 +597,64 @@ class Engine:
         views = _page_views(pages)
         N.check(N.lib.sr_load_pages(self._h, pages.num_vertices, pages.page_vertex_capacity,
                                     1 if pages.weighted else 0, views, len(pages.pages)), self._h)
+
+    # ---- device-side graph build ----
+    def build_graph(self, el: EdgeList, page_vertex_capacity: int, csr_edges: bool = True) -> None:
+        """build_csr + build_csc_pages (graph.cpp:30-94) on the GPU from a host
+        edge list; the result is resident as if loaded with load()/load_pages()."""
+        if page_vertex_capacity < 1:
+            raise ConfigError("page_vertex_capacity must be >= 1")
+        if el.weighted() and el.weights.size and int(el.weights.min()) < 1:
+            raise InputError("edge weight < 1")
+        N.check(N.lib.sr_build_graph(self._h, el.num_vertices, el.num_edges(), N.ptr(el.src),
+                                     N.ptr(el.dst), N.ptr(el.weights) if el.weighted() else None,
+                                     int(page_vertex_capacity),
+                                     N.BUILD_CSR_EDGES if csr_edges else 0), self._h)
+        self.num_vertices = el.num_vertices
+
+    def generate_graph(self, scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05,
+                       seed: int = 0, weights=None, symmetrize: bool = False,
+                       page_vertex_capacity: int = 0, csr_edges: bool = True) -> None:
+        """generate_rmat_fast (+ assign_weights_fast(seed=weights[2], lo, hi) when
+        weights=(lo, hi, seed), + symmetrize) and the build, all on the device."""
+        n = 1 << scale
+        spec = N.GraphSpec(scale, edge_factor, a, b, c, d, seed, 0, 0, 0, 1 if symmetrize else 0,
+                           page_vertex_capacity or (n + 15) // 16)
+        if weights is not None:
+            spec.weight_lo, spec.weight_hi, spec.weight_seed = weights
+        N.check(N.lib.sr_generate_graph(self._h, C.byref(spec),
+                                        N.BUILD_CSR_EDGES if csr_edges else 0), self._h)
+        self.num_vertices = n
+
+    def graph_info(self) -> dict:
+        gi = N.GraphInfo()
+        N.check(N.lib.sr_graph_info_get(self._h, C.byref(gi)), self._h)
+        return {k: getattr(gi, k) for k, _ in N.GraphInfo._fields_ if k != "pad_"}
+
+    def export_graph(self, arena=None, csr_edges: bool = True):
+        """(CsrGraph, PageSet, in_offsets, in_sources, in_weights): copies of the loaded
+        graph in the reference layouts (global CSC arrays behind the page views; arrays
+        from `arena.array` when given, e.g. pinned host memory)."""
+        gi = self.graph_info()
+        n, m = gi["num_vertices"], gi["num_edges"]
+        mk = (lambda k, dt: arena.array(k, dt)) if arena is not None else (lambda k, dt: np.empty(k, dt))
+        out_off = mk(n + 1, np.uint64)
+        want_nbr = csr_edges and gi["has_csr_edges"]
+        nbr = mk(m if want_nbr else 0, np.uint32)
+        ow = mk(m if (want_nbr and gi["csr_weighted"]) else 0, np.uint32)
+        in_off = np.empty(n + 1, np.uint64)
+        srcs = mk(m, np.uint32)
+        iw = mk(m if gi["weighted"] else 0, np.uint32)
+        N.check(N.lib.sr_export_graph(self._h, N.ptr(out_off), N.ptr(nbr) if want_nbr else None,
+                                      N.ptr(ow) if ow.size else None, N.ptr(in_off), N.ptr(srcs),
+                                      N.ptr(iw) if iw.size else None), self._h)
+        cap = gi["page_vertex_capacity"]
+        npg = (n + cap - 1) // cap
+        local = mk(n + npg, np.uint32)
+        if n:
+            N.check(N.lib.sr_page_offsets(n, cap, N.ptr(in_off), N.ptr(local)))
+        return (CsrGraph(n, out_off, nbr, ow),
+                pages_from_csc(n, cap, in_off, srcs, iw, local), in_off, srcs, iw)
 
     def attach_world(self, rank: int, world: int, unique_id: bytes) -> None:
         uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)

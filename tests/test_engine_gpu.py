@@ -485,7 +485,6 @@ def test_pagerank_source_blocked(blk, monkeypatch):
     """Source-blocked K8 sweeps (the path large graphs take when the contrib
     array outgrows L2), forced on a small graph: same ranks within 1e-6."""
     monkeypatch.setenv("SERAPH_PR_BLOCK_VERTS", blk)
-    monkeypatch.setenv("SERAPH_PR_RELABEL", "0")
     n = 1 << 14
     src, dst = O.generate_rmat(14, 16, seed=12)
     el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
@@ -524,25 +523,6 @@ def test_persistent_sparse_loop(monkeypatch):
         assert np.array_equal(r.values, oracle_values(sym, ps.AlgoKind.CC, 0))
 
 
-@pytest.mark.parametrize("scale", [12, 15])
-def test_pagerank_hot_source_relabel(scale, monkeypatch):
-    """Hot-source relabel (contributions stored by descending out-degree, the
-    path RMAT-26 takes), forced on small graphs with dangling vertices and
-    hubs: ranks within 1e-6 of the fp64 oracle, identical counters."""
-    monkeypatch.setenv("SERAPH_PR_RELABEL", "1")
-    n = 1 << scale
-    src, dst = O.generate_rmat(scale, 16, seed=21)
-    el = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
-    csr, pages = built(el, n // 16)
-    ref = O.pagerank(n, src, dst, 20, 0.85)
-    with ps.Engine(0) as eng:
-        r = eng.run_graph(csr, pages, ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL))
-        r2 = eng.run(ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL, pr_iterations=7))
-    assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
-    assert r.metrics.edges_read == 20 * src.size
-    assert np.abs(r2.ranks.astype(np.float64) - O.pagerank(n, src, dst, 7, 0.85)).max() < PR_TOL
-
-
 @pytest.mark.parametrize("blk", ["700", "5000"])
 def test_pull_source_blocked(blk, monkeypatch):
     """Source-blocked dense pulls (K1 over per-source-block sub-pages, the path
@@ -575,3 +555,85 @@ def test_pull_source_blocked(blk, monkeypatch):
             r = eng.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
             assert np.array_equal(r.values, want), pred
             assert eng.verify_fixpoint(ps.AlgoKind.CC, r.values) == 0
+
+
+# --------------------------------------------------------------------------
+# device-side graph build and generator
+# --------------------------------------------------------------------------
+def test_device_generator_matches_host():
+    host = ps.assign_weights_fast(ps.generate_rmat_fast(12, 8, seed=3), 7, 1, 64)
+    dev = ps.generate_rmat_device(12, 8, seed=3, weights=(1, 64, 7))
+    assert np.array_equal(host.src, dev.src) and np.array_equal(host.dst, dev.dst)
+    assert np.array_equal(host.weights, dev.weights)
+    u = ps.generate_rmat_device(10, 4, 0.25, 0.25, 0.25, 0.25, seed=5)
+    hu = ps.generate_rmat_fast(10, 4, 0.25, 0.25, 0.25, 0.25, seed=5)
+    assert np.array_equal(u.src, hu.src) and np.array_equal(u.dst, hu.dst)
+
+
+def _assert_same_graph(eng, el, cap):
+    csr_h, pages_h = built(el, cap)
+    csr_d, pages_d = eng.export_graph()[:2]
+    assert np.array_equal(csr_h.out_offsets, csr_d.out_offsets)
+    assert np.array_equal(csr_h.out_neighbors, csr_d.out_neighbors)
+    assert np.array_equal(csr_h.out_weights, csr_d.out_weights)
+    assert len(pages_h.pages) == len(pages_d.pages)
+    for ph, pd in zip(pages_h.pages, pages_d.pages):
+        assert (ph.vertex_begin, ph.vertex_end) == (pd.vertex_begin, pd.vertex_end)
+        assert np.array_equal(ph.in_offsets, pd.in_offsets)
+        assert np.array_equal(ph.in_sources, pd.in_sources)
+        assert np.array_equal(ph.in_weights, pd.in_weights)
+
+
+@pytest.mark.parametrize("chunk", [None, "997"])
+def test_device_build_bit_exact(chunk, monkeypatch):
+    """sr_build_graph = build_csr + build_csc_pages bit for bit (stable: input
+    order kept within a source/destination), single- and multi-chunk sorts;
+    runs on the device-built graph match the oracle."""
+    if chunk:
+        monkeypatch.setenv("SERAPH_BUILD_CHUNK", chunk)
+    rng = np.random.default_rng(31)
+    src, dst = O.generate_rmat(12, 8, seed=4)
+    w = O.assign_weights(src.size, 2, 1, 64)
+    cases = [(ps.EdgeList(1 << 12, src, dst, w), 256),
+             (ps.EdgeList(1 << 12, *O.symmetrize(src, dst, w)), 1000),
+             (random_edge_list(rng, 3000, 20000), 77),
+             (ps.EdgeList(5, np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.uint32)), 2)]
+    with ps.Engine(0) as eng:
+        for el, cap in cases:
+            eng.build_graph(el, cap)
+            _assert_same_graph(eng, el, cap)
+            for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+                if kind == ps.AlgoKind.SSSP and not el.weighted():
+                    continue
+                r = eng.run(program_for(kind, 0, el), cfg_of(pred=ps.PredictorMode.STRONG,
+                                                             clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, oracle_values(el, kind, 0)), kind
+        with pytest.raises(ps.InputError):
+            eng.build_graph(ps.EdgeList(4, np.array([0, 9], np.uint32), np.array([1, 2], np.uint32),
+                                        np.zeros(0, np.uint32)), 2)
+
+
+@pytest.mark.parametrize("sym", [False, True])
+def test_device_generate_graph(sym):
+    """sr_generate_graph (RMAT + weights + symmetrize + build on the device) =
+    the host pipeline; CC / SSSP on it match the oracle; lean build derives
+    the push adjacency."""
+    n = 1 << 13
+    el = ps.assign_weights_fast(ps.generate_rmat_fast(13, 16, seed=6), 9, 1, 64)
+    if sym:
+        el = ps.symmetrize(el)
+    with ps.Engine(0) as eng:
+        eng.generate_graph(13, 16, seed=6, weights=(1, 64, 9), symmetrize=sym,
+                           page_vertex_capacity=n // 16)
+        _assert_same_graph(eng, el, n // 16)
+        kind = ps.AlgoKind.CC if sym else ps.AlgoKind.SSSP
+        r = eng.run(program_for(kind, 0, el), cfg_of(pred=ps.PredictorMode.STRONG,
+                                                     clock=ps.ClockMode.WALL))
+        assert np.array_equal(r.values, oracle_values(el, kind, 0))
+        eng.generate_graph(13, 16, seed=6, weights=(1, 64, 9), symmetrize=sym,
+                           page_vertex_capacity=n // 16, csr_edges=False)
+        gi = eng.graph_info()
+        assert gi["has_csr_edges"] and gi["csr_derived"]
+        r = eng.run(program_for(kind, 0, el), cfg_of(clock=ps.ClockMode.WALL))
+        assert np.array_equal(r.values, oracle_values(el, kind, 0))
+        assert eng.verify_fixpoint(kind, r.values) == 0

@@ -30,12 +30,13 @@ def main():
     ap.add_argument("--verify", action="store_true")
     a = ap.parse_args()
     ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform,
-                            pages=a.pages, seed=0, lean=True)
-    W = bench.workload(ns)
-    print(f"# build {W['build_s']:.1f}s n={W['n']} m={W['m']}", flush=True)
+                            pages=a.pages, seed=0, lean=True, graph="device")
     eng = ps.Engine(0)
-    eng.load_csr(W["csr"], with_edges=False)
-    eng.load_pages(W["pages"])
+    W = bench.workload(ns, eng)
+    print(f"# build {W['build_s']:.1f}s n={W['n']} m={W['m']} ({W['graph']})", flush=True)
+    if not W["loaded"]:
+        eng.load_csr(W["csr"], with_edges=False)
+        eng.load_pages(W["pages"])
     kind = ps.AlgoKind(bench.ALGOS[a.algo])
     prog = ps.VertexProgram(kind, 0)
     cfg = ps.EngineConfig(predictor=ps.PredictorMode(bench.PREDS[a.predictor]),
