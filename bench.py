@@ -200,6 +200,17 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def gather_roofline(gathers_per_s, info, clocks):
+    """Second bound of the pull kernels: a random 4-byte gather touches its own
+    128 B line, and the L1TEX unit retires ~1 line (wavefront) per SM clock
+    (B300_MICROARCH.md: rt_L1tex_wf ~ 1.0 cyc/wf), so gathers/s <= SMs x f_SM."""
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = info["sm_count"] * mhz * 1e6
+    return {"achieved_gathers_per_s": round(gathers_per_s / 1e9, 2), "unit": "G/s",
+            "peak": round(peak / 1e9, 2), "frac": round(gathers_per_s / peak, 4),
+            "peak_basis": f"{info['sm_count']} SMs x {mhz:.0f} MHz x 1 L1TEX wavefront/cycle"}
+
+
 def profile_traffic(workload_key):
     """dram bytes per launch of K1 from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -332,7 +343,8 @@ def run_ours(args, rank, world, local_rank):
                 "per_unit": f"{per_edge} B/edge read + 4 B/gathered source + 8 B/attempted destination",
                 "gathered_fraction": round(k1_gathers / max(k1_edges, 1), 4),
                 "isolated_sweep": {"ms": round(ms, 4), "edges": edges,
-                                   "note": "gate-off sweep over the converged values"}}
+                                   "note": "gate-off sweep over the converged values"},
+                "gather_roofline": gather_roofline(k1_gathers / k1_s, info, clocks)}
     elif algo == 3:
         iters = args.pr_iters
         if args.budget_gb:
@@ -356,7 +368,8 @@ def run_ours(args, rank, world, local_rank):
                     "frac": round(achieved / peak, 4), "peak_source": src_,
                     "traffic": profile_traffic(f"pagerank-s{args.scale}"),
                     "algorithmic_bytes_per_launch": 8 * m + 16 * n,
-                    "per_unit": "8 B/edge + 16 B/destination per iteration"}
+                    "per_unit": "8 B/edge + 16 B/destination per iteration",
+                    "gather_roofline": gather_roofline(m * iters / step_s, info, clocks)}
 
     # the multi-pass subgraph-iteration schedules on the same resident graph
     schedules = {}

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <thread>
@@ -157,6 +158,7 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
 }
 
 void Engine::finish_csr() {
+  coverage_ = -1;  // hot_source_coverage follows the out-degrees
   const size_t npad = (size_t(n_) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
   outdeg_.reserve(npad);
   SR_CUDA(cudaMemsetAsync(outdeg_.p, 0, npad * 4, xs_));
@@ -1644,7 +1646,10 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 // 16 Mi vertices = 64 MB of f32; 0 disables).
 // ---------------------------------------------------------------------------
 bool Engine::build_src_blocks(uint64_t blk) {
-  if (sb_.built && sb_.blk_verts == blk) return true;
+  const char* bucket_env = std::getenv("SERAPH_SUBTILE_EDGES");
+  const std::string bucket = bucket_env ? bucket_env : "";
+  if (sb_.built && sb_.blk_verts == blk && sb_.bucket == bucket) return true;
+  sb_.bucket = bucket;
   if (!all_resident_ || world_ > 1 || comm_) return false;
   if (blk == 0 || n_ <= blk) return false;
   sb_.built = false;
@@ -1653,6 +1658,16 @@ bool Engine::build_src_blocks(uint64_t blk) {
     if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
   const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
   const uint32_t n_tiles = pages_.back().tile_end;
+  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!timing) return;
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[seraph] src blocks %s: %.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // 1) counts per (block, destination)
   DBuf<uint32_t> cnt;
   cnt.reserve(size_t(nb) * n_);
@@ -1664,7 +1679,9 @@ bool Engine::build_src_blocks(uint64_t blk) {
   goff.reserve(size_t(nb) * n_);
   bp_edges.reserve(size_t(nb) * np);
   bp_base.reserve(size_t(nb) * np);
+  stage("count");
   launch_src_block_scan(cnt.p, goff.p, page_desc_.p, np, nb, n_, bp_edges.p, cs_);
+  stage("scan");
   std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
   SR_CUDA(cudaMemcpyAsync(edges_h.data(), bp_edges.p, edges_h.size() * 8, cudaMemcpyDeviceToHost, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
@@ -1683,36 +1700,30 @@ bool Engine::build_src_blocks(uint64_t blk) {
   launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
                    cnt.p, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, bp_base.p,
                    sm_count_ * 8, cs_);
-  // 4) u32 local offsets, copied back to cut tiles on the host
+  stage("scatter");
+  // 4) u32 local offsets of every sub-page, then the tile cut on the device
   const size_t per_block = size_t(n_) + np;
   sb_.offs.reserve(size_t(nb) * per_block);
   launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
-  std::vector<uint32_t> offs_h(size_t(nb) * per_block);
-  SR_CUDA(cudaMemcpyAsync(offs_h.data(), sb_.offs.p, offs_h.size() * 4, cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaGetLastError());
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  std::vector<TileJob> jobs;
-  for (uint32_t b = 0; b < nb; ++b)
-    for (uint32_t p = 0; p < np; ++p) {
-      const uint32_t range = pages_[p].ve - pages_[p].vb;
-      for (uint32_t x = 0; x < range; x += (1u << 20))
-        jobs.push_back(TileJob{b * np + p, x, std::min(x + (1u << 20), range), {}, {}});
-    }
-  parallel_for(jobs.size(), [&](size_t j) {
-    const uint32_t k = jobs[j].page, b = k / np, p = k % np;
-    cut_tiles(offs_h.data() + size_t(b) * per_block + size_t(p) * cap_ + p, pages_[p].vb, jobs[j]);
-  });
-  std::vector<uint4> tiles;
-  std::vector<uint32_t> tpage;
+  const size_t K = size_t(nb) * n_;
+  DBuf<uint32_t> tcnt, tat;
+  tcnt.reserve(K + 1);
+  tat.reserve(K + 1);
+  SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));
+  launch_sub_tiles(0, n_, cap_, np, nb, sb_.offs.p, tcnt.p, nullptr, nullptr, nullptr, cs_);
+  launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, cs_);
   sb_.block_tile_begin.assign(nb + 1, 0);
-  for (auto& j : jobs) {
-    if (j.page % np == 0 && j.lo == 0) sb_.block_tile_begin[j.page / np] = uint32_t(tiles.size());
-    for (const uint4& t : j.tiles) {
-      tiles.push_back(t);
-      tpage.push_back(j.page);
-    }
-  }
-  sb_.block_tile_begin[nb] = uint32_t(tiles.size());
+  for (uint32_t b = 0; b <= nb; ++b)
+    SR_CUDA(cudaMemcpyAsync(&sb_.block_tile_begin[b], tat.p + size_t(b) * n_, 4,
+                            cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  const uint32_t n_sub_tiles = sb_.block_tile_begin[nb];
+  sb_.tiles.reserve(std::max<size_t>(n_sub_tiles, 1));
+  sb_.tile_page.reserve(std::max<size_t>(n_sub_tiles, 1));
+  launch_sub_tiles(1, n_, cap_, np, nb, sb_.offs.p, nullptr, tat.p, sb_.tiles.p, sb_.tile_page.p,
+                   cs_);
+  SR_CUDA(cudaGetLastError());
+  stage("offsets + tile cut");
   std::vector<PageDesc> desc(size_t(nb) * np);
   for (uint32_t b = 0; b < nb; ++b)
     for (uint32_t p = 0; p < np; ++p) {
@@ -1724,12 +1735,10 @@ bool Engine::build_src_blocks(uint64_t blk) {
       d.src = sb_.src.p + base_h[size_t(b) * np + p];
       d.w = weighted_ ? sb_.w.p + base_h[size_t(b) * np + p] : nullptr;
     }
-  sb_.tiles.reserve(std::max<size_t>(tiles.size(), 1));
-  sb_.tile_page.reserve(std::max<size_t>(tiles.size(), 1));
   sb_.desc.reserve(desc.size());
-  SR_CUDA(cudaMemcpy(sb_.tiles.p, tiles.data(), tiles.size() * 16, cudaMemcpyHostToDevice));
-  SR_CUDA(cudaMemcpy(sb_.tile_page.p, tpage.data(), tpage.size() * 4, cudaMemcpyHostToDevice));
-  SR_CUDA(cudaMemcpy(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc), cudaMemcpyHostToDevice));
+  SR_CUDA(cudaMemcpyAsync(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc),
+                          cudaMemcpyHostToDevice, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
   sb_.acc.reserve(n_);
   SR_CUDA(cudaMemset(sb_.acc.p, 0, size_t(n_) * 4));
   sb_.blk_verts = uint32_t(blk);
@@ -1747,13 +1756,49 @@ bool Engine::build_src_blocks(uint64_t blk) {
 // unchanged (min-combine is order independent; every destination sees
 // every in-edge once per pass).  Attempts/skips are counted on block 0,
 // edges on every block, valid updates = destinations changed in the pass.
-uint64_t Engine::pull_block_verts() const {
+//
+// Blocking pays only when the unblocked gathers have no L2 locality: by
+// default it is used when the vertex array exceeds half the L2 AND the
+// sources that fit there (the L2/8 highest out-degree vertices) carry less
+// than half of the edges -- true for uniform graphs (C4: ~15 %), false for
+// RMAT, whose hubs stay L2-resident anyway (RMAT-26 SSSP: 10.1 ms unblocked
+// vs 10.9 ms blocked; uniform-27 CC: 122 ms vs 22 ms).
+uint64_t Engine::pull_block_verts() {
   uint64_t blk = 16ull << 20;
-  if (const char* e = std::getenv("SERAPH_PULL_BLOCK_VERTS")) blk = std::strtoull(e, nullptr, 10);
+  const char* env = std::getenv("SERAPH_PULL_BLOCK_VERTS");
+  if (env) blk = std::strtoull(env, nullptr, 10);
   if (blk == 0 || n_ <= blk) return 0;
-  if (!std::getenv("SERAPH_PULL_BLOCK_VERTS") && uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2)
-    return 0;
-  return blk;
+  if (env) return blk;
+  if (uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return 0;
+  return hot_source_coverage(uint64_t(l2_bytes_) / 8) < 0.5 ? blk : 0;
+}
+
+// Fraction of the edges whose source is among the k highest out-degree
+// vertices (degree histogram on the device; cached per CSR).
+double Engine::hot_source_coverage(uint64_t k) {
+  if (coverage_k_ == k && coverage_ >= 0) return coverage_;
+  DBuf<unsigned long long> hv, he;
+  hv.reserve(kDegHistCap + 1);
+  he.reserve(kDegHistCap + 1);
+  SR_CUDA(cudaMemsetAsync(hv.p, 0, (kDegHistCap + 1) * 8, cs_));
+  SR_CUDA(cudaMemsetAsync(he.p, 0, (kDegHistCap + 1) * 8, cs_));
+  launch_degree_hist(outdeg_.p, n_, hv.p, he.p, cs_);
+  std::vector<unsigned long long> v(kDegHistCap + 1), e(kDegHistCap + 1);
+  SR_CUDA(cudaMemcpyAsync(v.data(), hv.p, v.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaMemcpyAsync(e.data(), he.p, e.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  uint64_t total = 0;
+  for (auto x : e) total += x;
+  double covered = 0;
+  uint64_t left = k;
+  for (int d = int(kDegHistCap); d >= 0 && left; --d) {
+    const uint64_t take = std::min<uint64_t>(left, v[d]);
+    if (v[d]) covered += double(e[d]) * double(take) / double(v[d]);
+    left -= take;
+  }
+  coverage_k_ = k;
+  coverage_ = total ? covered / double(total) : 1.0;
+  return coverage_;
 }
 
 bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {

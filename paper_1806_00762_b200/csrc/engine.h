@@ -288,9 +288,13 @@ class Engine {
     DBuf<PageDesc> desc;
     DBuf<float> acc;
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
+    std::string bucket;                      // SERAPH_SUBTILE_EDGES the tiles were cut with
   } sb_;
   bool build_src_blocks(uint64_t blk_verts);
-  uint64_t pull_block_verts() const;
+  uint64_t pull_block_verts();
+  double hot_source_coverage(uint64_t k);
+  double coverage_ = -1;
+  uint64_t coverage_k_ = 0;
   bool pull_blocked_pass(int gate, RunCtr* ctr);
   bool last_pass_blocked_ = false;
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();

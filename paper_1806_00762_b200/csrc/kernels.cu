@@ -12,11 +12,15 @@
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
 #include <cooperative_groups.h>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device_types.h"
+#include "errors.h"
 #include "kernels.h"
 
 namespace seraph {
@@ -1573,6 +1577,121 @@ __global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages
     if (i < range) offs[k] = uint32_t(goff[size_t(b) * n + vb + i]);
     else if (i == range) offs[k] = uint32_t(bp_edges[size_t(b) * n_pages + p]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Device tile cut of the source-blocked sub-pages (replaces the host cut for
+// them: no |V| x blocks offsets round trip).  Destination i of sub-page
+// (b, p) starts a tile when i == 0, i % kTileMaxDests == 0, it or its
+// predecessor is a hub (> kHubChunk in-edges: one tile per kHubChunk chunk),
+// or its first edge crosses a multiple of `bucket` (8 x kTileEdgeBudget); a
+// range tile ends at the next start (<= 128 destinations, < bucket + 1024
+// edges).
+// ---------------------------------------------------------------------------
+struct SubCut {
+  uint32_t n, cap, n_pages, bucket;  // bucket: range tiles split where edges cross it
+  const uint32_t* offs;  // [n_blocks][n + n_pages] sub-page local offsets
+};
+
+__device__ __forceinline__ const uint32_t* sub_offs(const SubCut& c, uint32_t b, uint32_t p) {
+  return c.offs + size_t(b) * (size_t(c.n) + c.n_pages) + size_t(p) * c.cap + p;
+}
+
+__device__ __forceinline__ bool sub_start(const uint32_t* o, uint32_t i, uint32_t bucket) {
+  if (i == 0 || i % kTileMaxDests == 0) return true;
+  const uint32_t a = o[i - 1], b = o[i], c = o[i + 1];
+  return (c - b) > kHubChunk || (b - a) > kHubChunk || (a / bucket) != (b / bucket);
+}
+
+// mode 0: tiles per destination into cnt; mode 1: write tiles at scan offsets
+__global__ void sub_tiles_kernel(int mode, SubCut c, uint32_t n_blocks, uint32_t* cnt,
+                                 const uint32_t* __restrict__ at, uint4* tiles,
+                                 uint32_t* tile_page) {
+  const uint64_t total = uint64_t(n_blocks) * c.n;
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(k / c.n), v = uint32_t(k % c.n);
+    const uint32_t p = v / c.cap, i = v - p * c.cap;
+    const uint32_t range = min(c.cap, c.n - p * c.cap);
+    const uint32_t* o = sub_offs(c, b, p);
+    const bool st = sub_start(o, i, c.bucket);
+    const uint32_t lo = o[i], deg = o[i + 1] - lo;
+    const bool hub = deg > kHubChunk;
+    const uint32_t t = st ? (hub ? (deg + kHubChunk - 1) / kHubChunk : 1u) : 0u;
+    if (mode == 0) {
+      cnt[k] = t;
+      continue;
+    }
+    if (!t) continue;
+    const uint32_t base = at[k];
+    const uint32_t sp = b * c.n_pages + p;
+    if (hub) {
+      for (uint32_t ch = 0; ch < t; ++ch) {
+        const uint32_t e0 = lo + ch * kHubChunk;
+        tiles[base + ch] = make_uint4(e0, min(e0 + kHubChunk, lo + deg), i, kHubFlag);
+        tile_page[base + ch] = sp;
+      }
+      continue;
+    }
+    uint32_t j = i + 1;
+    while (j < range && !sub_start(o, j, c.bucket)) ++j;
+    tiles[base] = make_uint4(lo, o[j], i, j);
+    tile_page[base] = sp;
+  }
+}
+
+void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                      const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
+                      uint4* tiles, uint32_t* tile_page, cudaStream_t s) {
+  if (!n || !n_blocks) return;
+  uint32_t bucket = 8 * kTileEdgeBudget;  // SERAPH_SUBTILE_EDGES (tools): edges per split
+  if (const char* e = std::getenv("SERAPH_SUBTILE_EDGES")) bucket = uint32_t(std::max(1L, std::atol(e)));
+  const SubCut c{n, cap, n_pages, bucket, offs};
+  sub_tiles_kernel<<<grid_for(uint64_t(n) * n_blocks, 256), 256, 0, s>>>(mode, c, n_blocks, cnt, at,
+                                                                         tiles, tile_page);
+}
+
+// Out-degree histogram (vertices and edges per degree, degrees >= kDegHistCap
+// pooled in the last bucket): block-level shared-memory counts, one global
+// atomic per non-empty bucket per block.
+__global__ void __launch_bounds__(256) degree_hist_kernel(const uint32_t* __restrict__ outdeg,
+                                                          uint32_t n, unsigned long long* hist_v,
+                                                          unsigned long long* hist_e) {
+  __shared__ uint32_t s_v[kDegHistCap + 1];
+  __shared__ unsigned long long s_e[kDegHistCap + 1];
+  for (uint32_t i = threadIdx.x; i <= kDegHistCap; i += blockDim.x) {
+    s_v[i] = 0;
+    s_e[i] = 0;
+  }
+  __syncthreads();
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t d = outdeg[v];
+    const uint32_t b = min(d, kDegHistCap);
+    atomicAdd(s_v + b, 1u);
+    atomicAdd(s_e + b, (unsigned long long)d);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i <= kDegHistCap; i += blockDim.x)
+    if (s_v[i]) {
+      atomicAdd(hist_v + i, (unsigned long long)s_v[i]);
+      atomicAdd(hist_e + i, s_e[i]);
+    }
+}
+
+void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* hist_v,
+                        unsigned long long* hist_e, cudaStream_t s) {
+  if (!n) return;
+  degree_hist_kernel<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(outdeg, n, hist_v, hist_e);
+}
+
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s) {
+  if (!count) return;
+  size_t tb = 0;
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, count, s));
+  void* tmp = nullptr;
+  SR_CUDA(cudaMallocAsync(&tmp, tb, s));
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, count, s));
+  SR_CUDA(cudaFreeAsync(tmp, s));
 }
 
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,

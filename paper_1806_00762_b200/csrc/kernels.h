@@ -63,6 +63,16 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
                       const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
                       const unsigned long long* bp_base, int grid, cudaStream_t s);
+// Tile cut of the source-blocked sub-pages on the device: mode 0 writes the
+// tile count of every (block, destination) to cnt; mode 1 writes the tiles at
+// the exclusive scan `at` of those counts.
+void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                      const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
+                      uint4* tiles, uint32_t* tile_page, cudaStream_t s);
+constexpr uint32_t kDegHistCap = 1024;  // degrees >= cap share the last histogram bucket
+void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* hist_v,
+                        unsigned long long* hist_e, cudaStream_t s);
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s);
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,
                            uint32_t* offs, cudaStream_t s);

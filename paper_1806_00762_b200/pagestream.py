@@ -155,7 +155,12 @@ class CsrGraph:
         return self.out_weights.size > 0
 
     def num_edges(self) -> int:
-        return int(self.out_neighbors.size)
+        # from the offsets: a lean CsrGraph (offsets only) has no adjacency arrays
+        return int(self.out_offsets[-1]) if self.out_offsets.size else int(self.out_neighbors.size)
+
+    def lean(self) -> bool:
+        """Offsets only: the engine derives the push adjacency from the resident pages."""
+        return self.out_neighbors.size == 0 and self.num_edges() > 0
 
     def out_degree(self, u: int) -> int:
         return int(self.out_offsets[u + 1] - self.out_offsets[u])
@@ -745,7 +750,7 @@ def _check_structures(csr: CsrGraph, pages: PageSet, program: VertexProgram) -> 
     # engine.cpp:423-431
     if csr.num_vertices != pages.num_vertices:
         raise ConfigError("csr and page set disagree on vertex count")
-    if program.uses_weights() and (not csr.weighted() or not pages.weighted):
+    if program.uses_weights() and (not (csr.weighted() or csr.lean()) or not pages.weighted):
         raise ConfigError("sssp requires weighted graph structures")
     if program.kind in (AlgoKind.BFS, AlgoKind.SSSP) and program.source >= csr.num_vertices:
         raise ConfigError("source vertex out of range")

@@ -46,5 +46,30 @@ def main(path, full=False):
         print(f"{n:5d} {t:12.1f} us {t / tot * 100:5.1f}% {b / 1e9:9.3f} GB {b / max(t, 1e-9) / 1e3:8.1f} GB/s  {name}")
 
 
+def to_json(path, out):
+    import json
+    import os
+    agg = {}
+    tot = 0.0
+    for r in rows(path):
+        if r["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        t_us = v / 1000.0 if r["Metric Unit"] == "ns" else (v * 1000.0 if r["Metric Unit"] == "ms" else v)
+        name = r["Kernel Name"].split("(")[0].replace("seraph::<unnamed>::", "")
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += t_us
+        tot += t_us
+    ks = [{"kernel": k, "launches": n, "total_us": round(t, 1), "share": round(t / tot, 4)}
+          for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])]
+    with open(out, "w") as fh:
+        json.dump({"source": os.path.basename(path), "total_us": round(tot, 1), "kernels": ks}, fh,
+                  indent=1)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1], "--full" in sys.argv)
+    if "--json" in sys.argv:
+        to_json(sys.argv[1], sys.argv[sys.argv.index("--json") + 1])
+    else:
+        main(sys.argv[1], "--full" in sys.argv)
