@@ -123,6 +123,14 @@ struct PushArgs {
   uint8_t* changed;
   RunCtr* ctr;
   Census* census;
+  // Frontier-queue mode (O(frontier) sparse passes; null stamp = changed
+  // flags + census/compaction): the first improvement of v in this pass
+  // (stamp[v] < epoch) appends v to q_list when it has out-edges and feeds
+  // census->changed / push_count / out_edges; push_count is the queue cursor.
+  uint32_t* stamp;
+  uint32_t epoch;
+  uint32_t* q_list;
+  const uint32_t* outdeg;
 };
 constexpr uint32_t kPushChunk = 256;  // flattened edges per warp task
 

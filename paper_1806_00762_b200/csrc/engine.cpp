@@ -728,6 +728,13 @@ void Engine::alloc_run_state(const sr_run_config& c) {
     }
     list_.reserve(npad);
     pref_.reserve(npad);
+    if (stamp_.n < npad) {  // frontier-queue dedup stamps (epochs never repeat)
+      stamp_.reserve(npad);
+      list2_.reserve(npad);
+      scan_tmp_.reserve(queue_prep_temp_bytes(uint32_t(std::min<size_t>(npad, 0xfffffffeu))));
+      SR_CUDA(cudaMemset(stamp_.p, 0, npad * 4));
+      fq_epoch_ = 0;
+    }
     chunk_start_.reserve(m_ / kPushChunk + 2);
     blk_cnt_.reserve(nb + 1);
     blk_edges_.reserve(nb + 1);
@@ -1235,11 +1242,33 @@ void Engine::build_push_list() {
                  list_.p, pref_.p, chunk_start_.p, cs_);
 }
 
+// Sparse passes keep their frontier as a queue (O(frontier) work, no
+// |V|-sized census or compaction) when the push is asynchronous, single-rank
+// and no weak-predictor bookkeeping needs the changed flags; a queue pass
+// starts from the compacted changed flags after a dense pass.
+bool Engine::queue_mode() const {
+  return !det_ && !comm_ && world_ == 1 && predictor_ != SR_PRED_WEAK &&
+         !std::getenv("SERAPH_NO_FRONTIER_QUEUE");
+}
+
 void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
   (void)cfg;
   const uint64_t n_list = census_h_.p->own_push;
   const uint64_t total = census_h_.p->own_edges;
-  build_push_list();
+  const bool queue = queue_mode();
+  if (queue && fq_ready_) {
+    launch_queue_prep(list_.p, uint32_t(n_list), outdeg_.p, pref_.p, chunk_start_.p, scan_tmp_.p,
+                      scan_tmp_.n, cs_);
+  } else {
+    build_push_list();
+  }
+  if (queue) {
+    SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
+    if (++fq_epoch_ == 0xffffffffu) {  // epochs exhausted: restart the stamps
+      SR_CUDA(cudaMemsetAsync(stamp_.p, 0, stamp_.n * 4, cs_));
+      fq_epoch_ = 1;
+    }
+  }
   RunCtr* slot = alloc_ctr(1);
   if (total > 0) {
     PushArgs a{};
@@ -1256,6 +1285,12 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
     a.changed = changed_.p;
     a.ctr = slot;
     a.census = census_.p;
+    if (queue) {
+      a.stamp = stamp_.p;
+      a.epoch = fq_epoch_;
+      a.q_list = list2_.p;
+      a.outdeg = outdeg_.p;
+    }
     const uint64_t chunks = (total + kPushChunk - 1) / kPushChunk;
     const int grid = int(std::max<uint64_t>(
         1, std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_, (chunks + kWarpsPerBlock - 1) / kWarpsPerBlock)));
@@ -1361,6 +1396,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   census(kPassInit);
   ctr_used_ = 0;
   read_census();
+  fq_ready_ = false;  // the initial frontier is in the changed flags
 
   uint64_t f_count = census_h_.p->changed;
   uint64_t f_out = census_h_.p->out_edges;
@@ -1402,6 +1438,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     // recovery_scan (engine.cpp:179-205): all-pull sweep, gate ignored,
     // scheduled as a baseline pass; changed vertices reset to status 0.
     begin_pass();
+    fq_ready_ = false;
     SR_CUDA(cudaMemsetAsync(changed_.p, 0, npad, cs_));
     PassOut po = det_ ? dense_pass_virtual(cfg, kGateOff, true, pass_index)
                       : dense_pass_wall(cfg, kGateOff, true, pass_index, false);
@@ -1436,8 +1473,16 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     RunStats dummy;
     push_pass(cfg, dummy);
     exchange_round(false);
-    census(kPassSparse);
-    read_census();
+    if (queue_mode()) {  // the push built the next frontier queue and its census
+      read_census();
+      census_h_.p->own_push = census_h_.p->push_count;
+      census_h_.p->own_edges = census_h_.p->out_edges;
+      std::swap(list_, list2_);
+      fq_ready_ = true;
+    } else {
+      census(kPassSparse);
+      read_census();
+    }
     after_census();
     sr_pass_stats st{};
     st.pass_index = pass_index;
@@ -1453,7 +1498,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   // round trip per pass); falls back to one host-driven pass when the device
   // or the configuration does not allow it.
   auto do_sparse_loop = [&]() -> bool {
-    if (det_ || comm_) return false;
+    if (det_ || comm_ || fq_ready_) return false;
     if (coop_ok_ < 0) {
       int v = 0;
       cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev_);
@@ -1537,6 +1582,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   auto do_dense = [&]() {
     // Runner::run_dense (engine.cpp:279-337)
     begin_pass();
+    fq_ready_ = false;  // the frontier after a dense pass is in the changed flags
     sr_pass_stats st{};
     st.pass_index = pass_index;
     st.kind = SR_PASS_DENSE_PULL;

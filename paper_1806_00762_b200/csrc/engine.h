@@ -228,6 +228,13 @@ class Engine {
   DBuf<uint32_t> values_, next_, round_snap_;
   DBuf<uint8_t> changed_, status_, logstate_;
   DBuf<uint32_t> list_, chunk_start_, blk_cnt_;
+  // frontier queue of the sparse passes (queue_mode): next queue, per-vertex
+  // epoch stamps that deduplicate appends, whether list_ holds a queue
+  DBuf<uint32_t> list2_, stamp_;
+  DBuf<uint8_t> scan_tmp_;  // cub scan temporaries of the queue prep (no per-pass malloc)
+  uint32_t fq_epoch_ = 0;
+  bool fq_ready_ = false;
+  bool queue_mode() const;
   DBuf<unsigned long long> pref_, blk_edges_, census_part_;
   DBuf<Census> census_;
   PinBuf<Census> census_h_;

@@ -864,9 +864,13 @@ __global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, flo
 // Body shared by the standalone push launch and the persistent sparse loop:
 // frontier list / prefix / chunk starts are read through L2 (__ldcg) because
 // the persistent loop rewrites them every pass from other SMs.
+struct QueueCtr {
+  unsigned long long changed, out_edges;
+};
+
 template <int A, bool DET>
 __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32_t nw, LaneCtr& c,
-                                          uint32_t& lane_min) {
+                                          uint32_t& lane_min, QueueCtr* qc = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned long long nchunks = (a.total_edges + kPushChunk - 1) / kPushChunk;
   for (unsigned long long ch = gw; ch < nchunks; ch += nw) {
@@ -898,6 +902,8 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
       const unsigned long long my_base_lo = __shfl_sync(kFull, (unsigned)ebase, k);
       const unsigned long long my_base_hi = __shfl_sync(kFull, (unsigned)(ebase >> 32), k);
       const uint32_t my_val = __shfl_sync(kFull, uval, k);
+      uint32_t app_v = 0;
+      bool app = false;
       if (qv) {
         const unsigned long long eidx =
             ((my_base_hi << 32) | my_base_lo) + (unsigned long long)((long long)lane - my_rel);
@@ -915,9 +921,29 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
           const uint32_t old = atomicMin(a.values + v, cand);
           if (cand < old) {
             c.valid += 1;
-            a.changed[v] = 1;
             lane_min = min(lane_min, cand);
+            if (a.stamp) {
+              if (atomicMax(a.stamp + v, a.epoch) < a.epoch) {  // first change this pass
+                const uint32_t d = __ldg(a.outdeg + v);
+                qc->changed += 1;
+                qc->out_edges += d;
+                app = d > 0;
+                app_v = v;
+              }
+            } else {
+              a.changed[v] = 1;
+            }
           }
+        }
+      }
+      if (!DET && a.stamp) {  // warp-aggregated append to the next frontier queue
+        const unsigned m = __ballot_sync(kFull, app);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(&a.census->push_count, (unsigned long long)__popc(m));
+          base = __shfl_sync(kFull, base, leader);
+          if (app) a.q_list[base + __popc(m & lanemask_lt())] = app_v;
         }
       }
       // advance the window start to the entry that contains q0 + 32
@@ -939,12 +965,46 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
 template <int A, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
   __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
+  __shared__ unsigned long long s_q[2][kWarpsPerBlock];
   LaneCtr c;
   c.clear();
+  QueueCtr qc{0, 0};
   uint32_t lane_min = kUnreached;
   push_body<A, DET>(a, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
-                    gridDim.x * kWarpsPerBlock, c, lane_min);
+                    gridDim.x * kWarpsPerBlock, c, lane_min, &qc);
+  if (a.stamp) {  // next-frontier size and out-edge volume: one atomic per block
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned long long ch = warp_sum(qc.changed), oe = warp_sum(qc.out_edges);
+    if (lane == 0) {
+      s_q[0][w] = ch;
+      s_q[1][w] = oe;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      unsigned long long t = 0;
+      for (int k = 0; k < kWarpsPerBlock; ++k) t += s_q[threadIdx.x][k];
+      if (t) atomicAdd(threadIdx.x == 0 ? &a.census->changed : &a.census->out_edges, t);
+    }
+  }
   block_flush(c, a.ctr, lane_min, a.census, s_scratch);
+}
+
+// Frontier queue -> push inputs: exclusive out-degree prefix of the queue
+// and the first queue entry of every kPushChunk-edge chunk.
+__global__ void queue_degrees_kernel(const uint32_t* __restrict__ list, uint32_t q,
+                                     const uint32_t* __restrict__ outdeg, unsigned long long* deg) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= q; i += gridDim.x * blockDim.x)
+    deg[i] = i < q ? outdeg[list[i]] : 0ull;
+}
+
+__global__ void queue_chunks_kernel(const unsigned long long* __restrict__ pref, uint32_t q,
+                                    uint32_t* chunk_start) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < q; i += gridDim.x * blockDim.x) {
+    const unsigned long long lo = pref[i], hi = pref[i + 1];
+    for (unsigned long long ch = (lo + kPushChunk - 1) / kPushChunk;
+         ch < (hi + kPushChunk - 1) / kPushChunk; ++ch)
+      chunk_start[ch] = i;
+  }
 }
 
 __global__ void push_commit_kernel(uint32_t* __restrict__ values, const uint32_t* __restrict__ next,
@@ -1465,6 +1525,22 @@ void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
                        cudaStream_t s) {
   inv_outdeg_kernel<<<grid_for(n, 256), 256, 0, s>>>(out_offsets, n, inv);
+}
+
+size_t queue_prep_temp_bytes(uint32_t max_q) {
+  size_t tb = 0;
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (unsigned long long*)nullptr,
+                                        (unsigned long long*)nullptr, uint64_t(max_q) + 1));
+  return tb;
+}
+
+void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
+                       unsigned long long* pref, uint32_t* chunk_start, void* tmp,
+                       size_t tmp_bytes, cudaStream_t s) {
+  if (!q) return;
+  queue_degrees_kernel<<<grid_for(uint64_t(q) + 1, 256), 256, 0, s>>>(list, q, outdeg, pref);
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pref, pref, uint64_t(q) + 1, s));
+  queue_chunks_kernel<<<grid_for(q, 256), 256, 0, s>>>(pref, q, chunk_start);
 }
 
 void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s) {

@@ -72,6 +72,12 @@ void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint
 constexpr uint32_t kDegHistCap = 1024;  // degrees >= cap share the last histogram bucket
 void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* hist_v,
                         unsigned long long* hist_e, cudaStream_t s);
+// Frontier queue (q entries) -> exclusive out-degree prefix (q+1 entries)
+// and push-chunk starts, the inputs of launch_push.
+size_t queue_prep_temp_bytes(uint32_t max_q);
+void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
+                       unsigned long long* pref, uint32_t* chunk_start, void* tmp,
+                       size_t tmp_bytes, cudaStream_t s);
 void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s);
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,

@@ -46,7 +46,10 @@ def main():
         var, vals = a.sweep.split("=", 1)
         base = None
         for v in vals.split(","):
-            os.environ[var] = v
+            if v == "unset":
+                os.environ.pop(var, None)
+            else:
+                os.environ[var] = v
             r = eng.run(prog, cfg, want_values=a.verify)  # builds per-setting structures
             extra = {}
             if a.verify and kind != ps.AlgoKind.PAGERANK:
