@@ -295,7 +295,6 @@ class Engine {
     DBuf<PageDesc> desc;
     DBuf<float> acc;
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
-    std::string bucket;                      // SERAPH_SUBTILE_EDGES the tiles were cut with
   } sb_;
   bool build_src_blocks(uint64_t blk_verts);
   uint64_t pull_block_verts();
@@ -305,6 +304,9 @@ class Engine {
   bool pull_blocked_pass(int gate, RunCtr* ctr);
   bool last_pass_blocked_ = false;
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
+  void l2_window(const void* base, size_t bytes);
+  int l2_persist_max_ = -1;  // persisting-L2 carve-out (bytes; 0 = unavailable/disabled)
+  bool l2_window_set_ = false;
   int l2_bytes_ = 0;
   // persistent sparse stage buffers
   DBuf<Census> loop_cz_;

@@ -1657,62 +1657,58 @@ __global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages
 
 // ---------------------------------------------------------------------------
 // Device tile cut of the source-blocked sub-pages (replaces the host cut for
-// them: no |V| x blocks offsets round trip).  Destination i of sub-page
-// (b, p) starts a tile when i == 0, i % kTileMaxDests == 0, it or its
-// predecessor is a hub (> kHubChunk in-edges: one tile per kHubChunk chunk),
-// or its first edge crosses a multiple of `bucket` (8 x kTileEdgeBudget); a
-// range tile ends at the next start (<= 128 destinations, < bucket + 1024
-// edges).
+// them: no |V| x blocks offsets round trip).  The cut_tiles rule of the
+// resident pages (engine.cpp) applied per 128-destination window, one thread
+// per window: a hub (> kHubChunk in-edges) becomes one tile per chunk, other
+// destinations are packed greedily into tiles of <= kTileMaxDests
+// destinations and <= kTileEdgeBudget edges.
 // ---------------------------------------------------------------------------
 struct SubCut {
-  uint32_t n, cap, n_pages, bucket;  // bucket: range tiles split where edges cross it
+  uint32_t n, cap, n_pages, wpp;  // wpp: 128-destination windows per page
   const uint32_t* offs;  // [n_blocks][n + n_pages] sub-page local offsets
 };
 
-__device__ __forceinline__ const uint32_t* sub_offs(const SubCut& c, uint32_t b, uint32_t p) {
-  return c.offs + size_t(b) * (size_t(c.n) + c.n_pages) + size_t(p) * c.cap + p;
-}
-
-__device__ __forceinline__ bool sub_start(const uint32_t* o, uint32_t i, uint32_t bucket) {
-  if (i == 0 || i % kTileMaxDests == 0) return true;
-  const uint32_t a = o[i - 1], b = o[i], c = o[i + 1];
-  return (c - b) > kHubChunk || (b - a) > kHubChunk || (a / bucket) != (b / bucket);
-}
-
-// mode 0: tiles per destination into cnt; mode 1: write tiles at scan offsets
+// mode 0: tile count of every window into cnt; mode 1: write the tiles at the
+// exclusive scan `at` of those counts
 __global__ void sub_tiles_kernel(int mode, SubCut c, uint32_t n_blocks, uint32_t* cnt,
                                  const uint32_t* __restrict__ at, uint4* tiles,
                                  uint32_t* tile_page) {
-  const uint64_t total = uint64_t(n_blocks) * c.n;
+  const uint64_t total = uint64_t(n_blocks) * c.n_pages * c.wpp;
   for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t b = uint32_t(k / c.n), v = uint32_t(k % c.n);
-    const uint32_t p = v / c.cap, i = v - p * c.cap;
+    const uint32_t bp = uint32_t(k / c.wpp), w = uint32_t(k % c.wpp);
+    const uint32_t b = bp / c.n_pages, p = bp % c.n_pages;
     const uint32_t range = min(c.cap, c.n - p * c.cap);
-    const uint32_t* o = sub_offs(c, b, p);
-    const bool st = sub_start(o, i, c.bucket);
-    const uint32_t lo = o[i], deg = o[i + 1] - lo;
-    const bool hub = deg > kHubChunk;
-    const uint32_t t = st ? (hub ? (deg + kHubChunk - 1) / kHubChunk : 1u) : 0u;
-    if (mode == 0) {
-      cnt[k] = t;
-      continue;
-    }
-    if (!t) continue;
-    const uint32_t base = at[k];
-    const uint32_t sp = b * c.n_pages + p;
-    if (hub) {
-      for (uint32_t ch = 0; ch < t; ++ch) {
-        const uint32_t e0 = lo + ch * kHubChunk;
-        tiles[base + ch] = make_uint4(e0, min(e0 + kHubChunk, lo + deg), i, kHubFlag);
-        tile_page[base + ch] = sp;
+    const uint32_t lo = w * kTileMaxDests, hi = min(lo + kTileMaxDests, range);
+    const uint32_t* o = c.offs + size_t(b) * (size_t(c.n) + c.n_pages) + size_t(p) * c.cap + p;
+    uint32_t t = mode ? at[k] : 0u;
+    uint32_t i = lo;
+    while (i < hi) {
+      const uint32_t e0 = o[i], deg = o[i + 1] - e0;
+      if (deg > kHubChunk) {
+        for (uint32_t e = e0; e < e0 + deg; e += kHubChunk, ++t)
+          if (mode) {
+            tiles[t] = make_uint4(e, min(e + kHubChunk, e0 + deg), i, kHubFlag);
+            tile_page[t] = bp;
+          }
+        ++i;
+        continue;
       }
-      continue;
+      uint32_t j = i + 1, e = o[j];
+      while (j < hi) {
+        const uint32_t e2 = o[j + 1];
+        if (e2 - e > kHubChunk || e2 - e0 > kTileEdgeBudget) break;
+        e = e2;
+        ++j;
+      }
+      if (mode) {
+        tiles[t] = make_uint4(e0, e, i, j);
+        tile_page[t] = bp;
+      }
+      ++t;
+      i = j;
     }
-    uint32_t j = i + 1;
-    while (j < range && !sub_start(o, j, c.bucket)) ++j;
-    tiles[base] = make_uint4(lo, o[j], i, j);
-    tile_page[base] = sp;
+    if (!mode) cnt[k] = t;
   }
 }
 
@@ -1720,11 +1716,14 @@ void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint
                       const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
                       uint4* tiles, uint32_t* tile_page, cudaStream_t s) {
   if (!n || !n_blocks) return;
-  uint32_t bucket = 8 * kTileEdgeBudget;  // SERAPH_SUBTILE_EDGES (tools): edges per split
-  if (const char* e = std::getenv("SERAPH_SUBTILE_EDGES")) bucket = uint32_t(std::max(1L, std::atol(e)));
-  const SubCut c{n, cap, n_pages, bucket, offs};
-  sub_tiles_kernel<<<grid_for(uint64_t(n) * n_blocks, 256), 256, 0, s>>>(mode, c, n_blocks, cnt, at,
-                                                                         tiles, tile_page);
+  const uint32_t wpp = (cap + kTileMaxDests - 1) / kTileMaxDests;
+  const SubCut c{n, cap, n_pages, wpp, offs};
+  sub_tiles_kernel<<<grid_for(uint64_t(n_blocks) * n_pages * wpp, 256), 256, 0, s>>>(
+      mode, c, n_blocks, cnt, at, tiles, tile_page);
+}
+
+uint64_t sub_tile_windows(uint32_t cap, uint32_t n_pages, uint32_t n_blocks) {
+  return uint64_t(n_blocks) * n_pages * ((cap + kTileMaxDests - 1) / kTileMaxDests);
 }
 
 // Out-degree histogram (vertices and edges per degree, degrees >= kDegHistCap

@@ -63,9 +63,11 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
                       const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
                       const unsigned long long* bp_base, int grid, cudaStream_t s);
-// Tile cut of the source-blocked sub-pages on the device: mode 0 writes the
-// tile count of every (block, destination) to cnt; mode 1 writes the tiles at
-// the exclusive scan `at` of those counts.
+// Tile cut of the source-blocked sub-pages on the device, one 128-destination
+// window per thread: mode 0 writes the tile count of every window to cnt
+// (sub_tile_windows entries, block-major); mode 1 writes the tiles at the
+// exclusive scan `at` of those counts.
+uint64_t sub_tile_windows(uint32_t cap, uint32_t n_pages, uint32_t n_blocks);
 void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                       const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
                       uint4* tiles, uint32_t* tile_page, cudaStream_t s);

@@ -24,21 +24,25 @@ def to_bytes(val, unit):
 
 def report(path, key, tag):
     import ncu_report
-    d = ncu_report.read(path)[0]
-    rd = to_bytes(*d["dram__bytes_read.sum"])
-    wr = to_bytes(*d["dram__bytes_write.sum"])
-    out = {"source": os.path.basename(path), "kernel": d["kernel"],
-           "duration_ms": float(d["gpu__time_duration.sum"][0]) *
-                          {"ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(d["gpu__time_duration.sum"][1], 1.0),
+    ds = ncu_report.read(path)
+    d = ds[0]
+    ms = [float(x["gpu__time_duration.sum"][0]) *
+          {"ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(x["gpu__time_duration.sum"][1], 1.0) for x in ds]
+    rds = [to_bytes(*x["dram__bytes_read.sum"]) for x in ds]
+    wrs = [to_bytes(*x["dram__bytes_write.sum"]) for x in ds]
+    rd, wr = sum(rds) / len(ds), sum(wrs) / len(ds)
+    out = {"source": os.path.basename(path), "kernel": d["kernel"], "launches": len(ds),
+           "duration_ms": sum(ms) / len(ds), "per_launch_ms": ms,
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
-           "metrics": {k: v for k, v in d.items() if k not in ("kernel",)}}
+           "metrics_per_launch": [{k: v for k, v in x.items() if k != "kernel"} for x in ds]}
     os.makedirs(PROF, exist_ok=True)
     with open(os.path.join(PROF, f"{tag}_k1.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     summ_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     summ[key] = {"tag": tag, "kernel": d["kernel"], "duration_ms": out["duration_ms"],
-                 "dram_bytes_per_launch": rd + wr}
+                 "dram_bytes_per_launch": rd + wr,
+                 "note": f"mean over the {len(ds)} captured launches of one converge run ({out['source']})"}
     with open(summ_path, "w") as fh:
         json.dump(summ, fh, indent=1)
     print(json.dumps(summ[key]))

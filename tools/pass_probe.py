@@ -28,9 +28,10 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--sweep", default="", help="VAR=v1,v2,...: time one run per setting")
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--graph", default="device", choices=["device", "host"])
     a = ap.parse_args()
     ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform,
-                            pages=a.pages, seed=0, lean=True, graph="device")
+                            pages=a.pages, seed=0, lean=True, graph=a.graph)
     eng = ps.Engine(0)
     W = bench.workload(ns, eng)
     print(f"# build {W['build_s']:.1f}s n={W['n']} m={W['m']} ({W['graph']})", flush=True)
