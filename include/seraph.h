@@ -275,6 +275,11 @@ int sr_build_graph(sr_ctx* ctx, uint32_t num_vertices, uint64_t num_edges, const
                    int flags);
 /* Generate + build entirely on the device (no host edge list). */
 int sr_generate_graph(sr_ctx* ctx, const sr_graph_spec* spec, int flags);
+/* load_binary (ingest.cpp:176-218): an SRPH edge-list file (header "SRPH",
+ * version 1, flags bit0 = weighted, u64 |V|, u64 |E|; records u32 src, dst
+ * [, w]) streamed onto the device and built as sr_build_graph does.  Errors:
+ * SR_E_FORMAT for the header/size checks and invalid edges, as the reference. */
+int sr_load_srph(sr_ctx* ctx, const char* path, uint32_t page_vertex_capacity, int flags);
 int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out);
 /* Copy the loaded graph back in the reference layouts (any pointer may be
  * NULL): CSR out_offsets (|V|+1) / out_neighbors / out_weights (|E|), global

@@ -171,6 +171,7 @@ def load_reference():
         "ref_generate_rmat": (C.c_int, [C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP]),
         "ref_assign_weights": (C.c_int, [_U32, _U64, _VP, _VP, _U64, _U32, _U32, _VP]),
         "ref_build_csr": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
+        "ref_save_binary": (C.c_int, [_U32, _U64, _VP, _VP, _VP, C.c_char_p]),
         "ref_build_csc_pages": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _U32, _VP, _VP, _VP]),
         "ref_reference_solve": (C.c_int, [_U32, _U64, _VP, _VP, _VP, C.c_int, _U32, _VP]),
         "ref_prepare": (_VP, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, _U32]),

@@ -77,6 +77,12 @@ int ref_assign_weights(uint32_t n, uint64_t m, const uint32_t* src, const uint32
   });
 }
 
+// save_binary (ingest.cpp:153-174): the reference's SRPH writer
+int ref_save_binary(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                    const uint32_t* w, const char* path) {
+  return guard([&] { save_binary(make_edges(n, m, src, dst, w), path); });
+}
+
 // build_csr (graph.cpp:30-48)
 int ref_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                   const uint32_t* w, uint64_t* off, uint32_t* nbr, uint32_t* ow) {

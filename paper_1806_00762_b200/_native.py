@@ -229,6 +229,7 @@ SIGNATURES = {
     "sr_build_graph": (C.c_int, [_VP, _U32, _U64, _VP, _VP, _VP, _U32, C.c_int]),
     "sr_generate_graph": (C.c_int, [_VP, C.POINTER(GraphSpec), C.c_int]),
     "sr_graph_info_get": (C.c_int, [_VP, C.POINTER(GraphInfo)]),
+    "sr_load_srph": (C.c_int, [_VP, C.c_char_p, _U32, C.c_int]),
     "sr_export_graph": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "sr_rmat_generate_device": (C.c_int, [C.c_int, C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP,
                                           _U64, _U32, _U32, _VP]),

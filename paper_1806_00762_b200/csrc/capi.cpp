@@ -140,6 +140,11 @@ int sr_generate_graph(sr_ctx* ctx, const sr_graph_spec* spec, int flags) {
   return guard(ctx, [&] { ctx->eng->generate_graph(*spec, flags & SR_BUILD_CSR_EDGES); });
 }
 
+int sr_load_srph(sr_ctx* ctx, const char* path, uint32_t cap, int flags) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->load_srph(path, cap, flags & SR_BUILD_CSR_EDGES); });
+}
+
 int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out) {
   if (!ctx || !out) return SR_E_CONFIG;
   ctx->eng->graph_info(*out);

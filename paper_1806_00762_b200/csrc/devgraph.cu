@@ -98,6 +98,28 @@ __global__ void check_ids_kernel(uint32_t n, uint64_t m, const uint32_t* __restr
   if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(bad, 1u);
 }
 
+// SRPH records (ingest.cpp:153-218): little-endian u32 src, dst[, w] per edge
+__global__ void deinterleave_kernel(uint64_t m, const uint32_t* __restrict__ rec, int weighted,
+                                    uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                    uint32_t* __restrict__ w) {
+  const uint32_t stride = weighted ? 3 : 2;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t* r = rec + i * stride;
+    src[i] = r[0];
+    dst[i] = r[1];
+    if (weighted) w[i] = r[2];
+  }
+}
+
+__global__ void check_weights_kernel(uint64_t m, const uint32_t* __restrict__ w, unsigned* bad) {
+  bool any = false;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    any |= w[i] < 1u;
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(bad, 1u);
+}
+
 __global__ void histogram_kernel(uint64_t len, const uint32_t* __restrict__ key, uint32_t* cnt) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -210,6 +232,24 @@ bool dg_ids_valid(uint32_t n, uint64_t m, const uint32_t* a, const uint32_t* b, 
   Tmp<unsigned> bad(1, s);
   SR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
   check_ids_kernel<<<grid_of(m), kThreads, 0, s>>>(n, m, a, b, bad.p);
+  unsigned h = 0;
+  SR_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  SR_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
+void dg_deinterleave(uint64_t m, const uint32_t* records, bool weighted, uint32_t* src,
+                     uint32_t* dst, uint32_t* w, cudaStream_t s) {
+  if (!m) return;
+  deinterleave_kernel<<<grid_of(m), kThreads, 0, s>>>(m, records, weighted ? 1 : 0, src, dst, w);
+  SR_CUDA(cudaGetLastError());
+}
+
+bool dg_weights_valid(uint64_t m, const uint32_t* w, cudaStream_t s) {
+  if (!m || !w) return true;
+  Tmp<unsigned> bad(1, s);
+  SR_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  check_weights_kernel<<<grid_of(m), kThreads, 0, s>>>(m, w, bad.p);
   unsigned h = 0;
   SR_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
   SR_CUDA(cudaStreamSynchronize(s));

@@ -25,6 +25,11 @@ bool dg_ids_valid(uint32_t n, uint64_t m, const uint32_t* a, const uint32_t* b, 
 void dg_stable_adjacency(uint32_t n, uint64_t m, const uint32_t* key, const uint32_t* other,
                          const uint32_t* w, unsigned long long* out_off, uint32_t* out_other,
                          uint32_t* out_w, cudaStream_t s);
+// SRPH edge records (src, dst[, w] u32 each) -> separate arrays
+void dg_deinterleave(uint64_t m, const uint32_t* records, bool weighted, uint32_t* src,
+                     uint32_t* dst, uint32_t* w, cudaStream_t s);
+// true when every weight is >= 1 (EdgeList::validate, graph.cpp:9-22; synchronises s)
+bool dg_weights_valid(uint64_t m, const uint32_t* w, cudaStream_t s);
 // page-local u32 offsets of pages of `cap` vertices (layout of sr_page_offsets)
 void dg_page_offsets(uint32_t n, uint32_t cap, const unsigned long long* off, uint32_t* local,
                      cudaStream_t s);

@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -281,6 +284,89 @@ void Engine::generate_graph(const sr_graph_spec& g, bool csr_edges) {
   d0.release();
   w0.release();
   build_graph_dev(n, 2 * m0, s1, d1, w1, weighted, g.page_vertex_capacity, csr_edges);
+}
+
+// load_binary (ingest.cpp:176-218) straight into the device build: the file's
+// edge records stream through two pinned staging buffers onto the GPU (copy
+// stream, double-buffered against the reads), are split into src/dst/w and
+// validated there.  Same checks and exception classes as the reference:
+// FormatError for a bad header/size, FormatError wrapping the edge-list
+// validation (ids < num_vertices, weights >= 1).
+void Engine::load_srph(const char* path, uint32_t cap, bool csr_edges) {
+  SR_CUDA(cudaSetDevice(dev_));
+  const std::string p = path ? path : "";
+  const int fd = ::open(p.c_str(), O_RDONLY);
+  if (fd < 0) throw EngineError(SR_E_FORMAT, "cannot open '" + p + "'");
+  struct FdGuard {
+    int fd;
+    ~FdGuard() { ::close(fd); }
+  } guard{fd};
+  struct stat stt {};
+  if (fstat(fd, &stt) != 0) throw EngineError(SR_E_FORMAT, "cannot stat '" + p + "'");
+  const uint64_t size = uint64_t(stt.st_size);
+  if (size < 24)
+    throw EngineError(SR_E_FORMAT, "'" + p + "': header needs 24 bytes, file has " +
+                                       std::to_string(size));
+  unsigned char hdr[24];
+  if (::pread(fd, hdr, 24, 0) != 24) throw EngineError(SR_E_FORMAT, "'" + p + "': short read");
+  if (std::memcmp(hdr, "SRPH", 4) != 0) throw EngineError(SR_E_FORMAT, "'" + p + "': bad magic");
+  if (hdr[4] != 1)
+    throw EngineError(SR_E_FORMAT, "'" + p + "': unsupported version " + std::to_string(hdr[4]));
+  const bool weighted = (hdr[5] & 1) != 0;
+  uint64_t nv = 0, m = 0;
+  for (int k = 7; k >= 0; --k) {
+    nv = (nv << 8) | hdr[8 + k];
+    m = (m << 8) | hdr[16 + k];
+  }
+  if (nv > 0xffffffffull)
+    throw EngineError(SR_E_FORMAT, "'" + p + "': vertex count exceeds 32-bit id range");
+  const uint64_t rec = weighted ? 12 : 8;
+  if (m > (size - 24) / rec || size != 24 + m * rec)
+    throw EngineError(SR_E_FORMAT, "'" + p + "': expected " + std::to_string(24 + m * rec) +
+                                       " bytes, file has " + std::to_string(size));
+  const uint64_t bytes = m * rec;
+  DBuf<uint32_t> raw;
+  raw.reserve(std::max<uint64_t>(bytes / 4, 1));
+  constexpr uint64_t kStage = 64ull << 20;
+  PinBuf<uint8_t> stage[2];
+  cudaEvent_t done[2];
+  for (int b = 0; b < 2; ++b) {
+    stage[b].reserve(kStage);
+    SR_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+  }
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } evg{done};
+  int k = 0;
+  for (uint64_t at = 0; at < bytes; at += kStage, k ^= 1) {
+    const uint64_t len = std::min(kStage, bytes - at);
+    SR_CUDA(cudaEventSynchronize(done[k]));  // the buffer's previous copy has landed
+    uint64_t got = 0;
+    while (got < len) {
+      const ssize_t r = ::pread(fd, stage[k].p + got, len - got, off_t(24 + at + got));
+      if (r <= 0) throw EngineError(SR_E_FORMAT, "'" + p + "': short read");
+      got += uint64_t(r);
+    }
+    SR_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(raw.p) + at, stage[k].p, len,
+                            cudaMemcpyHostToDevice, xs_));
+    SR_CUDA(cudaEventRecord(done[k], xs_));
+  }
+  SR_CUDA(cudaStreamSynchronize(xs_));
+  DBuf<uint32_t> src, dst, w;
+  src.reserve(std::max<uint64_t>(m, 1));
+  dst.reserve(std::max<uint64_t>(m, 1));
+  if (weighted) w.reserve(std::max<uint64_t>(m, 1));
+  dg_deinterleave(m, raw.p, weighted, src.p, dst.p, weighted ? w.p : nullptr, cs_);
+  raw.release();
+  if (!dg_ids_valid(uint32_t(nv), m, src.p, dst.p, cs_))
+    throw EngineError(SR_E_FORMAT, "'" + p + "': edge has id >= num_vertices " + std::to_string(nv));
+  if (weighted && !dg_weights_valid(m, w.p, cs_))
+    throw EngineError(SR_E_FORMAT, "'" + p + "': edge has weight < 1");
+  build_graph_dev(uint32_t(nv), m, src, dst, w, weighted, cap, csr_edges);
 }
 
 void Engine::graph_info(sr_graph_info& gi) const {

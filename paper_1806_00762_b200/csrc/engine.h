@@ -130,6 +130,7 @@ class Engine {
   void build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                    const uint32_t* w, uint32_t cap, bool csr_edges);
   void generate_graph(const sr_graph_spec& spec, bool csr_edges);
+  void load_srph(const char* path, uint32_t cap, bool csr_edges);
   void graph_info(sr_graph_info& gi) const;
   void export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w, uint64_t* in_off,
                     uint32_t* in_src, uint32_t* in_w);

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -630,6 +631,12 @@ class Engine:
         N.check(N.lib.sr_generate_graph(self._h, C.byref(spec),
                                         N.BUILD_CSR_EDGES if csr_edges else 0), self._h)
         self.num_vertices = n
+
+    def load_srph(self, path: str, page_vertex_capacity: int, csr_edges: bool = True) -> None:
+        """load_binary (ingest.cpp:176-218) + build + load, on the device."""
+        N.check(N.lib.sr_load_srph(self._h, os.fsencode(path), int(page_vertex_capacity),
+                                   N.BUILD_CSR_EDGES if csr_edges else 0), self._h)
+        self.num_vertices = self.graph_info()["num_vertices"]
 
     def graph_info(self) -> dict:
         gi = N.GraphInfo()

@@ -637,3 +637,52 @@ def test_device_generate_graph(sym):
         r = eng.run(program_for(kind, 0, el), cfg_of(clock=ps.ClockMode.WALL))
         assert np.array_equal(r.values, oracle_values(el, kind, 0))
         assert eng.verify_fixpoint(kind, r.values) == 0
+
+
+def _write_srph(path, n, src, dst, w=None):
+    """SRPH bytes (ingest.cpp:153-174 layout) without validation: for corrupt files."""
+    rec = np.stack([src, dst] + ([w] if w is not None else []), axis=1).astype("<u4")
+    hdr = b"SRPH" + bytes([1, 1 if w is not None else 0, 0, 0]) + \
+        np.array([n, src.size], "<u8").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(hdr + rec.tobytes())
+
+
+def test_srph_loader_reference_files(tmp_path):
+    """sr_load_srph reads files written by the reference's own save_binary
+    (oracle/_ref) into the same graph the host builders make; header, size
+    and edge errors raise FormatError like load_binary (ingest.cpp:176-218)."""
+    ref = O.load_reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    import ctypes
+    n = 1 << 12
+    src, dst = O.generate_rmat(12, 8, seed=7)
+    w = O.assign_weights(src.size, 3, 1, 64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    with ps.Engine(0) as eng:
+        for weighted in (True, False):
+            path = str(tmp_path / f"g{int(weighted)}.srph")
+            assert ref.ref_save_binary(n, src.size, ptr(src), ptr(dst), ptr(w) if weighted else None,
+                                       path.encode()) == 0
+            el = ps.EdgeList(n, src, dst, w if weighted else np.zeros(0, np.uint32))
+            eng.load_srph(path, 300)
+            _assert_same_graph(eng, el, 300)
+            r = eng.run(ps.make_bfs(0, n), cfg_of(clock=ps.ClockMode.WALL))
+            assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.BFS, 0))
+        good = str(tmp_path / "g1.srph")
+        data = open(good, "rb").read()
+        bad = str(tmp_path / "bad.srph")
+        for blob in (data[:20], b"XRPH" + data[4:], data[:4] + b"\x02" + data[5:], data[:-4]):
+            open(bad, "wb").write(blob)
+            with pytest.raises(ps.FormatError):
+                eng.load_srph(bad, 300)
+        _write_srph(bad, 4, np.array([0, 9], np.uint32), np.array([1, 2], np.uint32))
+        with pytest.raises(ps.FormatError):
+            eng.load_srph(bad, 2)
+        _write_srph(bad, 4, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
+                    np.array([3, 0], np.uint32))
+        with pytest.raises(ps.FormatError):
+            eng.load_srph(bad, 2)
+        with pytest.raises(ps.FormatError):
+            eng.load_srph(str(tmp_path / "missing.srph"), 2)
