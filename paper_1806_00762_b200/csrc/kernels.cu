@@ -103,15 +103,23 @@ struct ActEntry {
   uint32_t cur;     // destination value when the tile was gated
 };
 
+// Per-lane counters: 32-bit where a lane's share is bounded by the edges it
+// processes itself (registers are the K1 bottleneck), 64-bit for the edges
+// of attempted destinations (a lane counts whole hub in-degrees).
 struct LaneCtr {
-  unsigned long long attempts, valid, skipped, edges, gathers;
-  __device__ void clear() { attempts = valid = skipped = edges = gathers = 0; }
+  uint32_t attempts, valid, skipped, gathers;
+  unsigned long long edges;
+  __device__ void clear() {
+    attempts = valid = skipped = gathers = 0;
+    edges = 0;
+  }
 };
 
 __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
-  unsigned long long at = warp_sum(c.attempts), va = warp_sum(c.valid),
-                     sk = warp_sum(c.skipped), ed = warp_sum(c.edges),
-                     ga = warp_sum(c.gathers);
+  unsigned long long at = warp_sum<unsigned long long>(c.attempts),
+                     va = warp_sum<unsigned long long>(c.valid),
+                     sk = warp_sum<unsigned long long>(c.skipped), ed = warp_sum(c.edges),
+                     ga = warp_sum<unsigned long long>(c.gathers);
   if (lane == 0 && dst) {
     if (at) atomicAdd(&dst->attempts, at);
     if (va) atomicAdd(&dst->valid, va);
@@ -143,9 +151,10 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
   uint32_t* mins = scratch + 2 * kCtr * kWarpsPerBlock;
-  const unsigned long long v[kCtr] = {warp_sum(c.attempts), warp_sum(c.valid),
-                                      warp_sum(c.skipped), warp_sum(c.edges),
-                                      warp_sum(c.gathers)};
+  const unsigned long long v[kCtr] = {warp_sum<unsigned long long>(c.attempts),
+                                      warp_sum<unsigned long long>(c.valid),
+                                      warp_sum<unsigned long long>(c.skipped), warp_sum(c.edges),
+                                      warp_sum<unsigned long long>(c.gathers)};
   lane_min = warp_min(lane_min);
   __syncthreads();  // every warp is done with its tile scratch
   if (lane == 0) {
@@ -346,23 +355,22 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             if (pref_of[mid] <= q) lo = mid;
             else hi = mid - 1;
           }
+          // the run's entries: ent0 plus one step at every set bit of adv
+          // (entries hold >= 1 edge), so entry(t) = ent0 + popc(adv & (2<<t)-1)
+          const uint32_t ent0 = lo;
           uint32_t ent = lo;
           uint32_t nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
           bool att_e = (loc_of[ent] >> 31) != 0;
-          uint32_t cur_e = (A == kSssp) ? s_cur[warp][ent] : 0u;
-          uint32_t eid[kLaneEdges], ecur[kLaneEdges];
-          unsigned live = 0;
+          unsigned live = 0, adv = 0;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t) {
             const uint32_t pp = pos0 + t;
-            if (pp >= nxt && pp < span) {  // entries hold >= 1 edge: one step
+            if (pp >= nxt && pp < span) {
               ++ent;
+              adv |= 1u << t;
               nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
               att_e = (loc_of[ent] >> 31) != 0;
-              if (A == kSssp) cur_e = s_cur[warp][ent];
             }
-            eid[t] = ent;
-            ecur[t] = cur_e;
             if (pp >= lo_pos && pp < span && att_e) live |= 1u << t;
           }
           if (live) {
@@ -379,9 +387,12 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             if (A == kSssp) {
               // values are >= 0, so an edge with w >= the destination's value
               // cannot improve it: no gather (the wavefront-bound part of K1)
+              uint32_t et = ent0, cur_t = s_cur[warp][ent0];
 #pragma unroll
-              for (int t = 0; t < kLaneEdges; ++t)
-                if (wv[t] >= ecur[t]) live &= ~(1u << t);
+              for (int t = 0; t < kLaneEdges; ++t) {
+                if (adv >> t & 1u) cur_t = s_cur[warp][++et];
+                if (wv[t] >= cur_t) live &= ~(1u << t);
+              }
             }
             uint32_t sv[kLaneEdges];
 #pragma unroll
@@ -390,13 +401,14 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
                                               : gather_rw(a.values + sv_idx[t]))
                                        : kUnreached;
             c.gathers += __popc(live);
-            uint32_t run_ent = 0xffffffffu, run_best = kUnreached;
+            uint32_t run_ent = 0xffffffffu, run_best = kUnreached, et = ent0;
 #pragma unroll
             for (int t = 0; t < kLaneEdges; ++t) {
+              et += adv >> t & 1u;
               if (!(live >> t & 1u)) continue;
-              if (eid[t] != run_ent) {
+              if (et != run_ent) {
                 if (run_ent != 0xffffffffu) atomicMin(best_of + run_ent, run_best);
-                run_ent = eid[t];
+                run_ent = et;
                 run_best = kUnreached;
               }
               run_best = min(run_best, combine<A>(sv[t], wv[t]));
@@ -776,7 +788,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           }
           uint32_t ent = lo;
           uint32_t nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
-          uint32_t eid[kLaneEdges];
+          uint32_t eid[kLaneEdges];  // (K8 has registers to spare: measured faster than K1's adv mask)
           unsigned live = 0;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t) {
