@@ -1477,12 +1477,20 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   k_bfs_ = 0;
   s_cc_ = 0;
   l_sssp_ = 0;
-  if (algo_ == SR_ALGO_CC) SR_CUDA(cudaMemsetAsync(changed_.p, 1, n_, cs_));
-  else SR_CUDA(cudaMemsetAsync(changed_.p + source_, 1, 1, cs_));
-  census(kPassInit);
   ctr_used_ = 0;
-  read_census();
-  fq_ready_ = false;  // the initial frontier is in the changed flags
+  if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_) {
+    // the initial frontier {source} directly as a queue
+    SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
+    launch_seed_queue(source_, outdeg_.p, list_.p, census_.p, cs_);
+    read_census();
+    fq_ready_ = true;
+  } else {
+    if (algo_ == SR_ALGO_CC) SR_CUDA(cudaMemsetAsync(changed_.p, 1, n_, cs_));
+    else SR_CUDA(cudaMemsetAsync(changed_.p + source_, 1, 1, cs_));
+    census(kPassInit);
+    read_census();
+    fq_ready_ = false;  // the initial frontier is in the changed flags
+  }
 
   uint64_t f_count = census_h_.p->changed;
   uint64_t f_out = census_h_.p->out_edges;

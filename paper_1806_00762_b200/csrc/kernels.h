@@ -76,6 +76,8 @@ void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* 
                         unsigned long long* hist_e, cudaStream_t s);
 // Frontier queue (q entries) -> exclusive out-degree prefix (q+1 entries)
 // and push-chunk starts, the inputs of launch_push.
+void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, Census* cz,
+                       cudaStream_t s);
 size_t queue_prep_temp_bytes(uint32_t max_q);
 void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
                        unsigned long long* pref, uint32_t* chunk_start, void* tmp,
