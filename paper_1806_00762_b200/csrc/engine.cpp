@@ -932,7 +932,6 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
     if (tr) SR_CUDA(cudaEventRecord(tr->b, cs_));
-    ++launches_;
     seg = Segments{};
     seg_pages.clear();
   };
@@ -1278,7 +1277,6 @@ PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool reco
     SR_CUDA(cudaMemsetAsync(slot, 0, sizeof(RunCtr), cs_));
     launch_pages({page}, gate, true, slot, nullptr, false, false);
     launch_commit(values_.p, next_.p, pages_[page].vb, pages_[page].ve, cs_);
-    ++launches_;
     SR_CUDA(cudaMemcpyAsync(ctr_h_.p, slot, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
     SR_CUDA(cudaStreamSynchronize(cs_));
     RunStats st;
@@ -1382,7 +1380,6 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
         1, std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_, (chunks + kWarpsPerBlock - 1) / kWarpsPerBlock)));
     launch_push(algo_, det_, a, grid, cs_);
     SR_CUDA(cudaGetLastError());
-    ++launches_;
     if (det_) launch_push_commit(values_.p, next_.p, changed_.p, n_, slot, census_.p, cs_);
   }
   (void)st;
@@ -1434,7 +1431,6 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   trace.clear();
   std::memset(&m, 0, sizeof(m));
   passes.clear();
-  launches_ = 0;
   h2d_bytes_ = 0;
   first_touch_done_ = false;
   vwin_.reset(cfg.window_capacity);
@@ -1443,9 +1439,10 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   vmodel_.edges_per_unit_per_worker = cfg.edges_per_time_unit_per_worker;
   vmodel_.workers = cfg.worker_count;
   alloc_run_state(cfg);
+  const uint64_t launches0 = kernel_launch_count();
   if (cfg.algo == SR_ALGO_PAGERANK) run_pagerank(cfg, ranks_out, m, passes);
   else run_traversal(cfg, values_out, m, passes);
-  m.kernel_launches = launches_;
+  m.kernel_launches = kernel_launch_count() - launches0;  // every kernel of the run
   m.h2d_bytes = h2d_bytes_;
   m.gathers = gathers_total_;
   finish_wall_trace();
@@ -1640,7 +1637,6 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     L.result = loop_res_.p;
     const int grid = sm_count_ * sparse_loop_blocks(algo_);
     SR_CUDA(launch_sparse_loop(algo_, L, grid, cs_));
-    launches_ += 1;
     SR_CUDA(cudaMemcpyAsync(loop_res_h_.p, loop_res_.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, cs_));
     SR_CUDA(cudaMemcpyAsync(loop_cz_h_.p, loop_cz_.p, kMaxLoop * sizeof(Census), cudaMemcpyDeviceToHost, cs_));
     SR_CUDA(cudaMemcpyAsync(loop_ctr_h_.p, loop_ctr_.p, kMaxLoop * sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
@@ -2009,7 +2005,6 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
-    ++launches_;
   }
   l2_window(nullptr, 0);
   return true;
@@ -2066,7 +2061,6 @@ void Engine::pr_blocked_pass(float base, float damp) {
     launch_pr_pull(a, std::max(grid, 1), cs_);
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
-    ++launches_;
   }
   launch_pr_block_finalize(n_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p, base, damp, cs_);
 }

@@ -248,7 +248,6 @@ class Engine {
   unsigned* next_work_counter();
   DBuf<float> rank_a_, rank_b_, contrib_a_, contrib_b_, inv_outdeg_;
   uint32_t run_id_ = 0;
-  uint64_t launches_ = 0;
   uint64_t h2d_bytes_ = 0;
   uint64_t gathers_total_ = 0;
   int blocks_per_sm_ = 4;

@@ -25,6 +25,12 @@
 
 namespace seraph {
 
+// Kernels launched by this thread (sr_metrics.kernel_launches: every launch
+// wrapper below counts its own launches).
+thread_local uint64_t t_launches = 0;
+inline void note_launch(uint64_t k = 1) { t_launches += k; }
+uint64_t kernel_launch_count() { return t_launches; }
+
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -1462,11 +1468,13 @@ __global__ void set_page_desc_kernel(PageDesc* d, uint32_t page, const uint32_t*
 void launch_mark_changed(uint32_t n, const uint32_t* values, const uint32_t* snap,
                          uint8_t* changed, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   mark_changed_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, values, snap, changed);
 }
 
 void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, const uint32_t* src,
                           const uint32_t* w, cudaStream_t s) {
+  note_launch();
   set_page_desc_kernel<<<1, 1, 0, s>>>(d, page, offs, src, w);
 }
 
@@ -1475,6 +1483,7 @@ void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, cons
 // ---------------------------------------------------------------------------
 template <int A, int G, bool D>
 static void pull_dispatch3(const PullArgs& a, int grid, cudaStream_t s) {
+  note_launch();
   pull_relax_kernel<A, G, D><<<grid, kBlockThreads, 0, s>>>(a);
 }
 template <int A, int G>
@@ -1515,10 +1524,12 @@ int pull_blocks_per_sm(int algo, int gate, bool det) {
 void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t hi,
                    cudaStream_t s) {
   if (hi <= lo) return;
+  note_launch();
   commit_kernel<<<grid_for(hi - lo, 256), 256, 0, s>>>(values, next, lo, hi);
 }
 
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s) {
+  note_launch();
   pr_pull_kernel<<<grid, kBlockThreads, 0, s>>>(a);
 }
 
@@ -1526,6 +1537,7 @@ void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* 
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
                             float base, float damp, cudaStream_t s) {
   if (!n_hubs) return;
+  note_launch();
   pr_hub_finalize_kernel<<<(n_hubs + 255) / 256, 256, 0, s>>>(hub_vertex, n_hubs, hub_sum,
                                                               rank_out, contrib_out, inv_outdeg,
                                                               base, damp);
@@ -1533,11 +1545,13 @@ void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* 
 
 void launch_pr_init(float* rank, float* contrib, const float* inv_outdeg, uint32_t n, float init,
                     cudaStream_t s) {
+  note_launch();
   pr_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, contrib, inv_outdeg, n, init);
 }
 
 void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float* inv,
                        cudaStream_t s) {
+  note_launch();
   inv_outdeg_kernel<<<grid_for(n, 256), 256, 0, s>>>(out_offsets, n, inv);
 }
 
@@ -1563,6 +1577,7 @@ __global__ void seed_queue_kernel(uint32_t source, const uint32_t* __restrict__ 
 
 void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, Census* cz,
                        cudaStream_t s) {
+  note_launch();
   seed_queue_kernel<<<1, 1, 0, s>>>(source, outdeg, list, cz);
 }
 
@@ -1570,12 +1585,16 @@ void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
                        unsigned long long* pref, uint32_t* chunk_start, void* tmp,
                        size_t tmp_bytes, cudaStream_t s) {
   if (!q) return;
+  note_launch();
   queue_degrees_kernel<<<grid_for(uint64_t(q) + 1, 256), 256, 0, s>>>(list, q, outdeg, pref);
   SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pref, pref, uint64_t(q) + 1, s));
+  note_launch(2);  // cub: tile-state init + scan
+  note_launch();
   queue_chunks_kernel<<<grid_for(q, 256), 256, 0, s>>>(pref, q, chunk_start);
 }
 
 void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s) {
+  note_launch();
   switch (algo) {
     case kBfs:
       if (det) push_relax_kernel<kBfs, true><<<grid, kBlockThreads, 0, s>>>(a);
@@ -1608,11 +1627,13 @@ cudaError_t launch_sparse_loop(int algo, const SparseLoopArgs& a, int grid, cuda
   const void* fn = algo == kSssp ? (const void*)sparse_loop_kernel<kSssp>
                    : algo == kCc ? (const void*)sparse_loop_kernel<kCc>
                                  : (const void*)sparse_loop_kernel<kBfs>;
+  note_launch();
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, 0, s);
 }
 
 void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
                         uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s) {
+  note_launch();
   push_commit_kernel<<<grid_for(n, 256), 256, 0, s>>>(values, next, changed, n, ctr, c);
 }
 
@@ -1625,6 +1646,7 @@ void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t*
   (void)part;
   const uint32_t cap = 148u * 8u;  // measured: 592 / 1184 / 2368 / nb blocks -> 1184 best
   const int grid = int(nb < cap ? nb : cap);
+  note_launch();
   census_kernel<<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind, own_lo,
                                      own_hi, blk_cnt, blk_edges, c);
 }
@@ -1632,6 +1654,7 @@ void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t*
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
                         cudaStream_t s) {
   if (!nblocks) return;
+  note_launch();
   scan_blocks_kernel<<<1, 1024, 0, s>>>(nblocks, blk_cnt, blk_edges);
 }
 
@@ -1641,6 +1664,7 @@ void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* chang
                     uint32_t* chunk_start, cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
   if (!nb) return;
+  note_launch();
   compact_kernel<<<nb, 256, 0, s>>>(n, own_lo, own_hi, changed, out_offsets, blk_off, blk_eoff,
                                     list, pref, chunk_start);
 }
@@ -1652,6 +1676,7 @@ void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const 
   if (tile_hi <= tile_lo) return;
   const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (uint32_t(grid) > need) grid = int(need);
+  note_launch();
   csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, tile_lo, tile_hi,
                                                        out_off, cursor, out_nbr, out_w);
 }
@@ -1664,6 +1689,7 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
   if (tile_hi <= tile_lo) return;
   const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (uint32_t(grid) > need) grid = int(need);
+  note_launch();
   src_block_kernel<<<grid, kBlockThreads, 0, s>>>(mode, tiles, tile_page, pages, tile_lo, tile_hi,
                                                   n, blk_verts, n_pages, cnt, goff, out_src, out_w,
                                                   bp_base);
@@ -1751,6 +1777,7 @@ void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint
   if (!n || !n_blocks) return;
   const uint32_t wpp = (cap + kTileMaxDests - 1) / kTileMaxDests;
   const SubCut c{n, cap, n_pages, wpp, offs};
+  note_launch();
   sub_tiles_kernel<<<grid_for(uint64_t(n_blocks) * n_pages * wpp, 256), 256, 0, s>>>(
       mode, c, n_blocks, cnt, at, tiles, tile_page);
 }
@@ -1789,6 +1816,7 @@ __global__ void __launch_bounds__(256) degree_hist_kernel(const uint32_t* __rest
 void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* hist_v,
                         unsigned long long* hist_e, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   degree_hist_kernel<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(outdeg, n, hist_v, hist_e);
 }
 
@@ -1799,12 +1827,14 @@ void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, 
   void* tmp = nullptr;
   SR_CUDA(cudaMallocAsync(&tmp, tb, s));
   SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, count, s));
+  note_launch(2);
   SR_CUDA(cudaFreeAsync(tmp, s));
 }
 
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,
                            uint32_t* offs, cudaStream_t s) {
+  note_launch();
   src_block_offs_kernel<<<148 * 8, 256, 0, s>>>(n, cap, n_pages, n_blocks, goff, bp_edges, offs);
 }
 
@@ -1812,28 +1842,33 @@ void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const 
                            uint32_t n_pages, uint32_t n_blocks, uint32_t n,
                            unsigned long long* bp_edges, cudaStream_t s) {
   if (!n_pages || !n_blocks) return;
+  note_launch();
   src_block_scan_kernel<<<n_pages * n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges);
 }
 
 void launch_pr_block_finalize(uint32_t n, float* acc, float* rank_out, float* contrib_out,
                               const float* inv_outdeg, float base, float damp, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   pr_block_finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, acc, rank_out, contrib_out,
                                                             inv_outdeg, base, damp);
 }
 
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   outdeg_kernel<<<grid_for(n, 256), 256, 0, s>>>(off, n, deg);
 }
 
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   init_values_kernel<<<grid_for(n, 256), 256, 0, s>>>(algo, source, n, values);
 }
 
 void launch_init_hub_stamp(uint32_t* stamp, uint32_t n, cudaStream_t s) {
   if (!n) return;
+  note_launch();
   fill_u32_kernel<<<grid_for(n, 256), 256, 0, s>>>(stamp, n, 0u);
 }
 
@@ -1842,9 +1877,11 @@ void launch_verify(int algo, uint32_t n, const unsigned long long* out_offsets,
                    unsigned long long* violations, cudaStream_t s) {
   if (!n) return;
   const int g = grid_for((unsigned long long)n * 32, 256);
+  note_launch();
   switch (algo) {
     case kBfs: verify_kernel<kBfs><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
     case kCc: verify_kernel<kCc><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
+    note_launch();
     default: verify_kernel<kSssp><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
   }
 }

@@ -15,6 +15,8 @@ void launch_pull(int algo, int gate, bool det, const PullArgs& a, int grid, cuda
 void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t hi,
                    cudaStream_t s);
 // K8: PageRank pull-sum + hub finalize.
+// Kernels launched so far by the calling thread (all launch_* wrappers).
+uint64_t kernel_launch_count();
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,

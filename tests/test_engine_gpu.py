@@ -686,3 +686,32 @@ def test_srph_loader_reference_files(tmp_path):
             eng.load_srph(bad, 2)
         with pytest.raises(ps.FormatError):
             eng.load_srph(str(tmp_path / "missing.srph"), 2)
+
+
+def test_frontier_queue_matches_flag_path(monkeypatch):
+    """Sparse passes on the frontier queue (default: push appends first-time
+    improvements, no |V| census) and on the changed-flag census/compaction
+    (SERAPH_NO_FRONTIER_QUEUE) give the oracle's values and the same pass
+    structure for every algorithm, predictor and execution policy."""
+    n = 1 << 13
+    src, dst = O.generate_rmat(13, 16, seed=17)
+    w = O.assign_weights(src.size, 5, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    with ps.Engine(0) as eng:
+        for g, kinds in ((el, (ps.AlgoKind.BFS, ps.AlgoKind.SSSP)), (sym, (ps.AlgoKind.CC,))):
+            eng.load(*built(g, n // 16))
+            for kind in kinds:
+                want = oracle_values(g, kind, 3)
+                for pred in (ps.PredictorMode.OFF, ps.PredictorMode.STRONG):
+                    for ex in (ps.ExecutionPolicy.DENSITY_SWITCHED, ps.ExecutionPolicy.FORCE_SPARSE):
+                        c = cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex)
+                        prog = program_for(kind, 3, g)
+                        monkeypatch.delenv("SERAPH_NO_FRONTIER_QUEUE", raising=False)
+                        rq = eng.run(prog, c)
+                        monkeypatch.setenv("SERAPH_NO_FRONTIER_QUEUE", "1")
+                        rf = eng.run(prog, c)
+                        monkeypatch.delenv("SERAPH_NO_FRONTIER_QUEUE")
+                        assert np.array_equal(rq.values, want), (kind, pred, ex)
+                        assert np.array_equal(rf.values, want), (kind, pred, ex)
+                        assert rq.metrics.per_pass[-1].changed_vertices == 0
