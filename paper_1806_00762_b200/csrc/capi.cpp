@@ -222,7 +222,9 @@ int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const
       page_bytes += (uint64_t(pages[i].vertex_end - pages[i].vertex_begin) + 1 +
                      pages[i].edge_count * (weighted ? 2 : 1)) * 4;
     const bool derive = ctx->eng->world() == 1 && ctx->eng->fits_budget(page_bytes);
-    ctx->eng->load_csr(n, m, off, derive ? nullptr : nbr, derive ? nullptr : w);
+    // the offsets DMA stays queued ahead of the page DMAs on the copy stream
+    // (load_pages synchronises it before the host buffers are released)
+    ctx->eng->load_csr(n, m, off, derive ? nullptr : nbr, derive ? nullptr : w, /*sync=*/false);
     ctx->eng->load_pages(n, cap, weighted, pages, np);
     const double up = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     sr_metrics mm{};

@@ -128,7 +128,7 @@ Engine::~Engine() {
 // Graph upload
 // ---------------------------------------------------------------------------
 void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
-                      const uint32_t* w) {
+                      const uint32_t* w, bool sync) {
   SR_CUDA(cudaSetDevice(dev_));
   if (!off) throw EngineError(SR_E_INPUT, "csr: out_offsets is null");
   if (off[0] != 0 || off[n] != m)
@@ -154,19 +154,21 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   } else if (nbr && w) {
     csr_weighted_ = true;  // weighted graph without edges
   }
-  finish_csr();
+  finish_csr(sync);
   last_upload_bytes += bytes;
   last_upload_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-void Engine::finish_csr() {
+void Engine::finish_csr(bool sync) {
   coverage_ = -1;  // hot_source_coverage follows the out-degrees
   const size_t npad = (size_t(n_) + kCensusBlockVerts) / kCensusBlockVerts * kCensusBlockVerts + 16;
   outdeg_.reserve(npad);
   SR_CUDA(cudaMemsetAsync(outdeg_.p, 0, npad * 4, xs_));
   launch_outdeg(out_off_.p, n_, outdeg_.p, xs_);
-  SR_CUDA(cudaStreamSynchronize(xs_));
+  // unsynchronised only inside sr_run_graph, whose load_pages follows on the
+  // same copy stream and synchronises it before returning
+  if (sync) SR_CUDA(cudaStreamSynchronize(xs_));
   has_csr_ = true;
   csr_derived_ = false;
 }
@@ -742,6 +744,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       SR_CUDA(cudaMemcpyAsync(page_desc_.p, page_desc_h_.data(), np * sizeof(PageDesc),
                               cudaMemcpyHostToDevice, cs_));
     SR_CUDA(cudaStreamSynchronize(cs_));
+    SR_CUDA(cudaStreamSynchronize(xs_));  // a CSR upload queued by sr_run_graph
     if (csr_derived_) {  // the derived adjacency belonged to the previous page set
       has_csr_edges_ = false;
       csr_derived_ = false;

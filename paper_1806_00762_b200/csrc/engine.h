@@ -115,7 +115,7 @@ class Engine {
   ~Engine();
 
   void load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
-                const uint32_t* w);
+                const uint32_t* w, bool sync = true);
   void load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* pages,
                   uint32_t np);
   uint64_t page_bytes_total() const { return page_bytes_total_; }
@@ -198,7 +198,7 @@ class Engine {
   DBuf<uint32_t> out_nbr_, out_w_;
   DBuf<uint32_t> outdeg_;  // u32 out-degrees (census/compaction vector loads)
   void maybe_derive_csr();  // push adjacency = transpose of resident pages
-  void finish_csr();        // out-degrees + flags after the CSR arrays are in place
+  void finish_csr(bool sync = true);  // out-degrees + flags after the CSR arrays are in place
   void build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<uint32_t>& dst,
                        DBuf<uint32_t>& w, bool weighted, uint32_t cap, bool csr_edges);
   bool csr_derived_ = false;

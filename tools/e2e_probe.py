@@ -16,7 +16,8 @@ from paper_1806_00762_b200 import pagestream as ps  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
 a = ap.parse_args()
-ns = argparse.Namespace(algo="sssp", scale=a.scale, edge_factor=16, uniform=False, pages=16, seed=0)
+ns = argparse.Namespace(algo="sssp", scale=a.scale, edge_factor=16, uniform=False, pages=16, seed=0,
+                        lean=True, graph="device")
 W = bench.workload(ns)
 csr, pages = W["csr"], W["pages"]
 eng = ps.Engine(0)
@@ -39,3 +40,9 @@ print(f"run only (derived csr cached) {1e3*(time.time()-t0):.1f} ms", flush=True
 gb = N.C.c_double()
 N.check(N.lib.sr_bench_h2d(0, 1 << 30, 3, N.C.byref(gb)))
 print("h2d GB/s", gb.value)
+
+for rep in range(4):
+    t0 = time.time()
+    r = eng.run_graph(csr, pages, prog, cfg, values_out=vals)
+    print(f"run_graph {1e3*(time.time()-t0):.1f} ms (upload {1e3*r.metrics.upload_seconds:.1f} ms, "
+          f"device {1e3*r.metrics.device_seconds:.2f} ms)", flush=True)

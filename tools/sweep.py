@@ -24,12 +24,14 @@ def main():
     a = ap.parse_args()
     args = bench.parse.__wrapped__() if hasattr(bench.parse, "__wrapped__") else None
     ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform,
-                            pages=a.pages, seed=0)
+                            pages=a.pages, seed=0, lean=True, graph="device")
     t0 = time.time()
-    W = bench.workload(ns)
-    print(f"# build {time.time() - t0:.1f}s n={W['n']} m={W['m']}", flush=True)
     eng = ps.Engine(0)
-    eng.load(W["csr"], W["pages"])
+    W = bench.workload(ns, eng)
+    print(f"# build {time.time() - t0:.1f}s n={W['n']} m={W['m']}", flush=True)
+    if not W["loaded"]:
+        eng.load_csr(W["csr"], with_edges=False)
+        eng.load_pages(W["pages"])
     kind = ps.AlgoKind(bench.ALGOS[a.algo])
     prog = ps.VertexProgram(kind, 0)
     for mode in a.modes.split(","):
