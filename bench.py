@@ -345,31 +345,31 @@ def run_ours(args, rank, world, local_rank):
                 "isolated_sweep": {"ms": round(ms, 4), "edges": edges,
                                    "note": "gate-off sweep over the converged values"},
                 "gather_roofline": gather_roofline(k1_gathers / k1_s, info, clocks)}
+    elif args.budget_gb:
+        # out-of-core: the host link bounds; streamed bytes per run / run time
+        gbps = N.C.c_double()
+        N.check(N.lib.sr_bench_h2d(local_rank, 1 << 30, 3, N.C.byref(gbps)))
+        streamed = last.bytes_transferred
+        achieved = streamed / step_s / 1e9
+        kern = "pr_pull_kernel (K8)" if algo == 3 else "pull_relax_kernel (K1) + push (K3)"
+        roof = {"bound": "host-link", "kernel": kern + " + H2D page stream",
+                "achieved": round(achieved, 2), "peak": round(gbps.value, 2),
+                "unit": "GB/s", "frac": round(achieved / gbps.value, 4),
+                "peak_source": "measured (sr_bench_h2d, pinned 1 GiB)", "traffic": None,
+                "streamed_bytes_per_run": int(streamed),
+                "per_unit": "page_bytes of every admitted page (graph.cpp:96-100)"}
     elif algo == 3:
         iters = args.pr_iters
-        if args.budget_gb:
-            # out-of-core: the host link bounds; streamed bytes per run / run time
-            gbps = N.C.c_double()
-            N.check(N.lib.sr_bench_h2d(local_rank, 1 << 30, 3, N.C.byref(gbps)))
-            streamed = last.bytes_transferred
-            achieved = streamed / step_s / 1e9
-            roof = {"bound": "host-link", "kernel": "pr_pull_kernel (K8) + H2D page stream",
-                    "achieved": round(achieved, 2), "peak": round(gbps.value, 2),
-                    "unit": "GB/s", "frac": round(achieved / gbps.value, 4),
-                    "peak_source": "measured (sr_bench_h2d, pinned 1 GiB)", "traffic": None,
-                    "streamed_bytes_per_run": int(streamed),
-                    "per_unit": "page_bytes of every admitted page (graph.cpp:96-100)"}
-        else:
-            alg = (8 * m + 16 * n) * iters
-            peak, src_ = measured_peaks()
-            achieved = alg / step_s / 1e9
-            roof = {"bound": "hbm", "kernel": "pr_pull_kernel (K8), whole run",
-                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "peak_source": src_,
-                    "traffic": profile_traffic(f"pagerank-s{args.scale}"),
-                    "algorithmic_bytes_per_launch": 8 * m + 16 * n,
-                    "per_unit": "8 B/edge + 16 B/destination per iteration",
-                    "gather_roofline": gather_roofline(m * iters / step_s, info, clocks)}
+        alg = (8 * m + 16 * n) * iters
+        peak, src_ = measured_peaks()
+        achieved = alg / step_s / 1e9
+        roof = {"bound": "hbm", "kernel": "pr_pull_kernel (K8), whole run",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": src_,
+                "traffic": profile_traffic(f"pagerank-s{args.scale}"),
+                "algorithmic_bytes_per_launch": 8 * m + 16 * n,
+                "per_unit": "8 B/edge + 16 B/destination per iteration",
+                "gather_roofline": gather_roofline(m * iters / step_s, info, clocks)}
 
     # the multi-pass subgraph-iteration schedules on the same resident graph
     schedules = {}
