@@ -1315,10 +1315,15 @@ void Engine::census(int pass_kind) {
 }
 
 void Engine::read_census() {
-  SR_CUDA(cudaMemcpyAsync(census_h_.p, census_.p, sizeof(Census), cudaMemcpyDeviceToHost, cs_));
-  if (ctr_used_)
-    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
-                            cudaMemcpyDeviceToHost, cs_));
+  if (ctr_used_ <= 64 && !std::getenv("SERAPH_NO_PUBLISH")) {
+    // one kernel writes both into the mapped pinned buffers (UVA): no D2H DMAs
+    launch_publish(census_.p, census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, cs_);
+  } else {
+    SR_CUDA(cudaMemcpyAsync(census_h_.p, census_.p, sizeof(Census), cudaMemcpyDeviceToHost, cs_));
+    if (ctr_used_)
+      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
+                              cudaMemcpyDeviceToHost, cs_));
+  }
   SR_CUDA(cudaStreamSynchronize(cs_));
 }
 

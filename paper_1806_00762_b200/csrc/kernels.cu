@@ -1562,6 +1562,25 @@ size_t queue_prep_temp_bytes(uint32_t max_q) {
   return tb;
 }
 
+// Pass results to the host: the census and the run counters are written
+// straight into mapped pinned memory by one tiny kernel (no D2H copies).
+__global__ void publish_kernel(const Census* __restrict__ cz, Census* cz_host,
+                               const RunCtr* __restrict__ ctr, RunCtr* ctr_host, uint32_t n_ctr) {
+  const uint32_t words = sizeof(Census) / 4;
+  const uint32_t cwords = n_ctr * uint32_t(sizeof(RunCtr) / 8);
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(cz_host)[i] = reinterpret_cast<const uint32_t*>(cz)[i];
+  for (uint32_t i = threadIdx.x; i < cwords; i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(ctr_host)[i] =
+        reinterpret_cast<const unsigned long long*>(ctr)[i];
+}
+
+void launch_publish(const Census* cz, Census* cz_host, const RunCtr* ctr, RunCtr* ctr_host,
+                    uint32_t n_ctr, cudaStream_t s) {
+  note_launch();
+  publish_kernel<<<1, 256, 0, s>>>(cz, cz_host, ctr, ctr_host, n_ctr);
+}
+
 // Initial BFS/SSSP frontier {source} as a queue (initial_frontier,
 // engine.cpp:260-263) without the |V|-sized census and compaction.
 __global__ void seed_queue_kernel(uint32_t source, const uint32_t* __restrict__ outdeg,
