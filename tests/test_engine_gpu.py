@@ -715,3 +715,34 @@ def test_frontier_queue_matches_flag_path(monkeypatch):
                         assert np.array_equal(rq.values, want), (kind, pred, ex)
                         assert np.array_equal(rf.values, want), (kind, pred, ex)
                         assert rq.metrics.per_pass[-1].changed_vertices == 0
+
+
+@pytest.mark.parametrize("case", ["rmat20", "uniform20"])
+def test_scale20_parity_device_built(case, monkeypatch):
+    """Bigger-graph parity on the production paths: device-generated RMAT /
+    uniform scale-20 graphs (exported and checked against the oracle on the
+    same arrays), BFS/SSSP with the frontier queue, CC uniform on forced
+    source-blocked pulls (the C4 path) -- bit-exact for every predictor."""
+    n = 1 << 20
+    uniform = case == "uniform20"
+    quad = (0.25, 0.25, 0.25, 0.25) if uniform else (0.57, 0.19, 0.19, 0.05)
+    with ps.Engine(0) as eng:
+        eng.generate_graph(20, 16, *quad, seed=4, weights=(1, 64, 5), symmetrize=uniform,
+                           page_vertex_capacity=n // 16)
+        csr, pages, in_off, in_src, in_w = eng.export_graph()
+        m = int(in_off[-1])
+        # the oracle's edge list: the CSR rows expanded (same multiset of edges)
+        src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(csr.out_offsets).astype(np.int64))
+        el = ps.EdgeList(n, src, csr.out_neighbors, csr.out_weights)
+        assert src.size == m
+        if uniform:
+            monkeypatch.setenv("SERAPH_PULL_BLOCK_VERTS", str(1 << 17))
+            want = oracle_values(el, ps.AlgoKind.CC, 0)
+            for pred in PREDS:
+                r = eng.run(ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, want), pred
+        for kind in (ps.AlgoKind.BFS, ps.AlgoKind.SSSP):
+            want = oracle_values(el, kind, 1)
+            for pred in PREDS:
+                r = eng.run(program_for(kind, 1, el), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, want), (kind, pred)
