@@ -693,7 +693,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     SR_CUDA(cudaStreamSynchronize(cs_));
     uint64_t words = 0;
     for (uint32_t p = 0; p < np; ++p)
-      if (used[p]) words += pages_[p].bytes / 4;
+      if (used[p]) words += stream_image_words(pages_[p], weighted);
     stage_.reserve(std::max<uint64_t>(words, 1));
     uint64_t at = 0;
     std::vector<std::pair<uint32_t, uint64_t>> place;
@@ -706,7 +706,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       pm.on_device = false;
       if (!used[p]) continue;
       place.push_back({p, at});
-      at += pm.bytes / 4;
+      at += stream_image_words(pm, weighted);
     }
     auto on_device = [](const void* p) {
       cudaPointerAttributes at{};
@@ -717,23 +717,24 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     parallel_for(place.size(), [&](size_t k) {
       PageMeta& pm = pages_[place[k].first];
       uint32_t* base = stage_.p + place[k].second;
-      const size_t r1 = size_t(pm.ve - pm.vb) + 1;
+      const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
+      std::memset(base, 0, stream_image_words(pm, weighted) * 4);
       std::memcpy(base, pm.h_offs, r1 * 4);
       if (dev_src) {  // device-built graph under a forced budget: stage it on the host
-        SR_CUDA(cudaMemcpy(base + r1, pm.h_src, pm.edges * 4, cudaMemcpyDeviceToHost));
+        SR_CUDA(cudaMemcpy(base + so, pm.h_src, pm.edges * 4, cudaMemcpyDeviceToHost));
         if (weighted)
-          SR_CUDA(cudaMemcpy(base + r1 + pm.edges, pm.h_w, pm.edges * 4, cudaMemcpyDeviceToHost));
+          SR_CUDA(cudaMemcpy(base + wo, pm.h_w, pm.edges * 4, cudaMemcpyDeviceToHost));
         return;
       }
-      std::memcpy(base + r1, pm.h_src, pm.edges * 4);
-      if (weighted) std::memcpy(base + r1 + pm.edges, pm.h_w, pm.edges * 4);
+      std::memcpy(base + so, pm.h_src, pm.edges * 4);
+      if (weighted) std::memcpy(base + wo, pm.h_w, pm.edges * 4);
     });
     for (auto& [p, off] : place) {
       PageMeta& pm = pages_[p];
-      const size_t r1 = size_t(pm.ve - pm.vb) + 1;
+      const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
       pm.h_offs = stage_.p + off;
-      pm.h_src = stage_.p + off + r1;
-      pm.h_w = weighted ? stage_.p + off + r1 + pm.edges : nullptr;
+      pm.h_src = stage_.p + off + so;
+      pm.h_w = weighted ? stage_.p + off + wo : nullptr;
     }
     for (auto& pm : pages_)
       if (!pm.h_offs) pm.h_src = pm.h_w = nullptr;
@@ -835,6 +836,8 @@ void Engine::alloc_run_state(const sr_run_config& c) {
   // and run; every other launch aggregates into a single entry.
   size_t entries = size_t(std::max(1, c.max_reentry_times)) * np + np;
   entries += (np + 1) * size_t(std::max(1, c.buffer_repetitions)) + 4096 + 64;
+  if (c.algo == SR_ALGO_PAGERANK)  // all iterations' counters stay in the arena (run_pagerank)
+    entries = std::max(entries, (np + 2) * size_t(std::max<uint32_t>(c.pr_iterations, 1)) + 64);
   ctr_.reserve(entries);
   ctr_h_.reserve(entries);
 }
@@ -969,18 +972,15 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
     if (pages_[p].h_offs) used.push_back(p);
   const uint32_t want = std::max<uint32_t>(window, 2);
   const size_t U = used.size();
-  std::vector<uint64_t> suf_offs(U + 1, 0), suf_edges(U + 1, 0);
-  for (size_t k = U; k-- > 0;) {
-    const PageMeta& pm = pages_[used[k]];
-    suf_offs[k] = std::max<uint64_t>(suf_offs[k + 1], pm.ve - pm.vb + 1);
-    suf_edges[k] = std::max<uint64_t>(suf_edges[k + 1], pm.edges);
-  }
-  const uint64_t wmul = weighted_ ? 2 : 1;
+  // slot = the largest streamed page image (stream_image_words)
+  std::vector<uint64_t> suf_words(U + 1, 0);
+  for (size_t k = U; k-- > 0;)
+    suf_words[k] = std::max(suf_words[k + 1], stream_image_words(pages_[used[k]], weighted_));
   size_t K = 0;
   bool fits = false;
   uint64_t prefix = 0;
   for (size_t k = 0; k < U; ++k) {
-    const uint64_t slot_bytes = (suf_offs[k] + suf_edges[k] * wmul) * 4;
+    const uint64_t slot_bytes = suf_words[k] * 4;
     if (prefix + want * slot_bytes <= budget_) {
       K = k;
       fits = true;
@@ -990,9 +990,7 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
   if (!fits)
     throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(budget_) +
                                        " B cannot hold a window of " + std::to_string(want) +
-                                       " page slots of " +
-                                       std::to_string((suf_offs[0] + suf_edges[0] * wmul) * 4) + " B");
-  const uint64_t max_offs = suf_offs[K], max_edges = suf_edges[K];
+                                       " page slots of " + std::to_string(suf_words[0] * 4) + " B");
   const bool same_plan = plan_window_ == want && plan_cached_ == K && slots_.size() == want;
   if (same_plan) return;
   // (re)build the cache arena for pages used[0..K)
@@ -1041,12 +1039,10 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
   }
   slots_.clear();
   slots_.resize(want);
+  const uint64_t slot_words = std::max<uint64_t>(suf_words[K], 1);
   for (auto& s : slots_) {
-    s.offs.reserve(std::max<uint64_t>(max_offs, 1));
-    s.src.reserve(max_edges + 8);
-    if (weighted_) s.w.reserve(max_edges + 8);
-    s.cap_offs = max_offs;
-    s.cap_edges = max_edges;
+    s.buf.reserve(slot_words);
+    s.cap_words = slot_words;
     SR_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
     SR_CUDA(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
     SR_CUDA(cudaEventRecord(s.freed, cs_));
@@ -1083,14 +1079,12 @@ void Engine::make_resident(uint32_t page, long long step, const std::vector<char
     tr = &wtrace_.back();
     SR_CUDA(cudaEventRecord(tr->a, xs_));
   }
-  const size_t r1 = size_t(pm.ve - pm.vb) + 1;
-  SR_CUDA(cudaMemcpyAsync(sl.offs.p, pm.h_offs, r1 * 4, cudaMemcpyHostToDevice, xs_));
-  if (pm.edges) {
-    SR_CUDA(cudaMemcpyAsync(sl.src.p, pm.h_src, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
-    if (weighted_)
-      SR_CUDA(cudaMemcpyAsync(sl.w.p, pm.h_w, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
-  }
-  launch_set_page_desc(page_desc_.p, page, sl.offs.p, sl.src.p, weighted_ ? sl.w.p : nullptr, xs_);
+  // the staged page image (offsets | sources | weights, 32 B aligned) in ONE DMA
+  const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
+  SR_CUDA(cudaMemcpyAsync(sl.buf.p, pm.h_offs, stream_image_words(pm, weighted_) * 4, cudaMemcpyHostToDevice,
+                          xs_));
+  launch_set_page_desc(page_desc_.p, page, sl.buf.p, sl.buf.p + so,
+                       weighted_ ? sl.buf.p + wo : nullptr, xs_);
   if (tr) SR_CUDA(cudaEventRecord(tr->b, xs_));
   SR_CUDA(cudaEventRecord(sl.ready, xs_));
   sl.page = int(page);
@@ -2086,9 +2080,15 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
   launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
   if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
+  // The iterations are enqueued back to back with no host sync in between
+  // (the copy stream prefetches the next iteration's pages while the current
+  // one computes); each iteration's counters get their own slice of the
+  // counter arena, read back once at the end.
+  ctr_used_ = 0;
+  SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
+  std::vector<uint32_t> ctr_begin;
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
-    ctr_used_ = 0;
-    SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
+    ctr_begin.push_back(ctr_used_);
     if (comm_) {
       SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
       SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
@@ -2111,18 +2111,9 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
                              inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
     }
     exchange_round(true);
-    if (ctr_used_)
-      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
-                              cudaMemcpyDeviceToHost, cs_));
-    SR_CUDA(cudaStreamSynchronize(cs_));
     sr_pass_stats st{};
     st.pass_index = it;
     st.kind = SR_PASS_DENSE_PULL;
-    for (size_t i = 0; i < size_t(ctr_used_); ++i) {
-      gathers_total_ += ctr_h_.p[i].gathers;
-      st.attempts += ctr_h_.p[i].attempts;
-      st.edges_read += ctr_h_.p[i].edges;
-    }
     if (blocked) {  // every destination and edge once per iteration
       st.attempts = n_;
       st.edges_read = page_edges_total_;
@@ -2134,8 +2125,10 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     m.kernel_runs += po.kernel_runs;
     m.passes += 1;
     m.dense_passes += 1;
-    m.update_attempts += st.attempts;
-    m.edges_read += st.edges_read;
+    if (blocked) {
+      m.update_attempts += st.attempts;
+      m.edges_read += st.edges_read;
+    }
     passes.push_back(st);
     std::swap(rank_a_.p, rank_b_.p);
     std::swap(contrib_a_.p, contrib_b_.p);
@@ -2143,7 +2136,22 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   SR_CUDA(cudaEventRecord(ev_stop_, cs_));
   if (ranks_out)
     SR_CUDA(cudaMemcpyAsync(ranks_out, rank_a_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  if (ctr_used_)
+    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
+                            cudaMemcpyDeviceToHost, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
+  ctr_begin.push_back(ctr_used_);
+  for (size_t it = 0; it + 1 < ctr_begin.size(); ++it) {
+    if (blocked) continue;  // counted analytically above
+    sr_pass_stats& st = passes[passes.size() - (ctr_begin.size() - 1) + it];
+    for (uint32_t i = ctr_begin[it]; i < ctr_begin[it + 1]; ++i) {
+      gathers_total_ += ctr_h_.p[i].gathers;
+      st.attempts += ctr_h_.p[i].attempts;
+      st.edges_read += ctr_h_.p[i].edges;
+    }
+    m.update_attempts += st.attempts;
+    m.edges_read += st.edges_read;
+  }
   float ms = 0;
   SR_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_stop_));
   m.device_seconds = ms * 1e-3;

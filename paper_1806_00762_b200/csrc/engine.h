@@ -94,13 +94,21 @@ struct PageMeta {
 };
 
 struct StreamSlot {
-  DBuf<uint32_t> offs, src, w;
-  uint64_t cap_offs = 0, cap_edges = 0;
+  DBuf<uint32_t> buf;  // one streamed page image: offsets | sources | weights
+  uint64_t cap_words = 0;
   int page = -1;
   long long last_use = -1;   // step index of the last launch that read it
   cudaEvent_t ready = nullptr;  // copy finished (copy stream)
   cudaEvent_t freed = nullptr;  // last reader finished (compute stream)
 };
+
+inline uint64_t pad8(uint64_t words) { return (words + 7) & ~uint64_t(7); }
+// Words of a page's streaming image: offsets, sources and weights, each
+// starting 32 B aligned (K1's vector runs), + 8 words of read slack.
+inline uint64_t stream_image_words(const PageMeta& pm, bool weighted) {
+  const uint64_t e = pad8(pm.edges);
+  return pad8(uint64_t(pm.ve - pm.vb) + 1) + e * (weighted ? 2 : 1) + 8;
+}
 
 struct PassOut {
   RunStats totals;
