@@ -582,10 +582,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     if (used[p]) used_bytes += pages_[p].bytes;
   }
   all_resident_ = budget_ == 0 || used_bytes <= budget_;
-  for (auto& s : slots_) {
-    s.page = -1;
-    s.last_use = -1;
-  }
+  ring_reset();
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
   sb_.built = false;
@@ -965,11 +962,15 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
 // ---------------------------------------------------------------------------
 void Engine::ensure_slots(uint32_t window, PassOut& po) {
   // Budget plan for the out-of-core path: a ring of `window` slots sized for
-  // the largest streamed page, and the longest prefix of pages (id order,
-  // i.e. RMAT's heaviest pages first) that still fits cached permanently.
+  // the largest streamed page, and the heaviest pages cached permanently --
+  // the largest K for which the K biggest pages plus `window` slots of the
+  // (K+1)-th biggest fit (RMAT page sizes follow the popcount of the page
+  // index, so "heaviest" is not an id prefix).
   std::vector<uint32_t> used;
   for (uint32_t p = 0; p < pages_.size(); ++p)
     if (pages_[p].h_offs) used.push_back(p);
+  std::stable_sort(used.begin(), used.end(),
+                   [&](uint32_t x, uint32_t y) { return pages_[x].bytes > pages_[y].bytes; });
   const uint32_t want = std::max<uint32_t>(window, 2);
   const size_t U = used.size();
   // slot = the largest streamed page image (stream_image_words)
@@ -991,7 +992,7 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
     throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(budget_) +
                                        " B cannot hold a window of " + std::to_string(want) +
                                        " page slots of " + std::to_string(suf_words[0] * 4) + " B");
-  const bool same_plan = plan_window_ == want && plan_cached_ == K && slots_.size() == want;
+  const bool same_plan = plan_window_ == want && plan_cached_ == K && ring_words_ > 0;
   if (same_plan) return;
   // (re)build the cache arena for pages used[0..K)
   SR_CUDA(cudaStreamSynchronize(cs_));
@@ -1033,45 +1034,91 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
     po.bytes_transferred += pm.bytes;
     h2d_bytes_ += pm.bytes;
   }
-  for (auto& s : slots_) {
-    if (s.ready) cudaEventDestroy(s.ready);
-    if (s.freed) cudaEventDestroy(s.freed);
-  }
-  slots_.clear();
-  slots_.resize(want);
-  const uint64_t slot_words = std::max<uint64_t>(suf_words[K], 1);
-  for (auto& s : slots_) {
-    s.buf.reserve(slot_words);
-    s.cap_words = slot_words;
-    SR_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
-    SR_CUDA(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
-    SR_CUDA(cudaEventRecord(s.freed, cs_));
-  }
+  // the streaming ring: `window` images of the largest streamed page
+  ring_reset();
+  ring_words_ = std::max<uint64_t>(suf_words[K], 1) * want;
+  ring_.release();
+  ring_.reserve(ring_words_);
   SR_CUDA(cudaEventRecord(ev_step_, xs_));
   SR_CUDA(cudaStreamWaitEvent(cs_, ev_step_, 0));
   plan_window_ = want;
   plan_cached_ = K;
 }
 
-void Engine::make_resident(uint32_t page, long long step, const std::vector<char>& protect,
+void Engine::ring_reset() {
+  for (int e : ring_fifo_) {
+    if (slots_[e].page >= 0 && size_t(slots_[e].page) < pages_.size())
+      pages_[slots_[e].page].slot = -1;
+    slots_[e].page = -1;
+    slot_free_.push_back(e);
+  }
+  ring_fifo_.clear();
+  ring_head_ = 0;
+}
+
+// Drop the oldest image from the ring unless a step that is about to run
+// still needs it; the next copy into its space waits for its last reader.
+bool Engine::ring_evict_oldest(const std::vector<char>& protect) {
+  if (ring_fifo_.empty()) return false;
+  const int e = ring_fifo_.front();
+  StreamSlot& sl = slots_[e];
+  if (sl.page >= 0 && protect[sl.page]) return false;
+  SR_CUDA(cudaStreamWaitEvent(xs_, sl.freed, 0));
+  if (sl.page >= 0) pages_[sl.page].slot = -1;
+  sl.page = -1;
+  ring_fifo_.pop_front();
+  slot_free_.push_back(e);
+  if (ring_fifo_.empty()) ring_head_ = 0;
+  return true;
+}
+
+// Admit a page into the ring (one DMA of its staged image on the copy
+// stream).  Returns false when it cannot be placed without evicting an image
+// that `protect` marks as still needed.
+bool Engine::make_resident(uint32_t page, long long step, const std::vector<char>& protect,
                            PassOut& po) {
   PageMeta& pm = pages_[page];
-  if (pm.on_device || pm.slot >= 0) return;
-  int best = -1;
-  for (int s = 0; s < int(slots_.size()); ++s) {
-    const StreamSlot& sl = slots_[s];
-    if (sl.page < 0) {
-      best = s;
+  if (pm.on_device || pm.slot >= 0) return true;
+  const uint64_t need = stream_image_words(pm, weighted_);
+  if (need > ring_words_) throw EngineError(SR_E_CONTRACT, "page larger than the streaming ring");
+  uint64_t pos = 0;
+  for (;;) {
+    if (ring_fifo_.empty()) {
+      pos = 0;
       break;
     }
-    if (protect[sl.page]) continue;
-    if (best < 0 || sl.last_use < slots_[best].last_use) best = s;
+    const uint64_t tail = slots_[ring_fifo_.front()].start;
+    if (ring_head_ > tail) {
+      // live region [tail, head): free space at [head, end) and [0, tail)
+      if (ring_head_ + need <= ring_words_) {
+        pos = ring_head_;
+        break;
+      }
+      if (need <= tail) {
+        pos = 0;
+        break;
+      }
+    } else if (ring_head_ + need <= tail) {
+      // wrapped: free space [head, tail)
+      pos = ring_head_;
+      break;
+    }
+    if (!ring_evict_oldest(protect)) return false;
   }
-  if (best < 0) throw EngineError(SR_E_CONTRACT, "transfer scheduled with no slot available");
-  StreamSlot& sl = slots_[best];
-  if (sl.page >= 0) pages_[sl.page].slot = -1;
-  // the copy may only overwrite the slot once its last reader finished
-  SR_CUDA(cudaStreamWaitEvent(xs_, sl.freed, 0));
+  int e;
+  if (!slot_free_.empty()) {
+    e = slot_free_.back();
+    slot_free_.pop_back();
+  } else {
+    e = int(slots_.size());
+    slots_.emplace_back();
+    SR_CUDA(cudaEventCreateWithFlags(&slots_[e].ready, cudaEventDisableTiming));
+    SR_CUDA(cudaEventCreateWithFlags(&slots_[e].freed, cudaEventDisableTiming));
+    SR_CUDA(cudaEventRecord(slots_[e].freed, cs_));
+  }
+  StreamSlot& sl = slots_[e];
+  sl.start = pos;
+  sl.words = need;
   WallTraceRec* tr = nullptr;
   if (record_trace_) {
     wtrace_.push_back(WallTraceRec{trace_event(), trace_event(), {page}, SR_TRACE_XFER_START,
@@ -1080,19 +1127,21 @@ void Engine::make_resident(uint32_t page, long long step, const std::vector<char
     SR_CUDA(cudaEventRecord(tr->a, xs_));
   }
   // the staged page image (offsets | sources | weights, 32 B aligned) in ONE DMA
+  uint32_t* base = ring_.p + pos;
   const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
-  SR_CUDA(cudaMemcpyAsync(sl.buf.p, pm.h_offs, stream_image_words(pm, weighted_) * 4, cudaMemcpyHostToDevice,
-                          xs_));
-  launch_set_page_desc(page_desc_.p, page, sl.buf.p, sl.buf.p + so,
-                       weighted_ ? sl.buf.p + wo : nullptr, xs_);
+  SR_CUDA(cudaMemcpyAsync(base, pm.h_offs, need * 4, cudaMemcpyHostToDevice, xs_));
+  launch_set_page_desc(page_desc_.p, page, base, base + so, weighted_ ? base + wo : nullptr, xs_);
   if (tr) SR_CUDA(cudaEventRecord(tr->b, xs_));
   SR_CUDA(cudaEventRecord(sl.ready, xs_));
   sl.page = int(page);
   sl.last_use = step;
-  pm.slot = best;
+  pm.slot = e;
+  ring_fifo_.push_back(e);
+  ring_head_ = pos + need;
   po.pages_transferred += 1;
   po.bytes_transferred += pm.bytes;
   h2d_bytes_ += pm.bytes;
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1190,7 +1239,9 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
     const long long step_id = ++step_counter_;
     if (stream) {
       set_protect(si, si + 1);
-      for (uint32_t p : st.pages) make_resident(p, step_id, protect, po);
+      for (uint32_t p : st.pages)
+        if (!make_resident(p, step_id, protect, po))
+          throw EngineError(SR_E_CONFIG, "streaming ring cannot hold one schedule step");
       for (uint32_t p : st.pages)
         if (pages_[p].slot >= 0) SR_CUDA(cudaStreamWaitEvent(cs_, slots_[pages_[p].slot].ready, 0));
     }
@@ -1213,17 +1264,18 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
           slots_[s].last_use = step_id;
         }
       }
-      // prefetch the next step's pages; LRU victims (pages of older steps
-      // first), never the next step's pages nor the idle-fill victim
+      // prefetch the next step's pages into the ring (oldest images are
+      // evicted first, never those of the current or the next step)
       if (si + 1 < steps.size()) {
-        set_protect(si + 1, si + 2);
-        if (mode == SR_SCHED_PIPELINED_FINE && !st.pages.empty())
-          protect[*std::min_element(st.pages.begin(), st.pages.end())] = 1;
-        bool pending = false;
+        set_protect(si, si + 2);
+        bool pending = false, admitted = true;
         cudaEvent_t last_ready = nullptr;
         for (uint32_t p : steps[si + 1].pages) {
           const bool was = pages_[p].on_device || pages_[p].slot >= 0;
-          make_resident(p, step_id, protect, po);
+          if (!make_resident(p, step_id, protect, po)) {
+            admitted = false;
+            break;
+          }
           if (!was) {
             pending = true;
             last_ready = slots_[pages_[p].slot].ready;
@@ -1251,6 +1303,21 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
           }
           const int s = pages_[victim].slot;
           if (s >= 0) SR_CUDA(cudaEventRecord(slots_[s].freed, cs_));
+        }
+        // deeper lookahead: keep the copy engine busy while a long step (e.g.
+        // the cached heavy pages) computes -- admit later steps' pages as long
+        // as the ring has room that no step from here to there still needs
+        if (mode != SR_SCHED_PIPELINED_FINE && admitted) {
+          for (size_t sj = si + 2; sj < steps.size() && sj < si + 64; ++sj) {
+            set_protect(si, sj + 1);
+            bool all = true;
+            for (uint32_t p : steps[sj].pages)
+              if (!make_resident(p, step_id, protect, po)) {
+                all = false;
+                break;
+              }
+            if (!all) break;
+          }
         }
       }
     }

@@ -9,6 +9,7 @@
 #include <array>
 #include <atomic>
 #include <cstdint>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -93,9 +94,11 @@ struct PageMeta {
   int slot = -1;             // streaming slot holding the page
 };
 
+// One streamed page image placed in the byte ring (offsets | sources |
+// weights, 32 B aligned): entries are allocated contiguously and evicted
+// oldest first, so many small pages can be in flight at once.
 struct StreamSlot {
-  DBuf<uint32_t> buf;  // one streamed page image: offsets | sources | weights
-  uint64_t cap_words = 0;
+  uint64_t start = 0, words = 0;  // position in the ring (words)
   int page = -1;
   long long last_use = -1;   // step index of the last launch that read it
   cudaEvent_t ready = nullptr;  // copy finished (copy stream)
@@ -181,7 +184,7 @@ class Engine {
   void ensure_slots(uint32_t window, PassOut& po);
   uint32_t plan_window_ = 0;
   size_t plan_cached_ = size_t(-1);
-  void make_resident(uint32_t page, long long step, const std::vector<char>& protect,
+  bool make_resident(uint32_t page, long long step, const std::vector<char>& protect,
                      PassOut& po);
   void build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st);
   std::vector<cudaEvent_t> page_events_;  // resident upload: copy done per page
@@ -229,7 +232,13 @@ class Engine {
   DBuf<uint32_t> hub_vertex_, hub_stamp_;
   DBuf<float> hub_sum_;
   uint32_t n_hubs_ = 0;
-  std::vector<StreamSlot> slots_;
+  std::vector<StreamSlot> slots_;  // entry pool (events created once; index = PageMeta::slot)
+  std::vector<int> slot_free_;     // unused pool entries
+  std::deque<int> ring_fifo_;      // live entries, oldest first
+  DBuf<uint32_t> ring_;            // the streaming ring (HBM budget minus the cached pages)
+  uint64_t ring_words_ = 0, ring_head_ = 0;
+  void ring_reset();
+  bool ring_evict_oldest(const std::vector<char>& protect);
   long long step_counter_ = 0;
   bool first_touch_done_ = false;  // resident path: admission counted once per run
 
