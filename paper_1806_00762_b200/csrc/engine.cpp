@@ -1200,9 +1200,26 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
     default:
       if (!stream) {
         steps.push_back({order, 1, false});
+      } else if (n > n_dev) {
+        // pages still in the streaming ring first (before newer transfers
+        // evict them), then one step per streamed page with the permanently
+        // cached pages spread evenly over those steps (their compute then
+        // overlaps the transfers instead of stalling the link)
+        std::vector<uint32_t> ring_pages, cached;
+        for (size_t i = 0; i < n_dev; ++i)
+          (pages_[order[i]].on_device ? cached : ring_pages).push_back(order[i]);
+        if (!ring_pages.empty()) steps.push_back({ring_pages, 1, false});
+        const size_t ns = n - n_dev, nc = cached.size();
+        size_t next_c = 0;
+        for (size_t i = n_dev; i < n; ++i) {
+          std::vector<uint32_t> pg;
+          for (const size_t upto = (i - n_dev + 1) * nc / ns; next_c < upto; ++next_c)
+            pg.push_back(cached[next_c]);
+          pg.push_back(order[i]);
+          steps.push_back({pg, 1, false});
+        }
       } else {
-        if (n_dev) steps.push_back({slice(0, n_dev), 1, false});
-        for (size_t i = n_dev; i < n; ++i) steps.push_back({slice(i, i + 1), 1, false});
+        steps.push_back({order, 1, false});
       }
       break;
   }
