@@ -134,6 +134,40 @@ struct PushArgs {
 };
 constexpr uint32_t kPushChunk = 256;  // flattened edges per warp task
 
+// Small-frontier tail (K3 in one CTA): consecutive sparse passes whose queue
+// fits kTailMaxQueue vertices / kTailMaxEdges out-edges run inside ONE
+// single-block launch (block barriers only, no grid sync, no host round
+// trip); the loop leaves when the frontier is empty, dense enough for a
+// pull, or too big for one block.
+constexpr uint32_t kTailMaxQueue = 8192;
+constexpr uint32_t kTailMaxEdges = 1u << 16;
+constexpr uint32_t kTailMaxPasses = 64;
+struct TailRecord {
+  unsigned long long edges, valid, changed, out_edges, queued;
+};
+struct TailResult {
+  uint32_t passes;   // sparse passes run
+  uint32_t reason;   // 0 converged, 1 dense next, 2 frontier too big, 3 pass cap
+};
+struct TailArgs {
+  uint32_t* values;
+  const unsigned long long* out_offsets;
+  const uint32_t* out_neighbors;
+  const uint32_t* out_weights;
+  const uint32_t* outdeg;
+  uint32_t* stamp;
+  uint32_t epoch0;      // pass k uses epoch0 + k
+  uint32_t* list;       // in: the queue (q0 entries); out: the final queue
+  uint32_t* list2;      // scratch queue
+  uint32_t q0;
+  uint32_t max_passes;
+  double dense_threshold;  // density_switch: dense iff out-edges > this
+  int force_sparse;
+  Census* census;       // strong-predictor min_changed accumulator
+  TailRecord* rec;      // [max_passes] (mapped host memory)
+  TailResult* res;      // (mapped host memory)
+};
+
 // Persistent sparse stage (K3+K4 fused): consecutive sparse passes on the
 // device, leaving when the frontier is empty or dense enough for a pull.
 struct SparseLoopArgs {

@@ -1644,6 +1644,58 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     ++pass_index;
   };
 
+  // A small queued frontier: the consecutive sparse passes run inside one
+  // single-block launch (tail_loop_kernel) with the host loop's decisions;
+  // the passes are accounted from the per-pass records afterwards.
+  auto do_sparse_tail = [&]() -> bool {
+    if (!queue_mode() || !fq_ready_ || std::getenv("SERAPH_NO_TAIL")) return false;
+    const uint64_t q = census_h_.p->own_push, e = census_h_.p->own_edges;
+    if (q == 0 || q > kTailMaxQueue || e > kTailMaxEdges || f_count == 0) return false;
+    if (uint64_t(fq_epoch_) + kTailMaxPasses + 2 >= 0xffffffffull) return false;
+    tail_rec_.reserve(kTailMaxPasses);
+    tail_res_.reserve(1);
+    TailArgs t{};
+    t.values = values_.p;
+    t.out_offsets = out_off_.p;
+    t.out_neighbors = out_nbr_.p;
+    t.out_weights = csr_weighted_ ? out_w_.p : nullptr;
+    t.outdeg = outdeg_.p;
+    t.stamp = stamp_.p;
+    t.epoch0 = fq_epoch_ + 1;
+    t.list = list_.p;
+    t.list2 = list2_.p;
+    t.q0 = uint32_t(q);
+    t.max_passes = kTailMaxPasses;
+    t.dense_threshold = cfg.density_threshold_fraction * double(m_);
+    t.force_sparse = cfg.execution == SR_EXEC_FORCE_SPARSE ? 1 : 0;
+    t.census = census_.p;
+    t.rec = tail_rec_.p;
+    t.res = tail_res_.p;
+    launch_tail_loop(algo_, t, cs_);
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    const uint32_t np_run = tail_res_.p->passes;
+    fq_epoch_ += np_run;
+    for (uint32_t k = 0; k < np_run; ++k) {
+      const TailRecord& r = tail_rec_.p[k];
+      sr_pass_stats st{};
+      st.pass_index = pass_index;
+      st.kind = SR_PASS_SPARSE_PUSH;
+      st.attempts = r.edges;  // push: attempts and edges_read count edges (engine.cpp:77-78)
+      st.edges_read = r.edges;
+      st.valid_updates = r.valid;
+      st.changed_vertices = r.changed;
+      account(st);
+      m.sparse_passes += 1;
+      ++pass_index;
+      f_count = r.changed;
+      f_out = r.out_edges;
+      census_h_.p->own_push = census_h_.p->push_count = r.queued;
+      census_h_.p->own_edges = census_h_.p->out_edges = r.out_edges;
+      census_h_.p->changed = r.changed;
+    }
+    return np_run > 0;
+  };
+
   auto do_sparse = [&]() {
     // sparse_push_pass (engine.cpp:63-93) on the device frontier
     begin_pass();
@@ -1831,7 +1883,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
       continue;
     }
     if (sparse) {
-      if (!do_sparse_loop()) do_sparse();
+      if (!do_sparse_tail() && !do_sparse_loop()) do_sparse();
       prev_dense = false;
     } else {
       do_dense();

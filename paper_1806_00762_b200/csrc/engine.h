@@ -250,6 +250,8 @@ class Engine {
   // epoch stamps that deduplicate appends, whether list_ holds a queue
   DBuf<uint32_t> list2_, stamp_;
   DBuf<uint8_t> scan_tmp_;  // cub scan temporaries of the queue prep (no per-pass malloc)
+  PinBuf<TailRecord> tail_rec_;  // small-frontier tail: per-pass records (mapped)
+  PinBuf<TailResult> tail_res_;
   uint32_t fq_epoch_ = 0;
   bool fq_ready_ = false;
   bool queue_mode() const;

@@ -1562,6 +1562,142 @@ size_t queue_prep_temp_bytes(uint32_t max_q) {
   return tb;
 }
 
+// ---------------------------------------------------------------------------
+// Small-frontier tail: consecutive sparse passes (sparse_push_pass,
+// engine.cpp:63-93) in ONE block.  Per pass: block scan of the queue's
+// out-degrees into shared memory, edges strided over the 1024 threads (entry
+// by binary search over the prefix), asynchronous atomicMin relaxations, and
+// the next queue built from first-time improvements (epoch stamps) with a
+// shared cursor.  Same decisions as the host loop: stop when nothing
+// changed, when the next frontier's out-edges exceed the density threshold
+// (the host runs the dense pass), or when it outgrows one block.
+// ---------------------------------------------------------------------------
+template <int A>
+__global__ void __launch_bounds__(1024) tail_loop_kernel(TailArgs t) {
+  __shared__ uint32_t s_pref[kTailMaxQueue + 1];
+  __shared__ uint32_t s_wsum[32];
+  __shared__ unsigned long long s_red[5][32];
+  __shared__ uint32_t s_qn;
+  __shared__ unsigned s_stop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* cur = t.list;
+  uint32_t* nxt = t.list2;
+  uint32_t q = t.q0;
+  uint32_t lane_min = kUnreached;
+  uint32_t pass = 0;
+  unsigned reason = 3;
+  for (; pass < t.max_passes; ++pass) {
+    // exclusive out-degree prefix of the queue (q <= kTailMaxQueue: 8 per thread)
+    constexpr int kPer = kTailMaxQueue / 1024;
+    uint32_t d[kPer], loc = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t i = tid * kPer + k;
+      d[k] = i < q ? __ldg(t.outdeg + cur[i]) : 0u;
+      loc += d[k];
+    }
+    const uint32_t incl = warp_incl_scan(loc, lane);
+    if (lane == 31) s_wsum[warp] = incl;
+    if (tid == 0) s_qn = 0;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = s_wsum[lane];
+      s_wsum[lane] = warp_incl_scan(x, lane) - x;
+    }
+    __syncthreads();
+    uint32_t run = s_wsum[warp] + incl - loc;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t i = tid * kPer + k;
+      if (i <= q) s_pref[i] = run;
+      run += d[k];
+    }
+    if (tid == int(blockDim.x) - 1 && q == kTailMaxQueue) s_pref[kTailMaxQueue] = run;
+    __syncthreads();
+    const uint32_t total = s_pref[q];
+    // relax every out-edge of the queue
+    unsigned long long valid = 0, changed = 0, out_next = 0;
+    const uint32_t epoch = t.epoch0 + pass;
+    for (uint32_t e = tid; e < total; e += blockDim.x) {
+      uint32_t lo = 0, hi = q - 1;  // last entry with s_pref <= e
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (s_pref[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint32_t u = cur[lo];
+      const unsigned long long ei = t.out_offsets[u] + (e - s_pref[lo]);
+      const uint32_t v = t.out_neighbors[ei];
+      const uint32_t w = (A == kSssp) ? t.out_weights[ei] : 0u;
+      const uint32_t cand = combine<A>(__ldcg(t.values + u), w);
+      if (cand < *(volatile uint32_t*)(t.values + v)) {
+        const uint32_t old = atomicMin(t.values + v, cand);
+        if (cand < old) {
+          valid += 1;
+          lane_min = min(lane_min, cand);
+          if (atomicMax(t.stamp + v, epoch) < epoch) {
+            const uint32_t dv = __ldg(t.outdeg + v);
+            changed += 1;
+            out_next += dv;
+            if (dv) nxt[atomicAdd(&s_qn, 1u)] = v;  // the scratch queue holds |V|
+          }
+        }
+      }
+    }
+    const unsigned long long vals[3] = {warp_sum(valid), warp_sum(changed), warp_sum(out_next)};
+    if (lane == 0)
+      for (int k = 0; k < 3; ++k) s_red[k][warp] = vals[k];
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long tot[3] = {0, 0, 0};
+      for (int w = 0; w < int(blockDim.x >> 5); ++w)
+        for (int k = 0; k < 3; ++k) tot[k] += s_red[k][w];
+      TailRecord r;
+      r.edges = total;
+      r.valid = tot[0];
+      r.changed = tot[1];
+      r.out_edges = tot[2];
+      r.queued = s_qn;
+      t.rec[pass] = r;
+      unsigned stop = 0xffffffffu;
+      if (tot[1] == 0) stop = 0;
+      else if (!t.force_sparse && double(tot[2]) > t.dense_threshold) stop = 1;
+      else if (s_qn > kTailMaxQueue || tot[2] > kTailMaxEdges) stop = 2;
+      s_stop = stop;
+    }
+    __syncthreads();
+    const unsigned stop = s_stop;
+    q = s_qn;
+    uint32_t* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+    __syncthreads();  // s_pref / s_qn reuse
+    if (stop != 0xffffffffu) {
+      reason = stop;
+      ++pass;
+      break;
+    }
+  }
+  // the final queue (the next frontier) back in t.list for the host path
+  if (cur != t.list)
+    for (uint32_t i = tid; i < q; i += blockDim.x) t.list[i] = cur[i];
+  lane_min = warp_min(lane_min);
+  if (lane == 0 && lane_min != kUnreached) atomicMin(&t.census->min_changed, lane_min);
+  if (tid == 0) {
+    t.res->passes = pass;
+    t.res->reason = reason;
+  }
+}
+
+void launch_tail_loop(int algo, const TailArgs& a, cudaStream_t s) {
+  note_launch();
+  switch (algo) {
+    case kBfs: tail_loop_kernel<kBfs><<<1, 1024, 0, s>>>(a); break;
+    case kCc: tail_loop_kernel<kCc><<<1, 1024, 0, s>>>(a); break;
+    default: tail_loop_kernel<kSssp><<<1, 1024, 0, s>>>(a); break;
+  }
+}
+
 // Pass results to the host: the census and the run counters are written
 // straight into mapped pinned memory by one tiny kernel (no D2H copies).
 __global__ void publish_kernel(const Census* __restrict__ cz, Census* cz_host,

@@ -81,6 +81,8 @@ void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* 
 // census + n_ctr run counters -> mapped pinned host memory (one kernel)
 void launch_publish(const Census* cz, Census* cz_host, const RunCtr* ctr, RunCtr* ctr_host,
                     uint32_t n_ctr, cudaStream_t s);
+// consecutive small-frontier sparse passes in one single-block launch
+void launch_tail_loop(int algo, const TailArgs& a, cudaStream_t s);
 void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, Census* cz,
                        cudaStream_t s);
 size_t queue_prep_temp_bytes(uint32_t max_q);

@@ -690,9 +690,11 @@ def test_srph_loader_reference_files(tmp_path):
 
 def test_frontier_queue_matches_flag_path(monkeypatch):
     """Sparse passes on the frontier queue (default: push appends first-time
-    improvements, no |V| census) and on the changed-flag census/compaction
-    (SERAPH_NO_FRONTIER_QUEUE) give the oracle's values and the same pass
-    structure for every algorithm, predictor and execution policy."""
+    improvements, no |V| census; small frontiers in the single-block tail
+    loop), on the queue without the tail loop (SERAPH_NO_TAIL) and on the
+    changed-flag census/compaction (SERAPH_NO_FRONTIER_QUEUE) give the
+    oracle's values and consistent pass records for every algorithm,
+    predictor and execution policy."""
     n = 1 << 13
     src, dst = O.generate_rmat(13, 16, seed=17)
     w = O.assign_weights(src.size, 5, 1, 64)
@@ -709,11 +711,17 @@ def test_frontier_queue_matches_flag_path(monkeypatch):
                         prog = program_for(kind, 3, g)
                         monkeypatch.delenv("SERAPH_NO_FRONTIER_QUEUE", raising=False)
                         rq = eng.run(prog, c)
+                        monkeypatch.setenv("SERAPH_NO_TAIL", "1")
+                        rn = eng.run(prog, c)
+                        monkeypatch.delenv("SERAPH_NO_TAIL")
                         monkeypatch.setenv("SERAPH_NO_FRONTIER_QUEUE", "1")
                         rf = eng.run(prog, c)
                         monkeypatch.delenv("SERAPH_NO_FRONTIER_QUEUE")
-                        assert np.array_equal(rq.values, want), (kind, pred, ex)
-                        assert np.array_equal(rf.values, want), (kind, pred, ex)
+                        for r in (rq, rn, rf):
+                            assert np.array_equal(r.values, want), (kind, pred, ex)
+                            assert len(r.metrics.per_pass) == r.metrics.passes
+                            assert sum(p.edges_read for p in r.metrics.per_pass) == \
+                                r.metrics.edges_read
                         assert rq.metrics.per_pass[-1].changed_vertices == 0
 
 
