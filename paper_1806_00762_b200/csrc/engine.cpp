@@ -1242,8 +1242,11 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
   }
 
   last_pass_blocked_ = false;
+  // Source blocking pays for gathers only: once the previous dense pass
+  // gathered for < 5 % of its edges (converged labels/levels skip theirs), the
+  // per-block destination traffic would dominate -- sweep unblocked.
   if (mode == SR_SCHED_BASELINE && !stream && !pagerank && world_ == 1 && !comm_ &&
-      pull_block_verts()) {
+      last_gather_frac_ >= 0.05 && pull_block_verts()) {
     if (pull_blocked_pass(gate, alloc_ctr(1))) {
       last_pass_blocked_ = true;
       po.kernel_runs += order.size();
@@ -1560,6 +1563,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   k_bfs_ = 0;
   s_cc_ = 0;
   l_sssp_ = 0;
+  last_gather_frac_ = 1.0;  // the first dense pass gathers
   ctr_used_ = 0;
   if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_) {
     // the initial frontier {source} directly as a queue
@@ -1591,13 +1595,16 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     passes.push_back(st);
   };
   auto sum_ctr = [&](sr_pass_stats& st) {
+    uint64_t gathers = 0;
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
-      gathers_total_ += ctr_h_.p[i].gathers;
+      gathers += ctr_h_.p[i].gathers;
       st.attempts += ctr_h_.p[i].attempts;
       st.valid_updates += ctr_h_.p[i].valid;
       st.skipped += ctr_h_.p[i].skipped;
       st.edges_read += ctr_h_.p[i].edges;
     }
+    gathers_total_ += gathers;
+    last_gather_frac_ = st.edges_read ? double(gathers) / double(st.edges_read) : 0.0;
   };
   auto begin_pass = [&]() {
     ctr_used_ = 0;

@@ -322,6 +322,7 @@ class Engine {
   uint64_t coverage_k_ = 0;
   bool pull_blocked_pass(int gate, RunCtr* ctr);
   bool last_pass_blocked_ = false;
+  double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
   void l2_window(const void* base, size_t bytes);
   int l2_persist_max_ = -1;  // persisting-L2 carve-out (bytes; 0 = unavailable/disabled)
