@@ -301,6 +301,7 @@ def run_ours(args, rank, world, local_rank):
 
     # parity at full size: device fixpoint law + source value
     parity = {}
+    res = None
     if algo in (0, 2):
         res = eng.run(prog, cfg)
         viol = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
@@ -415,7 +416,10 @@ def run_ours(args, rank, world, local_rank):
     # CPU baseline: the reference's run() on the same graph, bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, W, sample_runs=1)
+        cpu = cpu_baseline(args, W, sample_runs=1,
+                           ours=res.values if res is not None else None)
+        if cpu and "bit_exact_vs_reference_run" in cpu:
+            parity["bit_exact_vs_reference_run"] = cpu.pop("bit_exact_vs_reference_run")
 
     ms_per_step = step_s * 1e3
     out = {
@@ -459,9 +463,11 @@ def _config_name(args):
     return "C5" if args.scale >= 29 else "C2"
 
 
-def cpu_baseline(args, W, sample_runs=1):
+def cpu_baseline(args, W, sample_runs=1, ours=None):
     """The reference run() (oracle/_ref) on this box's host cores, same graph and config.
-    Falls back to the oracle port (Dijkstra/BFS/CC restatement) if _ref was not built."""
+    Falls back to the oracle port (Dijkstra/BFS/CC restatement) if _ref was not built.
+    With `ours` (our values on the same graph) it also reports whether the
+    reference's values are bit-identical at full size."""
     from oracle import oracle as O
     cores = args.cpu_threads or os.cpu_count() or 1
     csr, pages = W["csr"], W["pages"]
@@ -471,14 +477,17 @@ def cpu_baseline(args, W, sample_runs=1):
         g = O.RefGraph(ref, W["n"], csr.out_offsets, csr.out_neighbors,
                        csr.out_weights if W["weighted"] else None, W["in_off"], W["in_src"],
                        W["in_w"], W["cap"])
-        secs, mets = [], None
+        secs, mets, vals = [], None, None
         for _ in range(sample_runs):
-            _, mets = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
-                            args.window, cores, 1, 0, 0.05)
+            vals, mets = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
+                               args.window, cores, 1, 0, 0.05, want_values=ours is not None)
             secs.append(mets["wall_seconds"])
         g.close()
         t = min(secs)
-        return {"value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
+        extra = {}
+        if ours is not None and vals is not None:
+            extra["bit_exact_vs_reference_run"] = bool(np.array_equal(np.asarray(vals), ours))
+        return {**extra, "value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
                 "kind": "reference", "seconds": round(t, 3),
                 "sample": f"{sample_runs} full reference run() of the same workload "
                           f"(ClockMode::Wall, {cores} OpenMP workers)",
