@@ -317,6 +317,13 @@ int sr_nccl_unique_id(uint8_t out[128]);
  * min (sum for PageRank) all-reduce over NVLink. */
 int sr_attach_world(sr_ctx* ctx, int rank, int world, const uint8_t unique_id[128]);
 
+/* Test/dev transport: make ctx rank `rank` of `world` contexts of THIS process
+ * (any devices, including one shared GPU) whose exchange all-reduces go
+ * through host memory instead of NCCL; `group` names the world.  Each rank's
+ * sr_run must be driven from its own thread.  Exercises the sharded round
+ * protocol of sr_attach_world where NCCL cannot (two ranks on one GPU). */
+int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group);
+
 /* ---- host-side graph utilities (no GPU needed) ------------------------- */
 /* Edge-balanced contiguous cut of the destination space into `parts`
  * ranges: cuts[0]=0 ... cuts[parts]=num_vertices, chosen so that every range

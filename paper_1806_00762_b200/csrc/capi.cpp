@@ -145,6 +145,11 @@ int sr_load_srph(sr_ctx* ctx, const char* path, uint32_t cap, int flags) {
   return guard(ctx, [&] { ctx->eng->load_srph(path, cap, flags & SR_BUILD_CSR_EDGES); });
 }
 
+int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group) {
+  if (!ctx || !group) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->attach_loopback(rank, world, group); });
+}
+
 int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out) {
   if (!ctx || !out) return SR_E_CONFIG;
   ctx->eng->graph_info(*out);

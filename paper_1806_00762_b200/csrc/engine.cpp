@@ -4,6 +4,7 @@
 // runs in the sm_100a kernels of kernels.cu.
 #include "engine.h"
 #include "devgraph.h"
+#include "loopback.h"
 
 #include <algorithm>
 #include <chrono>
@@ -792,7 +793,7 @@ void Engine::validate(const sr_run_config& c) const {
     if (!(c.pr_damping >= 0.0 && c.pr_damping < 1.0))
       throw EngineError(SR_E_CONFIG, "pagerank damping must be in [0, 1)");
   }
-  if (c.clock == SR_CLOCK_VIRTUAL && c.algo != SR_ALGO_PAGERANK && comm_)
+  if (c.clock == SR_CLOCK_VIRTUAL && c.algo != SR_ALGO_PAGERANK && attached())
     throw EngineError(SR_E_CONFIG, "virtual clock runs on a single device");
 }
 
@@ -826,7 +827,7 @@ void Engine::alloc_run_state(const sr_run_config& c) {
     blk_cnt_.reserve(nb + 1);
     blk_edges_.reserve(nb + 1);
     census_part_.reserve(size_t(nb + 1) * 13);
-    if (comm_) round_snap_.reserve(npad);
+    if (attached()) round_snap_.reserve(npad);
   }
   const size_t np = std::max<size_t>(pages_.size(), 1);
   // counter entries per pass: gated (reentry) runs keep one entry per page
@@ -1245,7 +1246,7 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
   // Source blocking pays for gathers only: once the previous dense pass
   // gathered for < 5 % of its edges (converged labels/levels skip theirs), the
   // per-block destination traffic would dominate -- sweep unblocked.
-  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && world_ == 1 && !comm_ &&
+  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && world_ == 1 && !attached() &&
       last_gather_frac_ >= 0.05 && pull_block_verts()) {
     if (pull_blocked_pass(gate, alloc_ctr(1))) {
       last_pass_blocked_ = true;
@@ -1420,7 +1421,7 @@ void Engine::build_push_list() {
 // and no weak-predictor bookkeeping needs the changed flags; a queue pass
 // starts from the compacted changed flags after a dense pass.
 bool Engine::queue_mode() const {
-  return !det_ && !comm_ && world_ == 1 && predictor_ != SR_PRED_WEAK &&
+  return !det_ && !attached() && world_ == 1 && predictor_ != SR_PRED_WEAK &&
          !std::getenv("SERAPH_NO_FRONTIER_QUEUE");
 }
 
@@ -1475,7 +1476,22 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
 }
 
 void Engine::exchange_round(bool pagerank) {
-  if (!comm_) return;  // attached to a world (any size, incl. 1): merge every round
+  if (!attached()) return;  // attached to a world (any size, incl. 1): merge every round
+  SR_CUDA(cudaSetDevice(dev_));
+  if (loop_) {  // in-process loopback (tests): the same reductions through host memory
+    if (pagerank) {
+      loopback_allreduce(loop_, rank_, rank_b_.p, n_, kLoopF32, kLoopSum, cs_);
+      loopback_allreduce(loop_, rank_, contrib_b_.p, n_, kLoopF32, kLoopSum, cs_);
+    } else {
+      loopback_allreduce(loop_, rank_, values_.p, n_, kLoopU32, kLoopMin, cs_);
+      loopback_allreduce(loop_, rank_, &census_.p->min_changed, 1, kLoopU32, kLoopMin, cs_);
+    }
+    // every rank reduces the same number of counter entries (same schedule)
+    loopback_allreduce(loop_, rank_, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), kLoopU64,
+                       kLoopSum, cs_);
+    if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
+    return;
+  }
   ncclResult_t r = ncclSuccess;
   SR_CUDA(cudaSetDevice(dev_));
   const NcclApi& nc = nccl();
@@ -1609,7 +1625,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   auto begin_pass = [&]() {
     ctr_used_ = 0;
     SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
-    if (comm_)
+    if (attached())
       SR_CUDA(cudaMemcpyAsync(round_snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
   };
   auto after_census = [&]() {
@@ -1734,7 +1750,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   // round trip per pass); falls back to one host-driven pass when the device
   // or the configuration does not allow it.
   auto do_sparse_loop = [&]() -> bool {
-    if (det_ || comm_ || fq_ready_) return false;
+    if (det_ || attached() || fq_ready_) return false;
     if (coop_ok_ < 0) {
       int v = 0;
       cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev_);
@@ -1928,7 +1944,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 // ---------------------------------------------------------------------------
 bool Engine::build_src_blocks(uint64_t blk) {
   if (sb_.built && sb_.blk_verts == blk) return true;
-  if (!all_resident_ || world_ > 1 || comm_) return false;
+  if (!all_resident_ || world_ > 1 || attached()) return false;
   if (blk == 0 || n_ <= blk) return false;
   sb_.built = false;
   const uint32_t np = uint32_t(pages_.size());
@@ -2232,7 +2248,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   std::vector<uint32_t> ctr_begin;
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
     ctr_begin.push_back(ctr_used_);
-    if (comm_) {
+    if (attached()) {
       SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
       SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
     }
@@ -2398,6 +2414,14 @@ void Engine::flush_l2(uint64_t bytes) {
   l2_flush_.reserve(bytes);
   SR_CUDA(cudaMemsetAsync(l2_flush_.p, int(++flush_gen_ & 0xff), bytes, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
+}
+
+void Engine::attach_loopback(int rank, int world, const std::string& key) {
+  if (world < 1 || rank < 0 || rank >= world) throw EngineError(SR_E_CONFIG, "bad rank/world");
+  if (pages_loaded_) throw EngineError(SR_E_CONFIG, "attach must precede load_pages");
+  loop_ = loopback_group(key, world);
+  rank_ = rank;
+  world_ = world;
 }
 
 void Engine::attach_world(int rank, int world, const uint8_t id[128]) {

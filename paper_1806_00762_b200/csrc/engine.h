@@ -20,6 +20,8 @@
 
 namespace seraph {
 
+struct LoopbackGroup;
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -147,6 +149,7 @@ class Engine {
                     uint32_t* in_src, uint32_t* in_w);
   void bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges);
   void attach_world(int rank, int world, const uint8_t id[128]);
+  void attach_loopback(int rank, int world, const std::string& key);
   void flush_l2(uint64_t bytes);
   DBuf<uint8_t> l2_flush_;
   unsigned flush_gen_ = 0;
@@ -341,6 +344,8 @@ class Engine {
   // multi-GPU
   int rank_ = 0, world_ = 1;
   ncclComm_t comm_ = nullptr;
+  LoopbackGroup* loop_ = nullptr;  // in-process loopback collective (tests)
+  bool attached() const { return comm_ != nullptr || loop_ != nullptr; }
   uint32_t own_lo_ = 0, own_hi_ = 0;  // owned destination range
 };
 

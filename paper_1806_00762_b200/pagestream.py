@@ -668,6 +668,11 @@ class Engine:
         return (CsrGraph(n, out_off, nbr, ow),
                 pages_from_csc(n, cap, in_off, srcs, iw, local), in_off, srcs, iw)
 
+    def attach_loopback(self, rank: int, world: int, group: str) -> None:
+        """Test/dev: rank of an in-process world whose exchange goes through host
+        memory (sr_attach_loopback); drive each rank's run() from its own thread."""
+        N.check(N.lib.sr_attach_loopback(self._h, rank, world, group.encode()), self._h)
+
     def attach_world(self, rank: int, world: int, unique_id: bytes) -> None:
         uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         N.check(N.lib.sr_attach_world(self._h, rank, world, C.byref(uid)), self._h)
