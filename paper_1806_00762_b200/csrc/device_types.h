@@ -168,23 +168,5 @@ struct TailArgs {
   TailResult* res;      // (mapped host memory)
 };
 
-// Persistent sparse stage (K3+K4 fused): consecutive sparse passes on the
-// device, leaving when the frontier is empty or dense enough for a pull.
-struct SparseLoopArgs {
-  PushArgs push;            // n_list / total_edges are taken per pass on device
-  uint32_t n, own_lo, own_hi;
-  const uint32_t* outdeg;
-  uint8_t* status;          // weak predictor (log bookkeeping) or null
-  uint8_t* logstate;
-  uint32_t* blk_cnt;
-  unsigned long long* blk_edges;
-  Census* cz_run;           // run record: last census on entry, accumulators
-  Census* cz_pass;          // [max_passes] per-pass census records (zeroed)
-  RunCtr* pass_ctr;         // [max_passes] push counters (zeroed)
-  uint32_t max_passes;
-  int force_sparse;         // ExecutionPolicy::ForceSparse
-  double dense_threshold;   // density_threshold_fraction * |E|
-  unsigned* result;         // [0] passes done, [1] exit reason (0 empty, 1 dense, 2 cap)
-};
 
 }  // namespace seraph

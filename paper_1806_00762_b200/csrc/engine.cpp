@@ -1746,89 +1746,6 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     ++pass_index;
   };
 
-  // Consecutive sparse passes in one persistent cooperative launch (no host
-  // round trip per pass); falls back to one host-driven pass when the device
-  // or the configuration does not allow it.
-  auto do_sparse_loop = [&]() -> bool {
-    if (det_ || attached() || fq_ready_) return false;
-    if (coop_ok_ < 0) {
-      int v = 0;
-      cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev_);
-      // measured neutral on C1/C2 (the per-pass cost is the O(|V|) census and
-      // compaction work, not the host round trip): opt-in via SERAPH_SPARSE_LOOP=1
-      const char* e = std::getenv("SERAPH_SPARSE_LOOP");
-      coop_ok_ = v && sparse_loop_blocks(algo_) > 0 && e && std::atoi(e) != 0;
-    }
-    if (!coop_ok_) return false;
-    constexpr uint32_t kMaxLoop = 256;
-    loop_cz_.reserve(kMaxLoop);
-    loop_ctr_.reserve(kMaxLoop);
-    loop_res_.reserve(2);
-    loop_cz_h_.reserve(kMaxLoop);
-    loop_ctr_h_.reserve(kMaxLoop);
-    loop_res_h_.reserve(2);
-    SR_CUDA(cudaMemsetAsync(loop_cz_.p, 0, kMaxLoop * sizeof(Census), cs_));
-    SR_CUDA(cudaMemsetAsync(loop_ctr_.p, 0, kMaxLoop * sizeof(RunCtr), cs_));
-    SparseLoopArgs L{};
-    L.push.list = list_.p;
-    L.push.pref = pref_.p;
-    L.push.chunk_start = chunk_start_.p;
-    L.push.out_offsets = out_off_.p;
-    L.push.out_neighbors = out_nbr_.p;
-    L.push.out_weights = csr_weighted_ ? out_w_.p : nullptr;
-    L.push.values = values_.p;
-    L.push.next = values_.p;
-    L.push.changed = changed_.p;
-    L.push.ctr = nullptr;
-    L.push.census = census_.p;
-    L.n = n_;
-    L.own_lo = own_lo_;
-    L.own_hi = own_hi_;
-    L.outdeg = outdeg_.p;
-    L.status = weak ? status_.p : nullptr;
-    L.logstate = weak ? logstate_.p : nullptr;
-    L.blk_cnt = blk_cnt_.p;
-    L.blk_edges = blk_edges_.p;
-    L.cz_run = census_.p;
-    L.cz_pass = loop_cz_.p;
-    L.pass_ctr = loop_ctr_.p;
-    L.max_passes = kMaxLoop;
-    L.force_sparse = cfg.execution == SR_EXEC_FORCE_SPARSE;
-    L.dense_threshold = cfg.density_threshold_fraction * double(m_);
-    L.result = loop_res_.p;
-    const int grid = sm_count_ * sparse_loop_blocks(algo_);
-    SR_CUDA(launch_sparse_loop(algo_, L, grid, cs_));
-    SR_CUDA(cudaMemcpyAsync(loop_res_h_.p, loop_res_.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, cs_));
-    SR_CUDA(cudaMemcpyAsync(loop_cz_h_.p, loop_cz_.p, kMaxLoop * sizeof(Census), cudaMemcpyDeviceToHost, cs_));
-    SR_CUDA(cudaMemcpyAsync(loop_ctr_h_.p, loop_ctr_.p, kMaxLoop * sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
-    SR_CUDA(cudaStreamSynchronize(cs_));
-    const uint32_t done = loop_res_h_.p[0];
-    for (uint32_t i = 0; i < done; ++i) {
-      const RunCtr& rc = loop_ctr_h_.p[i];
-      sr_pass_stats st{};
-      st.pass_index = pass_index;
-      st.kind = SR_PASS_SPARSE_PUSH;
-      st.attempts = rc.attempts;
-      st.valid_updates = rc.valid;
-      st.skipped = rc.skipped;
-      st.edges_read = rc.edges;
-      st.changed_vertices = loop_cz_h_.p[i].changed;
-      account(st);
-      m.sparse_passes += 1;
-      ++pass_index;
-    }
-    if (done) {
-      // the run record carries the last census (per-pass fields) forward
-      const Census& last = loop_cz_h_.p[done - 1];
-      SR_CUDA(cudaMemcpyAsync(census_.p, &loop_cz_.p[done - 1], kCensusResetBytes,
-                              cudaMemcpyDeviceToDevice, cs_));
-      std::memcpy(census_h_.p, &last, kCensusResetBytes);
-      f_count = last.changed;
-      f_out = last.out_edges;
-      for (int k = 0; k < 6; ++k) hist[k] = last.status_hist[k];
-    }
-    return true;
-  };
 
   auto do_dense = [&]() {
     // Runner::run_dense (engine.cpp:279-337)
@@ -1906,7 +1823,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
       continue;
     }
     if (sparse) {
-      if (!do_sparse_tail() && !do_sparse_loop()) do_sparse();
+      if (!do_sparse_tail()) do_sparse();
       prev_dense = false;
     } else {
       do_dense();

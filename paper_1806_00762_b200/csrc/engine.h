@@ -332,13 +332,6 @@ class Engine {
   bool l2_window_set_ = false;
   int l2_bytes_ = 0;
   // persistent sparse stage buffers
-  DBuf<Census> loop_cz_;
-  DBuf<RunCtr> loop_ctr_;
-  DBuf<unsigned> loop_res_;
-  PinBuf<Census> loop_cz_h_;
-  PinBuf<RunCtr> loop_ctr_h_;
-  PinBuf<unsigned> loop_res_h_;
-  int coop_ok_ = -1;
   void pr_blocked_pass(float base, float damp);
 
   // multi-GPU

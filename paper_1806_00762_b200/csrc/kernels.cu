@@ -11,7 +11,6 @@
 // The path is sparse and irregular: no tensor cores.  Everything is sized
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
-#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -1345,66 +1344,6 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_l
                 chunk_start);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent sparse stage: scan -> compaction -> push -> census -> density
-// decision, repeated on the device with grid-wide barriers (cooperative
-// launch), so consecutive sparse passes (engine.cpp:265-277 loop) cost no
-// host round trip.  Cross-block data is read through L2 (__ldcg): L1 is not
-// coherent across SMs inside one persistent launch.
-// ---------------------------------------------------------------------------
-template <int A>
-__global__ void __launch_bounds__(kBlockThreads) sparse_loop_kernel(SparseLoopArgs L) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
-  const uint32_t nchunks = (L.n + kCensusBlockVerts - 1) / kCensusBlockVerts;
-  uint32_t done = 0, reason = 2;
-  for (uint32_t it = 0; it < L.max_passes; ++it) {
-    const Census* prev = it == 0 ? L.cz_run : L.cz_pass + (it - 1);
-    // (1) exclusive scan of the chunk counts left by the previous census
-    if (blockIdx.x == 0) scan_body(nchunks, L.blk_cnt, L.blk_edges);
-    grid.sync();
-    // (2) ordered compaction into the push list (clears the changed flags)
-    for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x)
-      compact_chunk(ch, L.n, L.own_lo, L.own_hi, L.push.changed, L.outdeg, L.blk_cnt,
-                    L.blk_edges, const_cast<uint32_t*>(L.push.list),
-                    const_cast<unsigned long long*>(L.push.pref),
-                    const_cast<uint32_t*>(L.push.chunk_start));
-    grid.sync();
-    // (3) push
-    PushArgs pa = L.push;
-    pa.n_list = uint32_t(__ldcg(&prev->own_push));
-    pa.total_edges = __ldcg(&prev->own_edges);
-    LaneCtr c;
-    c.clear();
-    uint32_t lane_min = kUnreached;
-    push_body<A, false>(pa, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
-                        gridDim.x * kWarpsPerBlock, c, lane_min);
-    block_flush(c, L.pass_ctr + it, lane_min, L.cz_run, s_scratch);
-    grid.sync();
-    // (4) census of the new frontier
-    census_body(L.n, L.push.changed, L.status, L.logstate, L.outdeg, kPassSparse, L.own_lo,
-                L.own_hi, L.blk_cnt, L.blk_edges, L.cz_pass + it, L.cz_run, blockIdx.x,
-                gridDim.x);
-    grid.sync();
-    // (5) density_switch (engine.cpp:56-61), identical in every thread
-    done = it + 1;
-    const unsigned long long changed = __ldcg(&L.cz_pass[it].changed);
-    const unsigned long long out_edges = __ldcg(&L.cz_pass[it].out_edges);
-    if (changed == 0) {
-      reason = 0;
-      break;
-    }
-    if (!L.force_sparse && double(out_edges) > L.dense_threshold) {
-      reason = 1;
-      break;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    L.result[0] = done;
-    L.result[1] = reason;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K6: strong CC threshold.  The reference keeps exact per-label counts and
@@ -1766,25 +1705,6 @@ void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s
   }
 }
 
-int sparse_loop_blocks(int algo) {
-  int nb = 0;
-  if (algo == kSssp)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kSssp>, kBlockThreads, 0);
-  else if (algo == kCc)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kCc>, kBlockThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sparse_loop_kernel<kBfs>, kBlockThreads, 0);
-  return nb;
-}
-
-cudaError_t launch_sparse_loop(int algo, const SparseLoopArgs& a, int grid, cudaStream_t s) {
-  void* args[] = {const_cast<SparseLoopArgs*>(&a)};
-  const void* fn = algo == kSssp ? (const void*)sparse_loop_kernel<kSssp>
-                   : algo == kCc ? (const void*)sparse_loop_kernel<kCc>
-                                 : (const void*)sparse_loop_kernel<kBfs>;
-  note_launch();
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, 0, s);
-}
 
 void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
                         uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s) {

@@ -28,8 +28,6 @@ void launch_inv_outdeg(const unsigned long long* out_offsets, uint32_t n, float*
 // K3: sparse push over the compacted frontier.
 void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s);
 // Persistent sparse stage (cooperative launch): occupancy and launcher.
-int sparse_loop_blocks(int algo);
-cudaError_t launch_sparse_loop(int algo, const SparseLoopArgs& a, int grid, cudaStream_t s);
 // Deterministic push commit: for changed v with next[v] < values[v].
 void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
                         uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s);
