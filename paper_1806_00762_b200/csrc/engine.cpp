@@ -1246,8 +1246,8 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
   // Source blocking pays for gathers only: once the previous dense pass
   // gathered for < 5 % of its edges (converged labels/levels skip theirs), the
   // per-block destination traffic would dominate -- sweep unblocked.
-  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && world_ == 1 && !attached() &&
-      last_gather_frac_ >= 0.05 && pull_block_verts()) {
+  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && last_gather_frac_ >= 0.05 &&
+      pull_block_verts()) {
     if (pull_blocked_pass(gate, alloc_ctr(1))) {
       last_pass_blocked_ = true;
       po.kernel_runs += order.size();
@@ -1861,14 +1861,15 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 // ---------------------------------------------------------------------------
 bool Engine::build_src_blocks(uint64_t blk) {
   if (sb_.built && sb_.blk_verts == blk) return true;
-  if (!all_resident_ || world_ > 1 || attached()) return false;
+  if (!all_resident_) return false;  // sharded ranks block their own destinations
   if (blk == 0 || n_ <= blk) return false;
   sb_.built = false;
   const uint32_t np = uint32_t(pages_.size());
   for (uint32_t p = 0; p < np; ++p)
     if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
   const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
-  const uint32_t n_tiles = pages_.back().tile_end;
+  uint32_t n_tiles = 0;  // a sharded rank holds tiles for its own pages only
+  for (const PageMeta& pm : pages_) n_tiles = std::max(n_tiles, pm.tile_end);
   const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
   auto stage = [&](const char* what) {
@@ -1922,7 +1923,8 @@ bool Engine::build_src_blocks(uint64_t blk) {
   tcnt.reserve(K + 1);
   tat.reserve(K + 1);
   SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));
-  launch_sub_tiles(0, n_, cap_, np, nb, sb_.offs.p, tcnt.p, nullptr, nullptr, nullptr, cs_);
+  launch_sub_tiles(0, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, tcnt.p, nullptr, nullptr,
+                   nullptr, cs_);
   launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, cs_);
   sb_.block_tile_begin.assign(nb + 1, 0);
   for (uint32_t b = 0; b <= nb; ++b)
@@ -1932,8 +1934,8 @@ bool Engine::build_src_blocks(uint64_t blk) {
   const uint32_t n_sub_tiles = sb_.block_tile_begin[nb];
   sb_.tiles.reserve(std::max<size_t>(n_sub_tiles, 1));
   sb_.tile_page.reserve(std::max<size_t>(n_sub_tiles, 1));
-  launch_sub_tiles(1, n_, cap_, np, nb, sb_.offs.p, nullptr, tat.p, sb_.tiles.p, sb_.tile_page.p,
-                   cs_);
+  launch_sub_tiles(1, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, nullptr, tat.p, sb_.tiles.p,
+                   sb_.tile_page.p, cs_);
   SR_CUDA(cudaGetLastError());
   stage("offsets + tile cut");
   std::vector<PageDesc> desc(size_t(nb) * np);
@@ -2140,7 +2142,8 @@ void Engine::pr_blocked_pass(float base, float damp) {
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
   }
-  launch_pr_block_finalize(n_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p, base, damp, cs_);
+  launch_pr_block_finalize(own_lo_, own_hi_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p,
+                           base, damp, cs_);
 }
 
 // ---------------------------------------------------------------------------

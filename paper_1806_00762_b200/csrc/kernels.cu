@@ -661,10 +661,11 @@ __global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __
   if (threadIdx.x == 0) bp_edges[pb] = s_carry;
 }
 
-__global__ void pr_block_finalize_kernel(uint32_t n, float* acc, float* rank_out, float* contrib_out,
-                                         const float* __restrict__ inv_outdeg, float base,
-                                         float damp) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+__global__ void pr_block_finalize_kernel(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
+                                         float* contrib_out, const float* __restrict__ inv_outdeg,
+                                         float base, float damp) {
+  for (uint32_t v = lo + blockIdx.x * blockDim.x + threadIdx.x; v < hi;
+       v += gridDim.x * blockDim.x) {
     const float r = base + damp * acc[v];
     rank_out[v] = r;
     contrib_out[v] = r * inv_outdeg[v];
@@ -1799,6 +1800,7 @@ __global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages
 // ---------------------------------------------------------------------------
 struct SubCut {
   uint32_t n, cap, n_pages, wpp;  // wpp: 128-destination windows per page
+  uint32_t own_lo, own_hi;        // this rank's destinations (global ids)
   const uint32_t* offs;  // [n_blocks][n + n_pages] sub-page local offsets
 };
 
@@ -1812,8 +1814,11 @@ __global__ void sub_tiles_kernel(int mode, SubCut c, uint32_t n_blocks, uint32_t
        k += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t bp = uint32_t(k / c.wpp), w = uint32_t(k % c.wpp);
     const uint32_t b = bp / c.n_pages, p = bp % c.n_pages;
-    const uint32_t range = min(c.cap, c.n - p * c.cap);
-    const uint32_t lo = w * kTileMaxDests, hi = min(lo + kTileMaxDests, range);
+    const uint32_t vb = p * c.cap, range = min(c.cap, c.n - vb);
+    // the window, clipped to this rank's destination range
+    const uint32_t lo = max(w * kTileMaxDests, c.own_lo > vb ? min(c.own_lo - vb, range) : 0u);
+    const uint32_t hi = min(min(w * kTileMaxDests + kTileMaxDests, range),
+                            c.own_hi > vb ? min(c.own_hi - vb, range) : 0u);
     const uint32_t* o = c.offs + size_t(b) * (size_t(c.n) + c.n_pages) + size_t(p) * c.cap + p;
     uint32_t t = mode ? at[k] : 0u;
     uint32_t i = lo;
@@ -1847,11 +1852,11 @@ __global__ void sub_tiles_kernel(int mode, SubCut c, uint32_t n_blocks, uint32_t
 }
 
 void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
-                      const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
-                      uint4* tiles, uint32_t* tile_page, cudaStream_t s) {
+                      uint32_t own_lo, uint32_t own_hi, const uint32_t* offs, uint32_t* cnt,
+                      const uint32_t* at, uint4* tiles, uint32_t* tile_page, cudaStream_t s) {
   if (!n || !n_blocks) return;
   const uint32_t wpp = (cap + kTileMaxDests - 1) / kTileMaxDests;
-  const SubCut c{n, cap, n_pages, wpp, offs};
+  const SubCut c{n, cap, n_pages, wpp, own_lo, own_hi, offs};
   note_launch();
   sub_tiles_kernel<<<grid_for(uint64_t(n_blocks) * n_pages * wpp, 256), 256, 0, s>>>(
       mode, c, n_blocks, cnt, at, tiles, tile_page);
@@ -1921,12 +1926,14 @@ void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const 
   src_block_scan_kernel<<<n_pages * n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges);
 }
 
-void launch_pr_block_finalize(uint32_t n, float* acc, float* rank_out, float* contrib_out,
-                              const float* inv_outdeg, float base, float damp, cudaStream_t s) {
-  if (!n) return;
+void launch_pr_block_finalize(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
+                              float* contrib_out, const float* inv_outdeg, float base, float damp,
+                              cudaStream_t s) {
+  if (hi <= lo) return;
   note_launch();
-  pr_block_finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, acc, rank_out, contrib_out,
-                                                            inv_outdeg, base, damp);
+  pr_block_finalize_kernel<<<grid_for(hi - lo, 256), 256, 0, s>>>(lo, hi, acc, rank_out,
+                                                                   contrib_out, inv_outdeg, base,
+                                                                   damp);
 }
 
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s) {

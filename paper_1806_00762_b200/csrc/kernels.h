@@ -69,8 +69,8 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
 // exclusive scan `at` of those counts.
 uint64_t sub_tile_windows(uint32_t cap, uint32_t n_pages, uint32_t n_blocks);
 void launch_sub_tiles(int mode, uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
-                      const uint32_t* offs, uint32_t* cnt, const uint32_t* at,
-                      uint4* tiles, uint32_t* tile_page, cudaStream_t s);
+                      uint32_t own_lo, uint32_t own_hi, const uint32_t* offs, uint32_t* cnt,
+                      const uint32_t* at, uint4* tiles, uint32_t* tile_page, cudaStream_t s);
 constexpr uint32_t kDegHistCap = 1024;  // degrees >= cap share the last histogram bucket
 void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* hist_v,
                         unsigned long long* hist_e, cudaStream_t s);
@@ -94,8 +94,9 @@ void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t 
 void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
                            uint32_t n_pages, uint32_t n_blocks, uint32_t n,
                            unsigned long long* bp_edges, cudaStream_t s);
-void launch_pr_block_finalize(uint32_t n, float* acc, float* rank_out, float* contrib_out,
-                              const float* inv_outdeg, float base, float damp, cudaStream_t s);
+void launch_pr_block_finalize(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
+                              float* contrib_out, const float* inv_outdeg, float base, float damp,
+                              cudaStream_t s);
 // Values initialisation (VertexProgram::init, programs.hpp:20-28).
 void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
                         cudaStream_t s);

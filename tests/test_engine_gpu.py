@@ -784,13 +784,18 @@ def _run_world(world, g, prog, cfg, cap, key):
     return out
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_rounds_loopback_world(world):
+@pytest.mark.parametrize("world,blocked", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_rounds_loopback_world(world, blocked, monkeypatch):
     """The multi-GPU round protocol of sr_attach_world (edge-balanced
     destination shards, per-round merge of the replicated values, identical
     decisions on every rank) run on hardware: `world` contexts on one GPU,
     the exchange through the in-process loopback collective instead of NCCL.
-    Every rank ends with the oracle's values (PageRank within 1e-6)."""
+    Every rank ends with the oracle's values (PageRank within 1e-6); with
+    `blocked` every rank sweeps its own destinations through source-blocked
+    sub-pages (K1 and K8)."""
+    if blocked:
+        monkeypatch.setenv("SERAPH_PULL_BLOCK_VERTS", "700")
+        monkeypatch.setenv("SERAPH_PR_BLOCK_VERTS", "3000")
     n = 1 << 13
     src, dst = O.generate_rmat(13, 16, seed=23)
     w = O.assign_weights(src.size, 4, 1, 64)
@@ -805,13 +810,13 @@ def test_sharded_rounds_loopback_world(world):
                 k += 1
                 res = _run_world(world, g, program_for(kind, 2, g),
                                  cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex),
-                                 n // 16, f"w{world}-{k}")
+                                 n // 16, f"w{world}-{int(blocked)}-{k}")
                 for r in res:
                     assert np.array_equal(r.values, want), (kind, pred, ex)
                 assert len({r.metrics.passes for r in res}) == 1  # same decisions
     pr = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
     res = _run_world(world, pr, ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL),
-                     n // 16, f"w{world}-pr")
+                     n // 16, f"w{world}-{int(blocked)}-pr")
     ref = O.pagerank(n, src, dst, 20, 0.85)
     for r in res:
         assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
