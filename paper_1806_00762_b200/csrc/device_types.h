@@ -131,6 +131,7 @@ struct PushArgs {
   uint32_t epoch;
   uint32_t* q_list;
   const uint32_t* outdeg;
+  uint8_t* logstate;  // weak predictor: PredictionLog of first-time changes (else null)
 };
 constexpr uint32_t kPushChunk = 256;  // flattened edges per warp task
 
@@ -164,6 +165,7 @@ struct TailArgs {
   double dense_threshold;  // density_switch: dense iff out-edges > this
   int force_sparse;
   Census* census;       // strong-predictor min_changed accumulator
+  uint8_t* logstate;    // weak predictor: PredictionLog of first-time changes (else null)
   TailRecord* rec;      // [max_passes] (mapped host memory)
   TailResult* res;      // (mapped host memory)
 };

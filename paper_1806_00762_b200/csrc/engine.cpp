@@ -1421,7 +1421,7 @@ void Engine::build_push_list() {
 // and no weak-predictor bookkeeping needs the changed flags; a queue pass
 // starts from the compacted changed flags after a dense pass.
 bool Engine::queue_mode() const {
-  return !det_ && !attached() && world_ == 1 && predictor_ != SR_PRED_WEAK &&
+  return !det_ && !attached() && world_ == 1 &&
          !std::getenv("SERAPH_NO_FRONTIER_QUEUE");
 }
 
@@ -1464,6 +1464,7 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
       a.epoch = fq_epoch_;
       a.q_list = list2_.p;
       a.outdeg = outdeg_.p;
+      a.logstate = predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr;
     }
     const uint64_t chunks = (total + kPushChunk - 1) / kPushChunk;
     const int grid = int(std::max<uint64_t>(
@@ -1581,7 +1582,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   l_sssp_ = 0;
   last_gather_frac_ = 1.0;  // the first dense pass gathers
   ctr_used_ = 0;
-  if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_) {
+  if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_ && !weak) {  // weak: census seeds the DFA histogram
     // the initial frontier {source} directly as a queue
     SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
     launch_seed_queue(source_, outdeg_.p, list_.p, census_.p, cs_);
@@ -1692,6 +1693,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     t.dense_threshold = cfg.density_threshold_fraction * double(m_);
     t.force_sparse = cfg.execution == SR_EXEC_FORCE_SPARSE ? 1 : 0;
     t.census = census_.p;
+    t.logstate = predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr;
     t.rec = tail_rec_.p;
     t.res = tail_res_.p;
     launch_tail_loop(algo_, t, cs_);

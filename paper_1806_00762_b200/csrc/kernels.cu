@@ -885,8 +885,17 @@ __global__ void inv_outdeg_kernel(const unsigned long long* off, uint32_t n, flo
 // frontier list / prefix / chunk starts are read through L2 (__ldcg) because
 // the persistent loop rewrites them every pass from other SMs.
 struct QueueCtr {
-  unsigned long long changed, out_edges;
+  unsigned long long changed, out_edges, log_incorrect;
 };
+
+// PredictionLog::record_change (predictor.cpp:107-138) for a vertex that
+// changed: a pending "converged" prediction on it was wrong.
+__device__ __forceinline__ void log_first_change(uint8_t* logstate, uint32_t v,
+                                                 unsigned long long& incorrect) {
+  const uint8_t ls = logstate[v];
+  if (ls & 8) ++incorrect;
+  logstate[v] = 4;  // fails=0, armed, no pending
+}
 
 template <int A, bool DET>
 __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32_t nw, LaneCtr& c,
@@ -945,6 +954,7 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
             if (a.stamp) {
               if (atomicMax(a.stamp + v, a.epoch) < a.epoch) {  // first change this pass
                 const uint32_t d = __ldg(a.outdeg + v);
+                if (a.logstate) log_first_change(a.logstate, v, qc->log_incorrect);
                 qc->changed += 1;
                 qc->out_edges += d;
                 app = d > 0;
@@ -985,25 +995,30 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
 template <int A, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
   __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
-  __shared__ unsigned long long s_q[2][kWarpsPerBlock];
+  __shared__ unsigned long long s_q[3][kWarpsPerBlock];
   LaneCtr c;
   c.clear();
-  QueueCtr qc{0, 0};
+  QueueCtr qc{0, 0, 0};
   uint32_t lane_min = kUnreached;
   push_body<A, DET>(a, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
                     gridDim.x * kWarpsPerBlock, c, lane_min, &qc);
   if (a.stamp) {  // next-frontier size and out-edge volume: one atomic per block
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned long long ch = warp_sum(qc.changed), oe = warp_sum(qc.out_edges);
+    const unsigned long long ch = warp_sum(qc.changed), oe = warp_sum(qc.out_edges),
+                             li = warp_sum(qc.log_incorrect);
     if (lane == 0) {
       s_q[0][w] = ch;
       s_q[1][w] = oe;
+      s_q[2][w] = li;
     }
     __syncthreads();
-    if (threadIdx.x < 2) {
+    if (threadIdx.x < 3) {
       unsigned long long t = 0;
       for (int k = 0; k < kWarpsPerBlock; ++k) t += s_q[threadIdx.x][k];
-      if (t) atomicAdd(threadIdx.x == 0 ? &a.census->changed : &a.census->out_edges, t);
+      unsigned long long* dst = threadIdx.x == 0 ? &a.census->changed
+                                : threadIdx.x == 1 ? &a.census->out_edges
+                                                   : &a.census->log_incorrect;
+      if (t) atomicAdd(dst, t);
     }
   }
   block_flush(c, a.ctr, lane_min, a.census, s_scratch);
@@ -1556,7 +1571,7 @@ __global__ void __launch_bounds__(1024) tail_loop_kernel(TailArgs t) {
     __syncthreads();
     const uint32_t total = s_pref[q];
     // relax every out-edge of the queue
-    unsigned long long valid = 0, changed = 0, out_next = 0;
+    unsigned long long valid = 0, changed = 0, out_next = 0, log_inc = 0;
     const uint32_t epoch = t.epoch0 + pass;
     for (uint32_t e = tid; e < total; e += blockDim.x) {
       uint32_t lo = 0, hi = q - 1;  // last entry with s_pref <= e
@@ -1577,6 +1592,7 @@ __global__ void __launch_bounds__(1024) tail_loop_kernel(TailArgs t) {
           lane_min = min(lane_min, cand);
           if (atomicMax(t.stamp + v, epoch) < epoch) {
             const uint32_t dv = __ldg(t.outdeg + v);
+            if (t.logstate) log_first_change(t.logstate, v, log_inc);
             changed += 1;
             out_next += dv;
             if (dv) nxt[atomicAdd(&s_qn, 1u)] = v;  // the scratch queue holds |V|
@@ -1584,14 +1600,16 @@ __global__ void __launch_bounds__(1024) tail_loop_kernel(TailArgs t) {
         }
       }
     }
-    const unsigned long long vals[3] = {warp_sum(valid), warp_sum(changed), warp_sum(out_next)};
+    const unsigned long long vals[4] = {warp_sum(valid), warp_sum(changed), warp_sum(out_next),
+                                        warp_sum(log_inc)};
     if (lane == 0)
-      for (int k = 0; k < 3; ++k) s_red[k][warp] = vals[k];
+      for (int k = 0; k < 4; ++k) s_red[k][warp] = vals[k];
     __syncthreads();
     if (tid == 0) {
-      unsigned long long tot[3] = {0, 0, 0};
+      unsigned long long tot[4] = {0, 0, 0, 0};
       for (int w = 0; w < int(blockDim.x >> 5); ++w)
-        for (int k = 0; k < 3; ++k) tot[k] += s_red[k][w];
+        for (int k = 0; k < 4; ++k) tot[k] += s_red[k][w];
+      if (tot[3]) atomicAdd(&t.census->log_incorrect, tot[3]);
       TailRecord r;
       r.edges = total;
       r.valid = tot[0];

@@ -705,7 +705,7 @@ def test_frontier_queue_matches_flag_path(monkeypatch):
             eng.load(*built(g, n // 16))
             for kind in kinds:
                 want = oracle_values(g, kind, 3)
-                for pred in (ps.PredictorMode.OFF, ps.PredictorMode.STRONG):
+                for pred in PREDS:
                     for ex in (ps.ExecutionPolicy.DENSITY_SWITCHED, ps.ExecutionPolicy.FORCE_SPARSE):
                         c = cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex)
                         prog = program_for(kind, 3, g)
@@ -717,6 +717,11 @@ def test_frontier_queue_matches_flag_path(monkeypatch):
                         monkeypatch.setenv("SERAPH_NO_FRONTIER_QUEUE", "1")
                         rf = eng.run(prog, c)
                         monkeypatch.delenv("SERAPH_NO_FRONTIER_QUEUE")
+                        if pred == ps.PredictorMode.WEAK:  # PredictionLog kept by the queue path
+                            aq, af = rq.metrics.prediction_accuracy, rf.metrics.prediction_accuracy
+                            assert (aq is None) == (af is None)
+                            if aq is not None:
+                                assert abs(aq - af) < 0.05
                         for r in (rq, rn, rf):
                             assert np.array_equal(r.values, want), (kind, pred, ex)
                             assert len(r.metrics.per_pass) == r.metrics.passes
