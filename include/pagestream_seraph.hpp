@@ -9,8 +9,10 @@
 // reference's exception classes (proj/include/pagestream/errors.hpp:8-28).
 #pragma once
 
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "pagestream/engine.hpp"
@@ -149,6 +151,65 @@ inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProg
       r.trace.push_back(TraceEvent{e.time, TraceEventKind(e.kind), e.page_id, e.pass_index});
   }
   return r;
+}
+
+// build_csr + build_csc_pages (graph.cpp:30-94) on the GPU (sr_build_graph:
+// stable radix sorts, bit-identical arrays), returned as the reference's own
+// types.  Same validation and exception classes as EdgeList::validate.
+inline std::pair<CsrGraph, PageSet> build_graph(const EdgeList& el,
+                                                VertexId page_vertex_capacity, int device = 0) {
+  if (page_vertex_capacity < 1) throw ConfigError("page_vertex_capacity must be >= 1");
+  el.validate();  // InputError on the host, as the reference builders do
+  const uint64_t m = el.num_edges();
+  std::vector<uint32_t> src(m), dst(m);
+  for (uint64_t i = 0; i < m; ++i) {
+    src[i] = el.edges[i].src;
+    dst[i] = el.edges[i].dst;
+  }
+  const bool weighted = el.weighted();
+  DeviceContext& dc = device_context(device);
+  std::lock_guard<std::mutex> lk(dc.mu);
+  int rc = sr_build_graph(dc.ctx, el.num_vertices, m, src.data(), dst.data(),
+                          weighted ? el.weights.data() : nullptr, page_vertex_capacity,
+                          SR_BUILD_CSR_EDGES);
+  if (rc != SR_OK) rethrow(rc, sr_last_error(dc.ctx));
+  std::pair<CsrGraph, PageSet> out;
+  CsrGraph& csr = out.first;
+  PageSet& ps = out.second;
+  const uint32_t n = el.num_vertices;
+  csr.num_vertices = n;
+  csr.out_offsets.resize(size_t(n) + 1);
+  csr.out_neighbors.resize(m);
+  if (weighted) csr.out_weights.resize(m);
+  std::vector<uint64_t> in_off(size_t(n) + 1);
+  std::vector<uint32_t> in_src(m), in_w(weighted ? m : 0);
+  rc = sr_export_graph(dc.ctx, csr.out_offsets.data(), csr.out_neighbors.data(),
+                       weighted ? csr.out_weights.data() : nullptr, in_off.data(), in_src.data(),
+                       weighted ? in_w.data() : nullptr);
+  if (rc != SR_OK) rethrow(rc, sr_last_error(dc.ctx));
+  ps.num_vertices = n;
+  ps.page_vertex_capacity = page_vertex_capacity;
+  ps.weighted = weighted;
+  for (uint64_t vb = 0; vb < n; vb += page_vertex_capacity) {
+    const uint64_t ve = std::min<uint64_t>(vb + page_vertex_capacity, n);
+    CscPage pg;
+    pg.vertex_begin = VertexId(vb);
+    pg.vertex_end = VertexId(ve);
+    pg.in_offsets.resize(ve - vb + 1);
+    for (uint64_t v = vb; v <= ve; ++v) pg.in_offsets[v - vb] = uint32_t(in_off[v] - in_off[vb]);
+    pg.in_sources.assign(in_src.begin() + in_off[vb], in_src.begin() + in_off[ve]);
+    if (weighted) pg.in_weights.assign(in_w.begin() + in_off[vb], in_w.begin() + in_off[ve]);
+    ps.pages.push_back(std::move(pg));
+  }
+  return out;
+}
+
+inline CsrGraph build_csr(const EdgeList& el, int device = 0) {
+  return build_graph(el, std::max<VertexId>(el.num_vertices, 1), device).first;
+}
+
+inline PageSet build_csc_pages(const EdgeList& el, VertexId page_vertex_capacity, int device = 0) {
+  return build_graph(el, page_vertex_capacity, device).second;
 }
 
 }  // namespace pagestream::seraph

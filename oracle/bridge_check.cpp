@@ -65,6 +65,44 @@ int main() {
         }
     }
   }
+  // device-side builders: seraph::build_csr / build_csc_pages == the reference's
+  for (int iter = 0; iter < 20; ++iter) {
+    EdgeList el = random_edges(rng, 300, 3000);
+    if (iter % 2) el.weights.clear();
+    const VertexId cap = VertexId(rng() % 50 + 1);
+    CsrGraph a = build_csr(el), b = seraph::build_csr(el);
+    PageSet pa = build_csc_pages(el, cap), pb = seraph::build_csc_pages(el, cap);
+    bool same = a.out_offsets == b.out_offsets && a.out_neighbors == b.out_neighbors &&
+                a.out_weights == b.out_weights && pa.pages.size() == pb.pages.size() &&
+                pa.weighted == pb.weighted;
+    for (size_t i = 0; same && i < pa.pages.size(); ++i)
+      same = pa.pages[i].vertex_begin == pb.pages[i].vertex_begin &&
+             pa.pages[i].vertex_end == pb.pages[i].vertex_end &&
+             pa.pages[i].in_offsets == pb.pages[i].in_offsets &&
+             pa.pages[i].in_sources == pb.pages[i].in_sources &&
+             pa.pages[i].in_weights == pb.pages[i].in_weights;
+    ++cases;
+    if (!same) {
+      ++fails;
+      std::printf("BUILD MISMATCH iter %d\n", iter);
+    }
+  }
+  {  // InputError for an out-of-range endpoint, as EdgeList::validate
+    EdgeList bad;
+    bad.num_vertices = 2;
+    bad.edges = {{0, 5}};
+    bool threw_input = false;
+    try {
+      seraph::build_csr(bad);
+    } catch (const InputError&) {
+      threw_input = true;
+    }
+    ++cases;
+    if (!threw_input) {
+      ++fails;
+      std::printf("InputError not raised by seraph::build_csr\n");
+    }
+  }
   // exception mapping (errors.hpp): invalid window -> ConfigError
   bool threw = false;
   try {
