@@ -113,7 +113,8 @@ int sr_device_query(int device, sr_device_info* out) {
     out->cc_minor = prop.minor;
     out->total_mem = tot;
     out->free_mem = fr;
-    std::strncpy(out->name, prop.name, sizeof(out->name) - 1);
+    const size_t len = strnlen(prop.name, sizeof(out->name) - 1);  // name stays NUL-terminated
+    std::memcpy(out->name, prop.name, len);
   });
 }
 

@@ -1253,6 +1253,10 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
       po.kernel_runs += order.size();
       return po;
     }
+    --ctr_used_;  // the (zeroed) probe slot is the first one the unblocked steps take
+    // a probed pass falls back after block 0 already applied some updates:
+    // count valid updates as the destinations changed in the pass
+    last_pass_blocked_ = sb_.built && pull_block_verts() != 0;
   }
 
   for (size_t si = 0; si < steps.size(); ++si) {
@@ -2087,6 +2091,20 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    if (b == 0 && sb_.n_blocks > 1) {
+      // Probe: blocking pays for gathers only.  If block 0 gathered for < 5 %
+      // of its edges (converged labels/levels skip theirs), finish the pass
+      // with one unblocked sweep instead of n_blocks - 1 more destination
+      // passes (its relaxations are idempotent; the counters restart).
+      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+      SR_CUDA(cudaStreamSynchronize(cs_));
+      const RunCtr& c0 = ctr_h_.p[0];
+      if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
+        SR_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RunCtr), cs_));
+        l2_window(nullptr, 0);
+        return false;
+      }
+    }
   }
   l2_window(nullptr, 0);
   return true;
