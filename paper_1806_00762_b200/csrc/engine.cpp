@@ -1152,7 +1152,17 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
                                 uint32_t pass_index, bool pagerank) {
   cur_pass_ = pass_index;
   PassOut po;
-  const int mode = (recovery || pagerank) ? SR_SCHED_BASELINE : cfg.schedule;
+  // Double-buffer / pipelined(-fine) exist to overlap page transfers with
+  // compute (their re-runs fill the window while the next page is in flight,
+  // scheduler.cpp:293-390).  With the whole page set resident there is no
+  // transfer to hide, so the device-native schedule is the resident fast path
+  // (north_star: "becomes a resident-HBM fast path when partitions fit");
+  // ClockMode::Virtual keeps the reference's exact schedule.  Reentry keeps
+  // its meaning (re-run pages that still change: local convergence).
+  const bool resident_fast = !streaming() && (cfg.schedule == SR_SCHED_DOUBLE_BUFFER ||
+                                              cfg.schedule == SR_SCHED_PIPELINED ||
+                                              cfg.schedule == SR_SCHED_PIPELINED_FINE);
+  const int mode = (recovery || pagerank || resident_fast) ? SR_SCHED_BASELINE : cfg.schedule;
   const uint32_t B = cfg.window_capacity;
   // admission order: pages already on the device first (reference
   // scheduler.cpp:211-228), then the rest by id
