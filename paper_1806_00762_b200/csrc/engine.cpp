@@ -3,14 +3,10 @@
 // (proj/src/engine.cpp:225-416) decision for decision; all per-vertex work
 // runs in the sm_100a kernels of kernels.cu.
 #include "engine.h"
-#include "devgraph.h"
 #include "loopback.h"
 
 #include <algorithm>
 #include <chrono>
-#include <fcntl.h>
-#include <sys/stat.h>
-#include <unistd.h>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -172,257 +168,6 @@ void Engine::finish_csr(bool sync) {
   if (sync) SR_CUDA(cudaStreamSynchronize(xs_));
   has_csr_ = true;
   csr_derived_ = false;
-}
-
-// ---------------------------------------------------------------------------
-// Device-side graph build (devgraph.cu): the
-// reference's build_csr + build_csc_pages (graph.cpp:30-94) as stable radix
-// sorts on the GPU, then the normal residency path (tiles, arena, push
-// adjacency) with the page arrays copied device to device.
-// ---------------------------------------------------------------------------
-void Engine::build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<uint32_t>& dst,
-                             DBuf<uint32_t>& w, bool weighted, uint32_t cap, bool csr_edges) {
-  if (cap < 1) throw EngineError(SR_E_CONFIG, "page vertex capacity must be >= 1");
-  if (n == 0) throw EngineError(SR_E_INPUT, "graph has no vertices");
-  if (!dg_ids_valid(n, m, src.p, dst.p, cs_))
-    throw EngineError(SR_E_INPUT, "edge endpoint out of range (graph.cpp:9-22)");
-  const auto t0 = std::chrono::steady_clock::now();
-  const uint32_t np = uint32_t((uint64_t(n) + cap - 1) / cap);
-  DBuf<unsigned long long> in_off;
-  DBuf<uint32_t> in_src, in_w, local;
-  in_off.reserve(size_t(n) + 1);
-  in_src.reserve(std::max<uint64_t>(m, 1));
-  if (weighted) in_w.reserve(std::max<uint64_t>(m, 1));
-  dg_stable_adjacency(n, m, dst.p, src.p, weighted ? w.p : nullptr, in_off.p, in_src.p,
-                      weighted ? in_w.p : nullptr, cs_);
-  out_off_.reserve(size_t(n) + 1);
-  if (csr_edges) {
-    out_nbr_.reserve(std::max<uint64_t>(m, 1));
-    if (weighted) out_w_.reserve(std::max<uint64_t>(m, 1));
-  }
-  dg_stable_adjacency(n, m, src.p, csr_edges ? dst.p : nullptr, csr_edges && weighted ? w.p : nullptr,
-                      out_off_.p, csr_edges ? out_nbr_.p : nullptr,
-                      csr_edges && weighted ? out_w_.p : nullptr, cs_);
-  local.reserve(size_t(n) + np);
-  dg_page_offsets(n, cap, in_off.p, local.p, cs_);
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  src.release();
-  dst.release();
-  w.release();
-  n_ = n;
-  m_ = m;
-  has_csr_edges_ = csr_edges;
-  csr_weighted_ = csr_edges && weighted;
-  finish_csr();
-  PinBuf<uint32_t> local_h;
-  PinBuf<unsigned long long> in_off_h;
-  local_h.reserve(size_t(n) + np);
-  in_off_h.reserve(size_t(n) + 1);
-  SR_CUDA(cudaMemcpy(local_h.p, local.p, (size_t(n) + np) * 4, cudaMemcpyDeviceToHost));
-  SR_CUDA(cudaMemcpy(in_off_h.p, in_off.p, (size_t(n) + 1) * 8, cudaMemcpyDeviceToHost));
-  std::vector<sr_page_view> views(np);
-  for (uint32_t p = 0; p < np; ++p) {
-    const uint64_t vb = uint64_t(p) * cap, ve = std::min<uint64_t>(vb + cap, n);
-    const uint64_t e0 = in_off_h.p[vb], e1 = in_off_h.p[ve];
-    views[p] = sr_page_view{uint32_t(vb), uint32_t(ve), local_h.p + vb + p, in_src.p + e0,
-                            weighted ? in_w.p + e0 : nullptr, e1 - e0};
-  }
-  last_upload_seconds = 0;
-  last_upload_bytes = 0;
-  load_pages(n, cap, weighted, views.data(), np);  // device-to-device into the arena
-  SR_CUDA(cudaDeviceSynchronize());
-  last_upload_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-}
-
-void Engine::build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
-                         const uint32_t* w, uint32_t cap, bool csr_edges) {
-  SR_CUDA(cudaSetDevice(dev_));
-  if (m && (!src || !dst)) throw EngineError(SR_E_INPUT, "edge list: null endpoints");
-  DBuf<uint32_t> ds, dd, dw;
-  ds.reserve(std::max<uint64_t>(m, 1));
-  dd.reserve(std::max<uint64_t>(m, 1));
-  if (m) {
-    SR_CUDA(cudaMemcpyAsync(ds.p, src, m * 4, cudaMemcpyDefault, cs_));
-    SR_CUDA(cudaMemcpyAsync(dd.p, dst, m * 4, cudaMemcpyDefault, cs_));
-  }
-  if (w) {
-    dw.reserve(std::max<uint64_t>(m, 1));
-    if (m) SR_CUDA(cudaMemcpyAsync(dw.p, w, m * 4, cudaMemcpyDefault, cs_));
-  }
-  build_graph_dev(n, m, ds, dd, dw, w != nullptr, cap, csr_edges);
-}
-
-void Engine::generate_graph(const sr_graph_spec& g, bool csr_edges) {
-  SR_CUDA(cudaSetDevice(dev_));
-  if (g.scale < 1 || g.scale > 31 || g.edge_factor < 1)
-    throw EngineError(SR_E_CONFIG, "rmat: scale must be in [1, 31], edge factor >= 1");
-  const double sum = g.a + g.b + g.c + g.d;
-  if (g.a < 0 || g.b < 0 || g.c < 0 || g.d < 0 || sum < 1 - 1e-9 || sum > 1 + 1e-9)
-    throw EngineError(SR_E_CONFIG, "rmat quadrant probabilities must be >= 0 and sum to 1");
-  const bool weighted = g.weight_hi != 0;
-  if (weighted && (g.weight_lo < 1 || g.weight_lo > g.weight_hi))
-    throw EngineError(SR_E_CONFIG, "weights: need 1 <= lo <= hi");
-  const uint32_t n = uint32_t(uint64_t(1) << g.scale);
-  const uint64_t m0 = uint64_t(n) * g.edge_factor;
-  DBuf<uint32_t> s0, d0, w0;
-  s0.reserve(m0);
-  d0.reserve(m0);
-  dg_rmat(g.scale, m0, g.a, g.b, g.c, g.seed, s0.p, d0.p, cs_);
-  if (weighted) {
-    w0.reserve(m0);
-    dg_weights(m0, g.weight_seed, g.weight_lo, g.weight_hi, w0.p, cs_);
-  }
-  if (!g.symmetrize) {
-    build_graph_dev(n, m0, s0, d0, w0, weighted, g.page_vertex_capacity, csr_edges);
-    return;
-  }
-  DBuf<uint32_t> s1, d1, w1;
-  s1.reserve(2 * m0);
-  d1.reserve(2 * m0);
-  if (weighted) w1.reserve(2 * m0);
-  dg_symmetrize(m0, s0.p, d0.p, weighted ? w0.p : nullptr, s1.p, d1.p, weighted ? w1.p : nullptr,
-                cs_);
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  s0.release();
-  d0.release();
-  w0.release();
-  build_graph_dev(n, 2 * m0, s1, d1, w1, weighted, g.page_vertex_capacity, csr_edges);
-}
-
-// load_binary (ingest.cpp:176-218) straight into the device build: the file's
-// edge records stream through two pinned staging buffers onto the GPU (copy
-// stream, double-buffered against the reads), are split into src/dst/w and
-// validated there.  Same checks and exception classes as the reference:
-// FormatError for a bad header/size, FormatError wrapping the edge-list
-// validation (ids < num_vertices, weights >= 1).
-void Engine::load_srph(const char* path, uint32_t cap, bool csr_edges) {
-  SR_CUDA(cudaSetDevice(dev_));
-  const std::string p = path ? path : "";
-  const int fd = ::open(p.c_str(), O_RDONLY);
-  if (fd < 0) throw EngineError(SR_E_FORMAT, "cannot open '" + p + "'");
-  struct FdGuard {
-    int fd;
-    ~FdGuard() { ::close(fd); }
-  } guard{fd};
-  struct stat stt {};
-  if (fstat(fd, &stt) != 0) throw EngineError(SR_E_FORMAT, "cannot stat '" + p + "'");
-  const uint64_t size = uint64_t(stt.st_size);
-  if (size < 24)
-    throw EngineError(SR_E_FORMAT, "'" + p + "': header needs 24 bytes, file has " +
-                                       std::to_string(size));
-  unsigned char hdr[24];
-  if (::pread(fd, hdr, 24, 0) != 24) throw EngineError(SR_E_FORMAT, "'" + p + "': short read");
-  if (std::memcmp(hdr, "SRPH", 4) != 0) throw EngineError(SR_E_FORMAT, "'" + p + "': bad magic");
-  if (hdr[4] != 1)
-    throw EngineError(SR_E_FORMAT, "'" + p + "': unsupported version " + std::to_string(hdr[4]));
-  const bool weighted = (hdr[5] & 1) != 0;
-  uint64_t nv = 0, m = 0;
-  for (int k = 7; k >= 0; --k) {
-    nv = (nv << 8) | hdr[8 + k];
-    m = (m << 8) | hdr[16 + k];
-  }
-  if (nv > 0xffffffffull)
-    throw EngineError(SR_E_FORMAT, "'" + p + "': vertex count exceeds 32-bit id range");
-  const uint64_t rec = weighted ? 12 : 8;
-  if (m > (size - 24) / rec || size != 24 + m * rec)
-    throw EngineError(SR_E_FORMAT, "'" + p + "': expected " + std::to_string(24 + m * rec) +
-                                       " bytes, file has " + std::to_string(size));
-  const uint64_t bytes = m * rec;
-  DBuf<uint32_t> raw;
-  raw.reserve(std::max<uint64_t>(bytes / 4, 1));
-  constexpr uint64_t kStage = 64ull << 20;
-  PinBuf<uint8_t> stage[2];
-  cudaEvent_t done[2];
-  for (int b = 0; b < 2; ++b) {
-    stage[b].reserve(kStage);
-    SR_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
-  }
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() {
-      cudaEventDestroy(e[0]);
-      cudaEventDestroy(e[1]);
-    }
-  } evg{done};
-  int k = 0;
-  for (uint64_t at = 0; at < bytes; at += kStage, k ^= 1) {
-    const uint64_t len = std::min(kStage, bytes - at);
-    SR_CUDA(cudaEventSynchronize(done[k]));  // the buffer's previous copy has landed
-    uint64_t got = 0;
-    while (got < len) {
-      const ssize_t r = ::pread(fd, stage[k].p + got, len - got, off_t(24 + at + got));
-      if (r <= 0) throw EngineError(SR_E_FORMAT, "'" + p + "': short read");
-      got += uint64_t(r);
-    }
-    SR_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(raw.p) + at, stage[k].p, len,
-                            cudaMemcpyHostToDevice, xs_));
-    SR_CUDA(cudaEventRecord(done[k], xs_));
-  }
-  SR_CUDA(cudaStreamSynchronize(xs_));
-  DBuf<uint32_t> src, dst, w;
-  src.reserve(std::max<uint64_t>(m, 1));
-  dst.reserve(std::max<uint64_t>(m, 1));
-  if (weighted) w.reserve(std::max<uint64_t>(m, 1));
-  dg_deinterleave(m, raw.p, weighted, src.p, dst.p, weighted ? w.p : nullptr, cs_);
-  raw.release();
-  if (!dg_ids_valid(uint32_t(nv), m, src.p, dst.p, cs_))
-    throw EngineError(SR_E_FORMAT, "'" + p + "': edge has id >= num_vertices " + std::to_string(nv));
-  if (weighted && !dg_weights_valid(m, w.p, cs_))
-    throw EngineError(SR_E_FORMAT, "'" + p + "': edge has weight < 1");
-  build_graph_dev(uint32_t(nv), m, src, dst, w, weighted, cap, csr_edges);
-}
-
-void Engine::graph_info(sr_graph_info& gi) const {
-  gi = sr_graph_info{};
-  gi.num_vertices = n_;
-  gi.num_edges = m_;
-  gi.num_pages = uint32_t(pages_.size());
-  gi.page_vertex_capacity = cap_;
-  gi.weighted = weighted_ ? 1 : 0;
-  gi.has_csr_edges = has_csr_edges_ ? 1 : 0;
-  gi.csr_weighted = csr_weighted_ ? 1 : 0;
-  gi.csr_derived = csr_derived_ ? 1 : 0;
-}
-
-void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w, uint64_t* in_off,
-                          uint32_t* in_src, uint32_t* in_w) {
-  SR_CUDA(cudaSetDevice(dev_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  if ((out_off || out_nbr || out_w) && !has_csr_) throw EngineError(SR_E_DATA, "no csr loaded");
-  if (out_off) SR_CUDA(cudaMemcpy(out_off, out_off_.p, (size_t(n_) + 1) * 8, cudaMemcpyDeviceToHost));
-  if (out_nbr) {
-    if (!has_csr_edges_) throw EngineError(SR_E_DATA, "csr adjacency not on the device");
-    if (m_) SR_CUDA(cudaMemcpy(out_nbr, out_nbr_.p, m_ * 4, cudaMemcpyDeviceToHost));
-  }
-  if (out_w) {
-    if (!csr_weighted_) throw EngineError(SR_E_DATA, "csr has no weights");
-    if (m_) SR_CUDA(cudaMemcpy(out_w, out_w_.p, m_ * 4, cudaMemcpyDeviceToHost));
-  }
-  if (!(in_off || in_src || in_w)) return;
-  if (!pages_loaded_) throw EngineError(SR_E_DATA, "no pages loaded");
-  if (in_w && !weighted_) throw EngineError(SR_E_DATA, "pages have no weights");
-  uint64_t at = 0;
-  std::vector<uint32_t> loc;
-  for (uint32_t p = 0; p < pages_.size(); ++p) {
-    const PageMeta& pm = pages_[p];
-    const uint32_t range = pm.ve - pm.vb;
-    const bool dev = pm.h_offs == nullptr;  // resident: arena; out-of-core: pinned stage
-    const PageDesc& d = page_desc_h_[p];
-    const uint32_t* offs = dev ? d.offs : pm.h_offs;
-    const uint32_t* srcp = dev ? d.src : pm.h_src;
-    const uint32_t* wp = dev ? d.w : pm.h_w;
-    if (!offs) throw EngineError(SR_E_DATA, "page " + std::to_string(p) + " is not held");
-    if (in_off) {
-      loc.resize(size_t(range) + 1);
-      SR_CUDA(cudaMemcpy(loc.data(), offs, loc.size() * 4, cudaMemcpyDefault));
-      for (uint32_t i = 0; i <= range; ++i) in_off[pm.vb + i] = at + loc[i];
-    }
-    if (pm.edges) {
-      if (in_src) SR_CUDA(cudaMemcpy(in_src + at, srcp, pm.edges * 4, cudaMemcpyDefault));
-      if (in_w) SR_CUDA(cudaMemcpy(in_w + at, wp, pm.edges * 4, cudaMemcpyDefault));
-    }
-    at += pm.edges;
-  }
 }
 
 void Engine::maybe_derive_csr() {
@@ -956,193 +701,6 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
   }
   flush();
   return RunStats{};
-}
-
-// ---------------------------------------------------------------------------
-// Streaming window (out-of-core path)
-// ---------------------------------------------------------------------------
-void Engine::ensure_slots(uint32_t window, PassOut& po) {
-  // Budget plan for the out-of-core path: a ring of `window` slots sized for
-  // the largest streamed page, and the heaviest pages cached permanently --
-  // the largest K for which the K biggest pages plus `window` slots of the
-  // (K+1)-th biggest fit (RMAT page sizes follow the popcount of the page
-  // index, so "heaviest" is not an id prefix).
-  std::vector<uint32_t> used;
-  for (uint32_t p = 0; p < pages_.size(); ++p)
-    if (pages_[p].h_offs) used.push_back(p);
-  std::stable_sort(used.begin(), used.end(),
-                   [&](uint32_t x, uint32_t y) { return pages_[x].bytes > pages_[y].bytes; });
-  const uint32_t want = std::max<uint32_t>(window, 2);
-  const size_t U = used.size();
-  // slot = the largest streamed page image (stream_image_words)
-  std::vector<uint64_t> suf_words(U + 1, 0);
-  for (size_t k = U; k-- > 0;)
-    suf_words[k] = std::max(suf_words[k + 1], stream_image_words(pages_[used[k]], weighted_));
-  size_t K = 0;
-  bool fits = false;
-  uint64_t prefix = 0;
-  for (size_t k = 0; k < U; ++k) {
-    const uint64_t slot_bytes = suf_words[k] * 4;
-    if (prefix + want * slot_bytes <= budget_) {
-      K = k;
-      fits = true;
-    }
-    prefix += pages_[used[k]].bytes;
-  }
-  if (!fits)
-    throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(budget_) +
-                                       " B cannot hold a window of " + std::to_string(want) +
-                                       " page slots of " + std::to_string(suf_words[0] * 4) + " B");
-  const bool same_plan = plan_window_ == want && plan_cached_ == K && ring_words_ > 0;
-  if (same_plan) return;
-  // (re)build the cache arena for pages used[0..K)
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  for (auto& pm : pages_) {
-    pm.on_device = false;
-    pm.slot = -1;
-  }
-  uint64_t off_total = 0, edge_total = 0;
-  for (size_t k = 0; k < K; ++k) {
-    PageMeta& pm = pages_[used[k]];
-    pm.off_base = off_total;
-    pm.edge_base = edge_total;
-    off_total += pm.ve - pm.vb + 1;
-    edge_total += (pm.edges + 7) & ~7ull;
-  }
-  edge_total += 8;
-  arena_offs_.release();
-  arena_src_.release();
-  arena_w_.release();
-  if (K) {
-    arena_offs_.reserve(off_total);
-    arena_src_.reserve(std::max<uint64_t>(edge_total, 1));
-    if (weighted_) arena_w_.reserve(std::max<uint64_t>(edge_total, 1));
-  }
-  for (size_t k = 0; k < K; ++k) {
-    const uint32_t p = used[k];
-    PageMeta& pm = pages_[p];
-    uint32_t* o = arena_offs_.p + pm.off_base;
-    uint32_t* sp = arena_src_.p + pm.edge_base;
-    uint32_t* wp = weighted_ ? arena_w_.p + pm.edge_base : nullptr;
-    SR_CUDA(cudaMemcpyAsync(o, pm.h_offs, (size_t(pm.ve - pm.vb) + 1) * 4, cudaMemcpyHostToDevice, xs_));
-    if (pm.edges) {
-      SR_CUDA(cudaMemcpyAsync(sp, pm.h_src, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
-      if (wp) SR_CUDA(cudaMemcpyAsync(wp, pm.h_w, pm.edges * 4, cudaMemcpyHostToDevice, xs_));
-    }
-    launch_set_page_desc(page_desc_.p, p, o, sp, wp, xs_);
-    pm.on_device = true;
-    po.pages_transferred += 1;
-    po.bytes_transferred += pm.bytes;
-    h2d_bytes_ += pm.bytes;
-  }
-  // the streaming ring: `window` images of the largest streamed page
-  ring_reset();
-  ring_words_ = std::max<uint64_t>(suf_words[K], 1) * want;
-  ring_.release();
-  ring_.reserve(ring_words_);
-  SR_CUDA(cudaEventRecord(ev_step_, xs_));
-  SR_CUDA(cudaStreamWaitEvent(cs_, ev_step_, 0));
-  plan_window_ = want;
-  plan_cached_ = K;
-}
-
-void Engine::ring_reset() {
-  for (int e : ring_fifo_) {
-    if (slots_[e].page >= 0 && size_t(slots_[e].page) < pages_.size())
-      pages_[slots_[e].page].slot = -1;
-    slots_[e].page = -1;
-    slot_free_.push_back(e);
-  }
-  ring_fifo_.clear();
-  ring_head_ = 0;
-}
-
-// Drop the oldest image from the ring unless a step that is about to run
-// still needs it; the next copy into its space waits for its last reader.
-bool Engine::ring_evict_oldest(const std::vector<char>& protect) {
-  if (ring_fifo_.empty()) return false;
-  const int e = ring_fifo_.front();
-  StreamSlot& sl = slots_[e];
-  if (sl.page >= 0 && protect[sl.page]) return false;
-  SR_CUDA(cudaStreamWaitEvent(xs_, sl.freed, 0));
-  if (sl.page >= 0) pages_[sl.page].slot = -1;
-  sl.page = -1;
-  ring_fifo_.pop_front();
-  slot_free_.push_back(e);
-  if (ring_fifo_.empty()) ring_head_ = 0;
-  return true;
-}
-
-// Admit a page into the ring (one DMA of its staged image on the copy
-// stream).  Returns false when it cannot be placed without evicting an image
-// that `protect` marks as still needed.
-bool Engine::make_resident(uint32_t page, long long step, const std::vector<char>& protect,
-                           PassOut& po) {
-  PageMeta& pm = pages_[page];
-  if (pm.on_device || pm.slot >= 0) return true;
-  const uint64_t need = stream_image_words(pm, weighted_);
-  if (need > ring_words_) throw EngineError(SR_E_CONTRACT, "page larger than the streaming ring");
-  uint64_t pos = 0;
-  for (;;) {
-    if (ring_fifo_.empty()) {
-      pos = 0;
-      break;
-    }
-    const uint64_t tail = slots_[ring_fifo_.front()].start;
-    if (ring_head_ > tail) {
-      // live region [tail, head): free space at [head, end) and [0, tail)
-      if (ring_head_ + need <= ring_words_) {
-        pos = ring_head_;
-        break;
-      }
-      if (need <= tail) {
-        pos = 0;
-        break;
-      }
-    } else if (ring_head_ + need <= tail) {
-      // wrapped: free space [head, tail)
-      pos = ring_head_;
-      break;
-    }
-    if (!ring_evict_oldest(protect)) return false;
-  }
-  int e;
-  if (!slot_free_.empty()) {
-    e = slot_free_.back();
-    slot_free_.pop_back();
-  } else {
-    e = int(slots_.size());
-    slots_.emplace_back();
-    SR_CUDA(cudaEventCreateWithFlags(&slots_[e].ready, cudaEventDisableTiming));
-    SR_CUDA(cudaEventCreateWithFlags(&slots_[e].freed, cudaEventDisableTiming));
-    SR_CUDA(cudaEventRecord(slots_[e].freed, cs_));
-  }
-  StreamSlot& sl = slots_[e];
-  sl.start = pos;
-  sl.words = need;
-  WallTraceRec* tr = nullptr;
-  if (record_trace_) {
-    wtrace_.push_back(WallTraceRec{trace_event(), trace_event(), {page}, SR_TRACE_XFER_START,
-                                   cur_pass_});
-    tr = &wtrace_.back();
-    SR_CUDA(cudaEventRecord(tr->a, xs_));
-  }
-  // the staged page image (offsets | sources | weights, 32 B aligned) in ONE DMA
-  uint32_t* base = ring_.p + pos;
-  const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
-  SR_CUDA(cudaMemcpyAsync(base, pm.h_offs, need * 4, cudaMemcpyHostToDevice, xs_));
-  launch_set_page_desc(page_desc_.p, page, base, base + so, weighted_ ? base + wo : nullptr, xs_);
-  if (tr) SR_CUDA(cudaEventRecord(tr->b, xs_));
-  SR_CUDA(cudaEventRecord(sl.ready, xs_));
-  sl.page = int(page);
-  sl.last_use = step;
-  pm.slot = e;
-  ring_fifo_.push_back(e);
-  ring_head_ = pos + need;
-  po.pages_transferred += 1;
-  po.bytes_transferred += pm.bytes;
-  h2d_bytes_ += pm.bytes;
-  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1867,406 +1425,6 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     m.prediction_accuracy =
         double(census_h_.p->log_events - census_h_.p->log_incorrect) / double(census_h_.p->log_events);
   }
-}
-
-// ---------------------------------------------------------------------------
-// Source-blocked sub-pages for PageRank: when the contrib array outgrows the
-// L2, every iteration sweeps the sub-pages block by block so the gathers of
-// one sweep stay inside a blk_verts slice (SERAPH_PR_BLOCK_VERTS, default
-// 16 Mi vertices = 64 MB of f32; 0 disables).
-// ---------------------------------------------------------------------------
-bool Engine::build_src_blocks(uint64_t blk) {
-  if (sb_.built && sb_.blk_verts == blk) return true;
-  if (!all_resident_) return false;  // sharded ranks block their own destinations
-  if (blk == 0 || n_ <= blk) return false;
-  sb_.built = false;
-  const uint32_t np = uint32_t(pages_.size());
-  for (uint32_t p = 0; p < np; ++p)
-    if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
-  const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
-  uint32_t n_tiles = 0;  // a sharded rank holds tiles for its own pages only
-  for (const PageMeta& pm : pages_) n_tiles = std::max(n_tiles, pm.tile_end);
-  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
-  auto t_last = std::chrono::steady_clock::now();
-  auto stage = [&](const char* what) {
-    if (!timing) return;
-    SR_CUDA(cudaStreamSynchronize(cs_));
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[seraph] src blocks %s: %.1f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t_last).count());
-    t_last = now;
-  };
-  // 1) counts per (block, destination)
-  DBuf<uint32_t> cnt;
-  cnt.reserve(size_t(nb) * n_);
-  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
-  launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, nullptr, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
-  // 2) page-local offsets per sub-page, sub-page sizes
-  DBuf<unsigned long long> goff, bp_edges, bp_base;
-  goff.reserve(size_t(nb) * n_);
-  bp_edges.reserve(size_t(nb) * np);
-  bp_base.reserve(size_t(nb) * np);
-  stage("count");
-  launch_src_block_scan(cnt.p, goff.p, page_desc_.p, np, nb, n_, bp_edges.p, cs_);
-  stage("scan");
-  std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
-  SR_CUDA(cudaMemcpyAsync(edges_h.data(), bp_edges.p, edges_h.size() * 8, cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  unsigned long long at = 0;
-  for (size_t k = 0; k < edges_h.size(); ++k) {  // block-major, 32 B aligned sub-pages
-    base_h[k] = at;
-    at += (edges_h[k] + 7) & ~7ull;
-    if (edges_h[k] > 0xffffffffull) return false;
-  }
-  sb_.src.reserve(at + 8);
-  if (weighted_) sb_.w.reserve(at + 8);
-  else sb_.w.release();
-  SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
-  // 3) scatter the sources (cnt reused as cursors)
-  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
-  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, bp_base.p,
-                   sm_count_ * 8, cs_);
-  stage("scatter");
-  // 4) u32 local offsets of every sub-page, then the tile cut on the device
-  const size_t per_block = size_t(n_) + np;
-  sb_.offs.reserve(size_t(nb) * per_block);
-  launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
-  const size_t K = sub_tile_windows(cap_, np, nb);
-  const size_t K_blk = K / nb;  // windows per block
-  DBuf<uint32_t> tcnt, tat;
-  tcnt.reserve(K + 1);
-  tat.reserve(K + 1);
-  SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));
-  launch_sub_tiles(0, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, tcnt.p, nullptr, nullptr,
-                   nullptr, cs_);
-  launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, cs_);
-  sb_.block_tile_begin.assign(nb + 1, 0);
-  for (uint32_t b = 0; b <= nb; ++b)
-    SR_CUDA(cudaMemcpyAsync(&sb_.block_tile_begin[b], tat.p + size_t(b) * K_blk, 4,
-                            cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  const uint32_t n_sub_tiles = sb_.block_tile_begin[nb];
-  sb_.tiles.reserve(std::max<size_t>(n_sub_tiles, 1));
-  sb_.tile_page.reserve(std::max<size_t>(n_sub_tiles, 1));
-  launch_sub_tiles(1, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, nullptr, tat.p, sb_.tiles.p,
-                   sb_.tile_page.p, cs_);
-  SR_CUDA(cudaGetLastError());
-  stage("offsets + tile cut");
-  std::vector<PageDesc> desc(size_t(nb) * np);
-  for (uint32_t b = 0; b < nb; ++b)
-    for (uint32_t p = 0; p < np; ++p) {
-      PageDesc& d = desc[size_t(b) * np + p];
-      d.vertex_begin = pages_[p].vb;
-      d.range = pages_[p].ve - pages_[p].vb;
-      d.edge_count = edges_h[size_t(b) * np + p];
-      d.offs = sb_.offs.p + size_t(b) * per_block + size_t(p) * cap_ + p;
-      d.src = sb_.src.p + base_h[size_t(b) * np + p];
-      d.w = weighted_ ? sb_.w.p + base_h[size_t(b) * np + p] : nullptr;
-    }
-  sb_.desc.reserve(desc.size());
-  SR_CUDA(cudaMemcpyAsync(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc),
-                          cudaMemcpyHostToDevice, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  sb_.acc.reserve(n_);
-  SR_CUDA(cudaMemset(sb_.acc.p, 0, size_t(n_) * 4));
-  sb_.blk_verts = uint32_t(blk);
-  sb_.n_blocks = nb;
-  sb_.built = true;
-  return true;
-}
-
-// Source-blocked dense pull (K1): when the vertex array outgrows the L2,
-// a baseline-schedule dense pass sweeps the source-blocked sub-pages block by
-// block, so every launch gathers from one blk-vertex slice that stays in
-// L2 instead of 32-byte DRAM sectors spread over the whole array.
-// SERAPH_PULL_BLOCK_VERTS: block size (0 = off; default 16 Mi vertices =
-// 64 MB of values, used when the array exceeds half the L2).  Values are
-// unchanged (min-combine is order independent; every destination sees
-// every in-edge once per pass).  Attempts/skips are counted on block 0,
-// edges on every block, valid updates = destinations changed in the pass.
-//
-// Blocking pays only when the unblocked gathers have no L2 locality: by
-// default it is used when the vertex array exceeds half the L2 AND the
-// sources that fit there (the L2/8 highest out-degree vertices) carry less
-// than half of the edges -- true for uniform graphs (C4: ~15 %), false for
-// RMAT, whose hubs stay L2-resident anyway (RMAT-26 SSSP: 10.1 ms unblocked
-// vs 10.9 ms blocked; uniform-27 CC: 122 ms vs 22 ms).
-uint64_t Engine::pull_block_verts() {
-  uint64_t blk = 16ull << 20;
-  const char* env = std::getenv("SERAPH_PULL_BLOCK_VERTS");
-  if (env) blk = std::strtoull(env, nullptr, 10);
-  if (blk == 0 || n_ <= blk) return 0;
-  if (env) return blk;
-  if (uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return 0;
-  return hot_source_coverage(uint64_t(l2_bytes_) / 8) < 0.5 ? blk : 0;
-}
-
-// Fraction of the edges whose source is among the k highest out-degree
-// vertices (degree histogram on the device; cached per CSR).
-double Engine::hot_source_coverage(uint64_t k) {
-  if (coverage_k_ == k && coverage_ >= 0) return coverage_;
-  DBuf<unsigned long long> hv, he;
-  hv.reserve(kDegHistCap + 1);
-  he.reserve(kDegHistCap + 1);
-  SR_CUDA(cudaMemsetAsync(hv.p, 0, (kDegHistCap + 1) * 8, cs_));
-  SR_CUDA(cudaMemsetAsync(he.p, 0, (kDegHistCap + 1) * 8, cs_));
-  launch_degree_hist(outdeg_.p, n_, hv.p, he.p, cs_);
-  std::vector<unsigned long long> v(kDegHistCap + 1), e(kDegHistCap + 1);
-  SR_CUDA(cudaMemcpyAsync(v.data(), hv.p, v.size() * 8, cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaMemcpyAsync(e.data(), he.p, e.size() * 8, cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  uint64_t total = 0;
-  for (auto x : e) total += x;
-  double covered = 0;
-  uint64_t left = k;
-  for (int d = int(kDegHistCap); d >= 0 && left; --d) {
-    const uint64_t take = std::min<uint64_t>(left, v[d]);
-    if (v[d]) covered += double(e[d]) * double(take) / double(v[d]);
-    left -= take;
-  }
-  coverage_k_ = k;
-  coverage_ = total ? covered / double(total) : 1.0;
-  return coverage_;
-}
-
-// Pin the gathered slice of a source block in L2 for the launches that
-// follow on the compute stream (cudaAccessPolicyWindow, persisting lines;
-// the streamed page arrays are loaded evict-first).  bytes == 0 clears it.
-// SERAPH_L2_PERSIST=0 disables.  Measured: uniform-27 CC 22.3 -> 21.8 ms;
-// PageRank's 128 MB contribution blocks exceed the carve-out (105.9 vs
-// 103.2 ms with it), so K8 does not use it.
-void Engine::l2_window(const void* base, size_t bytes) {
-  if (l2_persist_max_ < 0) {
-    int mx = 0;
-    l2_persist_max_ =
-        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev_) == cudaSuccess ? mx : 0;
-  }
-  const char* e = std::getenv("SERAPH_L2_PERSIST");
-  if (e && std::atoi(e) == 0) bytes = 0;
-  if (!l2_persist_max_ || (bytes == 0 && !l2_window_set_)) return;
-  // the persisting carve-out shrinks the normal L2 for everything else: it
-  // exists only while a window is set
-  if (bytes && !l2_window_set_)
-    SR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(l2_persist_max_)));
-  cudaStreamAttrValue attr{};
-  attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  attr.accessPolicyWindow.num_bytes = bytes;
-  attr.accessPolicyWindow.hitRatio =
-      bytes ? float(std::min(1.0, double(l2_persist_max_) / double(bytes))) : 0.f;
-  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  SR_CUDA(cudaStreamSetAttribute(cs_, cudaStreamAttributeAccessPolicyWindow, &attr));
-  l2_window_set_ = bytes != 0;
-  if (!bytes) {
-    SR_CUDA(cudaCtxResetPersistingL2Cache());
-    SR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
-  }
-}
-
-bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
-  const uint64_t blk = pull_block_verts();
-  if (!blk || !build_src_blocks(blk)) return false;
-  const uint32_t run_id = ++run_id_;
-  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
-    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
-    if (t1 <= t0) continue;
-    l2_window(values_.p + uint64_t(b) * blk, std::min<uint64_t>(blk, n_ - uint64_t(b) * blk) * 4);
-    PullArgs a{};
-    a.work = next_work_counter();
-    a.tiles = sb_.tiles.p;
-    a.tile_page = sb_.tile_page.p;
-    a.pages = sb_.desc.p;
-    a.seg.n = 1;
-    a.seg.tile_begin[0] = t0;
-    a.seg.task_prefix[0] = 0;
-    a.seg.task_prefix[1] = t1 - t0;
-    a.values = values_.p;
-    a.next = values_.p;
-    a.changed = changed_.p;
-    a.status = status_.p;
-    a.hub_stamp = hub_stamp_.p;
-    a.run_id = run_id;
-    a.ctr = ctr;
-    a.census = census_.p;
-    a.count_dest = b == 0 ? 1u : 0u;
-    a.count_valid = 0;
-    a.k_bfs = k_bfs_;
-    a.s_cc = s_cc_;
-    a.l_sssp = l_sssp_;
-    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
-                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
-    auto* evp = relax_begin();
-    launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
-    SR_CUDA(cudaGetLastError());
-    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
-    if (b == 0 && sb_.n_blocks > 1) {
-      // Probe: blocking pays for gathers only.  If block 0 gathered for < 5 %
-      // of its edges (converged labels/levels skip theirs), finish the pass
-      // with one unblocked sweep instead of n_blocks - 1 more destination
-      // passes (its relaxations are idempotent; the counters restart).
-      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
-      SR_CUDA(cudaStreamSynchronize(cs_));
-      const RunCtr& c0 = ctr_h_.p[0];
-      if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
-        SR_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RunCtr), cs_));
-        l2_window(nullptr, 0);
-        return false;
-      }
-    }
-  }
-  l2_window(nullptr, 0);
-  return true;
-}
-
-std::pair<cudaEvent_t, cudaEvent_t>* Engine::relax_begin() {
-  if (!profile_kernels_) return nullptr;
-  if (relax_ev_used_ == relax_ev_.size()) {
-    std::pair<cudaEvent_t, cudaEvent_t> e;
-    SR_CUDA(cudaEventCreate(&e.first));
-    SR_CUDA(cudaEventCreate(&e.second));
-    relax_ev_.push_back(e);
-  }
-  auto* evp = &relax_ev_[relax_ev_used_++];
-  SR_CUDA(cudaEventRecord(evp->first, cs_));
-  return evp;
-}
-
-void Engine::pr_blocked_pass(float base, float damp) {
-  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
-    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
-    if (t1 <= t0) continue;
-    PrArgs a{};
-    a.work = next_work_counter();
-    a.tiles = sb_.tiles.p;
-    a.tile_page = sb_.tile_page.p;
-    a.pages = sb_.desc.p;
-    a.seg.n = 1;
-    a.seg.tile_begin[0] = t0;
-    a.seg.task_prefix[0] = 0;
-    a.seg.task_prefix[1] = t1 - t0;
-    a.contrib_in = contrib_a_.p;
-    a.rank_out = rank_b_.p;
-    a.contrib_out = contrib_b_.p;
-    a.inv_outdeg = inv_outdeg_.p;
-    a.hub_sum = hub_sum_.p;
-    a.acc = sb_.acc.p;
-    a.ctr = nullptr;
-    a.base = base;
-    a.damp = damp;
-    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
-                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
-    std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
-    if (profile_kernels_) {
-      if (relax_ev_used_ == relax_ev_.size()) {
-        std::pair<cudaEvent_t, cudaEvent_t> e;
-        SR_CUDA(cudaEventCreate(&e.first));
-        SR_CUDA(cudaEventCreate(&e.second));
-        relax_ev_.push_back(e);
-      }
-      evp = &relax_ev_[relax_ev_used_++];
-      SR_CUDA(cudaEventRecord(evp->first, cs_));
-    }
-    launch_pr_pull(a, std::max(grid, 1), cs_);
-    SR_CUDA(cudaGetLastError());
-    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
-  }
-  launch_pr_block_finalize(own_lo_, own_hi_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p,
-                           base, damp, cs_);
-}
-
-// ---------------------------------------------------------------------------
-// PageRank (new algorithm; conventions pinned in DESIGN.md §2)
-// ---------------------------------------------------------------------------
-void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
-                          std::vector<sr_pass_stats>& passes) {
-  uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
-  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
-  const bool blocked = build_src_blocks(pr_blk);
-  const auto wall0 = std::chrono::steady_clock::now();
-  SR_CUDA(cudaEventRecord(ev_start_, cs_));
-  launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
-  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
-  if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
-  // The iterations are enqueued back to back with no host sync in between
-  // (the copy stream prefetches the next iteration's pages while the current
-  // one computes); each iteration's counters get their own slice of the
-  // counter arena, read back once at the end.
-  ctr_used_ = 0;
-  SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
-  std::vector<uint32_t> ctr_begin;
-  for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
-    ctr_begin.push_back(ctr_used_);
-    if (attached()) {
-      SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
-      SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
-    }
-    PassOut po;
-    const float base = float((1.0 - cfg.pr_damping) / double(n_));
-    if (blocked) {
-      pr_blocked_pass(base, float(cfg.pr_damping));
-      po.kernel_runs = sb_.n_blocks * pages_.size();
-      if (!first_touch_done_) {
-        for (const auto& pm : pages_) {
-          po.pages_transferred += 1;
-          po.bytes_transferred += pm.bytes;
-        }
-        first_touch_done_ = true;
-      }
-    } else {
-      po = dense_pass_wall(cfg, kGateOff, false, it, true);
-      launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
-                             inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
-    }
-    exchange_round(true);
-    sr_pass_stats st{};
-    st.pass_index = it;
-    st.kind = SR_PASS_DENSE_PULL;
-    if (blocked) {  // every destination and edge once per iteration
-      st.attempts = n_;
-      st.edges_read = page_edges_total_;
-      gathers_total_ += page_edges_total_;
-    }
-    st.changed_vertices = n_;
-    m.pages_transferred += po.pages_transferred;
-    m.bytes_transferred += po.bytes_transferred;
-    m.kernel_runs += po.kernel_runs;
-    m.passes += 1;
-    m.dense_passes += 1;
-    if (blocked) {
-      m.update_attempts += st.attempts;
-      m.edges_read += st.edges_read;
-    }
-    passes.push_back(st);
-    std::swap(rank_a_.p, rank_b_.p);
-    std::swap(contrib_a_.p, contrib_b_.p);
-  }
-  SR_CUDA(cudaEventRecord(ev_stop_, cs_));
-  if (ranks_out)
-    SR_CUDA(cudaMemcpyAsync(ranks_out, rank_a_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
-  if (ctr_used_)
-    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
-                            cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
-  ctr_begin.push_back(ctr_used_);
-  for (size_t it = 0; it + 1 < ctr_begin.size(); ++it) {
-    if (blocked) continue;  // counted analytically above
-    sr_pass_stats& st = passes[passes.size() - (ctr_begin.size() - 1) + it];
-    for (uint32_t i = ctr_begin[it]; i < ctr_begin[it + 1]; ++i) {
-      gathers_total_ += ctr_h_.p[i].gathers;
-      st.attempts += ctr_h_.p[i].attempts;
-      st.edges_read += ctr_h_.p[i].edges;
-    }
-    m.update_attempts += st.attempts;
-    m.edges_read += st.edges_read;
-  }
-  float ms = 0;
-  SR_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_stop_));
-  m.device_seconds = ms * 1e-3;
-  if (ranks_out) m.d2h_bytes = uint64_t(n_) * 4;
-  m.wall_seconds =
-      std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
 }
 
 // ---------------------------------------------------------------------------

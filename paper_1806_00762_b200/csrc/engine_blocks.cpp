@@ -1,0 +1,415 @@
+// Source-blocked sweeps (K1 and K8 over per-source-block sub-pages, the
+// persisting-L2 window, the blocking heuristics) and the PageRank driver.
+#include "engine.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "kernels.h"
+
+namespace seraph {
+
+// ---------------------------------------------------------------------------
+// Source-blocked sub-pages for PageRank: when the contrib array outgrows the
+// L2, every iteration sweeps the sub-pages block by block so the gathers of
+// one sweep stay inside a blk_verts slice (SERAPH_PR_BLOCK_VERTS, default
+// 16 Mi vertices = 64 MB of f32; 0 disables).
+// ---------------------------------------------------------------------------
+bool Engine::build_src_blocks(uint64_t blk) {
+  if (sb_.built && sb_.blk_verts == blk) return true;
+  if (!all_resident_) return false;  // sharded ranks block their own destinations
+  if (blk == 0 || n_ <= blk) return false;
+  sb_.built = false;
+  const uint32_t np = uint32_t(pages_.size());
+  for (uint32_t p = 0; p < np; ++p)
+    if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
+  const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
+  uint32_t n_tiles = 0;  // a sharded rank holds tiles for its own pages only
+  for (const PageMeta& pm : pages_) n_tiles = std::max(n_tiles, pm.tile_end);
+  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!timing) return;
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[seraph] src blocks %s: %.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  // 1) counts per (block, destination)
+  DBuf<uint32_t> cnt;
+  cnt.reserve(size_t(nb) * n_);
+  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
+  launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
+                   cnt.p, nullptr, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
+  // 2) page-local offsets per sub-page, sub-page sizes
+  DBuf<unsigned long long> goff, bp_edges, bp_base;
+  goff.reserve(size_t(nb) * n_);
+  bp_edges.reserve(size_t(nb) * np);
+  bp_base.reserve(size_t(nb) * np);
+  stage("count");
+  launch_src_block_scan(cnt.p, goff.p, page_desc_.p, np, nb, n_, bp_edges.p, cs_);
+  stage("scan");
+  std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
+  SR_CUDA(cudaMemcpyAsync(edges_h.data(), bp_edges.p, edges_h.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  unsigned long long at = 0;
+  for (size_t k = 0; k < edges_h.size(); ++k) {  // block-major, 32 B aligned sub-pages
+    base_h[k] = at;
+    at += (edges_h[k] + 7) & ~7ull;
+    if (edges_h[k] > 0xffffffffull) return false;
+  }
+  sb_.src.reserve(at + 8);
+  if (weighted_) sb_.w.reserve(at + 8);
+  else sb_.w.release();
+  SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
+  // 3) scatter the sources (cnt reused as cursors)
+  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
+  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
+                   cnt.p, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, bp_base.p,
+                   sm_count_ * 8, cs_);
+  stage("scatter");
+  // 4) u32 local offsets of every sub-page, then the tile cut on the device
+  const size_t per_block = size_t(n_) + np;
+  sb_.offs.reserve(size_t(nb) * per_block);
+  launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
+  const size_t K = sub_tile_windows(cap_, np, nb);
+  const size_t K_blk = K / nb;  // windows per block
+  DBuf<uint32_t> tcnt, tat;
+  tcnt.reserve(K + 1);
+  tat.reserve(K + 1);
+  SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));
+  launch_sub_tiles(0, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, tcnt.p, nullptr, nullptr,
+                   nullptr, cs_);
+  launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, cs_);
+  sb_.block_tile_begin.assign(nb + 1, 0);
+  for (uint32_t b = 0; b <= nb; ++b)
+    SR_CUDA(cudaMemcpyAsync(&sb_.block_tile_begin[b], tat.p + size_t(b) * K_blk, 4,
+                            cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  const uint32_t n_sub_tiles = sb_.block_tile_begin[nb];
+  sb_.tiles.reserve(std::max<size_t>(n_sub_tiles, 1));
+  sb_.tile_page.reserve(std::max<size_t>(n_sub_tiles, 1));
+  launch_sub_tiles(1, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, nullptr, tat.p, sb_.tiles.p,
+                   sb_.tile_page.p, cs_);
+  SR_CUDA(cudaGetLastError());
+  stage("offsets + tile cut");
+  std::vector<PageDesc> desc(size_t(nb) * np);
+  for (uint32_t b = 0; b < nb; ++b)
+    for (uint32_t p = 0; p < np; ++p) {
+      PageDesc& d = desc[size_t(b) * np + p];
+      d.vertex_begin = pages_[p].vb;
+      d.range = pages_[p].ve - pages_[p].vb;
+      d.edge_count = edges_h[size_t(b) * np + p];
+      d.offs = sb_.offs.p + size_t(b) * per_block + size_t(p) * cap_ + p;
+      d.src = sb_.src.p + base_h[size_t(b) * np + p];
+      d.w = weighted_ ? sb_.w.p + base_h[size_t(b) * np + p] : nullptr;
+    }
+  sb_.desc.reserve(desc.size());
+  SR_CUDA(cudaMemcpyAsync(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc),
+                          cudaMemcpyHostToDevice, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  sb_.acc.reserve(n_);
+  SR_CUDA(cudaMemset(sb_.acc.p, 0, size_t(n_) * 4));
+  sb_.blk_verts = uint32_t(blk);
+  sb_.n_blocks = nb;
+  sb_.built = true;
+  return true;
+}
+
+// Source-blocked dense pull (K1): when the vertex array outgrows the L2,
+// a baseline-schedule dense pass sweeps the source-blocked sub-pages block by
+// block, so every launch gathers from one blk-vertex slice that stays in
+// L2 instead of 32-byte DRAM sectors spread over the whole array.
+// SERAPH_PULL_BLOCK_VERTS: block size (0 = off; default 16 Mi vertices =
+// 64 MB of values, used when the array exceeds half the L2).  Values are
+// unchanged (min-combine is order independent; every destination sees
+// every in-edge once per pass).  Attempts/skips are counted on block 0,
+// edges on every block, valid updates = destinations changed in the pass.
+//
+// Blocking pays only when the unblocked gathers have no L2 locality: by
+// default it is used when the vertex array exceeds half the L2 AND the
+// sources that fit there (the L2/8 highest out-degree vertices) carry less
+// than half of the edges -- true for uniform graphs (C4: ~15 %), false for
+// RMAT, whose hubs stay L2-resident anyway (RMAT-26 SSSP: 10.1 ms unblocked
+// vs 10.9 ms blocked; uniform-27 CC: 122 ms vs 22 ms).
+uint64_t Engine::pull_block_verts() {
+  uint64_t blk = 16ull << 20;
+  const char* env = std::getenv("SERAPH_PULL_BLOCK_VERTS");
+  if (env) blk = std::strtoull(env, nullptr, 10);
+  if (blk == 0 || n_ <= blk) return 0;
+  if (env) return blk;
+  if (uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return 0;
+  return hot_source_coverage(uint64_t(l2_bytes_) / 8) < 0.5 ? blk : 0;
+}
+
+// Fraction of the edges whose source is among the k highest out-degree
+// vertices (degree histogram on the device; cached per CSR).
+double Engine::hot_source_coverage(uint64_t k) {
+  if (coverage_k_ == k && coverage_ >= 0) return coverage_;
+  DBuf<unsigned long long> hv, he;
+  hv.reserve(kDegHistCap + 1);
+  he.reserve(kDegHistCap + 1);
+  SR_CUDA(cudaMemsetAsync(hv.p, 0, (kDegHistCap + 1) * 8, cs_));
+  SR_CUDA(cudaMemsetAsync(he.p, 0, (kDegHistCap + 1) * 8, cs_));
+  launch_degree_hist(outdeg_.p, n_, hv.p, he.p, cs_);
+  std::vector<unsigned long long> v(kDegHistCap + 1), e(kDegHistCap + 1);
+  SR_CUDA(cudaMemcpyAsync(v.data(), hv.p, v.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaMemcpyAsync(e.data(), he.p, e.size() * 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  uint64_t total = 0;
+  for (auto x : e) total += x;
+  double covered = 0;
+  uint64_t left = k;
+  for (int d = int(kDegHistCap); d >= 0 && left; --d) {
+    const uint64_t take = std::min<uint64_t>(left, v[d]);
+    if (v[d]) covered += double(e[d]) * double(take) / double(v[d]);
+    left -= take;
+  }
+  coverage_k_ = k;
+  coverage_ = total ? covered / double(total) : 1.0;
+  return coverage_;
+}
+
+// Pin the gathered slice of a source block in L2 for the launches that
+// follow on the compute stream (cudaAccessPolicyWindow, persisting lines;
+// the streamed page arrays are loaded evict-first).  bytes == 0 clears it.
+// SERAPH_L2_PERSIST=0 disables.  Measured: uniform-27 CC 22.3 -> 21.8 ms;
+// PageRank's 128 MB contribution blocks exceed the carve-out (105.9 vs
+// 103.2 ms with it), so K8 does not use it.
+void Engine::l2_window(const void* base, size_t bytes) {
+  if (l2_persist_max_ < 0) {
+    int mx = 0;
+    l2_persist_max_ =
+        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev_) == cudaSuccess ? mx : 0;
+  }
+  const char* e = std::getenv("SERAPH_L2_PERSIST");
+  if (e && std::atoi(e) == 0) bytes = 0;
+  if (!l2_persist_max_ || (bytes == 0 && !l2_window_set_)) return;
+  // the persisting carve-out shrinks the normal L2 for everything else: it
+  // exists only while a window is set
+  if (bytes && !l2_window_set_)
+    SR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(l2_persist_max_)));
+  cudaStreamAttrValue attr{};
+  attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  attr.accessPolicyWindow.num_bytes = bytes;
+  attr.accessPolicyWindow.hitRatio =
+      bytes ? float(std::min(1.0, double(l2_persist_max_) / double(bytes))) : 0.f;
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  SR_CUDA(cudaStreamSetAttribute(cs_, cudaStreamAttributeAccessPolicyWindow, &attr));
+  l2_window_set_ = bytes != 0;
+  if (!bytes) {
+    SR_CUDA(cudaCtxResetPersistingL2Cache());
+    SR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+  }
+}
+
+bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
+  const uint64_t blk = pull_block_verts();
+  if (!blk || !build_src_blocks(blk)) return false;
+  const uint32_t run_id = ++run_id_;
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
+    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
+    if (t1 <= t0) continue;
+    l2_window(values_.p + uint64_t(b) * blk, std::min<uint64_t>(blk, n_ - uint64_t(b) * blk) * 4);
+    PullArgs a{};
+    a.work = next_work_counter();
+    a.tiles = sb_.tiles.p;
+    a.tile_page = sb_.tile_page.p;
+    a.pages = sb_.desc.p;
+    a.seg.n = 1;
+    a.seg.tile_begin[0] = t0;
+    a.seg.task_prefix[0] = 0;
+    a.seg.task_prefix[1] = t1 - t0;
+    a.values = values_.p;
+    a.next = values_.p;
+    a.changed = changed_.p;
+    a.status = status_.p;
+    a.hub_stamp = hub_stamp_.p;
+    a.run_id = run_id;
+    a.ctr = ctr;
+    a.census = census_.p;
+    a.count_dest = b == 0 ? 1u : 0u;
+    a.count_valid = 0;
+    a.k_bfs = k_bfs_;
+    a.s_cc = s_cc_;
+    a.l_sssp = l_sssp_;
+    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    auto* evp = relax_begin();
+    launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
+    SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    if (b == 0 && sb_.n_blocks > 1) {
+      // Probe: blocking pays for gathers only.  If block 0 gathered for < 5 %
+      // of its edges (converged labels/levels skip theirs), finish the pass
+      // with one unblocked sweep instead of n_blocks - 1 more destination
+      // passes (its relaxations are idempotent; the counters restart).
+      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+      SR_CUDA(cudaStreamSynchronize(cs_));
+      const RunCtr& c0 = ctr_h_.p[0];
+      if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
+        SR_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RunCtr), cs_));
+        l2_window(nullptr, 0);
+        return false;
+      }
+    }
+  }
+  l2_window(nullptr, 0);
+  return true;
+}
+
+std::pair<cudaEvent_t, cudaEvent_t>* Engine::relax_begin() {
+  if (!profile_kernels_) return nullptr;
+  if (relax_ev_used_ == relax_ev_.size()) {
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    SR_CUDA(cudaEventCreate(&e.first));
+    SR_CUDA(cudaEventCreate(&e.second));
+    relax_ev_.push_back(e);
+  }
+  auto* evp = &relax_ev_[relax_ev_used_++];
+  SR_CUDA(cudaEventRecord(evp->first, cs_));
+  return evp;
+}
+
+void Engine::pr_blocked_pass(float base, float damp) {
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
+    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
+    if (t1 <= t0) continue;
+    PrArgs a{};
+    a.work = next_work_counter();
+    a.tiles = sb_.tiles.p;
+    a.tile_page = sb_.tile_page.p;
+    a.pages = sb_.desc.p;
+    a.seg.n = 1;
+    a.seg.tile_begin[0] = t0;
+    a.seg.task_prefix[0] = 0;
+    a.seg.task_prefix[1] = t1 - t0;
+    a.contrib_in = contrib_a_.p;
+    a.rank_out = rank_b_.p;
+    a.contrib_out = contrib_b_.p;
+    a.inv_outdeg = inv_outdeg_.p;
+    a.hub_sum = hub_sum_.p;
+    a.acc = sb_.acc.p;
+    a.ctr = nullptr;
+    a.base = base;
+    a.damp = damp;
+    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
+    if (profile_kernels_) {
+      if (relax_ev_used_ == relax_ev_.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        SR_CUDA(cudaEventCreate(&e.first));
+        SR_CUDA(cudaEventCreate(&e.second));
+        relax_ev_.push_back(e);
+      }
+      evp = &relax_ev_[relax_ev_used_++];
+      SR_CUDA(cudaEventRecord(evp->first, cs_));
+    }
+    launch_pr_pull(a, std::max(grid, 1), cs_);
+    SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+  }
+  launch_pr_block_finalize(own_lo_, own_hi_, sb_.acc.p, rank_b_.p, contrib_b_.p, inv_outdeg_.p,
+                           base, damp, cs_);
+}
+
+// ---------------------------------------------------------------------------
+// PageRank (new algorithm; conventions pinned in DESIGN.md §2)
+// ---------------------------------------------------------------------------
+void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
+                          std::vector<sr_pass_stats>& passes) {
+  uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
+  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
+  const bool blocked = build_src_blocks(pr_blk);
+  const auto wall0 = std::chrono::steady_clock::now();
+  SR_CUDA(cudaEventRecord(ev_start_, cs_));
+  launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
+  launch_pr_init(rank_a_.p, contrib_a_.p, inv_outdeg_.p, n_, n_ ? float(1.0 / double(n_)) : 0.f, cs_);
+  if (n_hubs_) SR_CUDA(cudaMemsetAsync(hub_sum_.p, 0, n_hubs_ * 4, cs_));
+  // The iterations are enqueued back to back with no host sync in between
+  // (the copy stream prefetches the next iteration's pages while the current
+  // one computes); each iteration's counters get their own slice of the
+  // counter arena, read back once at the end.
+  ctr_used_ = 0;
+  SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
+  std::vector<uint32_t> ctr_begin;
+  for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
+    ctr_begin.push_back(ctr_used_);
+    if (attached()) {
+      SR_CUDA(cudaMemsetAsync(rank_b_.p, 0, size_t(n_) * 4, cs_));
+      SR_CUDA(cudaMemsetAsync(contrib_b_.p, 0, size_t(n_) * 4, cs_));
+    }
+    PassOut po;
+    const float base = float((1.0 - cfg.pr_damping) / double(n_));
+    if (blocked) {
+      pr_blocked_pass(base, float(cfg.pr_damping));
+      po.kernel_runs = sb_.n_blocks * pages_.size();
+      if (!first_touch_done_) {
+        for (const auto& pm : pages_) {
+          po.pages_transferred += 1;
+          po.bytes_transferred += pm.bytes;
+        }
+        first_touch_done_ = true;
+      }
+    } else {
+      po = dense_pass_wall(cfg, kGateOff, false, it, true);
+      launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
+                             inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
+    }
+    exchange_round(true);
+    sr_pass_stats st{};
+    st.pass_index = it;
+    st.kind = SR_PASS_DENSE_PULL;
+    if (blocked) {  // every destination and edge once per iteration
+      st.attempts = n_;
+      st.edges_read = page_edges_total_;
+      gathers_total_ += page_edges_total_;
+    }
+    st.changed_vertices = n_;
+    m.pages_transferred += po.pages_transferred;
+    m.bytes_transferred += po.bytes_transferred;
+    m.kernel_runs += po.kernel_runs;
+    m.passes += 1;
+    m.dense_passes += 1;
+    if (blocked) {
+      m.update_attempts += st.attempts;
+      m.edges_read += st.edges_read;
+    }
+    passes.push_back(st);
+    std::swap(rank_a_.p, rank_b_.p);
+    std::swap(contrib_a_.p, contrib_b_.p);
+  }
+  SR_CUDA(cudaEventRecord(ev_stop_, cs_));
+  if (ranks_out)
+    SR_CUDA(cudaMemcpyAsync(ranks_out, rank_a_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  if (ctr_used_)
+    SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
+                            cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  ctr_begin.push_back(ctr_used_);
+  for (size_t it = 0; it + 1 < ctr_begin.size(); ++it) {
+    if (blocked) continue;  // counted analytically above
+    sr_pass_stats& st = passes[passes.size() - (ctr_begin.size() - 1) + it];
+    for (uint32_t i = ctr_begin[it]; i < ctr_begin[it + 1]; ++i) {
+      gathers_total_ += ctr_h_.p[i].gathers;
+      st.attempts += ctr_h_.p[i].attempts;
+      st.edges_read += ctr_h_.p[i].edges;
+    }
+    m.update_attempts += st.attempts;
+    m.edges_read += st.edges_read;
+  }
+  float ms = 0;
+  SR_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_stop_));
+  m.device_seconds = ms * 1e-3;
+  if (ranks_out) m.d2h_bytes = uint64_t(n_) * 4;
+  m.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+}
+
+}  // namespace seraph
