@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--budget-gb", type=float, default=0.0, help="forced HBM budget for pages")
     p.add_argument("--pr-iters", type=int, default=20)
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--exchange", default="allreduce", choices=["allreduce", "peer"],
+                   help="N>1: MIN all-reduce of the replicas per round, or peer stores over "
+                        "CUDA IPC + barrier")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
@@ -253,6 +256,7 @@ def run_ours(args, rank, world, local_rank):
             uid[0] = bytes(buf)
         dist.broadcast_object_list(uid, src=0)
         eng.attach_world(rank, world, uid[0])
+        eng.set_exchange(args.exchange == "peer")
     W = workload(args, eng)
     csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
     if not W["loaded"]:
@@ -439,7 +443,8 @@ def run_ours(args, rank, world, local_rank):
                          ("inputs larger than L2 (CSC %.2f GB vs %d MB L2)"
                           % (graph_bytes / 1e9, info["l2_bytes"] >> 20)),
                    "graph_build_s": round(W["build_s"], 2), "graph_build": W["graph"],
-                   "parallelism": f"dp{world}" if world > 1 else "single"},
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   **({"exchange": args.exchange} if world > 1 else {})},
         "time_to_converge_ms": round(ms_per_step, 4),
         "gteps_read": round(gteps_read, 4),
         "passes": {"total": last.passes, "dense": last.dense_passes, "sparse": last.sparse_passes,

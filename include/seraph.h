@@ -321,8 +321,17 @@ int sr_attach_world(sr_ctx* ctx, int rank, int world, const uint8_t unique_id[12
  * (any devices, including one shared GPU) whose exchange all-reduces go
  * through host memory instead of NCCL; `group` names the world.  Each rank's
  * sr_run must be driven from its own thread.  Exercises the sharded round
- * protocol of sr_attach_world where NCCL cannot (two ranks on one GPU). */
-int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group);
+ * protocol of sr_attach_world where NCCL cannot (two ranks on one GPU).
+ * flags & SR_EXCHANGE_PEER: the relax kernels store every improvement
+ * straight into the other ranks' value replicas (peer memory) and a round
+ * ends with a barrier instead of the |V|-sized MIN all-reduce. */
+#define SR_EXCHANGE_PEER 1
+int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group, int flags);
+/* Exchange of an attached world (either transport): 0 = |V|-sized MIN
+ * all-reduce per round (default), SR_EXCHANGE_PEER = peer stores + barrier
+ * (NCCL worlds map the peers' replicas with CUDA IPC; all GPUs of one node
+ * must have peer access over NVLink). */
+int sr_set_exchange(sr_ctx* ctx, int flags);
 
 /* ---- host-side graph utilities (no GPU needed) ------------------------- */
 /* Edge-balanced contiguous cut of the destination space into `parts`

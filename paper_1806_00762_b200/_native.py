@@ -240,7 +240,8 @@ SIGNATURES = {
     "sr_bench_h2d": (C.c_int, [C.c_int, _U64, _U32, C.POINTER(_D)]),
     "sr_flush_l2": (C.c_int, [_VP, _U64]),
     "sr_attach_world": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(C.c_uint8 * 128)]),
-    "sr_attach_loopback": (C.c_int, [_VP, C.c_int, C.c_int, C.c_char_p]),
+    "sr_attach_loopback": (C.c_int, [_VP, C.c_int, C.c_int, C.c_char_p, C.c_int]),
+    "sr_set_exchange": (C.c_int, [_VP, C.c_int]),
     "sr_shard_plan": (C.c_int, [_U32, _VP, _U32, _VP]),
     "sr_rmat_generate": (C.c_int, [C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP, C.c_int]),
     "sr_weights_generate": (C.c_int, [_U64, _U64, _U32, _U32, _VP, C.c_int]),

@@ -146,9 +146,16 @@ int sr_load_srph(sr_ctx* ctx, const char* path, uint32_t cap, int flags) {
   return guard(ctx, [&] { ctx->eng->load_srph(path, cap, flags & SR_BUILD_CSR_EDGES); });
 }
 
-int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group) {
+int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group, int flags) {
   if (!ctx || !group) return SR_E_CONFIG;
-  return guard(ctx, [&] { ctx->eng->attach_loopback(rank, world, group); });
+  return guard(ctx, [&] {
+    ctx->eng->attach_loopback(rank, world, group, (flags & SR_EXCHANGE_PEER) != 0);
+  });
+}
+
+int sr_set_exchange(sr_ctx* ctx, int flags) {
+  if (!ctx) return SR_E_CONFIG;
+  return guard(ctx, [&] { ctx->eng->set_exchange((flags & SR_EXCHANGE_PEER) != 0); });
 }
 
 int sr_graph_info_get(const sr_ctx* ctx, sr_graph_info* out) {

@@ -87,6 +87,8 @@ struct PullArgs {
   Census* census;          // min_changed accumulator
   uint32_t count_dest;     // 1: count attempts/skipped (0 on source blocks > 0)
   uint32_t count_valid;    // 1: count valid updates (0 in source-blocked passes)
+  uint32_t* const* peers;  // peer exchange: the other ranks' value replicas (else null)
+  uint32_t n_peers;
   unsigned long long k_bfs;  // strong thresholds (predictor.hpp:47-52)
   uint32_t s_cc;
   uint32_t l_sssp;
@@ -132,6 +134,8 @@ struct PushArgs {
   uint32_t* q_list;
   const uint32_t* outdeg;
   uint8_t* logstate;  // weak predictor: PredictionLog of first-time changes (else null)
+  uint32_t* const* peers;  // peer exchange: the other ranks' value replicas (else null)
+  uint32_t n_peers;
 };
 constexpr uint32_t kPushChunk = 256;  // flattened edges per warp task
 

@@ -100,6 +100,8 @@ Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
+  for (void* p : ipc_ptrs_)
+    if (p) cudaIpcCloseMemHandle(p);
   if (comm_) nccl().CommDestroy(comm_);
   for (cudaEvent_t e : page_events_) cudaEventDestroy(e);
   for (auto& s : slots_) {
@@ -673,6 +675,8 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.census = census_.p;
       a.count_dest = 1;
       a.count_valid = 1;
+      a.peers = peer_list();
+      a.n_peers = n_peers_;
       a.k_bfs = k_bfs_;
       a.s_cc = s_cc_;
       a.l_sssp = l_sssp_;
@@ -1031,6 +1035,8 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
     a.changed = changed_.p;
     a.ctr = slot;
     a.census = census_.p;
+    a.peers = peer_list();
+    a.n_peers = n_peers_;
     if (queue) {
       a.stamp = stamp_.p;
       a.epoch = fq_epoch_;
@@ -1051,6 +1057,30 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
 void Engine::exchange_round(bool pagerank) {
   if (!attached()) return;  // attached to a world (any size, incl. 1): merge every round
   SR_CUDA(cudaSetDevice(dev_));
+  if (n_peers_ && !pagerank) {
+    // peer exchange: every improvement is already in every replica once all
+    // ranks' kernels of the round have finished -- barrier, then only the
+    // scalars (min_changed, counters) are reduced
+    round_barrier();
+    if (loop_) {
+      loopback_allreduce(loop_, rank_, &census_.p->min_changed, 1, kLoopU32, kLoopMin, cs_);
+      loopback_allreduce(loop_, rank_, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8),
+                         kLoopU64, kLoopSum, cs_);
+    } else {
+      const NcclApi& nc = nccl();
+      nc.GroupStart();
+      ncclResult_t r = nc.AllReduce(&census_.p->min_changed, &census_.p->min_changed, 1,
+                                    ncclUint32, ncclMin, comm_, cs_);
+      if (r == ncclSuccess && ctr_used_)
+        r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), ncclUint64,
+                         ncclSum, comm_, cs_);
+      nc.GroupEnd();
+      if (r != ncclSuccess)
+        throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
+    }
+    launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
+    return;
+  }
   if (loop_) {  // in-process loopback (tests): the same reductions through host memory
     if (pagerank) {
       loopback_allreduce(loop_, rank_, rank_b_.p, n_, kLoopF32, kLoopSum, cs_);
@@ -1117,6 +1147,8 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   vmodel_.edges_per_unit_per_worker = cfg.edges_per_time_unit_per_worker;
   vmodel_.workers = cfg.worker_count;
   alloc_run_state(cfg);
+  if (cfg.algo != SR_ALGO_PAGERANK) setup_peers();  // every rank runs the same program
+  else n_peers_ = 0;
   const uint64_t launches0 = kernel_launch_count();
   if (cfg.algo == SR_ALGO_PAGERANK) run_pagerank(cfg, ranks_out, m, passes);
   else run_traversal(cfg, values_out, m, passes);
@@ -1200,6 +1232,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
     if (attached())
       SR_CUDA(cudaMemcpyAsync(round_snap_.p, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToDevice, cs_));
+    if (n_peers_) round_barrier();  // no rank writes into a replica before its owner's snapshot
   };
   auto after_census = [&]() {
     f_count = census_h_.p->changed;
@@ -1524,12 +1557,73 @@ void Engine::flush_l2(uint64_t bytes) {
   SR_CUDA(cudaStreamSynchronize(cs_));
 }
 
-void Engine::attach_loopback(int rank, int world, const std::string& key) {
+void Engine::attach_loopback(int rank, int world, const std::string& key, bool peer_exchange) {
   if (world < 1 || rank < 0 || rank >= world) throw EngineError(SR_E_CONFIG, "bad rank/world");
   if (pages_loaded_) throw EngineError(SR_E_CONFIG, "attach must precede load_pages");
   loop_ = loopback_group(key, world);
   rank_ = rank;
   world_ = world;
+  peer_xchg_ = peer_exchange;
+}
+
+// Peer exchange: every rank learns the device addresses of the other ranks'
+// value replicas (the loopback world shares one address space; an NCCL world
+// would map them with CUDA IPC handles).  Re-run each run: values_ may move.
+void Engine::setup_peers() {
+  n_peers_ = 0;
+  if (!peer_xchg_ || !attached() || world_ < 2) return;
+  std::vector<uint32_t*> others;
+  if (loop_) {
+    const std::vector<void*> all = loopback_allgather_ptr(loop_, rank_, values_.p);
+    for (int r = 0; r < world_; ++r)
+      if (r != rank_) others.push_back(static_cast<uint32_t*>(all[size_t(r)]));
+  } else {
+    // NCCL world: all-gather the CUDA IPC handles of every rank's replica and
+    // map the peers' (re-mapped only when a replica moved)
+    const NcclApi& nc = nccl();
+    cudaIpcMemHandle_t mine;
+    SR_CUDA(cudaIpcGetMemHandle(&mine, values_.p));
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    ipc_buf_.reserve(hs * size_t(world_ + 1));
+    SR_CUDA(cudaMemcpyAsync(ipc_buf_.p + hs * world_, &mine, hs, cudaMemcpyHostToDevice, cs_));
+    const ncclResult_t r = nc.AllGather(ipc_buf_.p + hs * world_, ipc_buf_.p, hs, ncclUint8,
+                                        comm_, cs_);
+    if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(world_));
+    SR_CUDA(cudaMemcpyAsync(all.data(), ipc_buf_.p, hs * world_, cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    ipc_handles_.resize(size_t(world_));
+    ipc_ptrs_.resize(size_t(world_), nullptr);
+    for (int q = 0; q < world_; ++q) {
+      if (q == rank_) continue;
+      if (!ipc_ptrs_[q] || std::memcmp(&ipc_handles_[q], &all[q], hs) != 0) {
+        if (ipc_ptrs_[q]) cudaIpcCloseMemHandle(ipc_ptrs_[q]);
+        SR_CUDA(cudaIpcOpenMemHandle(&ipc_ptrs_[q], all[q], cudaIpcMemLazyEnablePeerAccess));
+        ipc_handles_[q] = all[q];
+      }
+      others.push_back(static_cast<uint32_t*>(ipc_ptrs_[q]));
+    }
+  }
+  peers_dev_.reserve(others.size());
+  SR_CUDA(cudaMemcpy(peers_dev_.p, others.data(), others.size() * sizeof(uint32_t*),
+                     cudaMemcpyHostToDevice));
+  n_peers_ = uint32_t(others.size());
+}
+
+// Every rank's work enqueued so far has finished (loopback: host barrier
+// after a stream sync; NCCL: a one-word all-reduce on the compute stream,
+// which also fences this rank's earlier peer stores before later kernels).
+void Engine::round_barrier() {
+  if (loop_) {
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    loopback_barrier(loop_);
+    return;
+  }
+  barrier_word_.reserve(1);
+  const NcclApi& nc = nccl();
+  const ncclResult_t r =
+      nc.AllReduce(barrier_word_.p, barrier_word_.p, 1, ncclUint32, ncclMax, comm_, cs_);
+  if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
 }
 
 void Engine::attach_world(int rank, int world, const uint8_t id[128]) {

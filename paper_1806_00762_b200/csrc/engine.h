@@ -149,7 +149,7 @@ class Engine {
                     uint32_t* in_src, uint32_t* in_w);
   void bench_pull_sweep(int algo, uint32_t reps, double* ms, uint64_t* edges);
   void attach_world(int rank, int world, const uint8_t id[128]);
-  void attach_loopback(int rank, int world, const std::string& key);
+  void attach_loopback(int rank, int world, const std::string& key, bool peer_exchange);
   void flush_l2(uint64_t bytes);
   DBuf<uint8_t> l2_flush_;
   unsigned flush_gen_ = 0;
@@ -338,6 +338,24 @@ class Engine {
   int rank_ = 0, world_ = 1;
   ncclComm_t comm_ = nullptr;
   LoopbackGroup* loop_ = nullptr;  // in-process loopback collective (tests)
+  // peer exchange: improvements are stored straight into the other ranks'
+  // value replicas; a round ends with a barrier instead of a MIN all-reduce
+  bool peer_xchg_ = false;
+  DBuf<uint32_t*> peers_dev_;
+  uint32_t n_peers_ = 0;
+  void setup_peers();
+  void round_barrier();  // all ranks reached this point of the round (peer exchange)
+  // NCCL worlds: the peers' replicas mapped through CUDA IPC (cached per handle)
+  std::vector<cudaIpcMemHandle_t> ipc_handles_;
+  std::vector<void*> ipc_ptrs_;
+  DBuf<unsigned char> ipc_buf_;
+  DBuf<uint32_t> barrier_word_;
+
+ public:
+  void set_exchange(bool peer) { peer_xchg_ = peer; }
+
+ private:
+  uint32_t* const* peer_list() const { return n_peers_ ? peers_dev_.p : nullptr; }
   bool attached() const { return comm_ != nullptr || loop_ != nullptr; }
   uint32_t own_lo_ = 0, own_hi_ = 0;  // owned destination range
 };

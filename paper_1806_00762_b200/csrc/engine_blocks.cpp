@@ -235,6 +235,8 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     a.census = census_.p;
     a.count_dest = b == 0 ? 1u : 0u;
     a.count_valid = 0;
+    a.peers = peer_list();
+    a.n_peers = n_peers_;
     a.k_bfs = k_bfs_;
     a.s_cc = s_cc_;
     a.l_sssp = l_sssp_;

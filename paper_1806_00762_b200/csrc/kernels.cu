@@ -69,6 +69,21 @@ __device__ __forceinline__ uint32_t warp_min(uint32_t x) { return __reduce_min_s
 __device__ __forceinline__ uint32_t gather_rw(const uint32_t* p) { return *p; }
 __device__ __forceinline__ float gather_ro(const float* p) { return __ldg(p); }
 
+// Peer exchange (sr_attach_* with the peer transport): an improvement is
+// written straight into every other rank's replica of the value array (P2P
+// over NVLink between GPUs; same-device pointers in the loopback world), so
+// the round ends with a barrier instead of a |V|-sized MIN all-reduce.  A
+// pulled destination has one writer per round (its owner): plain stores;
+// hub chunks and pushes may race: atomicMin.
+__device__ __forceinline__ void peer_store(uint32_t* const* peers, uint32_t n, uint32_t v,
+                                           uint32_t x) {
+  for (uint32_t r = 0; r < n; ++r) __stcg(peers[r] + v, x);
+}
+__device__ __forceinline__ void peer_min(uint32_t* const* peers, uint32_t n, uint32_t v,
+                                         uint32_t x) {
+  for (uint32_t r = 0; r < n; ++r) atomicMin(peers[r] + v, x);
+}
+
 // VertexProgram::combine (programs.hpp:31-45): saturating at kUnreached.
 template <int A>
 __device__ __forceinline__ uint32_t combine(uint32_t a, uint32_t w) {
@@ -295,6 +310,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           } else {
             const uint32_t old = atomicMin(a.values + v, best);
             improved = best < old;
+            if (improved && a.n_peers) peer_min(a.peers, a.n_peers, v, best);
           }
           if (improved) {
             a.changed[v] = 1;
@@ -431,8 +447,12 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         const uint32_t b = best_of[i];
         if ((l >> 31) && b < s_cur[warp][i]) {
           const uint32_t v = vb + (l & 0x7fffffffu);
-          if (DET) a.next[v] = b;
-          else a.values[v] = b;
+          if (DET) {
+            a.next[v] = b;
+          } else {
+            a.values[v] = b;
+            if (a.n_peers) peer_store(a.peers, a.n_peers, v, b);
+          }
           a.changed[v] = 1;
           c.valid += a.count_valid;
           lane_min = min(lane_min, b);
@@ -951,6 +971,7 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
           if (cand < old) {
             c.valid += 1;
             lane_min = min(lane_min, cand);
+            if (a.n_peers) peer_min(a.peers, a.n_peers, v, cand);
             if (a.stamp) {
               if (atomicMax(a.stamp + v, a.epoch) < a.epoch) {  // first change this pass
                 const uint32_t d = __ldg(a.outdeg + v);

@@ -21,6 +21,7 @@ struct LoopbackGroup {
   int arrived = 0;
   uint64_t generation = 0;
   std::vector<std::vector<unsigned char>> slots;
+  std::vector<void*> ptrs;
 
   // generation barrier over the `world` ranks
   void barrier() {
@@ -68,8 +69,19 @@ LoopbackGroup* loopback_group(const std::string& key, int world) {
     g = std::make_unique<LoopbackGroup>();
     g->world = world;
     g->slots.resize(size_t(world));
+    g->ptrs.resize(size_t(world));
   }
   return g.get();
+}
+
+void loopback_barrier(LoopbackGroup* g) { g->barrier(); }
+
+std::vector<void*> loopback_allgather_ptr(LoopbackGroup* g, int rank, void* mine) {
+  g->ptrs[size_t(rank)] = mine;
+  g->barrier();
+  std::vector<void*> all = g->ptrs;
+  g->barrier();  // everyone has copied before the next allgather overwrites
+  return all;
 }
 
 void loopback_allreduce(LoopbackGroup* g, int rank, void* buf, size_t count, LoopType t, LoopOp op,

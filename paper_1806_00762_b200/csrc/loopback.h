@@ -9,6 +9,7 @@
 
 #include <cstddef>
 #include <string>
+#include <vector>
 
 namespace seraph {
 
@@ -23,5 +24,9 @@ LoopbackGroup* loopback_group(const std::string& key, int world);
 // is synchronised first); every rank of the group must call it in the same order.
 void loopback_allreduce(LoopbackGroup* g, int rank, void* buf, size_t count, LoopType t, LoopOp op,
                         cudaStream_t s);
+// Host barrier over the group's ranks.
+void loopback_barrier(LoopbackGroup* g);
+// Every rank's pointer, indexed by rank (peer exchange: the value replicas).
+std::vector<void*> loopback_allgather_ptr(LoopbackGroup* g, int rank, void* mine);
 
 }  // namespace seraph

@@ -668,14 +668,22 @@ class Engine:
         return (CsrGraph(n, out_off, nbr, ow),
                 pages_from_csc(n, cap, in_off, srcs, iw, local), in_off, srcs, iw)
 
-    def attach_loopback(self, rank: int, world: int, group: str) -> None:
+    def attach_loopback(self, rank: int, world: int, group: str, peer: bool = False) -> None:
         """Test/dev: rank of an in-process world whose exchange goes through host
-        memory (sr_attach_loopback); drive each rank's run() from its own thread."""
-        N.check(N.lib.sr_attach_loopback(self._h, rank, world, group.encode()), self._h)
+        memory (sr_attach_loopback); drive each rank's run() from its own thread.
+        peer=True: improvements go straight into the other ranks' replicas."""
+        N.check(N.lib.sr_attach_loopback(self._h, rank, world, group.encode(), 1 if peer else 0),
+                self._h)
 
     def attach_world(self, rank: int, world: int, unique_id: bytes) -> None:
         uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         N.check(N.lib.sr_attach_world(self._h, rank, world, C.byref(uid)), self._h)
+
+    def set_exchange(self, peer: bool) -> None:
+        """Exchange of the attached world: False = MIN all-reduce of the value
+        replicas per round (default); True = peer stores into the other ranks'
+        replicas + a barrier (NCCL worlds: replicas mapped over CUDA IPC)."""
+        N.check(N.lib.sr_set_exchange(self._h, 1 if peer else 0), self._h)
 
     # ---- run ----
     def run(self, program: VertexProgram, config: EngineConfig, values_out=None,

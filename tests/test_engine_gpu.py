@@ -761,13 +761,13 @@ def test_scale20_parity_device_built(case, monkeypatch):
                 assert np.array_equal(r.values, want), (kind, pred)
 
 
-def _run_world(world, g, prog, cfg, cap, key):
+def _run_world(world, g, prog, cfg, cap, key, peer=False):
     """`world` contexts on cuda:0 attached as one in-process world (loopback
     collective), each loaded with its shard and run from its own thread."""
     import threading
     engines = [ps.Engine(0) for _ in range(world)]
     for r, e in enumerate(engines):
-        e.attach_loopback(r, world, key)
+        e.attach_loopback(r, world, key, peer)
         e.load(*built(g, cap))
     out, errs = [None] * world, []
 
@@ -789,8 +789,10 @@ def _run_world(world, g, prog, cfg, cap, key):
     return out
 
 
-@pytest.mark.parametrize("world,blocked", [(2, False), (3, False), (2, True), (3, True)])
-def test_sharded_rounds_loopback_world(world, blocked, monkeypatch):
+@pytest.mark.parametrize("world,blocked,peer", [(2, False, False), (3, False, False),
+                                               (2, True, False), (3, True, False),
+                                               (2, False, True), (3, True, True)])
+def test_sharded_rounds_loopback_world(world, blocked, peer, monkeypatch):
     """The multi-GPU round protocol of sr_attach_world (edge-balanced
     destination shards, per-round merge of the replicated values, identical
     decisions on every rank) run on hardware: `world` contexts on one GPU,
@@ -815,13 +817,13 @@ def test_sharded_rounds_loopback_world(world, blocked, monkeypatch):
                 k += 1
                 res = _run_world(world, g, program_for(kind, 2, g),
                                  cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex),
-                                 n // 16, f"w{world}-{int(blocked)}-{k}")
+                                 n // 16, f"w{world}-{int(blocked)}-{int(peer)}-{k}", peer)
                 for r in res:
                     assert np.array_equal(r.values, want), (kind, pred, ex)
                 assert len({r.metrics.passes for r in res}) == 1  # same decisions
     pr = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
     res = _run_world(world, pr, ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL),
-                     n // 16, f"w{world}-{int(blocked)}-pr")
+                     n // 16, f"w{world}-{int(blocked)}-{int(peer)}-pr", peer)
     ref = O.pagerank(n, src, dst, 20, 0.85)
     for r in res:
         assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
