@@ -92,6 +92,7 @@ struct PullArgs {
   unsigned long long k_bfs;  // strong thresholds (predictor.hpp:47-52)
   uint32_t s_cc;
   uint32_t l_sssp;
+  uint32_t src_floor;  // SSSP: lower bound of every source that can still improve (0 = none)
 };
 
 struct PrArgs {

@@ -680,6 +680,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.k_bfs = k_bfs_;
       a.s_cc = s_cc_;
       a.l_sssp = l_sssp_;
+      a.src_floor = floor_sssp_;
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());
@@ -1184,6 +1185,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   k_bfs_ = 0;
   s_cc_ = 0;
   l_sssp_ = 0;
+  floor_sssp_ = 0;
   last_gather_frac_ = 1.0;  // the first dense pass gathers
   ctr_used_ = 0;
   if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_ && !weak) {  // weak: census seeds the DFA histogram
@@ -1397,6 +1399,18 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
       k_bfs_ += 1;
       if (algo_ == SR_ALGO_SSSP || algo_ == SR_ALGO_CC) {
         (algo_ == SR_ALGO_SSSP ? l_sssp_ : s_cc_) = census_h_.p->min_changed;
+        SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 4, cs_));
+      }
+    }
+    // K1's source floor (kernels.cu source_floor): the smallest value written
+    // since the previous dense pass bounds every source that can still
+    // improve a destination.  Not under the weak predictor, whose dormant
+    // destinations miss relaxations until a recovery sweep.
+    if (algo_ == SR_ALGO_SSSP && !weak) {
+      if (strong) {
+        floor_sssp_ = l_sssp_;
+      } else {
+        floor_sssp_ = census_h_.p->min_changed;
         SR_CUDA(cudaMemsetAsync(&census_.p->min_changed, 0xff, 4, cs_));
       }
     }

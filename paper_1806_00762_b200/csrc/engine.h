@@ -281,6 +281,7 @@ class Engine {
   bool det_ = false;
   unsigned long long k_bfs_ = 0;
   uint32_t s_cc_ = 0, l_sssp_ = 0;
+  uint32_t floor_sssp_ = 0;  // K1's source floor (PullArgs::src_floor)
   VWindow vwin_;
   VClock vclock_;
   VModel vmodel_;

@@ -240,6 +240,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     a.k_bfs = k_bfs_;
     a.s_cc = s_cc_;
     a.l_sssp = l_sssp_;
+    a.src_floor = floor_sssp_;
     const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
                                             (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
     auto* evp = relax_begin();

@@ -160,6 +160,29 @@ __device__ __forceinline__ uint32_t candidate_floor() {
   return A == kBfs ? 1u : 0u;
 }
 
+// SSSP source floor (PullArgs::src_floor, set by the host from the smallest
+// value written since the previous dense pass -- under the strong predictor
+// that is its l; 0 under the weak predictor).  Every pass relaxes every edge
+// whose source changed in the previous pass (dense pulls see all in-edges of
+// every gated-in destination, the strong gate only drops destinations below
+// l, pushes cover the whole frontier), so a source that did not change is
+// already folded into its destinations; the ones that did hold values >= the
+// floor, and every value written later is >= floor + 1.  Hence a candidate is
+// >= floor + w: destinations at <= floor + 1 cannot improve and an edge with
+// w >= value - floor cannot improve its destination -- neither is gathered.
+// Attempt/skip/edge counters and the values are unchanged (the reference's
+// accounting); only `gathers` drops.
+template <int A>
+__device__ __forceinline__ uint32_t source_floor(const PullArgs& a) {
+  return A == kSssp ? a.src_floor : 0u;
+}
+template <int A>
+__device__ __forceinline__ uint32_t dest_floor(const PullArgs& a) {
+  if (A != kSssp) return candidate_floor<A>();
+  const uint32_t f = a.src_floor;
+  return f >= kUnreached - 1 ? kUnreached : f + 1;  // weights >= 1 (graph.cpp:9-22)
+}
+
 // End-of-kernel flush: warp sums -> shared memory -> one atomic per counter
 // per block (thousands of same-address atomics per launch would serialise).
 // `scratch` reuses the caller's tile shared memory (>= 40 words): extra
@@ -270,7 +293,8 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           c.skipped += !att & a.count_dest;
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
-        if (!att || cur <= candidate_floor<A>()) continue;
+        if (!att || cur <= dest_floor<A>(a)) continue;
+        const uint32_t thr = cur - source_floor<A>(a);  // live edges: w < thr
         // lanes take aligned 8-edge runs (two uint4 loads of sources and
         // weights), drop edges that cannot improve, gather the rest back to
         // back (~47 % of RMAT in-edges are in hub chunks)
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
           unsigned live = 0;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t)
-            if (p0 + t >= tile.x && p0 + t < tile.y && (A != kSssp || wv[t] < cur))
+            if (p0 + t >= tile.x && p0 + t < tile.y && (A != kSssp || wv[t] < thr))
               live |= 1u << t;
           uint32_t sv[kLaneEdges];
 #pragma unroll
@@ -344,7 +368,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         c.attempts += att & a.count_dest;
         c.skipped += (in && !att) & a.count_dest;
         c.edges += att ? deg : 0u;
-        const bool need = att && cur > candidate_floor<A>();  // can it still improve?
+        const bool need = att && cur > dest_floor<A>(a);  // can it still improve?
         const bool has = in && deg > 0;
         const unsigned m = __ballot_sync(kFull, has);
         any_att |= __ballot_sync(kFull, has && need);
@@ -408,13 +432,16 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             const uint32_t sv_idx[kLaneEdges] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
             const uint32_t wv[kLaneEdges] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
             if (A == kSssp) {
-              // values are >= 0, so an edge with w >= the destination's value
-              // cannot improve it: no gather (the wavefront-bound part of K1)
+              // sources are >= source_floor, so an edge with w >= value - floor
+              // cannot improve its destination: no gather (the wavefront-bound
+              // part of K1).  Live entries have value > floor + 1; the others'
+              // bits are already clear, so their wrap-around is harmless.
+              const uint32_t fl = source_floor<A>(a);
               uint32_t et = ent0, cur_t = s_cur[warp][ent0];
 #pragma unroll
               for (int t = 0; t < kLaneEdges; ++t) {
                 if (adv >> t & 1u) cur_t = s_cur[warp][++et];
-                if (wv[t] >= cur_t) live &= ~(1u << t);
+                if (wv[t] >= cur_t - fl) live &= ~(1u << t);
               }
             }
             uint32_t sv[kLaneEdges];

@@ -730,6 +730,35 @@ def test_frontier_queue_matches_flag_path(monkeypatch):
                         assert rq.metrics.per_pass[-1].changed_vertices == 0
 
 
+def test_sssp_saturating_weights(engine, monkeypatch):
+    """combine() saturates at kUnreached instead of wrapping (programs.hpp:38-42,
+    test_algorithms.cpp:56): weights near 2^32 on every device path -- range
+    tiles, hub chunks (a destination with > 1024 in-edges), the push, the
+    single-block tail loop and source-blocked pulls."""
+    rng = np.random.default_rng(97)
+    n, m = 6000, 60000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    dst[:3000] = 7  # hub: 3000+ in-edges -> hub chunks
+    big = rng.integers(1 << 30, 1 << 32, m, dtype=np.uint64).astype(np.uint32)
+    small = rng.integers(1, 17, m).astype(np.uint32)
+    w = np.where(rng.random(m) < 0.5, big, small).astype(np.uint32)
+    w[rng.integers(0, m, 200)] = 0xFFFFFFFF
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, 1024)
+    want = oracle_values(el, ps.AlgoKind.SSSP, 0)
+    assert (want == 0xFFFFFFFF).any() and (want > (1 << 31)).any() and (want < 64).sum() > 1
+    for pol in ps.ExecutionPolicy:
+        for pred in PREDS:
+            r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True),
+                                 cfg_of(pred=pred, execution=pol, clock=ps.ClockMode.WALL))
+            assert np.array_equal(r.values, want), (pol, pred)
+    monkeypatch.setenv("SERAPH_PULL_BLOCK_VERTS", "512")
+    r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True),
+                         cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE, clock=ps.ClockMode.WALL))
+    assert np.array_equal(r.values, want)
+
+
 @pytest.mark.parametrize("case", ["rmat20", "uniform20"])
 def test_scale20_parity_device_built(case, monkeypatch):
     """Bigger-graph parity on the production paths: device-generated RMAT /
