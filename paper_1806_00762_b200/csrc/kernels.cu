@@ -1142,6 +1142,9 @@ __device__ __forceinline__ uint8_t log_attempt(uint8_t ls, bool changed,
 
 // Census body (grid-stride over 4096-vertex chunks, 256 threads); per-pass
 // totals go to cz_pass, run-long accumulators (prediction log) to cz_run.
+// ST: the weak predictor's status/log bytes are present (13 partials);
+// otherwise only the frontier counts (5 partials, fewer live registers).
+template <bool ST>
 __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, uint8_t* status,
                                             uint8_t* logstate, const uint32_t* __restrict__ outdeg,
                                             int pass_kind, uint32_t own_lo, uint32_t own_hi,
@@ -1151,12 +1154,14 @@ __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, 
   // grid-stride over 4096-vertex chunks; per-chunk (count, edges) for the
   // compaction scan, run totals reduced once per block (few global atomics)
   __shared__ unsigned long long s_chunk[2][8];
-  __shared__ unsigned long long s_tot[kCensusParts][8];
+  constexpr int kParts = ST ? kCensusParts : 5;
+  __shared__ unsigned long long s_tot[kParts][8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t nchunks = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
   unsigned long long tot[kCensusParts];
 #pragma unroll
   for (int k = 0; k < kCensusParts; ++k) tot[k] = 0;
+  if (!ST) status = logstate = nullptr;
   for (uint32_t ch = bid; ch < nchunks; ch += nblk) {
     const uint32_t v0 = ch * kCensusBlockVerts + threadIdx.x * 16;
     unsigned long long own_push = 0, own_edges = 0;
@@ -1247,12 +1252,12 @@ __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, 
     __syncthreads();
   }
 #pragma unroll
-  for (int k = 0; k < kCensusParts; ++k) {
+  for (int k = 0; k < kParts; ++k) {
     const unsigned long long x = warp_sum(tot[k]);
     if (lane == 0) s_tot[k][w] = x;
   }
   __syncthreads();
-  if (threadIdx.x < kCensusParts) {
+  if (threadIdx.x < kParts) {
     unsigned long long a = 0;
     for (int i = 0; i < 8; ++i) a += s_tot[threadIdx.x][i];
     if (a) {
@@ -1273,14 +1278,15 @@ __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, 
   __syncthreads();  // s_tot is reused by the next call in a persistent loop
 }
 
+template <bool ST>
 __global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
                                                      uint8_t* status, uint8_t* logstate,
                                                      const uint32_t* __restrict__ outdeg,
                                                      int pass_kind, uint32_t own_lo, uint32_t own_hi,
                                                      uint32_t* blk_cnt,
                                                      unsigned long long* blk_edges, Census* cz) {
-  census_body(n, changed, status, logstate, outdeg, pass_kind, own_lo, own_hi, blk_cnt, blk_edges,
-              cz, cz, blockIdx.x, gridDim.x);
+  census_body<ST>(n, changed, status, logstate, outdeg, pass_kind, own_lo, own_hi, blk_cnt,
+                  blk_edges, cz, cz, blockIdx.x, gridDim.x);
 }
 
 // Exclusive scan of the per-chunk (count, edges) pairs by ONE block (any
@@ -1789,8 +1795,12 @@ void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t*
   const uint32_t cap = 148u * 8u;  // measured: 592 / 1184 / 2368 / nb blocks -> 1184 best
   const int grid = int(nb < cap ? nb : cap);
   note_launch();
-  census_kernel<<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind, own_lo,
-                                     own_hi, blk_cnt, blk_edges, c);
+  if (status || logstate)
+    census_kernel<true><<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind,
+                                             own_lo, own_hi, blk_cnt, blk_edges, c);
+  else
+    census_kernel<false><<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind,
+                                              own_lo, own_hi, blk_cnt, blk_edges, c);
 }
 
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,

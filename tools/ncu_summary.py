@@ -53,25 +53,44 @@ def launches(path, tag):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    agg = defaultdict(lambda: [0, 0.0])
+    mi = h.index("Metric Name") if "Metric Name" in h else None
+    seq = []  # (kernel, ns) in launch order, duration rows only
     for r in rows[hdr + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
             continue
-        name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "")
-        agg[name][0] += 1
-        agg[name][1] += v
-    tot = sum(v[1] for v in agg.values())
-    out = {"source": os.path.basename(path), "total_us": round(tot / 1e3, 1),
-           "kernels": [{"kernel": k, "launches": c, "total_us": round(t / 1e3, 1),
-                        "share": round(t / tot, 4)}
-                       for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])]}
+        seq.append((r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", ""), v))
+
+    def table(part):
+        agg = defaultdict(lambda: [0, 0.0])
+        for name, v in part:
+            agg[name][0] += 1
+            agg[name][1] += v
+        tot = sum(v[1] for v in agg.values()) or 1.0
+        return {"total_us": round(tot / 1e3, 1),
+                "kernels": [{"kernel": k, "launches": c, "total_us": round(t / 1e3, 1),
+                             "share": round(t / tot, 4)}
+                            for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])]}
+
+    # one converge run: from the last init_values_kernel up to the next
+    # non-run kernel (fixpoint verification, graph export ...)
+    starts = [i for i, (k, _) in enumerate(seq) if "init_values_kernel" in k]
+    run = []
+    if starts:
+        for k, v in seq[starts[-1]:]:
+            if any(x in k for x in ("verify_kernel", "bench_pull", "flush")):
+                break
+            run.append((k, v))
+    out = {"source": os.path.basename(path), "whole_process": table(seq),
+           "last_converge_run": table(run)}
+    out.update(out["whole_process"])
     with open(os.path.join(PROF, f"{tag}_launches.json"), "w") as fh:
         json.dump(out, fh, indent=1)
-    for k in out["kernels"]:
+    print("last converge run: %.1f us" % out["last_converge_run"]["total_us"])
+    for k in out["last_converge_run"]["kernels"]:
         print(f"{k['kernel']:45s} {k['launches']:5d} {k['total_us']:10.1f}us {100 * k['share']:5.1f}%")
 
 

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--mode", default="baseline")
     ap.add_argument("--predictor", default="strong")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--execution", default="density_switched",
+                    choices=[e.name.lower() for e in ps.ExecutionPolicy])
     ap.add_argument("--sweep", default="", help="VAR=v1,v2,...: time one run per setting")
     ap.add_argument("--verify", action="store_true")
     ap.add_argument("--graph", default="device", choices=["device", "host"])
@@ -41,7 +43,8 @@ def main():
     kind = ps.AlgoKind(bench.ALGOS[a.algo])
     prog = ps.VertexProgram(kind, 0)
     cfg = ps.EngineConfig(predictor=ps.PredictorMode(bench.PREDS[a.predictor]),
-                          clock=ps.ClockMode.WALL, profile_kernels=True)
+                          clock=ps.ClockMode.WALL, profile_kernels=True,
+                          execution=ps.ExecutionPolicy[a.execution.upper()])
     cfg.schedule.kind = ps.ScheduleModeKind(bench.MODES[a.mode])
     if a.sweep:
         var, vals = a.sweep.split("=", 1)

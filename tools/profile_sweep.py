@@ -14,11 +14,14 @@ ap.add_argument("--algo", default="sssp")
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--converge", type=int, default=1)
+ap.add_argument("--uniform", action="store_true")
 a = ap.parse_args()
-ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=False, pages=16, seed=0)
-W = bench.workload(ns)
+ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.algo == "cc" and a.uniform,
+                        pages=16, seed=0, graph="device", lean=False)
 eng = ps.Engine(0)
-eng.load(W["csr"], W["pages"])
+W = bench.workload(ns, eng)
+if not W["loaded"]:
+    eng.load(W["csr"], W["pages"])
 kind = ps.AlgoKind(bench.ALGOS[a.algo])
 cfg = ps.EngineConfig(predictor=ps.PredictorMode.STRONG, clock=ps.ClockMode.WALL)
 for _ in range(a.converge):
