@@ -35,6 +35,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kCensusParts = 13;  // per-block census partials
 constexpr int kLaneEdges = 8;  // consecutive edges per lane per K1 phase-B round
+constexpr uint32_t kBndWords = 33;  // K1 entry-start bitmap words (span <= 1031 positions)
 constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -353,6 +354,14 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
       const uint32_t ebase = tile.x & ~7u;  // 32-byte aligned run grid
       uint32_t n_ent = 0;
       unsigned any_att = 0;
+      // entry starts as a bitmap over the tile's edge positions (span <=
+      // kTileEdgeBudget + 7 -> <= 33 words) + per-word prefix counts: a run's
+      // first entry and its entry steps come from one word, no search
+      uint32_t* bnd = s_pref[warp];        // words [0, kBndWords)
+      uint32_t* wpre = s_pref[warp] + 64;  // words [64, 64 + kBndWords)
+      bnd[lane] = 0;
+      if (lane < kBndWords - 32) bnd[32 + lane] = 0;
+      __syncwarp();
       for (uint32_t base = dl; base < dh; base += 32) {
         const uint32_t i = base + lane;
         const bool in = i < dh;
@@ -374,7 +383,8 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         any_att |= __ballot_sync(kFull, has && need);
         if (has) {
           const uint32_t pos = n_ent + __popc(m & lanemask_lt());
-          s_pref[warp][pos] = lo - ebase;
+          const uint32_t p0 = lo - ebase;
+          atomicOr(bnd + (p0 >> 5), 1u << (p0 & 31));
           s_loc[warp][pos] = i | (need ? 0x80000000u : 0u);
           s_cur[warp][pos] = cur;
           best_of[pos] = kUnreached;
@@ -386,39 +396,41 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
         __syncwarp();
         continue;
       }
-      const uint32_t* pref_of = s_pref[warp];
       const uint32_t* loc_of = s_loc[warp];
       const uint32_t lo_pos = tile.x - ebase;   // first valid position
       const uint32_t span = tile.y - ebase;     // one past the last position
+      {
+        const uint32_t c = __popc(bnd[lane]);
+        const uint32_t inc = warp_incl_scan(c, lane);
+        wpre[lane] = inc - c;
+        if (lane == 31) wpre[32] = inc;
+      }
+      __syncwarp();
 
       // ---- phase B: aligned 8-edge runs, vector loads, masked gathers --------
       for (uint32_t r0 = 0; r0 < span; r0 += 32 * kLaneEdges) {
         const uint32_t pos0 = r0 + lane * kLaneEdges;
         if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
           const uint32_t q = max(pos0, lo_pos);
-          uint32_t lo = 0, hi = n_ent - 1;  // last entry with pref <= q
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (pref_of[mid] <= q) lo = mid;
-            else hi = mid - 1;
-          }
-          // the run's entries: ent0 plus one step at every set bit of adv
-          // (entries hold >= 1 edge), so entry(t) = ent0 + popc(adv & (2<<t)-1)
-          const uint32_t ent0 = lo;
-          uint32_t ent = lo;
-          uint32_t nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
-          bool att_e = (loc_of[ent] >> 31) != 0;
-          unsigned live = 0, adv = 0;
-#pragma unroll
-          for (int t = 0; t < kLaneEdges; ++t) {
-            const uint32_t pp = pos0 + t;
-            if (pp >= nxt && pp < span) {
-              ++ent;
-              adv |= 1u << t;
-              nxt = (ent + 1 < n_ent) ? pref_of[ent + 1] : span;
-              att_e = (loc_of[ent] >> 31) != 0;
+          // runs are 8-aligned, so the run's 8 positions sit in one bitmap word
+          const uint32_t bw = bnd[pos0 >> 5];
+          const uint32_t ent0 = wpre[pos0 >> 5] + __popc(bw & (0xffffffffu >> (31 - (q & 31)))) - 1;
+          // adv bit t: an entry starts at position pos0 + t (after q)
+          const unsigned adv = (bw >> (pos0 & 31)) & (0xffu << (q - pos0 + 1)) & 0xffu;
+          const uint32_t hi_t = min(span - pos0, (uint32_t)kLaneEdges);
+          unsigned live = 0;
+          {
+            uint32_t e = ent0, from = q - pos0;
+            unsigned rem = adv;
+#pragma unroll 1
+            for (;;) {
+              const uint32_t upto = rem ? (uint32_t)__ffs(rem) - 1 : hi_t;
+              if (loc_of[e] >> 31) live |= (0xffu >> (8 - upto)) & (0xffu << from);
+              if (!rem) break;
+              from = upto;
+              rem &= rem - 1;
+              ++e;
             }
-            if (pp >= lo_pos && pp < span && att_e) live |= 1u << t;
           }
           if (live) {
             const uint4* sp = reinterpret_cast<const uint4*>(src + ebase + pos0);
