@@ -56,9 +56,10 @@ def parse():
     p.add_argument("--budget-gb", type=float, default=0.0, help="forced HBM budget for pages")
     p.add_argument("--pr-iters", type=int, default=20)
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--exchange", default="allreduce", choices=["allreduce", "peer"],
-                   help="N>1: MIN all-reduce of the replicas per round, or peer stores over "
-                        "CUDA IPC + barrier")
+    p.add_argument("--exchange", default="peer", choices=["allreduce", "peer"],
+                   help="N>1: peer stores into the other ranks' replicas over CUDA IPC + a "
+                        "barrier per round (falls back to the all-reduce when a peer cannot "
+                        "be mapped), or the MIN all-reduce of the replicas per round")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)

@@ -1585,7 +1585,8 @@ void Engine::attach_loopback(int rank, int world, const std::string& key, bool p
 // would map them with CUDA IPC handles).  Re-run each run: values_ may move.
 void Engine::setup_peers() {
   n_peers_ = 0;
-  if (!peer_xchg_ || !attached() || world_ < 2) return;
+  // (virtual-clock runs are single-device: validate() rejects them in a world)
+  if (!peer_xchg_ || !attached() || world_ < 2 || det_) return;
   std::vector<uint32_t*> others;
   if (loop_) {
     const std::vector<void*> all = loopback_allgather_ptr(loop_, rank_, values_.p);
@@ -1608,14 +1609,43 @@ void Engine::setup_peers() {
     SR_CUDA(cudaStreamSynchronize(cs_));
     ipc_handles_.resize(size_t(world_));
     ipc_ptrs_.resize(size_t(world_), nullptr);
+    uint32_t ok = 1;
     for (int q = 0; q < world_; ++q) {
       if (q == rank_) continue;
       if (!ipc_ptrs_[q] || std::memcmp(&ipc_handles_[q], &all[q], hs) != 0) {
         if (ipc_ptrs_[q]) cudaIpcCloseMemHandle(ipc_ptrs_[q]);
-        SR_CUDA(cudaIpcOpenMemHandle(&ipc_ptrs_[q], all[q], cudaIpcMemLazyEnablePeerAccess));
+        ipc_ptrs_[q] = nullptr;
+        if (cudaIpcOpenMemHandle(&ipc_ptrs_[q], all[q], cudaIpcMemLazyEnablePeerAccess) !=
+            cudaSuccess) {
+          (void)cudaGetLastError();
+          ipc_ptrs_[q] = nullptr;
+          ok = 0;
+          continue;
+        }
         ipc_handles_[q] = all[q];
       }
       others.push_back(static_cast<uint32_t*>(ipc_ptrs_[q]));
+    }
+    // every rank must take the same exchange: any rank that cannot map a
+    // peer (no P2P path) turns the world back to the all-reduce exchange
+    barrier_word_.reserve(2);
+    SR_CUDA(cudaMemcpyAsync(barrier_word_.p + 1, &ok, 4, cudaMemcpyHostToDevice, cs_));
+    const ncclResult_t r2 =
+        nc.AllReduce(barrier_word_.p + 1, barrier_word_.p + 1, 1, ncclUint32, ncclMin, comm_, cs_);
+    if (r2 != ncclSuccess)
+      throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r2));
+    SR_CUDA(cudaMemcpyAsync(&ok, barrier_word_.p + 1, 4, cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    if (!ok) {
+      for (void*& ptr : ipc_ptrs_)
+        if (ptr) {
+          cudaIpcCloseMemHandle(ptr);
+          ptr = nullptr;
+        }
+      if (rank_ == 0)
+        std::fprintf(stderr, "seraph: peer exchange unavailable (CUDA IPC over P2P failed); "
+                             "using the all-reduce exchange\n");
+      return;
     }
   }
   peers_dev_.reserve(others.size());

@@ -15,14 +15,17 @@ from paper_1806_00762_b200 import pagestream as ps  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
+ap.add_argument("--algo", default="sssp")
+ap.add_argument("--uniform", action="store_true")
 a = ap.parse_args()
-ns = argparse.Namespace(algo="sssp", scale=a.scale, edge_factor=16, uniform=False, pages=16, seed=0,
-                        lean=True, graph="device")
+ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform, pages=16,
+                        seed=0, lean=True, graph="device")
 W = bench.workload(ns)
 csr, pages = W["csr"], W["pages"]
 eng = ps.Engine(0)
 cfg = ps.EngineConfig(predictor=ps.PredictorMode.STRONG, clock=ps.ClockMode.WALL)
-prog = ps.make_sssp(0, W["n"], True)
+prog = (ps.make_sssp(0, W["n"], True) if a.algo == "sssp" else
+        ps.make_cc() if a.algo == "cc" else ps.make_bfs(0, W["n"]))
 vals = np.empty(W["n"], np.uint32)
 for rep in range(3):
     t0 = time.time()
