@@ -1180,63 +1180,57 @@ __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, 
     if (v0 < n) {
       const uint4 cw = __ldcg(reinterpret_cast<const uint4*>(changed + v0));
       const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
-      uint32_t dg[16];
-      if (outdeg && (cw.x | cw.y | cw.z | cw.w)) {
-        const uint4* dp = reinterpret_cast<const uint4*>(outdeg + v0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint4 d4 = dp[k];
-          dg[4 * k] = d4.x;
-          dg[4 * k + 1] = d4.y;
-          dg[4 * k + 2] = d4.z;
-          dg[4 * k + 3] = d4.w;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) dg[k] = 0;
-      }
+      const uint32_t cwv[4] = {cw.x, cw.y, cw.z, cw.w};
       uint4 sw{}, lw{};
       if (status) sw = __ldcg(reinterpret_cast<const uint4*>(status + v0));
       if (logstate) lw = __ldcg(reinterpret_cast<const uint4*>(logstate + v0));
       uint8_t* sb = reinterpret_cast<uint8_t*>(&sw);
       uint8_t* lb = reinterpret_cast<uint8_t*>(&lw);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t v = v0 + j;
-        if (v >= n) break;
-        const bool ch_ = cb[j] != 0;
-        if (ch_) {
-          const unsigned long long d = dg[j];
-          tot[0] += 1;
-          tot[1] += d > 0;
-          tot[2] += d;
-          if (v >= own_lo && v < own_hi) {
-            own_edges += d;
-            own_push += d > 0;
-          }
-        }
-        if (status) {
-          uint8_t st = sb[j];
-          if (pass_kind == kPassDense) {
-            const bool attempt_state = (st == 0 || st == 1 || st == 5);
-            if (attempt_state) {
-              if (logstate) lb[j] = log_attempt(lb[j], ch_, tot[5], tot[6]);
-              st = ch_ ? 0 : (st == 0 ? 5 : (st == 5 ? 3 : 4));
-            } else {
-              st = (st == 3) ? 2 : (st == 2 ? 1 : 3);
+      for (int k = 0; k < 4; ++k) {
+        // out-degrees only of 4-vertex groups holding a changed vertex
+        uint4 d4 = make_uint4(0, 0, 0, 0);
+        if (outdeg && cwv[k]) d4 = reinterpret_cast<const uint4*>(outdeg + v0)[k];
+        const uint32_t dk[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = 4 * k + jj;
+          const uint32_t v = v0 + j;
+          if (v >= n) break;
+          const bool ch_ = cb[j] != 0;
+          if (ch_) {
+            const unsigned long long d = dk[jj];
+            tot[0] += 1;
+            tot[1] += d > 0;
+            tot[2] += d;
+            if (v >= own_lo && v < own_hi) {
+              own_edges += d;
+              own_push += d > 0;
             }
-          } else if (ch_ && pass_kind != kPassInit) {
-            if (pass_kind == kPassRecovery) st = 0;
-            if (logstate) lb[j] = log_change(lb[j], tot[6]);
           }
-          sb[j] = st;
-          switch (st) {
-            case 0: tot[7]++; break;
-            case 1: tot[8]++; break;
-            case 2: tot[9]++; break;
-            case 3: tot[10]++; break;
-            case 4: tot[11]++; break;
-            default: tot[12]++; break;
+          if (status) {
+            uint8_t st = sb[j];
+            if (pass_kind == kPassDense) {
+              const bool attempt_state = (st == 0 || st == 1 || st == 5);
+              if (attempt_state) {
+                if (logstate) lb[j] = log_attempt(lb[j], ch_, tot[5], tot[6]);
+                st = ch_ ? 0 : (st == 0 ? 5 : (st == 5 ? 3 : 4));
+              } else {
+                st = (st == 3) ? 2 : (st == 2 ? 1 : 3);
+              }
+            } else if (ch_ && pass_kind != kPassInit) {
+              if (pass_kind == kPassRecovery) st = 0;
+              if (logstate) lb[j] = log_change(lb[j], tot[6]);
+            }
+            sb[j] = st;
+            switch (st) {
+              case 0: tot[7]++; break;
+              case 1: tot[8]++; break;
+              case 2: tot[9]++; break;
+              case 3: tot[10]++; break;
+              case 4: tot[11]++; break;
+              default: tot[12]++; break;
+            }
           }
         }
       }
@@ -1291,7 +1285,7 @@ __device__ __forceinline__ void census_body(uint32_t n, const uint8_t* changed, 
 }
 
 template <bool ST>
-__global__ void __launch_bounds__(256) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
+__global__ void __launch_bounds__(256, ST ? 1 : 8) census_kernel(uint32_t n, const uint8_t* __restrict__ changed,
                                                      uint8_t* status, uint8_t* logstate,
                                                      const uint32_t* __restrict__ outdeg,
                                                      int pass_kind, uint32_t own_lo, uint32_t own_hi,
