@@ -117,6 +117,7 @@ struct PushArgs {
   const unsigned long long* pref;    // exclusive prefix of out-degree
   const uint32_t* chunk_start;       // first list entry of every push chunk
   uint32_t n_list;
+  uint32_t chunk_shift;  // log2 of the edges per warp task (kPushChunk max)
   unsigned long long total_edges;
   const unsigned long long* out_offsets;
   const uint32_t* out_neighbors;

@@ -570,7 +570,7 @@ void Engine::alloc_run_state(const sr_run_config& c) {
       SR_CUDA(cudaMemset(stamp_.p, 0, npad * 4));
       fq_epoch_ = 0;
     }
-    chunk_start_.reserve(m_ / kPushChunk + 2);
+    chunk_start_.reserve(m_ / kPushChunk + uint64_t(sm_count_) * 48 * 2 + 2);
     blk_cnt_.reserve(nb + 1);
     blk_edges_.reserve(nb + 1);
     census_part_.reserve(size_t(nb + 1) * 13);
@@ -986,11 +986,21 @@ void Engine::read_census() {
   SR_CUDA(cudaStreamSynchronize(cs_));
 }
 
-void Engine::build_push_list() {
+// Edges per push warp task: enough tasks to give every resident warp one
+// (a pass of a few hub sources would otherwise leave most SMs idle behind
+// long per-warp chains), 32..kPushChunk, a power of two.
+uint32_t Engine::push_chunk_shift(uint64_t total) const {
+  const uint64_t warps = uint64_t(sm_count_) * 48;
+  uint32_t shift = 5;
+  while ((1ull << shift) < kPushChunk && (total >> shift) > warps) ++shift;
+  return shift;
+}
+
+void Engine::build_push_list(uint32_t shift) {
   const uint32_t nb = (n_ + kCensusBlockVerts - 1) / kCensusBlockVerts;
   launch_scan_blocks(nb, blk_cnt_.p, blk_edges_.p, cs_);
   launch_compact(n_, own_lo_, own_hi_, changed_.p, outdeg_.p, blk_cnt_.p, blk_edges_.p,
-                 list_.p, pref_.p, chunk_start_.p, cs_);
+                 list_.p, pref_.p, chunk_start_.p, shift, cs_);
 }
 
 // Sparse passes keep their frontier as a queue (O(frontier) work, no
@@ -1007,11 +1017,12 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
   const uint64_t n_list = census_h_.p->own_push;
   const uint64_t total = census_h_.p->own_edges;
   const bool queue = queue_mode();
+  const uint32_t shift = push_chunk_shift(total);
   if (queue && fq_ready_) {
-    launch_queue_prep(list_.p, uint32_t(n_list), outdeg_.p, pref_.p, chunk_start_.p, scan_tmp_.p,
-                      scan_tmp_.n, cs_);
+    launch_queue_prep(list_.p, uint32_t(n_list), outdeg_.p, pref_.p, chunk_start_.p, shift, total,
+                      scan_tmp_.p, scan_tmp_.n, cs_);
   } else {
-    build_push_list();
+    build_push_list(shift);
   }
   if (queue) {
     SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
@@ -1027,6 +1038,7 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
     a.pref = pref_.p;
     a.chunk_start = chunk_start_.p;
     a.n_list = uint32_t(n_list);
+    a.chunk_shift = shift;
     a.total_edges = total;
     a.out_offsets = out_off_.p;
     a.out_neighbors = out_nbr_.p;
@@ -1045,7 +1057,7 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
       a.outdeg = outdeg_.p;
       a.logstate = predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr;
     }
-    const uint64_t chunks = (total + kPushChunk - 1) / kPushChunk;
+    const uint64_t chunks = (total + (1ull << shift) - 1) >> shift;
     const int grid = int(std::max<uint64_t>(
         1, std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_, (chunks + kWarpsPerBlock - 1) / kWarpsPerBlock)));
     launch_push(algo_, det_, a, grid, cs_);

@@ -178,7 +178,8 @@ class Engine {
                         const RunCtr* prev, bool per_page, bool pagerank);
   void push_pass(const sr_run_config& cfg, RunStats& st);
   void census(int pass_kind);
-  void build_push_list();
+  void build_push_list(uint32_t shift);
+  uint32_t push_chunk_shift(uint64_t total) const;
   void read_census();
   void exchange_round(bool pagerank);
 

@@ -960,10 +960,11 @@ template <int A, bool DET>
 __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32_t nw, LaneCtr& c,
                                           uint32_t& lane_min, QueueCtr* qc = nullptr) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long nchunks = (a.total_edges + kPushChunk - 1) / kPushChunk;
+  const unsigned long long cmask = (1ull << a.chunk_shift) - 1;
+  const unsigned long long nchunks = (a.total_edges + cmask) >> a.chunk_shift;
   for (unsigned long long ch = gw; ch < nchunks; ch += nw) {
-    const unsigned long long q_lo = ch * kPushChunk;
-    const unsigned long long q_hi = min(q_lo + kPushChunk, a.total_edges);
+    const unsigned long long q_lo = ch << a.chunk_shift;
+    const unsigned long long q_hi = min(q_lo + cmask + 1, a.total_edges);
     uint32_t ad = __ldcg(a.chunk_start + ch);
     for (unsigned long long q0 = q_lo; q0 < q_hi; q0 += 32) {
       // window of up to 32 consecutive frontier entries starting at ad
@@ -1092,13 +1093,19 @@ __global__ void queue_degrees_kernel(const uint32_t* __restrict__ list, uint32_t
     deg[i] = i < q ? outdeg[list[i]] : 0ull;
 }
 
+// One thread per queue entry, or (`per_warp`: few entries with many chunks,
+// e.g. a hub source) one warp per entry with the lanes striding its chunks.
 __global__ void queue_chunks_kernel(const unsigned long long* __restrict__ pref, uint32_t q,
-                                    uint32_t* chunk_start) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < q; i += gridDim.x * blockDim.x) {
+                                    uint32_t shift, int per_warp, uint32_t* chunk_start) {
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nt = uint64_t(gridDim.x) * blockDim.x;
+  const uint32_t step = per_warp ? 32u : 1u;
+  const uint32_t sub = per_warp ? uint32_t(tid & 31) : 0u;
+  const unsigned long long cm = (1ull << shift) - 1;
+  for (uint64_t i = per_warp ? tid >> 5 : tid; i < q; i += per_warp ? nt >> 5 : nt) {
     const unsigned long long lo = pref[i], hi = pref[i + 1];
-    for (unsigned long long ch = (lo + kPushChunk - 1) / kPushChunk;
-         ch < (hi + kPushChunk - 1) / kPushChunk; ++ch)
-      chunk_start[ch] = i;
+    for (unsigned long long ch = ((lo + cm) >> shift) + sub; ch < ((hi + cm) >> shift); ch += step)
+      chunk_start[ch] = uint32_t(i);
   }
 }
 
@@ -1357,7 +1364,8 @@ __device__ __forceinline__ void compact_chunk(uint32_t chunk, uint32_t n, uint32
                                               const uint32_t* __restrict__ outdeg,
                                               const uint32_t* blk_off,
                                               const unsigned long long* blk_eoff, uint32_t* list,
-                                              unsigned long long* pref, uint32_t* chunk_start) {
+                                              unsigned long long* pref, uint32_t* chunk_start,
+                                              uint32_t shift) {
   __shared__ uint32_t s_c[8];
   __shared__ unsigned long long s_e[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1398,8 +1406,9 @@ __device__ __forceinline__ void compact_chunk(uint32_t chunk, uint32_t n, uint32
     if (deg[j] > 0) {
       list[pos] = v0 + j;
       pref[pos] = ep;
-      const unsigned long long c_lo = (ep + kPushChunk - 1) / kPushChunk;
-      const unsigned long long c_hi = (ep + deg[j] + kPushChunk - 1) / kPushChunk;
+      const unsigned long long cm = (1ull << shift) - 1;
+      const unsigned long long c_lo = (ep + cm) >> shift;
+      const unsigned long long c_hi = (ep + deg[j] + cm) >> shift;
       for (unsigned long long ch = c_lo; ch < c_hi; ++ch) chunk_start[ch] = pos;
       ++pos;
       ep += deg[j];
@@ -1415,9 +1424,9 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t n, uint32_t own_l
                                                       const uint32_t* __restrict__ blk_off,
                                                       const unsigned long long* __restrict__ blk_eoff,
                                                       uint32_t* list, unsigned long long* pref,
-                                                      uint32_t* chunk_start) {
+                                                      uint32_t* chunk_start, uint32_t shift) {
   compact_chunk(blockIdx.x, n, own_lo, own_hi, changed, outdeg, blk_off, blk_eoff, list, pref,
-                chunk_start);
+                chunk_start, shift);
 }
 
 
@@ -1755,15 +1764,18 @@ void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, 
 }
 
 void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
-                       unsigned long long* pref, uint32_t* chunk_start, void* tmp,
-                       size_t tmp_bytes, cudaStream_t s) {
+                       unsigned long long* pref, uint32_t* chunk_start, uint32_t shift,
+                       uint64_t total_edges, void* tmp, size_t tmp_bytes, cudaStream_t s) {
   if (!q) return;
   note_launch();
   queue_degrees_kernel<<<grid_for(uint64_t(q) + 1, 256), 256, 0, s>>>(list, q, outdeg, pref);
   SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pref, pref, uint64_t(q) + 1, s));
   note_launch(2);  // cub: tile-state init + scan
   note_launch();
-  queue_chunks_kernel<<<grid_for(q, 256), 256, 0, s>>>(pref, q, chunk_start);
+  const uint64_t chunks = (total_edges >> shift) + 1;
+  const int per_warp = chunks > 8ull * q ? 1 : 0;
+  queue_chunks_kernel<<<grid_for(per_warp ? uint64_t(q) * 32 : q, 256), 256, 0, s>>>(
+      pref, q, shift, per_warp, chunk_start);
 }
 
 void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s) {
@@ -1819,12 +1831,12 @@ void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long*
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
                     const uint32_t* out_offsets, const uint32_t* blk_off,
                     const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
-                    uint32_t* chunk_start, cudaStream_t s) {
+                    uint32_t* chunk_start, uint32_t shift, cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
   if (!nb) return;
   note_launch();
   compact_kernel<<<nb, 256, 0, s>>>(n, own_lo, own_hi, changed, out_offsets, blk_off, blk_eoff,
-                                    list, pref, chunk_start);
+                                    list, pref, chunk_start, shift);
 }
 
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,

@@ -42,7 +42,7 @@ void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long*
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
                     const uint32_t* outdeg, const uint32_t* blk_off,
                     const unsigned long long* blk_eoff, uint32_t* list, unsigned long long* pref,
-                    uint32_t* chunk_start, cudaStream_t s);
+                    uint32_t* chunk_start, uint32_t shift, cudaStream_t s);
 // Multi-GPU: flag vertices improved by any rank during the round.
 void launch_mark_changed(uint32_t n, const uint32_t* values, const uint32_t* snap,
                          uint8_t* changed, cudaStream_t s);
@@ -85,8 +85,8 @@ void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, 
                        cudaStream_t s);
 size_t queue_prep_temp_bytes(uint32_t max_q);
 void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
-                       unsigned long long* pref, uint32_t* chunk_start, void* tmp,
-                       size_t tmp_bytes, cudaStream_t s);
+                       unsigned long long* pref, uint32_t* chunk_start, uint32_t shift,
+                       uint64_t total_edges, void* tmp, size_t tmp_bytes, cudaStream_t s);
 void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s);
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,
