@@ -186,10 +186,10 @@ void Engine::maybe_derive_csr() {
   out_nbr_.reserve(m_);
   if (weighted_) out_w_.reserve(m_);
   csr_cursor_.reserve(n_);
-  SR_CUDA(cudaMemsetAsync(csr_cursor_.p, 0, size_t(n_) * 4, cs_));
+  SR_CUDA(cudaMemcpyAsync(csr_cursor_.p, out_off_.p, size_t(n_) * 8, cudaMemcpyDeviceToDevice, cs_));
   for (const PageMeta& pm : pages_)
     launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, pm.tile_begin, pm.tile_end,
-                          out_off_.p, csr_cursor_.p, out_nbr_.p, weighted_ ? out_w_.p : nullptr,
+                          csr_cursor_.p, out_nbr_.p, weighted_ ? out_w_.p : nullptr,
                           sm_count_ * 8, cs_);
   SR_CUDA(cudaGetLastError());
   has_csr_edges_ = true;
@@ -411,12 +411,13 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       out_nbr_.reserve(m_);
       if (weighted) out_w_.reserve(m_);
       csr_cursor_.reserve(n_);
-      SR_CUDA(cudaMemsetAsync(csr_cursor_.p, 0, size_t(n_) * 4, cs_));
+      SR_CUDA(cudaMemcpyAsync(csr_cursor_.p, out_off_.p, size_t(n_) * 8,
+                              cudaMemcpyDeviceToDevice, cs_));
       for (uint32_t p = 0; p < np; ++p) {
         if (!used[p]) continue;
         SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
         launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, pages_[p].tile_begin,
-                              pages_[p].tile_end, out_off_.p, csr_cursor_.p, out_nbr_.p,
+                              pages_[p].tile_end, csr_cursor_.p, out_nbr_.p,
                               weighted ? out_w_.p : nullptr, sm_count_ * 8, cs_);
       }
       SR_CUDA(cudaGetLastError());

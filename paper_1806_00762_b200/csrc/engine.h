@@ -196,7 +196,7 @@ class Engine {
   PinBuf<uint4> tile_stage_;
   PinBuf<uint32_t> tile_page_stage_, hub_stage_;
   PinBuf<PageDesc> desc_stage_;
-  DBuf<uint32_t> csr_cursor_;
+  DBuf<unsigned long long> csr_cursor_;  // CSR derivation: next free slot per source
 
   int dev_ = 0;
   uint64_t budget_ = 0;
@@ -314,6 +314,10 @@ class Engine {
     bool built = false;
     uint32_t blk_verts = 0, n_blocks = 0;
     DBuf<uint32_t> offs, src, w;
+    // build temporaries kept across builds (multi-GB for big graphs:
+    // cudaMalloc/cudaFree of them cost more than the build kernels)
+    DBuf<uint32_t> t_cnt, t_tcnt, t_tat;
+    DBuf<unsigned long long> t_goff;
     DBuf<uint4> tiles;
     DBuf<uint32_t> tile_page;
     DBuf<PageDesc> desc;

@@ -40,13 +40,14 @@ bool Engine::build_src_blocks(uint64_t blk) {
     t_last = now;
   };
   // 1) counts per (block, destination)
-  DBuf<uint32_t> cnt;
+  DBuf<uint32_t>& cnt = sb_.t_cnt;
   cnt.reserve(size_t(nb) * n_);
   SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
   launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
                    cnt.p, nullptr, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
   // 2) page-local offsets per sub-page, sub-page sizes
-  DBuf<unsigned long long> goff, bp_edges, bp_base;
+  DBuf<unsigned long long>& goff = sb_.t_goff;
+  DBuf<unsigned long long> bp_edges, bp_base;
   goff.reserve(size_t(nb) * n_);
   bp_edges.reserve(size_t(nb) * np);
   bp_base.reserve(size_t(nb) * np);
@@ -78,7 +79,8 @@ bool Engine::build_src_blocks(uint64_t blk) {
   launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
   const size_t K = sub_tile_windows(cap_, np, nb);
   const size_t K_blk = K / nb;  // windows per block
-  DBuf<uint32_t> tcnt, tat;
+  DBuf<uint32_t>& tcnt = sb_.t_tcnt;
+  DBuf<uint32_t>& tat = sb_.t_tat;
   tcnt.reserve(K + 1);
   tat.reserve(K + 1);
   SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));

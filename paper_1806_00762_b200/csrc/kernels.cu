@@ -518,8 +518,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
 __global__ void __launch_bounds__(kBlockThreads)
 csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
                       const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
-                      const unsigned long long* __restrict__ out_off, uint32_t* cursor,
-                      uint32_t* out_nbr, uint32_t* out_w) {
+                      unsigned long long* cursor, uint32_t* out_nbr, uint32_t* out_w) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
@@ -534,7 +533,7 @@ csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restric
       const uint32_t v = pd.vertex_begin + tile.z;
       for (uint32_t e = tile.x + lane; e < tile.y; e += 32) {
         const uint32_t s = src[e];
-        const unsigned long long pos = out_off[s] + atomicAdd(cursor + s, 1u);
+        const unsigned long long pos = atomicAdd(cursor + s, 1ull);
         out_nbr[pos] = v;
         if (out_w) out_w[pos] = wts[e];
       }
@@ -583,7 +582,7 @@ csr_from_pages_kernel(const uint4* __restrict__ tiles, const uint32_t* __restric
           if (pp < lo_pos) continue;
           const uint32_t e = ebase + pp;
           const uint32_t s = src[e];
-          const unsigned long long pos = out_off[s] + atomicAdd(cursor + s, 1u);
+          const unsigned long long pos = atomicAdd(cursor + s, 1ull);
           out_nbr[pos] = pd.vertex_begin + s_loc[warp][ent];
           if (out_w) out_w[pos] = wts[e];
         }
@@ -1840,15 +1839,14 @@ void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* chang
 }
 
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
-                           uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
-                           uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
-                           cudaStream_t s) {
+                           uint32_t tile_lo, uint32_t tile_hi, unsigned long long* cursor,
+                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s) {
   if (tile_hi <= tile_lo) return;
   const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (uint32_t(grid) > need) grid = int(need);
   note_launch();
   csr_from_pages_kernel<<<grid, kBlockThreads, 0, s>>>(tiles, tile_page, pages, tile_lo, tile_hi,
-                                                       out_off, cursor, out_nbr, out_w);
+                                                       cursor, out_nbr, out_w);
 }
 
 void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,

@@ -52,9 +52,8 @@ void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, cons
 // K6: strong CC threshold (net label-population change since the last refresh).
 // Device-side CSR adjacency from resident CSC pages; out-degrees (u32).
 void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const PageDesc* pages,
-                           uint32_t tile_lo, uint32_t tile_hi, const unsigned long long* out_off,
-                           uint32_t* cursor, uint32_t* out_nbr, uint32_t* out_w, int grid,
-                           cudaStream_t s);
+                           uint32_t tile_lo, uint32_t tile_hi, unsigned long long* cursor,
+                           uint32_t* out_nbr, uint32_t* out_w, int grid, cudaStream_t s);
 void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cudaStream_t s);
 // Source-blocked page split for PageRank locality (count / scan / scatter)
 // and the per-iteration finalize of the accumulated partial sums.

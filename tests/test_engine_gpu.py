@@ -788,6 +788,11 @@ def test_scale20_parity_device_built(case, monkeypatch):
             for pred in PREDS:
                 r = eng.run(program_for(kind, 1, el), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
                 assert np.array_equal(r.values, want), (kind, pred)
+            # push-only: frontiers from one vertex to millions of out-edges (every
+            # push task size, queue and compaction list builds)
+            r = eng.run(program_for(kind, 1, el),
+                        cfg_of(clock=ps.ClockMode.WALL, execution=ps.ExecutionPolicy.FORCE_SPARSE))
+            assert np.array_equal(r.values, want), (kind, "force_sparse")
 
 
 def _run_world(world, g, prog, cfg, cap, key, peer=False):
