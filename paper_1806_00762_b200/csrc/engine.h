@@ -317,6 +317,7 @@ class Engine {
     // build temporaries kept across builds (multi-GB for big graphs:
     // cudaMalloc/cudaFree of them cost more than the build kernels)
     DBuf<uint32_t> t_cnt, t_tcnt, t_tat;
+    DBuf<unsigned char> t_scan;
     DBuf<unsigned long long> t_goff;
     DBuf<uint4> tiles;
     DBuf<uint32_t> tile_page;

@@ -44,7 +44,7 @@ bool Engine::build_src_blocks(uint64_t blk) {
   cnt.reserve(size_t(nb) * n_);
   SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
   launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, nullptr, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
+                   cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
   // 2) page-local offsets per sub-page, sub-page sizes
   DBuf<unsigned long long>& goff = sb_.t_goff;
   DBuf<unsigned long long> bp_edges, bp_base;
@@ -67,16 +67,16 @@ bool Engine::build_src_blocks(uint64_t blk) {
   if (weighted_) sb_.w.reserve(at + 8);
   else sb_.w.release();
   SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
-  // 3) scatter the sources (cnt reused as cursors)
-  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
-  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, bp_base.p,
-                   sm_count_ * 8, cs_);
-  stage("scatter");
-  // 4) u32 local offsets of every sub-page, then the tile cut on the device
+  // 3) u32 local offsets of every sub-page (from the page-local goff)
   const size_t per_block = size_t(n_) + np;
   sb_.offs.reserve(size_t(nb) * per_block);
   launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
+  // 4) scatter the sources: goff becomes absolute cursors (one atomic per edge)
+  launch_src_block_abs(goff.p, n_, cap_, np, nb, bp_base.p, cs_);
+  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
+                   nullptr, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, sm_count_ * 8, cs_);
+  stage("scatter");
+  // 5) the tile cut on the device
   const size_t K = sub_tile_windows(cap_, np, nb);
   const size_t K_blk = K / nb;  // windows per block
   DBuf<uint32_t>& tcnt = sb_.t_tcnt;
@@ -86,7 +86,8 @@ bool Engine::build_src_blocks(uint64_t blk) {
   SR_CUDA(cudaMemsetAsync(tcnt.p + K, 0, 4, cs_));
   launch_sub_tiles(0, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, tcnt.p, nullptr, nullptr,
                    nullptr, cs_);
-  launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, cs_);
+  sb_.t_scan.reserve(exclusive_scan_u32_temp_bytes(K + 1));
+  launch_exclusive_scan_u32(tcnt.p, tat.p, K + 1, sb_.t_scan.p, sb_.t_scan.n, cs_);
   sb_.block_tile_begin.assign(nb + 1, 0);
   for (uint32_t b = 0; b <= nb; ++b)
     SR_CUDA(cudaMemcpyAsync(&sb_.block_tile_begin[b], tat.p + size_t(b) * K_blk, 4,

@@ -604,8 +604,7 @@ __global__ void __launch_bounds__(kBlockThreads)
 src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __restrict__ tile_page,
                  const PageDesc* __restrict__ pages, uint32_t tile_lo, uint32_t tile_hi,
                  uint32_t n, uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                 const unsigned long long* __restrict__ goff, uint32_t* out_src, uint32_t* out_w,
-                 const unsigned long long* __restrict__ bp_base) {
+                 unsigned long long* goff, uint32_t* out_src, uint32_t* out_w) {
   __shared__ uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
@@ -615,9 +614,8 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
     const size_t k = size_t(b) * n + v;
     if (mode == 0) {
       atomicAdd(cnt + k, 1u);
-    } else {
-      const uint32_t at = atomicAdd(cnt + k, 1u);
-      const unsigned long long o = bp_base[size_t(b) * n_pages + p] + goff[k] + at;
+    } else {  // goff holds absolute cursors (src_block_abs_kernel)
+      const unsigned long long o = atomicAdd(goff + k, 1ull);
       out_src[o] = s;
       if (out_w) out_w[o] = *wp;
     }
@@ -717,6 +715,20 @@ __global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __
     __syncthreads();
   }
   if (threadIdx.x == 0) bp_edges[pb] = s_carry;
+}
+
+// Page-local sub-page offsets -> absolute scatter cursors into the
+// sub-page source array: goff[b*n + v] += base of sub-page (page(v), b).
+__global__ void src_block_abs_kernel(unsigned long long* goff, uint32_t n, uint32_t cap,
+                                     uint32_t n_pages, uint32_t n_blocks,
+                                     const unsigned long long* __restrict__ bp_base) {
+  const size_t total = size_t(n_blocks) * n;
+  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
+       k += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(k / n), v = uint32_t(k % n);
+    const uint32_t p = min(v / cap, n_pages - 1);
+    goff[k] += bp_base[size_t(b) * n_pages + p];
+  }
 }
 
 __global__ void pr_block_finalize_kernel(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
@@ -1852,15 +1864,21 @@ void launch_csr_from_pages(const uint4* tiles, const uint32_t* tile_page, const 
 void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                      const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
-                      const unsigned long long* bp_base, int grid, cudaStream_t s) {
+                      unsigned long long* goff, uint32_t* out_src, uint32_t* out_w, int grid,
+                      cudaStream_t s) {
   if (tile_hi <= tile_lo) return;
   const uint32_t need = (tile_hi - tile_lo + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (uint32_t(grid) > need) grid = int(need);
   note_launch();
   src_block_kernel<<<grid, kBlockThreads, 0, s>>>(mode, tiles, tile_page, pages, tile_lo, tile_hi,
-                                                  n, blk_verts, n_pages, cnt, goff, out_src, out_w,
-                                                  bp_base);
+                                                  n, blk_verts, n_pages, cnt, goff, out_src, out_w);
+}
+
+void launch_src_block_abs(unsigned long long* goff, uint32_t n, uint32_t cap, uint32_t n_pages,
+                          uint32_t n_blocks, const unsigned long long* bp_base, cudaStream_t s) {
+  if (!n || !n_pages || !n_blocks) return;
+  note_launch();
+  src_block_abs_kernel<<<148 * 8, 256, 0, s>>>(goff, n, cap, n_pages, n_blocks, bp_base);
 }
 
 __global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
@@ -1992,15 +2010,20 @@ void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* 
   degree_hist_kernel<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(outdeg, n, hist_v, hist_e);
 }
 
-void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s) {
-  if (!count) return;
+size_t exclusive_scan_u32_temp_bytes(size_t count) {
   size_t tb = 0;
-  SR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, count, s));
-  void* tmp = nullptr;
-  SR_CUDA(cudaMallocAsync(&tmp, tb, s));
-  SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, count, s));
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, static_cast<const uint32_t*>(nullptr),
+                                        static_cast<uint32_t*>(nullptr), count));
+  return tb;
+}
+
+// The caller owns the temporary storage (stream-ordered allocations inside
+// a build showed multi-100 ms stalls next to multi-GB buffers).
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, void* tmp,
+                               size_t tmp_bytes, cudaStream_t s) {
+  if (!count) return;
+  SR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, count, s));
   note_launch(2);
-  SR_CUDA(cudaFreeAsync(tmp, s));
 }
 
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,

@@ -60,8 +60,11 @@ void launch_outdeg(const unsigned long long* off, uint32_t n, uint32_t* deg, cud
 void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       const PageDesc* pages, uint32_t tile_lo, uint32_t tile_hi, uint32_t n,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
-                      const unsigned long long* goff, uint32_t* out_src, uint32_t* out_w,
-                      const unsigned long long* bp_base, int grid, cudaStream_t s);
+                      unsigned long long* goff, uint32_t* out_src, uint32_t* out_w, int grid,
+                      cudaStream_t s);
+// goff (page-local sub-page offsets) += sub-page bases: absolute scatter cursors
+void launch_src_block_abs(unsigned long long* goff, uint32_t n, uint32_t cap, uint32_t n_pages,
+                          uint32_t n_blocks, const unsigned long long* bp_base, cudaStream_t s);
 // Tile cut of the source-blocked sub-pages on the device, one 128-destination
 // window per thread: mode 0 writes the tile count of every window to cnt
 // (sub_tile_windows entries, block-major); mode 1 writes the tiles at the
@@ -86,7 +89,9 @@ size_t queue_prep_temp_bytes(uint32_t max_q);
 void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
                        unsigned long long* pref, uint32_t* chunk_start, uint32_t shift,
                        uint64_t total_edges, void* tmp, size_t tmp_bytes, cudaStream_t s);
-void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, cudaStream_t s);
+size_t exclusive_scan_u32_temp_bytes(size_t count);
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, void* tmp,
+                               size_t tmp_bytes, cudaStream_t s);
 void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
                            const unsigned long long* goff, const unsigned long long* bp_edges,
                            uint32_t* offs, cudaStream_t s);
