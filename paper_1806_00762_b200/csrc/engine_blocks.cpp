@@ -15,8 +15,8 @@ namespace seraph {
 // ---------------------------------------------------------------------------
 // Source-blocked sub-pages for PageRank: when the contrib array outgrows the
 // L2, every iteration sweeps the sub-pages block by block so the gathers of
-// one sweep stay inside a blk_verts slice (SERAPH_PR_BLOCK_VERTS, default
-// 16 Mi vertices = 64 MB of f32; 0 disables).
+// one sweep stay inside a blk_verts slice (PageRank: SERAPH_PR_BLOCK_VERTS,
+// default 32 Mi vertices = 128 MB of f32; K1: pull_block_verts; 0 disables).
 // ---------------------------------------------------------------------------
 bool Engine::build_src_blocks(uint64_t blk) {
   if (sb_.built && sb_.blk_verts == blk) return true;
