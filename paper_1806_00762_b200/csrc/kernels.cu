@@ -1386,13 +1386,19 @@ __device__ __forceinline__ void compact_chunk(uint32_t chunk, uint32_t n, uint32
   const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cw);
   uint32_t cnt = 0;
   unsigned long long edges = 0;
-  unsigned long long deg[16];
+  uint32_t deg[16];
+  const uint32_t cwv[4] = {cw.x, cw.y, cw.z, cw.w};
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    deg[j] = 0;
-    const uint32_t v = v0 + j;
-    if (v < n && cb[j] && v >= own_lo && v < own_hi) {
-      deg[j] = outdeg[v];
+  for (int k = 0; k < 4; ++k) {
+    // out-degrees only of 4-vertex groups holding a changed vertex
+    uint4 d4 = make_uint4(0, 0, 0, 0);
+    if (cwv[k]) d4 = reinterpret_cast<const uint4*>(outdeg + v0)[k];
+    const uint32_t dk[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * k + jj;
+      const uint32_t v = v0 + j;
+      deg[j] = (v < n && cb[j] && v >= own_lo && v < own_hi) ? dk[jj] : 0u;
       cnt += deg[j] > 0;
       edges += deg[j];
     }
@@ -1425,7 +1431,8 @@ __device__ __forceinline__ void compact_chunk(uint32_t chunk, uint32_t n, uint32
       ep += deg[j];
     }
   }
-  if (v0 < n) *reinterpret_cast<uint4*>(changed + v0) = make_uint4(0, 0, 0, 0);
+  if (v0 < n && (cw.x | cw.y | cw.z | cw.w))
+    *reinterpret_cast<uint4*>(changed + v0) = make_uint4(0, 0, 0, 0);
   __syncthreads();  // s_c/s_e reused by the next chunk
 }
 
