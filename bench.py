@@ -393,7 +393,40 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         e2e_eng = ps.Engine(local_rank, budget)
         if world > 1:
-            e2e = None
+            # every rank makes the same sr_run_graph call on its own context,
+            # attached as a world of its own (shards, exchange as above);
+            # wall time per step = max over ranks, bytes summed over ranks
+            vals = W["arena"].array(n, np.uint32) if algo != 3 else None
+            uid = [None]
+            if rank == 0:
+                buf = (N.C.c_uint8 * 128)()
+                N.check(N.lib.sr_nccl_unique_id(N.C.byref(buf)))
+                uid[0] = bytes(buf)
+            dist.broadcast_object_list(uid, src=0)
+            e2e_eng.attach_world(rank, world, uid[0])
+            e2e_eng.set_exchange(args.exchange == "peer")
+            e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
+            sync()
+            dist.barrier()
+            t1 = time.time()
+            reps = max(1, min(args.steps, 5))
+            for _ in range(reps):
+                rr = e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)
+            sync()
+            tt = torch.tensor([(time.time() - t1) / reps, float(rr.metrics.h2d_bytes),
+                               float(n * 4), rr.metrics.upload_seconds],
+                              dtype=torch.float64, device=f"cuda:{local_rank}")
+            mx = tt.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            e2e_s = float(mx[0].item())
+            e2e = {"value": round(m * iters / e2e_s / 1e9, 4), "unit": "GTEPS",
+                   "seconds_per_step": round(e2e_s, 5),
+                   "h2d_bytes_per_step": int(tt[1].item()),
+                   "d2h_bytes_per_step": int(tt[2].item()),
+                   "upload_seconds": round(float(mx[3].item()), 5),
+                   "call": "sr_run_graph on every rank (pagestream::run drop-in, one "
+                           "shard per GPU), pinned host inputs; max over ranks"}
         else:
             vals = W["arena"].array(n, np.uint32) if algo != 3 else None  # pinned result buffer
             e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
