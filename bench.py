@@ -72,7 +72,7 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
-def workload(args, eng=None):
+def workload(args, eng=None, device=0):
     """Synthetic RMAT graph of the named scale: CSR + 16 CSC pages, all arrays in
     pinned host memory (e2e / reference inputs).  --graph device (default):
     generated and built on the GPU (sr_generate_graph, bit-identical to the host
@@ -90,7 +90,7 @@ def workload(args, eng=None):
     arena = N.PinnedArena()
     if getattr(args, "graph", "host") == "device":
         try:
-            builder = eng if eng is not None else ps.Engine(0)
+            builder = eng if eng is not None else ps.Engine(device)
             builder.generate_graph(args.scale, args.edge_factor, *quad, seed=args.seed,
                                    weights=(1, 64, args.seed + 1) if weighted else None,
                                    symmetrize=args.algo == "cc", page_vertex_capacity=cap,
@@ -258,7 +258,9 @@ def run_ours(args, rank, world, local_rank):
         dist.broadcast_object_list(uid, src=0)
         eng.attach_world(rank, world, uid[0])
         eng.set_exchange(args.exchange == "peer")
-    W = workload(args, eng)
+    # a sharded rank holds only its own pages: build the whole graph in a
+    # scratch context on this GPU, export it, then load the shard
+    W = workload(args, eng if world == 1 else None, device=local_rank)
     csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
     if not W["loaded"]:
         eng.load_csr(csr, with_edges=not W.get("lean"))
