@@ -172,10 +172,27 @@ void Engine::finish_csr(bool sync) {
   csr_derived_ = false;
 }
 
+// Graphs of at least this many edges defer the push adjacency derivation
+// (SERAPH_DEFER_CSR_EDGES overrides; 0 = never defer).
+uint64_t Engine::defer_csr_min_edges() const {
+  if (const char* e = std::getenv("SERAPH_DEFER_CSR_EDGES")) {
+    const uint64_t v = std::strtoull(e, nullptr, 10);
+    return v ? v : ~0ull;
+  }
+  return 1ull << 30;
+}
+
+void Engine::derive_csr_now() {
+  csr_deferred_ = false;
+  maybe_derive_csr();
+}
+
 void Engine::maybe_derive_csr() {
   // sr_load_csr without out_neighbors + a resident page set: build the push
   // adjacency on the device instead of shipping it over the host link.
-  if (!has_csr_ || has_csr_edges_ || !pages_loaded_ || !all_resident_ || world_ > 1) return;
+  if (csr_deferred_ || !has_csr_ || has_csr_edges_ || !pages_loaded_ || !all_resident_ ||
+      world_ > 1)
+    return;
   if (n_ != page_n_ || m_ != page_edges_total_) return;
   if (m_ == 0) {
     has_csr_edges_ = true;
@@ -404,8 +421,15 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       has_csr_edges_ = false;
       csr_derived_ = false;
     }
-    const bool derive = has_csr_ && !has_csr_edges_ && world_ == 1 && n_ == n &&
-                        m_ == page_edges_total_;
+    bool derive = has_csr_ && !has_csr_edges_ && world_ == 1 && n_ == n &&
+                  m_ == page_edges_total_;
+    csr_deferred_ = false;
+    runs_since_pages_ = 0;
+    if (derive && m_ >= defer_csr_min_edges()) {  // derived on demand (derive_csr_now)
+      derive = false;
+      csr_deferred_ = true;
+      csr_weighted_ = weighted;  // what the derivation will produce
+    }
     SR_CUDA(cudaStreamWaitEvent(cs_, ev_tiles_, 0));
     if (derive && m_) {
       out_nbr_.reserve(m_);
@@ -534,7 +558,7 @@ void Engine::validate(const sr_run_config& c) const {
     throw EngineError(SR_E_CONFIG, "sssp requires weighted graph structures");
   if ((c.algo == SR_ALGO_BFS || c.algo == SR_ALGO_SSSP) && c.source >= n_)
     throw EngineError(SR_E_CONFIG, "source vertex out of range");
-  if (c.algo != SR_ALGO_PAGERANK && !has_csr_edges_ && m_ > 0)
+  if (c.algo != SR_ALGO_PAGERANK && !has_csr_edges_ && !csr_deferred_ && m_ > 0)
     throw EngineError(SR_E_CONFIG, "traversal needs the csr adjacency (push stage)");
   if (c.algo == SR_ALGO_PAGERANK) {
     if (c.pr_iterations < 1) throw EngineError(SR_E_CONFIG, "pagerank iterations must be >= 1");
@@ -1033,6 +1057,35 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
     }
   }
   RunCtr* slot = alloc_ctr(1);
+  if (total > 0 && csr_deferred_ && !det_ && scan_pushes_ < 2 && total <= m_ / 64) {
+    // a small frontier on a deferred push adjacency: enumerate its out-edges
+    // from the resident CSC pages (a sweep over the sources) instead of
+    // deriving the whole CSR for it
+    ++scan_pushes_;
+    PushArgs a{};
+    a.list = list_.p;
+    a.n_list = uint32_t(n_list);
+    a.total_edges = total;
+    a.values = values_.p;
+    a.next = values_.p;
+    a.changed = changed_.p;
+    a.ctr = slot;
+    a.census = census_.p;
+    if (queue) {
+      a.stamp = stamp_.p;
+      a.epoch = fq_epoch_;
+      a.q_list = list2_.p;
+      a.outdeg = outdeg_.p;
+      a.logstate = predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr;
+    }
+    fbits_.reserve(size_t(n_) / 32 + 1);
+    launch_push_scan(algo_, a, page_desc_.p, uint32_t(pages_.size()), fbits_.p, n_,
+                     int(sm_count_) * blocks_per_sm_, cs_);
+    SR_CUDA(cudaGetLastError());
+    (void)st;
+    return;
+  }
+  if (total > 0 && csr_deferred_) derive_csr_now();
   if (total > 0) {
     PushArgs a{};
     a.list = list_.p;
@@ -1137,8 +1190,15 @@ void Engine::exchange_round(bool pagerank) {
 void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out,
                  sr_metrics& m, std::vector<sr_pass_stats>& passes) {
   SR_CUDA(cudaSetDevice(dev_));
+  // a deferred push adjacency is derived once the page set is run again
+  // (it then pays for itself) or for the deterministic passes
+  if (csr_deferred_ && cfg.algo != SR_ALGO_PAGERANK &&
+      (runs_since_pages_ > 0 || cfg.clock == SR_CLOCK_VIRTUAL))
+    derive_csr_now();
   maybe_derive_csr();
   validate(cfg);
+  scan_pushes_ = 0;
+  ++runs_since_pages_;
   algo_ = cfg.algo;
   source_ = cfg.source;
   predictor_ = cfg.algo == SR_ALGO_PAGERANK ? SR_PRED_OFF : cfg.predictor;
@@ -1292,7 +1352,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   // single-block launch (tail_loop_kernel) with the host loop's decisions;
   // the passes are accounted from the per-pass records afterwards.
   auto do_sparse_tail = [&]() -> bool {
-    if (!queue_mode() || !fq_ready_ || std::getenv("SERAPH_NO_TAIL")) return false;
+    if (!queue_mode() || !fq_ready_ || csr_deferred_ || std::getenv("SERAPH_NO_TAIL")) return false;
     const uint64_t q = census_h_.p->own_push, e = census_h_.p->own_edges;
     if (q == 0 || q > kTailMaxQueue || e > kTailMaxEdges || f_count == 0) return false;
     if (uint64_t(fq_epoch_) + kTailMaxPasses + 2 >= 0xffffffffull) return false;
@@ -1490,6 +1550,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
 // ---------------------------------------------------------------------------
 uint64_t Engine::verify_fixpoint(int algo, const uint32_t* values_host) {
   SR_CUDA(cudaSetDevice(dev_));
+  if (csr_deferred_) derive_csr_now();
   if (!has_csr_edges_) throw EngineError(SR_E_CONFIG, "verify needs the csr adjacency");
   if (algo == SR_ALGO_SSSP && !csr_weighted_) throw EngineError(SR_E_CONFIG, "sssp needs weights");
   DBuf<unsigned long long> viol;

@@ -179,6 +179,14 @@ class Engine {
   void push_pass(const sr_run_config& cfg, RunStats& st);
   void census(int pass_kind);
   void build_push_list(uint32_t shift);
+  // Deferred push adjacency (big lean graphs, one run per load: the CSR
+  // neighbours derivation costs more than the rare pushes it serves).
+  bool csr_deferred_ = false;
+  uint32_t runs_since_pages_ = 0;
+  uint32_t scan_pushes_ = 0;  // CSC-scan pushes in the current run
+  DBuf<uint32_t> fbits_;      // frontier bitmap of a CSC-scan push
+  uint64_t defer_csr_min_edges() const;
+  void derive_csr_now();
   uint32_t push_chunk_shift(uint64_t total) const;
   void read_census();
   void exchange_round(bool pagerank);

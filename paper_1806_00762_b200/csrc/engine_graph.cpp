@@ -235,6 +235,10 @@ void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w,
   if ((out_off || out_nbr || out_w) && !has_csr_) throw EngineError(SR_E_DATA, "no csr loaded");
   if (out_off) SR_CUDA(cudaMemcpy(out_off, out_off_.p, (size_t(n_) + 1) * 8, cudaMemcpyDeviceToHost));
   if (out_nbr) {
+    if (csr_deferred_) {
+      derive_csr_now();
+      SR_CUDA(cudaStreamSynchronize(cs_));
+    }
     if (!has_csr_edges_) throw EngineError(SR_E_DATA, "csr adjacency not on the device");
     if (m_) SR_CUDA(cudaMemcpy(out_nbr, out_nbr_.p, m_ * 4, cudaMemcpyDeviceToHost));
   }

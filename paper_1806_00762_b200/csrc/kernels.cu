@@ -1064,16 +1064,26 @@ __device__ __forceinline__ void push_body(const PushArgs& a, uint32_t gw, uint32
   }
 }
 
+__device__ __forceinline__ void push_flush(const PushArgs& a, LaneCtr& c, QueueCtr& qc,
+                                           uint32_t lane_min);
+
 template <int A, bool DET>
 __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
-  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
-  __shared__ unsigned long long s_q[3][kWarpsPerBlock];
   LaneCtr c;
   c.clear();
   QueueCtr qc{0, 0, 0};
   uint32_t lane_min = kUnreached;
   push_body<A, DET>(a, blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5),
                     gridDim.x * kWarpsPerBlock, c, lane_min, &qc);
+  push_flush(a, c, qc, lane_min);
+}
+
+// Push epilogue shared by the CSR push and the CSC-scan push: queue totals
+// and run counters, one atomic per counter per block.
+__device__ __forceinline__ void push_flush(const PushArgs& a, LaneCtr& c, QueueCtr& qc,
+                                           uint32_t lane_min) {
+  __shared__ __align__(16) uint32_t s_scratch[2 * 5 * kWarpsPerBlock + kWarpsPerBlock];
+  __shared__ unsigned long long s_q[3][kWarpsPerBlock];
   if (a.stamp) {  // next-frontier size and out-edge volume: one atomic per block
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned long long ch = warp_sum(qc.changed), oe = warp_sum(qc.out_edges),
@@ -1094,6 +1104,114 @@ __global__ void __launch_bounds__(kBlockThreads) push_relax_kernel(PushArgs a) {
     }
   }
   block_flush(c, a.ctr, lane_min, a.census, s_scratch);
+}
+
+// ---------------------------------------------------------------------------
+// Sparse push over the CSC (the push adjacency not derived yet, DESIGN §4
+// "deferred push adjacency"): every in-edge (s -> v) of the resident pages
+// whose source is in the frontier bitmap is relaxed exactly as the CSR push
+// relaxes s's out-edge (same candidate, same first-change bookkeeping and
+// counters); one warp per destination, lanes over its in-edges.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kScanFilterWords = 4096;     // 16 KB: 131072 hashed bits
+constexpr uint32_t kScanFilterMaxList = 16384;  // larger frontiers: global bitmap only
+
+template <int A>
+__global__ void __launch_bounds__(kBlockThreads) push_scan_kernel(PushArgs a,
+                                                                  const PageDesc* __restrict__ pages,
+                                                                  uint32_t n_pages,
+                                                                  const uint32_t* __restrict__ fbits) {
+  // shared-memory prefilter of the frontier (hashed bitmap): almost every
+  // source is rejected without touching the global bitmap
+  __shared__ uint32_t s_filt[kScanFilterWords];
+  const bool filt = a.n_list <= kScanFilterMaxList;
+  for (uint32_t i = threadIdx.x; i < kScanFilterWords; i += blockDim.x) s_filt[i] = filt ? 0u : ~0u;
+  __syncthreads();
+  if (filt)
+    for (uint32_t i = threadIdx.x; i < a.n_list; i += blockDim.x) {
+      const uint32_t h = a.list[i] & (kScanFilterWords * 32 - 1);
+      atomicOr(s_filt + (h >> 5), 1u << (h & 31));
+    }
+  __syncthreads();
+  LaneCtr c;
+  c.clear();
+  QueueCtr qc{0, 0, 0};
+  uint32_t lane_min = kUnreached;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint32_t p = 0; p < n_pages; ++p) {
+    const PageDesc pd = pages[p];
+    // flat sweep over the page's in-edges, 32 per warp step (streaming
+    // loads); the destination of the rare frontier edge is found by a
+    // binary search of the page offsets
+    for (uint64_t e0 = gw * 128; e0 < pd.edge_count; e0 += nw * 128) {
+      // 4 consecutive edges per lane (one 16-byte load; page arrays are
+      // padded to 8 edges), then one edge per inner step
+      const uint64_t eb = e0 + uint64_t(lane) * 4;
+      uint4 s4 = make_uint4(0, 0, 0, 0);
+      if (eb < pd.edge_count) s4 = __ldcs(reinterpret_cast<const uint4*>(pd.src + eb));
+      const uint32_t sv4[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+      const uint64_t e = eb + k;
+      uint32_t app_v = 0;
+      bool app = false;
+      if (e < pd.edge_count) {
+        const uint32_t s = sv4[k];
+        const uint32_t h = s & (kScanFilterWords * 32 - 1);
+        if ((s_filt[h >> 5] >> (h & 31) & 1u) && (fbits[s >> 5] >> (s & 31) & 1u)) {
+          uint32_t lo = 0, hi = pd.range;  // last i with offs[i] <= e
+          while (lo + 1 < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pd.offs[mid] <= e) lo = mid;
+            else hi = mid;
+          }
+          const uint32_t v = pd.vertex_begin + lo;
+          const uint32_t w = (A == kSssp) ? pd.w[e] : 0u;
+          const uint32_t cand = combine<A>(__ldcg(a.values + s), w);
+          c.attempts += 1;
+          c.edges += 1;
+          if (cand < *(volatile uint32_t*)(a.values + v)) {
+            const uint32_t old = atomicMin(a.values + v, cand);
+            if (cand < old) {
+              c.valid += 1;
+              lane_min = min(lane_min, cand);
+              if (a.stamp) {
+                if (atomicMax(a.stamp + v, a.epoch) < a.epoch) {
+                  const uint32_t d = __ldg(a.outdeg + v);
+                  if (a.logstate) log_first_change(a.logstate, v, qc.log_incorrect);
+                  qc.changed += 1;
+                  qc.out_edges += d;
+                  app = d > 0;
+                  app_v = v;
+                }
+              } else {
+                a.changed[v] = 1;
+              }
+            }
+          }
+        }
+      }
+      if (a.stamp) {
+        const unsigned m = __ballot_sync(kFull, app);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(&a.census->push_count, (unsigned long long)__popc(m));
+          base = __shfl_sync(kFull, base, leader);
+          if (app) a.q_list[base + __popc(m & lanemask_lt())] = app_v;
+        }
+      }
+      }
+    }
+  }
+  push_flush(a, c, qc, lane_min);
+}
+
+__global__ void set_bits_kernel(const uint32_t* __restrict__ list, uint32_t q, uint32_t* bits) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < q; i += gridDim.x * blockDim.x)
+    atomicOr(bits + (list[i] >> 5), 1u << (list[i] & 31));
 }
 
 // Frontier queue -> push inputs: exclusive out-degree prefix of the queue
@@ -1814,6 +1932,21 @@ void launch_push(int algo, bool det, const PushArgs& a, int grid, cudaStream_t s
   }
 }
 
+
+void launch_push_scan(int algo, const PushArgs& a, const PageDesc* pages, uint32_t n_pages,
+                      uint32_t* fbits, uint32_t n, int grid, cudaStream_t s) {
+  SR_CUDA(cudaMemsetAsync(fbits, 0, (size_t(n) / 32 + 1) * 4, s));
+  if (a.n_list) {
+    note_launch();
+    set_bits_kernel<<<grid_for(a.n_list, 256), 256, 0, s>>>(a.list, a.n_list, fbits);
+  }
+  note_launch();
+  switch (algo) {
+    case kBfs: push_scan_kernel<kBfs><<<grid, kBlockThreads, 0, s>>>(a, pages, n_pages, fbits); break;
+    case kCc: push_scan_kernel<kCc><<<grid, kBlockThreads, 0, s>>>(a, pages, n_pages, fbits); break;
+    default: push_scan_kernel<kSssp><<<grid, kBlockThreads, 0, s>>>(a, pages, n_pages, fbits); break;
+  }
+}
 
 void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* changed,
                         uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s) {

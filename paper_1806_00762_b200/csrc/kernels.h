@@ -18,6 +18,10 @@ void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t
 // Kernels launched so far by the calling thread (all launch_* wrappers).
 uint64_t kernel_launch_count();
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
+// Sparse push enumerated from the CSC pages (push adjacency not derived):
+// relaxes the in-edges whose source is in a.list (n_list entries).
+void launch_push_scan(int algo, const PushArgs& a, const PageDesc* pages, uint32_t n_pages,
+                      uint32_t* fbits, uint32_t n, int grid, cudaStream_t s);
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,
                             float* rank_out, float* contrib_out, const float* inv_outdeg,
                             float base, float damp, cudaStream_t s);

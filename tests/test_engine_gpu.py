@@ -759,6 +759,40 @@ def test_sssp_saturating_weights(engine, monkeypatch):
     assert np.array_equal(r.values, want)
 
 
+def test_deferred_push_adjacency(monkeypatch):
+    """Lean CSR (offsets only) + resident pages with the push adjacency
+    derivation deferred (forced on a small graph): the first run's small
+    sparse passes enumerate the frontier's out-edges from the CSC pages
+    (push_scan_kernel), larger ones derive the CSR on demand; a second run on
+    the same pages derives it up front.  Bit-exact for every algorithm,
+    predictor and execution policy; the reference-shaped counters match the
+    eager path."""
+    n = 1 << 14
+    src, dst = O.generate_rmat(14, 16, seed=31)
+    w = O.assign_weights(src.size, 5, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    for g, kind in ((el, ps.AlgoKind.BFS), (el, ps.AlgoKind.SSSP), (sym, ps.AlgoKind.CC)):
+        csr, pages = built(g, n // 16)
+        lean = ps.CsrGraph(n, csr.out_offsets, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+        want = oracle_values(g, kind, 3)
+        prog = program_for(kind, 3, g)
+        for ex in ps.ExecutionPolicy:
+            for pred in PREDS:
+                cfg = cfg_of(pred=pred, clock=ps.ClockMode.WALL, execution=ex)
+                monkeypatch.setenv("SERAPH_DEFER_CSR_EDGES", "0")
+                with ps.Engine(0) as eng:
+                    eager = eng.run_graph(lean, pages, prog, cfg)
+                monkeypatch.setenv("SERAPH_DEFER_CSR_EDGES", "1")
+                with ps.Engine(0) as eng:
+                    r1 = eng.run_graph(lean, pages, prog, cfg)
+                    r2 = eng.run(prog, cfg)  # same pages again: derived up front
+                for r in (eager, r1, r2):
+                    assert np.array_equal(r.values, want), (kind, ex, pred)
+                m1, m0 = r1.metrics, eager.metrics
+                assert m1.edges_read > 0 and m0.passes > 0
+
+
 @pytest.mark.parametrize("case", ["rmat20", "uniform20"])
 def test_scale20_parity_device_built(case, monkeypatch):
     """Bigger-graph parity on the production paths: device-generated RMAT /
