@@ -238,6 +238,7 @@ int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const
     // the offsets DMA stays queued ahead of the page DMAs on the copy stream
     // (load_pages synchronises it before the host buffers are released)
     ctx->eng->load_csr(n, m, off, derive ? nullptr : nbr, derive ? nullptr : w, /*sync=*/false);
+    ctx->eng->set_load_algo(cfg->algo);
     ctx->eng->load_pages(n, cap, weighted, pages, np);
     const double up = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     sr_metrics mm{};

@@ -172,14 +172,19 @@ void Engine::finish_csr(bool sync) {
   csr_derived_ = false;
 }
 
-// Graphs of at least this many edges defer the push adjacency derivation
-// (SERAPH_DEFER_CSR_EDGES overrides; 0 = never defer).
-uint64_t Engine::defer_csr_min_edges() const {
+// Defer the push adjacency derivation of a one-shot sr_run_graph when the
+// run will need it only for a few small sparse passes: connected components
+// (the initial frontier is every vertex, so its sparse passes come last) on
+// >= 2^30 edges.  BFS/SSSP start with sparse passes from the source and keep
+// the derivation overlapped with the upload (SSSP RMAT-26: 198 ms per call
+// eager vs 311 ms deferred).  SERAPH_DEFER_CSR_EDGES=<edges> forces the
+// threshold for every algorithm (0 = never defer).
+bool Engine::defer_csr(uint64_t m, int algo) const {
   if (const char* e = std::getenv("SERAPH_DEFER_CSR_EDGES")) {
     const uint64_t v = std::strtoull(e, nullptr, 10);
-    return v ? v : ~0ull;
+    return v != 0 && m >= v;
   }
-  return 1ull << 30;
+  return algo == SR_ALGO_CC && m >= (1ull << 30);
 }
 
 void Engine::derive_csr_now() {
@@ -273,6 +278,8 @@ void Engine::build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st) {
 
 void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* views,
                         uint32_t np) {
+  const int algo_hint = load_algo_;  // one load only (sr_run_graph sets it)
+  load_algo_ = -1;
   SR_CUDA(cudaSetDevice(dev_));
   const auto t0 = std::chrono::steady_clock::now();
   if (np == 0 && n != 0) throw EngineError(SR_E_INPUT, "page set has no pages");
@@ -425,7 +432,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
                   m_ == page_edges_total_;
     csr_deferred_ = false;
     runs_since_pages_ = 0;
-    if (derive && m_ >= defer_csr_min_edges()) {  // derived on demand (derive_csr_now)
+    if (derive && defer_csr(m_, algo_hint)) {  // derived on demand (derive_csr_now)
       derive = false;
       csr_deferred_ = true;
       csr_weighted_ = weighted;  // what the derivation will produce

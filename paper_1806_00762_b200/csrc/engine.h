@@ -185,8 +185,15 @@ class Engine {
   uint32_t runs_since_pages_ = 0;
   uint32_t scan_pushes_ = 0;  // CSC-scan pushes in the current run
   DBuf<uint32_t> fbits_;      // frontier bitmap of a CSC-scan push
-  uint64_t defer_csr_min_edges() const;
+  bool defer_csr(uint64_t m, int algo) const;
   void derive_csr_now();
+
+ public:
+  // sr_run_graph: the algorithm the next load_pages is for (-1 = unknown)
+  void set_load_algo(int algo) { load_algo_ = algo; }
+
+ private:
+  int load_algo_ = -1;
   uint32_t push_chunk_shift(uint64_t total) const;
   void read_census();
   void exchange_round(bool pagerank);
