@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
   const int lane = threadIdx.x & 31;
   uint32_t* best_of = s_best[warp];
   const uint32_t total = a.seg.task_prefix[a.seg.n];
+  const uint32_t grab = a.grab ? a.grab : kGrab;
 
   LaneCtr c;
   c.clear();
@@ -263,10 +264,10 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
 
   for (;;) {
     uint32_t t0 = 0;
-    if (lane == 0) t0 = atomicAdd(a.work, kGrab);
+    if (lane == 0) t0 = atomicAdd(a.work, grab);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= total) break;
-    const uint32_t t1 = min(t0 + kGrab, total);
+    const uint32_t t1 = min(t0 + grab, total);
     for (uint32_t t = t0; t < t1; ++t) {
       const uint32_t ti = task_to_tile(a.seg, t);
       const uint32_t p = a.tile_page[ti];
