@@ -713,6 +713,15 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.s_cc = s_cc_;
       a.l_sssp = l_sssp_;
       a.src_floor = floor_sssp_;
+      {
+        // tiles per work grab: about 1/16 of a warp's share of the launch,
+        // 1..8 (measured best: C1 1, C2 2, SSSP RMAT-26 8 -- small launches
+        // with big grabs leave warps idle, big ones amortise the atomic)
+        const uint64_t warps = uint64_t(std::max(grid, 1)) * kWarpsPerBlock;
+        const uint64_t share = uint64_t(seg.task_prefix[seg.n]) / (warps * 16);
+        a.grab = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, share)));
+        if (const char* e = std::getenv("SERAPH_K1_GRAB")) a.grab = uint32_t(std::atoi(e));
+      }
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());
