@@ -49,6 +49,13 @@ def _load_oracle():
         "oracle_brute_fixpoint": (None, [_U32, _U64, _VP, _VP, _VP, C.c_int, _U32, _VP]),
         "oracle_pagerank": (None, [_U32, _VP, _VP, _VP, _U32, _D, _VP]),
         "oracle_mt64_nth": (_U64, [_U64, _U64]),
+        # oracle_par.c (OpenMP)
+        "oracle_generate_rmat_par": (C.c_int, [C.c_int, _U64, _D, _D, _D, _U64, _VP, _VP, C.c_int]),
+        "oracle_assign_weights_par": (C.c_int, [_U64, _U64, _U32, _U32, _VP, C.c_int]),
+        "oracle_symmetrize_par": (None, [_U64, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
+        "oracle_build_adjacency_par": (C.c_int, [_U32, _U64, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
+        "oracle_pagerank_par": (None, [_U32, _VP, _VP, _VP, _U32, _D, _VP, C.c_int]),
+        "oracle_pr_compare": (None, [_U32, _VP, _VP, _D, _VP, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -67,6 +74,59 @@ def generate_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, d=0.05, seed=0)
     rc = lib.oracle_generate_rmat(scale, edge_factor, a, b, c, seed, _p(src), _p(dst))
     assert rc == 0
     return src, dst
+
+
+def generate_rmat_par(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, d=0.05, seed=0, threads=0):
+    """generate_rmat on `threads` OpenMP threads (jump-ahead chunks), bit-exact."""
+    m = (1 << scale) * edge_factor
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    assert lib.oracle_generate_rmat_par(scale, edge_factor, a, b, c, seed, _p(src), _p(dst),
+                                        threads) == 0
+    return src, dst
+
+
+def assign_weights_par(m, seed, lo=1, hi=64, threads=0):
+    w = np.empty(m, np.uint32)
+    assert lib.oracle_assign_weights_par(m, seed, lo, hi, _p(w), threads) == 0
+    return w
+
+
+def symmetrize_par(src, dst, w=None, threads=0):
+    m = src.size
+    os_, od = np.empty(2 * m, np.uint32), np.empty(2 * m, np.uint32)
+    ow = np.empty(2 * m, np.uint32) if w is not None and w.size else None
+    lib.oracle_symmetrize_par(m, _p(src), _p(dst), _p(w) if ow is not None else None, _p(os_),
+                              _p(od), _p(ow), threads)
+    return os_, od, ow
+
+
+def build_adjacency_par(n, key, other, w=None, threads=0):
+    """Stable counting sort by key: (offsets u64[n+1], other, w) -- build_csr with
+    key=src, the global CSC of build_csc_pages with key=dst."""
+    m = key.size
+    off = np.zeros(n + 1, np.uint64)
+    oo = np.empty(m, np.uint32)
+    ow = np.empty(m, np.uint32) if w is not None and w.size else None
+    assert lib.oracle_build_adjacency_par(n, m, _p(key), _p(other),
+                                          _p(w) if ow is not None else None, _p(off), _p(oo),
+                                          _p(ow), threads) == 0
+    return off, oo, ow
+
+
+def pagerank_par(n, in_off, in_src, out_off, iters=20, damping=0.85, threads=0):
+    """fp64 PageRank checker over a global CSC + CSR offsets (OpenMP)."""
+    r = np.empty(n, np.float64)
+    lib.oracle_pagerank_par(n, _p(in_off), _p(in_src), _p(out_off), iters, damping, _p(r), threads)
+    return r
+
+
+def pr_compare(got_f32, want_f64, rel_floor=1e-12, threads=0):
+    """(max |d|, max |d|/want over want > rel_floor, sum |d|)."""
+    out = np.zeros(3, np.float64)
+    lib.oracle_pr_compare(want_f64.size, _p(np.ascontiguousarray(got_f32, np.float32)),
+                          _p(want_f64), rel_floor, _p(out), threads)
+    return float(out[0]), float(out[1]), float(out[2])
 
 
 def assign_weights(m, seed, lo=1, hi=64):

@@ -1,10 +1,9 @@
 // Device-side graph construction.
 //
-//  * dg_rmat / dg_weights: the counter-based RMAT generator and uniform
-//    weights of hostgraph.cpp (quadrant law of the reference's generate_rmat,
-//    ingest.cpp:112-141; assign_weights range rule, ingest.cpp:143-152) on
-//    the GPU, bit-identical to the host version (same splitmix64 stream, same
-//    IEEE double comparisons).
+//  * dg_rmat / dg_weights: the reference's generate_rmat and assign_weights
+//    (ingest.cpp:112-152) bit-for-bit: its sequential std::mt19937_64
+//    stream, cut into chunks by GF(2) jump-ahead (mt64.h), one warp per
+//    chunk.
 //  * dg_symmetrize: symmetrize (graph.cpp:102-118): edge i, then its reverse.
 //  * dg_stable_adjacency: the reference's build_csr / build_csc_pages
 //    (graph.cpp:30-94) -- a STABLE counting sort by key, so within a source
@@ -20,20 +19,15 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "devgraph.h"
+#include "mt64.h"
 #include "errors.h"
 
 namespace seraph {
 
 namespace {
-
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ull;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
-}
 
 constexpr int kThreads = 256;
 
@@ -42,35 +36,150 @@ inline unsigned grid_of(uint64_t work) {
   return unsigned(std::min<uint64_t>(std::max<uint64_t>(g, 1), 148ull * 32));
 }
 
-__global__ void rmat_kernel(int scale, uint64_t m, double a, double ab, double abc, uint64_t seed,
-                            uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
-  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
-       e += uint64_t(gridDim.x) * blockDim.x) {
-    uint64_t s = mix64(seed ^ mix64(e));
-    uint32_t u = 0, v = 0;
-    for (int bit = scale - 1; bit >= 0; --bit) {
-      s += 0x9e3779b97f4a7c15ull;
-      const double r = double(mix64(s) >> 11) * 0x1.0p-53;
-      if (r < a) {
-      } else if (r < ab) {
-        v |= 1u << bit;
-      } else if (r < abc) {
-        u |= 1u << bit;
-      } else {
-        u |= 1u << bit;
-        v |= 1u << bit;
+// ---- std::mt19937_64 on the device (mt64.h) --------------------------------
+// The reference's generate_rmat / assign_weights draw from ONE sequential
+// std::mt19937_64 stream (ingest.cpp:112-152).  The stream is cut into
+// chunks of whole edges; every chunk starts from its own engine window,
+// obtained by GF(2) jump-ahead (mt_jump_kernel), and one warp generates it.
+namespace mtd {
+constexpr int N = mt64::kN, M = mt64::kM;
+constexpr int kGenWarps = 8;
+
+__device__ __forceinline__ uint64_t twist(uint64_t xk, uint64_t xk1, uint64_t xm) {
+  const uint64_t y = (xk & mt64::kUpper) | (xk1 & mt64::kLower);
+  return xm ^ (y >> 1) ^ ((y & 1) ? mt64::kMatrixA : 0ull);
+}
+__device__ __forceinline__ uint64_t temper(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  return y ^ (y >> 43);
+}
+// one twist of a warp's window: nxt = the next 312 raw words after cur
+__device__ __forceinline__ void warp_twist(const uint64_t* cur, uint64_t* nxt, int lane) {
+  for (int t = lane; t < M; t += 32) nxt[t] = twist(cur[t], cur[t + 1], cur[t + M]);
+  __syncwarp();
+  for (int t = M + lane; t < N; t += 32)
+    nxt[t] = twist(cur[t], t + 1 < N ? cur[t + 1] : nxt[0], nxt[t - M]);
+  __syncwarp();
+}
+}  // namespace mtd
+
+// Jump: out window (dst0 + task) = g(T) window (src0 + task).  The block
+// expands its window into the next 20 280 raw words in shared memory (two
+// parallel phases per twist), then thread j XORs word i + j over the set
+// bits i of g (mt64.h).
+__global__ void __launch_bounds__(320) mt_jump_kernel(uint64_t* wins, uint32_t src0, uint32_t dst0,
+                                                      const uint64_t* __restrict__ poly) {
+  extern __shared__ uint64_t sm[];
+  uint64_t* seq = sm;
+  uint64_t* g = sm + mt64::kSeqWords;
+  const int tid = threadIdx.x;
+  const uint64_t* win = wins + size_t(src0 + blockIdx.x) * mtd::N;
+  for (int i = tid; i < mtd::N; i += blockDim.x) {
+    seq[i] = win[i];
+    g[i] = poly[i];
+  }
+  __syncthreads();
+  for (int b = 0; b + 1 < mt64::kSeqWords / mtd::N; ++b) {
+    const int k = b * mtd::N + tid;
+    if (tid < mtd::M) seq[k + mtd::N] = mtd::twist(seq[k], seq[k + 1], seq[k + mtd::M]);
+    __syncthreads();
+    if (tid >= mtd::M && tid < mtd::N)
+      seq[k + mtd::N] = mtd::twist(seq[k], seq[k + 1], seq[k + mtd::M]);
+    __syncthreads();
+  }
+  if (tid < mtd::N) {
+    uint64_t acc = 0;
+    for (int w = 0; w < mt64::kPolyWords; ++w) {
+      uint64_t bits = g[w];
+      while (bits) {
+        const int i = w * 64 + __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        acc ^= seq[i + tid];
       }
     }
-    src[e] = u;
-    dst[e] = v;
+    wins[size_t(dst0 + blockIdx.x) * mtd::N + tid] = acc;
   }
 }
 
-__global__ void weights_kernel(uint64_t m, uint64_t seed, uint32_t lo, uint64_t span,
-                               uint32_t* __restrict__ w) {
-  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
-       e += uint64_t(gridDim.x) * blockDim.x)
-    w[e] = uint32_t(lo + mix64(seed ^ mix64(e + 0x51ull)) % span);
+// generate_rmat (ingest.cpp:112-141): chunk ch = edges [ch*per, ch*per+per);
+// edge e consumes draws e*scale .. e*scale+scale-1 of the stream, one
+// quadrant per draw from the most significant bit down.  Lanes turn the
+// warp's 312 fresh draws into 2-bit quadrant codes in a byte ring, then build
+// the edges whose draws are all present (consecutive lanes, consecutive edges).
+__global__ void __launch_bounds__(256) mt_rmat_kernel(const uint64_t* __restrict__ wins,
+                                                      uint32_t chunks, uint64_t per, uint64_t m,
+                                                      int scale, uint64_t ta, uint64_t tab,
+                                                      uint64_t tabc, uint32_t* __restrict__ src,
+                                                      uint32_t* __restrict__ dst) {
+  __shared__ uint64_t win[mtd::kGenWarps][2][mtd::N];
+  __shared__ uint8_t ring[mtd::kGenWarps][1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ch = blockIdx.x * mtd::kGenWarps + warp;
+  if (ch >= chunks) return;
+  uint64_t e = uint64_t(ch) * per;
+  const uint64_t e_end = min(m, e + per);
+  uint64_t* cur = win[warp][0];
+  uint64_t* nxt = win[warp][1];
+  uint8_t* rg = ring[warp];
+  for (int i = lane; i < mtd::N; i += 32) cur[i] = wins[size_t(ch) * mtd::N + i];
+  __syncwarp();
+  uint32_t head = 0, have = 0;
+  while (e < e_end) {
+    mtd::warp_twist(cur, nxt, lane);
+    for (int t = lane; t < mtd::N; t += 32) {
+      const uint64_t k = mtd::temper(nxt[t]) >> 11;  // unit_draw = k * 2^-53 (ingest.cpp:21-23)
+      rg[(head + have + t) & 1023] = uint8_t((k >= ta) + (k >= tab) + (k >= tabc));
+    }
+    __syncwarp();
+    have += mtd::N;
+    const uint64_t left = e_end - e, full = have / uint32_t(scale);
+    const uint32_t ne = uint32_t(full < left ? full : left);
+    for (uint32_t i = lane; i < ne; i += 32) {
+      uint32_t u = 0, v = 0, at = head + i * uint32_t(scale);
+      for (int bit = scale - 1; bit >= 0; --bit, ++at) {
+        const uint32_t c = rg[at & 1023];  // 0: a, 1: b (dst bit), 2: c (src bit), 3: d (both)
+        u |= (c >> 1) << bit;
+        v |= (c & 1u) << bit;
+      }
+      src[e + i] = u;
+      dst[e + i] = v;
+    }
+    __syncwarp();
+    e += ne;
+    head += ne * uint32_t(scale);
+    have -= ne * uint32_t(scale);
+    uint64_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+// assign_weights (ingest.cpp:143-152): w[e] = lo + (draw e) % span.
+__global__ void __launch_bounds__(256) mt_weights_kernel(const uint64_t* __restrict__ wins,
+                                                         uint32_t chunks, uint64_t per, uint64_t m,
+                                                         uint32_t lo, uint64_t span,
+                                                         uint32_t* __restrict__ w) {
+  __shared__ uint64_t win[mtd::kGenWarps][2][mtd::N];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ch = blockIdx.x * mtd::kGenWarps + warp;
+  if (ch >= chunks) return;
+  uint64_t e = uint64_t(ch) * per;
+  const uint64_t e_end = min(m, e + per);
+  uint64_t* cur = win[warp][0];
+  uint64_t* nxt = win[warp][1];
+  for (int i = lane; i < mtd::N; i += 32) cur[i] = wins[size_t(ch) * mtd::N + i];
+  __syncwarp();
+  for (; e < e_end; e += mtd::N) {
+    mtd::warp_twist(cur, nxt, lane);
+    for (int t = lane; t < mtd::N; t += 32)
+      if (e + t < e_end) w[e + t] = uint32_t(lo + mtd::temper(nxt[t]) % span);
+    __syncwarp();
+    uint64_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
 }
 
 __global__ void symmetrize_kernel(uint64_t m, const uint32_t* __restrict__ src,
@@ -206,17 +315,77 @@ int key_bits(uint32_t n) {
 
 }  // namespace
 
+namespace {
+
+// chunk count of a device stream: one warp per chunk, ~1 K draws minimum
+uint32_t mt_chunks(uint64_t units, uint64_t draws_per_unit) {
+  uint64_t c = std::max<uint64_t>(1, units * draws_per_unit / 65536);
+  c = std::min<uint64_t>(c, 4096);
+  if (const char* e = std::getenv("SERAPH_MT_CHUNKS")) c = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  return uint32_t(std::min<uint64_t>(c, std::max<uint64_t>(units, 1)));
+}
+
+// Engine windows W_{c*J}, c = 0..chunks-1, of std::mt19937_64(seed), on the
+// device: W_0 (seeding) and W_1 on the host, W_J = x^{J-1}(T) W_1, then a
+// doubling tree of jumps by J*2^r (polynomials x^{J 2^r} mod phi from the host).
+void mt_windows(uint64_t seed, uint64_t J, uint32_t chunks, uint64_t* wins, cudaStream_t s) {
+  constexpr int N = mt64::kN;
+  std::vector<uint64_t> w0(N), w1(N);
+  mt64::seed_window(seed, w0.data());
+  SR_CUDA(cudaMemcpyAsync(wins, w0.data(), N * 8, cudaMemcpyHostToDevice, s));
+  if (chunks > 1) {
+    w1 = w0;
+    mt64::advance_window(w1.data());
+    std::vector<uint64_t> polys;
+    const mt64::Poly p0 = mt64::xpow_mod(J - 1);
+    polys.insert(polys.end(), p0.begin(), p0.end());
+    mt64::Poly q = mt64::xpow_mod(J);
+    int rounds = 0;
+    for (uint64_t span = 1; span < chunks - 1; span <<= 1, ++rounds) {
+      if (rounds) q = mt64::sqr_mod(q);
+      polys.insert(polys.end(), q.begin(), q.end());
+    }
+    Tmp<uint64_t> dpoly(polys.size(), s);
+    SR_CUDA(cudaMemcpyAsync(dpoly.p, polys.data(), polys.size() * 8, cudaMemcpyHostToDevice, s));
+    SR_CUDA(cudaMemcpyAsync(wins + size_t(chunks) * N, w1.data(), N * 8, cudaMemcpyHostToDevice, s));
+    const int smem = int((mt64::kSeqWords + mt64::kPolyWords) * sizeof(uint64_t));
+    SR_CUDA(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    mt_jump_kernel<<<1, 320, smem, s>>>(wins, chunks, 1, dpoly.p);
+    SR_CUDA(cudaGetLastError());
+    int r = 0;
+    for (uint32_t span = 1; span < chunks - 1; span <<= 1, ++r) {
+      const uint32_t tasks = std::min(span, chunks - 1 - span);
+      mt_jump_kernel<<<tasks, 320, smem, s>>>(wins, 1, 1 + span, dpoly.p + size_t(1 + r) * N);
+      SR_CUDA(cudaGetLastError());
+    }
+    SR_CUDA(cudaStreamSynchronize(s));  // host vectors and dpoly go out of scope
+  }
+}
+
+}  // namespace
+
 void dg_rmat(int scale, uint64_t m, double a, double b, double c, uint64_t seed, uint32_t* src,
              uint32_t* dst, cudaStream_t s) {
   if (!m) return;
-  const double ab = a + b, abc = ab + c;
-  rmat_kernel<<<grid_of(m), kThreads, 0, s>>>(scale, m, a, ab, abc, seed, src, dst);
+  const double ab = a + b, abc = ab + c;  // ingest.cpp:119-120
+  const uint32_t chunks = mt_chunks(m, uint64_t(scale));
+  const uint64_t per = (m + chunks - 1) / chunks;
+  Tmp<uint64_t> wins(size_t(chunks + 1) * mt64::kN, s);
+  mt_windows(seed, per * uint64_t(scale), chunks, wins.p, s);
+  mt_rmat_kernel<<<(chunks + mtd::kGenWarps - 1) / mtd::kGenWarps, 256, 0, s>>>(
+      wins.p, chunks, per, m, scale, mt64::draw_threshold(a), mt64::draw_threshold(ab),
+      mt64::draw_threshold(abc), src, dst);
   SR_CUDA(cudaGetLastError());
 }
 
 void dg_weights(uint64_t m, uint64_t seed, uint32_t lo, uint32_t hi, uint32_t* w, cudaStream_t s) {
   if (!m) return;
-  weights_kernel<<<grid_of(m), kThreads, 0, s>>>(m, seed, lo, uint64_t(hi) - lo + 1, w);
+  const uint32_t chunks = mt_chunks(m, 1);
+  const uint64_t per = (m + chunks - 1) / chunks;
+  Tmp<uint64_t> wins(size_t(chunks + 1) * mt64::kN, s);
+  mt_windows(seed, per, chunks, wins.p, s);
+  mt_weights_kernel<<<(chunks + mtd::kGenWarps - 1) / mtd::kGenWarps, 256, 0, s>>>(
+      wins.p, chunks, per, m, lo, uint64_t(hi) - lo + 1, w);
   SR_CUDA(cudaGetLastError());
 }
 
@@ -254,6 +423,12 @@ bool dg_weights_valid(uint64_t m, const uint32_t* w, cudaStream_t s) {
   SR_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
   SR_CUDA(cudaStreamSynchronize(s));
   return h == 0;
+}
+
+void dg_weights_check_async(uint64_t m, const uint32_t* w, unsigned* bad, cudaStream_t s) {
+  if (!m || !w) return;
+  check_weights_kernel<<<grid_of(m), kThreads, 0, s>>>(m, w, bad);
+  SR_CUDA(cudaGetLastError());
 }
 
 void dg_page_offsets(uint32_t n, uint32_t cap, const unsigned long long* off, uint32_t* local,

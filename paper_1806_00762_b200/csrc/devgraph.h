@@ -30,6 +30,8 @@ void dg_deinterleave(uint64_t m, const uint32_t* records, bool weighted, uint32_
                      uint32_t* dst, uint32_t* w, cudaStream_t s);
 // true when every weight is >= 1 (EdgeList::validate, graph.cpp:9-22; synchronises s)
 bool dg_weights_valid(uint64_t m, const uint32_t* w, cudaStream_t s);
+// ORs 1 into *bad (device word) when any of the m weights is < 1; no sync.
+void dg_weights_check_async(uint64_t m, const uint32_t* w, unsigned* bad, cudaStream_t s);
 // page-local u32 offsets of pages of `cap` vertices (layout of sr_page_offsets)
 void dg_page_offsets(uint32_t n, uint32_t cap, const unsigned long long* off, uint32_t* local,
                      cudaStream_t s);

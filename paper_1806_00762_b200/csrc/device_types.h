@@ -93,6 +93,7 @@ struct PullArgs {
   uint32_t s_cc;
   uint32_t l_sssp;
   uint32_t src_floor;  // SSSP: lower bound of every source that can still improve (0 = none)
+  uint32_t floor_step; // SSSP: smallest edge weight bound (1; 0 when a page holds weight-0 edges)
   uint32_t grab;       // tiles per work-counter grab (0 = kGrab)
 };
 

@@ -13,6 +13,7 @@
 #include <thread>
 
 #include "kernels.h"
+#include "devgraph.h"
 #include "nccl_dyn.h"
 
 namespace seraph {
@@ -276,6 +277,19 @@ void Engine::build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st) {
   run_id_ = 0;
 }
 
+// K1 tiles per work-counter grab: about 1/16 of a warp's share of the
+// launch, clamped to 1..8; `env` overrides within the same range (A/B knob).
+uint32_t k1_grab(uint64_t tiles, int grid, const char* env) {
+  const uint64_t warps = uint64_t(std::max(grid, 1)) * kWarpsPerBlock;
+  uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(8, tiles / (warps * 16)));
+  if (const char* e = std::getenv(env)) {
+    char* end = nullptr;
+    const unsigned long v = std::strtoul(e, &end, 10);
+    if (end != e && *end == 0 && v >= 1 && v <= 64) g = v;
+  }
+  return uint32_t(g);
+}
+
 void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* views,
                         uint32_t np) {
   const int algo_hint = load_algo_;  // one load only (sr_run_graph sets it)
@@ -461,6 +475,17 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     // compute work on the pages is ordered after every copy
     for (uint32_t p = 0; p < np; ++p)
       if (used[p]) SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
+    weights_ge1_ = true;
+    if (weighted) {  // one device scan of the resident weights (~0.15 ms per G edges)
+      wflag_.reserve(1);
+      SR_CUDA(cudaMemsetAsync(wflag_.p, 0, 4, cs_));
+      for (uint32_t p = 0; p < np; ++p)
+        if (used[p]) dg_weights_check_async(pages_[p].edges, page_desc_h_[p].w, wflag_.p, cs_);
+      unsigned bad = 0;
+      SR_CUDA(cudaMemcpyAsync(&bad, wflag_.p, 4, cudaMemcpyDeviceToHost, cs_));
+      SR_CUDA(cudaStreamSynchronize(cs_));
+      weights_ge1_ = bad == 0;
+    }
     SR_CUDA(cudaStreamSynchronize(xs_));  // host buffers are borrowed only for the call
     for (auto& pm : pages_) pm.h_offs = pm.h_src = pm.h_w = nullptr;
   } else {
@@ -491,6 +516,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
              at.type == cudaMemoryTypeDevice;
     };
     const bool dev_src = !place.empty() && on_device(pages_[place[0].first].h_src);
+    std::vector<char> zero_w(place.size(), 0);
     parallel_for(place.size(), [&](size_t k) {
       PageMeta& pm = pages_[place[k].first];
       uint32_t* base = stage_.p + place[k].second;
@@ -501,11 +527,18 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
         SR_CUDA(cudaMemcpy(base + so, pm.h_src, pm.edges * 4, cudaMemcpyDeviceToHost));
         if (weighted)
           SR_CUDA(cudaMemcpy(base + wo, pm.h_w, pm.edges * 4, cudaMemcpyDeviceToHost));
-        return;
+      } else {
+        std::memcpy(base + so, pm.h_src, pm.edges * 4);
+        if (weighted) std::memcpy(base + wo, pm.h_w, pm.edges * 4);
       }
-      std::memcpy(base + so, pm.h_src, pm.edges * 4);
-      if (weighted) std::memcpy(base + wo, pm.h_w, pm.edges * 4);
+      if (weighted) {
+        const uint32_t* wp = base + wo;
+        uint32_t mn = 1;
+        for (uint64_t e = 0; e < pm.edges; ++e) mn = std::min(mn, wp[e]);
+        zero_w[k] = mn < 1;
+      }
     });
+    weights_ge1_ = std::find(zero_w.begin(), zero_w.end(), 1) == zero_w.end();
     for (auto& [p, off] : place) {
       PageMeta& pm = pages_[p];
       const size_t r1 = size_t(pm.ve - pm.vb) + 1, so = pad8(r1), wo = so + pad8(pm.edges);
@@ -713,14 +746,12 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.s_cc = s_cc_;
       a.l_sssp = l_sssp_;
       a.src_floor = floor_sssp_;
+      a.floor_step = weights_ge1_ ? 1u : 0u;
       {
         // tiles per work grab: about 1/16 of a warp's share of the launch,
         // 1..8 (measured best: C1 1, C2 2, SSSP RMAT-26 8 -- small launches
         // with big grabs leave warps idle, big ones amortise the atomic)
-        const uint64_t warps = uint64_t(std::max(grid, 1)) * kWarpsPerBlock;
-        const uint64_t share = uint64_t(seg.task_prefix[seg.n]) / (warps * 16);
-        a.grab = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, share)));
-        if (const char* e = std::getenv("SERAPH_K1_GRAB")) a.grab = uint32_t(std::atoi(e));
+        a.grab = k1_grab(seg.task_prefix[seg.n], grid, "SERAPH_K1_GRAB");
       }
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
@@ -1495,7 +1526,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     // since the previous dense pass bounds every source that can still
     // improve a destination.  Not under the weak predictor, whose dormant
     // destinations miss relaxations until a recovery sweep.
-    if (algo_ == SR_ALGO_SSSP && !weak) {
+    if (algo_ == SR_ALGO_SSSP && !weak && weights_ge1_) {
       if (strong) {
         floor_sssp_ = l_sssp_;
       } else {

@@ -20,6 +20,8 @@
 
 namespace seraph {
 
+uint32_t k1_grab(uint64_t tiles, int grid, const char* env);
+
 struct LoopbackGroup;
 
 template <typename T>
@@ -298,6 +300,11 @@ class Engine {
   unsigned long long k_bfs_ = 0;
   uint32_t s_cc_ = 0, l_sssp_ = 0;
   uint32_t floor_sssp_ = 0;  // K1's source floor (PullArgs::src_floor)
+  // every loaded page weight >= 1 (EdgeList::validate, graph.cpp:9-22); the
+  // SSSP source floor assumes it, so hand-built page sets with weight-0
+  // edges run without it (the reference's run() accepts them)
+  bool weights_ge1_ = true;
+  DBuf<unsigned> wflag_;
   VWindow vwin_;
   VClock vclock_;
   VModel vmodel_;

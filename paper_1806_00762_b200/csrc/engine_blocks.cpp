@@ -244,12 +244,13 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     a.s_cc = s_cc_;
     a.l_sssp = l_sssp_;
     a.src_floor = floor_sssp_;
-    // sub-page tiles are small and numerous: bigger grabs (CC uniform-26:
-    // 4 -> 8 tiles per grab, 9.0 -> 8.6 ms)
-    a.grab = 8;
-    if (const char* e = std::getenv("SERAPH_K1_GRAB_BLOCKED")) a.grab = uint32_t(std::atoi(e));
+    a.floor_step = weights_ge1_ ? 1u : 0u;
     const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
                                             (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    // sub-page tiles are small and numerous: big launches grab 8 tiles
+    // (CC uniform-26: 4 -> 8, 9.0 -> 8.6 ms); a sharded rank's clipped
+    // blocks get the same per-launch share rule as launch_pages
+    a.grab = k1_grab(t1 - t0, grid, "SERAPH_K1_GRAB_BLOCKED");
     auto* evp = relax_begin();
     launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
     SR_CUDA(cudaGetLastError());

@@ -30,6 +30,8 @@ void Engine::build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<u
   if (n == 0) throw EngineError(SR_E_INPUT, "graph has no vertices");
   if (!dg_ids_valid(n, m, src.p, dst.p, cs_))
     throw EngineError(SR_E_INPUT, "edge endpoint out of range (graph.cpp:9-22)");
+  if (weighted && !dg_weights_valid(m, w.p, cs_))
+    throw EngineError(SR_E_INPUT, "edge has weight < 1 (graph.cpp:9-22)");
   const auto t0 = std::chrono::steady_clock::now();
   const uint32_t np = uint32_t((uint64_t(n) + cap - 1) / cap);
   DBuf<unsigned long long> in_off;
@@ -108,13 +110,25 @@ void Engine::generate_graph(const sr_graph_spec& g, bool csr_edges) {
     throw EngineError(SR_E_CONFIG, "weights: need 1 <= lo <= hi");
   const uint32_t n = uint32_t(uint64_t(1) << g.scale);
   const uint64_t m0 = uint64_t(n) * g.edge_factor;
+  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!timing) return;
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[seraph] generate_graph %s: %.3f s\n", what,
+                 std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
+  };
   DBuf<uint32_t> s0, d0, w0;
   s0.reserve(m0);
   d0.reserve(m0);
   dg_rmat(g.scale, m0, g.a, g.b, g.c, g.seed, s0.p, d0.p, cs_);
+  stage("rmat");
   if (weighted) {
     w0.reserve(m0);
     dg_weights(m0, g.weight_seed, g.weight_lo, g.weight_hi, w0.p, cs_);
+    stage("weights");
   }
   if (!g.symmetrize) {
     build_graph_dev(n, m0, s0, d0, w0, weighted, g.page_vertex_capacity, csr_edges);
@@ -127,10 +141,12 @@ void Engine::generate_graph(const sr_graph_spec& g, bool csr_edges) {
   dg_symmetrize(m0, s0.p, d0.p, weighted ? w0.p : nullptr, s1.p, d1.p, weighted ? w1.p : nullptr,
                 cs_);
   SR_CUDA(cudaStreamSynchronize(cs_));
+  stage("symmetrize");
   s0.release();
   d0.release();
   w0.release();
   build_graph_dev(n, 2 * m0, s1, d1, w1, weighted, g.page_vertex_capacity, csr_edges);
+  stage("build");
 }
 
 // load_binary (ingest.cpp:176-218) straight into the device build: the file's

@@ -1,6 +1,7 @@
 // Host-side graph utilities of libseraph (no GPU needed):
-//  * counter-based parallel RMAT generator (quadrant law of the reference's
-//    generate_rmat, ingest.cpp:112-141, on a splitmix64 counter stream);
+//  * the reference's generate_rmat / assign_weights (ingest.cpp:112-152)
+//    bit-for-bit -- its std::mt19937_64 stream cut into chunks by GF(2)
+//    jump-ahead (mt64.h) and generated on all host threads;
 //  * parallel, stable counting-sort builders producing the reference's CSR
 //    (build_csr, graph.cpp:30-48) and CSC page layouts (build_csc_pages,
 //    graph.cpp:50-94) bit-for-bit: within a source (CSR) or destination
@@ -12,16 +13,12 @@
 #include <thread>
 #include <vector>
 
+#include "mt64.h"
 #include "seraph.h"
 
-namespace {
+namespace mt64 = seraph::mt64;
 
-inline uint64_t mix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ull;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
-}
+namespace {
 
 int clamp_threads(int t) {
   if (t <= 0) {
@@ -108,28 +105,37 @@ int sr_rmat_generate(int scale, uint64_t edge_factor, double a, double b, double
   if (scale < 1 || scale > 31 || edge_factor < 1 || !src || !dst) return SR_E_CONFIG;
   if (a < 0 || b < 0 || c < 0 || d < 0 || std::abs(a + b + c + d - 1.0) > 1e-9) return SR_E_CONFIG;
   const uint64_t m = (uint64_t(1) << scale) * edge_factor;
+  // the reference's sums (ingest.cpp:119-120) as integer draw thresholds
   const double ab = a + b, abc = ab + c;
+  const uint64_t ta = mt64::draw_threshold(a), tab = mt64::draw_threshold(ab),
+                 tabc = mt64::draw_threshold(abc);
   const int T = clamp_threads(threads);
-  run_threads(T, [&](int t) {
-    const uint64_t lo = m * t / T, hi = m * (t + 1) / T;
-    for (uint64_t e = lo; e < hi; ++e) {
-      uint64_t s = mix64(seed ^ mix64(e));
-      uint32_t u = 0, v = 0;
-      for (int bit = scale - 1; bit >= 0; --bit) {
-        s += 0x9e3779b97f4a7c15ull;
-        const double r = double(mix64(s) >> 11) * 0x1.0p-53;
-        if (r < a) {
-        } else if (r < ab) {
-          v |= 1u << bit;
-        } else if (r < abc) {
-          u |= 1u << bit;
-        } else {
-          u |= 1u << bit;
-          v |= 1u << bit;
+  const uint32_t chunks = uint32_t(std::min<uint64_t>(m, uint64_t(T) * 4));
+  const uint64_t per = (m + chunks - 1) / chunks;  // edges per chunk
+  const std::vector<uint64_t> wins = mt64::chunk_windows(seed, per * uint64_t(scale), chunks, T);
+  std::atomic<uint32_t> next{0};
+  run_threads(T, [&](int) {
+    for (uint32_t ch; (ch = next.fetch_add(1)) < chunks;) {
+      mt64::Engine g;
+      g.load(wins.data() + size_t(ch) * mt64::kN);
+      const uint64_t lo = uint64_t(ch) * per, hi = std::min(m, lo + per);
+      for (uint64_t e = lo; e < hi; ++e) {
+        uint32_t u = 0, v = 0;
+        for (int bit = scale - 1; bit >= 0; --bit) {
+          const uint64_t k = g() >> 11;  // unit_draw (ingest.cpp:21-23) = k * 2^-53
+          if (k < ta) {
+          } else if (k < tab) {
+            v |= 1u << bit;
+          } else if (k < tabc) {
+            u |= 1u << bit;
+          } else {
+            u |= 1u << bit;
+            v |= 1u << bit;
+          }
         }
+        src[e] = u;
+        dst[e] = v;
       }
-      src[e] = u;
-      dst[e] = v;
     }
   });
   return SR_OK;
@@ -138,11 +144,20 @@ int sr_rmat_generate(int scale, uint64_t edge_factor, double a, double b, double
 int sr_weights_generate(uint64_t m, uint64_t seed, uint32_t lo, uint32_t hi, uint32_t* w,
                         int threads) {
   if (lo < 1 || lo > hi || (!w && m)) return SR_E_CONFIG;
+  if (!m) return SR_OK;
   const uint64_t span = uint64_t(hi) - lo + 1;
   const int T = clamp_threads(threads);
-  run_threads(T, [&](int t) {
-    const uint64_t a = m * t / T, b = m * (t + 1) / T;
-    for (uint64_t e = a; e < b; ++e) w[e] = uint32_t(lo + mix64(seed ^ mix64(e + 0x51ull)) % span);
+  const uint32_t chunks = uint32_t(std::min<uint64_t>(m, uint64_t(T) * 4));
+  const uint64_t per = (m + chunks - 1) / chunks;
+  const std::vector<uint64_t> wins = mt64::chunk_windows(seed, per, chunks, T);
+  std::atomic<uint32_t> next{0};
+  run_threads(T, [&](int) {
+    for (uint32_t ch; (ch = next.fetch_add(1)) < chunks;) {
+      mt64::Engine g;
+      g.load(wins.data() + size_t(ch) * mt64::kN);
+      const uint64_t a = uint64_t(ch) * per, b = std::min(m, a + per);
+      for (uint64_t e = a; e < b; ++e) w[e] = uint32_t(lo + g() % span);  // ingest.cpp:150
+    }
   });
   return SR_OK;
 }

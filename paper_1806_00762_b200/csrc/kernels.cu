@@ -181,7 +181,9 @@ template <int A>
 __device__ __forceinline__ uint32_t dest_floor(const PullArgs& a) {
   if (A != kSssp) return candidate_floor<A>();
   const uint32_t f = a.src_floor;
-  return f >= kUnreached - 1 ? kUnreached : f + 1;  // weights >= 1 (graph.cpp:9-22)
+  // weights >= 1 (graph.cpp:9-22); pages loaded with weight-0 edges (the
+  // reference's run() accepts hand-built PageSets) run with floor_step 0
+  return f >= kUnreached - 1 ? kUnreached : f + a.floor_step;
 }
 
 // End-of-kernel flush: warp sums -> shared memory -> one atomic per counter

@@ -276,8 +276,9 @@ def resolve_page_capacity(configured: int, num_vertices: int) -> int:
 
 def generate_rmat_fast(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05,
                        seed: int = 0, threads: int = 0) -> EdgeList:
-    """Parallel RMAT with the quadrant law of generate_rmat (ingest.cpp:112-141)
-    on a counter-based stream (not the reference's mt19937_64 sequence)."""
+    """generate_rmat (ingest.cpp:112-141) bit-for-bit on all host threads: the
+    reference's single std::mt19937_64 stream cut into chunks by GF(2)
+    jump-ahead (csrc/mt64.h)."""
     n = 1 << scale
     m = n * edge_factor
     src = np.empty(m, np.uint32)
@@ -289,8 +290,9 @@ def generate_rmat_fast(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19
 
 def generate_rmat_device(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, d=0.05,
                          seed: int = 0, weights=None, device: int = 0) -> EdgeList:
-    """generate_rmat_fast (+ assign_weights_fast when weights=(lo, hi, seed)) on the
-    GPU, copied back: bit-identical to the host generator."""
+    """generate_rmat (+ assign_weights when weights=(lo, hi, seed)) on the GPU --
+    the reference's std::mt19937_64 streams, one warp per jump-ahead chunk --
+    copied back: bit-identical to the reference and the host generator."""
     n = 1 << scale
     m = n * edge_factor
     src = np.empty(m, np.uint32)

@@ -6,6 +6,8 @@ SPEC acceptance criterion 1).  The oracle is oracle/liboracle.so, itself pinned
 to the reference (tests/test_oracle.py).  Bar: bit-exact u32 values for
 BFS/CC/SSSP; PageRank within 1e-6 absolute per vertex (north_star).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -560,14 +562,27 @@ def test_pull_source_blocked(blk, monkeypatch):
 # --------------------------------------------------------------------------
 # device-side graph build and generator
 # --------------------------------------------------------------------------
-def test_device_generator_matches_host():
-    host = ps.assign_weights_fast(ps.generate_rmat_fast(12, 8, seed=3), 7, 1, 64)
+@pytest.mark.parametrize("chunks", [None, "1", "3", "64"])
+def test_device_generator_matches_host(chunks, monkeypatch):
+    """The device generator emits the reference's own std::mt19937_64 streams
+    (generate_rmat + assign_weights, ingest.cpp:112-152) for any chunking
+    (jump-ahead tree on the device); = the host generator."""
+    if chunks:
+        monkeypatch.setenv("SERAPH_MT_CHUNKS", chunks)
     dev = ps.generate_rmat_device(12, 8, seed=3, weights=(1, 64, 7))
-    assert np.array_equal(host.src, dev.src) and np.array_equal(host.dst, dev.dst)
-    assert np.array_equal(host.weights, dev.weights)
+    s, d = O.generate_rmat(12, 8, seed=3)
+    assert np.array_equal(dev.src, s) and np.array_equal(dev.dst, d)
+    assert np.array_equal(dev.weights, O.assign_weights(s.size, 7, 1, 64))
     u = ps.generate_rmat_device(10, 4, 0.25, 0.25, 0.25, 0.25, seed=5)
     hu = ps.generate_rmat_fast(10, 4, 0.25, 0.25, 0.25, 0.25, seed=5)
     assert np.array_equal(u.src, hu.src) and np.array_equal(u.dst, hu.dst)
+
+
+def test_device_generator_reference_fixture():
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "rmat_s10_ef16_seed0.npz"))
+    dev = ps.generate_rmat_device(10, 16, seed=0)
+    assert np.array_equal(dev.src, g["src"]) and np.array_equal(dev.dst, g["dst"])
 
 
 def _assert_same_graph(eng, el, cap):
@@ -757,6 +772,35 @@ def test_sssp_saturating_weights(engine, monkeypatch):
     r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True),
                          cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE, clock=ps.ClockMode.WALL))
     assert np.array_equal(r.values, want)
+
+
+def test_sssp_zero_weight_pages(engine):
+    """Hand-built page sets may hold weight-0 edges: the reference's run() relaxes
+    them as plain Bellman-Ford (engine.cpp:103-128), so the engine must not
+    apply its weight>=1 source floor.  Resident and streamed."""
+    rng = np.random.default_rng(5)
+    n, m = 3000, 30000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    dst[:2000] = 11  # hub chunks
+    w1 = rng.integers(1, 3, m).astype(np.uint32)  # valid for the builders
+    el = ps.EdgeList(n, src, dst, w1)
+    csr, pages = built(el, 256)
+    csr.out_weights -= 1  # now in [0, 1]: half of the edges weigh 0
+    for p in pages.pages:
+        p.in_weights -= 1
+    want = O.solve(n, src, dst, w1 - 1, 2, 0)
+    assert (want == 0).sum() > 1
+    for pol in ps.ExecutionPolicy:
+        for pred in (ps.PredictorMode.OFF, ps.PredictorMode.STRONG):
+            r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True),
+                                 cfg_of(pred=pred, execution=pol, clock=ps.ClockMode.WALL))
+            assert np.array_equal(r.values, want), (pol, pred)
+    with ps.Engine(0, hbm_budget_bytes=64 << 10) as small:
+        r = small.run_graph(csr, pages, ps.make_sssp(0, n, True),
+                            cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE,
+                                   clock=ps.ClockMode.WALL))
+        assert np.array_equal(r.values, want)
 
 
 def test_deferred_push_adjacency(monkeypatch):

@@ -119,6 +119,11 @@ def test_fast_rmat_law_and_determinism():
     a = ps.generate_rmat_fast(12, 16, seed=3, threads=4)
     b = ps.generate_rmat_fast(12, 16, seed=3, threads=7)
     assert np.array_equal(a.src, b.src) and np.array_equal(a.dst, b.dst)
+    # the reference's own stream (generate_rmat, ingest.cpp:112-141)
+    s, d = O.generate_rmat(12, 16, seed=3)
+    assert np.array_equal(a.src, s) and np.array_equal(a.dst, d)
+    w = ps.assign_weights_fast(a, 11, 1, 64, threads=5).weights
+    assert np.array_equal(w, O.assign_weights(a.num_edges(), 11, 1, 64))
     assert a.num_edges() == 16 * 4096 and int(a.src.max()) < 4096
     # quadrant law: P(top bit of dst set) = b + d = 0.24
     frac = float(((a.dst >> 11) & 1).mean())

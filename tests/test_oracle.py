@@ -123,3 +123,53 @@ def test_pagerank_oracle_known_answers():
     r = O.pagerank(5, _arr([1, 2, 3, 4]), _arr([0, 0, 0, 0]), 20, d)
     leaf = (1 - d) / 5
     assert np.allclose(r[1:], leaf) and abs(r[0] - (leaf + d * 4 * leaf)) < 1e-15
+
+
+# ---- multi-threaded oracle pipeline (oracle_par.c): equal to the sequential,
+# reference-pinned restatements ---------------------------------------------------
+@pytest.mark.parametrize("case", [(8, 16, 3, 1), (10, 16, 0, 7), (12, 8, 1, 3), (11, 3, 9, 16)])
+def test_parallel_generator_equals_sequential(case):
+    scale, ef, seed, threads = case
+    for q in ((0.57, 0.19, 0.19, 0.05), (0.25, 0.25, 0.25, 0.25)):
+        s1, d1 = O.generate_rmat(scale, ef, *q[:3], seed=seed)
+        s2, d2 = O.generate_rmat_par(scale, ef, *q, seed=seed, threads=threads)
+        assert np.array_equal(s1, s2) and np.array_equal(d1, d2)
+    w1 = O.assign_weights(s1.size, seed + 1, 1, 64)
+    assert np.array_equal(w1, O.assign_weights_par(s1.size, seed + 1, 1, 64, threads))
+
+
+def test_parallel_generator_matches_reference_fixture():
+    g = load("rmat_s10_ef16_seed0")
+    src, dst = O.generate_rmat_par(10, 16, seed=0, threads=5)
+    assert np.array_equal(src, g["src"]) and np.array_equal(dst, g["dst"])
+
+
+@pytest.mark.parametrize("threads", [1, 4, 13])
+def test_parallel_builders_equal_sequential(threads):
+    rng = np.random.default_rng(threads)
+    for n, m in ((1, 0), (7, 50), (3000, 40000), (70000, 300000)):
+        src = rng.integers(0, n, m).astype(np.uint32)
+        dst = rng.integers(0, n, m).astype(np.uint32)
+        w = rng.integers(1, 65, m).astype(np.uint32)
+        off, nbr, ow = O.build_csr(n, src, dst, w)
+        off2, nbr2, ow2 = O.build_adjacency_par(n, src, dst, w, threads)
+        assert np.array_equal(off, off2) and np.array_equal(nbr, nbr2)
+        assert m == 0 or np.array_equal(ow, ow2)
+        ioff, isrc, iw, _ = O.build_csc(n, src, dst, w, max(n, 1))
+        ioff2, isrc2, iw2 = O.build_adjacency_par(n, dst, src, w, threads)
+        assert np.array_equal(ioff, ioff2) and np.array_equal(isrc, isrc2)
+        ss, sd, sw = O.symmetrize(src, dst, w)
+        ss2, sd2, sw2 = O.symmetrize_par(src, dst, w, threads)
+        assert np.array_equal(ss, ss2) and np.array_equal(sd, sd2)
+
+
+def test_parallel_pagerank_equals_sequential():
+    src, dst = O.generate_rmat(12, 8, seed=2)
+    n = 1 << 12
+    want = O.pagerank(n, src, dst, 20, 0.85)
+    ioff, isrc, _ = O.build_adjacency_par(n, dst, src)
+    ooff, _, _ = O.build_adjacency_par(n, src, dst)
+    got = O.pagerank_par(n, ioff, isrc, ooff, 20, 0.85, threads=6)
+    assert np.max(np.abs(got - want)) < 1e-15
+    mx, mr, l1 = O.pr_compare(got.astype(np.float32), want)
+    assert mx < 1e-9 and mr < 1e-6 and l1 < 1e-6
