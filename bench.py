@@ -1,20 +1,30 @@
 #!/usr/bin/env python3
 """Benchmark of the subgraph-iteration hot path (BASELINE.json metric).
 
-Default workload (N=1): configs[1] of BASELINE.json -- SSSP on RMAT scale-24
-(edge factor 16, uint32 weights in [1,64]), multi-pass subgraph iteration,
-16 CSC pages, one B200.  A "step" is one pagestream::run() to convergence.
+Default workload (N=1): configs[3] of BASELINE.json, the configuration the
+metric is quoted on at 1/2/4/8 B200 -- C4: connected components on the
+uniform-random (a=b=c=d=0.25) scale-27 graph, symmetrized (4.29 G directed
+edges), predictive vertex updating on (strong predictor), 16 CSC pages.
+`--config C1|C2|C3|C4` selects the other BASELINE configs; single flags
+override a preset.  Every graph is the reference's own instance:
+generate_rmat / assign_weights (ingest.cpp:112-152, std::mt19937_64, seed 0;
+weights seed 1 in [1, 64]) -- generated on the GPU here and by the OpenMP
+oracle in the reference arm, bit-identical streams (jump-ahead chunks).
 
-  value  = |E| / time-to-converge (graph GTEPS) with the graph resident in HBM,
-           timed with CUDA events on the engine's stream, max over ranks;
-  e2e    = the same metric through the public C-ABI call sr_run_graph with the
-           graph in pinned host memory (H2D upload + D2H of the values inside
-           the timed region);
-  roofline = the dominant kernel (K1 dense pull sweep) against measured HBM BW;
+A "step" is one pagestream::run() to convergence (PageRank: 20 iterations).
+  value    = |E| * iterations / time-to-converge (graph GTEPS), graph resident
+             in HBM, CUDA-event time on the engine stream, max over ranks;
+  e2e      = the same metric through the public C-ABI call sr_run_graph (the
+             pagestream::run drop-in) with the graph in pinned host memory:
+             upload + run + values D2H inside the timed region;
+  roofline = the dominant kernel (K1 pull / K8 PageRank) per launch, bytes per
+             SURVEY §8(d) (plus the gathered-only model), vs MEASURED_PEAKS;
   cpu_baseline = the reference's own run() (oracle/_ref, compiled from the
-           reference sources) on the box's host cores, same graph and config.
+             reference sources) on the box's host cores, same graph and config
+             (PageRank: the OpenMP fp64 oracle -- the reference has none).
 
-`--impl reference` times the reference run() alone (rank 0 only under torchrun).
+`--impl reference` runs the reference arm: the graph is built by the oracle
+(no libseraph, no GPU) and the reference's run() is timed (rank 0 only).
 """
 from __future__ import annotations
 
@@ -36,6 +46,21 @@ METRIC = "GTEPS and time-to-converge (BFS/SSSP/PR/CC, RMAT) at 1/2/4/8 B200 vs C
 ALGOS = {"bfs": 0, "cc": 1, "sssp": 2, "pagerank": 3}
 MODES = {"baseline": 0, "reentry": 1, "double-buffer": 2, "pipelined": 3, "pipelined-fine": 4}
 PREDS = {"off": 0, "strong": 1, "weak": 2}
+RMAT = (0.57, 0.19, 0.19, 0.05)
+UNIFORM = (0.25, 0.25, 0.25, 0.25)
+L2_LABEL_BYTES = 126 << 20  # B200 L2 (for the workload label; the GPU arm queries the device)
+
+# BASELINE.json configs (C5 needs 8 GPUs with host-streamed shards: not a 1-GPU preset)
+PRESETS = {
+    "C1": dict(algo="bfs", scale=20, uniform=False, pages=16, mode="baseline", predictor="strong",
+               budget_gb=0.0),
+    "C2": dict(algo="sssp", scale=24, uniform=False, pages=16, mode="pipelined",
+               predictor="strong", budget_gb=0.0),
+    "C3": dict(algo="pagerank", scale=26, uniform=False, pages=256, mode="baseline",
+               predictor="off", budget_gb=2.0),
+    "C4": dict(algo="cc", scale=27, uniform=True, pages=16, mode="baseline", predictor="strong",
+               budget_gb=0.0),
+}
 
 
 def parse():
@@ -44,111 +69,100 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--algo", default="sssp", choices=list(ALGOS))
-    p.add_argument("--scale", type=int, default=24)
+    p.add_argument("--config", default="C4", choices=list(PRESETS))
+    p.add_argument("--algo", choices=list(ALGOS))
+    p.add_argument("--scale", type=int)
     p.add_argument("--edge-factor", type=int, default=16)
-    p.add_argument("--uniform", action="store_true", help="a=b=c=d=0.25 (uniform random)")
-    p.add_argument("--pages", type=int, default=16)
-    p.add_argument("--mode", default="baseline", choices=list(MODES))
-    p.add_argument("--predictor", default="strong", choices=list(PREDS))
+    p.add_argument("--uniform", action="store_true", default=None,
+                   help="a=b=c=d=0.25 (uniform random)")
+    p.add_argument("--rmat", dest="uniform", action="store_false",
+                   help="Graph500 quadrants .57/.19/.19/.05")
+    p.add_argument("--pages", type=int)
+    p.add_argument("--mode", choices=list(MODES))
+    p.add_argument("--predictor", choices=list(PREDS))
     p.add_argument("--window", type=int, default=8)
     p.add_argument("--mrt", type=int, default=2)
-    p.add_argument("--budget-gb", type=float, default=0.0, help="forced HBM budget for pages")
+    p.add_argument("--budget-gb", type=float, help="forced HBM budget (out-of-core path)")
     p.add_argument("--pr-iters", type=int, default=20)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--exchange", default="peer", choices=["allreduce", "peer"],
                    help="N>1: peer stores into the other ranks' replicas over CUDA IPC + a "
-                        "barrier per round (falls back to the all-reduce when a peer cannot "
-                        "be mapped), or the MIN all-reduce of the replicas per round")
+                        "barrier per round, or the MIN all-reduce of the replicas per round")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
-    p.add_argument("--graph", default="device", choices=["device", "host"],
-                   help="generate + build the graph on the GPU (sr_generate_graph) or on the host")
     a = p.parse_args()
-    # lean host graph (no host CSR adjacency) when nothing on this run needs it
-    a.lean = a.impl == "ours" and a.no_cpu_baseline and not a.budget_gb and a.gpus == 1
+    for k, v in PRESETS[a.config].items():
+        if getattr(a, k) is None:
+            setattr(a, k, v)
+    a.weighted = a.algo == "sssp"
+    a.symmetric = a.algo == "cc"
     return a
 
 
 # ---------------------------------------------------------------------------
-def workload(args, eng=None, device=0):
-    """Synthetic RMAT graph of the named scale: CSR + 16 CSC pages, all arrays in
-    pinned host memory (e2e / reference inputs).  --graph device (default):
-    generated and built on the GPU (sr_generate_graph, bit-identical to the host
-    pipeline) inside `eng` (left loaded: W["loaded"]) or a scratch context, then
-    exported; --graph host (or no GPU): the parallel host generator/builders."""
-    from paper_1806_00762_b200 import _native as N
-    from paper_1806_00762_b200 import pagestream as ps
-
-    t0 = time.time()
-    quad = (0.25, 0.25, 0.25, 0.25) if args.uniform else (0.57, 0.19, 0.19, 0.05)
-    weighted = args.algo == "sssp"
-    n = 1 << args.scale
-    cap = (n + args.pages - 1) // args.pages
-    lean = getattr(args, "lean", False)
-    arena = N.PinnedArena()
-    if getattr(args, "graph", "host") == "device":
-        try:
-            builder = eng if eng is not None else ps.Engine(device)
-            builder.generate_graph(args.scale, args.edge_factor, *quad, seed=args.seed,
-                                   weights=(1, 64, args.seed + 1) if weighted else None,
-                                   symmetrize=args.algo == "cc", page_vertex_capacity=cap,
-                                   csr_edges=not lean)
-            csr, pages, in_off, in_src, in_w = builder.export_graph(arena, csr_edges=not lean)
-            if eng is None:
-                builder.close()
-            return dict(csr=csr, pages=pages, n=n, m=int(in_off[-1]), cap=cap, in_off=in_off,
-                        in_src=in_src, in_w=in_w if weighted else None, weighted=weighted,
-                        build_s=time.time() - t0, arena=arena, pinned=True, lean=lean,
-                        loaded=eng is not None, graph="device (sr_generate_graph)")
-        except (N.Error, OSError) as e:  # no device: host pipeline
-            print(f"# device graph build unavailable ({e}); host build", file=sys.stderr)
-    el = ps.generate_rmat_fast(args.scale, args.edge_factor, *quad, seed=args.seed)
-    if weighted:
-        el = ps.assign_weights_fast(el, args.seed + 1, 1, 64)
-    if args.algo == "cc":
-        el = ps.symmetrize(el)
-    n, m = el.num_vertices, el.num_edges()
-
-    pin = [True]
-
-    def pinned(count, dtype):
-        if pin[0]:
-            try:
-                return arena.array(count, dtype)
-            except N.Error:
-                pin[0] = False  # no device (CPU-only reference arm): pageable memory
-        return np.empty(count, dtype)
-
-    # The host CSR adjacency is only needed by the reference (cpu_baseline,
-    # --impl reference) and by the out-of-core path; otherwise the engine
-    # derives it on the device from the resident pages and only the
-    # out-degree prefix is built here.
-    out_off = pinned(n + 1, np.uint64)
-    out_nbr = pinned(0 if lean else m, np.uint32)
-    out_w = pinned(m if (weighted and not lean) else 0, np.uint32)
-    in_off = np.zeros(n + 1, np.uint64)
-    in_src = pinned(m, np.uint32)
-    in_w = pinned(m if weighted else 0, np.uint32)
-    if lean:
-        N.check(N.lib.sr_out_offsets(n, m, N.ptr(el.src), N.ptr(out_off), 0))
-    else:
-        N.check(N.lib.sr_build_csr(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
-                                   N.ptr(out_off), N.ptr(out_nbr), N.ptr(out_w), 0))
-    N.check(N.lib.sr_build_csc(n, m, N.ptr(el.src), N.ptr(el.dst), N.ptr(el.weights),
-                               N.ptr(in_off), N.ptr(in_src), N.ptr(in_w), 0))
-    npg = (n + cap - 1) // cap
-    local = pinned(n + npg, np.uint32)
-    N.check(N.lib.sr_page_offsets(n, cap, N.ptr(in_off), N.ptr(local)))
-    csr = ps.CsrGraph(n, out_off, out_nbr, out_w)
-    pages = ps.pages_from_csc(n, cap, in_off, in_src, in_w, local)
-    del el
-    return dict(csr=csr, pages=pages, n=n, m=m, cap=cap, in_off=in_off, in_src=in_src,
-                in_w=in_w if weighted else None, weighted=weighted, build_s=time.time() - t0,
-                arena=arena, pinned=pin[0], lean=lean, loaded=False, graph="host (parallel C++)")
+# the workload, identical in both arms
+# ---------------------------------------------------------------------------
+def config_name(a):
+    return {"bfs": "C1", "sssp": "C5" if a.scale >= 29 else "C2", "pagerank": "C3",
+            "cc": "C4"}[a.algo]
 
 
+def csc_bytes(a, n, m):
+    """Σ page_bytes (graph.cpp:96-100) of the page set."""
+    return ((n + a.pages) + m * (2 if a.weighted else 1)) * 4
+
+
+def workload_config(a, n, m):
+    quad = UNIFORM if a.uniform else RMAT
+    kind = "uniform" if a.uniform else "RMAT"
+    label = (f"{config_name(a)}: {a.algo.upper()} {kind}-{a.scale} ef{a.edge_factor}"
+             f"{' symmetrized' if a.symmetric else ''}{' w[1,64]' if a.weighted else ''}, "
+             f"{a.pages} pages, {a.mode}/{a.predictor}, window {a.window}"
+             f"{f', {a.pr_iters} iterations d=0.85' if a.algo == 'pagerank' else ''}"
+             f"{f', HBM budget {a.budget_gb:g} GB (out-of-core)' if a.budget_gb else ''}")
+    gb = csc_bytes(a, n, m)
+    inst = (f"generate_rmat(scale={a.scale}, ef={a.edge_factor}, a/b/c/d={'/'.join(map(str, quad))}, "
+            f"seed={a.seed}) [std::mt19937_64, ingest.cpp:112-141]")
+    if a.weighted:
+        inst += f" + assign_weights(seed={a.seed + 1}, 1, 64)"
+    if a.symmetric:
+        inst += " + symmetrize"
+    cfg = {"workload": label, "algo": a.algo, "graph": kind.lower(), "quadrants": list(quad),
+           "scale": a.scale, "edge_factor": a.edge_factor, "vertices": n, "edges": m,
+           "pages": a.pages, "schedule": a.mode, "predictor": a.predictor, "window": a.window,
+           "hbm_budget_gb": a.budget_gb or None, "instance": inst,
+           "l2": ("inputs larger than L2 (CSC %.2f GB vs 126 MB L2)" % (gb / 1e9))
+           if gb >= 4 * L2_LABEL_BYTES else
+           ("CSC %.3f GB < 4x L2: the GPU arm flushes L2 before every step" % (gb / 1e9)),
+           "parallelism": f"dp{a.gpus}" if a.gpus > 1 else "single"}
+    if a.algo in ("bfs", "sssp"):
+        cfg["source"] = 0
+    if a.algo == "pagerank":
+        cfg["iterations"] = a.pr_iters
+        cfg["damping"] = 0.85
+    return cfg
+
+
+def degree_hash(out_off):
+    """Instance fingerprint: the CSR degree sequence hashed (wrapping u64)."""
+    off = np.asarray(out_off, np.uint64)
+    k = np.arange(off.size, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15) | np.uint64(1)
+    with np.errstate(over="ignore"):
+        return "%016x" % int(np.bitwise_xor.reduce(off * k) ^ np.uint64(off.size))
+
+
+def value_signature(algo, vals):
+    """Run fingerprint shared by both arms (values are bit-exact across them)."""
+    v = np.asarray(vals)
+    if algo == 1:
+        return {"components": int(np.count_nonzero(v == np.arange(v.size, dtype=np.uint32))),
+                "label_sum": int(v.astype(np.uint64).sum())}
+    reach = v != 0xFFFFFFFF
+    return {"reached": int(reach.sum()), "value_sum": int(v[reach].astype(np.uint64).sum())}
+
+
+# ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -196,12 +210,12 @@ class ClockSampler:
 
 
 def measured_peaks():
-    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
-        if os.path.exists(p):
-            with open(p) as fh:
-                d = json.load(fh)
-            return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def gather_roofline(gathers_per_s, info, clocks):
@@ -215,83 +229,153 @@ def gather_roofline(gathers_per_s, info, clocks):
             "peak_basis": f"{info['sm_count']} SMs x {mhz:.0f} MHz x 1 L1TEX wavefront/cycle"}
 
 
-def profile_traffic(workload_key):
-    """dram bytes per launch of K1 from the committed ncu --set full capture."""
+def profile_traffic(key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
         return None
     with open(path) as fh:
         d = json.load(fh)
-    e = d.get(workload_key)
+    e = d.get(key)
     return e.get("dram_bytes_per_launch") if e else None
 
 
+def k1_roofline(a, runs, info, clocks, step_s):
+    """K1 (dense pull, incl. source-blocked launches) per launch against HBM.
+    SURVEY §8(d) bytes: per edge read 8 B (BFS/CC: in_sources + gathered value)
+    or 12 B (SSSP: + weight), per attempted destination 8 B (in_offsets +
+    value; +1 B status under the weak predictor), per valid update 4 B.  The
+    gathered-only model charges 4 B only for source values actually loaded
+    (edges that provably cannot improve are not gathered)."""
+    from paper_1806_00762_b200 import pagestream as ps
+    per_edge = 12 if a.weighted else 8
+    per_dest = 9 if a.predictor == "weak" else 8
+    b8d = bcons = k1_s = 0.0
+    launches = gathers = edges = 0
+    for r in runs:
+        for st in r.metrics.per_pass:
+            if st.kind != ps.PassKind.SPARSE_PUSH:
+                b8d += per_edge * st.edges_read + per_dest * st.attempts + 4 * st.valid_updates
+                bcons += (per_edge - 4) * st.edges_read + per_dest * st.attempts
+                edges += st.edges_read
+        bcons += 4 * r.metrics.gathers
+        gathers += r.metrics.gathers
+        k1_s += r.metrics.relax_seconds
+        launches += r.metrics.relax_launches
+    if not launches or k1_s <= 0:
+        return None
+    peak, src = measured_peaks()
+    ach = b8d / k1_s / 1e9
+    cons = bcons / k1_s / 1e9
+    return {"bound": "hbm", "kernel": "pull_relax_kernel (K1), every launch inside the timed runs",
+            "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "peak_source": src, "traffic": profile_traffic(f"{a.algo}-s{a.scale}"),
+            "model": f"SURVEY §8(d): {per_edge} B/edge read + {per_dest} B/attempted destination"
+                     " + 4 B/valid update",
+            "algorithmic_bytes_per_launch": int(b8d / launches),
+            "launch_ms": round(k1_s / launches * 1e3, 4), "launches": launches,
+            "share_of_step": round(k1_s / (step_s * len(runs)), 3),
+            "gathered_only_model": {
+                "achieved": round(cons, 1), "frac": round(cons / peak, 4),
+                "bytes_per_launch": int(bcons / launches),
+                "per_unit": f"{per_edge - 4} B/edge read + 4 B/gathered source + "
+                            f"{per_dest} B/attempted destination",
+                "gathered_fraction": round(gathers / max(edges, 1), 4)},
+            "gather_roofline": gather_roofline(gathers / k1_s, info, clocks)}
+
+
 # ---------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank):
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(a, rank, world, local_rank):
     from paper_1806_00762_b200 import _native as N
     from paper_1806_00762_b200 import pagestream as ps
 
-    algo = ALGOS[args.algo]
+    algo = ALGOS[a.algo]
+    pr = algo == 3
     prog = ps.VertexProgram(ps.AlgoKind(algo), 0)
-    cfg = ps.EngineConfig(predictor=ps.PredictorMode(PREDS[args.predictor]),
-                          window_capacity=args.window, clock=ps.ClockMode.WALL,
-                          pr_iterations=args.pr_iters, profile_kernels=True)
-    cfg.schedule.kind = ps.ScheduleModeKind(MODES[args.mode])
-    cfg.schedule.max_reentry_times = args.mrt
-    budget = int(args.budget_gb * 2**30)
+    cfg = ps.EngineConfig(predictor=ps.PredictorMode(PREDS[a.predictor]),
+                          window_capacity=a.window, clock=ps.ClockMode.WALL,
+                          pr_iterations=a.pr_iters, profile_kernels=True)
+    cfg.schedule.kind = ps.ScheduleModeKind(MODES[a.mode])
+    cfg.schedule.max_reentry_times = a.mrt
+    budget = int(a.budget_gb * 2**30)
+    quad = UNIFORM if a.uniform else RMAT
+    n = 1 << a.scale
+    cap = (n + a.pages - 1) // a.pages
 
     def sync():
         N.check(N.lib.sr_device_sync(local_rank))
 
-    dist = None
+    dist = torch = None
     if world > 1:
         import torch
         import torch.distributed as dist
 
-    eng = ps.Engine(local_rank, budget)
-    if world > 1:
+    def world_uid():
         uid = [None]
         if rank == 0:
             buf = (N.C.c_uint8 * 128)()
             N.check(N.lib.sr_nccl_unique_id(N.C.byref(buf)))
             uid[0] = bytes(buf)
         dist.broadcast_object_list(uid, src=0)
-        eng.attach_world(rank, world, uid[0])
-        eng.set_exchange(args.exchange == "peer")
-    # a sharded rank holds only its own pages: build the whole graph in a
-    # scratch context on this GPU, export it, then load the shard
-    W = workload(args, eng if world == 1 else None, device=local_rank)
-    csr, pages, n, m = W["csr"], W["pages"], W["n"], W["m"]
-    if not W["loaded"]:
-        eng.load_csr(csr, with_edges=not W.get("lean"))
-        eng.load_pages(pages)
+        return uid[0]
+
+    need_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
+    need_host = (not a.no_e2e) or need_cpu
+    # the push adjacency: traversals derive it on the device from the resident
+    # pages; PageRank never reads it (out-degrees only)
+    csr_edges = False
+    t0 = time.time()
+    eng = ps.Engine(local_rank, budget)
+    if world > 1:
+        eng.attach_world(rank, world, world_uid())
+        eng.set_exchange(a.exchange == "peer")
+    gen = dict(seed=a.seed, weights=(1, 64, a.seed + 1) if a.weighted else None,
+               symmetrize=a.symmetric, page_vertex_capacity=cap)
+    arena = N.PinnedArena()
+    host = None
+    if world == 1:
+        eng.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=csr_edges, **gen)
+        build_s = time.time() - t0
+        if need_host:  # the reference's run() also needs the push adjacency
+            host = eng.export_graph(arena, csr_edges=need_cpu and not pr)
+    else:
+        # a sharded rank holds only its own pages: the whole graph is built in a
+        # scratch context on this GPU, exported, and the shard loaded
+        with ps.Engine(local_rank) as scratch:
+            scratch.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=csr_edges, **gen)
+            host = scratch.export_graph(arena, csr_edges=False)
+        eng.load_csr(host[0], with_edges=False)
+        eng.load_pages(host[1])
+        build_s = time.time() - t0
+    m = eng.graph_info()["num_edges"]
 
     info = ps.device_info(local_rank)
-    graph_bytes = sum(ps.page_bytes(p, W["weighted"]) for p in pages.pages)
-    flush = graph_bytes < 4 * info["l2_bytes"]  # small inputs: evict L2 before every step
+    gbytes = csc_bytes(a, n, m)
+    flush = gbytes < 4 * info["l2_bytes"]  # small inputs: evict L2 before every step
 
-    def one():
+    def one(want=False):
         if flush:
             eng.flush_l2(4 * info["l2_bytes"])
-        r = eng.run(prog, cfg, want_values=False)
-        return r
+        return eng.run(prog, cfg, want_values=want)
 
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.4)  # nvidia-smi needs a moment before its first sample
-    for _ in range(max(args.warmup, 0)):
+    for _ in range(max(a.warmup, 0)):
         one()
     if world > 1:
         dist.barrier()
     sync()
     dev_s, runs = [], []
-    t0 = time.time()
-    for _ in range(args.steps):
+    t1 = time.time()
+    for _ in range(a.steps):
         r = one()
         dev_s.append(r.metrics.device_seconds)
         runs.append(r)
     sync()
-    wall = time.time() - t0
+    wall = time.time() - t1
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -301,311 +385,291 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_s = float(t.item())
     last = runs[-1].metrics
-    iters = args.pr_iters if algo == 3 else 1
+    iters = a.pr_iters if pr else 1
     value = m * iters / step_s / 1e9
-    gteps_read = last.edges_read / (dev_s[-1]) / 1e9
     launches = sum(r.metrics.kernel_launches for r in runs)
 
-    # parity at full size: device fixpoint law + source value
+    # parity at full size: device fixpoint law + the run's value signature
+    res = one(want=True)
     parity = {}
-    res = None
-    if algo in (0, 2):
-        res = eng.run(prog, cfg)
-        viol = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
-        parity = {"fixpoint_violations": viol, "source_value": int(res.values[0]),
-                  "reached": int((res.values != ps.kUnreached).sum())}
-    elif algo == 1:
-        res = eng.run(prog, cfg)
-        parity = {"fixpoint_violations": eng.verify_fixpoint(ps.AlgoKind.CC, res.values)}
+    if not pr:
+        parity["fixpoint_violations"] = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
+        parity["signature"] = value_signature(algo, res.values)
+        if algo != 1:
+            parity["source_value"] = int(res.values[0])
 
-    # roofline: the dominant kernel (K1 dense pull) timed launch by launch with
-    # CUDA events on the engine stream inside the timed runs.  Algorithmic
-    # bytes per SURVEY §8(d) -- per edge read: in_sources 4 [+ weight 4];
-    # per gathered source value: 4 (destinations/edges that provably cannot
-    # improve are not gathered and not charged); per attempted destination 8 --
-    # over the dense/recovery passes.
+    # roofline of the dominant kernel
     roof = None
-    if not args.budget_gb and algo != 3:
-        per_edge = 8 if algo == 2 else 4
-        k1_bytes = k1_s = 0.0
-        k1_launches = k1_gathers = k1_edges = 0
-        for r in runs:
-            for st in r.metrics.per_pass:
-                if st.kind != ps.PassKind.SPARSE_PUSH:
-                    k1_bytes += per_edge * st.edges_read + 8 * st.attempts
-                    k1_edges += st.edges_read
-            k1_bytes += 4 * r.metrics.gathers
-            k1_gathers += r.metrics.gathers
-            k1_s += r.metrics.relax_seconds
-            k1_launches += r.metrics.relax_launches
-        peak, src_ = measured_peaks()
-        achieved = k1_bytes / k1_s / 1e9
-        ms, edges = eng.bench_pull_sweep(ps.AlgoKind(algo), 20)
-        roof = {"bound": "hbm", "kernel": "pull_relax_kernel (K1), launches inside the timed runs",
-                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "peak_source": src_,
-                "traffic": profile_traffic(f"{args.algo}-s{args.scale}"),
-                "algorithmic_bytes_per_launch": int(k1_bytes / max(k1_launches, 1)),
-                "launch_ms": round(k1_s / max(k1_launches, 1) * 1e3, 4),
-                "launches": k1_launches, "share_of_step": round(k1_s / sum(dev_s), 3),
-                "per_unit": f"{per_edge} B/edge read + 4 B/gathered source + 8 B/attempted destination",
-                "gathered_fraction": round(k1_gathers / max(k1_edges, 1), 4),
-                "isolated_sweep": {"ms": round(ms, 4), "edges": edges,
-                                   "note": "gate-off sweep over the converged values"},
-                "gather_roofline": gather_roofline(k1_gathers / k1_s, info, clocks)}
-    elif args.budget_gb:
+    if a.budget_gb:
         # out-of-core: the host link bounds; streamed bytes per run / run time
         gbps = N.C.c_double()
         N.check(N.lib.sr_bench_h2d(local_rank, 1 << 30, 3, N.C.byref(gbps)))
         streamed = last.bytes_transferred
-        achieved = streamed / step_s / 1e9
-        kern = "pr_pull_kernel (K8)" if algo == 3 else "pull_relax_kernel (K1) + push (K3)"
+        ach = streamed / step_s / 1e9
+        kern = "pr_pull_kernel (K8)" if pr else "pull_relax_kernel (K1) + push (K3)"
         roof = {"bound": "host-link", "kernel": kern + " + H2D page stream",
-                "achieved": round(achieved, 2), "peak": round(gbps.value, 2),
-                "unit": "GB/s", "frac": round(achieved / gbps.value, 4),
-                "peak_source": "measured (sr_bench_h2d, pinned 1 GiB)", "traffic": None,
-                "streamed_bytes_per_run": int(streamed),
-                "per_unit": "page_bytes of every admitted page (graph.cpp:96-100)"}
-    elif algo == 3:
-        iters = args.pr_iters
+                "achieved": round(ach, 2), "peak": round(gbps.value, 2), "unit": "GB/s",
+                "frac": round(ach / gbps.value, 4),
+                "peak_source": "measured (sr_bench_h2d, pinned 1 GiB, this run)",
+                "traffic": None, "streamed_bytes_per_run": int(streamed),
+                "model": "page_bytes of every admitted page (graph.cpp:96-100)"}
+    elif pr:
         alg = (8 * m + 16 * n) * iters
-        peak, src_ = measured_peaks()
-        achieved = alg / step_s / 1e9
-        roof = {"bound": "hbm", "kernel": "pr_pull_kernel (K8), whole run",
-                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "peak_source": src_,
-                "traffic": profile_traffic(f"pagerank-s{args.scale}"),
-                "algorithmic_bytes_per_launch": 8 * m + 16 * n,
-                "per_unit": "8 B/edge + 16 B/destination per iteration",
-                "gather_roofline": gather_roofline(m * iters / step_s, info, clocks)}
+        k8_s = sum(r.metrics.relax_seconds for r in runs) / len(runs)
+        k8_l = sum(r.metrics.relax_launches for r in runs) / len(runs)
+        peak, src = measured_peaks()
+        ach = alg / k8_s / 1e9
+        roof = {"bound": "hbm", "kernel": "pr_pull_kernel (K8), every launch of the timed runs",
+                "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "peak_source": src,
+                "traffic": profile_traffic(f"pagerank-s{a.scale}"),
+                "model": "SURVEY §8(d): 8 B/edge + 16 B/destination per iteration",
+                "algorithmic_bytes_per_launch": int(alg / max(k8_l, 1)),
+                "launch_ms": round(k8_s / max(k8_l, 1) * 1e3, 4), "launches": int(k8_l),
+                "share_of_step": round(k8_s / step_s, 3),
+                "gather_roofline": gather_roofline(m * iters / k8_s, info, clocks)}
+    else:
+        roof = k1_roofline(a, runs, info, clocks, step_s)
+        if roof:
+            ms, edges = eng.bench_pull_sweep(ps.AlgoKind(algo), 10)
+            roof["isolated_sweep"] = {"ms": round(ms, 4), "edges": edges,
+                                      "note": "gate-off K1 sweep over the converged values"}
 
     # the multi-pass subgraph-iteration schedules on the same resident graph
     schedules = {}
-    if algo != 3 and world == 1:
-        for mode in ("reentry", "pipelined"):
-            c2 = ps.EngineConfig(predictor=cfg.predictor, window_capacity=args.window,
+    if not pr and world == 1 and not a.budget_gb:
+        for mode in ("baseline", "reentry", "pipelined"):
+            if mode == a.mode:
+                continue
+            c2 = ps.EngineConfig(predictor=cfg.predictor, window_capacity=a.window,
                                  clock=ps.ClockMode.WALL)
             c2.schedule.kind = ps.ScheduleModeKind(MODES[mode])
             eng.run(prog, c2, want_values=False)
             t = min(eng.run(prog, c2, want_values=False).metrics.device_seconds for _ in range(3))
-            schedules[mode] = {"ms": round(t * 1e3, 3), "gteps": round(m / t / 1e9, 2)}
+            schedules[mode] = {"ms": round(t * 1e3, 3), "gteps": round(m * iters / t / 1e9, 2)}
 
     # e2e: the public C-ABI one-shot call with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not a.no_e2e:
+        # the CSR offsets only: the engine derives the push adjacency from the pages
+        csr = ps.CsrGraph(n, host[0].out_offsets, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+        pages = host[1]
         e2e_eng = ps.Engine(local_rank, budget)
         if world > 1:
-            # every rank makes the same sr_run_graph call on its own context,
-            # attached as a world of its own (shards, exchange as above);
-            # wall time per step = max over ranks, bytes summed over ranks
-            vals = W["arena"].array(n, np.uint32) if algo != 3 else None
-            uid = [None]
-            if rank == 0:
-                buf = (N.C.c_uint8 * 128)()
-                N.check(N.lib.sr_nccl_unique_id(N.C.byref(buf)))
-                uid[0] = bytes(buf)
-            dist.broadcast_object_list(uid, src=0)
-            e2e_eng.attach_world(rank, world, uid[0])
-            e2e_eng.set_exchange(args.exchange == "peer")
-            e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
-            sync()
+            e2e_eng.attach_world(rank, world, world_uid())
+            e2e_eng.set_exchange(a.exchange == "peer")
+        vals = arena.array(n, np.uint32) if not pr else None
+        e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
+        sync()
+        if world > 1:
             dist.barrier()
-            t1 = time.time()
-            reps = max(1, min(args.steps, 5))
-            for _ in range(reps):
-                rr = e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)
-            sync()
-            tt = torch.tensor([(time.time() - t1) / reps, float(rr.metrics.h2d_bytes),
-                               float(n * 4), rr.metrics.upload_seconds],
-                              dtype=torch.float64, device=f"cuda:{local_rank}")
+        reps = max(1, min(a.steps, 5))
+        t2 = time.time()
+        for _ in range(reps):
+            rr = e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)
+        sync()
+        e2e_s = (time.time() - t2) / reps
+        h2d = int(csr.out_offsets.nbytes + sum(p.in_offsets.nbytes + p.in_sources.nbytes +
+                                               p.in_weights.nbytes for p in pages.pages))
+        d2h = n * 4
+        up = rr.metrics.upload_seconds
+        if world > 1:
+            tt = torch.tensor([e2e_s, float(h2d), float(d2h), up], dtype=torch.float64,
+                              device=f"cuda:{local_rank}")
             mx = tt.clone()
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-            e2e_s = float(mx[0].item())
-            e2e = {"value": round(m * iters / e2e_s / 1e9, 4), "unit": "GTEPS",
-                   "seconds_per_step": round(e2e_s, 5),
-                   "h2d_bytes_per_step": int(tt[1].item()),
-                   "d2h_bytes_per_step": int(tt[2].item()),
-                   "upload_seconds": round(float(mx[3].item()), 5),
-                   "call": "sr_run_graph on every rank (pagestream::run drop-in, one "
-                           "shard per GPU), pinned host inputs; max over ranks"}
-        else:
-            vals = W["arena"].array(n, np.uint32) if algo != 3 else None  # pinned result buffer
-            e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
-            sync()
-            t1 = time.time()
-            reps = max(1, min(args.steps, 5))
-            for _ in range(reps):
-                rr = e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)
-            sync()
-            e2e_s = (time.time() - t1) / reps
-            # the engine uploads the CSR offsets and the pages; the push adjacency is
-            # derived on the device from the resident pages (rr.metrics.h2d_bytes)
-            csr_bytes = csr.out_offsets.nbytes
-            page_bytes = sum(p.in_offsets.nbytes + p.in_sources.nbytes + p.in_weights.nbytes
-                             for p in pages.pages)
-            e2e = {"value": round(m * iters / e2e_s / 1e9, 4), "unit": "GTEPS",
-                   "seconds_per_step": round(e2e_s, 5),
-                   "h2d_bytes_per_step": int(csr_bytes + page_bytes),
-                   "d2h_bytes_per_step": int(n * 4),
-                   "upload_seconds": round(rr.metrics.upload_seconds, 5),
-                   "h2d_bytes_measured": int(rr.metrics.h2d_bytes),
-                   "call": "sr_run_graph (pagestream::run drop-in), pinned host inputs"}
+            e2e_s, h2d, d2h, up = float(mx[0]), int(tt[1]), int(tt[2]), float(mx[3])
+        e2e = {"value": round(m * iters / e2e_s / 1e9, 4), "unit": "GTEPS",
+               "seconds_per_step": round(e2e_s, 5), "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "upload_seconds": round(up, 5),
+               "h2d_bytes_measured": int(rr.metrics.h2d_bytes),
+               "call": "sr_run_graph (pagestream::run drop-in), pinned host inputs"
+                       + (", one shard per GPU, max over ranks" if world > 1 else "")}
         e2e_eng.close()
 
-    # CPU baseline: the reference's run() on the same graph, bounded sample
+    # CPU baseline on this box's host cores (rank 0, N=1), same graph
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, W, sample_runs=1,
-                           ours=res.values if res is not None else None)
-        if cpu and "bit_exact_vs_reference_run" in cpu:
-            parity["bit_exact_vs_reference_run"] = cpu.pop("bit_exact_vs_reference_run")
+    instance = {"degree_hash": degree_hash(host[0].out_offsets)} if host else {}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a, host, n, m, res)
+        for k in ("bit_exact_vs_reference_run", "pagerank"):
+            if k in cpu:
+                parity[k] = cpu.pop(k)
 
     ms_per_step = step_s * 1e3
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "u32" if algo != 3 else "f32", "data": "synthetic",
-        "config": {"workload": f"{_config_name(args)}: {args.algo.upper()} RMAT-{args.scale} ef{args.edge_factor}"
-                               f"{' w[1,64]' if W['weighted'] else ''}, {len(pages.pages)} pages,"
-                               f" {args.mode}/{args.predictor}, window {args.window}",
-                   "algo": args.algo, "scale": args.scale, "vertices": n, "edges": m,
-                   "pages": len(pages.pages), "schedule": args.mode,
-                   "predictor": args.predictor, "window": args.window, "source": 0,
-                   "hbm_budget_gb": args.budget_gb or None,
-                   "l2": ("L2 flushed before every step (%d MB memset; CSC %.3f GB)"
-                          % (4 * info["l2_bytes"] >> 20, graph_bytes / 1e9)) if flush else
-                         ("inputs larger than L2 (CSC %.2f GB vs %d MB L2)"
-                          % (graph_bytes / 1e9, info["l2_bytes"] >> 20)),
-                   "graph_build_s": round(W["build_s"], 2), "graph_build": W["graph"],
-                   "parallelism": f"dp{world}" if world > 1 else "single",
-                   **({"exchange": args.exchange} if world > 1 else {})},
+        "vs_baseline": None, "dtype": "f32" if pr else "u32", "data": "synthetic",
+        "config": workload_config(a, n, m),
         "time_to_converge_ms": round(ms_per_step, 4),
-        "gteps_read": round(gteps_read, 4),
+        "gteps_read": round(last.edges_read / dev_s[-1] / 1e9, 4),
         "passes": {"total": last.passes, "dense": last.dense_passes, "sparse": last.sparse_passes,
                    "recovery": last.recovery_passes, "edges_read": last.edges_read},
-        "wall_ms_per_step": round(wall / args.steps * 1e3, 4),
+        "wall_ms_per_step": round(wall / a.steps * 1e3, 4),
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
         "clocks": clocks, "parity": parity, "schedules": schedules,
+        "instance": instance,
+        "build": {"graph_build_s": round(build_s, 2),
+                  "how": "device: sr_generate_graph (mt19937_64 jump-ahead chunks) + stable "
+                         "radix-sort build_csr/build_csc_pages",
+                  "l2_flush_per_step": bool(flush)},
     }
+    if world > 1:
+        out["config"]["exchange"] = a.exchange
     eng.close()
+    arena.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
 
 
-def _config_name(args):
-    if args.algo == "pagerank":
-        return "C3"
-    if args.algo == "cc":
-        return "C4"
-    if args.algo == "bfs":
-        return "C1"
-    return "C5" if args.scale >= 29 else "C2"
-
-
-def cpu_baseline(args, W, sample_runs=1, ours=None):
-    """The reference run() (oracle/_ref) on this box's host cores, same graph and config.
-    Falls back to the oracle port (Dijkstra/BFS/CC restatement) if _ref was not built.
-    With `ours` (our values on the same graph) it also reports whether the
-    reference's values are bit-identical at full size."""
+def cpu_baseline(a, host, n, m, res):
+    """The reference's run() (oracle/_ref) on this box's host cores, same graph and
+    config, one full run (bounded sample); reports whether its values are
+    bit-identical to ours.  PageRank: the OpenMP fp64 oracle (the reference has
+    none) -- timed as the baseline and used as the checker of our ranks."""
     from oracle import oracle as O
-    cores = args.cpu_threads or os.cpu_count() or 1
-    csr, pages = W["csr"], W["pages"]
-    algo = ALGOS[args.algo]
-    ref = O.load_reference()
-    if ref is not None and algo != 3:
-        g = O.RefGraph(ref, W["n"], csr.out_offsets, csr.out_neighbors,
-                       csr.out_weights if W["weighted"] else None, W["in_off"], W["in_src"],
-                       W["in_w"], W["cap"])
-        secs, mets, vals = [], None, None
-        for _ in range(sample_runs):
-            vals, mets = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
-                               args.window, cores, 1, 0, 0.05, want_values=ours is not None)
-            secs.append(mets["wall_seconds"])
-        g.close()
-        t = min(secs)
-        extra = {}
-        if ours is not None and vals is not None:
-            extra["bit_exact_vs_reference_run"] = bool(np.array_equal(np.asarray(vals), ours))
-        return {**extra, "value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
-                "kind": "reference", "seconds": round(t, 3),
-                "sample": f"{sample_runs} full reference run() of the same workload "
-                          f"(ClockMode::Wall, {cores} OpenMP workers)",
-                "edges_read": mets["edges_read"], "passes": mets["passes"]}
-    # port: the oracle's sequential solver on the same CSR
-    t0 = time.time()
+    cores = a.cpu_threads or os.cpu_count() or 1
+    csr, pages, in_off, in_src, in_w = host
+    algo = ALGOS[a.algo]
     if algo == 3:
+        t = time.time()
+        want = O.pagerank_par(n, in_off, in_src, csr.out_offsets, a.pr_iters, 0.85, cores)
+        t = time.time() - t
+        mx, mr, l1 = O.pr_compare(res.ranks, want, 1e-12, cores)
+        return {"value": round(m * a.pr_iters / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
+                "kind": "port", "seconds": round(t, 3),
+                "sample": f"1 full fp64 PageRank ({a.pr_iters} iterations) by the OpenMP "
+                          "oracle (oracle_pagerank_par) on the same graph",
+                "pagerank": {"max_abs": mx, "max_rel": mr, "l1_sum": l1,
+                             "rel_floor": 1e-12, "checker": "oracle_pagerank_par (fp64)"}}
+    ref = O.load_reference()
+    if ref is None:
         return None
-    O.solve_csr(algo, W["n"], csr.out_offsets, csr.out_neighbors,
-                csr.out_weights if W["weighted"] else None, 0)
-    t = time.time() - t0
-    return {"value": round(W["m"] / t / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "port",
-            "seconds": round(t, 3), "sample": "oracle sequential solver, full graph"}
+    # the push adjacency exported from the device (derived from the pages: the
+    # order within a source may differ from build_csr's, which run()'s values
+    # do not depend on)
+    g = O.RefGraph(ref, n, csr.out_offsets, csr.out_neighbors,
+                   csr.out_weights if a.weighted else None, in_off, in_src,
+                   in_w if a.weighted else None, (n + a.pages - 1) // a.pages)
+    vals, mets = g.run(algo, 0, PREDS[a.predictor], MODES[a.mode], a.mrt, 3, a.window, cores,
+                       1, 0, 0.05, want_values=True)
+    g.close()
+    t = mets["wall_seconds"]
+    return {"bit_exact_vs_reference_run": bool(np.array_equal(vals, res.values)),
+            "value": round(m / t / 1e9, 5), "unit": "GTEPS", "cores": cores, "kind": "reference",
+            "seconds": round(t, 3),
+            "sample": f"1 full reference run() of the same workload (ClockMode::Wall, "
+                      f"{cores} OpenMP workers)",
+            "edges_read": mets["edges_read"], "passes": mets["passes"]}
 
 
-def run_reference(args, rank):
+# ---------------------------------------------------------------------------
+# reference arm: oracle-built graph (no libseraph, no GPU), the reference's run()
+# ---------------------------------------------------------------------------
+def ref_workload(a, cores):
+    from oracle import oracle as O
+    quad = UNIFORM if a.uniform else RMAT
+    n = 1 << a.scale
+    src, dst = O.generate_rmat_par(a.scale, a.edge_factor, *quad, seed=a.seed, threads=cores)
+    w = O.assign_weights_par(src.size, a.seed + 1, 1, 64, cores) if a.weighted else None
+    if a.symmetric:
+        src, dst, w = O.symmetrize_par(src, dst, w, cores)
+    out_off, out_nbr, out_w = O.build_adjacency_par(n, src, dst, w, cores)
+    in_off, in_src, in_w = O.build_adjacency_par(n, dst, src, w, cores)
+    return n, int(src.size), (out_off, out_nbr, out_w, in_off, in_src, in_w)
+
+
+def run_reference(a, rank):
     if rank != 0:
         return
-    W = workload(args)
     from oracle import oracle as O
+    cores = a.cpu_threads or os.cpu_count() or 1
+    algo = ALGOS[a.algo]
+    t0 = time.time()
+    n, m, (out_off, out_nbr, out_w, in_off, in_src, in_w) = ref_workload(a, cores)
+    build_s = time.time() - t0
+    iters = a.pr_iters if algo == 3 else 1
     ref = O.load_reference()
-    algo = ALGOS[args.algo]
-    cores = args.cpu_threads or os.cpu_count() or 1
-    if ref is None or algo == 3:
-        why = "oracle/_ref not built" if ref is None else "reference has no PageRank"
-        print(json.dumps({"impl": "reference", "unavailable": why}))
-        return
-    csr, pages = W["csr"], W["pages"]
-    g = O.RefGraph(ref, W["n"], csr.out_offsets, csr.out_neighbors,
-                   csr.out_weights if W["weighted"] else None, W["in_off"], W["in_src"],
-                   W["in_w"], W["cap"])
+    if algo == 3:
+        kind, what = "port", ("the OpenMP fp64 PageRank oracle (oracle_pagerank_par): the "
+                              "reference has no PageRank (SPEC.md:8)")
+        del out_nbr, out_w
 
-    def one():
-        _, met = g.run(algo, 0, PREDS[args.predictor], MODES[args.mode], args.mrt, 3,
-                       args.window, cores, 1, 0, 0.05)
-        return met
+        def one(want=False):
+            t = time.time()
+            r = O.pagerank_par(n, in_off, in_src, out_off, a.pr_iters, 0.85, cores)
+            return time.time() - t, None, r
+    else:
+        if ref is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        kind, what = "reference", "the reference's run() (oracle/_ref, ClockMode::Wall)"
+        g = O.RefGraph(ref, n, out_off, out_nbr, out_w, in_off, in_src, in_w,
+                       (n + a.pages - 1) // a.pages)
+        del out_nbr, out_w, in_src, in_w
 
-    for _ in range(max(args.warmup, 0)):
+        def one(want=False):
+            vals, met = g.run(algo, 0, PREDS[a.predictor], MODES[a.mode], a.mrt, 3, a.window,
+                              cores, 1, 0, 0.05, want_values=want)
+            return met["wall_seconds"], met, vals
+
+    # the reference's CPU run() has nothing to warm beyond first-touch page
+    # faults: at most one untimed run keeps the arm within a few minutes
+    warm = min(max(a.warmup, 0), 1)
+    for _ in range(warm):
         one()
-    secs, met = [], None
-    for _ in range(args.steps):
-        met = one()
-        secs.append(met["wall_seconds"])
-    g.close()
+    secs, met, vals = [], None, None
+    for i in range(a.steps):
+        s, met, vals = one(want=i == a.steps - 1)
+        secs.append(s)
     t = sum(secs) / len(secs)
-    value = W["m"] / t / 1e9
-    print(json.dumps({
+    value = m * iters / t / 1e9
+    parity = {}
+    if algo != 3 and vals is not None:
+        parity["signature"] = value_signature(algo, vals)
+        if algo != 1:
+            parity["source_value"] = int(vals[0])
+    out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "GTEPS",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "warmup_runs_done": warm,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"C2: {args.algo.upper()} RMAT-{args.scale}, {len(pages.pages)} pages,"
-                               f" {args.mode}/{args.predictor}, window {args.window}",
-                   "algo": args.algo, "scale": args.scale, "edges": W["m"]},
-        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores,
-                         "kind": "reference",
-                         "sample": "full reference run() per step (ClockMode::Wall)"},
+        "vs_baseline": None, "dtype": "f64" if algo == 3 else "u32", "data": "synthetic",
+        "config": workload_config(a, n, m),
+        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores, "kind": kind,
+                         "sample": f"one full run per step: {what}, {cores} threads"},
         "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "passes": met["passes"], "edges_read": met["edges_read"],
-    }), flush=True)
+        "parity": parity, "instance": {"degree_hash": degree_hash(out_off)},
+        "build": {"graph_build_s": round(build_s, 2),
+                  "how": "oracle (OpenMP): generate_rmat/assign_weights jump-ahead chunks, "
+                         "symmetrize, stable counting-sort build_csr/build_csc"},
+    }
+    if met is not None:
+        out["passes"] = met["passes"]
+        out["edges_read"] = met["edges_read"]
+    if algo != 3:
+        g.close()
+    print(json.dumps(out), flush=True)
 
 
 def main():
-    args = parse()
+    a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank)
+    a.gpus = max(a.gpus, world)
+    if a.impl == "reference":
+        run_reference(a, rank)
         return
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    run_ours(args, rank, world, local_rank)
+    run_ours(a, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -317,6 +317,29 @@ def test_pagerank_rmat_vs_oracle(engine, scale):
 # --------------------------------------------------------------------------
 # bigger graphs: hub chunks, many tiles, sparse/dense switching
 # --------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["resident", "blocked", "streamed"])
+def test_pagerank_rmat18_relative(case, monkeypatch):
+    """PageRank at RMAT-18 (4.2 M edges) against the fp64 OpenMP oracle with a
+    RELATIVE bound (mean rank 2^-18: an absolute 1e-6 would be vacuous):
+    max |d|/rank <= 1e-5 over ranks > 1e-12, sum |d| <= 1e-6, max |d| <= 1e-6
+    (north_star's per-vertex bound).  Resident, source-blocked (K8 partial
+    sums) and streamed through a 16 MB budget."""
+    n = 1 << 18
+    if case == "blocked":
+        monkeypatch.setenv("SERAPH_PR_BLOCK_VERTS", str(n // 4))
+    budget = (16 << 20) if case == "streamed" else 0
+    cfg = cfg_of(clock=ps.ClockMode.WALL)
+    with ps.Engine(0, budget) as eng:
+        eng.generate_graph(18, 16, seed=0, page_vertex_capacity=n // 64, csr_edges=False)
+        csr, _, in_off, in_src, _ = eng.export_graph(csr_edges=False)
+        r = eng.run(ps.make_pagerank(), cfg)
+        if case == "streamed":
+            assert r.metrics.bytes_transferred > 0
+    want = O.pagerank_par(n, in_off, in_src, csr.out_offsets, 20, 0.85)
+    mx, mr, l1 = O.pr_compare(r.ranks, want, 1e-12)
+    assert mx <= 1e-6 and mr <= 1e-5 and l1 <= 1e-6, (mx, mr, l1)
+
+
 @pytest.mark.parametrize("scale", [14, 16])
 def test_rmat_large_parity(engine, scale):
     n = 1 << scale
@@ -796,10 +819,11 @@ def test_sssp_zero_weight_pages(engine):
             r = engine.run_graph(csr, pages, ps.make_sssp(0, n, True),
                                  cfg_of(pred=pred, execution=pol, clock=ps.ClockMode.WALL))
             assert np.array_equal(r.values, want), (pol, pred)
-    with ps.Engine(0, hbm_budget_bytes=64 << 10) as small:
+    with ps.Engine(0, hbm_budget_bytes=128 << 10) as small:  # pages stream (250 KB CSC)
         r = small.run_graph(csr, pages, ps.make_sssp(0, n, True),
-                            cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE,
+                            cfg_of(execution=ps.ExecutionPolicy.FORCE_DENSE, window=2,
                                    clock=ps.ClockMode.WALL))
+        assert r.metrics.bytes_transferred > 0
         assert np.array_equal(r.values, want)
 
 
