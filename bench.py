@@ -486,6 +486,30 @@ def run_ours(a, rank, world, local_rank):
                "h2d_bytes_measured": int(rr.metrics.h2d_bytes),
                "call": "sr_run_graph (pagestream::run drop-in), pinned host inputs"
                        + (", one shard per GPU, max over ranks" if world > 1 else "")}
+        if world == 1:
+            # the C++ drop-in's callers pass std::vector (pageable) arrays: same
+            # call from pageable copies (the engine stages them through pinned
+            # chunks on several host threads, csrc/stager.cpp)
+            csr_p = ps.CsrGraph(n, np.array(csr.out_offsets), csr.out_neighbors,
+                                csr.out_weights)
+            pages_p = ps.PageSet(pages.num_vertices, pages.page_vertex_capacity, pages.weighted,
+                                 [ps.CscPage(p.vertex_begin, p.vertex_end, np.array(p.in_offsets),
+                                             np.array(p.in_sources), np.array(p.in_weights))
+                                  for p in pages.pages])
+            vals_p = np.empty(n, np.uint32) if not pr else None
+            e2e_eng.run_graph(csr_p, pages_p, prog, cfg, values_out=vals_p)  # warm-up
+            sync()
+            t3 = time.time()
+            for _ in range(reps):
+                rp = e2e_eng.run_graph(csr_p, pages_p, prog, cfg, values_out=vals_p)
+            sync()
+            pg_s = (time.time() - t3) / reps
+            e2e["pageable"] = {"value": round(m * iters / pg_s / 1e9, 4),
+                               "seconds_per_step": round(pg_s, 5),
+                               "upload_seconds": round(rp.metrics.upload_seconds, 5),
+                               "call": "sr_run_graph from pageable host arrays (what the C++ "
+                                       "drop-in pagestream::seraph::run passes)"}
+            del csr_p, pages_p
         e2e_eng.close()
 
     # CPU baseline on this box's host cores (rank 0, N=1), same graph

@@ -265,7 +265,9 @@ typedef struct {
   int32_t has_csr_edges; /* push adjacency on the device */
   int32_t csr_weighted;
   int32_t csr_derived;   /* adjacency derived from the pages (order within a source arbitrary) */
-  int32_t pad_;
+  /* the push adjacency lives in pinned host memory, read zero-copy by the
+   * sparse passes: pages + adjacency exceed the context's hbm budget */
+  int32_t adjacency_on_host;
 } sr_graph_info;
 
 /* Edge list in host or device memory (src/dst/w: num_edges entries, w NULL

@@ -199,7 +199,7 @@ class GraphInfo(C.Structure):
         ("has_csr_edges", C.c_int32),
         ("csr_weighted", C.c_int32),
         ("csr_derived", C.c_int32),
-        ("pad_", C.c_int32),
+        ("adjacency_on_host", C.c_int32),
     ]
 
 

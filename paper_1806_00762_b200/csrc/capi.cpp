@@ -234,7 +234,13 @@ int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const
     for (uint32_t i = 0; i < np; ++i)
       page_bytes += (uint64_t(pages[i].vertex_end - pages[i].vertex_begin) + 1 +
                      pages[i].edge_count * (weighted ? 2 : 1)) * 4;
-    const bool derive = ctx->eng->world() == 1 && ctx->eng->fits_budget(page_bytes);
+    // A forced budget covers pages + adjacency: derive on the device only when
+    // both fit, else hand the adjacency over (load_pages keeps it in pinned
+    // host memory when it does not fit).  PageRank needs only the offsets.
+    const uint64_t adj_bytes = m * 4 * (w ? 2 : 1);
+    const bool pagerank = cfg->algo == SR_ALGO_PAGERANK;
+    const bool derive = pagerank ||
+                        (ctx->eng->world() == 1 && ctx->eng->fits_budget(page_bytes + adj_bytes));
     // the offsets DMA stays queued ahead of the page DMAs on the copy stream
     // (load_pages synchronises it before the host buffers are released)
     ctx->eng->load_csr(n, m, off, derive ? nullptr : nbr, derive ? nullptr : w, /*sync=*/false);

@@ -22,6 +22,16 @@ constexpr uint32_t kTileEdgeBudget = 1024;
 constexpr uint32_t kHubChunk = 1024;      // edges per hub chunk tile
 constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id
 constexpr int kMaxSegments = 8;           // tile ranges per launch
+// K8 hot-source staging (pr_pull_kernel<true, kHotWarps>): blocks of
+// kHotWarps warps (1.5 KB of tile scratch each) + a shared-memory table of
+// f32 contributions of the hottest sources, encoded kHotBit | slot.  Measured
+// on RMAT-26 (tools/c3ab.sh): 8 warps x 2048 entries (5 blocks/SM, L1 keeps
+// ~128 KB) is best, -4.5 %; bigger tables cost L1 capacity and occupancy
+// (16 K entries: +28 %, 64 K: +250 %).
+constexpr int kHotWarps = 8;
+constexpr uint32_t kHotDefault = 2048;
+constexpr uint32_t kHotSmemBytes = 232448;  // 227 KB opt-in per CTA
+constexpr uint32_t kHotBit = 0x80000000u;
 
 // Tile (uint4): x = edge_lo, y = edge_hi (page-local edge indices),
 // z = dest_lo (page-local), w = dest_hi (exclusive) or kHubFlag|hub_id.
@@ -112,6 +122,8 @@ struct PrArgs {
   RunCtr* ctr;
   float base;   // (1-d)/N
   float damp;   // d
+  const float* hot_contrib;  // hot-source contributions (null: no staging)
+  uint32_t n_hot;
 };
 
 struct PushArgs {

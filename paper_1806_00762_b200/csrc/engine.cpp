@@ -137,17 +137,42 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   n_ = n;
   m_ = m;
   out_off_.reserve(size_t(n) + 1);
-  SR_CUDA(cudaMemcpyAsync(out_off_.p, off, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice, xs_));
+  stager_.h2d(out_off_.p, off, (size_t(n) + 1) * 8, xs_);
   uint64_t bytes = (uint64_t(n) + 1) * 8;
   has_csr_edges_ = nbr != nullptr;
   csr_weighted_ = false;
-  if (nbr && m) {
+  adj_host_ = false;
+  if (nbr && m && budget_ != 0) {
+    // forced budget: stage the adjacency in pinned host memory; load_pages
+    // decides where it lives (place_adjacency)
+    out_nbr_.release();
+    out_w_.release();
+    host_nbr_.reserve(m);
+    if (w) host_w_.reserve(m);
+    auto on_dev = [](const void* p) {
+      cudaPointerAttributes at{};
+      return cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+    };
+    if (on_dev(nbr) || (w && on_dev(w))) {
+      SR_CUDA(cudaMemcpy(host_nbr_.p, nbr, m * 4, cudaMemcpyDefault));
+      if (w) SR_CUDA(cudaMemcpy(host_w_.p, w, m * 4, cudaMemcpyDefault));
+    } else {
+      const uint64_t chunk = 16ull << 20;
+      parallel_for((m + chunk - 1) / chunk, [&](size_t k) {
+        const uint64_t a = k * chunk, b = std::min(m, a + chunk);
+        std::memcpy(host_nbr_.p + a, nbr + a, (b - a) * 4);
+        if (w) std::memcpy(host_w_.p + a, w + a, (b - a) * 4);
+      });
+    }
+    adj_host_ = true;
+    csr_weighted_ = w != nullptr;
+  } else if (nbr && m) {
     out_nbr_.reserve(m);
-    SR_CUDA(cudaMemcpyAsync(out_nbr_.p, nbr, m * 4, cudaMemcpyDefault, xs_));
+    stager_.h2d(out_nbr_.p, nbr, m * 4, xs_);
     bytes += m * 4;
     if (w) {
       out_w_.reserve(m);
-      SR_CUDA(cudaMemcpyAsync(out_w_.p, w, m * 4, cudaMemcpyDefault, xs_));
+      stager_.h2d(out_w_.p, w, m * 4, xs_);
       bytes += m * 4;
       csr_weighted_ = true;
     }
@@ -193,12 +218,49 @@ void Engine::derive_csr_now() {
   maybe_derive_csr();
 }
 
+void Engine::place_adjacency(uint64_t used, PassOut* po) {
+  if (budget_ == 0) {
+    page_budget_ = 0;
+    return;
+  }
+  const uint64_t ab = has_csr_edges_ && !csr_derived_ ? m_ * 4 * (csr_weighted_ ? 2 : 1) : 0;
+  const bool fit = used + ab <= budget_;
+  if (ab && fit && adj_host_) {  // both fit: the adjacency goes to HBM
+    out_nbr_.reserve(m_);
+    SR_CUDA(cudaMemcpyAsync(out_nbr_.p, host_nbr_.p, m_ * 4, cudaMemcpyHostToDevice, xs_));
+    if (csr_weighted_) {
+      out_w_.reserve(m_);
+      SR_CUDA(cudaMemcpyAsync(out_w_.p, host_w_.p, m_ * 4, cudaMemcpyHostToDevice, xs_));
+    }
+    SR_CUDA(cudaStreamSynchronize(xs_));
+    last_upload_bytes += ab;
+    adj_host_ = false;
+    host_nbr_.release();
+    host_w_.release();
+  } else if (ab && !fit && !adj_host_) {  // device-built graph: move the adjacency out
+    SR_CUDA(cudaDeviceSynchronize());
+    host_nbr_.reserve(m_);
+    SR_CUDA(cudaMemcpy(host_nbr_.p, out_nbr_.p, m_ * 4, cudaMemcpyDeviceToHost));
+    if (csr_weighted_) {
+      host_w_.reserve(m_);
+      SR_CUDA(cudaMemcpy(host_w_.p, out_w_.p, m_ * 4, cudaMemcpyDeviceToHost));
+    }
+    out_nbr_.release();
+    out_w_.release();
+    adj_host_ = true;
+  }
+  (void)po;
+  page_budget_ = budget_ - (ab && !adj_host_ ? ab : 0);
+}
+
 void Engine::maybe_derive_csr() {
   // sr_load_csr without out_neighbors + a resident page set: build the push
-  // adjacency on the device instead of shipping it over the host link.
+  // adjacency on the device instead of shipping it over the host link
+  // (only when pages + adjacency fit a forced budget).
   if (csr_deferred_ || !has_csr_ || has_csr_edges_ || !pages_loaded_ || !all_resident_ ||
       world_ > 1)
     return;
+  if (budget_ != 0 && page_bytes_total_ + m_ * 4 * (weighted_ ? 2 : 1) > budget_) return;
   if (n_ != page_n_ || m_ != page_edges_total_) return;
   if (m_ == 0) {
     has_csr_edges_ = true;
@@ -367,11 +429,13 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     used[p] = pages_[p].vb < own_hi_ && pages_[p].ve > own_lo_;
     if (used[p]) used_bytes += pages_[p].bytes;
   }
-  all_resident_ = budget_ == 0 || used_bytes <= budget_;
+  place_adjacency(used_bytes, nullptr);
+  all_resident_ = budget_ == 0 || used_bytes <= page_budget_;
   ring_reset();
   plan_window_ = 0;
   plan_cached_ = size_t(-1);
   sb_.built = false;
+  pr_hot_.built = false;
   page_desc_h_.assign(np, PageDesc{});
   for (uint32_t p = 0; p < np; ++p) {
     page_desc_h_[p].vertex_begin = pages_[p].vb;
@@ -410,14 +474,11 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     auto copy_page = [&](uint32_t p) {
       PageMeta& pm = pages_[p];
       const PageDesc& d = page_desc_h_[p];
-      SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.offs), pm.h_offs, (size_t(d.range) + 1) * 4,
-                              cudaMemcpyHostToDevice, xs_));
-      if (pm.edges) {  // host (pinned/pageable) or device (sr_build_graph) sources
-        SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.src), pm.h_src, pm.edges * 4,
-                                cudaMemcpyDefault, xs_));
-        if (weighted)
-          SR_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(d.w), pm.h_w, pm.edges * 4,
-                                  cudaMemcpyDefault, xs_));
+      // host (pinned/pageable: stager) or device (sr_build_graph) sources
+      stager_.h2d(const_cast<uint32_t*>(d.offs), pm.h_offs, (size_t(d.range) + 1) * 4, xs_);
+      if (pm.edges) {
+        stager_.h2d(const_cast<uint32_t*>(d.src), pm.h_src, pm.edges * 4, xs_);
+        if (weighted) stager_.h2d(const_cast<uint32_t*>(d.w), pm.h_w, pm.edges * 4, xs_);
       }
       SR_CUDA(cudaEventRecord(page_events_[p], xs_));
       pm.on_device = true;
@@ -443,7 +504,8 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       csr_derived_ = false;
     }
     bool derive = has_csr_ && !has_csr_edges_ && world_ == 1 && n_ == n &&
-                  m_ == page_edges_total_;
+                  m_ == page_edges_total_ && algo_hint != SR_ALGO_PAGERANK &&
+                  (budget_ == 0 || used_bytes + m_ * 4 * (weighted ? 2 : 1) <= budget_);
     csr_deferred_ = false;
     runs_since_pages_ = 0;
     if (derive && defer_csr(m_, algo_hint)) {  // derived on demand (derive_csr_now)
@@ -711,6 +773,14 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       a.tiles = tiles_.p;
       a.tile_page = tile_page_.p;
       a.pages = page_desc_.p;
+      if (pr_hot_.built && !pr_hot_.blocked) {
+        a.pages = pr_hot_.desc.p;
+        a.hot_contrib = pr_hot_.hot_contrib.p;
+        a.n_hot = pr_hot_.n_hot;
+        grid = std::max(1, int(std::min<uint64_t>(
+                               uint64_t(sm_count_) * pr_hot_.blocks_per_sm,
+                               (uint64_t(tasks) + pr_hot_warps() - 1) / pr_hot_warps())));
+      }
       a.seg = seg;
       a.contrib_in = contrib_a_.p;
       a.rank_out = rank_b_.p;
@@ -1142,8 +1212,8 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
     a.chunk_shift = shift;
     a.total_edges = total;
     a.out_offsets = out_off_.p;
-    a.out_neighbors = out_nbr_.p;
-    a.out_weights = csr_weighted_ ? out_w_.p : nullptr;
+    a.out_neighbors = nbr_ptr();
+    a.out_weights = w_ptr();
     a.values = values_.p;
     a.next = det_ ? next_.p : values_.p;
     a.changed = changed_.p;
@@ -1408,8 +1478,8 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     TailArgs t{};
     t.values = values_.p;
     t.out_offsets = out_off_.p;
-    t.out_neighbors = out_nbr_.p;
-    t.out_weights = csr_weighted_ ? out_w_.p : nullptr;
+    t.out_neighbors = nbr_ptr();
+    t.out_weights = w_ptr();
     t.outdeg = outdeg_.p;
     t.stamp = stamp_.p;
     t.epoch0 = fq_epoch_ + 1;
@@ -1610,7 +1680,7 @@ uint64_t Engine::verify_fixpoint(int algo, const uint32_t* values_host) {
     throw EngineError(SR_E_DATA, "verify: no values from a previous run");
   }
   SR_CUDA(cudaMemsetAsync(viol.p, 0, 8, cs_));
-  launch_verify(algo, n_, out_off_.p, out_nbr_.p, csr_weighted_ ? out_w_.p : nullptr, values_.p,
+  launch_verify(algo, n_, out_off_.p, nbr_ptr(), w_ptr(), values_.p,
                 viol.p, cs_);
   unsigned long long h = 0;
   SR_CUDA(cudaMemcpyAsync(&h, viol.p, 8, cudaMemcpyDeviceToHost, cs_));

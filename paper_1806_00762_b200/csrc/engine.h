@@ -16,6 +16,7 @@
 #include "device_types.h"
 #include "errors.h"
 #include "seraph.h"
+#include "stager.h"
 #include "vsched.h"
 
 namespace seraph {
@@ -136,6 +137,9 @@ class Engine {
   uint64_t page_bytes_total() const { return page_bytes_total_; }
   // True when a page set of `bytes` would be held resident (no streaming).
   bool fits_budget(uint64_t bytes) const { return budget_ == 0 || bytes <= budget_; }
+  // the push adjacency lives in pinned host memory (read zero-copy by the
+  // sparse passes) because pages + adjacency exceed the HBM budget
+  bool adjacency_on_host() const { return adj_host_; }
   int world() const { return world_; }
   void run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_out, sr_metrics& m,
            std::vector<sr_pass_stats>& passes);
@@ -234,6 +238,20 @@ class Engine {
   void build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<uint32_t>& dst,
                        DBuf<uint32_t>& w, bool weighted, uint32_t cap, bool csr_edges);
   bool csr_derived_ = false;
+  // Forced HBM budget = CSC pages + push adjacency.  The adjacency is staged
+  // in pinned host memory at load_csr and placed by load_pages once the page
+  // bytes are known: on the device when pages + adjacency fit, else it stays
+  // on the host and the sparse passes (K3 push, tail loop) read the
+  // frontier's rows zero-copy over the host link -- the pages keep the HBM.
+  PinBuf<uint32_t> host_nbr_, host_w_;
+  HostStager stager_;  // pageable host -> device uploads through pinned chunks
+  bool adj_host_ = false;
+  uint64_t page_budget_ = 0;  // HBM left for pages (budget_ - device adjacency)
+  void place_adjacency(uint64_t used_page_bytes, PassOut* po);
+  const uint32_t* nbr_ptr() const { return adj_host_ ? host_nbr_.p : out_nbr_.p; }
+  const uint32_t* w_ptr() const {
+    return csr_weighted_ ? (adj_host_ ? host_w_.p : out_w_.p) : nullptr;
+  }
 
   // pages
   bool pages_loaded_ = false;
@@ -348,6 +366,22 @@ class Engine {
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
   } sb_;
   bool build_src_blocks(uint64_t blk_verts);
+  // K8 hot-source staging (pr_pull_kernel<true>): the highest out-degree
+  // sources' contributions live in shared memory; K8 reads an encoded copy
+  // of its source array (hot sources -> kHotBit | slot) through its own page
+  // descriptors.  Built once per page set / source-block layout.
+  struct PrHot {
+    bool built = false;
+    bool blocked = false;
+    const uint32_t* key = nullptr;  // source array the encoding was made from
+    uint32_t n_hot = 0;
+    int blocks_per_sm = 1;
+    DBuf<uint32_t> enc, hot_vertex, slot_of;
+    DBuf<float> hot_contrib;
+    DBuf<PageDesc> desc;
+    DBuf<unsigned long long> cnt;
+  } pr_hot_;
+  bool prepare_pr_hot(bool blocked);
   uint64_t pull_block_verts();
   double hot_source_coverage(uint64_t k);
   double coverage_ = -1;

@@ -23,6 +23,7 @@ bool Engine::build_src_blocks(uint64_t blk) {
   if (!all_resident_) return false;  // sharded ranks block their own destinations
   if (blk == 0 || n_ <= blk) return false;
   sb_.built = false;
+  if (pr_hot_.blocked) pr_hot_.built = false;
   const uint32_t np = uint32_t(pages_.size());
   for (uint32_t p = 0; p < np; ++p)
     if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
@@ -309,8 +310,15 @@ void Engine::pr_blocked_pass(float base, float damp) {
     a.ctr = nullptr;
     a.base = base;
     a.damp = damp;
-    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
-                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                      (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    if (pr_hot_.built && pr_hot_.blocked) {
+      a.pages = pr_hot_.desc.p;
+      a.hot_contrib = pr_hot_.hot_contrib.p;
+      a.n_hot = pr_hot_.n_hot;
+      grid = int(std::min<uint64_t>(uint64_t(sm_count_) * pr_hot_.blocks_per_sm,
+                                    (uint64_t(t1 - t0) + pr_hot_warps() - 1) / pr_hot_warps()));
+    }
     std::pair<cudaEvent_t, cudaEvent_t>* evp = nullptr;
     if (profile_kernels_) {
       if (relax_ev_used_ == relax_ev_.size()) {
@@ -331,6 +339,83 @@ void Engine::pr_blocked_pass(float base, float damp) {
 }
 
 // ---------------------------------------------------------------------------
+// K8 hot-source staging.  Hot set = every vertex whose out-degree is at least
+// the smallest threshold D that admits <= H of them (H = kHotDefault, or
+// SERAPH_PR_HOT entries up to what the block shape holds; default on when
+// |V| > 1 Mi, i.e. when the contribution array outgrows what the L1s serve).
+// The encoded source copy costs 4 B/edge of HBM; without room for it K8 runs
+// unstaged.
+// ---------------------------------------------------------------------------
+bool Engine::prepare_pr_hot(bool blocked) {
+  uint64_t cap = n_ > (1u << 20) ? kHotDefault : 0;
+  if (const char* e = std::getenv("SERAPH_PR_HOT")) cap = std::strtoull(e, nullptr, 10);
+  cap = std::min<uint64_t>(cap, pr_hot_table_max());
+  if (cap == 0 || !all_resident_ || !has_csr_ || n_ == 0) return false;
+  const uint32_t* key = blocked ? sb_.src.p : arena_src_.p;
+  const uint64_t words = blocked ? sb_.src.n : arena_src_.n;
+  if (pr_hot_.built && pr_hot_.blocked == blocked && pr_hot_.key == key) return true;
+  pr_hot_.built = false;
+  size_t free_b = 0, total_b = 0;
+  SR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t need = (words + 4) * 4 + uint64_t(n_) * 4 + (256ull << 20);
+  if (pr_hot_.enc.n < words + 4 && free_b + pr_hot_.enc.n * 4 < need) return false;
+  // 1) threshold: smallest D >= 1 with |{v : deg(v) >= D}| <= cap
+  pr_hot_.cnt.reserve(1);
+  auto count_ge = [&](uint32_t d) {
+    SR_CUDA(cudaMemsetAsync(pr_hot_.cnt.p, 0, 8, cs_));
+    launch_count_deg_ge(outdeg_.p, n_, d, pr_hot_.cnt.p, cs_);
+    unsigned long long k = 0;
+    SR_CUDA(cudaMemcpyAsync(&k, pr_hot_.cnt.p, 8, cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+    return uint64_t(k);
+  };
+  uint32_t lo = 1, hi = 0xffffffffu;  // count_ge(hi) == 0 <= cap
+  if (count_ge(1) <= cap) hi = 1;
+  while (lo < hi) {  // invariant: count_ge(hi) <= cap, and count_ge(d) > cap for d < lo
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (count_ge(mid) <= cap) hi = mid;
+    else lo = mid + 1;
+  }
+  const uint32_t d = hi;
+  // 2) slots
+  pr_hot_.slot_of.reserve(n_);
+  pr_hot_.hot_vertex.reserve(cap);
+  pr_hot_.hot_contrib.reserve((cap + 3) & ~uint64_t(3));
+  SR_CUDA(cudaMemsetAsync(pr_hot_.cnt.p, 0, 8, cs_));
+  launch_hot_assign(outdeg_.p, n_, d, uint32_t(cap), reinterpret_cast<unsigned*>(pr_hot_.cnt.p),
+                    pr_hot_.slot_of.p, pr_hot_.hot_vertex.p, cs_);
+  unsigned long long nh = 0;
+  SR_CUDA(cudaMemcpyAsync(&nh, pr_hot_.cnt.p, 8, cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  pr_hot_.n_hot = uint32_t(std::min<unsigned long long>(nh, cap));
+  if (pr_hot_.n_hot == 0) return false;
+  pr_hot_.blocks_per_sm = pr_hot_blocks_per_sm(pr_hot_.n_hot);
+  // 3) encoded source copy + descriptors pointing into it
+  pr_hot_.enc.reserve(words + 4);
+  launch_hot_encode(key, pr_hot_.enc.p, words & ~uint64_t(3), pr_hot_.slot_of.p, n_, cs_);
+  std::vector<PageDesc> desc;
+  if (blocked) {
+    desc.resize(size_t(sb_.n_blocks) * pages_.size());
+    SR_CUDA(cudaMemcpyAsync(desc.data(), sb_.desc.p, desc.size() * sizeof(PageDesc),
+                            cudaMemcpyDeviceToHost, cs_));
+    SR_CUDA(cudaStreamSynchronize(cs_));
+  } else {
+    desc = page_desc_h_;
+  }
+  for (PageDesc& pd : desc)
+    if (pd.src) pd.src = pr_hot_.enc.p + (pd.src - key);
+  pr_hot_.desc.reserve(std::max<size_t>(desc.size(), 1));
+  SR_CUDA(cudaMemcpyAsync(pr_hot_.desc.p, desc.data(), desc.size() * sizeof(PageDesc),
+                          cudaMemcpyHostToDevice, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  pr_hot_.slot_of.release();
+  pr_hot_.blocked = blocked;
+  pr_hot_.key = key;
+  pr_hot_.built = true;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // PageRank (new algorithm; conventions pinned in DESIGN.md §2)
 // ---------------------------------------------------------------------------
 void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
@@ -338,6 +423,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
   if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
   const bool blocked = build_src_blocks(pr_blk);
+  const bool hot = prepare_pr_hot(blocked);
   const auto wall0 = std::chrono::steady_clock::now();
   SR_CUDA(cudaEventRecord(ev_start_, cs_));
   launch_inv_outdeg(out_off_.p, n_, inv_outdeg_.p, cs_);
@@ -358,6 +444,9 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     }
     PassOut po;
     const float base = float((1.0 - cfg.pr_damping) / double(n_));
+    if (hot)
+      launch_pr_hot_gather(pr_hot_.hot_vertex.p, pr_hot_.n_hot, contrib_a_.p,
+                           pr_hot_.hot_contrib.p, cs_);
     if (blocked) {
       pr_blocked_pass(base, float(cfg.pr_damping));
       po.kernel_runs = sb_.n_blocks * pages_.size();

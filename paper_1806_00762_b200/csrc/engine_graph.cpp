@@ -59,6 +59,7 @@ void Engine::build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<u
   m_ = m;
   has_csr_edges_ = csr_edges;
   csr_weighted_ = csr_edges && weighted;
+  adj_host_ = false;  // built in HBM; load_pages moves it out if it breaks a budget
   finish_csr();
   PinBuf<uint32_t> local_h;
   PinBuf<unsigned long long> in_off_h;
@@ -242,6 +243,7 @@ void Engine::graph_info(sr_graph_info& gi) const {
   gi.has_csr_edges = has_csr_edges_ ? 1 : 0;
   gi.csr_weighted = csr_weighted_ ? 1 : 0;
   gi.csr_derived = csr_derived_ ? 1 : 0;
+  gi.adjacency_on_host = adj_host_ ? 1 : 0;
 }
 
 void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w, uint64_t* in_off,
@@ -256,11 +258,11 @@ void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w,
       SR_CUDA(cudaStreamSynchronize(cs_));
     }
     if (!has_csr_edges_) throw EngineError(SR_E_DATA, "csr adjacency not on the device");
-    if (m_) SR_CUDA(cudaMemcpy(out_nbr, out_nbr_.p, m_ * 4, cudaMemcpyDeviceToHost));
+    if (m_) SR_CUDA(cudaMemcpy(out_nbr, nbr_ptr(), m_ * 4, cudaMemcpyDefault));
   }
   if (out_w) {
     if (!csr_weighted_) throw EngineError(SR_E_DATA, "csr has no weights");
-    if (m_) SR_CUDA(cudaMemcpy(out_w, out_w_.p, m_ * 4, cudaMemcpyDeviceToHost));
+    if (m_) SR_CUDA(cudaMemcpy(out_w, w_ptr(), m_ * 4, cudaMemcpyDefault));
   }
   if (!(in_off || in_src || in_w)) return;
   if (!pages_loaded_) throw EngineError(SR_E_DATA, "no pages loaded");

@@ -39,14 +39,14 @@ void Engine::ensure_slots(uint32_t window, PassOut& po) {
   uint64_t prefix = 0;
   for (size_t k = 0; k < U; ++k) {
     const uint64_t slot_bytes = suf_words[k] * 4;
-    if (prefix + want * slot_bytes <= budget_) {
+    if (prefix + want * slot_bytes <= page_budget_) {
       K = k;
       fits = true;
     }
     prefix += pages_[used[k]].bytes;
   }
   if (!fits)
-    throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(budget_) +
+    throw EngineError(SR_E_CONFIG, "hbm budget " + std::to_string(page_budget_) +
                                        " B cannot hold a window of " + std::to_string(want) +
                                        " page slots of " + std::to_string(suf_words[0] * 4) + " B");
   const bool same_plan = plan_window_ == want && plan_cached_ == K && ring_words_ > 0;

@@ -37,6 +37,7 @@ constexpr int kCensusParts = 13;  // per-block census partials
 constexpr int kLaneEdges = 8;  // consecutive edges per lane per K1 phase-B round
 constexpr uint32_t kBndWords = 33;  // K1 entry-start bitmap words (span <= 1031 positions)
 constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
+constexpr uint32_t kNone = 0xffffffffu;  // no entry (K8 segmented merge)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -191,9 +192,11 @@ __device__ __forceinline__ uint32_t dest_floor(const PullArgs& a) {
 // `scratch` reuses the caller's tile shared memory (>= 40 words): extra
 // static shared memory would push 4 blocks/SM past a carveout step and
 // shrink the L1 that serves the gathers.
+template <int W = kWarpsPerBlock>
 __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t lane_min,
                                             Census* census, uint32_t* scratch) {
   constexpr int kCtr = 5;
+  constexpr int kWarpsPerBlock = W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
   uint32_t* mins = scratch + 2 * kCtr * kWarpsPerBlock;
@@ -765,10 +768,21 @@ __global__ void commit_kernel(uint32_t* __restrict__ values, const uint32_t* __r
 // with uint4 source loads, gathers of contrib[src], per-lane fold and a
 // shared-memory float atomicAdd merge; hub chunks go through hub_sum.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
-  __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
-  __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
-  __shared__ float s_sum[kWarpsPerBlock][kTileMaxDests];
+//
+// HOT (north_star "shared-memory staging of hot vertex values"): the n_hot
+// highest out-degree sources have their contributions staged in shared memory
+// once per launch (a.hot_contrib, compacted by pr_hot_gather_kernel), and the
+// launch reads a source array in which those sources are encoded as
+// kHotBit | slot (Engine::prepare_pr_hot).  A random 4-byte gather through
+// L1 costs one L1TEX wavefront per lane (one 128 B line each); a shared-memory
+// gather costs one bank cycle per conflicting lane, so every hot-source edge
+// leaves the L1 gather queue.  One block of W warps per SM holds the table.
+template <bool HOT, int W>
+__global__ void __launch_bounds__(W * 32) pr_pull_kernel(PrArgs a) {
+  __shared__ __align__(16) uint32_t s_pref[W][kTileMaxDests];
+  __shared__ uint32_t s_loc[W][kTileMaxDests];
+  __shared__ float s_sum[W][kTileMaxDests];
+  extern __shared__ float s_hot[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   float* sum_of = s_sum[warp];
@@ -778,6 +792,16 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
   uint32_t cur_page = 0xffffffffu;
   PageDesc pd{};
   const float* __restrict__ contrib = a.contrib_in;
+  if (HOT) {
+    const float4* h4 = reinterpret_cast<const float4*>(a.hot_contrib);
+    float4* s4 = reinterpret_cast<float4*>(s_hot);
+    for (uint32_t i = threadIdx.x; i < (a.n_hot + 3) / 4; i += W * 32) s4[i] = __ldcg(h4 + i);
+    __syncthreads();
+  }
+  auto gather = [&](uint32_t s) -> float {
+    if (HOT && (s & kHotBit)) return s_hot[s & ~kHotBit];
+    return gather_ro(contrib + s);
+  };
 
   for (;;) {
     uint32_t t0 = 0;
@@ -813,7 +837,7 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           float x[kLaneEdges];
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t)
-            x[t] = (p0 + t >= tile.x && p0 + t < tile.y) ? gather_ro(contrib + si[t]) : 0.f;
+            x[t] = (p0 + t >= tile.x && p0 + t < tile.y) ? gather(si[t]) : 0.f;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t) sum += x[t];
         }
@@ -857,8 +881,17 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
         continue;
       }
       const uint32_t lo_pos = tile.x - ebase, span = tile.y - ebase;
+      // Per-destination merge without shared-memory atomics (a float
+      // atomicAdd on shared memory is a CAS spin loop, ATOMS.CAST.SPIN): a
+      // lane's runs strictly inside its 8 positions are complete destinations
+      // (plain store); its first/last runs may continue across lanes, so
+      // their partial sums are combined by a segmented warp scan and written
+      // once, by the lane where the destination's run ends in this round.
       for (uint32_t r0 = 0; r0 < span; r0 += 32 * kLaneEdges) {
         const uint32_t pos0 = r0 + lane * kLaneEdges;
+        uint32_t id_f = kNone, id_l = kNone;
+        float s_f = 0.f, s_l = 0.f;
+        bool multi = false;
         if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
           const uint32_t q = max(pos0, lo_pos);
           uint32_t lo = 0, hi = n_ent - 1;
@@ -887,22 +920,54 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
           float x[kLaneEdges];
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t)
-            x[t] = (live >> t & 1u) ? gather_ro(contrib + sidx[t]) : 0.f;
+            x[t] = (live >> t & 1u) ? gather(sidx[t]) : 0.f;
           c.gathers += __popc(live);
-          uint32_t run_ent = 0xffffffffu;
+          uint32_t run_ent = kNone;
           float run = 0.f;
 #pragma unroll
           for (int t = 0; t < kLaneEdges; ++t) {
             if (!(live >> t & 1u)) continue;
             if (eid[t] != run_ent) {
-              if (run_ent != 0xffffffffu) atomicAdd(sum_of + run_ent, run);
+              if (run_ent != kNone) {
+                if (!multi) {
+                  id_f = run_ent;
+                  s_f = run;
+                } else {
+                  sum_of[run_ent] = run;  // complete inside this lane
+                }
+                multi = true;
+              }
               run_ent = eid[t];
               run = 0.f;
             }
             run += x[t];
           }
-          if (run_ent != 0xffffffffu) atomicAdd(sum_of + run_ent, run);
+          id_l = run_ent;
+          s_l = run;
+          if (!multi) {
+            id_f = run_ent;
+            s_f = run;
+          }
         }
+        uint32_t prev_l = __shfl_up_sync(kFull, id_l, 1);
+        uint32_t next_f = __shfl_down_sync(kFull, id_f, 1);
+        if (lane == 0) prev_l = kNone;
+        if (lane == 31) next_f = kNone;
+        const bool cont = id_f != kNone && id_f == prev_l;
+        // segmented inclusive scan of the last-run partials; a segment head
+        // is every lane except a single-run lane continuing its predecessor
+        const unsigned heads = __ballot_sync(kFull, multi || !cont);
+        const int head = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+        float X = s_l;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float y = __shfl_up_sync(kFull, X, off);
+          if (lane - off >= head) X += y;
+        }
+        const float x_prev = __shfl_up_sync(kFull, X, 1);
+        if (multi) sum_of[id_f] += s_f + (cont ? x_prev : 0.f);
+        if (id_l != kNone && next_f != id_l) sum_of[id_l] += X;
+        __syncwarp();
       }
       __syncwarp();
       for (uint32_t i = lane; i < n_ent; i += 32) {
@@ -918,7 +983,62 @@ __global__ void __launch_bounds__(kBlockThreads) pr_pull_kernel(PrArgs a) {
       __syncwarp();
     }
   }
-  block_flush(c, a.ctr, kUnreached, nullptr, &s_pref[0][0]);
+  block_flush<W>(c, a.ctr, kUnreached, nullptr, &s_pref[0][0]);
+}
+
+// Hot-set staging for K8 (see pr_pull_kernel): compact the hot sources'
+// contributions of this iteration (n_hot random gathers, once per launch).
+__global__ void pr_hot_gather_kernel(const uint32_t* __restrict__ hot_vertex, uint32_t n_hot,
+                                     const float* __restrict__ contrib, float* hot_contrib) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_hot) hot_contrib[i] = contrib[hot_vertex[i]];
+}
+
+// Vertices with out-degree >= d (binary search of the hot threshold).
+__global__ void count_deg_ge_kernel(const uint32_t* __restrict__ deg, uint32_t n, uint32_t d,
+                                    unsigned long long* out) {
+  uint32_t k = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    k += deg[v] >= d;
+  k = __reduce_add_sync(kFull, k);
+  if ((threadIdx.x & 31) == 0 && k) atomicAdd(out, (unsigned long long)k);
+}
+
+// Slots of the hot set: every vertex with out-degree >= d (at most cap of
+// them by the threshold choice); slot_of[v] = slot (else kUnreached).
+__global__ void hot_assign_kernel(const uint32_t* __restrict__ deg, uint32_t n, uint32_t d,
+                                  uint32_t cap, unsigned* counter, uint32_t* slot_of,
+                                  uint32_t* hot_vertex) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    uint32_t slot = kUnreached;
+    if (deg[v] >= d) {
+      const uint32_t k = atomicAdd(counter, 1u);
+      if (k < cap) {
+        slot = k;
+        hot_vertex[k] = v;
+      }
+    }
+    slot_of[v] = slot;
+  }
+}
+
+// Encoded source stream: hot sources -> kHotBit | slot, others unchanged
+// (words >= n are alignment padding and are copied as they are).
+__global__ void hot_encode_kernel(const uint4* __restrict__ in, uint4* out, uint64_t n4,
+                                  const uint32_t* __restrict__ slot_of, uint32_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint4 v = __ldcs(in + i);
+    uint32_t* e = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (e[k] < n) {
+        const uint32_t sl = slot_of[e[k]];
+        if (sl != kUnreached) e[k] = kHotBit | sl;
+      }
+    }
+    __stcs(out + i, v);
+  }
 }
 
 __global__ void pr_hub_finalize_kernel(const uint32_t* hub_vertex, uint32_t n_hubs,
@@ -1691,9 +1811,99 @@ void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t
   commit_kernel<<<grid_for(hi - lo, 256), 256, 0, s>>>(values, next, lo, hi);
 }
 
+// Hot-staged K8: warps per block (SERAPH_PR_HOT_WARPS = 8 | 16 | 32; A/B knob)
+int pr_hot_warps() {
+  static int w = [] {
+    const char* e = std::getenv("SERAPH_PR_HOT_WARPS");
+    const int v = e ? std::atoi(e) : kHotWarps;
+    return (v == 8 || v == 16 || v == 32) ? v : kHotWarps;
+  }();
+  return w;
+}
+
+template <int W>
+static void set_hot_attr() {
+  static bool attr = false;
+  if (!attr) {
+    SR_CUDA(cudaFuncSetAttribute(pr_pull_kernel<true, W>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kHotSmemBytes - W * 1536)));
+    attr = true;
+  }
+}
+
+template <int W>
+static int hot_occupancy(size_t dyn) {
+  set_hot_attr<W>();
+  int b = 0;
+  SR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pr_pull_kernel<true, W>, W * 32, dyn));
+  return b;
+}
+
+// Resident blocks per SM of the hot-staged K8 with an n_hot-entry table.
+int pr_hot_blocks_per_sm(uint32_t n_hot) {
+  const size_t dyn = size_t((n_hot + 3) & ~3u) * 4;
+  int b = 1;
+  switch (pr_hot_warps()) {
+    case 8: b = hot_occupancy<8>(dyn); break;
+    case 32: b = hot_occupancy<32>(dyn); break;
+    default: b = hot_occupancy<16>(dyn);
+  }
+  return std::max(b, 1);
+}
+
+// Largest table the selected block shape can hold.
+uint32_t pr_hot_table_max() {
+  return uint32_t((kHotSmemBytes - pr_hot_warps() * 1536) / 4) & ~255u;
+}
+
+template <int W>
+static void launch_pr_hot_w(const PrArgs& a, int grid, size_t dyn, cudaStream_t s) {
+  set_hot_attr<W>();
+  pr_pull_kernel<true, W><<<grid, W * 32, dyn, s>>>(a);
+}
+
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s) {
   note_launch();
-  pr_pull_kernel<<<grid, kBlockThreads, 0, s>>>(a);
+  if (a.hot_contrib) {
+    const size_t dyn = size_t((a.n_hot + 3) & ~3u) * 4;
+    switch (pr_hot_warps()) {
+      case 8: launch_pr_hot_w<8>(a, grid, dyn, s); break;
+      case 32: launch_pr_hot_w<32>(a, grid, dyn, s); break;
+      default: launch_pr_hot_w<16>(a, grid, dyn, s);
+    }
+    return;
+  }
+  pr_pull_kernel<false, kWarpsPerBlock><<<grid, kBlockThreads, 0, s>>>(a);
+}
+
+void launch_pr_hot_gather(const uint32_t* hot_vertex, uint32_t n_hot, const float* contrib,
+                          float* hot_contrib, cudaStream_t s) {
+  if (!n_hot) return;
+  note_launch();
+  pr_hot_gather_kernel<<<(n_hot + 255) / 256, 256, 0, s>>>(hot_vertex, n_hot, contrib,
+                                                           hot_contrib);
+}
+
+void launch_count_deg_ge(const uint32_t* deg, uint32_t n, uint32_t d, unsigned long long* out,
+                         cudaStream_t s) {
+  note_launch();
+  count_deg_ge_kernel<<<grid_for(n, 256), 256, 0, s>>>(deg, n, d, out);
+}
+
+void launch_hot_assign(const uint32_t* deg, uint32_t n, uint32_t d, uint32_t cap,
+                       unsigned* counter, uint32_t* slot_of, uint32_t* hot_vertex, cudaStream_t s) {
+  note_launch();
+  hot_assign_kernel<<<grid_for(n, 256), 256, 0, s>>>(deg, n, d, cap, counter, slot_of, hot_vertex);
+}
+
+void launch_hot_encode(const uint32_t* in, uint32_t* out, uint64_t words, const uint32_t* slot_of,
+                       uint32_t n, cudaStream_t s) {
+  if (!words) return;
+  note_launch();
+  const uint64_t n4 = (words + 3) / 4;
+  hot_encode_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(in), reinterpret_cast<uint4*>(out), n4, slot_of, n);
 }
 
 void launch_pr_hub_finalize(const uint32_t* hub_vertex, uint32_t n_hubs, float* hub_sum,

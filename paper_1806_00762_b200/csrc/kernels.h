@@ -18,6 +18,19 @@ void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t
 // Kernels launched so far by the calling thread (all launch_* wrappers).
 uint64_t kernel_launch_count();
 void launch_pr_pull(const PrArgs& a, int grid, cudaStream_t s);
+int pr_hot_warps();
+int pr_hot_blocks_per_sm(uint32_t n_hot);
+uint32_t pr_hot_table_max();
+// K8 hot-source staging (pr_pull_kernel<true>): per-iteration compaction of
+// the hot contributions, threshold count, slot assignment, source encoding.
+void launch_pr_hot_gather(const uint32_t* hot_vertex, uint32_t n_hot, const float* contrib,
+                          float* hot_contrib, cudaStream_t s);
+void launch_count_deg_ge(const uint32_t* deg, uint32_t n, uint32_t d, unsigned long long* out,
+                         cudaStream_t s);
+void launch_hot_assign(const uint32_t* deg, uint32_t n, uint32_t d, uint32_t cap,
+                       unsigned* counter, uint32_t* slot_of, uint32_t* hot_vertex, cudaStream_t s);
+void launch_hot_encode(const uint32_t* in, uint32_t* out, uint64_t words, const uint32_t* slot_of,
+                       uint32_t n, cudaStream_t s);
 // Sparse push enumerated from the CSC pages (push adjacency not derived):
 // relaxes the in-edges whose source is in a.list (n_list entries).
 void launch_push_scan(int algo, const PushArgs& a, const PageDesc* pages, uint32_t n_pages,

@@ -1,0 +1,125 @@
+#include "stager.h"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "errors.h"
+
+namespace seraph {
+
+HostStager::~HostStager() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_job_.notify_all();
+  for (auto& t : pool_) t.join();
+  for (size_t i = 0; i < ev_.size(); ++i) {
+    if (ev_live_[i]) cudaEventSynchronize(ev_[i]);
+    cudaEventDestroy(ev_[i]);
+  }
+  for (void* b : buf_) cudaFreeHost(b);
+}
+
+bool HostStager::pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+void HostStager::ensure() {
+  if (!buf_.empty()) return;
+  SR_CUDA(cudaGetDevice(&device_));
+  for (int i = 0; i < kBufs; ++i) {
+    void* b = nullptr;
+    SR_CUDA(cudaHostAlloc(&b, kChunk, cudaHostAllocPortable));
+    buf_.push_back(b);
+    cudaEvent_t e;
+    SR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_.push_back(e);
+    ev_live_.push_back(false);
+  }
+  unsigned h = std::thread::hardware_concurrency();
+  int t = h ? int(std::min<unsigned>(h, 8)) : 4;
+  if (const char* e = std::getenv("SERAPH_STAGE_THREADS")) t = std::max(1, std::atoi(e));
+  threads_ = t;
+  for (int k = 1; k < threads_; ++k) pool_.emplace_back(&HostStager::worker, this, k);
+}
+
+void HostStager::worker(int k) {
+  uint64_t seen = 0;
+  for (;;) {
+    char* dst;
+    const char* src;
+    size_t bytes;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_job_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      dst = job_dst_;
+      src = job_src_;
+      bytes = job_bytes_;
+    }
+    const size_t a = bytes * k / threads_, b = bytes * (k + 1) / threads_;
+    std::memcpy(dst + a, src + a, b - a);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) cv_done_.notify_one();
+    }
+  }
+}
+
+void HostStager::copy_parallel(void* dst, const void* src, size_t bytes) {
+  if (threads_ <= 1 || bytes < (1u << 20)) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_dst_ = static_cast<char*>(dst);
+    job_src_ = static_cast<const char*>(src);
+    job_bytes_ = bytes;
+    pending_ = threads_ - 1;
+    ++gen_;
+  }
+  cv_job_.notify_all();
+  std::memcpy(dst, src, bytes / threads_);  // slice 0 on the calling thread
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_done_.wait(lk, [&] { return pending_ == 0; });
+}
+
+void HostStager::h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return;
+  if (!pageable(src)) {
+    SR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    return;
+  }
+  ensure();
+  for (size_t off = 0; off < bytes; off += kChunk) {
+    const size_t len = std::min(kChunk, bytes - off);
+    const int b = next_;
+    next_ = (next_ + 1) % kBufs;
+    if (ev_live_[b]) SR_CUDA(cudaEventSynchronize(ev_[b]));  // its previous DMA is done
+    copy_parallel(buf_[b], static_cast<const char*>(src) + off, len);
+    SR_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf_[b], len, cudaMemcpyHostToDevice, s));
+    SR_CUDA(cudaEventRecord(ev_[b], s));
+    ev_live_[b] = true;
+    staged_ += len;
+  }
+}
+
+void HostStager::sync() {
+  for (size_t i = 0; i < ev_.size(); ++i)
+    if (ev_live_[i]) {
+      SR_CUDA(cudaEventSynchronize(ev_[i]));
+      ev_live_[i] = false;
+    }
+}
+
+}  // namespace seraph

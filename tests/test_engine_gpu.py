@@ -260,6 +260,46 @@ def test_virtual_clock_is_deterministic(engine):
 # --------------------------------------------------------------------------
 # out-of-core path (forced HBM budget)
 # --------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", [ps.AlgoKind.BFS, ps.AlgoKind.SSSP, ps.AlgoKind.CC])
+def test_out_of_core_traversal_adjacency_budget(kind):
+    """The HBM budget covers pages AND the push adjacency: when both do not fit
+    the adjacency stays in pinned host memory and the sparse passes read the
+    frontier's rows zero-copy (engine.cpp:63-93 push over a host-resident
+    CSR); when they fit it is uploaded.  Density-switched runs (sparse and
+    dense passes) stay bit-exact either way, and a device-built graph moves its
+    adjacency out of HBM when it breaks the budget."""
+    scale = 12
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=6)
+    w = O.assign_weights(src.size, 4, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    if kind == ps.AlgoKind.CC:
+        el = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    csr, pages = built(el, n // 64)
+    sizes = [ps.page_bytes(p, True) for p in pages.pages]
+    total = sum(sizes)
+    adj = el.num_edges() * 8
+    want = oracle_values(el, kind, 0)
+    c = cfg_of(clock=ps.ClockMode.WALL, window=4, pred=ps.PredictorMode.STRONG)
+    for budget, on_host, streamed in ((4 * max(sizes) + total // 8, 1, True),  # both streamed
+                                      (total + adj // 2, 1, False),            # pages fit, adj not
+                                      (total + adj + 4096, 0, False)):         # both fit
+        with ps.Engine(0, budget) as eng:
+            r = eng.run_graph(csr, pages, program_for(kind, 0, el), c)
+            assert np.array_equal(r.values, want), (kind, budget)
+            assert eng.graph_info()["adjacency_on_host"] == on_host, (kind, budget)
+            assert r.metrics.sparse_passes > 0
+            if streamed:
+                assert r.metrics.bytes_transferred >= total
+            r2 = eng.run(program_for(kind, 0, el), c)  # second run on the same placement
+            assert np.array_equal(r2.values, want)
+    # device-built graph (adjacency built in HBM) under a budget it breaks
+    with ps.Engine(0, 4 * max(sizes) + total // 8) as eng:
+        eng.build_graph(el, n // 64, csr_edges=True)
+        assert eng.graph_info()["adjacency_on_host"] == 1
+        r = eng.run(program_for(kind, 0, el), c)
+        assert np.array_equal(r.values, want)
+
 @pytest.mark.parametrize("mode", MODES)
 def test_streaming_matches_resident(mode):
     scale = 12
@@ -317,7 +357,7 @@ def test_pagerank_rmat_vs_oracle(engine, scale):
 # --------------------------------------------------------------------------
 # bigger graphs: hub chunks, many tiles, sparse/dense switching
 # --------------------------------------------------------------------------
-@pytest.mark.parametrize("case", ["resident", "blocked", "streamed"])
+@pytest.mark.parametrize("case", ["resident", "blocked", "streamed", "hot", "hot-blocked"])
 def test_pagerank_rmat18_relative(case, monkeypatch):
     """PageRank at RMAT-18 (4.2 M edges) against the fp64 OpenMP oracle with a
     RELATIVE bound (mean rank 2^-18: an absolute 1e-6 would be vacuous):
@@ -325,8 +365,11 @@ def test_pagerank_rmat18_relative(case, monkeypatch):
     (north_star's per-vertex bound).  Resident, source-blocked (K8 partial
     sums) and streamed through a 16 MB budget."""
     n = 1 << 18
-    if case == "blocked":
+    if case.endswith("blocked"):
         monkeypatch.setenv("SERAPH_PR_BLOCK_VERTS", str(n // 4))
+    # hot-source staging (K8 <true>): the top out-degree sources from shared
+    # memory, forced on at this size (default: |V| > 1 Mi)
+    monkeypatch.setenv("SERAPH_PR_HOT", {"hot": "4096", "hot-blocked": "777"}.get(case, "0"))
     budget = (16 << 20) if case == "streamed" else 0
     cfg = cfg_of(clock=ps.ClockMode.WALL)
     with ps.Engine(0, budget) as eng:
