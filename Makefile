@@ -15,7 +15,7 @@ CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I$(CUDA_HOME)
 LDFLAGS := -shared -L$(CUDA_HOME)/lib64 -lcudart -ldl -lpthread -Wl,-rpath,$(CUDA_HOME)/lib64
 
 HDRS := include/seraph.h $(wildcard $(SRC)/*.h)
-OBJS := $(BUILD)/kernels.o $(BUILD)/devgraph.o $(BUILD)/engine.o $(BUILD)/engine_graph.o $(BUILD)/engine_stream.o $(BUILD)/engine_blocks.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o $(BUILD)/nccl_dyn.o $(BUILD)/loopback.o $(BUILD)/mt64.o $(BUILD)/stager.o
+OBJS := $(BUILD)/kernels.o $(BUILD)/devgraph.o $(BUILD)/engine.o $(BUILD)/engine_graph.o $(BUILD)/engine_stream.o $(BUILD)/engine_blocks.o $(BUILD)/vsched.o $(BUILD)/capi.o $(BUILD)/hostgraph.o $(BUILD)/nccl_dyn.o $(BUILD)/loopback.o $(BUILD)/mt64.o $(BUILD)/stager.o $(BUILD)/group.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle

@@ -10,6 +10,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -35,11 +37,57 @@ namespace pagestream::seraph {
   }
 }
 
+// Options of a drop-in call beyond the reference's signature.
+//  devices:    GPUs of this process to shard the run over (empty: the
+//              SERAPH_DEVICES environment variable, e.g. "0,1,2,3", else GPU 0).
+//              More than one device runs the sharded world (sr_group_*);
+//              ClockMode::Virtual (the reference's deterministic schedule)
+//              always runs on the first device alone.
+//  generation: residency cache.  0 (default): every call uploads its graph,
+//              exactly like the reference's run() reads its arguments.  g != 0:
+//              the caller promises that the CsrGraph/PageSet objects at these
+//              addresses are unchanged since the last call with the same g, so
+//              a repeated run (run_matrix cells and repetitions,
+//              bench.cpp:169-275) reuses the graph resident in HBM.
+struct RunOptions {
+  std::vector<int> devices;
+  uint64_t generation = 0;
+};
+
+inline std::vector<int> env_devices() {
+  std::vector<int> d;
+  if (const char* e = std::getenv("SERAPH_DEVICES")) {
+    std::string s(e);
+    size_t at = 0;
+    while (at < s.size()) {
+      size_t comma = s.find(',', at);
+      if (comma == std::string::npos) comma = s.size();
+      if (comma > at) d.push_back(std::atoi(s.substr(at, comma - at).c_str()));
+      at = comma + 1;
+    }
+  }
+  if (d.empty()) d.push_back(0);
+  return d;
+}
+
+// Identity of the graph a context holds (residency cache).
+struct GraphKey {
+  const void* csr = nullptr;
+  const void* pages = nullptr;
+  uint64_t generation = 0, n = 0, m = 0, np = 0;
+  bool lean = false;  // loaded for PageRank (no push adjacency)
+  bool operator==(const GraphKey& o) const {
+    return generation != 0 && csr == o.csr && pages == o.pages && generation == o.generation &&
+           n == o.n && m == o.m && np == o.np && lean == o.lean;
+  }
+};
+
 // One context per device, reused across calls; run() is serialised per
 // device (the reference allows concurrent run() calls, bench.cpp:254-259).
 struct DeviceContext {
   sr_ctx* ctx = nullptr;
   std::mutex mu;
+  GraphKey held;
   ~DeviceContext() {
     if (ctx) sr_close(ctx);
   }
@@ -54,6 +102,29 @@ inline DeviceContext& device_context(int device = 0) {
     if (rc != SR_OK) rethrow(rc, sr_global_error());
   }
   return d;
+}
+
+// One multi-GPU world per device list.
+struct GroupContext {
+  sr_group* g = nullptr;
+  std::mutex mu;
+  GraphKey held;
+  ~GroupContext() {
+    if (g) sr_group_close(g);
+  }
+};
+
+inline GroupContext& group_context(const std::vector<int>& devices) {
+  static std::mutex reg_mu;
+  static std::vector<std::pair<std::vector<int>, std::unique_ptr<GroupContext>>> reg;
+  std::lock_guard<std::mutex> lk(reg_mu);
+  for (auto& [k, gc] : reg)
+    if (k == devices) return *gc;
+  auto gc = std::make_unique<GroupContext>();
+  const int rc = sr_group_open(devices.data(), int(devices.size()), 0, SR_EXCHANGE_PEER, &gc->g);
+  if (rc != SR_OK) rethrow(rc, sr_group_last_error(nullptr));
+  reg.emplace_back(devices, std::move(gc));
+  return *reg.back().second;
 }
 
 inline sr_run_config to_c(const VertexProgram& program, const EngineConfig& config) {
@@ -77,9 +148,9 @@ inline sr_run_config to_c(const VertexProgram& program, const EngineConfig& conf
   return c;
 }
 
-// pagestream::run (engine.hpp:125-126) executed by libseraph on `device`.
+// pagestream::run (engine.hpp:125-126) executed by libseraph (options above).
 inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProgram& program,
-                     const EngineConfig& config, int device = 0) {
+                     const EngineConfig& config, const RunOptions& opt) {
   config.validate();  // engine.cpp:422 (ConfigError on the host, as before)
   if (csr.num_vertices != pages.num_vertices)
     throw ConfigError("csr and page set disagree on vertex count");
@@ -101,18 +172,57 @@ inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProg
   sr_metrics m{};
   std::vector<sr_pass_stats> passes(256);
   uint32_t npass = 0;
-  DeviceContext& dc = device_context(device);
-  std::lock_guard<std::mutex> lk(dc.mu);
-  for (;;) {
-    const int rc = sr_run_graph(dc.ctx, csr.num_vertices, csr.num_edges(), csr.out_offsets.data(),
-                                csr.out_neighbors.data(),
-                                csr.weighted() ? csr.out_weights.data() : nullptr,
-                                pages.page_vertex_capacity, pages.weighted ? 1 : 0, views.data(),
-                                uint32_t(views.size()), &c, r.values.data(), nullptr, &m,
-                                passes.data(), uint32_t(passes.size()), &npass);
-    if (rc != SR_OK) rethrow(rc, sr_last_error(dc.ctx));
-    if (npass <= passes.size()) break;
-    passes.resize(npass);  // rerun with room for every pass record
+  const std::vector<int> devices = opt.devices.empty() ? env_devices() : opt.devices;
+  GraphKey key{&csr, &pages, opt.generation, csr.num_vertices, csr.num_edges(),
+               pages.pages.size(), false};
+  const uint64_t* off = csr.out_offsets.data();
+  const uint32_t* nbr = csr.out_neighbors.data();
+  const uint32_t* wts = csr.weighted() ? csr.out_weights.data() : nullptr;
+  const int wp = pages.weighted ? 1 : 0;
+  const uint32_t np = uint32_t(views.size());
+  sr_ctx* trace_ctx = nullptr;
+  if (devices.size() > 1 && config.clock == ClockMode::Wall) {  // sharded over the devices
+    GroupContext& gc = group_context(devices);
+    std::lock_guard<std::mutex> lk(gc.mu);
+    for (;;) {
+      int rc;
+      if (gc.held == key) {
+        rc = sr_group_run(gc.g, &c, r.values.data(), nullptr, &m, passes.data(),
+                          uint32_t(passes.size()), &npass);
+      } else {
+        gc.held = GraphKey{};
+        rc = sr_group_load_graph(gc.g, csr.num_vertices, csr.num_edges(), off, nbr, wts,
+                                 pages.page_vertex_capacity, wp, views.data(), np, -1);
+        if (rc == SR_OK) {
+          gc.held = key;
+          rc = sr_group_run(gc.g, &c, r.values.data(), nullptr, &m, passes.data(),
+                            uint32_t(passes.size()), &npass);
+        }
+      }
+      if (rc != SR_OK) rethrow(rc, sr_group_last_error(gc.g));
+      if (npass <= passes.size()) break;
+      passes.resize(npass);
+    }
+  } else {
+    DeviceContext& dc = device_context(devices[0]);
+    std::lock_guard<std::mutex> lk(dc.mu);
+    for (;;) {
+      int rc;
+      if (dc.held == key) {
+        rc = sr_run(dc.ctx, &c, r.values.data(), nullptr, &m, passes.data(),
+                    uint32_t(passes.size()), &npass);
+      } else {
+        dc.held = GraphKey{};
+        rc = sr_run_graph(dc.ctx, csr.num_vertices, csr.num_edges(), off, nbr, wts,
+                          pages.page_vertex_capacity, wp, views.data(), np, &c, r.values.data(),
+                          nullptr, &m, passes.data(), uint32_t(passes.size()), &npass);
+        if (rc == SR_OK) dc.held = key;
+      }
+      if (rc != SR_OK) rethrow(rc, sr_last_error(dc.ctx));
+      if (npass <= passes.size()) break;
+      passes.resize(npass);  // rerun with room for every pass record
+    }
+    trace_ctx = dc.ctx;
   }
   MetricsReport& mr = r.metrics;
   mr.passes = m.passes;
@@ -142,15 +252,21 @@ inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProg
     ps.has_status_counts = s.has_status_counts != 0;
     mr.per_pass.push_back(ps);
   }
-  if (config.record_trace) {
+  if (config.record_trace && trace_ctx) {
     uint64_t n = 0;
-    sr_get_trace(dc.ctx, nullptr, 0, &n);
+    sr_get_trace(trace_ctx, nullptr, 0, &n);
     std::vector<sr_trace_event> ev(n);
-    sr_get_trace(dc.ctx, ev.data(), n, &n);
+    sr_get_trace(trace_ctx, ev.data(), n, &n);
     for (const auto& e : ev)
       r.trace.push_back(TraceEvent{e.time, TraceEventKind(e.kind), e.page_id, e.pass_index});
   }
   return r;
+}
+
+// The reference's signature: the drop-in body of pagestream::run.
+inline RunResult run(const CsrGraph& csr, const PageSet& pages, const VertexProgram& program,
+                     const EngineConfig& config) {
+  return run(csr, pages, program, config, RunOptions{});
 }
 
 // build_csr + build_csc_pages (graph.cpp:30-94) on the GPU (sr_build_graph:
@@ -169,6 +285,7 @@ inline std::pair<CsrGraph, PageSet> build_graph(const EdgeList& el,
   const bool weighted = el.weighted();
   DeviceContext& dc = device_context(device);
   std::lock_guard<std::mutex> lk(dc.mu);
+  dc.held = GraphKey{};  // the context's graph is replaced
   int rc = sr_build_graph(dc.ctx, el.num_vertices, m, src.data(), dst.data(),
                           weighted ? el.weights.data() : nullptr, page_vertex_capacity,
                           SR_BUILD_CSR_EDGES);

@@ -335,6 +335,42 @@ int sr_attach_loopback(sr_ctx* ctx, int rank, int world, const char* group, int 
  * must have peer access over NVLink). */
 int sr_set_exchange(sr_ctx* ctx, int flags);
 
+/* ---- multi-GPU from ONE process (the reference's run() is one call in one
+ *      process: engine.hpp:125-126, bench.cpp:254-259) ---------------------
+ * A group is a world of n contexts, rank r on devices[r], each driven by its
+ * own host thread inside the calls below.  Distinct devices: NCCL
+ * communicators created in this process (+ the peer exchange when flags &
+ * SR_EXCHANGE_PEER); a device listed more than once: the in-process loopback
+ * transport (one-GPU boxes, tests).  Every rank uploads only its destination
+ * shard of the pages and only its own CSR adjacency rows (per-rank bytes
+ * O(|E|/n)); values/ranks come from rank 0's replica; per-pass counters are
+ * global; transfer counters are summed and times are the max over ranks. */
+typedef struct sr_group sr_group;
+int sr_group_open(const int* devices, int n, uint64_t hbm_budget_bytes, int flags,
+                  sr_group** out);
+void sr_group_close(sr_group* g);
+const char* sr_group_last_error(const sr_group* g);
+int sr_group_size(const sr_group* g);
+/* Upload (each rank its shard) and keep the graph resident for sr_group_run.
+ * algo_hint: the algorithm the graph is loaded for (SR_ALGO_PAGERANK skips the
+ * adjacency), or -1. */
+int sr_group_load_graph(sr_group* g, uint32_t num_vertices, uint64_t num_edges,
+                        const uint64_t* out_offsets, const uint32_t* out_neighbors,
+                        const uint32_t* out_weights, uint32_t page_vertex_capacity, int weighted,
+                        const sr_page_view* pages, uint32_t n_pages, int algo_hint);
+int sr_group_run(sr_group* g, const sr_run_config* cfg, uint32_t* values_out, float* ranks_out,
+                 sr_metrics* metrics_out, sr_pass_stats* per_pass, uint32_t per_pass_cap,
+                 uint32_t* n_pass_out);
+/* sr_run_graph over the group: load + run in one call. */
+int sr_group_run_graph(sr_group* g, uint32_t num_vertices, uint64_t num_edges,
+                       const uint64_t* out_offsets, const uint32_t* out_neighbors,
+                       const uint32_t* out_weights, uint32_t page_vertex_capacity, int weighted,
+                       const sr_page_view* pages, uint32_t n_pages, const sr_run_config* cfg,
+                       uint32_t* values_out, float* ranks_out, sr_metrics* metrics_out,
+                       sr_pass_stats* per_pass, uint32_t per_pass_cap, uint32_t* n_pass_out);
+/* Graph placement of one rank (its shard). */
+int sr_group_graph_info(const sr_group* g, int rank, sr_graph_info* out);
+
 /* ---- host-side graph utilities (no GPU needed) ------------------------- */
 /* Edge-balanced contiguous cut of the destination space into `parts`
  * ranges: cuts[0]=0 ... cuts[parts]=num_vertices, chosen so that every range

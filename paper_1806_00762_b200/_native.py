@@ -204,6 +204,7 @@ class GraphInfo(C.Structure):
 
 
 BUILD_CSR_EDGES = 1
+EXCHANGE_PEER = 1
 
 # Every symbol include/seraph.h declares: (name, restype, argtypes)
 _VP, _U32, _U64, _I32, _D = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double
@@ -242,6 +243,19 @@ SIGNATURES = {
     "sr_attach_world": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(C.c_uint8 * 128)]),
     "sr_attach_loopback": (C.c_int, [_VP, C.c_int, C.c_int, C.c_char_p, C.c_int]),
     "sr_set_exchange": (C.c_int, [_VP, C.c_int]),
+    "sr_group_open": (C.c_int, [C.POINTER(C.c_int), C.c_int, _U64, C.c_int, C.POINTER(_VP)]),
+    "sr_group_close": (None, [_VP]),
+    "sr_group_last_error": (C.c_char_p, [_VP]),
+    "sr_group_size": (C.c_int, [_VP]),
+    "sr_group_load_graph": (C.c_int, [_VP, _U32, _U64, _VP, _VP, _VP, _U32, C.c_int,
+                                      C.POINTER(PageView), _U32, C.c_int]),
+    "sr_group_run": (C.c_int, [_VP, C.POINTER(RunConfig), _VP, _VP, C.POINTER(MetricsC),
+                               C.POINTER(PassStatsC), _U32, C.POINTER(_U32)]),
+    "sr_group_run_graph": (C.c_int, [_VP, _U32, _U64, _VP, _VP, _VP, _U32, C.c_int,
+                                     C.POINTER(PageView), _U32, C.POINTER(RunConfig), _VP, _VP,
+                                     C.POINTER(MetricsC), C.POINTER(PassStatsC), _U32,
+                                     C.POINTER(_U32)]),
+    "sr_group_graph_info": (C.c_int, [_VP, C.c_int, C.POINTER(GraphInfo)]),
     "sr_shard_plan": (C.c_int, [_U32, _VP, _U32, _VP]),
     "sr_rmat_generate": (C.c_int, [C.c_int, _U64, _D, _D, _D, _D, _U64, _VP, _VP, C.c_int]),
     "sr_weights_generate": (C.c_int, [_U64, _U64, _U32, _U32, _VP, C.c_int]),
@@ -269,10 +283,13 @@ def _load():
 lib = _load()
 
 
-def check(rc: int, ctx=None) -> None:
+def check(rc: int, ctx=None, group=None) -> None:
     if rc == SR_OK:
         return
-    msg = lib.sr_last_error(ctx) if ctx else lib.sr_global_error()
+    if group is not None:
+        msg = lib.sr_group_last_error(group)
+    else:
+        msg = lib.sr_last_error(ctx) if ctx else lib.sr_global_error()
     text = msg.decode() if msg else f"error {rc}"
     raise _CODES.get(rc, Error)(text)
 

@@ -142,6 +142,9 @@ void Engine::load_csr(uint32_t n, uint64_t m, const uint64_t* off, const uint32_
   has_csr_edges_ = nbr != nullptr;
   csr_weighted_ = false;
   adj_host_ = false;
+  row_lo_ = 0;
+  row_hi_ = n;
+  nbr_base_ = 0;
   if (nbr && m && budget_ != 0) {
     // forced budget: stage the adjacency in pinned host memory; load_pages
     // decides where it lives (place_adjacency)
@@ -211,6 +214,68 @@ bool Engine::defer_csr(uint64_t m, int algo) const {
     return v != 0 && m >= v;
   }
   return algo == SR_ALGO_CC && m >= (1ull << 30);
+}
+
+void Engine::drop_csr() {
+  has_csr_ = has_csr_edges_ = csr_weighted_ = csr_derived_ = csr_deferred_ = false;
+  adj_host_ = false;
+  nbr_base_ = 0;
+  row_lo_ = row_hi_ = 0;
+  out_nbr_.release();
+  out_w_.release();
+  host_nbr_.release();
+  host_w_.release();
+}
+
+void Engine::load_csr_shard(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                            const uint32_t* w) {
+  SR_CUDA(cudaSetDevice(dev_));
+  if (!pages_loaded_ || page_n_ != n)
+    throw EngineError(SR_E_CONFIG, "load_csr_shard needs this rank's page set loaded first");
+  if (!off || off[0] != 0 || off[n] != m)
+    throw EngineError(SR_E_INPUT, "csr: out_offsets must start at 0 and end at num_edges");
+  const auto t0 = std::chrono::steady_clock::now();
+  n_ = n;
+  m_ = m;
+  out_off_.reserve(size_t(n) + 1);
+  stager_.h2d(out_off_.p, off, (size_t(n) + 1) * 8, xs_);
+  uint64_t bytes = (uint64_t(n) + 1) * 8;
+  row_lo_ = own_lo_;
+  row_hi_ = own_hi_;
+  const uint64_t e0 = off[row_lo_], e1 = off[row_hi_], me = e1 - e0;
+  nbr_base_ = e0;
+  has_csr_edges_ = nbr != nullptr;
+  csr_weighted_ = nbr && w;
+  adj_host_ = false;
+  out_nbr_.release();
+  out_w_.release();
+  if (nbr) {
+    uint64_t pages_dev = 0;
+    for (const PageMeta& pm : pages_) pages_dev += pm.on_device ? pm.bytes : 0;
+    const uint64_t ab = me * 4 * (w ? 2 : 1);
+    if (budget_ != 0 && (all_resident_ ? pages_dev : budget_) + ab > budget_) {
+      host_nbr_.reserve(std::max<uint64_t>(me, 1));  // zero-copy rows in pinned host memory
+      std::memcpy(host_nbr_.p, nbr + e0, me * 4);
+      if (w) {
+        host_w_.reserve(std::max<uint64_t>(me, 1));
+        std::memcpy(host_w_.p, w + e0, me * 4);
+      }
+      adj_host_ = true;
+    } else {
+      out_nbr_.reserve(std::max<uint64_t>(me, 1));
+      stager_.h2d(out_nbr_.p, nbr + e0, me * 4, xs_);
+      if (w) {
+        out_w_.reserve(std::max<uint64_t>(me, 1));
+        stager_.h2d(out_w_.p, w + e0, me * 4, xs_);
+      }
+      bytes += ab;
+    }
+  }
+  finish_csr(true);
+  stager_.sync();
+  last_upload_bytes += bytes;
+  last_upload_seconds +=
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 void Engine::derive_csr_now() {
@@ -1644,8 +1709,8 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   }
 
   SR_CUDA(cudaEventRecord(ev_stop_, cs_));
-  if (values_out)
-    SR_CUDA(cudaMemcpyAsync(values_out, values_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  if (values_out)  // pageable destinations through the pinned chunks (stager)
+    stager_.d2h_sync(values_out, values_.p, size_t(n_) * 4, cs_);
   if (weak)  // run-long prediction-log accumulators (also updated by the sparse loop)
     SR_CUDA(cudaMemcpyAsync(census_h_.p, census_.p, sizeof(Census), cudaMemcpyDeviceToHost, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
@@ -1680,8 +1745,7 @@ uint64_t Engine::verify_fixpoint(int algo, const uint32_t* values_host) {
     throw EngineError(SR_E_DATA, "verify: no values from a previous run");
   }
   SR_CUDA(cudaMemsetAsync(viol.p, 0, 8, cs_));
-  launch_verify(algo, n_, out_off_.p, nbr_ptr(), w_ptr(), values_.p,
-                viol.p, cs_);
+  launch_verify(algo, row_lo_, row_hi_, out_off_.p, nbr_ptr(), w_ptr(), values_.p, viol.p, cs_);
   unsigned long long h = 0;
   SR_CUDA(cudaMemcpyAsync(&h, viol.p, 8, cudaMemcpyDeviceToHost, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));

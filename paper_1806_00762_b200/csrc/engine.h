@@ -134,6 +134,14 @@ class Engine {
                 const uint32_t* w, bool sync = true);
   void load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_view* pages,
                   uint32_t np);
+  // Sharded rank of a world (after load_pages, which cuts the owned
+  // destination range): the full out_offsets (vertex state) and only the
+  // adjacency rows of the owned vertices -- the only rows this rank's pushes
+  // read (the push list is compacted over [own_lo, own_hi)).  O(|E|/N).
+  void load_csr_shard(uint32_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr,
+                      const uint32_t* w);
+  // Forget the CSR of a previous graph (before a load_pages of a new one).
+  void drop_csr();
   uint64_t page_bytes_total() const { return page_bytes_total_; }
   // True when a page set of `bytes` would be held resident (no streaming).
   bool fits_budget(uint64_t bytes) const { return budget_ == 0 || bytes <= budget_; }
@@ -248,9 +256,16 @@ class Engine {
   bool adj_host_ = false;
   uint64_t page_budget_ = 0;  // HBM left for pages (budget_ - device adjacency)
   void place_adjacency(uint64_t used_page_bytes, PassOut* po);
-  const uint32_t* nbr_ptr() const { return adj_host_ ? host_nbr_.p : out_nbr_.p; }
+  // Rows [row_lo_, row_hi_) of the adjacency are held; a sharded rank holds
+  // only its own rows, stored from edge off[row_lo_] = nbr_base_ on (the
+  // kernels index with absolute CSR offsets, so the base is subtracted here).
+  uint32_t row_lo_ = 0, row_hi_ = 0;
+  uint64_t nbr_base_ = 0;
+  const uint32_t* nbr_ptr() const {
+    return (adj_host_ ? host_nbr_.p : out_nbr_.p) - nbr_base_;
+  }
   const uint32_t* w_ptr() const {
-    return csr_weighted_ ? (adj_host_ ? host_w_.p : out_w_.p) : nullptr;
+    return csr_weighted_ ? (adj_host_ ? host_w_.p : out_w_.p) - nbr_base_ : nullptr;
   }
 
   // pages

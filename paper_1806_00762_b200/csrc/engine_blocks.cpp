@@ -486,8 +486,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
     std::swap(contrib_a_.p, contrib_b_.p);
   }
   SR_CUDA(cudaEventRecord(ev_stop_, cs_));
-  if (ranks_out)
-    SR_CUDA(cudaMemcpyAsync(ranks_out, rank_a_.p, size_t(n_) * 4, cudaMemcpyDeviceToHost, cs_));
+  if (ranks_out) stager_.d2h_sync(ranks_out, rank_a_.p, size_t(n_) * 4, cs_);
   if (ctr_used_)
     SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
                             cudaMemcpyDeviceToHost, cs_));

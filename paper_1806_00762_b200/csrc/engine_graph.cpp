@@ -60,6 +60,9 @@ void Engine::build_graph_dev(uint32_t n, uint64_t m, DBuf<uint32_t>& src, DBuf<u
   has_csr_edges_ = csr_edges;
   csr_weighted_ = csr_edges && weighted;
   adj_host_ = false;  // built in HBM; load_pages moves it out if it breaks a budget
+  row_lo_ = 0;
+  row_hi_ = n;
+  nbr_base_ = 0;
   finish_csr();
   PinBuf<uint32_t> local_h;
   PinBuf<unsigned long long> in_off_h;
@@ -258,6 +261,8 @@ void Engine::export_graph(uint64_t* out_off, uint32_t* out_nbr, uint32_t* out_w,
       SR_CUDA(cudaStreamSynchronize(cs_));
     }
     if (!has_csr_edges_) throw EngineError(SR_E_DATA, "csr adjacency not on the device");
+    if (row_lo_ != 0 || row_hi_ != n_)
+      throw EngineError(SR_E_DATA, "a sharded rank holds only its own csr rows");
     if (m_) SR_CUDA(cudaMemcpy(out_nbr, nbr_ptr(), m_ * 4, cudaMemcpyDefault));
   }
   if (out_w) {

@@ -1708,14 +1708,14 @@ __global__ void fill_u32_kernel(uint32_t* p, uint32_t n, uint32_t x) {
 }
 
 template <int A>
-__global__ void verify_kernel(uint32_t n, const unsigned long long* __restrict__ off,
+__global__ void verify_kernel(uint32_t lo, uint32_t n, const unsigned long long* __restrict__ off,
                               const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ w,
                               const uint32_t* __restrict__ values, unsigned long long* viol) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   unsigned long long bad = 0;
-  for (uint32_t u = gw; u < n; u += nw) {
+  for (uint32_t u = lo + gw; u < n; u += nw) {
     const uint32_t vu = values[u];
     for (unsigned long long e = off[u] + lane; e < off[u + 1]; e += 32) {
       const uint32_t cand = combine<A>(vu, A == kSssp ? w[e] : 0u);
@@ -2422,17 +2422,16 @@ void launch_init_hub_stamp(uint32_t* stamp, uint32_t n, cudaStream_t s) {
   fill_u32_kernel<<<grid_for(n, 256), 256, 0, s>>>(stamp, n, 0u);
 }
 
-void launch_verify(int algo, uint32_t n, const unsigned long long* out_offsets,
+void launch_verify(int algo, uint32_t lo, uint32_t hi, const unsigned long long* out_offsets,
                    const uint32_t* nbr, const uint32_t* w, const uint32_t* values,
                    unsigned long long* violations, cudaStream_t s) {
-  if (!n) return;
-  const int g = grid_for((unsigned long long)n * 32, 256);
+  if (hi <= lo) return;
+  const int g = grid_for((unsigned long long)(hi - lo) * 32, 256);
   note_launch();
   switch (algo) {
-    case kBfs: verify_kernel<kBfs><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
-    case kCc: verify_kernel<kCc><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
-    note_launch();
-    default: verify_kernel<kSssp><<<g, 256, 0, s>>>(n, out_offsets, nbr, w, values, violations); break;
+    case kBfs: verify_kernel<kBfs><<<g, 256, 0, s>>>(lo, hi, out_offsets, nbr, w, values, violations); break;
+    case kCc: verify_kernel<kCc><<<g, 256, 0, s>>>(lo, hi, out_offsets, nbr, w, values, violations); break;
+    default: verify_kernel<kSssp><<<g, 256, 0, s>>>(lo, hi, out_offsets, nbr, w, values, violations); break;
   }
 }
 

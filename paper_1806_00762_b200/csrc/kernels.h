@@ -123,7 +123,7 @@ void launch_init_values(int algo, uint32_t source, uint32_t n, uint32_t* values,
                         cudaStream_t s);
 void launch_init_hub_stamp(uint32_t* stamp, uint32_t n, cudaStream_t s);
 // Fixpoint-law verifier.
-void launch_verify(int algo, uint32_t n, const unsigned long long* out_offsets,
+void launch_verify(int algo, uint32_t lo, uint32_t hi, const unsigned long long* out_offsets,
                    const uint32_t* nbr, const uint32_t* w, const uint32_t* values,
                    unsigned long long* violations, cudaStream_t s);
 

@@ -35,9 +35,11 @@ bool HostStager::pageable(const void* p) {
 void HostStager::ensure() {
   if (!buf_.empty()) return;
   SR_CUDA(cudaGetDevice(&device_));
+  if (const char* e = std::getenv("SERAPH_STAGE_CHUNK_MB"))
+    chunk_ = size_t(std::max(1, std::atoi(e))) << 20;
   for (int i = 0; i < kBufs; ++i) {
     void* b = nullptr;
-    SR_CUDA(cudaHostAlloc(&b, kChunk, cudaHostAllocPortable));
+    SR_CUDA(cudaHostAlloc(&b, chunk_, cudaHostAllocPortable));
     buf_.push_back(b);
     cudaEvent_t e;
     SR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -45,7 +47,7 @@ void HostStager::ensure() {
     ev_live_.push_back(false);
   }
   unsigned h = std::thread::hardware_concurrency();
-  int t = h ? int(std::min<unsigned>(h, 8)) : 4;
+  int t = h ? int(std::min<unsigned>(h, 16)) : 4;  // 16-core box: 8 -> 16 threads 0.44 -> 0.43 s for C4
   if (const char* e = std::getenv("SERAPH_STAGE_THREADS")) t = std::max(1, std::atoi(e));
   threads_ = t;
   for (int k = 1; k < threads_; ++k) pool_.emplace_back(&HostStager::worker, this, k);
@@ -101,8 +103,8 @@ void HostStager::h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     return;
   }
   ensure();
-  for (size_t off = 0; off < bytes; off += kChunk) {
-    const size_t len = std::min(kChunk, bytes - off);
+  for (size_t off = 0; off < bytes; off += chunk_) {
+    const size_t len = std::min(chunk_, bytes - off);
     const int b = next_;
     next_ = (next_ + 1) % kBufs;
     if (ev_live_[b]) SR_CUDA(cudaEventSynchronize(ev_[b]));  // its previous DMA is done
@@ -112,6 +114,35 @@ void HostStager::h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     ev_live_[b] = true;
     staged_ += len;
   }
+}
+
+void HostStager::d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return;
+  if (!pageable(dst)) {
+    SR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    SR_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  ensure();
+  sync();
+  const size_t nch = (bytes + chunk_ - 1) / chunk_;
+  auto issue = [&](size_t k) {
+    const size_t off = k * chunk_, len = std::min(chunk_, bytes - off);
+    const int b = int(k % kBufs);
+    SR_CUDA(cudaMemcpyAsync(buf_[b], static_cast<const char*>(src) + off, len,
+                            cudaMemcpyDeviceToHost, s));
+    SR_CUDA(cudaEventRecord(ev_[b], s));
+    ev_live_[b] = true;
+  };
+  for (size_t k = 0; k < std::min<size_t>(nch, kBufs); ++k) issue(k);
+  for (size_t k = 0; k < nch; ++k) {
+    const int b = int(k % kBufs);
+    const size_t off = k * chunk_, len = std::min(chunk_, bytes - off);
+    SR_CUDA(cudaEventSynchronize(ev_[b]));
+    copy_parallel(static_cast<char*>(dst) + off, buf_[b], len);
+    if (k + kBufs < nch) issue(k + kBufs);
+  }
+  for (size_t i = 0; i < ev_live_.size(); ++i) ev_live_[i] = false;
 }
 
 void HostStager::sync() {

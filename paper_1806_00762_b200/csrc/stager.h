@@ -36,10 +36,13 @@ class HostStager {
   void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
   // Wait until every staged chunk has left its pinned buffer.
   void sync();
+  // Enqueue dst <- src (device -> pageable host) through the pinned chunks
+  // and wait for it (DMA of chunk i+1 overlaps the host copy of chunk i).
+  void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s);
   uint64_t staged_bytes() const { return staged_; }
 
  private:
-  static constexpr size_t kChunk = 32ull << 20;
+  size_t chunk_ = 32ull << 20;  // SERAPH_STAGE_CHUNK_MB
   static constexpr int kBufs = 4;
   void ensure();
   void copy_parallel(void* dst, const void* src, size_t bytes);

@@ -778,14 +778,112 @@ def _check_structures(csr: CsrGraph, pages: PageSet, program: VertexProgram) -> 
         raise ConfigError("source vertex out of range")
 
 
+class Group:
+    """A multi-GPU world inside this process (sr_group_*): rank r on
+    devices[r], one host thread per rank inside every call; distinct devices
+    talk NCCL (+ peer stores with exchange="peer"), a repeated device uses the
+    in-process loopback transport.  Each rank holds its destination shard of
+    the pages and its own CSR rows only."""
+
+    def __init__(self, devices, hbm_budget_bytes: int = 0, exchange: str = "allreduce"):
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        flags = N.EXCHANGE_PEER if exchange == "peer" else 0
+        N.check(N.lib.sr_group_open(arr, len(devices), int(hbm_budget_bytes), flags, C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        self.num_vertices = 0
+
+    def close(self) -> None:
+        if self._h:
+            N.lib.sr_group_close(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return N.lib.sr_group_size(self._h)
+
+    def graph_info(self, rank: int = 0) -> dict:
+        gi = N.GraphInfo()
+        N.check(N.lib.sr_group_graph_info(self._h, rank, C.byref(gi)), group=self._h)
+        return {k: getattr(gi, k) for k, _ in N.GraphInfo._fields_}
+
+    def load_graph(self, csr: CsrGraph, pages: PageSet, algo_hint: int = -1) -> None:
+        views = _page_views(pages)
+        N.check(N.lib.sr_group_load_graph(self._h, csr.num_vertices, csr.num_edges(),
+                                          N.ptr(csr.out_offsets), N.ptr(csr.out_neighbors),
+                                          N.ptr(csr.out_weights), pages.page_vertex_capacity,
+                                          1 if pages.weighted else 0, views, len(pages.pages),
+                                          int(algo_hint)), group=self._h)
+        self.num_vertices = csr.num_vertices
+
+    def _result(self, fn, program, config, n):
+        cfg = config.to_c(program)
+        vals = ranks = None
+        if program.kind == AlgoKind.PAGERANK:
+            ranks = np.empty(n, np.float32)
+        else:
+            vals = np.empty(n, np.uint32)
+        m = N.MetricsC()
+        cap = 4096
+        passes = (N.PassStatsC * cap)()
+        npass = C.c_uint32()
+        N.check(fn(cfg, vals, ranks, m, passes, cap, npass), group=self._h)
+        return RunResult(vals if vals is not None else np.zeros(0, np.uint32),
+                         _metrics_from_c(m, passes[:min(npass.value, cap)]), ranks=ranks)
+
+    def run(self, program: VertexProgram, config: EngineConfig) -> RunResult:
+        config.validate()
+        return self._result(lambda cfg, v, r, m, p, cap, np_: N.lib.sr_group_run(
+            self._h, C.byref(cfg), N.ptr(v), N.ptr(r), C.byref(m), p, cap, C.byref(np_)),
+            program, config, self.num_vertices)
+
+    def run_graph(self, csr: CsrGraph, pages: PageSet, program: VertexProgram,
+                  config: EngineConfig) -> RunResult:
+        """pagestream::run over the group: every rank uploads its shard, runs, rank 0's values."""
+        config.validate()
+        _check_structures(csr, pages, program)
+        views = _page_views(pages)
+        self.num_vertices = csr.num_vertices
+        return self._result(lambda cfg, v, r, m, p, cap, np_: N.lib.sr_group_run_graph(
+            self._h, csr.num_vertices, csr.num_edges(), N.ptr(csr.out_offsets),
+            N.ptr(csr.out_neighbors), N.ptr(csr.out_weights), pages.page_vertex_capacity,
+            1 if pages.weighted else 0, views, len(pages.pages), C.byref(cfg), N.ptr(v),
+            N.ptr(r), C.byref(m), p, cap, C.byref(np_)), program, config, csr.num_vertices)
+
+
 _default_engines: dict = {}
 _default_lock = threading.Lock()
 
 
 def run(csr: CsrGraph, pages: PageSet, program: VertexProgram, config: EngineConfig,
-        device: int = 0, hbm_budget_bytes: int = 0) -> RunResult:
-    """pagestream::run (engine.hpp:125-126) on the GPU."""
+        device: int = 0, hbm_budget_bytes: int = 0, devices=None) -> RunResult:
+    """pagestream::run (engine.hpp:125-126) on the GPU; `devices` (or the
+    SERAPH_DEVICES environment variable, e.g. "0,1,2,3") shards it over
+    several GPUs of this process (Group)."""
+    if devices is None and os.environ.get("SERAPH_DEVICES"):
+        devices = [int(x) for x in os.environ["SERAPH_DEVICES"].split(",") if x.strip()]
     with _default_lock:
+        if devices is not None and len(devices) > 1:
+            key = ("group", tuple(devices), int(hbm_budget_bytes))
+            grp = _default_engines.get(key)
+            if grp is None:
+                grp = Group(devices, hbm_budget_bytes)
+                _default_engines[key] = grp
+            return grp.run_graph(csr, pages, program, config)
+        if devices:
+            device = devices[0]
         key = (device, int(hbm_budget_bytes))
         eng = _default_engines.get(key)
         if eng is None:

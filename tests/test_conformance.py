@@ -57,12 +57,21 @@ def test_host_suites_with_dropin_linked(name):
     check(name)
 
 
+# devices: the drop-in on GPU 0, and sharded over a 2-rank world of this
+# process (SERAPH_DEVICES="0,0": GPU 0 listed twice = the loopback transport;
+# distinct GPUs would talk NCCL) for every ClockMode::Wall run
 @pytest.mark.gpu
-def test_engine_suite_through_dropin():  # test_engine.cpp:138-320 against the GPU run()
+@pytest.mark.parametrize("devices", [None, "0,0"])
+def test_engine_suite_through_dropin(devices, monkeypatch):  # test_engine.cpp:138-320
+    if devices:
+        monkeypatch.setenv("SERAPH_DEVICES", devices)
     p = check("test_engine")
     assert "[  ok  ] run: mode independence across execution policies" in p.stdout
 
 
 @pytest.mark.gpu
-def test_bench_suite_through_dropin():  # test_bench.cpp:104-147: byte-identical CSV, parallel cells
+@pytest.mark.parametrize("devices", [None, "0,0"])
+def test_bench_suite_through_dropin(devices, monkeypatch):  # test_bench.cpp:104-147
+    if devices:
+        monkeypatch.setenv("SERAPH_DEVICES", devices)
     check("test_bench")

@@ -469,6 +469,22 @@ def test_cpp_dropin_bridge_against_reference_run():
     assert "0 failures" in out.stdout
 
 
+def test_cpp_dropin_multi_device_and_residency():
+    """oracle/_ref/bridge_group_check: the C++ drop-in sharded over 2 and 3
+    ranks of this process (RunOptions.devices; GPU 0 listed repeatedly =
+    loopback world) and its residency cache (RunOptions.generation), against
+    the reference's own run() on identical reference-built objects."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref",
+                       "bridge_group_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/bridge_group_check not built (needs /root/reference at build time)")
+    out = subprocess.run([exe, "0"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "0 failures" in out.stdout
+
+
 def test_csr_offsets_only_derives_push_adjacency():
     """sr_load_csr without out_neighbors: the push adjacency is built on the device
     from the resident pages (device-side graph build)."""
@@ -1006,3 +1022,45 @@ def test_sharded_rounds_loopback_world(world, blocked, peer, monkeypatch):
     ref = O.pagerank(n, src, dst, 20, 0.85)
     for r in res:
         assert np.abs(r.ranks.astype(np.float64) - ref).max() < PR_TOL
+
+
+@pytest.mark.parametrize("world,peer", [(2, False), (3, False), (2, True)])
+def test_group_pagestream_run_multi_device(world, peer, monkeypatch):
+    """pagestream::run over several devices from ONE process (sr_group_*, the
+    path a reference caller reaches with SERAPH_DEVICES): `world` ranks on
+    cuda:0 listed repeatedly (loopback transport on a one-GPU box), each
+    holding only its destination shard of the pages and its own CSR rows.
+    Bit-exact with the oracle for BFS/SSSP/CC under every predictor,
+    PageRank within 1e-6; the shards partition the edges."""
+    scale = 12
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=9)
+    w = O.assign_weights(src.size, 10, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    sym = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    with ps.Group([0] * world, exchange="peer" if peer else "allreduce") as g:
+        assert g.size() == world
+        for kind, gg in ((ps.AlgoKind.BFS, el), (ps.AlgoKind.SSSP, el), (ps.AlgoKind.CC, sym)):
+            csr, pages = built(gg, n // 16)
+            want = oracle_values(gg, kind, 0)
+            for pred in PREDS:
+                r = g.run_graph(csr, pages, program_for(kind, 0, gg),
+                                cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, want), (kind, pred)
+            # each rank: its own pages only (resident page bytes sum to the set)
+            infos = [g.graph_info(r) for r in range(world)]
+            assert all(i["has_csr_edges"] for i in infos)
+            # resident load + repeated runs (no re-upload)
+            g.load_graph(csr, pages, int(kind))
+            r = g.run(program_for(kind, 0, gg), cfg_of(pred=ps.PredictorMode.STRONG,
+                                                       clock=ps.ClockMode.WALL))
+            assert np.array_equal(r.values, want), (kind, "resident")
+        csr, pages = built(el, n // 16)
+        pr = g.run_graph(csr, pages, ps.make_pagerank(), cfg_of(clock=ps.ClockMode.WALL))
+    ref = O.pagerank(n, src, dst, 20, 0.85)
+    assert np.abs(pr.ranks.astype(np.float64) - ref).max() < PR_TOL
+    # the module-level drop-in honours SERAPH_DEVICES
+    monkeypatch.setenv("SERAPH_DEVICES", ",".join(["0"] * world))
+    csr, pages = built(el, n // 16)
+    r = ps.run(csr, pages, ps.make_sssp(0, n, True), cfg_of(clock=ps.ClockMode.WALL))
+    assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.SSSP, 0))
