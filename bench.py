@@ -108,6 +108,11 @@ def config_name(a):
             "cc": "C4"}[a.algo]
 
 
+def m_est(a, n):
+    """|E| of the generated graph (symmetrize doubles the RMAT edges)."""
+    return n * a.edge_factor * (2 if a.symmetric else 1)
+
+
 def csc_bytes(a, n, m):
     """Σ page_bytes (graph.cpp:96-100) of the page set."""
     return ((n + a.pages) + m * (2 if a.weighted else 1)) * 4
@@ -327,27 +332,53 @@ def run_ours(a, rank, world, local_rank):
     # pages; PageRank never reads it (out-degrees only)
     csr_edges = False
     t0 = time.time()
-    eng = ps.Engine(local_rank, budget)
-    if world > 1:
-        eng.attach_world(rank, world, world_uid())
-        eng.set_exchange(a.exchange == "peer")
     gen = dict(seed=a.seed, weights=(1, 64, a.seed + 1) if a.weighted else None,
                symmetrize=a.symmetric, page_vertex_capacity=cap)
     arena = N.PinnedArena()
     host = None
-    if world == 1:
+    footprint = None
+    e2e_skip = None
+    if world == 1 and budget:
+        # out of core: the graph is built in a scratch context and exported to
+        # pinned host memory; the budgeted engine loads it from there, so its
+        # device footprint (cudaMemGetInfo delta) is the budget's honest test:
+        # pages + push adjacency <= budget, plus O(|V|) vertex state
+        with ps.Engine(local_rank) as scratch:
+            scratch.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=not pr, **gen)
+            host = scratch.export_graph(arena, csr_edges=not pr)
+        build_s = time.time() - t0
+        free0 = ps.device_info(local_rank)["free_mem"]
+        eng = ps.Engine(local_rank, budget)
+        eng.load_csr(host[0], with_edges=not pr)
+        eng.load_pages(host[1])
+        footprint = {"free_before": free0}
+    elif world == 1:
+        eng = ps.Engine(local_rank, budget)
         eng.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=csr_edges, **gen)
         build_s = time.time() - t0
         if need_host:  # the reference's run() also needs the push adjacency
             host = eng.export_graph(arena, csr_edges=need_cpu and not pr)
     else:
-        # a sharded rank holds only its own pages: the whole graph is built in a
-        # scratch context on this GPU, exported, and the shard loaded
-        with ps.Engine(local_rank) as scratch:
-            scratch.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=csr_edges, **gen)
-            host = scratch.export_graph(arena, csr_edges=False)
-        eng.load_csr(host[0], with_edges=False)
-        eng.load_pages(host[1])
+        eng = ps.Engine(local_rank, budget)
+        eng.attach_world(rank, world, world_uid())
+        eng.set_exchange(a.exchange == "peer")
+        # a sharded rank keeps only its shard: every rank generates the whole
+        # graph on its own GPU (seconds) and load_pages keeps the pages of its
+        # destination range and the CSR rows of its vertices (O(|E|/N))
+        if not a.no_e2e:
+            # the e2e leg needs the graph in host memory on every rank: only
+            # when world copies fit comfortably in this node's RAM
+            import psutil
+            need = (n + 1) * 8 + m_est(a, n) * 4 * (2 if a.weighted else 1) * (1 if pr else 2)
+            if world * need < 0.6 * psutil.virtual_memory().available:
+                with ps.Engine(local_rank) as scratch:
+                    scratch.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=not pr,
+                                           **gen)
+                    host = scratch.export_graph(arena, csr_edges=not pr)
+            else:
+                e2e_skip = (f"{world} host copies of the graph ({world * need / 2**30:.0f} GiB) "
+                            f"exceed 60 % of this node's available RAM")
+        eng.generate_graph(a.scale, a.edge_factor, *quad, csr_edges=not pr, **gen)
         build_s = time.time() - t0
     m = eng.graph_info()["num_edges"]
 
@@ -388,6 +419,20 @@ def run_ours(a, rank, world, local_rank):
     iters = a.pr_iters if pr else 1
     value = m * iters / step_s / 1e9
     launches = sum(r.metrics.kernel_launches for r in runs)
+
+    if footprint is not None:
+        # vertex state: values/next/snapshot, flags, frontier lists, stamps,
+        # out-degrees, u64 out-offsets and prefixes, PageRank vectors
+        vs = n * (4 * 3 + 3 + 4 * 4 + 4 + 8 * 2 + (4 * 5 if pr else 0))
+        used = footprint["free_before"] - ps.device_info(local_rank)["free_mem"]
+        gi = eng.graph_info()
+        footprint = {"device_bytes": int(used), "budget_bytes": budget,
+                     "vertex_state_bytes_est": int(vs),
+                     "within_budget_plus_vertex_state": bool(used <= budget + vs),
+                     "adjacency_on_host": bool(gi.get("adjacency_on_host", 0)),
+                     "page_bytes": int(csc_bytes(a, n, m)),
+                     "adjacency_bytes": 0 if pr else int(m * (8 if a.weighted else 4)),
+                     "how": "cudaMemGetInfo before the budgeted context vs after the timed runs"}
 
     # parity at full size: device fixpoint law + the run's value signature
     res = one(want=True)
@@ -450,9 +495,17 @@ def run_ours(a, rank, world, local_rank):
 
     # e2e: the public C-ABI one-shot call with pinned host buffers
     e2e = None
-    if not a.no_e2e:
-        # the CSR offsets only: the engine derives the push adjacency from the pages
-        csr = ps.CsrGraph(n, host[0].out_offsets, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    if e2e_skip:
+        e2e = {"value": None, "unit": "GTEPS", "skipped": e2e_skip}
+    elif not a.no_e2e:
+        # the CSR offsets only: the engine derives the push adjacency from the
+        # pages -- unless a budget keeps pages + adjacency from fitting: then the
+        # adjacency is passed and stays in pinned host memory (zero-copy pushes)
+        if (budget or world > 1) and not pr and host[0].out_neighbors.size:
+            csr = host[0]  # sharded ranks upload only their own rows of it
+        else:
+            csr = ps.CsrGraph(n, host[0].out_offsets, np.zeros(0, np.uint32),
+                              np.zeros(0, np.uint32))
         pages = host[1]
         e2e_eng = ps.Engine(local_rank, budget)
         if world > 1:
@@ -534,6 +587,7 @@ def run_ours(a, rank, world, local_rank):
                    "recovery": last.recovery_passes, "edges_read": last.edges_read},
         "wall_ms_per_step": round(wall / a.steps * 1e3, 4),
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
+        **({"device_footprint": footprint} if footprint else {}),
         "clocks": clocks, "parity": parity, "schedules": schedules,
         "instance": instance,
         "build": {"graph_build_s": round(build_s, 2),

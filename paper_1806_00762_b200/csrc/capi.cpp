@@ -239,6 +239,22 @@ int sr_run_graph(sr_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* off, const
     // host memory when it does not fit).  PageRank needs only the offsets.
     const uint64_t adj_bytes = m * 4 * (w ? 2 : 1);
     const bool pagerank = cfg->algo == SR_ALGO_PAGERANK;
+    if (ctx->eng->world() > 1) {  // sharded rank: its pages, then only its own CSR rows
+      ctx->eng->drop_csr();
+      ctx->eng->set_load_algo(cfg->algo);
+      ctx->eng->load_pages(n, cap, weighted, pages, np);
+      ctx->eng->load_csr_shard(n, m, off, pagerank ? nullptr : nbr, pagerank ? nullptr : w);
+      const double up =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      sr_metrics mm{};
+      std::vector<sr_pass_stats> passes;
+      ctx->eng->run(*cfg, values_out, ranks_out, mm, passes);
+      mm.upload_seconds = up;
+      mm.h2d_bytes += ctx->eng->last_upload_bytes;
+      if (metrics_out) *metrics_out = mm;
+      copy_passes(passes, per_pass, pcap, n_pass);
+      return;
+    }
     const bool derive = pagerank ||
                         (ctx->eng->world() == 1 && ctx->eng->fits_budget(page_bytes + adj_bytes));
     // the offsets DMA stays queued ahead of the page DMAs on the copy stream

@@ -487,6 +487,26 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     own_hi_ = cut_at(before[np] * uint64_t(rank_ + 1) / uint64_t(world_));
     if (rank_ == world_ - 1) own_hi_ = n;
   }
+  // ---- a sharded rank keeps only its own CSR rows (its pushes read no others)
+  if (world_ > 1 && has_csr_edges_ && !adj_host_ && n_ == n && row_lo_ == 0 && row_hi_ == n &&
+      m_ > 0) {
+    unsigned long long e0 = 0, e1 = 0;
+    SR_CUDA(cudaStreamSynchronize(xs_));
+    SR_CUDA(cudaMemcpy(&e0, out_off_.p + own_lo_, 8, cudaMemcpyDeviceToHost));
+    SR_CUDA(cudaMemcpy(&e1, out_off_.p + own_hi_, 8, cudaMemcpyDeviceToHost));
+    DBuf<uint32_t> nb, wb;
+    nb.reserve(std::max<uint64_t>(e1 - e0, 1));
+    SR_CUDA(cudaMemcpy(nb.p, out_nbr_.p + e0, (e1 - e0) * 4, cudaMemcpyDeviceToDevice));
+    if (csr_weighted_) {
+      wb.reserve(std::max<uint64_t>(e1 - e0, 1));
+      SR_CUDA(cudaMemcpy(wb.p, out_w_.p + e0, (e1 - e0) * 4, cudaMemcpyDeviceToDevice));
+    }
+    out_nbr_ = std::move(nb);
+    out_w_ = std::move(wb);
+    nbr_base_ = e0;
+    row_lo_ = own_lo_;
+    row_hi_ = own_hi_;
+  }
   // ---- residency: the whole (owned) page set in HBM when it fits ----
   uint64_t used_bytes = 0;
   std::vector<char> used(np, 0);

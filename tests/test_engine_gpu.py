@@ -1064,3 +1064,50 @@ def test_group_pagestream_run_multi_device(world, peer, monkeypatch):
     csr, pages = built(el, n // 16)
     r = ps.run(csr, pages, ps.make_sssp(0, n, True), cfg_of(clock=ps.ClockMode.WALL))
     assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.SSSP, 0))
+
+
+def test_sharded_run_graph_and_device_built_shards():
+    """The per-rank paths of a torchrun world, on loopback ranks of one GPU:
+    (1) sr_run_graph on an attached rank uploads its pages, then only its own
+    CSR rows (bench.py e2e at N > 1); (2) a graph generated on the device by
+    an attached rank keeps only its shard (load_pages trims the CSR rows)."""
+    import threading
+    scale, world = 12, 2
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=13)
+    w = O.assign_weights(src.size, 14, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    csr, pages = built(el, n // 16)
+    want = oracle_values(el, ps.AlgoKind.SSSP, 0)
+    engines = [ps.Engine(0) for _ in range(world)]
+    for r, e in enumerate(engines):
+        e.attach_loopback(r, world, "sharded-run-graph")
+    out, errs = [None] * world, []
+
+    def go(r):
+        try:
+            c = cfg_of(pred=ps.PredictorMode.STRONG, clock=ps.ClockMode.WALL)
+            out[r] = [engines[r].run_graph(csr, pages, ps.make_sssp(0, n, True), c)]
+            engines[r].generate_graph(scale, 16, seed=0, weights=(1, 64, 1),
+                                      page_vertex_capacity=n // 16, csr_edges=True)
+            out[r].append(engines[r].run(ps.make_sssp(0, n, True), c))
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    th = [threading.Thread(target=go, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    assert not errs, errs
+    for r in range(world):
+        assert np.array_equal(out[r][0].values, want), r
+    # the device-generated instance: compare with a single-context run
+    with ps.Engine(0) as one:
+        one.generate_graph(scale, 16, seed=0, weights=(1, 64, 1), page_vertex_capacity=n // 16,
+                           csr_edges=True)
+        ref = one.run(ps.make_sssp(0, n, True), cfg_of(clock=ps.ClockMode.WALL))
+    for r in range(world):
+        assert np.array_equal(out[r][1].values, ref.values), r
+    for e in engines:
+        e.close()
