@@ -438,7 +438,12 @@ def run_ours(a, rank, world, local_rank):
     res = one(want=True)
     parity = {}
     if not pr:
-        parity["fixpoint_violations"] = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
+        viol = eng.verify_fixpoint(ps.AlgoKind(algo), res.values)
+        if world > 1:  # a sharded rank checks its own CSR rows: sum over ranks
+            t = torch.tensor([viol], dtype=torch.int64, device=f"cuda:{local_rank}")
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            viol = int(t.item())
+        parity["fixpoint_violations"] = viol
         parity["signature"] = value_signature(algo, res.values)
         if algo != 1:
             parity["source_value"] = int(res.values[0])
