@@ -115,6 +115,7 @@ Engine::~Engine() {
   if (ev_stop_) cudaEventDestroy(ev_stop_);
   if (ev_step_) cudaEventDestroy(ev_step_);
   if (ev_tiles_) cudaEventDestroy(ev_tiles_);
+  if (ev_csr_) cudaEventDestroy(ev_csr_);
   for (auto& e : relax_ev_) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -572,6 +573,8 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     uint32_t first = np;
     for (uint32_t p = 0; p < np && first == np; ++p)
       if (used[p]) first = p;
+    if (!ev_csr_) SR_CUDA(cudaEventCreateWithFlags(&ev_csr_, cudaEventDisableTiming));
+    SR_CUDA(cudaEventRecord(ev_csr_, xs_));  // load_csr's offsets + out-degrees (queued first)
     if (first < np) copy_page(first);
     // 2) cut tiles on the host while that DMA runs, then the small uploads
     build_tiles(own_lo_, own_hi_, xs_);
@@ -581,9 +584,10 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
     SR_CUDA(cudaMemcpyAsync(page_desc_.p, desc_stage_.p, np * sizeof(PageDesc),
                             cudaMemcpyHostToDevice, xs_));
     SR_CUDA(cudaEventRecord(ev_tiles_, xs_));
-    for (uint32_t p = first + 1; p < np; ++p)
-      if (used[p]) copy_page(p);
-    // 3) device-side push adjacency, page by page as each copy lands
+    // 3) per-page device work as each copy lands, enqueued between the copies
+    //    (pageable inputs keep the host busy staging: the kernels of page p
+    //    must already be queued while page p+1 is being staged): the push
+    //    adjacency derivation and the source-blocked sub-pages
     if (csr_derived_) {
       has_csr_edges_ = false;
       csr_derived_ = false;
@@ -599,21 +603,34 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       csr_weighted_ = weighted;  // what the derivation will produce
     }
     SR_CUDA(cudaStreamWaitEvent(cs_, ev_tiles_, 0));
-    if (derive && m_) {
+    // source-blocked sub-pages for the run this load is for (sr_run_graph
+    // names it): decided from the out-degrees, built page by page
+    bool prebuild = false;
+    if (algo_hint >= 0 && world_ == 1 && has_csr_ && n_ == n && !std::getenv("SERAPH_NO_PREBUILD")) {
+      SR_CUDA(cudaStreamWaitEvent(cs_, ev_csr_, 0));
+      const uint64_t blk = algo_hint == SR_ALGO_PAGERANK ? pr_block_verts() : pull_block_verts();
+      prebuild = blk && sb_begin(blk);
+    }
+    const bool derive_now = derive && m_;
+    if (derive_now) {
       out_nbr_.reserve(m_);
       if (weighted) out_w_.reserve(m_);
       csr_cursor_.reserve(n_);
       SR_CUDA(cudaMemcpyAsync(csr_cursor_.p, out_off_.p, size_t(n_) * 8,
                               cudaMemcpyDeviceToDevice, cs_));
-      for (uint32_t p = 0; p < np; ++p) {
-        if (!used[p]) continue;
-        SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
+    }
+    for (uint32_t p = first; p < np; ++p) {
+      if (!used[p]) continue;
+      if (p != first) copy_page(p);
+      if (!derive_now && !prebuild) continue;
+      SR_CUDA(cudaStreamWaitEvent(cs_, page_events_[p], 0));
+      if (derive_now)
         launch_csr_from_pages(tiles_.p, tile_page_.p, page_desc_.p, pages_[p].tile_begin,
                               pages_[p].tile_end, csr_cursor_.p, out_nbr_.p,
                               weighted ? out_w_.p : nullptr, sm_count_ * 8, cs_);
-      }
-      SR_CUDA(cudaGetLastError());
+      if (prebuild) sb_page(p);
     }
+    SR_CUDA(cudaGetLastError());
     if (derive) {
       has_csr_edges_ = true;
       csr_weighted_ = weighted;
@@ -633,6 +650,7 @@ void Engine::load_pages(uint32_t n, uint32_t cap, bool weighted, const sr_page_v
       SR_CUDA(cudaStreamSynchronize(cs_));
       weights_ge1_ = bad == 0;
     }
+    if (prebuild) sb_finish();
     SR_CUDA(cudaStreamSynchronize(xs_));  // host buffers are borrowed only for the call
     for (auto& pm : pages_) pm.h_offs = pm.h_src = pm.h_w = nullptr;
   } else {

@@ -222,6 +222,7 @@ class Engine {
   void build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st);
   std::vector<cudaEvent_t> page_events_;  // resident upload: copy done per page
   cudaEvent_t ev_tiles_ = nullptr;
+  cudaEvent_t ev_csr_ = nullptr;  // load_csr's work on the copy stream (before the pages)
   PinBuf<uint4> tile_stage_;
   PinBuf<uint32_t> tile_page_stage_, hub_stage_;
   PinBuf<PageDesc> desc_stage_;
@@ -373,7 +374,9 @@ class Engine {
     // cudaMalloc/cudaFree of them cost more than the build kernels)
     DBuf<uint32_t> t_cnt, t_tcnt, t_tat;
     DBuf<unsigned char> t_scan;
-    DBuf<unsigned long long> t_goff;
+    DBuf<unsigned long long> t_goff, bp_edges, bp_base;
+    std::vector<unsigned long long> page_base;
+    bool pending = false;  // sb_begin done, sb_finish not yet
     DBuf<uint4> tiles;
     DBuf<uint32_t> tile_page;
     DBuf<PageDesc> desc;
@@ -381,6 +384,9 @@ class Engine {
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
   } sb_;
   bool build_src_blocks(uint64_t blk_verts);
+  bool sb_begin(uint64_t blk_verts);  // layout + buffers (page-major sub-pages)
+  void sb_page(uint32_t p);           // page p's sub-pages (enqueued on cs_)
+  bool sb_finish();                   // tile cut + descriptors (syncs cs_)
   // K8 hot-source staging (pr_pull_kernel<true>): the highest out-degree
   // sources' contributions live in shared memory; K8 reads an encoded copy
   // of its source array (hot sources -> kHotBit | slot) through its own page
@@ -398,6 +404,7 @@ class Engine {
   } pr_hot_;
   bool prepare_pr_hot(bool blocked);
   uint64_t pull_block_verts();
+  uint64_t pr_block_verts() const;  // K8 source-block size (0: unblocked)
   double hot_source_coverage(uint64_t k);
   double coverage_ = -1;
   uint64_t coverage_k_ = 0;

@@ -20,64 +20,79 @@ namespace seraph {
 // ---------------------------------------------------------------------------
 bool Engine::build_src_blocks(uint64_t blk) {
   if (sb_.built && sb_.blk_verts == blk) return true;
-  if (!all_resident_) return false;  // sharded ranks block their own destinations
-  if (blk == 0 || n_ <= blk) return false;
+  if (!sb_begin(blk)) return false;
+  for (uint32_t p = 0; p < pages_.size(); ++p) sb_page(p);
+  return sb_finish();
+}
+
+// Page-major layout: sub-page (p, b) at page_base[p] + sum_{b'<b} pad8(edges(p, b')),
+// page_base[p] = sum_{q<p} (pad8(edges(q)) + 8 * n_blocks), all 32 B aligned
+// (K1/K8 read aligned uint4 runs): every page's sub-pages are
+// built from that page alone (sb_page), so sr_run_graph builds them page by
+// page while the rest of the page set is still crossing the host link.
+bool Engine::sb_begin(uint64_t blk) {
   sb_.built = false;
+  sb_.pending = false;
   if (pr_hot_.blocked) pr_hot_.built = false;
+  if (!all_resident_) return false;  // sharded ranks block their own destinations
+  if (blk == 0 || n_ <= blk || page_n_ != n_) return false;
   const uint32_t np = uint32_t(pages_.size());
   for (uint32_t p = 0; p < np; ++p)
     if (pages_[p].vb != uint64_t(p) * cap_) return false;  // uniform cut (graph.cpp:75-92)
   const uint32_t nb = uint32_t((n_ + blk - 1) / blk);
-  uint32_t n_tiles = 0;  // a sharded rank holds tiles for its own pages only
-  for (const PageMeta& pm : pages_) n_tiles = std::max(n_tiles, pm.tile_end);
-  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
-  auto t_last = std::chrono::steady_clock::now();
-  auto stage = [&](const char* what) {
-    if (!timing) return;
-    SR_CUDA(cudaStreamSynchronize(cs_));
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[seraph] src blocks %s: %.1f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t_last).count());
-    t_last = now;
-  };
-  // 1) counts per (block, destination)
-  DBuf<uint32_t>& cnt = sb_.t_cnt;
-  cnt.reserve(size_t(nb) * n_);
-  SR_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(nb) * n_ * 4, cs_));
-  launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
-  // 2) page-local offsets per sub-page, sub-page sizes
-  DBuf<unsigned long long>& goff = sb_.t_goff;
-  DBuf<unsigned long long> bp_edges, bp_base;
-  goff.reserve(size_t(nb) * n_);
-  bp_edges.reserve(size_t(nb) * np);
-  bp_base.reserve(size_t(nb) * np);
-  stage("count");
-  launch_src_block_scan(cnt.p, goff.p, page_desc_.p, np, nb, n_, bp_edges.p, cs_);
-  stage("scan");
-  std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
-  SR_CUDA(cudaMemcpyAsync(edges_h.data(), bp_edges.p, edges_h.size() * 8, cudaMemcpyDeviceToHost, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
+  sb_.page_base.assign(np, 0);
   unsigned long long at = 0;
-  for (size_t k = 0; k < edges_h.size(); ++k) {  // block-major, 32 B aligned sub-pages
-    base_h[k] = at;
-    at += (edges_h[k] + 7) & ~7ull;
-    if (edges_h[k] > 0xffffffffull) return false;
+  for (uint32_t p = 0; p < np; ++p) {
+    sb_.page_base[p] = at;
+    if (pages_[p].tile_end > pages_[p].tile_begin) at += pad8(pages_[p].edges) + 8ull * nb;
   }
+  sb_.t_cnt.reserve(size_t(nb) * n_);
+  sb_.t_goff.reserve(size_t(nb) * n_);
+  sb_.bp_edges.reserve(size_t(nb) * np);
+  sb_.bp_base.reserve(size_t(nb) * np);
+  SR_CUDA(cudaMemsetAsync(sb_.bp_edges.p, 0, size_t(nb) * np * 8, cs_));
+  SR_CUDA(cudaMemsetAsync(sb_.bp_base.p, 0, size_t(nb) * np * 8, cs_));
   sb_.src.reserve(at + 8);
   if (weighted_) sb_.w.reserve(at + 8);
   else sb_.w.release();
-  SR_CUDA(cudaMemcpyAsync(bp_base.p, base_h.data(), base_h.size() * 8, cudaMemcpyHostToDevice, cs_));
-  // 3) u32 local offsets of every sub-page (from the page-local goff)
   const size_t per_block = size_t(n_) + np;
   sb_.offs.reserve(size_t(nb) * per_block);
-  launch_src_block_offs(n_, cap_, np, nb, goff.p, bp_edges.p, sb_.offs.p, cs_);
-  // 4) scatter the sources: goff becomes absolute cursors (one atomic per edge)
-  launch_src_block_abs(goff.p, n_, cap_, np, nb, bp_base.p, cs_);
-  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, 0, n_tiles, n_, uint32_t(blk), np,
-                   nullptr, goff.p, sb_.src.p, weighted_ ? sb_.w.p : nullptr, sm_count_ * 8, cs_);
-  stage("scatter");
-  // 5) the tile cut on the device
+  sb_.blk_verts = uint32_t(blk);
+  sb_.n_blocks = nb;
+  sb_.pending = true;
+  return true;
+}
+
+void Engine::sb_page(uint32_t p) {
+  const PageMeta& pm = pages_[p];
+  if (pm.tile_end <= pm.tile_begin) return;  // not this rank's / no in-edges
+  const uint32_t nb = sb_.n_blocks, np = uint32_t(pages_.size());
+  const uint32_t range = pm.ve - pm.vb;
+  // 1) counts per (block, destination) of this page
+  SR_CUDA(cudaMemset2DAsync(sb_.t_cnt.p + pm.vb, size_t(n_) * 4, 0, size_t(range) * 4, nb, cs_));
+  launch_src_block(0, tiles_.p, tile_page_.p, page_desc_.p, pm.tile_begin, pm.tile_end, n_,
+                   sb_.blk_verts, np, sb_.t_cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
+  // 2) page-local offsets, sub-page sizes and bases, u32 offsets, cursors
+  launch_src_block_page(sb_.t_cnt.p, sb_.t_goff.p, page_desc_.p, p, pm.vb, range, n_, cap_, np,
+                        nb, sb_.page_base[p], sb_.bp_edges.p, sb_.bp_base.p, sb_.offs.p, cs_);
+  // 3) scatter the sources (one atomic per edge on the cursors)
+  launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, pm.tile_begin, pm.tile_end, n_,
+                   sb_.blk_verts, np, nullptr, sb_.t_goff.p, sb_.src.p,
+                   weighted_ ? sb_.w.p : nullptr, sm_count_ * 8, cs_);
+}
+
+bool Engine::sb_finish() {
+  if (!sb_.pending) return sb_.built;
+  sb_.pending = false;
+  const uint32_t nb = sb_.n_blocks, np = uint32_t(pages_.size());
+  const bool timing = std::getenv("SERAPH_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<unsigned long long> edges_h(size_t(nb) * np), base_h(size_t(nb) * np);
+  SR_CUDA(cudaMemcpyAsync(edges_h.data(), sb_.bp_edges.p, edges_h.size() * 8,
+                          cudaMemcpyDeviceToHost, cs_));
+  SR_CUDA(cudaMemcpyAsync(base_h.data(), sb_.bp_base.p, base_h.size() * 8, cudaMemcpyDeviceToHost,
+                          cs_));
+  // the tile cut on the device (per 128-destination window of every sub-page)
   const size_t K = sub_tile_windows(cap_, np, nb);
   const size_t K_blk = K / nb;  // windows per block
   DBuf<uint32_t>& tcnt = sb_.t_tcnt;
@@ -100,7 +115,7 @@ bool Engine::build_src_blocks(uint64_t blk) {
   launch_sub_tiles(1, n_, cap_, np, nb, own_lo_, own_hi_, sb_.offs.p, nullptr, tat.p, sb_.tiles.p,
                    sb_.tile_page.p, cs_);
   SR_CUDA(cudaGetLastError());
-  stage("offsets + tile cut");
+  const size_t per_block = size_t(n_) + np;
   std::vector<PageDesc> desc(size_t(nb) * np);
   for (uint32_t b = 0; b < nb; ++b)
     for (uint32_t p = 0; p < np; ++p) {
@@ -115,11 +130,13 @@ bool Engine::build_src_blocks(uint64_t blk) {
   sb_.desc.reserve(desc.size());
   SR_CUDA(cudaMemcpyAsync(sb_.desc.p, desc.data(), desc.size() * sizeof(PageDesc),
                           cudaMemcpyHostToDevice, cs_));
-  SR_CUDA(cudaStreamSynchronize(cs_));
   sb_.acc.reserve(n_);
-  SR_CUDA(cudaMemset(sb_.acc.p, 0, size_t(n_) * 4));
-  sb_.blk_verts = uint32_t(blk);
-  sb_.n_blocks = nb;
+  SR_CUDA(cudaMemsetAsync(sb_.acc.p, 0, size_t(n_) * 4, cs_));
+  SR_CUDA(cudaStreamSynchronize(cs_));
+  if (timing)
+    std::fprintf(stderr, "[seraph] src blocks finish (after the last page): %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                     .count());
   sb_.built = true;
   return true;
 }
@@ -148,6 +165,12 @@ uint64_t Engine::pull_block_verts() {
   if (env) return blk;
   if (uint64_t(n_) * 4 <= uint64_t(l2_bytes_) / 2) return 0;
   return hot_source_coverage(uint64_t(l2_bytes_) / 8) < 0.5 ? blk : 0;
+}
+
+uint64_t Engine::pr_block_verts() const {
+  uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
+  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
+  return pr_blk < n_ ? pr_blk : 0;
 }
 
 // Fraction of the edges whose source is among the k highest out-degree
@@ -420,9 +443,7 @@ bool Engine::prepare_pr_hot(bool blocked) {
 // ---------------------------------------------------------------------------
 void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics& m,
                           std::vector<sr_pass_stats>& passes) {
-  uint64_t pr_blk = 32ull << 20;  // tools/pr_blocks.py: 32 Mi best on RMAT-26, smaller lose
-  if (const char* e = std::getenv("SERAPH_PR_BLOCK_VERTS")) pr_blk = std::strtoull(e, nullptr, 10);
-  const bool blocked = build_src_blocks(pr_blk);
+  const bool blocked = build_src_blocks(pr_block_verts());
   const bool hot = prepare_pr_hot(blocked);
   const auto wall0 = std::chrono::steady_clock::now();
   SR_CUDA(cudaEventRecord(ev_start_, cs_));

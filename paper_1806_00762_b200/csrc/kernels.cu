@@ -620,7 +620,7 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
     const size_t k = size_t(b) * n + v;
     if (mode == 0) {
       atomicAdd(cnt + k, 1u);
-    } else {  // goff holds absolute cursors (src_block_abs_kernel)
+    } else {  // goff holds absolute cursors (src_block_page_fix_kernel)
       const unsigned long long o = atomicAdd(goff + k, 1ull);
       out_src[o] = s;
       if (out_w) out_w[o] = *wp;
@@ -692,11 +692,14 @@ __global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __
                                                               unsigned long long* goff,
                                                               const PageDesc* __restrict__ pages,
                                                               uint32_t n_pages, uint32_t n,
-                                                              unsigned long long* bp_edges) {
+                                                              unsigned long long* bp_edges,
+                                                              uint32_t p_only) {
   __shared__ unsigned long long s_w[32];
   __shared__ unsigned long long s_carry;
-  const uint32_t pb = blockIdx.x;  // = b * n_pages + p
-  const uint32_t p = pb % n_pages, b = pb / n_pages;
+  // one thread block per (block, page): all pages, or the blocks of page p_only
+  const uint32_t p = p_only != kNone ? p_only : blockIdx.x % n_pages;
+  const uint32_t b = p_only != kNone ? blockIdx.x : blockIdx.x / n_pages;
+  const uint32_t pb = b * n_pages + p;
   const PageDesc pd = pages[p];
   const size_t base = size_t(b) * n + pd.vertex_begin;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -721,20 +724,6 @@ __global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __
     __syncthreads();
   }
   if (threadIdx.x == 0) bp_edges[pb] = s_carry;
-}
-
-// Page-local sub-page offsets -> absolute scatter cursors into the
-// sub-page source array: goff[b*n + v] += base of sub-page (page(v), b).
-__global__ void src_block_abs_kernel(unsigned long long* goff, uint32_t n, uint32_t cap,
-                                     uint32_t n_pages, uint32_t n_blocks,
-                                     const unsigned long long* __restrict__ bp_base) {
-  const size_t total = size_t(n_blocks) * n;
-  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
-       k += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t b = uint32_t(k / n), v = uint32_t(k % n);
-    const uint32_t p = min(v / cap, n_pages - 1);
-    goff[k] += bp_base[size_t(b) * n_pages + p];
-  }
 }
 
 __global__ void pr_block_finalize_kernel(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
@@ -2227,32 +2216,6 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                                                   n, blk_verts, n_pages, cnt, goff, out_src, out_w);
 }
 
-void launch_src_block_abs(unsigned long long* goff, uint32_t n, uint32_t cap, uint32_t n_pages,
-                          uint32_t n_blocks, const unsigned long long* bp_base, cudaStream_t s) {
-  if (!n || !n_pages || !n_blocks) return;
-  note_launch();
-  src_block_abs_kernel<<<148 * 8, 256, 0, s>>>(goff, n, cap, n_pages, n_blocks, bp_base);
-}
-
-__global__ void src_block_offs_kernel(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
-                                      const unsigned long long* __restrict__ goff,
-                                      const unsigned long long* __restrict__ bp_edges,
-                                      uint32_t* offs) {
-  // sub-page (p, b) local offsets live at b*(n + n_pages) + p*cap + p
-  const size_t total = size_t(n_blocks) * (size_t(n) + n_pages);
-  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
-       k += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t b = uint32_t(k / (size_t(n) + n_pages));
-    const uint32_t r = uint32_t(k % (size_t(n) + n_pages));  // = p*cap + p + i
-    const uint32_t p = r / (cap + 1) < n_pages ? r / (cap + 1) : n_pages - 1;
-    const uint32_t i = r - p * (cap + 1);
-    const uint32_t vb = p * cap;
-    const uint32_t range = min(cap, n - vb);
-    if (i < range) offs[k] = uint32_t(goff[size_t(b) * n + vb + i]);
-    else if (i == range) offs[k] = uint32_t(bp_edges[size_t(b) * n_pages + p]);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Device tile cut of the source-blocked sub-pages (replaces the host cut for
 // them: no |V| x blocks offsets round trip).  The cut_tiles rule of the
@@ -2379,19 +2342,57 @@ void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, 
   note_launch(2);
 }
 
-void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
-                           const unsigned long long* goff, const unsigned long long* bp_edges,
-                           uint32_t* offs, cudaStream_t s) {
-  note_launch();
-  src_block_offs_kernel<<<148 * 8, 256, 0, s>>>(n, cap, n_pages, n_blocks, goff, bp_edges, offs);
+// ---- page-major per-page build (Engine::sb_page): sub-page (p, b) lives at
+// page_base + sum_{b' < b} pad8(edges(p, b')), so page p's sub-pages are
+// built from page p alone, as soon as its DMA has landed ----
+__global__ void src_block_page_base_kernel(uint32_t p, uint32_t n_pages, uint32_t n_blocks,
+                                           unsigned long long page_base,
+                                           const unsigned long long* __restrict__ bp_edges,
+                                           unsigned long long* bp_base) {
+  if (threadIdx.x != 0) return;
+  unsigned long long at = page_base;
+  for (uint32_t b = 0; b < n_blocks; ++b) {
+    bp_base[size_t(b) * n_pages + p] = at;
+    at += (bp_edges[size_t(b) * n_pages + p] + 7) & ~7ull;
+  }
 }
 
-void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
-                           uint32_t n_pages, uint32_t n_blocks, uint32_t n,
-                           unsigned long long* bp_edges, cudaStream_t s) {
-  if (!n_pages || !n_blocks) return;
-  note_launch();
-  src_block_scan_kernel<<<n_pages * n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges);
+// page p: u32 sub-page local offsets from the page-local goff, then goff +=
+// the sub-page base (absolute scatter cursors)
+__global__ void src_block_page_fix_kernel(uint32_t p, uint32_t vb, uint32_t range, uint32_t n,
+                                          uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
+                                          unsigned long long* goff,
+                                          const unsigned long long* __restrict__ bp_edges,
+                                          const unsigned long long* __restrict__ bp_base,
+                                          uint32_t* offs) {
+  const size_t per = size_t(range) + 1;
+  const size_t total = size_t(n_blocks) * per;
+  for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
+       k += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(k / per), i = uint32_t(k % per);
+    uint32_t* o = offs + size_t(b) * (size_t(n) + n_pages) + size_t(p) * cap + p;
+    if (i < range) {
+      const size_t g = size_t(b) * n + vb + i;
+      const unsigned long long x = goff[g];
+      o[i] = uint32_t(x);
+      goff[g] = x + bp_base[size_t(b) * n_pages + p];
+    } else {
+      o[range] = uint32_t(bp_edges[size_t(b) * n_pages + p]);
+    }
+  }
+}
+
+void launch_src_block_page(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
+                           uint32_t p, uint32_t vb, uint32_t range, uint32_t n, uint32_t cap,
+                           uint32_t n_pages, uint32_t n_blocks, unsigned long long page_base,
+                           unsigned long long* bp_edges, unsigned long long* bp_base,
+                           uint32_t* offs, cudaStream_t s) {
+  if (!n_blocks) return;
+  note_launch(3);
+  src_block_scan_kernel<<<n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges, p);
+  src_block_page_base_kernel<<<1, 32, 0, s>>>(p, n_pages, n_blocks, page_base, bp_edges, bp_base);
+  src_block_page_fix_kernel<<<grid_for(uint64_t(n_blocks) * (range + 1), 256), 256, 0, s>>>(
+      p, vb, range, n, cap, n_pages, n_blocks, goff, bp_edges, bp_base, offs);
 }
 
 void launch_pr_block_finalize(uint32_t lo, uint32_t hi, float* acc, float* rank_out,

@@ -79,9 +79,14 @@ void launch_src_block(int mode, const uint4* tiles, const uint32_t* tile_page,
                       uint32_t blk_verts, uint32_t n_pages, uint32_t* cnt,
                       unsigned long long* goff, uint32_t* out_src, uint32_t* out_w, int grid,
                       cudaStream_t s);
-// goff (page-local sub-page offsets) += sub-page bases: absolute scatter cursors
-void launch_src_block_abs(unsigned long long* goff, uint32_t n, uint32_t cap, uint32_t n_pages,
-                          uint32_t n_blocks, const unsigned long long* bp_base, cudaStream_t s);
+// Page-major per-page build of the sub-pages of page p (after its count):
+// scan, sub-page bases, u32 local offsets and absolute scatter cursors.
+void launch_src_block_page(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
+                           uint32_t p, uint32_t vb, uint32_t range, uint32_t n, uint32_t cap,
+                           uint32_t n_pages, uint32_t n_blocks, unsigned long long page_base,
+                           unsigned long long* bp_edges, unsigned long long* bp_base,
+                           uint32_t* offs, cudaStream_t s);
+
 // Tile cut of the source-blocked sub-pages on the device, one 128-destination
 // window per thread: mode 0 writes the tile count of every window to cnt
 // (sub_tile_windows entries, block-major); mode 1 writes the tiles at the
@@ -109,12 +114,8 @@ void launch_queue_prep(const uint32_t* list, uint32_t q, const uint32_t* outdeg,
 size_t exclusive_scan_u32_temp_bytes(size_t count);
 void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, void* tmp,
                                size_t tmp_bytes, cudaStream_t s);
-void launch_src_block_offs(uint32_t n, uint32_t cap, uint32_t n_pages, uint32_t n_blocks,
-                           const unsigned long long* goff, const unsigned long long* bp_edges,
-                           uint32_t* offs, cudaStream_t s);
-void launch_src_block_scan(const uint32_t* cnt, unsigned long long* goff, const PageDesc* pages,
-                           uint32_t n_pages, uint32_t n_blocks, uint32_t n,
-                           unsigned long long* bp_edges, cudaStream_t s);
+
+
 void launch_pr_block_finalize(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
                               float* contrib_out, const float* inv_outdeg, float base, float damp,
                               cudaStream_t s);
