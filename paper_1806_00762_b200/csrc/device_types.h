@@ -107,6 +107,16 @@ struct PullArgs {
   uint32_t grab;       // tiles per work-counter grab (0 = kGrab)
 };
 
+// K2 (pull_reentry_kernel): up to `runs` runs of one page set in one
+// cooperative launch; run r uses work[r] and ctr[r * ctr_stride ...].
+struct ReentryArgs {
+  unsigned* work;
+  RunCtr* ctr;
+  uint32_t ctr_stride;  // counters per run (pages of the set, per-page gating)
+  uint32_t runs;        // MRT
+  uint32_t* runs_done;  // runs actually executed (device -> host)
+};
+
 struct PrArgs {
   unsigned* work;  // per-launch tile counter
   const uint4* tiles;

@@ -953,6 +953,81 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
   return RunStats{};
 }
 
+// K2 launch: `runs` reentry runs of a resident page set in one cooperative
+// kernel (pull_reentry_kernel).  False when the set needs more than one
+// launch segment or the grid cannot be co-resident: the host loop runs it.
+bool Engine::reentry_on_device(const std::vector<uint32_t>& pages, int gate, int runs,
+                               bool per_page) {
+  Segments seg{};
+  uint32_t last_end = 0xffffffffu;
+  for (uint32_t p : pages) {
+    const PageMeta& pm = pages_[p];
+    if (pm.tile_end <= pm.tile_begin) continue;
+    if (seg.n > 0 && pm.tile_begin == last_end) {
+      seg.task_prefix[seg.n] += pm.tile_end - pm.tile_begin;
+    } else {
+      if (seg.n == kMaxSegments) return false;
+      seg.tile_begin[seg.n] = pm.tile_begin;
+      seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (pm.tile_end - pm.tile_begin);
+      ++seg.n;
+    }
+    last_end = pm.tile_end;
+  }
+  if (seg.n == 0) return true;
+  const uint32_t np = uint32_t(pages_.size());
+  const size_t stride = per_page ? std::max<size_t>(np, 1) : 1;
+  if (size_t(ctr_used_) + stride * runs > ctr_.n) return false;
+  if (work_used_ + size_t(runs) > work_.n || !work_.p) {  // contiguous, zeroed counters
+    next_work_counter();
+    if (work_used_ + size_t(runs) > work_.n) {
+      SR_CUDA(cudaMemsetAsync(work_.p, 0, work_.n * sizeof(unsigned), cs_));
+      work_used_ = 0;
+    }
+  }
+  unsigned* work = work_.p + work_used_;
+  work_used_ += runs;
+  if (!runs_done_.p) runs_done_.reserve(1);
+  const uint32_t tasks = seg.task_prefix[seg.n];
+  const int grid = std::max(1, int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                                      (uint64_t(tasks) + kWarpsPerBlock - 1) /
+                                                          kWarpsPerBlock)));
+  PullArgs a{};
+  a.work = work;
+  a.tiles = tiles_.p;
+  a.tile_page = tile_page_.p;
+  a.pages = page_desc_.p;
+  a.seg = seg;
+  a.values = values_.p;
+  a.next = values_.p;
+  a.changed = changed_.p;
+  a.status = status_.p;
+  a.hub_stamp = hub_stamp_.p;
+  a.run_id = run_id_ + 1;
+  a.ctr_per_page = per_page ? 1u : 0u;
+  a.census = census_.p;
+  a.count_dest = 1;
+  a.count_valid = 1;
+  a.peers = peer_list();
+  a.n_peers = n_peers_;
+  a.k_bfs = k_bfs_;
+  a.s_cc = s_cc_;
+  a.l_sssp = l_sssp_;
+  a.src_floor = floor_sssp_;
+  a.floor_step = weights_ge1_ ? 1u : 0u;
+  a.grab = k1_grab(tasks, grid, "SERAPH_K1_GRAB");
+  ReentryArgs r{work, ctr_.p + ctr_used_, uint32_t(stride), uint32_t(runs), runs_done_.p};
+  auto* evp = relax_begin();
+  if (!launch_pull_reentry(algo_, gate, a, r, grid, cs_)) {
+    if (evp) --relax_ev_used_;
+    return false;
+  }
+  SR_CUDA(cudaGetLastError());
+  if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+  ctr_used_ += uint32_t(stride * runs);
+  run_id_ += uint32_t(runs);
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // Dense pass, device-native schedule (ClockMode::Wall)
 // ---------------------------------------------------------------------------
@@ -1089,6 +1164,13 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
         if (pages_[p].slot >= 0) SR_CUDA(cudaStreamWaitEvent(cs_, slots_[pages_[p].slot].ready, 0));
     }
     const bool per_page = st.gated && st.pages.size() > 1;
+    // K2: the reentry runs of a resident set loop on the device (one
+    // cooperative launch, stops at the first quiet run)
+    if (st.gated && st.reps > 1 && !stream && !pagerank && !record_trace_ &&
+        !std::getenv("SERAPH_NO_K2") && reentry_on_device(st.pages, gate, st.reps, per_page)) {
+      po.kernel_runs += st.pages.size() * size_t(st.reps);
+      continue;
+    }
     RunCtr* prev = nullptr;
     for (int r = 0; r < st.reps; ++r) {
       RunCtr* slot = alloc_ctr(per_page ? std::max<size_t>(np, 1) : 1);

@@ -191,6 +191,8 @@ class Engine {
   RunStats launch_pages(const std::vector<uint32_t>& pages, int gate, bool det, RunCtr* ctr,
                         const RunCtr* prev, bool per_page, bool pagerank);
   void push_pass(const sr_run_config& cfg, RunStats& st);
+  bool reentry_on_device(const std::vector<uint32_t>& pages, int gate, int runs, bool per_page);
+  DBuf<uint32_t> runs_done_;  // K2: runs the last cooperative reentry launch executed
   void census(int pass_kind);
   void build_push_list(uint32_t shift);
   // Deferred push adjacency (big lean graphs, one run per load: the CSR

@@ -11,6 +11,7 @@
 // The path is sparse and irregular: no tensor cores.  Everything is sized
 // for HBM/L2 bandwidth: warp-cooperative, coalesced edge streams, shuffle
 // based segmented reductions, ballot/prefix-sum compaction, persistent grids.
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -21,6 +22,8 @@
 #include "device_types.h"
 #include "errors.h"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace seraph {
 
@@ -249,7 +252,8 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
 // 6 blocks x 8 warps per SM at <= 40 registers (measured best: 5 blocks at 48
 // registers and 7-8 blocks at 32 registers with spills are 3-20 % slower)
 template <int A, int G, bool DET>
-__global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a) {
+__device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_work, RunCtr* a_ctr,
+                                                const RunCtr* a_prev_ctr, uint32_t a_run_id) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_cur[kWarpsPerBlock][kTileMaxDests];
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
 
   for (;;) {
     uint32_t t0 = 0;
-    if (lane == 0) t0 = atomicAdd(a.work, grab);
+    if (lane == 0) t0 = atomicAdd(a_work, grab);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= total) break;
     const uint32_t t1 = min(t0 + grab, total);
@@ -277,11 +281,13 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
       const uint32_t ti = task_to_tile(a.seg, t);
       const uint32_t p = a.tile_page[ti];
       if (p != cur_page) {
-        if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
+        if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a_ctr + cur_page, lane);
         cur_page = p;
         pd = a.pages[p];
       }
-      if (a.prev_ctr && a.prev_ctr[a.ctr_per_page ? p : 0].valid == 0) continue;  // quiet page
+      // quiet page (L2 read: in the K2 loop the previous run's counters were
+      // written by other SMs' atomics within this launch)
+      if (a_prev_ctr && __ldcg(&a_prev_ctr[a.ctr_per_page ? p : 0].valid) == 0) continue;
       const uint4 tile = a.tiles[ti];
       const uint32_t vb = pd.vertex_begin;
       const uint32_t* __restrict__ offs = pd.offs;
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
             a.changed[v] = 1;
             lane_min = min(lane_min, best);
             const uint32_t hub = tile.w & ~kHubFlag;
-            if (a.count_valid && atomicMax(a.hub_stamp + hub, a.run_id) < a.run_id) c.valid += 1;
+            if (a.count_valid && atomicMax(a.hub_stamp + hub, a_run_id) < a_run_id) c.valid += 1;
           }
         }
         continue;
@@ -507,10 +513,41 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
     }
   }
   if (a.ctr_per_page) {
-    if (cur_page != 0xffffffffu) flush_ctr(c, a.ctr + cur_page, lane);
+    if (cur_page != 0xffffffffu) flush_ctr(c, a_ctr + cur_page, lane);
     block_flush(c, nullptr, lane_min, a.census, &s_pref[0][0]);
   } else {
-    block_flush(c, a.ctr, lane_min, a.census, &s_pref[0][0]);
+    block_flush(c, a_ctr, lane_min, a.census, &s_pref[0][0]);
+  }
+}
+
+template <int A, int G, bool DET>
+__global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a) {
+  pull_relax_body<A, G, DET>(a, a.work, a.ctr, a.prev_ctr, a.run_id);
+}
+
+// ---------------------------------------------------------------------------
+// K2: local convergence on the device (reentry, scheduler.cpp:272-291: re-run
+// the resident set while it still changes, up to MRT runs).  ONE cooperative
+// launch loops: run r relaxes every page whose run r-1 had valid updates
+// (device quiet-page gate), a grid barrier, and the loop stops as soon as a
+// whole run was quiet -- no host round trip and no launch per re-run.
+// ---------------------------------------------------------------------------
+template <int A, int G>
+__global__ void __launch_bounds__(kBlockThreads, 6) pull_reentry_kernel(PullArgs a,
+                                                                         ReentryArgs r) {
+  cg::grid_group grid = cg::this_grid();
+  for (uint32_t it = 0; it < r.runs; ++it) {
+    RunCtr* ctr = r.ctr + size_t(it) * r.ctr_stride;
+    pull_relax_body<A, G, false>(a, r.work + it, ctr,
+                                 it ? r.ctr + size_t(it - 1) * r.ctr_stride : nullptr,
+                                 a.run_id + it);
+    grid.sync();  // every page's counters of run `it` are final and visible
+    unsigned long long v = 0;
+    for (uint32_t p = 0; p < r.ctr_stride; ++p) v += __ldcg(&ctr[p].valid);
+    if (v == 0 || it + 1 == r.runs) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *r.runs_done = it + 1;
+      break;
+    }
   }
 }
 
@@ -1777,6 +1814,47 @@ void launch_pull(int algo, int gate, bool det, const PullArgs& a, int grid, cuda
     case kBfs: pull_dispatch1<kBfs>(gate, det, a, grid, s); break;
     case kCc: pull_dispatch1<kCc>(gate, det, a, grid, s); break;
     default: pull_dispatch1<kSssp>(gate, det, a, grid, s); break;
+  }
+}
+
+template <int A, int G>
+static bool reentry_launch(const PullArgs& a, const ReentryArgs& r, int grid, cudaStream_t s) {
+  static int max_grid = -1;
+  if (max_grid < 0) {
+    int nb = 0, dev = 0, sms = 0;
+    SR_CUDA(cudaGetDevice(&dev));
+    SR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_reentry_kernel<A, G>,
+                                                          kBlockThreads, 0));
+    max_grid = nb * sms;
+  }
+  if (max_grid < 1) return false;
+  grid = std::min(grid, max_grid);  // persistent warps: any grid works, all co-resident
+  PullArgs aa = a;
+  ReentryArgs rr = r;
+  void* args[] = {&aa, &rr};
+  SR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pull_reentry_kernel<A, G>),
+                                      dim3(grid), dim3(kBlockThreads), args, 0, s));
+  note_launch();
+  return true;
+}
+
+template <int A>
+static bool reentry_dispatch(int gate, const PullArgs& a, const ReentryArgs& r, int grid,
+                             cudaStream_t s) {
+  switch (gate) {
+    case kGateStrong: return reentry_launch<A, kGateStrong>(a, r, grid, s);
+    case kGateWeak: return reentry_launch<A, kGateWeak>(a, r, grid, s);
+    default: return reentry_launch<A, kGateOff>(a, r, grid, s);
+  }
+}
+
+bool launch_pull_reentry(int algo, int gate, const PullArgs& a, const ReentryArgs& r, int grid,
+                         cudaStream_t s) {
+  switch (algo) {
+    case kBfs: return reentry_dispatch<kBfs>(gate, a, r, grid, s);
+    case kCc: return reentry_dispatch<kCc>(gate, a, r, grid, s);
+    default: return reentry_dispatch<kSssp>(gate, a, r, grid, s);
   }
 }
 

@@ -11,6 +11,10 @@ namespace seraph {
 
 // K1 / K7: dense pull relaxation over a set of tile segments.
 void launch_pull(int algo, int gate, bool det, const PullArgs& a, int grid, cudaStream_t s);
+// K2: reentry runs of one page set in one cooperative launch (false: the
+// grid does not fit co-resident -- the caller launches the runs itself).
+bool launch_pull_reentry(int algo, int gate, const PullArgs& a, const ReentryArgs& r, int grid,
+                         cudaStream_t s);
 // Deterministic mode commit: values[v] = next[v] for v in [lo, hi).
 void launch_commit(uint32_t* values, const uint32_t* next, uint32_t lo, uint32_t hi,
                    cudaStream_t s);

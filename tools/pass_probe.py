@@ -30,16 +30,15 @@ def main():
                     choices=[e.name.lower() for e in ps.ExecutionPolicy])
     ap.add_argument("--sweep", default="", help="VAR=v1,v2,...: time one run per setting")
     ap.add_argument("--verify", action="store_true")
-    ap.add_argument("--graph", default="device", choices=["device", "host"])
     a = ap.parse_args()
-    ns = argparse.Namespace(algo=a.algo, scale=a.scale, edge_factor=16, uniform=a.uniform,
-                            pages=a.pages, seed=0, lean=True, graph=a.graph)
     eng = ps.Engine(0)
-    W = bench.workload(ns, eng)
-    print(f"# build {W['build_s']:.1f}s n={W['n']} m={W['m']} ({W['graph']})", flush=True)
-    if not W["loaded"]:
-        eng.load_csr(W["csr"], with_edges=False)
-        eng.load_pages(W["pages"])
+    n = 1 << a.scale
+    quad = bench.UNIFORM if a.uniform else bench.RMAT
+    eng.generate_graph(a.scale, 16, *quad, seed=0,
+                       weights=(1, 64, 1) if a.algo == "sssp" else None,
+                       symmetrize=a.algo == "cc", page_vertex_capacity=(n + a.pages - 1) // a.pages,
+                       csr_edges=False)
+    print(f"# n={n} m={eng.graph_info()['num_edges']}", flush=True)
     kind = ps.AlgoKind(bench.ALGOS[a.algo])
     prog = ps.VertexProgram(kind, 0)
     cfg = ps.EngineConfig(predictor=ps.PredictorMode(bench.PREDS[a.predictor]),
