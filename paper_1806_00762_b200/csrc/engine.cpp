@@ -1164,10 +1164,15 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
         if (pages_[p].slot >= 0) SR_CUDA(cudaStreamWaitEvent(cs_, slots_[pages_[p].slot].ready, 0));
     }
     const bool per_page = st.gated && st.pages.size() > 1;
-    // K2: the reentry runs of a resident set loop on the device (one
-    // cooperative launch, stops at the first quiet run)
-    if (st.gated && st.reps > 1 && !stream && !pagerank && !record_trace_ &&
-        !std::getenv("SERAPH_NO_K2") && reentry_on_device(st.pages, gate, st.reps, per_page)) {
+    // K2 (SERAPH_K2=1): the reentry runs of a resident set loop on the device
+    // in one cooperative launch that stops at the first quiet run.  Measured
+    // on C2 reentry: 2.86 ms vs 2.58 ms for the host-enqueued runs (whose
+    // device quiet-page gate already makes a converged re-run nearly free),
+    // so the default stays the host-enqueued form.
+    const char* k2e = std::getenv("SERAPH_K2");
+    const bool k2 = k2e && std::atoi(k2e) != 0;
+    if (k2 && st.gated && st.reps > 1 && !stream && !pagerank && !record_trace_ &&
+        reentry_on_device(st.pages, gate, st.reps, per_page)) {
       po.kernel_runs += st.pages.size() * size_t(st.reps);
       continue;
     }

@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a
 // whole run was quiet -- no host round trip and no launch per re-run.
 // ---------------------------------------------------------------------------
 template <int A, int G>
-__global__ void __launch_bounds__(kBlockThreads, 6) pull_reentry_kernel(PullArgs a,
+__global__ void __launch_bounds__(kBlockThreads, 5) pull_reentry_kernel(PullArgs a,
                                                                          ReentryArgs r) {
   cg::grid_group grid = cg::this_grid();
   for (uint32_t it = 0; it < r.runs; ++it) {

@@ -1111,3 +1111,29 @@ def test_sharded_run_graph_and_device_built_shards():
         assert np.array_equal(out[r][1].values, ref.values), r
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("kind", [ps.AlgoKind.BFS, ps.AlgoKind.SSSP, ps.AlgoKind.CC])
+def test_k2_device_reentry_loop(kind, monkeypatch):
+    """K2 (SERAPH_K2=1): reentry's re-runs of the resident page set inside ONE
+    cooperative launch with grid barriers, stopping at the first quiet run
+    (scheduler.cpp:272-291 on the device): bit-exact with the oracle under
+    every predictor and MRT."""
+    monkeypatch.setenv("SERAPH_K2", "1")
+    scale = 13
+    n = 1 << scale
+    src, dst = O.generate_rmat(scale, 16, seed=21)
+    w = O.assign_weights(src.size, 22, 1, 64)
+    el = ps.EdgeList(n, src, dst, w)
+    if kind == ps.AlgoKind.CC:
+        el = ps.EdgeList(n, *O.symmetrize(src, dst, w))
+    csr, pages = built(el, n // 16)
+    want = oracle_values(el, kind, 0)
+    with ps.Engine(0) as eng:
+        for pred in PREDS:
+            for mrt in (1, 2, 5):
+                c = cfg_of(mode=ps.ScheduleModeKind.REENTRY, pred=pred, clock=ps.ClockMode.WALL,
+                           execution=ps.ExecutionPolicy.FORCE_DENSE)
+                c.schedule.max_reentry_times = mrt
+                r = eng.run_graph(csr, pages, program_for(kind, 0, el), c)
+                assert np.array_equal(r.values, want), (kind, pred, mrt)
