@@ -365,7 +365,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
       const uint32_t dl = tile.z, dh = tile.w;
       const uint32_t ebase = tile.x & ~7u;  // 32-byte aligned run grid
       uint32_t n_ent = 0;
-      unsigned any_att = 0;
+      unsigned any_att = 0, any_dead = 0;
       // entry starts as a bitmap over the tile's edge positions (span <=
       // kTileEdgeBudget + 7 -> <= 33 words) + per-word prefix counts: a run's
       // first entry and its entry steps come from one word, no search
@@ -393,6 +393,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
         const bool has = in && deg > 0;
         const unsigned m = __ballot_sync(kFull, has);
         any_att |= __ballot_sync(kFull, has && need);
+        any_dead |= __ballot_sync(kFull, has && !need);
         if (has) {
           const uint32_t pos = n_ent + __popc(m & lanemask_lt());
           const uint32_t p0 = lo - ebase;
@@ -430,8 +431,11 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
           // adv bit t: an entry starts at position pos0 + t (after q)
           const unsigned adv = (bw >> (pos0 & 31)) & (0xffu << (q - pos0 + 1)) & 0xffu;
           const uint32_t hi_t = min(span - pos0, (uint32_t)kLaneEdges);
-          unsigned live = 0;
-          {
+          // every entry of the tile can still improve (the common case of a
+          // first dense pass): the live positions are the run's valid ones
+          unsigned live = (0xffu >> (8 - hi_t)) & (0xffu << (q - pos0)) & 0xffu;
+          if (any_dead) {
+            live = 0;
             uint32_t e = ent0, from = q - pos0;
             unsigned rem = adv;
 #pragma unroll 1
