@@ -1139,11 +1139,27 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
   // Source blocking pays for gathers only: once the previous dense pass
   // gathered for < 5 % of its edges (converged labels/levels skip theirs), the
   // per-block destination traffic would dominate -- sweep unblocked.
-  if (mode == SR_SCHED_BASELINE && !stream && !pagerank && last_gather_frac_ >= 0.05 &&
-      pull_block_verts()) {
-    if (pull_blocked_pass(gate, alloc_ctr(1))) {
+  // Resident reentry takes the same blocked sweeps: its re-runs of the
+  // whole resident set (local convergence, scheduler.cpp:272-291) repeat the
+  // blocked pass while the previous run still changed something, up to MRT.
+  const bool reentry_res = mode == SR_SCHED_REENTRY && !stream;
+  if ((mode == SR_SCHED_BASELINE || reentry_res) && !stream && !pagerank &&
+      last_gather_frac_ >= 0.05 && pull_block_verts()) {
+    RunCtr* slot = alloc_ctr(1);
+    if (pull_blocked_pass(gate, slot, reentry_res)) {
       last_pass_blocked_ = true;
       po.kernel_runs += order.size();
+      for (int r = 1; reentry_res && r < cfg.max_reentry_times; ++r) {
+        SR_CUDA(cudaMemcpyAsync(ctr_h_.p, slot, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+        SR_CUDA(cudaStreamSynchronize(cs_));
+        if (ctr_h_.p[0].valid == 0) break;  // quiet: locally converged
+        slot = alloc_ctr(1);
+        trace_reentry_ = true;
+        if (!pull_blocked_pass(gate, slot, true))  // probe: gathers are rare now
+          launch_pages(order, gate, false, slot, nullptr, false, false);
+        trace_reentry_ = false;
+        po.kernel_runs += order.size();
+      }
       return po;
     }
     --ctr_used_;  // the (zeroed) probe slot is the first one the unblocked steps take

@@ -410,7 +410,7 @@ class Engine {
   double hot_source_coverage(uint64_t k);
   double coverage_ = -1;
   uint64_t coverage_k_ = 0;
-  bool pull_blocked_pass(int gate, RunCtr* ctr);
+  bool pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid = false);
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();

@@ -235,7 +235,7 @@ void Engine::l2_window(const void* base, size_t bytes) {
   }
 }
 
-bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
+bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
   const uint64_t blk = pull_block_verts();
   if (!blk || !build_src_blocks(blk)) return false;
   const uint32_t run_id = ++run_id_;
@@ -261,7 +261,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr) {
     a.ctr = ctr;
     a.census = census_.p;
     a.count_dest = b == 0 ? 1u : 0u;
-    a.count_valid = 0;
+    a.count_valid = count_valid ? 1u : 0u;  // reentry's "did the run change anything"
     a.peers = peer_list();
     a.n_peers = n_peers_;
     a.k_bfs = k_bfs_;

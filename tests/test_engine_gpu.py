@@ -639,6 +639,16 @@ def test_pull_source_blocked(blk, monkeypatch):
             r = eng.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
             assert np.array_equal(r.values, want), pred
             assert eng.verify_fixpoint(ps.AlgoKind.CC, r.values) == 0
+        # resident reentry over the blocked sweeps (re-run the set while it changes)
+        for kind, g, cs, pg in ((ps.AlgoKind.BFS, el, csr, pages), (ps.AlgoKind.SSSP, el, csr, pages),
+                                (ps.AlgoKind.CC, sym, csr2, pages2)):
+            want = oracle_values(g, kind, 0)
+            for pred in PREDS:
+                for mrt in (2, 4):
+                    c = cfg_of(mode=ps.ScheduleModeKind.REENTRY, pred=pred, clock=ps.ClockMode.WALL)
+                    c.schedule.max_reentry_times = mrt
+                    r = eng.run_graph(cs, pg, program_for(kind, 0, g), c)
+                    assert np.array_equal(r.values, want), (kind, pred, mrt)
 
 
 # --------------------------------------------------------------------------
