@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <exception>
@@ -129,8 +130,9 @@ int sr_group_open(const int* devices, int n, uint64_t budget, int flags, sr_grou
       });
       if (rcg != SR_OK) throw seraph::EngineError(rcg, g->err);
     } else {  // a device listed more than once: in-process loopback transport
+      static std::atomic<unsigned long long> seq{0};  // never reuse a (possibly abandoned) key
       char key[64];
-      std::snprintf(key, sizeof(key), "sr_group:%p", static_cast<void*>(g));
+      std::snprintf(key, sizeof(key), "sr_group:%llu", seq.fetch_add(1) + 1);
       for (int r = 0; r < n; ++r) g->ranks[r]->attach_loopback(r, n, key, peer);
     }
   });
