@@ -875,7 +875,9 @@ def run(csr: CsrGraph, pages: PageSet, program: VertexProgram, config: EngineCon
     if devices is None and os.environ.get("SERAPH_DEVICES"):
         devices = [int(x) for x in os.environ["SERAPH_DEVICES"].split(",") if x.strip()]
     with _default_lock:
-        if devices is not None and len(devices) > 1:
+        # ClockMode::Virtual (the reference's deterministic schedule) runs on
+        # the first device alone, as in the C++ drop-in
+        if devices is not None and len(devices) > 1 and config.clock == ClockMode.WALL:
             key = ("group", tuple(devices), int(hbm_budget_bytes))
             grp = _default_engines.get(key)
             if grp is None:
