@@ -432,6 +432,8 @@ bool Engine::prepare_pr_hot(bool blocked) {
                           cudaMemcpyHostToDevice, cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
   pr_hot_.slot_of.release();
+  if (std::getenv("SERAPH_TIMING"))
+    std::fprintf(stderr, "[seraph] pr hot set: %u sources (out-degree >= %u)\n", pr_hot_.n_hot, d);
   pr_hot_.blocked = blocked;
   pr_hot_.key = key;
   pr_hot_.built = true;
