@@ -516,7 +516,7 @@ def run_ours(a, rank, world, local_rank):
         if world > 1:
             e2e_eng.attach_world(rank, world, world_uid())
             e2e_eng.set_exchange(a.exchange == "peer")
-        vals = arena.array(n, np.uint32) if not pr else None
+        vals = arena.array(n, np.float32 if pr else np.uint32)  # reused output (values / ranks)
         e2e_eng.run_graph(csr, pages, prog, cfg, values_out=vals)  # warm-up
         sync()
         if world > 1:
@@ -554,7 +554,7 @@ def run_ours(a, rank, world, local_rank):
                                  [ps.CscPage(p.vertex_begin, p.vertex_end, np.array(p.in_offsets),
                                              np.array(p.in_sources), np.array(p.in_weights))
                                   for p in pages.pages])
-            vals_p = np.empty(n, np.uint32) if not pr else None
+            vals_p = np.zeros(n, np.float32 if pr else np.uint32)  # reused, pages touched
             e2e_eng.run_graph(csr_p, pages_p, prog, cfg, values_out=vals_p)  # warm-up
             sync()
             t3 = time.time()

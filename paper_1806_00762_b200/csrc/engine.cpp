@@ -1518,7 +1518,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   if (csr_deferred_ && cfg.algo != SR_ALGO_PAGERANK &&
       (runs_since_pages_ > 0 || cfg.clock == SR_CLOCK_VIRTUAL))
     derive_csr_now();
-  maybe_derive_csr();
+  if (cfg.algo != SR_ALGO_PAGERANK) maybe_derive_csr();  // PageRank reads out-degrees only
   validate(cfg);
   scan_pushes_ = 0;
   ++runs_since_pages_;

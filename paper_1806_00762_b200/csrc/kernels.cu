@@ -656,17 +656,7 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  auto emit = [&](uint32_t p, uint32_t v, uint32_t s, const uint32_t* wp) {
-    const uint32_t b = s / blk_verts;
-    const size_t k = size_t(b) * n + v;
-    if (mode == 0) {
-      atomicAdd(cnt + k, 1u);
-    } else {  // goff holds absolute cursors (src_block_page_fix_kernel)
-      const unsigned long long o = atomicAdd(goff + k, 1ull);
-      out_src[o] = s;
-      if (out_w) out_w[o] = *wp;
-    }
-  };
+  // mode 1: goff holds absolute cursors (src_block_page_fix_kernel)
   for (uint32_t ti = tile_lo + blockIdx.x * kWarpsPerBlock + warp; ti < tile_hi;
        ti += gridDim.x * kWarpsPerBlock) {
     const uint32_t pg = tile_page[ti];
@@ -674,8 +664,31 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
     const uint4 tile = tiles[ti];
     const uint32_t* __restrict__ src = pd.src;
     if (tile.w & kHubFlag) {
+      // one destination, up to kHubChunk in-edges: lanes whose sources fall
+      // in the same block share ONE atomic (match_any groups) -- RMAT hubs
+      // would otherwise serialise thousands of atomics on one counter
       const uint32_t v = pd.vertex_begin + tile.z;
-      for (uint32_t e = tile.x + lane; e < tile.y; e += 32) emit(pg, v, src[e], pd.w + e);
+      for (uint32_t e0 = tile.x; e0 < tile.y; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const bool ok = e < tile.y;
+        const uint32_t sv = ok ? src[e] : 0u;
+        const uint32_t b = ok ? sv / blk_verts : kNone;
+        const unsigned grp = __match_any_sync(kFull, b);
+        const int leader = __ffs(grp) - 1;
+        const uint32_t k_n = __popc(grp);
+        const size_t k = size_t(b) * n + v;
+        if (mode == 0) {
+          if (ok && lane == leader) atomicAdd(cnt + k, k_n);
+        } else {
+          unsigned long long o = 0;
+          if (ok && lane == leader) o = atomicAdd(goff + k, (unsigned long long)k_n);
+          o = __shfl_sync(kFull, o, leader) + __popc(grp & lanemask_lt());
+          if (ok) {
+            out_src[o] = sv;
+            if (out_w) out_w[o] = pd.w[e];
+          }
+        }
+      }
       continue;
     }
     const uint32_t dl = tile.z, dh = tile.w;
@@ -718,7 +731,15 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
             nxt = (ent + 1 < n_ent) ? s_pref[warp][ent + 1] : span;
           }
           if (pp < lo_pos) continue;
-          emit(pg, pd.vertex_begin + s_loc[warp][ent], src[ebase + pp], pd.w + ebase + pp);
+          const uint32_t sv = src[ebase + pp];
+          const size_t k = size_t(sv / blk_verts) * n + pd.vertex_begin + s_loc[warp][ent];
+          if (mode == 0) {
+            atomicAdd(cnt + k, 1u);
+          } else {
+            const unsigned long long o = atomicAdd(goff + k, 1ull);
+            out_src[o] = sv;
+            if (out_w) out_w[o] = pd.w[ebase + pp];
+          }
         }
       }
     }

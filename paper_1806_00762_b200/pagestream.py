@@ -695,8 +695,9 @@ class Engine:
         n = self.num_vertices
         vals = None
         ranks = None
-        if program.kind == AlgoKind.PAGERANK:
-            ranks = np.empty(n, np.float32) if want_values else None
+        if program.kind == AlgoKind.PAGERANK:  # values_out: an f32 array for the ranks
+            ranks = values_out if values_out is not None else (np.empty(n, np.float32)
+                                                                if want_values else None)
         else:
             vals = values_out if values_out is not None else (np.empty(n, np.uint32)
                                                               if want_values else None)
@@ -720,8 +721,8 @@ class Engine:
         cfg = config.to_c(program)
         n = csr.num_vertices
         vals = ranks = None
-        if program.kind == AlgoKind.PAGERANK:
-            ranks = np.empty(n, np.float32)
+        if program.kind == AlgoKind.PAGERANK:  # values_out: an f32 array for the ranks
+            ranks = values_out if values_out is not None else np.empty(n, np.float32)
         else:
             vals = values_out if values_out is not None else np.empty(n, np.uint32)
         views = _page_views(pages)
