@@ -1144,7 +1144,7 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
   // blocked pass while the previous run still changed something, up to MRT.
   const bool reentry_res = mode == SR_SCHED_REENTRY && !stream;
   if ((mode == SR_SCHED_BASELINE || reentry_res) && !stream && !pagerank &&
-      last_gather_frac_ >= 0.05 && pull_block_verts()) {
+      last_gather_frac_ >= 0.05 && last_block_gather_frac_ >= 0.05 && pull_block_verts()) {
     RunCtr* slot = alloc_ctr(1);
     if (pull_blocked_pass(gate, slot, reentry_res)) {
       last_pass_blocked_ = true;
@@ -1583,6 +1583,8 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   l_sssp_ = 0;
   floor_sssp_ = 0;
   last_gather_frac_ = 1.0;  // the first dense pass gathers
+  last_block_gather_frac_ = 1.0;
+  sb_last_slot_ = -1;
   ctr_used_ = 0;
   if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_ && !weak) {  // weak: census seeds the DFA histogram
     // the initial frontier {source} directly as a queue
@@ -1624,6 +1626,12 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     }
     gathers_total_ += gathers;
     last_gather_frac_ = st.edges_read ? double(gathers) / double(st.edges_read) : 0.0;
+    last_block_gather_frac_ = 1.0;
+    if (sb_last_slot_ >= 0 && size_t(sb_last_slot_) < size_t(ctr_used_)) {
+      const RunCtr& lc = ctr_h_.p[sb_last_slot_];
+      if (lc.edges) last_block_gather_frac_ = double(lc.gathers) / double(lc.edges);
+    }
+    sb_last_slot_ = -1;
   };
   auto begin_pass = [&]() {
     ctr_used_ = 0;

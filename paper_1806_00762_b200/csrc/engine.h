@@ -413,6 +413,11 @@ class Engine {
   bool pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid = false);
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
+  // A blocked pass's last block launch counts into its own slot: when even
+  // its gathers were rare (labels / levels at the floor), the next dense pass
+  // sweeps unblocked without probing block 0 first.
+  int sb_last_slot_ = -1;
+  double last_block_gather_frac_ = 1.0;
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
   void l2_window(const void* base, size_t bytes);
   int l2_persist_max_ = -1;  // persisting-L2 carve-out (bytes; 0 = unavailable/disabled)

@@ -239,6 +239,14 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
   const uint64_t blk = pull_block_verts();
   if (!blk || !build_src_blocks(blk)) return false;
   const uint32_t run_id = ++run_id_;
+  uint32_t last_b = sb_.n_blocks;  // the last block with tiles gets its own counter slot
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b)
+    if (sb_.block_tile_begin[b + 1] > sb_.block_tile_begin[b]) last_b = b;
+  RunCtr* last_ctr = nullptr;
+  if (last_b > 0 && last_b < sb_.n_blocks && size_t(ctr_used_) + 1 <= ctr_.n) {
+    last_ctr = alloc_ctr(1);
+    sb_last_slot_ = int(last_ctr - ctr_.p);
+  }
   for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
     const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
     if (t1 <= t0) continue;
@@ -258,7 +266,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     a.status = status_.p;
     a.hub_stamp = hub_stamp_.p;
     a.run_id = run_id;
-    a.ctr = ctr;
+    a.ctr = (b == last_b && last_ctr) ? last_ctr : ctr;
     a.census = census_.p;
     a.count_dest = b == 0 ? 1u : 0u;
     a.count_valid = count_valid ? 1u : 0u;  // reentry's "did the run change anything"
@@ -289,6 +297,10 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
       const RunCtr& c0 = ctr_h_.p[0];
       if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
         SR_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RunCtr), cs_));
+        if (last_ctr) {  // the unblocked finish reuses the slots from the probe's on
+          --ctr_used_;
+          sb_last_slot_ = -1;
+        }
         l2_window(nullptr, 0);
         return false;
       }
