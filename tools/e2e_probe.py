@@ -43,3 +43,26 @@ for rep in range(3):
 t = time.time()
 r = eng.run(prog, cfg)
 print(f"run only {1e3*(time.time()-t):.1f} ms (device {1e3*r.metrics.device_seconds:.2f} ms)")
+
+# pageable copies (what the C++ drop-in passes): the same call and its phases
+csr_p = ps.CsrGraph(n, np.array(csr.out_offsets), csr.out_neighbors, csr.out_weights)
+pages_p = ps.PageSet(pages.num_vertices, pages.page_vertex_capacity, pages.weighted,
+                     [ps.CscPage(p.vertex_begin, p.vertex_end, np.array(p.in_offsets),
+                                 np.array(p.in_sources), np.array(p.in_weights))
+                      for p in pages.pages])
+out = np.zeros(n, np.float32 if a.algo == "pagerank" else np.uint32)
+for rep in range(3):
+    t = time.time()
+    r = eng.run_graph(csr_p, pages_p, prog, cfg, values_out=out)
+    print(f"pageable run_graph {1e3*(time.time()-t):.1f} ms (upload {1e3*r.metrics.upload_seconds:.1f}"
+          f" ms, device {1e3*r.metrics.device_seconds:.2f} ms)", flush=True)
+for rep in range(2):
+    t0 = time.time()
+    eng.load_csr(csr_p, with_edges=False)
+    t1 = time.time()
+    eng.load_pages(pages_p)
+    t2 = time.time()
+    r = eng.run(prog, cfg, values_out=out)
+    t3 = time.time()
+    print(f"pageable phases: load_csr {1e3*(t1-t0):.1f} load_pages {1e3*(t2-t1):.1f} "
+          f"run+d2h {1e3*(t3-t2):.1f} ms", flush=True)
