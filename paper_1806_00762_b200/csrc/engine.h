@@ -376,7 +376,7 @@ class Engine {
     // cudaMalloc/cudaFree of them cost more than the build kernels)
     DBuf<uint32_t> t_cnt, t_tcnt, t_tat;
     DBuf<unsigned char> t_scan;
-    DBuf<unsigned long long> t_goff, bp_edges, bp_base;
+    DBuf<unsigned long long> t_goff, bp_edges, bp_base, t_part;
     std::vector<unsigned long long> page_base;
     bool pending = false;  // sb_begin done, sb_finish not yet
     DBuf<uint4> tiles;

@@ -50,6 +50,7 @@ bool Engine::sb_begin(uint64_t blk) {
   sb_.t_goff.reserve(size_t(nb) * n_);
   sb_.bp_edges.reserve(size_t(nb) * np);
   sb_.bp_base.reserve(size_t(nb) * np);
+  sb_.t_part.reserve(std::max<uint32_t>(src_block_scan_parts(cap_, nb), 1));
   SR_CUDA(cudaMemsetAsync(sb_.bp_edges.p, 0, size_t(nb) * np * 8, cs_));
   SR_CUDA(cudaMemsetAsync(sb_.bp_base.p, 0, size_t(nb) * np * 8, cs_));
   sb_.src.reserve(at + 8);
@@ -74,7 +75,8 @@ void Engine::sb_page(uint32_t p) {
                    sb_.blk_verts, np, sb_.t_cnt.p, nullptr, nullptr, nullptr, sm_count_ * 8, cs_);
   // 2) page-local offsets, sub-page sizes and bases, u32 offsets, cursors
   launch_src_block_page(sb_.t_cnt.p, sb_.t_goff.p, page_desc_.p, p, pm.vb, range, n_, cap_, np,
-                        nb, sb_.page_base[p], sb_.bp_edges.p, sb_.bp_base.p, sb_.offs.p, cs_);
+                        nb, sb_.page_base[p], sb_.bp_edges.p, sb_.bp_base.p, sb_.offs.p,
+                        sb_.t_part.p, cs_);
   // 3) scatter the sources (one atomic per edge on the cursors)
   launch_src_block(1, tiles_.p, tile_page_.p, page_desc_.p, pm.tile_begin, pm.tile_end, n_,
                    sb_.blk_verts, np, nullptr, sb_.t_goff.p, sb_.src.p,

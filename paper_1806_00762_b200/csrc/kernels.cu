@@ -747,47 +747,6 @@ src_block_kernel(int mode, const uint4* __restrict__ tiles, const uint32_t* __re
   }
 }
 
-// Per-block exclusive scan helper: goff[b*n + v] = sum_{u < v, u in the same
-// page} cnt[b*n + u] (page-local offsets, u64), one thread block per
-// (page, block) pair, sequential chunks of 1024 with warp scans.
-__global__ void __launch_bounds__(1024) src_block_scan_kernel(const uint32_t* __restrict__ cnt,
-                                                              unsigned long long* goff,
-                                                              const PageDesc* __restrict__ pages,
-                                                              uint32_t n_pages, uint32_t n,
-                                                              unsigned long long* bp_edges,
-                                                              uint32_t p_only) {
-  __shared__ unsigned long long s_w[32];
-  __shared__ unsigned long long s_carry;
-  // one thread block per (block, page): all pages, or the blocks of page p_only
-  const uint32_t p = p_only != kNone ? p_only : blockIdx.x % n_pages;
-  const uint32_t b = p_only != kNone ? blockIdx.x : blockIdx.x / n_pages;
-  const uint32_t pb = b * n_pages + p;
-  const PageDesc pd = pages[p];
-  const size_t base = size_t(b) * n + pd.vertex_begin;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint32_t c0 = 0; c0 < pd.range; c0 += 1024) {
-    const uint32_t i = c0 + threadIdx.x;
-    const unsigned long long x = i < pd.range ? cnt[base + i] : 0ull;
-    const unsigned long long incl = warp_incl_scan(x, lane);
-    if (lane == 31) s_w[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      const unsigned long long t = s_w[lane];
-      const unsigned long long si = warp_incl_scan(t, lane);
-      s_w[lane] = si - t;
-    }
-    __syncthreads();
-    const unsigned long long ex = s_carry + s_w[w] + incl - x;
-    if (i < pd.range) goff[base + i] = ex;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = ex + x;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) bp_edges[pb] = s_carry;
-}
-
 __global__ void pr_block_finalize_kernel(uint32_t lo, uint32_t hi, float* acc, float* rank_out,
                                          float* contrib_out, const float* __restrict__ inv_outdeg,
                                          float base, float damp) {
@@ -2445,6 +2404,99 @@ void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, 
   note_launch(2);
 }
 
+// ---- per-page exclusive scan of the (block, destination) counts of page p:
+// nb segments of `range` u32 counts -> u64 page-local offsets, in parallel
+// chunks (a segment scanned by one thread block took ~8 ms per page) ----
+constexpr uint32_t kSegChunk = 4096;  // 1024 threads x 4
+
+__global__ void __launch_bounds__(1024) seg_chunk_sum_kernel(const uint32_t* __restrict__ cnt,
+                                                             size_t n, uint32_t vb, uint32_t range,
+                                                             uint32_t chunks,
+                                                             unsigned long long* part) {
+  __shared__ unsigned long long s_w[32];
+  const uint32_t b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+  const uint32_t* seg = cnt + size_t(b) * n + vb;
+  unsigned long long x = 0;
+  for (uint32_t i = c * kSegChunk + threadIdx.x; i < min(range, (c + 1) * kSegChunk); i += 1024)
+    x += seg[i];
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    x = warp_sum(s_w[threadIdx.x]);
+    if (threadIdx.x == 0) part[blockIdx.x] = x;
+  }
+}
+
+// per block b: exclusive scan of its chunk sums in place; the total -> bp_edges
+__global__ void __launch_bounds__(1024) seg_part_scan_kernel(unsigned long long* part,
+                                                             uint32_t chunks, uint32_t p,
+                                                             uint32_t n_pages,
+                                                             unsigned long long* bp_edges) {
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const uint32_t b = blockIdx.x;
+  unsigned long long* q = part + size_t(b) * chunks;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < chunks; c0 += 1024) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned long long x = i < chunks ? q[i] : 0ull;
+    const unsigned long long incl = warp_incl_scan(x, lane);
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned long long t = s_w[lane];
+      s_w[lane] = warp_incl_scan(t, lane) - t;
+    }
+    __syncthreads();
+    const unsigned long long ex = s_carry + s_w[w] + incl - x;
+    if (i < chunks) q[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = ex + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bp_edges[size_t(b) * n_pages + p] = s_carry;
+}
+
+__global__ void __launch_bounds__(1024) seg_chunk_scan_kernel(const uint32_t* __restrict__ cnt,
+                                                              size_t n, uint32_t vb,
+                                                              uint32_t range, uint32_t chunks,
+                                                              const unsigned long long* part,
+                                                              unsigned long long* goff) {
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const uint32_t b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+  const uint32_t* seg = cnt + size_t(b) * n + vb;
+  unsigned long long* out = goff + size_t(b) * n + vb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = part[blockIdx.x];
+  __syncthreads();
+  const uint32_t end = min(range, (c + 1) * kSegChunk);
+  for (uint32_t c0 = c * kSegChunk; c0 < end; c0 += 1024) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned long long x = i < end ? seg[i] : 0ull;
+    const unsigned long long incl = warp_incl_scan(x, lane);
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned long long t = s_w[lane];
+      s_w[lane] = warp_incl_scan(t, lane) - t;
+    }
+    __syncthreads();
+    const unsigned long long ex = s_carry + s_w[w] + incl - x;
+    if (i < end) out[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = ex + x;
+    __syncthreads();
+  }
+}
+
+uint32_t src_block_scan_parts(uint32_t cap, uint32_t n_blocks) {
+  return n_blocks * ((cap + kSegChunk - 1) / kSegChunk);
+}
+
 // ---- page-major per-page build (Engine::sb_page): sub-page (p, b) lives at
 // page_base + sum_{b' < b} pad8(edges(p, b')), so page p's sub-pages are
 // built from page p alone, as soon as its DMA has landed ----
@@ -2489,10 +2541,14 @@ void launch_src_block_page(const uint32_t* cnt, unsigned long long* goff, const 
                            uint32_t p, uint32_t vb, uint32_t range, uint32_t n, uint32_t cap,
                            uint32_t n_pages, uint32_t n_blocks, unsigned long long page_base,
                            unsigned long long* bp_edges, unsigned long long* bp_base,
-                           uint32_t* offs, cudaStream_t s) {
+                           uint32_t* offs, unsigned long long* part, cudaStream_t s) {
   if (!n_blocks) return;
-  note_launch(3);
-  src_block_scan_kernel<<<n_blocks, 1024, 0, s>>>(cnt, goff, pages, n_pages, n, bp_edges, p);
+  (void)pages;
+  note_launch(5);
+  const uint32_t chunks = std::max<uint32_t>(1, (range + kSegChunk - 1) / kSegChunk);
+  seg_chunk_sum_kernel<<<n_blocks * chunks, 1024, 0, s>>>(cnt, n, vb, range, chunks, part);
+  seg_part_scan_kernel<<<n_blocks, 1024, 0, s>>>(part, chunks, p, n_pages, bp_edges);
+  seg_chunk_scan_kernel<<<n_blocks * chunks, 1024, 0, s>>>(cnt, n, vb, range, chunks, part, goff);
   src_block_page_base_kernel<<<1, 32, 0, s>>>(p, n_pages, n_blocks, page_base, bp_edges, bp_base);
   src_block_page_fix_kernel<<<grid_for(uint64_t(n_blocks) * (range + 1), 256), 256, 0, s>>>(
       p, vb, range, n, cap, n_pages, n_blocks, goff, bp_edges, bp_base, offs);

@@ -89,7 +89,9 @@ void launch_src_block_page(const uint32_t* cnt, unsigned long long* goff, const 
                            uint32_t p, uint32_t vb, uint32_t range, uint32_t n, uint32_t cap,
                            uint32_t n_pages, uint32_t n_blocks, unsigned long long page_base,
                            unsigned long long* bp_edges, unsigned long long* bp_base,
-                           uint32_t* offs, cudaStream_t s);
+                           uint32_t* offs, unsigned long long* part, cudaStream_t s);
+// chunk-sum temporaries launch_src_block_page needs for pages of <= cap vertices
+uint32_t src_block_scan_parts(uint32_t cap, uint32_t n_blocks);
 
 // Tile cut of the source-blocked sub-pages on the device, one 128-destination
 // window per thread: mode 0 writes the tile count of every window to cnt
