@@ -384,6 +384,7 @@ class Engine {
     DBuf<PageDesc> desc;
     DBuf<float> acc;
     std::vector<uint32_t> block_tile_begin;  // n_blocks + 1
+    std::vector<uint32_t> sub_tile_begin;    // n_blocks * n_pages + 1 (first tile of (b, p))
   } sb_;
   bool build_src_blocks(uint64_t blk_verts);
   bool sb_begin(uint64_t blk_verts);  // layout + buffers (page-major sub-pages)
@@ -411,6 +412,7 @@ class Engine {
   double coverage_ = -1;
   uint64_t coverage_k_ = 0;
   bool pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid = false);
+  Segments diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   // A blocked pass's last block launch counts into its own slot: when even

@@ -110,6 +110,13 @@ bool Engine::sb_finish() {
   for (uint32_t b = 0; b <= nb; ++b)
     SR_CUDA(cudaMemcpyAsync(&sb_.block_tile_begin[b], tat.p + size_t(b) * K_blk, 4,
                             cudaMemcpyDeviceToHost, cs_));
+  // first tile of every sub-page (b, p) (windows are block-major, page-major
+  // inside a block): the diagonal-first launch order of pull_blocked_pass
+  const size_t wpp = K_blk / std::max<uint32_t>(np, 1);
+  sb_.sub_tile_begin.assign(size_t(nb) * np + 1, 0);
+  for (size_t k = 0; k <= size_t(nb) * np; ++k)
+    SR_CUDA(cudaMemcpyAsync(&sb_.sub_tile_begin[k], tat.p + k * wpp, 4, cudaMemcpyDeviceToHost,
+                            cs_));
   SR_CUDA(cudaStreamSynchronize(cs_));
   const uint32_t n_sub_tiles = sb_.block_tile_begin[nb];
   sb_.tiles.reserve(std::max<size_t>(n_sub_tiles, 1));
@@ -258,10 +265,10 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     a.tiles = sb_.tiles.p;
     a.tile_page = sb_.tile_page.p;
     a.pages = sb_.desc.p;
-    a.seg.n = 1;
-    a.seg.tile_begin[0] = t0;
-    a.seg.task_prefix[0] = 0;
-    a.seg.task_prefix[1] = t1 - t0;
+    // Diagonal first: the sub-pages whose destinations are this block's own
+    // sources go first, so the labels / levels / distances they improve are
+    // already visible to the rest of the launch's gathers (async, a15)
+    a.seg = diag_first_segments(b, t0, t1);
     a.values = values_.p;
     a.next = values_.p;
     a.changed = changed_.p;
@@ -310,6 +317,36 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
   }
   l2_window(nullptr, 0);
   return true;
+}
+
+Segments Engine::diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const {
+  Segments seg{};
+  const uint32_t np = uint32_t(pages_.size());
+  auto one = [&]() {
+    seg.n = 1;
+    seg.tile_begin[0] = t0;
+    seg.task_prefix[0] = 0;
+    seg.task_prefix[1] = t1 - t0;
+    return seg;
+  };
+  if (std::getenv("SERAPH_NO_DIAG_FIRST") || sb_.sub_tile_begin.size() != size_t(sb_.n_blocks) * np + 1 ||
+      cap_ == 0)
+    return one();
+  const uint64_t lo = uint64_t(b) * sb_.blk_verts;
+  const uint64_t hi = std::min<uint64_t>(lo + sb_.blk_verts, n_);
+  const uint32_t p_lo = uint32_t(lo / cap_), p_hi = uint32_t(std::min<uint64_t>((hi - 1) / cap_ + 1, np));
+  const uint32_t d0 = sb_.sub_tile_begin[size_t(b) * np + p_lo];
+  const uint32_t d1 = sb_.sub_tile_begin[size_t(b) * np + p_hi];
+  if (d0 < t0 || d1 > t1 || d1 <= d0) return one();
+  const uint32_t r[3][2] = {{d0, d1}, {t0, d0}, {d1, t1}};
+  seg.task_prefix[0] = 0;
+  for (const auto& x : r) {
+    if (x[1] <= x[0]) continue;
+    seg.tile_begin[seg.n] = x[0];
+    seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (x[1] - x[0]);
+    ++seg.n;
+  }
+  return seg;
 }
 
 std::pair<cudaEvent_t, cudaEvent_t>* Engine::relax_begin() {
