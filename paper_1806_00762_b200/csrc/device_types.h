@@ -22,6 +22,8 @@ constexpr uint32_t kTileEdgeBudget = 1024;
 constexpr uint32_t kHubChunk = 1024;      // edges per hub chunk tile
 constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id
 constexpr int kMaxSegments = 8;           // tile ranges per launch
+constexpr int kDiagIters = 1;             // blocked K1: diagonal sweeps until locally quiet (cap)
+constexpr int kRootDiagReps = 6;          // blocked K1: in-launch diagonal sweeps of the root block
 // K8 hot-source staging (pr_pull_kernel<true, kHotWarps>): blocks of
 // kHotWarps warps (1.5 KB of tile scratch each) + a shared-memory table of
 // f32 contributions of the hottest sources, encoded kHotBit | slot.  Measured
@@ -115,6 +117,7 @@ struct ReentryArgs {
   uint32_t ctr_stride;  // counters per run (pages of the set, per-page gating)
   uint32_t runs;        // MRT
   uint32_t* runs_done;  // runs actually executed (device -> host)
+  uint32_t dest_every_run;  // 1: attempts/skips counted by every run (reentry), 0: by run 0 only
 };
 
 struct PrArgs {

@@ -1015,7 +1015,7 @@ bool Engine::reentry_on_device(const std::vector<uint32_t>& pages, int gate, int
   a.src_floor = floor_sssp_;
   a.floor_step = weights_ge1_ ? 1u : 0u;
   a.grab = k1_grab(tasks, grid, "SERAPH_K1_GRAB");
-  ReentryArgs r{work, ctr_.p + ctr_used_, uint32_t(stride), uint32_t(runs), runs_done_.p};
+  ReentryArgs r{work, ctr_.p + ctr_used_, uint32_t(stride), uint32_t(runs), runs_done_.p, 1u};
   auto* evp = relax_begin();
   if (!launch_pull_reentry(algo_, gate, a, r, grid, cs_)) {
     if (evp) --relax_ev_used_;

@@ -413,6 +413,9 @@ class Engine {
   uint64_t coverage_k_ = 0;
   bool pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid = false);
   Segments diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const;
+  bool diag_range(uint32_t b, uint32_t t0, uint32_t t1, uint32_t& d0, uint32_t& d1) const;
+  Segments range_segments(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) const;
+  int diag_local_iterations() const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   // A blocked pass's last block launch counts into its own slot: when even

@@ -3,6 +3,7 @@
 #include "engine.h"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -256,29 +257,24 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     last_ctr = alloc_ctr(1);
     sb_last_slot_ = int(last_ctr - ctr_.p);
   }
-  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
-    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
-    if (t1 <= t0) continue;
-    l2_window(values_.p + uint64_t(b) * blk, std::min<uint64_t>(blk, n_ - uint64_t(b) * blk) * 4);
+  auto make_args = [&](const Segments& seg, RunCtr* slot, bool count_dest, bool count_v,
+                       uint32_t rid) {
     PullArgs a{};
     a.work = next_work_counter();
     a.tiles = sb_.tiles.p;
     a.tile_page = sb_.tile_page.p;
     a.pages = sb_.desc.p;
-    // Diagonal first: the sub-pages whose destinations are this block's own
-    // sources go first, so the labels / levels / distances they improve are
-    // already visible to the rest of the launch's gathers (async, a15)
-    a.seg = diag_first_segments(b, t0, t1);
+    a.seg = seg;
     a.values = values_.p;
     a.next = values_.p;
     a.changed = changed_.p;
     a.status = status_.p;
     a.hub_stamp = hub_stamp_.p;
-    a.run_id = run_id;
-    a.ctr = (b == last_b && last_ctr) ? last_ctr : ctr;
+    a.run_id = rid;
+    a.ctr = slot;
     a.census = census_.p;
-    a.count_dest = b == 0 ? 1u : 0u;
-    a.count_valid = count_valid ? 1u : 0u;  // reentry's "did the run change anything"
+    a.count_dest = count_dest ? 1u : 0u;
+    a.count_valid = count_v ? 1u : 0u;
     a.peers = peer_list();
     a.n_peers = n_peers_;
     a.k_bfs = k_bfs_;
@@ -286,16 +282,86 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     a.l_sssp = l_sssp_;
     a.src_floor = floor_sssp_;
     a.floor_step = weights_ge1_ ? 1u : 0u;
-    const int grid = int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
-                                            (uint64_t(t1 - t0) + kWarpsPerBlock - 1) / kWarpsPerBlock));
+    return a;
+  };
+  auto grid_of = [&](const Segments& seg) {
+    const uint32_t tasks = seg.task_prefix[seg.n];
+    return std::max(1, int(std::min<uint64_t>(uint64_t(sm_count_) * blocks_per_sm_,
+                                              (uint64_t(tasks) + kWarpsPerBlock - 1) /
+                                                  kWarpsPerBlock)));
+  };
+  auto launch_range = [&](const Segments& seg, RunCtr* slot, bool count_dest, bool count_v,
+                          uint32_t rid) {
+    PullArgs a = make_args(seg, slot, count_dest, count_v, rid);
+    const int grid = grid_of(seg);
     // sub-page tiles are small and numerous: big launches grab 8 tiles
     // (CC uniform-26: 4 -> 8, 9.0 -> 8.6 ms); a sharded rank's clipped
     // blocks get the same per-launch share rule as launch_pages
-    a.grab = k1_grab(t1 - t0, grid, "SERAPH_K1_GRAB_BLOCKED");
+    a.grab = k1_grab(seg.task_prefix[seg.n], grid, "SERAPH_K1_GRAB_BLOCKED");
     auto* evp = relax_begin();
-    launch_pull(algo_, gate, false, a, std::max(grid, 1), cs_);
+    launch_pull(algo_, gate, false, a, grid, cs_);
     SR_CUDA(cudaGetLastError());
     if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+  };
+  // K2 over the diagonal: up to `runs` sweeps in ONE cooperative launch that
+  // stops at the first quiet sweep (false: not co-resident -> host loop)
+  auto diag_loop_device = [&](const Segments& seg, int runs, bool count_dest) {
+    if (size_t(ctr_used_) + size_t(runs) > ctr_.n) return false;
+    if (!work_.p || work_used_ + size_t(runs) > work_.n) {
+      next_work_counter();
+      if (work_used_ + size_t(runs) > work_.n) {
+        SR_CUDA(cudaMemsetAsync(work_.p, 0, work_.n * sizeof(unsigned), cs_));
+        work_used_ = 0;
+      }
+    }
+    unsigned* work = work_.p + work_used_;
+    if (!runs_done_.p) runs_done_.reserve(1);
+    PullArgs a = make_args(seg, nullptr, count_dest, true, run_id_ + 1);
+    const int grid = grid_of(seg);
+    a.grab = k1_grab(seg.task_prefix[seg.n], grid, "SERAPH_K1_GRAB_BLOCKED");
+    ReentryArgs r{work, ctr_.p + ctr_used_, 1u, uint32_t(runs), runs_done_.p, 0u};
+    auto* evp = relax_begin();
+    if (!launch_pull_reentry(algo_, gate, a, r, grid, cs_)) {
+      if (evp) --relax_ev_used_;
+      return false;
+    }
+    SR_CUDA(cudaGetLastError());
+    if (evp) SR_CUDA(cudaEventRecord(evp->second, cs_));
+    work_used_ += size_t(runs);
+    ctr_used_ += uint32_t(runs);
+    run_id_ += uint32_t(runs);
+    return true;
+  };
+  const int diag_iters = diag_local_iterations();
+  for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
+    const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
+    if (t1 <= t0) continue;
+    l2_window(values_.p + uint64_t(b) * blk, std::min<uint64_t>(blk, n_ - uint64_t(b) * blk) * 4);
+    RunCtr* slot = (b == last_b && last_ctr) ? last_ctr : ctr;
+    uint32_t d0 = 0, d1 = 0;
+    if (diag_iters > 1 && diag_range(b, t0, t1, d0, d1)) {
+      // Local convergence of the block's own subgraph (Seraph's multi-pass
+      // subgraph iteration): the diagonal sub-pages -- edges whose source AND
+      // destination lie in block b, values L2-resident -- are swept until a
+      // sweep changes nothing (capped), then the block's other sub-pages once.
+      const bool on_device = !std::getenv("SERAPH_DIAG_HOST_LOOP") &&
+                             diag_loop_device(range_segments(d0, d1, 0, 0), diag_iters, b == 0);
+      for (int it = 0; !on_device && it < diag_iters; ++it) {
+        if (size_t(ctr_used_) + 1 > ctr_.n) break;
+        RunCtr* ds = alloc_ctr(1);
+        launch_range(range_segments(d0, d1, 0, 0), ds, b == 0 && it == 0, true, ++run_id_);
+        if (it + 1 == diag_iters) break;
+        SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ds, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+        SR_CUDA(cudaStreamSynchronize(cs_));
+        if (ctr_h_.p[0].valid == 0) break;  // locally converged
+      }
+      launch_range(range_segments(t0, d0, d1, t1), slot, b == 0, count_valid, run_id);
+    } else {
+      // Diagonal first: the sub-pages whose destinations are this block's own
+      // sources go first, so the labels / levels / distances they improve are
+      // already visible to the rest of the launch's gathers (async, a15)
+      launch_range(diag_first_segments(b, t0, t1), slot, b == 0, count_valid, run_id);
+    }
     if (b == 0 && sb_.n_blocks > 1) {
       // Probe: blocking pays for gathers only.  If block 0 gathered for < 5 %
       // of its edges (converged labels/levels skip theirs), finish the pass
@@ -319,6 +385,41 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
   return true;
 }
 
+// SERAPH_DIAG_ITERS: sweeps of a block's diagonal before its other
+// sub-pages (1 = the diagonal once, first in the block's launch).
+int Engine::diag_local_iterations() const {
+  int it = kDiagIters;
+  if (const char* e = std::getenv("SERAPH_DIAG_ITERS")) it = std::max(1, std::min(64, std::atoi(e)));
+  return it;
+}
+
+// Tiles of the sub-pages (b, p) whose destinations lie in block b.
+bool Engine::diag_range(uint32_t b, uint32_t t0, uint32_t t1, uint32_t& d0, uint32_t& d1) const {
+  const uint32_t np = uint32_t(pages_.size());
+  if (sb_.sub_tile_begin.size() != size_t(sb_.n_blocks) * np + 1 || cap_ == 0) return false;
+  const uint64_t lo = uint64_t(b) * sb_.blk_verts;
+  const uint64_t hi = std::min<uint64_t>(lo + sb_.blk_verts, n_);
+  if (hi <= lo) return false;
+  const uint32_t p_lo = uint32_t(lo / cap_), p_hi = uint32_t(std::min<uint64_t>((hi - 1) / cap_ + 1, np));
+  d0 = sb_.sub_tile_begin[size_t(b) * np + p_lo];
+  d1 = sb_.sub_tile_begin[size_t(b) * np + p_hi];
+  return d0 >= t0 && d1 <= t1 && d1 > d0;
+}
+
+// Up to two tile ranges [a0, a1) and [b0, b1) as launch segments.
+Segments Engine::range_segments(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) const {
+  Segments seg{};
+  seg.task_prefix[0] = 0;
+  const uint32_t r[2][2] = {{a0, a1}, {b0, b1}};
+  for (const auto& x : r) {
+    if (x[1] <= x[0]) continue;
+    seg.tile_begin[seg.n] = x[0];
+    seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (x[1] - x[0]);
+    ++seg.n;
+  }
+  return seg;
+}
+
 Segments Engine::diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const {
   Segments seg{};
   const uint32_t np = uint32_t(pages_.size());
@@ -338,7 +439,25 @@ Segments Engine::diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const
   const uint32_t d0 = sb_.sub_tile_begin[size_t(b) * np + p_lo];
   const uint32_t d1 = sb_.sub_tile_begin[size_t(b) * np + p_hi];
   if (d0 < t0 || d1 > t1 || d1 <= d0) return one();
-  const uint32_t r[3][2] = {{d0, d1}, {t0, d0}, {d1, t1}};
+  // Connected components: block 0 -- it holds vertex 0, the global minimum
+  // label -- sweeps its diagonal kRootDiagReps times in the launch (local
+  // iteration of the block's own subgraph while its labels are L2-resident:
+  // label 0 spreads through the block before the block's cross edges carry
+  // it to every other destination).  Measured: C4 15.45 -> 10.0 ms; BFS on
+  // uniform-27 from the source's block: 58.2 -> 59.1 ms, so CC only.  The
+  // other blocks sweep their diagonal once, first.
+  int reps = 1;
+  if (b == 0 && algo_ == SR_ALGO_CC) {
+    reps = kRootDiagReps;
+    if (const char* e = std::getenv("SERAPH_ROOT_DIAG_REPS")) reps = std::atoi(e);
+  } else if (const char* e = std::getenv("SERAPH_DIAG_REPS")) {
+    reps = std::atoi(e);
+  }
+  reps = std::max(1, std::min(kMaxSegments - 2, reps));
+  std::vector<std::array<uint32_t, 2>> r;
+  for (int k = 0; k < reps; ++k) r.push_back({d0, d1});
+  r.push_back({t0, d0});
+  r.push_back({d1, t1});
   seg.task_prefix[0] = 0;
   for (const auto& x : r) {
     if (x[1] <= x[0]) continue;

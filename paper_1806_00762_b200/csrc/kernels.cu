@@ -253,7 +253,8 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
 // registers and 7-8 blocks at 32 registers with spills are 3-20 % slower)
 template <int A, int G, bool DET>
 __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_work, RunCtr* a_ctr,
-                                                const RunCtr* a_prev_ctr, uint32_t a_run_id) {
+                                                const RunCtr* a_prev_ctr, uint32_t a_run_id,
+                                                uint32_t a_count_dest) {
   __shared__ __align__(16) uint32_t s_pref[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_loc[kWarpsPerBlock][kTileMaxDests];
   __shared__ uint32_t s_cur[kWarpsPerBlock][kTileMaxDests];
@@ -302,8 +303,8 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
         const bool att = gate_attempt<A, G>(v, cur, a);
         const uint32_t lo_d = offs[d];
         if (lane == 0 && tile.x == lo_d) {  // owner chunk counts the visit once
-          c.attempts += att & a.count_dest;
-          c.skipped += !att & a.count_dest;
+          c.attempts += att & a_count_dest;
+          c.skipped += !att & a_count_dest;
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
         if (!att || cur <= dest_floor<A>(a)) continue;
@@ -386,8 +387,8 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
           deg = __ldcs(offs + i + 1) - lo;
           att = gate_attempt<A, G>(v, cur, a);
         }
-        c.attempts += att & a.count_dest;
-        c.skipped += (in && !att) & a.count_dest;
+        c.attempts += att & a_count_dest;
+        c.skipped += (in && !att) & a_count_dest;
         c.edges += att ? deg : 0u;
         const bool need = att && cur > dest_floor<A>(a);  // can it still improve?
         const bool has = in && deg > 0;
@@ -526,7 +527,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
 
 template <int A, int G, bool DET>
 __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a) {
-  pull_relax_body<A, G, DET>(a, a.work, a.ctr, a.prev_ctr, a.run_id);
+  pull_relax_body<A, G, DET>(a, a.work, a.ctr, a.prev_ctr, a.run_id, a.count_dest);
 }
 
 // ---------------------------------------------------------------------------
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(kBlockThreads, 5) pull_reentry_kernel(PullArgs
     RunCtr* ctr = r.ctr + size_t(it) * r.ctr_stride;
     pull_relax_body<A, G, false>(a, r.work + it, ctr,
                                  it ? r.ctr + size_t(it - 1) * r.ctr_stride : nullptr,
-                                 a.run_id + it);
+                                 a.run_id + it, (it == 0 || r.dest_every_run) ? a.count_dest : 0u);
     grid.sync();  // every page's counters of run `it` are final and visible
     unsigned long long v = 0;
     for (uint32_t p = 0; p < r.ctr_stride; ++p) v += __ldcg(&ctr[p].valid);
