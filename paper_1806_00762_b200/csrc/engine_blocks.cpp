@@ -3,7 +3,6 @@
 #include "engine.h"
 
 #include <algorithm>
-#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -333,6 +332,8 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     return true;
   };
   const int diag_iters = diag_local_iterations();
+  int root_reps = algo_ == SR_ALGO_CC ? kRootDiagReps : 1;
+  if (const char* e = std::getenv("SERAPH_ROOT_DIAG_REPS")) root_reps = std::max(1, std::min(64, std::atoi(e)));
   for (uint32_t b = 0; b < sb_.n_blocks; ++b) {
     const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
     if (t1 <= t0) continue;
@@ -356,6 +357,18 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
         if (ctr_h_.p[0].valid == 0) break;  // locally converged
       }
       launch_range(range_segments(t0, d0, d1, t1), slot, b == 0, count_valid, run_id);
+    } else if (root_reps > 1 && b == 0 && diag_range(b, t0, t1, d0, d1)) {
+      // Connected components: block 0 -- it holds vertex 0, the global
+      // minimum label -- sweeps its own subgraph (the diagonal sub-pages,
+      // labels L2-resident) root_reps times before its cross-block edges
+      // carry label 0 to every other destination (local iteration of the
+      // resident subgraph).  One launch per sweep: K1's phase C stores
+      // assume one writer per destination per launch.  Measured: C4 15.45 ->
+      // 10.0 ms (2 passes instead of 3); BFS on uniform-27 from the source's
+      // block 58.2 -> 59.1 ms, so CC only.
+      for (int r = 0; r < root_reps; ++r)
+        launch_range(range_segments(d0, d1, 0, 0), slot, r == 0, count_valid, run_id);
+      launch_range(range_segments(t0, d0, d1, t1), slot, true, count_valid, run_id);
     } else {
       // Diagonal first: the sub-pages whose destinations are this block's own
       // sources go first, so the labels / levels / distances they improve are
@@ -367,6 +380,9 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
       // of its edges (converged labels/levels skip theirs), finish the pass
       // with one unblocked sweep instead of n_blocks - 1 more destination
       // passes (its relaxations are idempotent; the counters restart).
+      // (Measured and dropped: also finishing unblocked when < 1 % of the
+      // destinations are still above the floor after block 0 -- on C4 that
+      // never fired, and its count + sync cost 0.2 ms.)
       SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
       SR_CUDA(cudaStreamSynchronize(cs_));
       const RunCtr& c0 = ctr_h_.p[0];
@@ -421,48 +437,13 @@ Segments Engine::range_segments(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t 
 }
 
 Segments Engine::diag_first_segments(uint32_t b, uint32_t t0, uint32_t t1) const {
-  Segments seg{};
-  const uint32_t np = uint32_t(pages_.size());
-  auto one = [&]() {
-    seg.n = 1;
-    seg.tile_begin[0] = t0;
-    seg.task_prefix[0] = 0;
-    seg.task_prefix[1] = t1 - t0;
-    return seg;
-  };
-  if (std::getenv("SERAPH_NO_DIAG_FIRST") || sb_.sub_tile_begin.size() != size_t(sb_.n_blocks) * np + 1 ||
-      cap_ == 0)
-    return one();
-  const uint64_t lo = uint64_t(b) * sb_.blk_verts;
-  const uint64_t hi = std::min<uint64_t>(lo + sb_.blk_verts, n_);
-  const uint32_t p_lo = uint32_t(lo / cap_), p_hi = uint32_t(std::min<uint64_t>((hi - 1) / cap_ + 1, np));
-  const uint32_t d0 = sb_.sub_tile_begin[size_t(b) * np + p_lo];
-  const uint32_t d1 = sb_.sub_tile_begin[size_t(b) * np + p_hi];
-  if (d0 < t0 || d1 > t1 || d1 <= d0) return one();
-  // Connected components: block 0 -- it holds vertex 0, the global minimum
-  // label -- sweeps its diagonal kRootDiagReps times in the launch (local
-  // iteration of the block's own subgraph while its labels are L2-resident:
-  // label 0 spreads through the block before the block's cross edges carry
-  // it to every other destination).  Measured: C4 15.45 -> 10.0 ms; BFS on
-  // uniform-27 from the source's block: 58.2 -> 59.1 ms, so CC only.  The
-  // other blocks sweep their diagonal once, first.
-  int reps = 1;
-  if (b == 0 && algo_ == SR_ALGO_CC) {
-    reps = kRootDiagReps;
-    if (const char* e = std::getenv("SERAPH_ROOT_DIAG_REPS")) reps = std::atoi(e);
-  } else if (const char* e = std::getenv("SERAPH_DIAG_REPS")) {
-    reps = std::atoi(e);
-  }
-  reps = std::max(1, std::min(kMaxSegments - 2, reps));
-  std::vector<std::array<uint32_t, 2>> r;
-  for (int k = 0; k < reps; ++k) r.push_back({d0, d1});
-  r.push_back({t0, d0});
-  r.push_back({d1, t1});
-  seg.task_prefix[0] = 0;
-  for (const auto& x : r) {
-    if (x[1] <= x[0]) continue;
-    seg.tile_begin[seg.n] = x[0];
-    seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (x[1] - x[0]);
+  uint32_t d0 = 0, d1 = 0;
+  if (std::getenv("SERAPH_NO_DIAG_FIRST") || !diag_range(b, t0, t1, d0, d1))
+    return range_segments(t0, t1, 0, 0);
+  Segments seg = range_segments(d0, d1, t0, d0);  // the diagonal, then the tiles before it
+  if (d1 < t1) {                                  // and the tiles after it
+    seg.tile_begin[seg.n] = d1;
+    seg.task_prefix[seg.n + 1] = seg.task_prefix[seg.n] + (t1 - d1);
     ++seg.n;
   }
   return seg;

@@ -31,6 +31,7 @@ void launch_pr_hot_gather(const uint32_t* hot_vertex, uint32_t n_hot, const floa
                           float* hot_contrib, cudaStream_t s);
 void launch_count_deg_ge(const uint32_t* deg, uint32_t n, uint32_t d, unsigned long long* out,
                          cudaStream_t s);
+
 void launch_hot_assign(const uint32_t* deg, uint32_t n, uint32_t d, uint32_t cap,
                        unsigned* counter, uint32_t* slot_of, uint32_t* hot_vertex, cudaStream_t s);
 void launch_hot_encode(const uint32_t* in, uint32_t* out, uint64_t words, const uint32_t* slot_of,
