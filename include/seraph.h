@@ -148,6 +148,10 @@ typedef struct {
   double relax_seconds;    /* sum of timed K1/K8 launch durations (profile_kernels) */
   uint64_t relax_launches;
   uint64_t gathers;        /* source values K1/K8 actually loaded (skips excluded) */
+  /* edges whose source (+ weight) K1 streamed in: edges of destinations that
+   * cannot improve are counted in edges_read (the reference's definition)
+   * but never loaded */
+  uint64_t edges_streamed;
 } sr_metrics;
 
 typedef struct {

@@ -145,6 +145,7 @@ class MetricsC(C.Structure):
         ("relax_seconds", C.c_double),
         ("relax_launches", C.c_uint64),
         ("gathers", C.c_uint64),
+        ("edges_streamed", C.c_uint64),
     ]
 
 

@@ -56,6 +56,7 @@ struct RunCtr {
   unsigned long long skipped;
   unsigned long long edges;
   unsigned long long gathers;  // source values actually loaded (roofline bytes)
+  unsigned long long streamed;  // edges whose source (+ weight) K1 actually streamed in
 };
 
 // Scalars produced by the per-pass census (K4/K5), read back once per pass.

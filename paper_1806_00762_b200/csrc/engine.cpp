@@ -1295,6 +1295,7 @@ PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool reco
     st.skipped = ctr_h_.p[0].skipped;
     st.edges = ctr_h_.p[0].edges;
     gathers_total_ += ctr_h_.p[0].gathers;
+    streamed_total_ += ctr_h_.p[0].streamed;
     return st;
   };
   (void)np;
@@ -1531,6 +1532,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   profile_kernels_ = cfg.profile_kernels != 0;
   relax_ev_used_ = 0;
   gathers_total_ = 0;
+  streamed_total_ = 0;
   wtrace_.clear();
   wtrace_pool_used_ = 0;
   trace.clear();
@@ -1552,6 +1554,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   m.kernel_launches = kernel_launch_count() - launches0;  // every kernel of the run
   m.h2d_bytes = h2d_bytes_;
   m.gathers = gathers_total_;
+  m.edges_streamed = streamed_total_;
   finish_wall_trace();
   if (profile_kernels_) {
     m.relax_seconds = collect_relax_seconds();
@@ -1619,6 +1622,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     uint64_t gathers = 0;
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
       gathers += ctr_h_.p[i].gathers;
+      streamed_total_ += ctr_h_.p[i].streamed;
       st.attempts += ctr_h_.p[i].attempts;
       st.valid_updates += ctr_h_.p[i].valid;
       st.skipped += ctr_h_.p[i].skipped;

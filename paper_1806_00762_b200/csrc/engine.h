@@ -326,6 +326,7 @@ class Engine {
   uint32_t run_id_ = 0;
   uint64_t h2d_bytes_ = 0;
   uint64_t gathers_total_ = 0;
+  uint64_t streamed_total_ = 0;  // edges K1 streamed in (RunCtr::streamed)
   int blocks_per_sm_ = 4;
 
   // algorithm state of the current run

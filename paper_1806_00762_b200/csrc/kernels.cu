@@ -134,8 +134,9 @@ struct ActEntry {
 struct LaneCtr {
   uint32_t attempts, valid, skipped, gathers;
   unsigned long long edges;
+  uint32_t runs;  // warp-uniform: 8-edge runs streamed in (x8 = RunCtr::streamed)
   __device__ void clear() {
-    attempts = valid = skipped = gathers = 0;
+    attempts = valid = skipped = gathers = runs = 0;
     edges = 0;
   }
 };
@@ -151,6 +152,7 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
     if (sk) atomicAdd(&dst->skipped, sk);
     if (ed) atomicAdd(&dst->edges, ed);
     if (ga) atomicAdd(&dst->gathers, ga);
+    if (c.runs) atomicAdd(&dst->streamed, 8ull * c.runs);
   }
   c.clear();
 }
@@ -198,7 +200,7 @@ __device__ __forceinline__ uint32_t dest_floor(const PullArgs& a) {
 template <int W = kWarpsPerBlock>
 __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t lane_min,
                                             Census* census, uint32_t* scratch) {
-  constexpr int kCtr = 5;
+  constexpr int kCtr = 6;
   constexpr int kWarpsPerBlock = W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
@@ -206,7 +208,8 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
   const unsigned long long v[kCtr] = {warp_sum<unsigned long long>(c.attempts),
                                       warp_sum<unsigned long long>(c.valid),
                                       warp_sum<unsigned long long>(c.skipped), warp_sum(c.edges),
-                                      warp_sum<unsigned long long>(c.gathers)};
+                                      warp_sum<unsigned long long>(c.gathers),
+                                      8ull * c.runs};  // runs: warp-uniform
   lane_min = warp_min(lane_min);
   __syncthreads();  // every warp is done with its tile scratch
   if (lane == 0) {
@@ -308,6 +311,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
           c.edges += att ? (unsigned long long)(offs[d + 1] - lo_d) : 0ull;
         }
         if (!att || cur <= dest_floor<A>(a)) continue;
+        c.runs += (tile.y - (tile.x & ~7u) + 7) >> 3;
         const uint32_t thr = cur - source_floor<A>(a);  // live edges: w < thr
         // lanes take aligned 8-edge runs (two uint4 loads of sources and
         // weights), drop edges that cannot improve, gather the rest back to
@@ -424,6 +428,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
       // ---- phase B: aligned 8-edge runs, vector loads, masked gathers --------
       for (uint32_t r0 = 0; r0 < span; r0 += 32 * kLaneEdges) {
         const uint32_t pos0 = r0 + lane * kLaneEdges;
+        bool loaded = false;  // this lane streams its run in (live positions)
         if (pos0 < span && pos0 + kLaneEdges > lo_pos) {
           const uint32_t q = max(pos0, lo_pos);
           // runs are 8-aligned, so the run's 8 positions sit in one bitmap word
@@ -449,6 +454,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
               ++e;
             }
           }
+          loaded = live != 0;
           if (live) {
             const uint4* sp = reinterpret_cast<const uint4*>(src + ebase + pos0);
             const uint4 s0 = __ldcs(sp), s1 = __ldcs(sp + 1);
@@ -495,6 +501,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
             atomicMin(best_of + run_ent, run_best);
           }
         }
+        c.runs += __popc(__ballot_sync(kFull, loaded));
       }
       __syncwarp();
       // ---- phase C: one lane per attempted destination stores its minimum ---

@@ -639,6 +639,15 @@ def test_pull_source_blocked(blk, monkeypatch):
             r = eng.run_graph(csr2, pages2, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
             assert np.array_equal(r.values, want), pred
             assert eng.verify_fixpoint(ps.AlgoKind.CC, r.values) == 0
+            # settled label-0 groups are skipped but counted as the gate counts
+            # them: every dense pass attempts each destination once, and every
+            # dense pass after the first (whose block-0 subgraph sweeps re-read
+            # edges) reads each in-edge once
+            if pred == ps.PredictorMode.OFF:
+                dense = [st for st in r.metrics.per_pass if st.kind != ps.PassKind.SPARSE_PUSH]
+                assert all(st.attempts == n for st in dense), [st.attempts for st in dense]
+                assert all(st.edges_read == sym.num_edges() for st in dense[1:])
+                assert dense[0].edges_read >= sym.num_edges()
         # resident reentry over the blocked sweeps (re-run the set while it changes)
         for kind, g, cs, pg in ((ps.AlgoKind.BFS, el, csr, pages), (ps.AlgoKind.SSSP, el, csr, pages),
                                 (ps.AlgoKind.CC, sym, csr2, pages2)):
