@@ -248,10 +248,11 @@ def profile_traffic(key):
 def k1_roofline(a, runs, info, clocks, step_s):
     """K1 (dense pull, incl. source-blocked launches) per launch against HBM.
     SURVEY §8(d) per-unit bytes -- per edge 4 B in_sources (+4 B weight for
-    SSSP) + 4 B gathered value, per attempted destination 8 B (in_offsets +
-    value; +1 B status under the weak predictor), per valid update 4 B --
-    applied to the units K1 actually processes: the edges it streams in
-    (`edges_streamed`) and the source values it gathers (`gathers`).  Edges of
+    SSSP) + 4 B gathered value, per destination 8 B (in_offsets + value; +1 B
+    status under the weak predictor), per valid update 4 B -- applied to the
+    units K1 actually processes: the edges it streams in (`edges_streamed`),
+    the source values it gathers (`gathers`) and the destinations its phase A
+    scans (`dest_visits`: once per launch, i.e. once per source block).  Edges of
     destinations that provably cannot improve (at the floor) are counted in the
     reference's edges_read but never loaded; `reference_units_model` charges
     §8(d) on edges_read as well (it exceeds 1 when such skips dominate)."""
@@ -264,9 +265,10 @@ def k1_roofline(a, runs, info, clocks, step_s):
         for st in r.metrics.per_pass:
             if st.kind != ps.PassKind.SPARSE_PUSH:
                 bref += (per_src + 4) * st.edges_read + per_dest * st.attempts + 4 * st.valid_updates
-                b8d += per_dest * st.attempts + 4 * st.valid_updates
+                b8d += 4 * st.valid_updates
                 edges += st.edges_read
-        b8d += per_src * r.metrics.edges_streamed + 4 * r.metrics.gathers
+        b8d += (per_src * r.metrics.edges_streamed + 4 * r.metrics.gathers +
+                per_dest * r.metrics.dest_visits)
         gathers += r.metrics.gathers
         streamed += r.metrics.edges_streamed
         k1_s += r.metrics.relax_seconds
@@ -280,14 +282,15 @@ def k1_roofline(a, runs, info, clocks, step_s):
             "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
             "peak_source": src, "traffic": profile_traffic(f"{a.algo}-s{a.scale}"),
             "model": f"SURVEY §8(d) per-unit bytes on the units K1 processes: {per_src} B/edge "
-                     f"streamed + 4 B/gathered source + {per_dest} B/attempted destination + "
+                     f"streamed + 4 B/gathered source + {per_dest} B/destination scanned + "
                      "4 B/valid update",
             "algorithmic_bytes_per_launch": int(b8d / launches),
             "launch_ms": round(k1_s / launches * 1e3, 4), "launches": launches,
             "share_of_step": round(k1_s / (step_s * len(runs)), 3),
             "units_per_run": {"edges_read_reference": edges // len(runs),
                               "edges_streamed": streamed // len(runs),
-                              "gathers": gathers // len(runs)},
+                              "gathers": gathers // len(runs),
+                              "dest_visits": sum(r.metrics.dest_visits for r in runs) // len(runs)},
             "reference_units_model": {
                 "achieved": round(ref, 1), "frac": round(ref / peak, 4),
                 "bytes_per_launch": int(bref / launches),

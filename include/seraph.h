@@ -152,6 +152,9 @@ typedef struct {
    * cannot improve are counted in edges_read (the reference's definition)
    * but never loaded */
   uint64_t edges_streamed;
+  /* destinations K1's phase A scanned (value + in_offsets read), every
+   * launch: a source-blocked pass scans each destination once per block */
+  uint64_t dest_visits;
 } sr_metrics;
 
 typedef struct {

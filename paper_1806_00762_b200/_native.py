@@ -146,6 +146,7 @@ class MetricsC(C.Structure):
         ("relax_launches", C.c_uint64),
         ("gathers", C.c_uint64),
         ("edges_streamed", C.c_uint64),
+        ("dest_visits", C.c_uint64),
     ]
 
 

@@ -57,6 +57,7 @@ struct RunCtr {
   unsigned long long edges;
   unsigned long long gathers;  // source values actually loaded (roofline bytes)
   unsigned long long streamed;  // edges whose source (+ weight) K1 actually streamed in
+  unsigned long long visits;    // destinations K1's phase A scanned (value + offsets read)
 };
 
 // Scalars produced by the per-pass census (K4/K5), read back once per pass.

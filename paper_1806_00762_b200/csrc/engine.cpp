@@ -1296,6 +1296,7 @@ PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool reco
     st.edges = ctr_h_.p[0].edges;
     gathers_total_ += ctr_h_.p[0].gathers;
     streamed_total_ += ctr_h_.p[0].streamed;
+    visits_total_ += ctr_h_.p[0].visits;
     return st;
   };
   (void)np;
@@ -1533,6 +1534,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   relax_ev_used_ = 0;
   gathers_total_ = 0;
   streamed_total_ = 0;
+  visits_total_ = 0;
   wtrace_.clear();
   wtrace_pool_used_ = 0;
   trace.clear();
@@ -1555,6 +1557,7 @@ void Engine::run(const sr_run_config& cfg, uint32_t* values_out, float* ranks_ou
   m.h2d_bytes = h2d_bytes_;
   m.gathers = gathers_total_;
   m.edges_streamed = streamed_total_;
+  m.dest_visits = visits_total_;
   finish_wall_trace();
   if (profile_kernels_) {
     m.relax_seconds = collect_relax_seconds();
@@ -1623,6 +1626,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
       gathers += ctr_h_.p[i].gathers;
       streamed_total_ += ctr_h_.p[i].streamed;
+      visits_total_ += ctr_h_.p[i].visits;
       st.attempts += ctr_h_.p[i].attempts;
       st.valid_updates += ctr_h_.p[i].valid;
       st.skipped += ctr_h_.p[i].skipped;

@@ -327,6 +327,7 @@ class Engine {
   uint64_t h2d_bytes_ = 0;
   uint64_t gathers_total_ = 0;
   uint64_t streamed_total_ = 0;  // edges K1 streamed in (RunCtr::streamed)
+  uint64_t visits_total_ = 0;    // destinations K1 scanned (RunCtr::visits)
   int blocks_per_sm_ = 4;
 
   // algorithm state of the current run

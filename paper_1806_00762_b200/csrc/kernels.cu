@@ -134,9 +134,10 @@ struct ActEntry {
 struct LaneCtr {
   uint32_t attempts, valid, skipped, gathers;
   unsigned long long edges;
-  uint32_t runs;  // warp-uniform: 8-edge runs streamed in (x8 = RunCtr::streamed)
+  uint32_t runs;    // warp-uniform: 8-edge runs streamed in (x8 = RunCtr::streamed)
+  uint32_t visits;  // warp-uniform: destinations scanned by phase A (RunCtr::visits)
   __device__ void clear() {
-    attempts = valid = skipped = gathers = runs = 0;
+    attempts = valid = skipped = gathers = runs = visits = 0;
     edges = 0;
   }
 };
@@ -153,6 +154,7 @@ __device__ __forceinline__ void flush_ctr(LaneCtr& c, RunCtr* dst, int lane) {
     if (ed) atomicAdd(&dst->edges, ed);
     if (ga) atomicAdd(&dst->gathers, ga);
     if (c.runs) atomicAdd(&dst->streamed, 8ull * c.runs);
+    if (c.visits) atomicAdd(&dst->visits, (unsigned long long)c.visits);
   }
   c.clear();
 }
@@ -200,7 +202,7 @@ __device__ __forceinline__ uint32_t dest_floor(const PullArgs& a) {
 template <int W = kWarpsPerBlock>
 __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t lane_min,
                                             Census* census, uint32_t* scratch) {
-  constexpr int kCtr = 6;
+  constexpr int kCtr = 7;
   constexpr int kWarpsPerBlock = W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* red = reinterpret_cast<unsigned long long*>(scratch);
@@ -209,7 +211,8 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
                                       warp_sum<unsigned long long>(c.valid),
                                       warp_sum<unsigned long long>(c.skipped), warp_sum(c.edges),
                                       warp_sum<unsigned long long>(c.gathers),
-                                      8ull * c.runs};  // runs: warp-uniform
+                                      8ull * c.runs,  // runs, visits: warp-uniform
+                                      (unsigned long long)c.visits};
   lane_min = warp_min(lane_min);
   __syncthreads();  // every warp is done with its tile scratch
   if (lane == 0) {
@@ -312,6 +315,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
         }
         if (!att || cur <= dest_floor<A>(a)) continue;
         c.runs += (tile.y - (tile.x & ~7u) + 7) >> 3;
+        c.visits += tile.x == lo_d;  // the hub's first chunk reads its value and offsets
         const uint32_t thr = cur - source_floor<A>(a);  // live edges: w < thr
         // lanes take aligned 8-edge runs (two uint4 loads of sources and
         // weights), drop edges that cannot improve, gather the rest back to
@@ -371,6 +375,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
       const uint32_t ebase = tile.x & ~7u;  // 32-byte aligned run grid
       uint32_t n_ent = 0;
       unsigned any_att = 0, any_dead = 0;
+      c.visits += dh - dl;
       // entry starts as a bitmap over the tile's edge positions (span <=
       // kTileEdgeBudget + 7 -> <= 33 words) + per-word prefix counts: a run's
       // first entry and its entry steps come from one word, no search

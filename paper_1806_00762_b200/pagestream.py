@@ -471,6 +471,7 @@ class MetricsReport:
     relax_launches: int = 0
     gathers: int = 0
     edges_streamed: int = 0
+    dest_visits: int = 0
 
     def throughput(self) -> float:  # metrics.hpp:51-56
         t = self.wall_seconds if self.wall_seconds > 0 else self.virtual_makespan
@@ -531,7 +532,8 @@ def _metrics_from_c(m: N.MetricsC, passes) -> MetricsReport:
               "bytes_transferred", "update_attempts", "valid_updates", "skipped_vertices",
               "edges_read", "virtual_makespan", "wall_seconds", "device_seconds",
               "upload_seconds", "kernel_launches", "kernel_runs", "h2d_bytes", "d2h_bytes",
-              "relax_seconds", "relax_launches", "gathers", "edges_streamed"):
+              "relax_seconds", "relax_launches", "gathers", "edges_streamed",
+              "dest_visits"):
         setattr(r, f, getattr(m, f))
     if m.has_prediction_accuracy:
         r.prediction_accuracy = m.prediction_accuracy
