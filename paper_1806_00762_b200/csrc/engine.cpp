@@ -1155,14 +1155,17 @@ PassOut Engine::dense_pass_wall(const sr_run_config& cfg, int gate, bool recover
         if (ctr_h_.p[0].valid == 0) break;  // quiet: locally converged
         slot = alloc_ctr(1);
         trace_reentry_ = true;
-        if (!pull_blocked_pass(gate, slot, true))  // probe: gathers are rare now
+        if (!pull_blocked_pass(gate, slot, true)) {  // probe: gathers are rare now
+          slot = alloc_ctr(1);  // the blocked attempt released its slots (zeroed)
           launch_pages(order, gate, false, slot, nullptr, false, false);
+        }
         trace_reentry_ = false;
         po.kernel_runs += order.size();
       }
       return po;
     }
-    --ctr_used_;  // the (zeroed) probe slot is the first one the unblocked steps take
+    // (the probe zeroed the reference counters of this pass's blocked slots;
+    // the unblocked steps below count the pass afresh)
     // a probed pass falls back after block 0 already applied some updates:
     // count valid updates as the destinations changed in the pass
     last_pass_blocked_ = sb_.built && pull_block_verts() != 0;
@@ -1591,6 +1594,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   last_gather_frac_ = 1.0;  // the first dense pass gathers
   last_block_gather_frac_ = 1.0;
   sb_last_slot_ = -1;
+  fallback_frac_ = -1;
   ctr_used_ = 0;
   if (algo_ != SR_ALGO_CC && queue_mode() && has_csr_ && !weak) {  // weak: census seeds the DFA histogram
     // the initial frontier {source} directly as a queue
@@ -1638,6 +1642,10 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     if (sb_last_slot_ >= 0 && size_t(sb_last_slot_) < size_t(ctr_used_)) {
       const RunCtr& lc = ctr_h_.p[sb_last_slot_];
       if (lc.edges) last_block_gather_frac_ = double(lc.gathers) / double(lc.edges);
+    }
+    if (fallback_frac_ >= 0) {  // the pass finished unblocked after a rare-gathers probe
+      last_block_gather_frac_ = fallback_frac_;
+      fallback_frac_ = -1;
     }
     sb_last_slot_ = -1;
   };

@@ -418,6 +418,7 @@ class Engine {
   bool diag_range(uint32_t b, uint32_t t0, uint32_t t1, uint32_t& d0, uint32_t& d1) const;
   Segments range_segments(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) const;
   int diag_local_iterations() const;
+  bool probe_every_block() const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   // A blocked pass's last block launch counts into its own slot: when even
@@ -425,6 +426,7 @@ class Engine {
   // sweeps unblocked without probing block 0 first.
   int sb_last_slot_ = -1;
   double last_block_gather_frac_ = 1.0;
+  double fallback_frac_ = -1;  // gathers/edges of the probe that ended a blocked pass
   std::pair<cudaEvent_t, cudaEvent_t>* relax_begin();
   void l2_window(const void* base, size_t bytes);
   int l2_persist_max_ = -1;  // persisting-L2 carve-out (bytes; 0 = unavailable/disabled)

@@ -338,7 +338,11 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     const uint32_t t0 = sb_.block_tile_begin[b], t1 = sb_.block_tile_begin[b + 1];
     if (t1 <= t0) continue;
     l2_window(values_.p + uint64_t(b) * blk, std::min<uint64_t>(blk, n_ - uint64_t(b) * blk) * 4);
-    RunCtr* slot = (b == last_b && last_ctr) ? last_ctr : ctr;
+    // every block but the last counts into its own slot: the probe below
+    // reads each block's gathers / edges
+    RunCtr* slot = (b == last_b && last_ctr) ? last_ctr
+                   : (b == 0 || size_t(ctr_used_) + 1 > ctr_.n) ? ctr
+                                                                : alloc_ctr(1);
     uint32_t d0 = 0, d1 = 0;
     if (diag_iters > 1 && diag_range(b, t0, t1, d0, d1)) {
       // Local convergence of the block's own subgraph (Seraph's multi-pass
@@ -375,23 +379,27 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
       // already visible to the rest of the launch's gathers (async, a15)
       launch_range(diag_first_segments(b, t0, t1), slot, b == 0, count_valid, run_id);
     }
-    if (b == 0 && sb_.n_blocks > 1) {
-      // Probe: blocking pays for gathers only.  If block 0 gathered for < 5 %
-      // of its edges (converged labels/levels skip theirs), finish the pass
-      // with one unblocked sweep instead of n_blocks - 1 more destination
-      // passes (its relaxations are idempotent; the counters restart).
-      // (Measured and dropped: also finishing unblocked when < 1 % of the
-      // destinations are still above the floor after block 0 -- on C4 that
-      // never fired, and its count + sync cost 0.2 ms.)
-      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
+    if (b < last_b && (b == 0 || probe_every_block())) {
+      // Probe: blocking pays for gathers only.  If this block gathered for
+      // < 5 % of its edges (converged labels/levels skip theirs), finish the
+      // pass with one unblocked sweep -- destinations at the floor read no
+      // edges there -- instead of more block launches that each scan every
+      // destination (the relaxations are idempotent; the pass's counters
+      // restart).  (Measured and dropped: finishing unblocked when < 1 % of
+      // the destinations are still above the floor after block 0 -- on C4
+      // that never fired, and its count + sync cost 0.2 ms.)
+      SR_CUDA(cudaMemcpyAsync(ctr_h_.p, slot, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
       SR_CUDA(cudaStreamSynchronize(cs_));
       const RunCtr& c0 = ctr_h_.p[0];
       if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
-        SR_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RunCtr), cs_));
-        if (last_ctr) {  // the unblocked finish reuses the slots from the probe's on
-          --ctr_used_;
-          sb_last_slot_ = -1;
-        }
+        // the reference's per-pass counters (attempts, valid, skipped,
+        // edges_read) restart with the unblocked sweep; the work counters
+        // (gathers, edges streamed, destinations scanned) keep what the
+        // blocked launches did
+        const size_t from = size_t(ctr - ctr_.p), k = size_t(ctr_used_) - from;
+        SR_CUDA(cudaMemset2DAsync(ctr, sizeof(RunCtr), 0, 4 * sizeof(unsigned long long), k, cs_));
+        sb_last_slot_ = -1;
+        fallback_frac_ = double(c0.gathers) / double(c0.edges);
         l2_window(nullptr, 0);
         return false;
       }
@@ -399,6 +407,12 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
   }
   l2_window(nullptr, 0);
   return true;
+}
+
+// SERAPH_PROBE_BLOCKS=0: probe block 0 only (the round-1 rule).
+bool Engine::probe_every_block() const {
+  const char* e = std::getenv("SERAPH_PROBE_BLOCKS");
+  return !e || std::atoi(e) != 0;
 }
 
 // SERAPH_DIAG_ITERS: sweeps of a block's diagonal before its other
