@@ -1035,6 +1035,16 @@ def test_sharded_rounds_loopback_world(world, blocked, peer, monkeypatch):
                 for r in res:
                     assert np.array_equal(r.values, want), (kind, pred, ex)
                 assert len({r.metrics.passes for r in res}) == 1  # same decisions
+        # reentry: each rank re-runs its own shard until locally quiet (up to
+        # MRT) before the round's exchange (SURVEY §8(e) "local iteration")
+        k += 1
+        c = cfg_of(mode=ps.ScheduleModeKind.REENTRY, pred=ps.PredictorMode.STRONG,
+                   clock=ps.ClockMode.WALL)
+        c.schedule.max_reentry_times = 3
+        res = _run_world(world, g, program_for(kind, 2, g), c, n // 16,
+                         f"w{world}-{int(blocked)}-{int(peer)}-{k}", peer)
+        for r in res:
+            assert np.array_equal(r.values, want), (kind, "reentry")
     pr = ps.EdgeList(n, src, dst, np.zeros(0, np.uint32))
     res = _run_world(world, pr, ps.make_pagerank(), ps.EngineConfig(clock=ps.ClockMode.WALL),
                      n // 16, f"w{world}-{int(blocked)}-{int(peer)}-pr", peer)
