@@ -1449,9 +1449,17 @@ void Engine::push_pass(const sr_run_config& cfg, RunStats& st) {
   (void)st;
 }
 
-void Engine::exchange_round(bool pagerank) {
+void Engine::exchange_round(bool pagerank, uint32_t ctr_from) {
+  agg_slot_ = -1;
   if (!attached()) return;  // attached to a world (any size, incl. 1): merge every round
   SR_CUDA(cudaSetDevice(dev_));
+  // The round's counters travel as ONE aggregate entry (sum of this round's
+  // slots): ranks may use different numbers of slots in a pass (per-block
+  // probes, fallbacks), so the slot arrays do not line up across ranks.
+  RunCtr* agg = alloc_ctr(1);
+  agg_slot_ = int(agg - ctr_.p);
+  launch_sum_ctr_slots(ctr_.p, ctr_from, uint32_t(agg_slot_), agg, cs_);
+  const size_t agg_words = sizeof(RunCtr) / 8;
   if (n_peers_ && !pagerank) {
     // peer exchange: every improvement is already in every replica once all
     // ranks' kernels of the round have finished -- barrier, then only the
@@ -1459,16 +1467,14 @@ void Engine::exchange_round(bool pagerank) {
     round_barrier();
     if (loop_) {
       loopback_allreduce(loop_, rank_, &census_.p->min_changed, 1, kLoopU32, kLoopMin, cs_);
-      loopback_allreduce(loop_, rank_, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8),
-                         kLoopU64, kLoopSum, cs_);
+      loopback_allreduce(loop_, rank_, agg, agg_words, kLoopU64, kLoopSum, cs_);
     } else {
       const NcclApi& nc = nccl();
       nc.GroupStart();
       ncclResult_t r = nc.AllReduce(&census_.p->min_changed, &census_.p->min_changed, 1,
                                     ncclUint32, ncclMin, comm_, cs_);
-      if (r == ncclSuccess && ctr_used_)
-        r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), ncclUint64,
-                         ncclSum, comm_, cs_);
+      if (r == ncclSuccess)
+        r = nc.AllReduce(agg, agg, agg_words, ncclUint64, ncclSum, comm_, cs_);
       nc.GroupEnd();
       if (r != ncclSuccess)
         throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
@@ -1484,9 +1490,7 @@ void Engine::exchange_round(bool pagerank) {
       loopback_allreduce(loop_, rank_, values_.p, n_, kLoopU32, kLoopMin, cs_);
       loopback_allreduce(loop_, rank_, &census_.p->min_changed, 1, kLoopU32, kLoopMin, cs_);
     }
-    // every rank reduces the same number of counter entries (same schedule)
-    loopback_allreduce(loop_, rank_, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), kLoopU64,
-                       kLoopSum, cs_);
+    loopback_allreduce(loop_, rank_, agg, agg_words, kLoopU64, kLoopSum, cs_);
     if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
     return;
   }
@@ -1504,9 +1508,7 @@ void Engine::exchange_round(bool pagerank) {
       r = nc.AllReduce(&census_.p->min_changed, &census_.p->min_changed, 1, ncclUint32, ncclMin,
                        comm_, cs_);
   }
-  if (r == ncclSuccess && ctr_used_)
-    r = nc.AllReduce(ctr_.p, ctr_.p, size_t(ctr_used_) * (sizeof(RunCtr) / 8), ncclUint64,
-                     ncclSum, comm_, cs_);
+  if (r == ncclSuccess) r = nc.AllReduce(agg, agg, agg_words, ncclUint64, ncclSum, comm_, cs_);
   nc.GroupEnd();
   if (r != ncclSuccess) throw EngineError(SR_E_NCCL, std::string("nccl: ") + nc.GetErrorString(r));
   if (!pagerank) launch_mark_changed(n_, values_.p, round_snap_.p, changed_.p, cs_);
@@ -1626,16 +1628,29 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     passes.push_back(st);
   };
   auto sum_ctr = [&](sr_pass_stats& st) {
+    // the pass's reference counters: this rank's slots, or in a world the
+    // round's all-reduced aggregate (exchange_round); the work counters
+    // (gathers, streamed edges, destination scans) stay this rank's own
     uint64_t gathers = 0;
     for (size_t i = 0; i < size_t(ctr_used_); ++i) {
+      if (int(i) == agg_slot_) continue;
       gathers += ctr_h_.p[i].gathers;
       streamed_total_ += ctr_h_.p[i].streamed;
       visits_total_ += ctr_h_.p[i].visits;
+      if (agg_slot_ >= 0) continue;
       st.attempts += ctr_h_.p[i].attempts;
       st.valid_updates += ctr_h_.p[i].valid;
       st.skipped += ctr_h_.p[i].skipped;
       st.edges_read += ctr_h_.p[i].edges;
     }
+    if (agg_slot_ >= 0 && size_t(agg_slot_) < size_t(ctr_used_)) {
+      const RunCtr& ag = ctr_h_.p[agg_slot_];
+      st.attempts += ag.attempts;
+      st.valid_updates += ag.valid;
+      st.skipped += ag.skipped;
+      st.edges_read += ag.edges;
+    }
+    agg_slot_ = -1;
     gathers_total_ += gathers;
     last_gather_frac_ = st.edges_read ? double(gathers) / double(st.edges_read) : 0.0;
     last_block_gather_frac_ = 1.0;

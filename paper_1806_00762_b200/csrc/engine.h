@@ -212,7 +212,8 @@ class Engine {
   int load_algo_ = -1;
   uint32_t push_chunk_shift(uint64_t total) const;
   void read_census();
-  void exchange_round(bool pagerank);
+  void exchange_round(bool pagerank, uint32_t ctr_from = 0);
+  int agg_slot_ = -1;  // counter slot holding the round's all-reduced aggregate (worlds)
 
   // streaming
   bool streaming() const { return !all_resident_; }

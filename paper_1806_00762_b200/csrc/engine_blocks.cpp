@@ -624,6 +624,7 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   ctr_used_ = 0;
   SR_CUDA(cudaMemsetAsync(ctr_.p, 0, ctr_.n * sizeof(RunCtr), cs_));
   std::vector<uint32_t> ctr_begin;
+  std::vector<int> pr_agg;  // per iteration: the all-reduced aggregate slot (worlds) or -1
   for (uint32_t it = 0; it < cfg.pr_iterations; ++it) {
     ctr_begin.push_back(ctr_used_);
     if (attached()) {
@@ -650,7 +651,8 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
       launch_pr_hub_finalize(hub_vertex_.p, n_hubs_, hub_sum_.p, rank_b_.p, contrib_b_.p,
                              inv_outdeg_.p, base, float(cfg.pr_damping), cs_);
     }
-    exchange_round(true);
+    exchange_round(true, ctr_begin.back());
+    pr_agg.push_back(agg_slot_);
     sr_pass_stats st{};
     st.pass_index = it;
     st.kind = SR_PASS_DENSE_PULL;
@@ -683,10 +685,17 @@ void Engine::run_pagerank(const sr_run_config& cfg, float* ranks_out, sr_metrics
   for (size_t it = 0; it + 1 < ctr_begin.size(); ++it) {
     if (blocked) continue;  // counted analytically above
     sr_pass_stats& st = passes[passes.size() - (ctr_begin.size() - 1) + it];
+    const int ag = it < pr_agg.size() ? pr_agg[it] : -1;  // a world's reduced aggregate
     for (uint32_t i = ctr_begin[it]; i < ctr_begin[it + 1]; ++i) {
+      if (int(i) == ag) continue;
       gathers_total_ += ctr_h_.p[i].gathers;
+      if (ag >= 0) continue;
       st.attempts += ctr_h_.p[i].attempts;
       st.edges_read += ctr_h_.p[i].edges;
+    }
+    if (ag >= 0) {
+      st.attempts += ctr_h_.p[ag].attempts;
+      st.edges_read += ctr_h_.p[ag].edges;
     }
     m.update_attempts += st.attempts;
     m.edges_read += st.edges_read;

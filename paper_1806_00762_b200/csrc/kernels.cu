@@ -1017,6 +1017,21 @@ __global__ void pr_hot_gather_kernel(const uint32_t* __restrict__ hot_vertex, ui
   if (i < n_hot) hot_contrib[i] = contrib[hot_vertex[i]];
 }
 
+// Round aggregate of a world's counters: out = sum of slots [from, to) (the
+// exchange all-reduces this one fixed-size entry: ranks may use different
+// numbers of counter slots in a pass -- probes, fallbacks -- so the slot
+// arrays themselves do not line up across ranks).
+__global__ void sum_ctr_slots_kernel(const RunCtr* slots, uint32_t from, uint32_t to,
+                                     RunCtr* out) {
+  constexpr uint32_t kWords = sizeof(RunCtr) / 8;
+  const uint32_t f = threadIdx.x;
+  if (f >= kWords) return;
+  const unsigned long long* w = reinterpret_cast<const unsigned long long*>(slots);
+  unsigned long long s = 0;
+  for (uint32_t i = from; i < to; ++i) s += w[size_t(i) * kWords + f];
+  reinterpret_cast<unsigned long long*>(out)[f] = s;
+}
+
 // Vertices with out-degree >= d (binary search of the hot threshold).
 __global__ void count_deg_ge_kernel(const uint32_t* __restrict__ deg, uint32_t n, uint32_t d,
                                     unsigned long long* out) {
@@ -1947,6 +1962,12 @@ void launch_pr_hot_gather(const uint32_t* hot_vertex, uint32_t n_hot, const floa
   note_launch();
   pr_hot_gather_kernel<<<(n_hot + 255) / 256, 256, 0, s>>>(hot_vertex, n_hot, contrib,
                                                            hot_contrib);
+}
+
+void launch_sum_ctr_slots(const RunCtr* slots, uint32_t from, uint32_t to, RunCtr* out,
+                          cudaStream_t s) {
+  note_launch();
+  sum_ctr_slots_kernel<<<1, 32, 0, s>>>(slots, from, to, out);
 }
 
 void launch_count_deg_ge(const uint32_t* deg, uint32_t n, uint32_t d, unsigned long long* out,

@@ -31,6 +31,9 @@ void launch_pr_hot_gather(const uint32_t* hot_vertex, uint32_t n_hot, const floa
                           float* hot_contrib, cudaStream_t s);
 void launch_count_deg_ge(const uint32_t* deg, uint32_t n, uint32_t d, unsigned long long* out,
                          cudaStream_t s);
+// out <- sum of counter slots [from, to) (the per-round aggregate a world reduces)
+void launch_sum_ctr_slots(const RunCtr* slots, uint32_t from, uint32_t to, RunCtr* out,
+                          cudaStream_t s);
 
 void launch_hot_assign(const uint32_t* deg, uint32_t n, uint32_t d, uint32_t cap,
                        unsigned* counter, uint32_t* slot_of, uint32_t* hot_vertex, cudaStream_t s);

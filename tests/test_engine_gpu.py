@@ -1035,6 +1035,12 @@ def test_sharded_rounds_loopback_world(world, blocked, peer, monkeypatch):
                 for r in res:
                     assert np.array_equal(r.values, want), (kind, pred, ex)
                 assert len({r.metrics.passes for r in res}) == 1  # same decisions
+                if pred == ps.PredictorMode.OFF and ex == ps.ExecutionPolicy.FORCE_DENSE:
+                    # the world's per-pass counters (one all-reduced aggregate per
+                    # round): every dense pass attempts each destination once
+                    for r in res:
+                        assert all(st.attempts == n for st in r.metrics.per_pass), \
+                            [st.attempts for st in r.metrics.per_pass]
         # reentry: each rank re-runs its own shard until locally quiet (up to
         # MRT) before the round's exchange (SURVEY §8(e) "local iteration")
         k += 1
