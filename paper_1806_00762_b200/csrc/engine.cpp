@@ -1320,14 +1320,26 @@ PassOut Engine::dense_pass_virtual(const sr_run_config& cfg, int gate, bool reco
 // ---------------------------------------------------------------------------
 void Engine::census(int pass_kind) {
   SR_CUDA(cudaMemsetAsync(census_.p, 0, kCensusResetBytes, cs_));
+  // every census is read right after (read_census): its last block publishes
+  Publish pub{};
+  if (ctr_used_ <= 64 && !std::getenv("SERAPH_NO_PUBLISH")) {
+    if (!pub_done_.p) {
+      pub_done_.reserve(1);
+      SR_CUDA(cudaMemsetAsync(pub_done_.p, 0, 4, cs_));
+    }
+    pub = Publish{census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, pub_done_.p};
+    published_ = true;
+  }
   launch_census(n_, changed_.p, predictor_ == SR_PRED_WEAK ? status_.p : nullptr,
                 predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr,
                 has_csr_ ? outdeg_.p : nullptr, pass_kind, own_lo_, own_hi_, blk_cnt_.p,
-                blk_edges_.p, census_part_.p, census_.p, cs_);
+                blk_edges_.p, census_part_.p, census_.p, pub, cs_);
 }
 
 void Engine::read_census() {
-  if (ctr_used_ <= 64 && !std::getenv("SERAPH_NO_PUBLISH")) {
+  if (published_) {  // the census kernel already wrote them into mapped memory
+    published_ = false;
+  } else if (ctr_used_ <= 64 && !std::getenv("SERAPH_NO_PUBLISH")) {
     // one kernel writes both into the mapped pinned buffers (UVA): no D2H DMAs
     launch_publish(census_.p, census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, cs_);
   } else {

@@ -212,6 +212,8 @@ class Engine {
   int load_algo_ = -1;
   uint32_t push_chunk_shift(uint64_t total) const;
   void read_census();
+  bool published_ = false;  // the last census published itself (read_census only syncs)
+  DBuf<unsigned> pub_done_;
   void exchange_round(bool pagerank, uint32_t ctr_from = 0);
   int agg_slot_ = -1;  // counter slot holding the round's all-reduced aggregate (worlds)
 

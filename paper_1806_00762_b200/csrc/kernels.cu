@@ -1587,9 +1587,30 @@ __global__ void __launch_bounds__(256, ST ? 1 : 8) census_kernel(uint32_t n, con
                                                      const uint32_t* __restrict__ outdeg,
                                                      int pass_kind, uint32_t own_lo, uint32_t own_hi,
                                                      uint32_t* blk_cnt,
-                                                     unsigned long long* blk_edges, Census* cz) {
+                                                     unsigned long long* blk_edges, Census* cz,
+                                                     Publish pub) {
   census_body<ST>(n, changed, status, logstate, outdeg, pass_kind, own_lo, own_hi, blk_cnt,
                   blk_edges, cz, cz, blockIdx.x, gridDim.x);
+  if (!pub.done) return;
+  // the last block to finish publishes the pass's census and run counters
+  // into the mapped pinned buffers (no separate publish launch per pass)
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(pub.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint32_t words = sizeof(Census) / 4;
+  const uint32_t cwords = pub.n_ctr * uint32_t(sizeof(RunCtr) / 8);
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(pub.cz_host)[i] = __ldcg(reinterpret_cast<const uint32_t*>(cz) + i);
+  for (uint32_t i = threadIdx.x; i < cwords; i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(pub.ctr_host)[i] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(pub.ctr) + i);
+  if (threadIdx.x == 0) *pub.done = 0;  // ready for the next pass
 }
 
 // Exclusive scan of the per-chunk (count, edges) pairs by ONE block (any
@@ -2255,7 +2276,7 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
                    const uint32_t* out_offsets, int pass_kind, uint32_t own_lo,
                    uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges,
-                   unsigned long long* part, Census* c, cudaStream_t s) {
+                   unsigned long long* part, Census* c, const Publish& pub, cudaStream_t s) {
   const uint32_t nb = (n + kCensusBlockVerts - 1) / kCensusBlockVerts;
   if (!nb) return;
   (void)part;
@@ -2264,10 +2285,10 @@ void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t*
   note_launch();
   if (status || logstate)
     census_kernel<true><<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind,
-                                             own_lo, own_hi, blk_cnt, blk_edges, c);
+                                             own_lo, own_hi, blk_cnt, blk_edges, c, pub);
   else
     census_kernel<false><<<grid, 256, 0, s>>>(n, changed, status, logstate, out_offsets, pass_kind,
-                                              own_lo, own_hi, blk_cnt, blk_edges, c);
+                                              own_lo, own_hi, blk_cnt, blk_edges, c, pub);
 }
 
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,

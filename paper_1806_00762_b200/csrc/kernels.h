@@ -58,10 +58,19 @@ void launch_push_commit(uint32_t* values, const uint32_t* next, const uint8_t* c
                         uint32_t n, RunCtr* ctr, Census* c, cudaStream_t s);
 // K4/K5: per-pass census (+ weak DFA step, prediction log, status histogram).
 constexpr uint32_t kCensusBlockVerts = 4096;
+// pub.done != null: the census's last block also publishes the census and
+// pub.n_ctr run counters into the mapped pinned buffers (launch_publish fused)
+struct Publish {
+  Census* cz_host;
+  const RunCtr* ctr;
+  RunCtr* ctr_host;
+  uint32_t n_ctr;
+  unsigned* done;  // zeroed block ticket (the last block resets it)
+};
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
                    const uint32_t* outdeg, int pass_kind, uint32_t own_lo,
                    uint32_t own_hi, uint32_t* blk_cnt, unsigned long long* blk_edges,
-                   unsigned long long* part, Census* c, cudaStream_t s);
+                   unsigned long long* part, Census* c, const Publish& pub, cudaStream_t s);
 void launch_scan_blocks(uint32_t nblocks, uint32_t* blk_cnt, unsigned long long* blk_edges,
                         cudaStream_t s);
 void launch_compact(uint32_t n, uint32_t own_lo, uint32_t own_hi, uint8_t* changed,
