@@ -2,7 +2,9 @@
 #include "loopback.h"
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -23,7 +25,9 @@ struct LoopbackGroup {
   std::vector<std::vector<unsigned char>> slots;
   std::vector<void*> ptrs;
 
-  // generation barrier over the `world` ranks
+  // generation barrier over the `world` ranks; a rank that never arrives
+  // (it failed before the collective) turns into an error here instead of a
+  // hang (SERAPH_LOOPBACK_TIMEOUT_S, default 600 s)
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const uint64_t gen = generation;
@@ -32,7 +36,12 @@ struct LoopbackGroup {
       ++generation;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return generation != gen; });
+      long secs = 600;
+      if (const char* e = std::getenv("SERAPH_LOOPBACK_TIMEOUT_S")) secs = std::max(1L, std::atol(e));
+      if (!cv.wait_for(lk, std::chrono::seconds(secs), [&] { return generation != gen; })) {
+        --arrived;
+        throw EngineError(SR_E_INTERNAL, "loopback world: a rank did not reach the collective");
+      }
     }
   }
 };
