@@ -284,6 +284,59 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= total) break;
     const uint32_t t1 = min(t0 + grab, total);
+    // Grab-wide gate scan: when the grab's tiles are consecutive range tiles
+    // of one page (one contiguous destination range), gate that range with
+    // coalesced loads first.  If no destination in it can still improve (the
+    // later passes of a converging run; sub-pages after the root block
+    // settled) the grab is counted here and none of its tiles is entered;
+    // otherwise the scan stops at the first live chunk and the tiles run.
+    if (A != kSssp && !a_prev_ctr && t1 - t0 > 1 && t1 - t0 <= 32) {
+      const uint32_t n = t1 - t0;
+      uint32_t tp = 0;
+      uint4 tl = make_uint4(0, 0, 0, 0);
+      if (lane < n) {
+        const uint32_t ti = task_to_tile(a.seg, t0 + lane);
+        tp = a.tile_page[ti];
+        tl = a.tiles[ti];
+      }
+      const uint32_t p0 = __shfl_sync(kFull, tp, 0);
+      const uint32_t prev_w = __shfl_up_sync(kFull, tl.w, 1);
+      const bool ok = lane >= n || (tp == p0 && !(tl.w & kHubFlag) && (lane == 0 || tl.z == prev_w));
+      if (__all_sync(kFull, ok)) {
+        if (p0 != cur_page) {
+          if (a.ctr_per_page && cur_page != 0xffffffffu) flush_ctr(c, a_ctr + cur_page, lane);
+          cur_page = p0;
+          pd = a.pages[p0];
+        }
+        const uint32_t dl = __shfl_sync(kFull, tl.z, 0), dh = __shfl_sync(kFull, tl.w, n - 1);
+        const uint32_t vb = pd.vertex_begin;
+        const uint32_t* __restrict__ offs = pd.offs;
+        uint32_t n_att = 0, n_skip = 0, n_edges = 0;
+        bool live = false;
+#pragma unroll 1
+        for (uint32_t base = dl; base < dh; base += 32) {
+          const uint32_t i = base + lane;
+          if (i < dh) {
+            const uint32_t v = vb + i;
+            const uint32_t cur = DET ? __ldg(values_ro + v) : a.values[v];
+            const uint32_t deg = offs[i + 1] - offs[i];
+            const bool att = gate_attempt<A, G>(v, cur, a);
+            n_att += att;
+            n_skip += !att;
+            n_edges += att ? deg : 0u;
+            live = att && deg > 0 && cur > dest_floor<A>(a);
+          }
+          if (__any_sync(kFull, live)) break;
+        }
+        if (!__any_sync(kFull, live)) {
+          c.attempts += n_att & (0u - a_count_dest);
+          c.skipped += n_skip & (0u - a_count_dest);
+          c.edges += n_edges;
+          c.visits += dh - dl;
+          continue;
+        }
+      }
+    }
     for (uint32_t t = t0; t < t1; ++t) {
       const uint32_t ti = task_to_tile(a.seg, t);
       const uint32_t p = a.tile_page[ti];
