@@ -21,7 +21,7 @@
 
 namespace seraph {
 
-uint32_t k1_grab(uint64_t tiles, int grid, const char* env);
+uint32_t k1_grab(uint64_t tiles, int grid, const char* env, uint32_t cap = 8);
 
 struct LoopbackGroup;
 

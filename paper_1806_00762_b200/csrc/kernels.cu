@@ -50,6 +50,10 @@ constexpr uint32_t kBndWords = 33;  // K1 entry-start bitmap words (span <= 1031
 #endif
 constexpr int kInplaceMax = SERAPH_INPLACE_MAX;
 constexpr uint32_t kInplaceDeg = SERAPH_INPLACE_DEG;
+#ifndef SERAPH_SCAN_U
+#define SERAPH_SCAN_U 4
+#endif
+constexpr int kScanU = SERAPH_SCAN_U;  // 32-destination chunks per step of the grab-wide gate scan
 constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
 constexpr uint32_t kNone = 0xffffffffu;  // no entry (K8 segmented merge)
 
@@ -324,18 +328,34 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
         const uint32_t* __restrict__ offs = pd.offs;
         uint32_t n_att = 0, n_skip = 0, n_edges = 0;
         bool live = false;
+        // kScanU chunks of 32 destinations per step, all loads issued
+        // before the first use (one memory round trip per step)
 #pragma unroll 1
-        for (uint32_t base = dl; base < dh; base += 32) {
-          const uint32_t i = base + lane;
-          if (i < dh) {
-            const uint32_t v = vb + i;
-            const uint32_t cur = DET ? __ldg(values_ro + v) : a.values[v];
-            const uint32_t deg = offs[i + 1] - offs[i];
-            const bool att = gate_attempt<A, G>(v, cur, a);
-            n_att += att;
-            n_skip += !att;
-            n_edges += att ? deg : 0u;
-            live = att && deg > 0 && cur > dest_floor<A>(a);
+        for (uint32_t base = dl; base < dh; base += 32 * kScanU) {
+          uint32_t cu[kScanU], o0[kScanU];
+#pragma unroll
+          for (int u = 0; u < kScanU; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            cu[u] = kUnreached;
+            o0[u] = 0;
+            if (i <= dh) o0[u] = offs[i];
+            if (i < dh) cu[u] = DET ? __ldg(values_ro + vb + i) : a.values[vb + i];
+          }
+#pragma unroll
+          for (int u = 0; u < kScanU; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            // offs[i + 1]: the next lane's load (lane 31: the next chunk's lane 0)
+            uint32_t o1 = __shfl_down_sync(kFull, o0[u], 1);
+            const uint32_t nx = __shfl_sync(kFull, u + 1 < kScanU ? o0[u + 1 < kScanU ? u + 1 : u] : 0u, 0);
+            if (lane == 31) o1 = (u + 1 < kScanU) ? nx : (i < dh ? offs[i + 1] : 0u);
+            if (i < dh) {
+              const uint32_t deg = o1 - o0[u];
+              const bool att = gate_attempt<A, G>(vb + i, cu[u], a);
+              n_att += att;
+              n_skip += !att;
+              n_edges += att ? deg : 0u;
+              live = live || (att && deg > 0 && cu[u] > dest_floor<A>(a));
+            }
           }
           if (__any_sync(kFull, live)) break;
         }
