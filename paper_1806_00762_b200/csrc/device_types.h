@@ -23,7 +23,8 @@ constexpr uint32_t kHubChunk = 1024;      // edges per hub chunk tile
 constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id
 constexpr int kMaxSegments = 8;           // tile ranges per launch
 constexpr int kDiagIters = 1;             // blocked K1: diagonal sweeps until locally quiet (cap)
-constexpr int kRootDiagReps = 6;          // blocked K1: in-launch diagonal sweeps of the root block
+constexpr int kRootDiagReps = 6;
+constexpr double kListFrac = 0.3;        // gathers/edges of the previous launch below which K1 runs its LIST variant          // blocked K1: in-launch diagonal sweeps of the root block
 // K8 hot-source staging (pr_pull_kernel<true, kHotWarps>): blocks of
 // kHotWarps warps (1.5 KB of tile scratch each) + a shared-memory table of
 // f32 contributions of the hottest sources, encoded kHotBit | slot.  Measured
@@ -109,6 +110,8 @@ struct PullArgs {
   uint32_t src_floor;  // SSSP: lower bound of every source that can still improve (0 = none)
   uint32_t floor_step; // SSSP: smallest edge weight bound (1; 0 when a page holds weight-0 edges)
   uint32_t grab;       // tiles per work-counter grab (0 = kGrab)
+  uint32_t list;       // converging launch (few gathers expected): K1's LIST
+                       // variant relaxes sparse live destinations in its scan
 };
 
 // K2 (pull_reentry_kernel): up to `runs` runs of one page set in one

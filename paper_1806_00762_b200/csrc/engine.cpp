@@ -405,6 +405,12 @@ void Engine::build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st) {
   run_id_ = 0;
 }
 
+// K1's LIST variant (SERAPH_K1_LIST=0 disables).
+bool Engine::list_ok() const {
+  const char* e = std::getenv("SERAPH_K1_LIST");
+  return !e || std::atoi(e) != 0;
+}
+
 // K1 tiles per work-counter grab: about 1/16 of a warp's share of the
 // launch, clamped to 1..cap; `env` overrides (1..64, A/B knob).
 uint32_t k1_grab(uint64_t tiles, int grid, const char* env, uint32_t cap) {
@@ -931,6 +937,9 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
         a.grab = k1_grab(seg.task_prefix[seg.n], grid, "SERAPH_K1_GRAB",
                          algo_ == SR_ALGO_SSSP ? 8u : 32u);
       }
+      // a converging sweep: the previous pass gathered little, or this is
+      // the unblocked finish of a blocked pass whose probe found gathers rare
+      a.list = list_ok() && (last_gather_frac_ < kListFrac || fallback_frac_ >= 0) ? 1u : 0u;
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());

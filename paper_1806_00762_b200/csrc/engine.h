@@ -422,6 +422,7 @@ class Engine {
   Segments range_segments(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) const;
   int diag_local_iterations() const;
   bool probe_every_block() const;
+  bool list_ok() const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
   // A blocked pass's last block launch counts into its own slot: when even

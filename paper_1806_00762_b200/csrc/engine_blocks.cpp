@@ -256,9 +256,14 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     last_ctr = alloc_ctr(1);
     sb_last_slot_ = int(last_ctr - ctr_.p);
   }
+  // LIST variant for a block launch expected to gather little: the previous
+  // block's probe (or, for block 0, the previous pass) gathered for < 30 %
+  double prev_frac = last_block_gather_frac_;
+  bool list = false, root_done = false;
   auto make_args = [&](const Segments& seg, RunCtr* slot, bool count_dest, bool count_v,
                        uint32_t rid) {
     PullArgs a{};
+    a.list = list ? 1u : 0u;
     a.work = next_work_counter();
     a.tiles = sb_.tiles.p;
     a.tile_page = sb_.tile_page.p;
@@ -344,6 +349,9 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
                    : (b == 0 || size_t(ctr_used_) + 1 > ctr_.n) ? ctr
                                                                 : alloc_ctr(1);
     uint32_t d0 = 0, d1 = 0;
+    // (after the CC root block's sweeps carried label 0 out, the later
+    // blocks' launches find most destinations at the floor: LIST too)
+    list = list_ok() && (prev_frac < kListFrac || (b > 0 && root_done));
     if (diag_iters > 1 && diag_range(b, t0, t1, d0, d1)) {
       // Local convergence of the block's own subgraph (Seraph's multi-pass
       // subgraph iteration): the diagonal sub-pages -- edges whose source AND
@@ -373,6 +381,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
       for (int r = 0; r < root_reps; ++r)
         launch_range(range_segments(d0, d1, 0, 0), slot, r == 0, count_valid, run_id);
       launch_range(range_segments(t0, d0, d1, t1), slot, true, count_valid, run_id);
+      root_done = true;
     } else {
       // Diagonal first: the sub-pages whose destinations are this block's own
       // sources go first, so the labels / levels / distances they improve are
@@ -391,6 +400,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
       SR_CUDA(cudaMemcpyAsync(ctr_h_.p, slot, sizeof(RunCtr), cudaMemcpyDeviceToHost, cs_));
       SR_CUDA(cudaStreamSynchronize(cs_));
       const RunCtr& c0 = ctr_h_.p[0];
+      if (c0.edges > 0) prev_frac = double(c0.gathers) / double(c0.edges);
       if (c0.edges > 0 && double(c0.gathers) < 0.05 * double(c0.edges)) {
         // the reference's per-pass counters (attempts, valid, skipped,
         // edges_read) restart with the unblocked sweep; the work counters

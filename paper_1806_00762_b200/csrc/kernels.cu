@@ -54,6 +54,14 @@ constexpr uint32_t kInplaceDeg = SERAPH_INPLACE_DEG;
 #define SERAPH_SCAN_U 4
 #endif
 constexpr int kScanU = SERAPH_SCAN_U;  // 32-destination chunks per step of the grab-wide gate scan
+#ifndef SERAPH_SCAN_LIST
+#define SERAPH_SCAN_LIST 1
+#endif
+#ifndef SERAPH_LIST_DEG
+#define SERAPH_LIST_DEG 64
+#endif
+constexpr bool kScanList = SERAPH_SCAN_LIST != 0;  // PullArgs::list launches use the LIST kernel
+constexpr uint32_t kListDeg = SERAPH_LIST_DEG;       // ... of at most this in-degree
 constexpr uint32_t kGrab = 4;   // tiles a warp takes per work-counter atomic
 constexpr uint32_t kNone = 0xffffffffu;  // no entry (K8 segmented merge)
 
@@ -269,10 +277,42 @@ __device__ __forceinline__ void block_flush(LaneCtr& c, RunCtr* dst, uint32_t la
 // Hub tile: one kHubChunk slice of a high in-degree destination; warp
 // min-reduce, global atomicMin, and a run-id stamp that counts the
 // destination's valid update once per run.
+// One lane relaxes its own destination v (BFS/CC: no weights): its deg
+// in-edges 4 source loads at a time, then their gathers; stores the minimum
+// if it improves the gated value cur (one writer per destination, as phase C).
+template <int A, bool DET>
+__device__ __forceinline__ void relax_own(const PullArgs& a, const uint32_t* __restrict__ es,
+                                          uint32_t deg, uint32_t v, uint32_t cur, LaneCtr& c,
+                                          uint32_t& lane_min) {
+  uint32_t best = kUnreached;
+#pragma unroll 1
+  for (uint32_t e = 0; e < deg; e += 4) {
+    uint32_t sx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sx[k] = e + k < deg ? __ldcs(es + e + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (e + k < deg)
+        best = min(best, combine<A>(DET ? __ldg(a.values + sx[k]) : gather_rw(a.values + sx[k]), 0u));
+  }
+  c.gathers += deg;
+  if (best < cur) {
+    if (DET) {
+      a.next[v] = best;
+    } else {
+      a.values[v] = best;
+      if (a.n_peers) peer_store(a.peers, a.n_peers, v, best);
+    }
+    a.changed[v] = 1;
+    c.valid += a.count_valid;
+    lane_min = min(lane_min, best);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // 6 blocks x 8 warps per SM at <= 40 registers (measured best: 5 blocks at 48
 // registers and 7-8 blocks at 32 registers with spills are 3-20 % slower)
-template <int A, int G, bool DET>
+template <int A, int G, bool DET, bool LIST>
 __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_work, RunCtr* a_ctr,
                                                 const RunCtr* a_prev_ctr, uint32_t a_run_id,
                                                 uint32_t a_count_dest) {
@@ -326,7 +366,8 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
         const uint32_t dl = __shfl_sync(kFull, tl.z, 0), dh = __shfl_sync(kFull, tl.w, n - 1);
         const uint32_t vb = pd.vertex_begin;
         const uint32_t* __restrict__ offs = pd.offs;
-        uint32_t n_att = 0, n_skip = 0, n_edges = 0;
+        const uint32_t* __restrict__ gsrc = pd.src;
+        uint32_t n_att = 0, n_skip = 0, n_edges = 0, n_list = 0;
         bool live = false;
         // kScanU chunks of 32 destinations per step, all loads issued
         // before the first use (one memory round trip per step)
@@ -348,13 +389,38 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
             uint32_t o1 = __shfl_down_sync(kFull, o0[u], 1);
             const uint32_t nx = __shfl_sync(kFull, u + 1 < kScanU ? o0[u + 1 < kScanU ? u + 1 : u] : 0u, 0);
             if (lane == 31) o1 = (u + 1 < kScanU) ? nx : (i < dh ? offs[i + 1] : 0u);
+            uint32_t deg = 0;
+            bool lv = false;
             if (i < dh) {
-              const uint32_t deg = o1 - o0[u];
+              deg = o1 - o0[u];
               const bool att = gate_attempt<A, G>(vb + i, cu[u], a);
               n_att += att;
               n_skip += !att;
               n_edges += att ? deg : 0u;
-              live = live || (att && deg > 0 && cu[u] > dest_floor<A>(a));
+              lv = att && deg > 0 && cu[u] > dest_floor<A>(a);
+            }
+            if (LIST) {
+              // sparse live destinations of low in-degree are listed (shared
+              // memory) and relaxed in place after the scan; a denser or
+              // heavier chunk sends the whole grab to the tile path
+              const unsigned lm = __ballot_sync(kFull, lv);
+              if (lm) {
+                const uint32_t k = __popc(lm);
+                if (n_list + k <= kTileMaxDests && __all_sync(kFull, !lv || deg <= kListDeg)) {
+                  if (lv) {
+                    const uint32_t pos = n_list + __popc(lm & lanemask_lt());
+                    s_loc[warp][pos] = vb + i;
+                    s_pref[warp][pos] = o0[u];
+                    s_cur[warp][pos] = cu[u];
+                    best_of[pos] = deg;
+                  }
+                  n_list += k;
+                } else {
+                  live = true;
+                }
+              }
+            } else {
+              live = live || lv;
             }
           }
           if (__any_sync(kFull, live)) break;
@@ -364,6 +430,18 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
           c.skipped += n_skip & (0u - a_count_dest);
           c.edges += n_edges;
           c.visits += dh - dl;
+          if (LIST && n_list) {
+            __syncwarp();
+            uint32_t runs_l = 0;
+            for (uint32_t j = lane; j < n_list; j += 32) {
+              const uint32_t deg = best_of[j];
+              relax_own<A, DET>(a, gsrc + s_pref[warp][j], deg, s_loc[warp][j], s_cur[warp][j], c,
+                                lane_min);
+              runs_l += (deg + 7) >> 3;
+            }
+            c.runs += __reduce_add_sync(kFull, runs_l);
+            __syncwarp();
+          }
           continue;
         }
       }
@@ -508,32 +586,7 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
           const unsigned lm = __ballot_sync(kFull, has && need);
           if (lm && __popc(lm) <= kInplaceMax &&
               __all_sync(kFull, !(has && need) || deg <= kInplaceDeg)) {
-            if (has && need) {
-              const uint32_t v = vb + i;
-              uint32_t best = kUnreached;
-#pragma unroll 1
-              for (uint32_t e = 0; e < deg; e += 4) {
-                uint32_t sx[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) sx[k] = e + k < deg ? __ldcs(src + lo + e + k) : 0u;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  if (e + k < deg)
-                    best = min(best, combine<A>(DET ? __ldg(values_ro + sx[k]) : gather_rw(a.values + sx[k]), 0u));
-              }
-              c.gathers += deg;
-              if (best < cur) {
-                if (DET) {
-                  a.next[v] = best;
-                } else {
-                  a.values[v] = best;
-                  if (a.n_peers) peer_store(a.peers, a.n_peers, v, best);
-                }
-                a.changed[v] = 1;
-                c.valid += a.count_valid;
-                lane_min = min(lane_min, best);
-              }
-            }
+            if (has && need) relax_own<A, DET>(a, src + lo, deg, vb + i, cur, c, lane_min);
             c.runs += __reduce_add_sync(kFull, (has && need) ? (deg + 7) >> 3 : 0u);
             need = false;
           }
@@ -680,9 +733,13 @@ __device__ __forceinline__ void pull_relax_body(const PullArgs& a, unsigned* a_w
   }
 }
 
-template <int A, int G, bool DET>
+// LIST: the converging-launch variant (PullArgs::list): its grab-wide scan
+// also relaxes sparse live destinations itself.  A separate instantiation:
+// the list state costs registers (spills) that the gather-heavy launches
+// must not pay.
+template <int A, int G, bool DET, bool LIST>
 __global__ void __launch_bounds__(kBlockThreads, 6) pull_relax_kernel(PullArgs a) {
-  pull_relax_body<A, G, DET>(a, a.work, a.ctr, a.prev_ctr, a.run_id, a.count_dest);
+  pull_relax_body<A, G, DET, LIST>(a, a.work, a.ctr, a.prev_ctr, a.run_id, a.count_dest);
 }
 
 // ---------------------------------------------------------------------------
@@ -698,7 +755,7 @@ __global__ void __launch_bounds__(kBlockThreads, 5) pull_reentry_kernel(PullArgs
   cg::grid_group grid = cg::this_grid();
   for (uint32_t it = 0; it < r.runs; ++it) {
     RunCtr* ctr = r.ctr + size_t(it) * r.ctr_stride;
-    pull_relax_body<A, G, false>(a, r.work + it, ctr,
+    pull_relax_body<A, G, false, false>(a, r.work + it, ctr,
                                  it ? r.ctr + size_t(it - 1) * r.ctr_stride : nullptr,
                                  a.run_id + it, (it == 0 || r.dest_every_run) ? a.count_dest : 0u);
     grid.sync();  // every page's counters of run `it` are final and visible
@@ -1969,7 +2026,10 @@ void launch_set_page_desc(PageDesc* d, uint32_t page, const uint32_t* offs, cons
 template <int A, int G, bool D>
 static void pull_dispatch3(const PullArgs& a, int grid, cudaStream_t s) {
   note_launch();
-  pull_relax_kernel<A, G, D><<<grid, kBlockThreads, 0, s>>>(a);
+  if (A != kSssp && !D && kScanList && a.list)
+    pull_relax_kernel<A, G, D, A != kSssp && !D><<<grid, kBlockThreads, 0, s>>>(a);
+  else
+    pull_relax_kernel<A, G, D, false><<<grid, kBlockThreads, 0, s>>>(a);
 }
 template <int A, int G>
 static void pull_dispatch2(bool det, const PullArgs& a, int grid, cudaStream_t s) {
@@ -2039,10 +2099,10 @@ int pull_blocks_per_sm(int algo, int gate, bool det) {
   (void)gate;
   (void)det;
   if (algo == kSssp)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kSssp, kGateOff, false>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kSssp, kGateOff, false, false>,
                                                   kBlockThreads, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kBfs, kGateOff, false>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pull_relax_kernel<kBfs, kGateOff, false, false>,
                                                   kBlockThreads, 0);
   return nb > 0 ? nb : 1;
 }

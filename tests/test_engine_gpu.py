@@ -1172,3 +1172,39 @@ def test_k2_device_reentry_loop(kind, monkeypatch):
                 c.schedule.max_reentry_times = mrt
                 r = eng.run_graph(csr, pages, program_for(kind, 0, el), c)
                 assert np.array_equal(r.values, want), (kind, pred, mrt)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("list_on", ["0", "1"])
+def test_k1_list_variant(list_on, monkeypatch):
+    """K1's LIST instantiation (converging launches: the grab-wide scan relaxes
+    sparse live destinations itself) on the C4 path in miniature -- CC on a
+    symmetrized uniform graph, source-blocked, root-block sweeps, then blocks
+    and the confirming pass run the LIST kernel -- and BFS/CC dense passes
+    after a sparse-gathering pass: bit-exact with it forced off and on, and the
+    reference-shaped counters of a gate-off run unchanged."""
+    monkeypatch.setenv("SERAPH_K1_LIST", list_on)
+    n = 1 << 15
+    src, dst = O.generate_rmat(15, 16, a=0.25, b=0.25, c=0.25, d=0.25, seed=5)
+    s2, d2, _ = O.symmetrize(src, dst, None)
+    sym = ps.EdgeList(n, s2, d2)
+    el = ps.EdgeList(n, src, dst)
+    csr, pages = built(sym, n // 16)
+    csr1, pages1 = built(el, n // 16)
+    want = oracle_values(sym, ps.AlgoKind.CC, 0)
+    for blk in (str(n // 8), "0"):
+        monkeypatch.setenv("SERAPH_PULL_BLOCK_VERTS", blk)
+        with ps.Engine(0) as eng:
+            for pred in PREDS:
+                r = eng.run_graph(csr, pages, ps.make_cc(), cfg_of(pred=pred, clock=ps.ClockMode.WALL))
+                assert np.array_equal(r.values, want), (blk, pred)
+                if pred == ps.PredictorMode.OFF:
+                    dense = [st for st in r.metrics.per_pass if st.kind != ps.PassKind.SPARSE_PUSH]
+                    assert all(st.attempts == n for st in dense)
+                    assert all(st.edges_read == sym.num_edges() for st in dense[1:])
+                assert r.metrics.per_pass[-1].valid_updates == 0
+            for pred in PREDS:
+                r = eng.run_graph(csr1, pages1, program_for(ps.AlgoKind.BFS, 0, el),
+                                  cfg_of(pred=pred, clock=ps.ClockMode.WALL,
+                                         execution=ps.ExecutionPolicy.FORCE_DENSE))
+                assert np.array_equal(r.values, oracle_values(el, ps.AlgoKind.BFS, 0)), (blk, pred)
