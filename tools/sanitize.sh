@@ -16,10 +16,10 @@ or test_frontier_queue or test_sssp_saturating or test_sssp_zero_weight or test_
 or test_device_build_bit_exact or test_device_generate_graph or test_sharded_rounds_loopback_world \
 or test_group_pagestream_run_multi_device or test_out_of_core_traversal_adjacency_budget \
 or test_sharded_run_graph_and_device_built_shards or test_k2_device_reentry_loop \
-or test_pagerank_rmat18_relative"
+or test_pagerank_rmat18_relative or test_k1_list_variant"
 SEL_RACE="test_fixpoint_law_random or test_pagerank_known_answers or test_sparse_pass_chains \
 or test_dense_pull_counts or test_pull_source_blocked or test_frontier_queue \
-or test_pagerank_rmat_vs_oracle or test_k2_device_reentry_loop or test_pagerank_source_blocked"
+or test_pagerank_rmat_vs_oracle or test_k2_device_reentry_loop or test_pagerank_source_blocked or test_k1_list_variant"
 for tool in memcheck racecheck synccheck; do
   extra=""
   sel="$SEL"
