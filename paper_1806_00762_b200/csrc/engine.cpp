@@ -939,7 +939,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       }
       // a converging sweep: the previous pass gathered little, or this is
       // the unblocked finish of a blocked pass whose probe found gathers rare
-      a.list = list_ok() && (last_gather_frac_ < kListFrac || fallback_frac_ >= 0) ? 1u : 0u;
+      a.list = list_ok() && (dense_gather_frac_ < kListFrac || fallback_frac_ >= 0) ? 1u : 0u;
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());
@@ -1620,6 +1620,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
   l_sssp_ = 0;
   floor_sssp_ = 0;
   last_gather_frac_ = 1.0;  // the first dense pass gathers
+  dense_gather_frac_ = 1.0;
   last_block_gather_frac_ = 1.0;
   sb_last_slot_ = -1;
   fallback_frac_ = -1;
@@ -1846,6 +1847,7 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     } else {
       sum_ctr(st);
       if (last_pass_blocked_) st.valid_updates = f_count;  // destinations changed
+      dense_gather_frac_ = last_gather_frac_;
     }
     st.changed_vertices = f_count;
     if (strong) {

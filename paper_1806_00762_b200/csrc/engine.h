@@ -424,7 +424,8 @@ class Engine {
   bool probe_every_block() const;
   bool list_ok() const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
-  double last_gather_frac_ = 1.0;  // gathers / edges read of the last dense pass
+  double last_gather_frac_ = 1.0;  // gathers / edges read of the last pass
+  double dense_gather_frac_ = 1.0;  // ... of the last dense pass (K1 LIST choice)
   // A blocked pass's last block launch counts into its own slot: when even
   // its gathers were rare (labels / levels at the floor), the next dense pass
   // sweeps unblocked without probing block 0 first.
