@@ -6,6 +6,7 @@
 #include "loopback.h"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -97,6 +98,8 @@ Engine::Engine(int device, uint64_t budget) : dev_(device), budget_(budget) {
   blocks_per_sm_ = pull_blocks_per_sm(kSssp, kGateOff, false);
   census_.reserve(1);
   census_h_.reserve(1);
+  pub_seq_h_.reserve(1);
+  *pub_seq_h_.p = 0;
 }
 
 Engine::~Engine() {
@@ -1341,7 +1344,7 @@ void Engine::census(int pass_kind) {
       pub_done_.reserve(1);
       SR_CUDA(cudaMemsetAsync(pub_done_.p, 0, 4, cs_));
     }
-    pub = Publish{census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, pub_done_.p};
+    pub = Publish{census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, pub_done_.p, pub_seq_h_.p, ++pub_seq_};
     published_ = true;
   }
   launch_census(n_, changed_.p, predictor_ == SR_PRED_WEAK ? status_.p : nullptr,
@@ -1353,14 +1356,42 @@ void Engine::census(int pass_kind) {
 void Engine::read_census() {
   if (published_) {  // the census kernel already wrote them into mapped memory
     published_ = false;
+    wait_published(pub_seq_);
+    return;
   } else if (ctr_used_ <= 64 && !std::getenv("SERAPH_NO_PUBLISH")) {
     // one kernel writes both into the mapped pinned buffers (UVA): no D2H DMAs
-    launch_publish(census_.p, census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, cs_);
+    launch_publish(census_.p, census_h_.p, ctr_.p, ctr_h_.p, ctr_used_, pub_seq_h_.p, ++pub_seq_,
+                   cs_);
+    wait_published(pub_seq_);
+    return;
   } else {
     SR_CUDA(cudaMemcpyAsync(census_h_.p, census_.p, sizeof(Census), cudaMemcpyDeviceToHost, cs_));
     if (ctr_used_)
       SR_CUDA(cudaMemcpyAsync(ctr_h_.p, ctr_.p, size_t(ctr_used_) * sizeof(RunCtr),
                               cudaMemcpyDeviceToHost, cs_));
+  }
+  SR_CUDA(cudaStreamSynchronize(cs_));
+}
+
+// The publishing kernel stores `seq` into pinned memory after a system-scope
+// fence, behind the census and counters it wrote: the host spins on that word
+// instead of a stream synchronize (whose wake-up costs several us per pass on
+// small graphs), polling the stream now and then so that an idle stream (or
+// an error, which the synchronize then throws) ends the wait.
+// SERAPH_NO_SPIN=1: plain stream synchronize.
+void Engine::wait_published(unsigned seq) {
+  static const bool no_spin = [] {
+    const char* e = std::getenv("SERAPH_NO_SPIN");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!no_spin) {
+    for (uint32_t it = 1;; ++it) {
+      if (*reinterpret_cast<volatile unsigned*>(pub_seq_h_.p) == seq) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return;
+      }
+      if ((it & 1023) == 0 && cudaStreamQuery(cs_) != cudaErrorNotReady) break;
+    }
   }
   SR_CUDA(cudaStreamSynchronize(cs_));
 }

@@ -214,6 +214,9 @@ class Engine {
   void read_census();
   bool published_ = false;  // the last census published itself (read_census only syncs)
   DBuf<unsigned> pub_done_;
+  PinBuf<unsigned> pub_seq_h_;  // last publish sequence number (read_census spins on it)
+  unsigned pub_seq_ = 0;
+  void wait_published(unsigned seq);
   void exchange_round(bool pagerank, uint32_t ctr_from = 0);
   int agg_slot_ = -1;  // counter slot holding the round's all-reduced aggregate (worlds)
 

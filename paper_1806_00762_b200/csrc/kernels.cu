@@ -1810,6 +1810,11 @@ __global__ void __launch_bounds__(256, ST ? 1 : 8) census_kernel(uint32_t n, con
   for (uint32_t i = threadIdx.x; i < cwords; i += blockDim.x)
     reinterpret_cast<unsigned long long*>(pub.ctr_host)[i] =
         __ldcg(reinterpret_cast<const unsigned long long*>(pub.ctr) + i);
+  if (pub.seq_host) {  // the host spins on this word instead of a stream sync
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(pub.seq_host) = pub.seq;
+  }
   if (threadIdx.x == 0) *pub.done = 0;  // ready for the next pass
 }
 
@@ -2386,7 +2391,8 @@ void launch_tail_loop(int algo, const TailArgs& a, cudaStream_t s) {
 // Pass results to the host: the census and the run counters are written
 // straight into mapped pinned memory by one tiny kernel (no D2H copies).
 __global__ void publish_kernel(const Census* __restrict__ cz, Census* cz_host,
-                               const RunCtr* __restrict__ ctr, RunCtr* ctr_host, uint32_t n_ctr) {
+                               const RunCtr* __restrict__ ctr, RunCtr* ctr_host, uint32_t n_ctr,
+                               unsigned* seq_host, unsigned seq) {
   const uint32_t words = sizeof(Census) / 4;
   const uint32_t cwords = n_ctr * uint32_t(sizeof(RunCtr) / 8);
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
@@ -2394,12 +2400,17 @@ __global__ void publish_kernel(const Census* __restrict__ cz, Census* cz_host,
   for (uint32_t i = threadIdx.x; i < cwords; i += blockDim.x)
     reinterpret_cast<unsigned long long*>(ctr_host)[i] =
         reinterpret_cast<const unsigned long long*>(ctr)[i];
+  if (seq_host) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(seq_host) = seq;
+  }
 }
 
 void launch_publish(const Census* cz, Census* cz_host, const RunCtr* ctr, RunCtr* ctr_host,
-                    uint32_t n_ctr, cudaStream_t s) {
+                    uint32_t n_ctr, unsigned* seq_host, unsigned seq, cudaStream_t s) {
   note_launch();
-  publish_kernel<<<1, 256, 0, s>>>(cz, cz_host, ctr, ctr_host, n_ctr);
+  publish_kernel<<<1, 256, 0, s>>>(cz, cz_host, ctr, ctr_host, n_ctr, seq_host, seq);
 }
 
 // Initial BFS/SSSP frontier {source} as a queue (initial_frontier,

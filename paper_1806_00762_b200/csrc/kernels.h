@@ -66,6 +66,8 @@ struct Publish {
   RunCtr* ctr_host;
   uint32_t n_ctr;
   unsigned* done;  // zeroed block ticket (the last block resets it)
+  unsigned* seq_host = nullptr;  // pinned: `seq` stored last, after a system fence
+  unsigned seq = 0;
 };
 void launch_census(uint32_t n, const uint8_t* changed, uint8_t* status, uint8_t* logstate,
                    const uint32_t* outdeg, int pass_kind, uint32_t own_lo,
@@ -121,7 +123,7 @@ void launch_degree_hist(const uint32_t* outdeg, uint32_t n, unsigned long long* 
 // and push-chunk starts, the inputs of launch_push.
 // census + n_ctr run counters -> mapped pinned host memory (one kernel)
 void launch_publish(const Census* cz, Census* cz_host, const RunCtr* ctr, RunCtr* ctr_host,
-                    uint32_t n_ctr, cudaStream_t s);
+                    uint32_t n_ctr, unsigned* seq_host, unsigned seq, cudaStream_t s);
 // consecutive small-frontier sparse passes in one single-block launch
 void launch_tail_loop(int algo, const TailArgs& a, cudaStream_t s);
 void launch_seed_queue(uint32_t source, const uint32_t* outdeg, uint32_t* list, Census* cz,
