@@ -1379,14 +1379,33 @@ void Engine::read_census() {
 // small graphs), polling the stream now and then so that an idle stream (or
 // an error, which the synchronize then throws) ends the wait.
 // SERAPH_NO_SPIN=1: plain stream synchronize.
-void Engine::wait_published(unsigned seq) {
+static bool spin_waits() {
   static const bool no_spin = [] {
     const char* e = std::getenv("SERAPH_NO_SPIN");
     return e && std::atoi(e) != 0;
   }();
-  if (!no_spin) {
+  return !no_spin;
+}
+
+void Engine::wait_published(unsigned seq) {
+  if (spin_waits()) {
     for (uint32_t it = 1;; ++it) {
       if (*reinterpret_cast<volatile unsigned*>(pub_seq_h_.p) == seq) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return;
+      }
+      if ((it & 1023) == 0 && cudaStreamQuery(cs_) != cudaErrorNotReady) break;
+    }
+  }
+  SR_CUDA(cudaStreamSynchronize(cs_));
+}
+
+// The same wait for a pinned word a kernel stores last (fenced): until it
+// differs from `pending`.
+void Engine::wait_word(const uint32_t* word, uint32_t pending) {
+  if (spin_waits()) {
+    for (uint32_t it = 1;; ++it) {
+      if (*reinterpret_cast<const volatile uint32_t*>(word) != pending) {
         std::atomic_thread_fence(std::memory_order_acquire);
         return;
       }
@@ -1796,8 +1815,9 @@ void Engine::run_traversal(const sr_run_config& cfg, uint32_t* values_out, sr_me
     t.logstate = predictor_ == SR_PRED_WEAK ? logstate_.p : nullptr;
     t.rec = tail_rec_.p;
     t.res = tail_res_.p;
+    *reinterpret_cast<volatile uint32_t*>(&tail_res_.p->passes) = kTailPending;
     launch_tail_loop(algo_, t, cs_);
-    SR_CUDA(cudaStreamSynchronize(cs_));
+    wait_word(&tail_res_.p->passes, kTailPending);
     const uint32_t np_run = tail_res_.p->passes;
     fq_epoch_ += np_run;
     for (uint32_t k = 0; k < np_run; ++k) {

@@ -217,6 +217,8 @@ class Engine {
   PinBuf<unsigned> pub_seq_h_;  // last publish sequence number (read_census spins on it)
   unsigned pub_seq_ = 0;
   void wait_published(unsigned seq);
+  void wait_word(const uint32_t* word, uint32_t pending);
+  static constexpr uint32_t kTailPending = 0xffffffffu;  // tail_res_.passes until the tail loop ends
   void exchange_round(bool pagerank, uint32_t ctr_from = 0);
   int agg_slot_ = -1;  // counter slot holding the round's all-reduced aggregate (worlds)
 

@@ -2373,9 +2373,14 @@ __global__ void __launch_bounds__(1024) tail_loop_kernel(TailArgs t) {
     for (uint32_t i = tid; i < q; i += blockDim.x) t.list[i] = cur[i];
   lane_min = warp_min(lane_min);
   if (lane == 0 && lane_min != kUnreached) atomicMin(&t.census->min_changed, lane_min);
+  // pinned results: the per-pass records and the reason first, `passes` last
+  // behind a system fence (the host spins on it, Engine::do_sparse_tail)
+  __threadfence_system();
+  __syncthreads();
   if (tid == 0) {
-    t.res->passes = pass;
     t.res->reason = reason;
+    __threadfence_system();
+    *reinterpret_cast<volatile uint32_t*>(&t.res->passes) = pass;
   }
 }
 
