@@ -24,7 +24,7 @@ constexpr uint32_t kHubFlag = 0x80000000u;  // tile.w flag: w & ~flag = hub id
 constexpr int kMaxSegments = 8;           // tile ranges per launch
 constexpr int kDiagIters = 1;             // blocked K1: diagonal sweeps until locally quiet (cap)
 constexpr int kRootDiagReps = 6;
-constexpr double kListFrac = 0.3;        // gathers/edges of the previous launch below which K1 runs its LIST variant          // blocked K1: in-launch diagonal sweeps of the root block
+constexpr double kListFrac = 0.3;        // gathers/edges of the previous launch below which K1 runs its LIST variant
 // K8 hot-source staging (pr_pull_kernel<true, kHotWarps>): blocks of
 // kHotWarps warps (1.5 KB of tile scratch each) + a shared-memory table of
 // f32 contributions of the hottest sources, encoded kHotBit | slot.  Measured

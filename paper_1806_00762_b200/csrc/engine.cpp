@@ -408,6 +408,16 @@ void Engine::build_tiles(uint32_t lo, uint32_t hi, cudaStream_t st) {
   run_id_ = 0;
 }
 
+// Gather fraction below which a launch takes K1's LIST variant
+// (SERAPH_LIST_FRAC overrides kListFrac; A/B knob).
+double Engine::list_frac() const {
+  static const double f = [] {
+    const char* e = std::getenv("SERAPH_LIST_FRAC");
+    return e ? std::atof(e) : kListFrac;
+  }();
+  return f;
+}
+
 // K1's LIST variant (SERAPH_K1_LIST=0 disables).
 bool Engine::list_ok() const {
   const char* e = std::getenv("SERAPH_K1_LIST");
@@ -942,7 +952,7 @@ RunStats Engine::launch_pages(const std::vector<uint32_t>& pages, int gate, bool
       }
       // a converging sweep: the previous pass gathered little, or this is
       // the unblocked finish of a blocked pass whose probe found gathers rare
-      a.list = list_ok() && (dense_gather_frac_ < kListFrac || fallback_frac_ >= 0) ? 1u : 0u;
+      a.list = list_ok() && (dense_gather_frac_ < list_frac() || fallback_frac_ >= 0) ? 1u : 0u;
       launch_pull(algo_, gate, det, a, grid, cs_);
     }
     SR_CUDA(cudaGetLastError());

@@ -428,6 +428,7 @@ class Engine {
   int diag_local_iterations() const;
   bool probe_every_block() const;
   bool list_ok() const;
+  double list_frac() const;
   bool last_pass_blocked_ = false;  // valid updates of the pass = destinations changed
   double last_gather_frac_ = 1.0;  // gathers / edges read of the last pass
   double dense_gather_frac_ = 1.0;  // ... of the last dense pass (K1 LIST choice)

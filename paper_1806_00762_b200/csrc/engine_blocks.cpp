@@ -351,7 +351,7 @@ bool Engine::pull_blocked_pass(int gate, RunCtr* ctr, bool count_valid) {
     uint32_t d0 = 0, d1 = 0;
     // (after the CC root block's sweeps carried label 0 out, the later
     // blocks' launches find most destinations at the floor: LIST too)
-    list = list_ok() && (prev_frac < kListFrac || (b > 0 && root_done));
+    list = list_ok() && (prev_frac < list_frac() || (b > 0 && root_done));
     if (diag_iters > 1 && diag_range(b, t0, t1, d0, d1)) {
       // Local convergence of the block's own subgraph (Seraph's multi-pass
       // subgraph iteration): the diagonal sub-pages -- edges whose source AND
